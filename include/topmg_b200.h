@@ -1,0 +1,160 @@
+/*
+ * topmg_b200 — C ABI of the B200 PCG + multiscale-multigrid solve path.
+ *
+ * This is the drop-in boundary for the reference's linear-solve hot path
+ * (/root/reference/proj/core). Each entry point cites the reference interface
+ * it replaces. Plain pointers and sizes only; every host array is in the
+ * reference's x-fastest cell order i + nx*(j + ny*k) (grid.hpp:27-29,44-46).
+ * All arithmetic is FP64. Errors follow the reference's three exception
+ * classes (grid.hpp:16-24, solver.cpp:486-492) as return codes; the message
+ * is available from tmg_last_error(). Non-convergence is not an error
+ * (solver.hpp:179-182): it is reported through tmg_report.converged = 0.
+ *
+ * A context owns one GPU's device memory, one CUDA stream and the captured
+ * iteration graph. It is thread-compatible, not thread-safe.
+ */
+#ifndef TOPMG_B200_H
+#define TOPMG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes. */
+#define TMG_OK 0
+#define TMG_ECONFIG 1 /* topmg::ConfigError   (grid.hpp:16-19)        */
+#define TMG_ESOLVER 2 /* topmg::SolverError   (grid.hpp:21-24)        */
+#define TMG_EARG 3    /* std::invalid_argument (solver.cpp:486-492)   */
+#define TMG_ECUDA 4   /* CUDA runtime failure                          */
+#define TMG_ENOTSUP 5 /* configuration outside what the GPU path builds */
+
+/* PrecondKind (solver.hpp:160). */
+#define TMG_PRECOND_NONE 0
+#define TMG_PRECOND_JACOBI 1
+#define TMG_PRECOND_BLOCK_JACOBI 2 /* not built on GPU: returns TMG_ENOTSUP */
+#define TMG_PRECOND_TWO_GRID 3     /* not built on GPU yet: TMG_ENOTSUP     */
+#define TMG_PRECOND_MMG 4
+
+/* Faces, topmg::Face (grid.hpp:57). */
+#define TMG_FACE_XLO 0
+#define TMG_FACE_XHI 1
+#define TMG_FACE_YLO 2
+#define TMG_FACE_YHI 3
+#define TMG_FACE_ZLO 4
+#define TMG_FACE_ZHI 5
+
+typedef struct tmg_ctx tmg_ctx;
+
+/* GridSpec (grid.hpp:30-55) + build_hierarchy(spec, ncc, sd) (grid.hpp:127-129). */
+typedef struct {
+  int64_t nx, ny, nz;
+  double lx, ly, lz;
+  int64_t ncc[3];
+  int64_t sd;
+} tmg_grid;
+
+/* DirichletPatch (grid.hpp:61-66). */
+typedef struct {
+  int face;
+  double u0, v0, u1, v1, value;
+} tmg_patch;
+
+/* MmgOptions (solver.hpp:141-146) + PrecondKind. Zero eig_* fields select
+ * the defaults of the batched local eigensolver. */
+typedef struct {
+  int kind;
+  int64_t num_local_basis; /* L_c  (reference default 4) */
+  int64_t num_cc_basis;    /* L_cc (reference default 8) */
+  int smoother_sweeps;     /* nu   (reference default 1) */
+  double eig_tol;
+  int eig_degree;
+  int eig_max_outer;
+} tmg_mmg_options;
+
+/* SolveReport (solver.hpp:15-22). */
+typedef struct {
+  int iterations;
+  int converged;
+  int status; /* 0 running,1 converged,2 max iterations,3 zero rhs,4 indefinite,5 non-finite */
+  double setup_seconds;
+  double solve_seconds;
+  double final_relative_residual; /* ||r||/||b|| of the recurrence residual */
+} tmg_report;
+
+/* Context ------------------------------------------------------------------ */
+
+/* Validates the hierarchy like build_hierarchy (grid.cpp:196-218; ConfigError
+ * on non-divisible axes) and allocates the context on CUDA device `device`. */
+int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out);
+void tmg_destroy(tmg_ctx* ctx);
+/* Message of the last failed call on this context (or of tmg_create when ctx
+ * is NULL). */
+const char* tmg_last_error(const tmg_ctx* ctx);
+
+/* Problem ------------------------------------------------------------------ */
+
+/* Conductivity per cell + Dirichlet patches: the inputs of assemble_system
+ * (fvm.cpp:33-51: ConfigError on kappa <= 0, bad patches, or no Dirichlet
+ * face). The operator A is then applied matrix-free from kappa. */
+int tmg_set_conductivity(tmg_ctx* ctx, const double* kappa, const tmg_patch* patches,
+                         int npatches);
+/* SIMP design (rho per cell) -> kappa on the device, MaterialModel +
+ * conductivity (material.cpp:8-15,45-59). */
+int tmg_set_design(tmg_ctx* ctx, const double* rho, double kappa_lo, double kappa_hi, int p,
+                   const tmg_patch* patches, int npatches);
+/* The rhs of assemble_system (fvm.cpp:63-112): f*vol + Dirichlet terms.
+ * source may be NULL (f = 0). */
+int tmg_assemble_rhs(tmg_ctx* ctx, const double* source, double* rhs_out);
+
+/* Preconditioner set-up: make_preconditioner (solver.cpp:462-481). */
+int tmg_setup(tmg_ctx* ctx, const tmg_mmg_options* opts);
+
+/* Solve -------------------------------------------------------------------- */
+
+/* topmg::pcg (solver.cpp:483-575): same stopping rule ||r||/||b|| <= rtol on
+ * the recurrence residual, same failure (pAp <= 0 -> TMG_ESOLVER), x0 may be
+ * NULL (zero start). history (nullable) receives max_iterations entries at
+ * most, the relative residual after each iteration. Host buffers. */
+int tmg_pcg(tmg_ctx* ctx, const double* b, const double* x0, double rtol, int max_iterations,
+            double* x_out, double* history, tmg_report* report);
+
+/* y = A x, SparseOperator::apply on the assembled TPFA matrix (sparse.cpp:71-84). */
+int tmg_apply_operator(tmg_ctx* ctx, const double* x, double* y);
+/* z = M r, Preconditioner::apply (solver.hpp:28). */
+int tmg_apply_preconditioner(tmg_ctx* ctx, const double* r, double* z);
+
+/* Device-resident variant used by the benchmark: b stays in HBM between
+ * solves; tmg_solve_resident times only the device solve. */
+int tmg_upload_rhs(tmg_ctx* ctx, const double* b);
+int tmg_upload_x0(tmg_ctx* ctx, const double* x0);
+int tmg_solve_resident(tmg_ctx* ctx, double rtol, int max_iterations, int use_x0,
+                       tmg_report* report);
+int tmg_download_solution(tmg_ctx* ctx, double* x);
+
+/* Introspection / measurement ------------------------------------------- */
+
+/* Local bases in the reference's R_c row order: phi[(I*Lc + a)*cells + i] is
+ * entry i (cells_of_coarse order) of basis a of coarse cell I; evals[I*Lc+a]. */
+int tmg_get_local_bases(tmg_ctx* ctx, double* phi, double* evals, int* eig_iterations);
+/* Dense coarse operator A_c (n_c x n_c, n_c = L_c * m_c, R_c row order). */
+int tmg_get_coarse_operator(tmg_ctx* ctx, double* ac_dense);
+/* R_cc as dense (n_cc x n_c). */
+int tmg_get_cc_restriction(tmg_ctx* ctx, double* rcc_dense);
+/* Sizes: [M, m_c, n_c, m_cc, n_cc, cells_per_coarse]. */
+int tmg_get_sizes(tmg_ctx* ctx, int64_t* sizes6);
+/* One solve launching every kernel separately with CUDA events around each
+ * (names: search, update, restrict, coarse_down, gemv, coarse_up, post,
+ * jacobi_step, init). ms_total[k] / count[k] per kernel k (9 slots). */
+int tmg_profile_solve(tmg_ctx* ctx, double rtol, int max_iterations, double* ms_total,
+                      int* count);
+/* Bytes of device memory held by the context. */
+int64_t tmg_device_bytes(const tmg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for external event timing. */
+void* tmg_stream(tmg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,254 @@
+"""ORACLE — test infrastructure only.
+
+ctypes front-end for ``oracle/liboracle.so`` (the plain-C restatement of the
+reference hot path, ``oracle/topmg_oracle.c``) and, when it has been built, for
+``oracle/_ref/libtopmg_ref.so`` (the reference's own ``proj/core`` sources
+compiled here, see ``oracle/build_ref.sh``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this module, and only as the checker.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+_REF = None
+
+I64 = C.c_int64
+DP = C.POINTER(C.c_double)
+IP = C.POINTER(C.c_int64)
+
+KIND = {"none": 0, "jacobi": 1, "block_jacobi": 2, "two_grid": 3, "mmg": 4}
+BLOCKS = {"cc": 0, "point": 1, "cell": 2, "box2": 18, "box4": 20, "box8": 24}
+FACE = {"xlo": 0, "xhi": 1, "ylo": 2, "yhi": 3, "zlo": 4, "zhi": 5}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class Grid(C.Structure):
+    _fields_ = [("nx", I64), ("ny", I64), ("nz", I64),
+                ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double)]
+
+
+class Patch(C.Structure):
+    _fields_ = [("face", C.c_int), ("u0", C.c_double), ("v0", C.c_double),
+                ("u1", C.c_double), ("v1", C.c_double), ("value", C.c_double)]
+
+
+class HGrid(C.Structure):
+    _fields_ = [("spec", Grid), ("ncc", I64 * 3), ("sd", I64),
+                ("nc", I64 * 3), ("cpc", I64 * 3)]
+
+
+class Csr(C.Structure):
+    _fields_ = [("rows", I64), ("cols", I64), ("off", IP), ("col", IP), ("val", DP)]
+
+
+class Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int),
+                ("solve_seconds", C.c_double), ("setup_seconds", C.c_double)]
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(HERE, "liboracle.so")
+        if not os.path.exists(path):
+            import subprocess
+            subprocess.check_call(["make", "-s", "-C", HERE, "liboracle.so"])
+        L = C.CDLL(path)
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_precond_op.restype = C.POINTER(Csr)
+        L.orc_count_dirichlet_faces.restype = I64
+        _LIB = L
+    return _LIB
+
+
+def _d(a):
+    return a.ctypes.data_as(DP)
+
+
+def _check(rc):
+    if rc != 0:
+        raise OracleError(rc, lib().orc_last_error().decode())
+
+
+def bottom_center_patch(lx=1.0, ly=1.0, side=0.2, value=0.0):
+    """BoundarySpec::bottom_center_patch (proj/core/src/grid.cpp:107-119)."""
+    return [(4, 0.5 * (lx - side), 0.5 * (ly - side), 0.5 * (lx + side),
+             0.5 * (ly + side), value)]
+
+
+def _patches(patches):
+    arr = (Patch * max(1, len(patches)))()
+    for i, p in enumerate(patches):
+        arr[i] = Patch(*p)
+    return arr, len(patches)
+
+
+def grid(n, l=(1.0, 1.0, 1.0)):
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    return Grid(nx, ny, nz, *l)
+
+
+def csr_to_scipy(c):
+    import scipy.sparse as sp
+    nnz = c.off[c.rows]
+    off = np.ctypeslib.as_array(c.off, shape=(c.rows + 1,)).copy()
+    col = np.ctypeslib.as_array(c.col, shape=(nnz,)).copy() if nnz else np.zeros(0, np.int64)
+    val = np.ctypeslib.as_array(c.val, shape=(nnz,)).copy() if nnz else np.zeros(0)
+    return sp.csr_matrix((val, col, off), shape=(c.rows, c.cols))
+
+
+def conductivity(rho, kappa_lo, kappa_hi=1.0, p=3):
+    rho = np.ascontiguousarray(rho, dtype=np.float64)
+    out = np.empty_like(rho)
+    _check(lib().orc_conductivity(I64(rho.size), _d(rho), C.c_double(kappa_lo),
+                                  C.c_double(kappa_hi), C.c_int(p), _d(out)))
+    return out
+
+
+def box_filter_design(g, vf, seed=20240501, passes=3, radius=2):
+    out = np.empty(g.nx * g.ny * g.nz)
+    lib().orc_box_filter_design(C.byref(g), C.c_double(vf), C.c_uint64(seed),
+                                C.c_int(passes), C.c_int(radius), _d(out))
+    return out
+
+
+def frozen_bench_design(g, vstar, seed=20240501, passes=2):
+    out = np.empty(g.nx * g.ny * g.nz)
+    lib().orc_frozen_bench_design(C.byref(g), C.c_double(vstar), C.c_uint64(seed),
+                                  C.c_int(passes), _d(out))
+    return out
+
+
+class System:
+    """AssembledSystem (proj/core/include/topmg/fvm.hpp:20-26)."""
+
+    def __init__(self, g, kappa, source, patches):
+        self.grid = g
+        self.kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+        self.source = np.ascontiguousarray(source, dtype=np.float64)
+        self.patches = list(patches)
+        self.csr = Csr()
+        self.rhs = np.empty(self.kappa.size)
+        parr, np_ = _patches(self.patches)
+        _check(lib().orc_assemble(C.byref(g), _d(self.kappa), _d(self.source), parr,
+                                  C.c_int(np_), C.byref(self.csr), _d(self.rhs)))
+
+    def __del__(self):
+        try:
+            lib().orc_csr_free(C.byref(self.csr))
+        except Exception:
+            pass
+
+    @property
+    def matrix(self):
+        return csr_to_scipy(self.csr)
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.csr.rows)
+        lib().orc_spmv(C.byref(self.csr), _d(x), _d(y))
+        return y
+
+
+def hierarchy(g, ncc, sd):
+    h = HGrid()
+    ncc3 = (I64 * 3)(*((ncc,) * 3 if np.isscalar(ncc) else ncc))
+    _check(lib().orc_build_hierarchy(C.byref(g), ncc3, I64(sd), C.byref(h)))
+    return h
+
+
+def local_basis(h, kappa, cid, count):
+    n = h.cpc[0] * h.cpc[1] * h.cpc[2]
+    vals = np.empty(count)
+    vecs = np.empty(count * n)
+    _check(lib().orc_local_basis(C.byref(h), _d(kappa), I64(cid), I64(count),
+                                 _d(vals), _d(vecs)))
+    return vals, vecs.reshape(count, n)
+
+
+class Precond:
+    """make_preconditioner (solver.cpp:462-481) with explicit smoother blocks."""
+
+    def __init__(self, kind, system, h=None, lc=4, lcc=8, sweeps=1,
+                 fine_blocks="point", coarse_blocks="cell"):
+        self.ptr = C.c_void_p()
+        self.system = system
+        hh = C.byref(h) if h is not None else None
+        _check(lib().orc_make_preconditioner(
+            C.c_int(KIND[kind]), C.byref(system.csr), hh, _d(system.kappa),
+            I64(lc), I64(lcc), C.c_int(sweeps), C.c_int(BLOCKS[fine_blocks]),
+            C.c_int(BLOCKS[coarse_blocks]), C.byref(self.ptr)))
+
+    def __del__(self):
+        try:
+            lib().orc_precond_free(self.ptr)
+        except Exception:
+            pass
+
+    def apply(self, r):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.empty_like(r)
+        _check(lib().orc_precond_apply(self.ptr, _d(r), _d(z)))
+        return z
+
+    def op(self, which):
+        p = lib().orc_precond_op(self.ptr, C.c_int(which))
+        return csr_to_scipy(p.contents) if p else None
+
+
+@dataclass
+class PcgResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+    solve_seconds: float
+
+
+def pcg(system, b, m, rtol=1e-6, max_iterations=10000, x0=None):
+    """topmg::pcg (proj/core/src/solver.cpp:483-575)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty_like(b)
+    hist = np.zeros(max(1, max_iterations))
+    rep = Report()
+    x0p = _d(np.ascontiguousarray(x0, dtype=np.float64)) if x0 is not None else None
+    _check(lib().orc_pcg(C.byref(system.csr), _d(b), m.ptr, C.c_double(rtol),
+                         C.c_int(max_iterations), x0p, _d(x), _d(hist), C.byref(rep)))
+    return PcgResult(x, rep.iterations, bool(rep.converged), hist[:rep.iterations].copy(),
+                     rep.solve_seconds)
+
+
+def syev_smallest(a, k):
+    a = np.array(a, dtype=np.float64, order="C")
+    n = a.shape[0]
+    w = np.empty(k)
+    v = np.empty((n, k))
+    L = lib()
+    rc = L.dla_syev_smallest(C.c_int(n), C.c_int(k), _d(a), _d(w), _d(v))
+    if rc:
+        raise OracleError(rc, "eigensolver failed")
+    return w, v
+
+
+def syev_all(a):
+    a = np.array(a, dtype=np.float64, order="C")
+    n = a.shape[0]
+    w = np.empty(n)
+    v = np.empty((n, n))
+    rc = lib().dla_syev_all(C.c_int(n), _d(a), _d(w), _d(v))
+    if rc:
+        raise OracleError(rc, "eigensolver failed")
+    return w, v

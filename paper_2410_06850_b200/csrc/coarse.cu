@@ -1,0 +1,543 @@
+// Coarse and coarse-coarse levels (north_star items 3, 4 (second level), 6).
+//
+// A_c = R_c A R_c^T (solver.cpp:265, galerkin_product sparse.cpp:261-270) is a
+// block 7-point operator because every R_c row lives in one coarse cell and A
+// is 7-point: block (I, J) = Phi_I^T A_IJ Phi_J, stored as Ac[I][dir][a][b],
+// dir = self, x-lo, x-hi, y-lo, y-hi, z-lo, z-hi. The coarse-coarse spectral
+// problem of one cc element (coarse_coarse_basis, coarse_space.cpp:343-406) is
+// P S_E P^T = A_c restricted to the element's children minus, on the diagonal
+// blocks, the face terms that cross the element boundary and the Dirichlet
+// terms (S_E uses only faces strictly inside the element); it is solved densely
+// per element (cyclic Jacobi, one warp) and its L_cc lowest eigenvectors are
+// the rows of R_cc. A_cc = R_cc A_c R_cc^T is again block 7-point at the cc
+// level and is assembled densely for the direct solve.
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace tmg {
+
+constexpr int LC = 4;  // compiled L_c (BASELINE "4 local eigenvectors per coarse cell")
+
+// ------------------------------------------------------------ A_c blocks
+
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
+                                                               const double* __restrict__ kappa,
+                                                               const uint8_t* __restrict__ dmask,
+                                                               const double* __restrict__ phi,
+                                                               double* Ac, double* Bc) {
+  constexpr int C = CB * CB * CB, NW = C / 32;
+  __shared__ double kt[Tile<CB>::N];
+  __shared__ double ph[LC][C];
+  __shared__ double red[LC * LC * NW + LC * LC + 8];
+  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  load_tile<CB, true>(kappa, kt, g, bc);
+  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  double f[LC];
+#pragma unroll
+  for (int a = 0; a < LC; ++a) {
+    f[a] = phi[(bc.b * LC + a) * C + t];
+    ph[a][t] = f[a];
+  }
+  __syncthreads();
+  const unsigned dm = brick_on_boundary(g, bc) ? dmask[bc.b * C + t] : 0u;
+  const FaceSet fs = cell_faces<CB>(kt, li, lj, lk, g, bc, dm);
+  // --- self block: sum_l d_l f_a f_b - sum_{+x,+y,+z in brick} T (f_a(l) f_b(j) + f_a(j) f_b(l))
+  {
+    double v[LC * LC];
+    const int st[3] = {1, CB, CB * CB};
+    const int co[3] = {li, lj, lk};
+#pragma unroll
+    for (int a = 0; a < LC; ++a)
+#pragma unroll
+      for (int b = 0; b < LC; ++b) v[a * LC + b] = fs.diag * f[a] * f[b];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (co[ax] + 1 >= CB) continue;
+      const int j = t + st[ax];
+      const double T = fs.t[2 * ax + 1];
+#pragma unroll
+      for (int a = 0; a < LC; ++a)
+#pragma unroll
+        for (int b = 0; b < LC; ++b) v[a * LC + b] -= T * (f[a] * ph[b][j] + ph[a][j] * f[b]);
+    }
+    block_sum_k<C, LC * LC>(v, red);
+    if (t < LC * LC) Ac[(bc.b * 7 + 0) * LC * LC + t] = v[t];
+  }
+  // --- face blocks: -T_lj f_a(l) phi_J,b(j) over the CB^2 face pairs
+  const int64_t nbr[6] = {bc.bi > 0 ? bc.b - 1 : -1,
+                          bc.bi + 1 < g.nbx ? bc.b + 1 : -1,
+                          bc.bj > 0 ? bc.b - g.nbx : -1,
+                          bc.bj + 1 < g.nby ? bc.b + g.nbx : -1,
+                          bc.bk > 0 ? bc.b - g.nbx * g.nby : -1,
+                          bc.bk + 1 < g.nbz ? bc.b + g.nbx * g.nby : -1};
+  const int co[3] = {li, lj, lk};
+  for (int fc = 0; fc < 6; ++fc) {
+    double v[LC * LC];
+#pragma unroll
+    for (int e = 0; e < LC * LC; ++e) v[e] = 0.0;
+    const int ax = fc >> 1;
+    const bool on_face = (fc & 1) ? co[ax] == CB - 1 : co[ax] == 0;
+    if (nbr[fc] >= 0 && on_face) {
+      // neighbour local index: mirror coordinate on this axis
+      int nc3[3] = {li, lj, lk};
+      nc3[ax] = (fc & 1) ? 0 : CB - 1;
+      const int lj2 = nc3[0] + CB * (nc3[1] + CB * nc3[2]);
+      const double T = fs.t[fc];
+#pragma unroll
+      for (int b = 0; b < LC; ++b) {
+        const double pj = phi[(nbr[fc] * LC + b) * C + lj2];
+#pragma unroll
+        for (int a = 0; a < LC; ++a) v[a * LC + b] = -T * f[a] * pj;
+      }
+    }
+    block_sum_k<C, LC * LC>(v, red);
+    if (t < LC * LC) Ac[(bc.b * 7 + 1 + fc) * LC * LC + t] = v[t];
+  }
+  // --- cc-boundary correction: faces leaving the cc element + Dirichlet terms
+  {
+    const int64_t bco[3] = {bc.bi, bc.bj, bc.bk};
+    double e = 0.0;
+#pragma unroll
+    for (int fc = 0; fc < 6; ++fc) {
+      const int ax = fc >> 1;
+      const bool hi = fc & 1;
+      const bool on_face = hi ? co[ax] == CB - 1 : co[ax] == 0;
+      if (!on_face) continue;
+      if (fs.nbmask & (1 << fc)) {
+        const bool crosses = hi ? ((bco[ax] + 1) % g.sd == 0) : (bco[ax] % g.sd == 0);
+        if (crosses) e += fs.t[fc];
+      } else if (dm & (1u << fc)) {
+        e += fs.t[fc];
+      }
+    }
+    double v[LC * LC];
+#pragma unroll
+    for (int a = 0; a < LC; ++a)
+#pragma unroll
+      for (int b = 0; b < LC; ++b) v[a * LC + b] = e * f[a] * f[b];
+    block_sum_k<C, LC * LC>(v, red);
+    if (t < LC * LC) Bc[bc.b * LC * LC + t] = v[t];
+  }
+}
+
+// ----------------------------------------------------- per-element helpers
+
+struct ElemCoord {
+  int64_t ei, ej, ek, e;
+};
+__device__ __forceinline__ ElemCoord elem_coord(const GridParams& g, int64_t e) {
+  return {e % g.ncx, (e / g.ncx) % g.ncy, e / (g.ncx * g.ncy), e};
+}
+// coarse cell (brick) id of child c (di + sd*(dj + sd*dk)) of element E
+// (HierarchicalGrid::coarse_children, grid.cpp:183-194)
+__device__ __forceinline__ int64_t child_brick(const GridParams& g, const ElemCoord& ec, int c) {
+  const int di = c % g.sd, dj = (c / g.sd) % g.sd, dk = c / (g.sd * g.sd);
+  return (ec.ei * g.sd + di) + g.nbx * ((ec.ej * g.sd + dj) + g.nby * (ec.ek * g.sd + dk));
+}
+__device__ __forceinline__ int64_t brick_nbr(const GridParams& g, int64_t b, int dir /*0..5*/) {
+  const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
+  switch (dir) {
+    case 0: return bi > 0 ? b - 1 : -1;
+    case 1: return bi + 1 < g.nbx ? b + 1 : -1;
+    case 2: return bj > 0 ? b - g.nbx : -1;
+    case 3: return bj + 1 < g.nby ? b + g.nbx : -1;
+    case 4: return bk > 0 ? b - g.nbx * g.nby : -1;
+    default: return bk + 1 < g.nbz ? b + g.nbx * g.nby : -1;
+  }
+}
+// element-local child index of brick b, or -1 if b is not in element e
+__device__ __forceinline__ int child_index(const GridParams& g, const ElemCoord& ec, int64_t b) {
+  const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
+  const int64_t di = bi - ec.ei * g.sd, dj = bj - ec.ej * g.sd, dk = bk - ec.ek * g.sd;
+  if (di < 0 || dj < 0 || dk < 0 || di >= g.sd || dj >= g.sd || dk >= g.sd) return -1;
+  return (int)(di + g.sd * (dj + g.sd * dk));
+}
+
+// Element matrix (q x q, q = sd^3 * LC) into smem: A_c restricted to E's
+// children, optionally minus Bc on diagonal blocks. Symmetrised.
+__device__ void build_elem_matrix(const GridParams& g, const ElemCoord& ec, const double* Ac,
+                                  const double* Bc, bool subtract_bc, double* M, int q) {
+  const int nch = g.sd * g.sd * g.sd;
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) M[e] = 0.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < nch * 7 * LC * LC; e += blockDim.x) {
+    const int ci = e / (7 * LC * LC), rem = e % (7 * LC * LC);
+    const int dir = rem / (LC * LC), ab = rem % (LC * LC), a = ab / LC, b = ab % LC;
+    const int64_t I = child_brick(g, ec, ci);
+    int cj;
+    if (dir == 0) cj = ci;
+    else {
+      const int64_t J = brick_nbr(g, I, dir - 1);
+      cj = J >= 0 ? child_index(g, ec, J) : -1;
+    }
+    if (cj < 0) continue;
+    double v = Ac[(I * 7 + dir) * LC * LC + ab];
+    if (dir == 0 && subtract_bc) v -= Bc[I * LC * LC + ab];
+    M[(ci * LC + a) * q + cj * LC + b] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int i = e / q, j = e % q;
+    if (i < j) {
+      const double s = 0.5 * (M[i * q + j] + M[j * q + i]);
+      M[i * q + j] = s;
+      M[j * q + i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Warp-parallel cyclic Jacobi on q x q (q <= 64) symmetric M in smem;
+// V (q x q) eigenvectors in columns. Lanes own rows r = lane, lane+32.
+__device__ void warp_jacobi(double* M, double* V, int q) {
+  const int lane = threadIdx.x & 31;
+  for (int r = lane; r < q; r += 32)
+    for (int c = 0; c < q; ++c) V[r * q + c] = r == c ? 1.0 : 0.0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int r = lane; r < q; r += 32)
+      for (int c = 0; c < q; ++c) {
+        const double v = M[r * q + c] * M[r * q + c];
+        tot += v;
+        if (r != c) off += v;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if (off <= 1e-30 * tot || off == 0.0) break;
+    for (int p = 0; p < q - 1; ++p)
+      for (int qq = p + 1; qq < q; ++qq) {
+        const double apq = M[p * q + qq];
+        const double app = M[p * q + p], aqq = M[qq * q + qq];
+        if (fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq))) continue;
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+        __syncwarp();
+        for (int r = lane; r < q; r += 32) {
+          const double akp = M[r * q + p], akq = M[r * q + qq];
+          M[r * q + p] = c * akp - s * akq;
+          M[r * q + qq] = s * akp + c * akq;
+          const double vkp = V[r * q + p], vkq = V[r * q + qq];
+          V[r * q + p] = c * vkp - s * vkq;
+          V[r * q + qq] = s * vkp + c * vkq;
+        }
+        __syncwarp();
+        for (int r = lane; r < q; r += 32) {
+          const double apk = M[p * q + r], aqk = M[qq * q + r];
+          M[p * q + r] = c * apk - s * aqk;
+          M[qq * q + r] = s * apk + c * aqk;
+        }
+        __syncwarp();
+      }
+  }
+}
+
+// One warp per cc element: projected matrix, eigenpairs, R_cc rows.
+__global__ void k_cc_basis(GridParams g, const double* __restrict__ Ac,
+                           const double* __restrict__ Bc, double* Rcc, double* cc_evals) {
+  extern __shared__ double sm[];
+  const int q = g.sd * g.sd * g.sd * LC;
+  double* M = sm;
+  double* V = M + q * q;
+  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  build_elem_matrix(g, ec, Ac, Bc, true, M, q);
+  if (threadIdx.x < 32) warp_jacobi(M, V, q);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // selection of the lcc smallest (ascending, ties by index)
+    int* used = (int*)(V + q * q);
+    for (int i = 0; i < q; ++i) used[i] = 0;
+    for (int k = 0; k < g.lcc; ++k) {
+      int best = -1;
+      for (int i = 0; i < q; ++i)
+        if (!used[i] && (best < 0 || M[i * q + i] < M[best * q + best])) best = i;
+      used[best] = 1;
+      cc_evals[blockIdx.x * g.lcc + k] = M[best * q + best];
+      double s = 0.0;
+      for (int r = 0; r < q; ++r) s += V[r * q + best];
+      const double sg = s < 0.0 ? -1.0 : 1.0;
+      for (int r = 0; r < q; ++r) Rcc[((int64_t)blockIdx.x * g.lcc + k) * q + r] = sg * V[r * q + best];
+    }
+  }
+}
+
+// In-place Gauss-Jordan inversion of an SPD matrix in smem (block-wide).
+// Records the pivots (LDL^T pivots) and applies the reference's rule.
+__device__ bool smem_gj_inverse(double* M, int n, double* col, double* rowp, double* pivs) {
+  for (int p = 0; p < n; ++p) {
+    const double pv = M[p * n + p];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      col[i] = M[i * n + p];
+      rowp[i] = M[p * n + i];
+    }
+    if (threadIdx.x == 0) pivs[p] = pv;
+    __syncthreads();
+    const double inv = 1.0 / pv;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e % n;
+      double v;
+      if (i == p && j == p) v = inv;
+      else if (i == p) v = rowp[j] * inv;
+      else if (j == p) v = -col[i] * inv;
+      else v = M[e] - col[i] * (rowp[j] * inv);
+      M[e] = v;
+    }
+    __syncthreads();
+  }
+  bool ok = true;
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int p = 0; p < n; ++p) mx = fmax(mx, fabs(pivs[p]));
+    for (int p = 0; p < n; ++p)
+      if (!(pivs[p] > 1e-14 * mx)) ok = false;
+    pivs[n] = ok ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  ok = pivs[n] != 0.0;
+  // symmetrise
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    if (i < j) {
+      const double s = 0.5 * (M[i * n + j] + M[j * n + i]);
+      M[i * n + j] = s;
+      M[j * n + i] = s;
+    }
+  }
+  __syncthreads();
+  return ok;
+}
+
+// Coarse smoother: exact inverse of A_c over each cc element's rows
+// (coarse_blocks_by_cc, solver.cpp:362-374) -> Winv[E][q][q].
+__global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, double* Winv,
+                                  int* status) {
+  extern __shared__ double sm[];
+  const int q = g.sd * g.sd * g.sd * LC;
+  double* M = sm;
+  double* col = M + q * q;
+  double* rowp = col + q;
+  double* pivs = rowp + q;
+  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  build_elem_matrix(g, ec, Ac, nullptr, false, M, q);
+  const bool ok = smem_gj_inverse(M, q, col, rowp, pivs);
+  if (!ok && threadIdx.x == 0) atomicExch(status, 2);
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Winv[(int64_t)blockIdx.x * q * q + e] = M[e];
+}
+
+// A_cc block (E, F) for F in {E, 6 face neighbours}: sum over coupled child
+// pairs (I in E, J in F) of R_E[:, I] Ac_IJ R_F[:, J]^T, written into the dense
+// n_cc x n_cc matrix. grid = (m_cc, 7), block = lcc*lcc threads.
+__global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
+                               const double* __restrict__ Rcc, double* Acc, int64_t ldacc) {
+  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
+  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  const int fdir = blockIdx.y;  // 0 self, 1..6 faces
+  int64_t F = ec.e;
+  if (fdir > 0) {
+    const int64_t coords[3] = {ec.ei, ec.ej, ec.ek};
+    const int64_t n3[3] = {g.ncx, g.ncy, g.ncz};
+    const int ax = (fdir - 1) >> 1;
+    const bool hi = (fdir - 1) & 1;
+    if (hi ? coords[ax] + 1 >= n3[ax] : coords[ax] == 0) return;
+    const int64_t strides[3] = {1, g.ncx, g.ncx * g.ncy};
+    F = hi ? ec.e + strides[ax] : ec.e - strides[ax];
+  }
+  const ElemCoord fc = elem_coord(g, F);
+  const int bb = threadIdx.x / g.lcc, bp = threadIdx.x % g.lcc;
+  if (bb >= g.lcc) return;
+  const double* RE = Rcc + (ec.e * g.lcc + bb) * q;
+  const double* RF = Rcc + (F * g.lcc + bp) * q;
+  double acc = 0.0;
+  for (int ci = 0; ci < nch; ++ci) {
+    const int64_t I = child_brick(g, ec, ci);
+    for (int dir = 0; dir < 7; ++dir) {
+      int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
+      if (J < 0) continue;
+      const int cj = child_index(g, fc, J);
+      if (cj < 0) continue;
+      const double* blk = Ac + (I * 7 + dir) * LC * LC;
+      for (int a = 0; a < LC; ++a) {
+        double s = 0.0;
+        for (int b = 0; b < LC; ++b) s += blk[a * LC + b] * RF[cj * LC + b];
+        acc += RE[ci * LC + a] * s;
+      }
+    }
+  }
+  Acc[(ec.e * g.lcc + bb) * ldacc + F * g.lcc + bp] = acc;
+}
+
+// ------------------------------------------------ coarse part of the V-cycle
+
+// C12: rc0 = Winv rc (per element), wc = rc - A_c rc0, rcc = R_cc wc.
+// rc0 at neighbouring elements is recomputed from their Winv rows.
+__global__ void k_coarse_down(GridParams g, const int* __restrict__ done,
+                              const double* __restrict__ Ac, const double* __restrict__ Winv,
+                              const double* __restrict__ Rcc, const double* __restrict__ rc,
+                              double* rc0, double* rcc) {
+  if (*done) return;
+  extern __shared__ double sm[];
+  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
+  double* r0 = sm;       // q: rc0 of this element
+  double* wc = r0 + q;   // q
+  // (rcc reduction is done by one thread per output, see below)
+  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const int64_t gi = child_brick(g, ec, i / LC) * LC + i % LC;
+    (void)gi;
+    const double* W = Winv + ((int64_t)ec.e * q + i) * q;
+    double s = 0.0;
+    for (int j = 0; j < q; ++j) s += W[j] * rc[child_brick(g, ec, j / LC) * LC + j % LC];
+    r0[i] = s;
+    rc0[child_brick(g, ec, i / LC) * LC + i % LC] = s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const int ci = i / LC, a = i % LC;
+    const int64_t I = child_brick(g, ec, ci);
+    double s = 0.0;
+    for (int dir = 0; dir < 7; ++dir) {
+      const int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
+      if (J < 0) continue;
+      const double* blk = Ac + (I * 7 + dir) * LC * LC + a * LC;
+      const int cj = child_index(g, ec, J);
+      double xj[LC];
+      if (cj >= 0) {
+        for (int b = 0; b < LC; ++b) xj[b] = r0[cj * LC + b];
+      } else {
+        // neighbour element: recompute its rc0 rows for brick J
+        const int64_t Fe = (J % g.nbx) / g.sd + g.ncx * (((J / g.nbx) % g.nby) / g.sd +
+                                                          g.ncy * ((J / (g.nbx * g.nby)) / g.sd));
+        const ElemCoord fe = elem_coord(g, Fe);
+        const int cjf = child_index(g, fe, J);
+        for (int b = 0; b < LC; ++b) {
+          const double* W = Winv + ((int64_t)Fe * q + cjf * LC + b) * q;
+          double t = 0.0;
+          for (int j = 0; j < q; ++j) t += W[j] * rc[child_brick(g, fe, j / LC) * LC + j % LC];
+          xj[b] = t;
+        }
+      }
+      for (int b = 0; b < LC; ++b) s += blk[b] * xj[b];
+    }
+    wc[i] = rc[I * LC + a] - s;
+  }
+  __syncthreads();
+  // rcc_(E,b) = sum_i R[E][b][i] wc_i   (deterministic: thread b sums in order)
+  for (int b = threadIdx.x; b < g.lcc; b += blockDim.x) {
+    const double* R = Rcc + ((int64_t)ec.e * g.lcc + b) * q;
+    double s = 0.0;
+    for (int i = 0; i < q; ++i) s += R[i] * wc[i];
+    rcc[ec.e * g.lcc + b] = s;
+  }
+
+  (void)nch;
+}
+
+// C45: rc1 = rc0 + R_cc^T ecc (recomputed at neighbouring elements' cells),
+// tc = rc - A_c rc1, ec = rc1 + Winv tc.
+__global__ void k_coarse_up(GridParams g, const int* __restrict__ done,
+                            const double* __restrict__ Ac, const double* __restrict__ Winv,
+                            const double* __restrict__ Rcc, const double* __restrict__ rc,
+                            const double* __restrict__ rc0, const double* __restrict__ ecc,
+                            double* ec_out) {
+  if (*done) return;
+  extern __shared__ double sm[];
+  const int q = g.sd * g.sd * g.sd * LC;
+  double* r1 = sm;      // q
+  double* tc = r1 + q;  // q
+  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  auto rc1_at = [&](int64_t J, int b) -> double {
+    // rc1 of coarse dof (J, b): rc0 + sum_k R[F][k][(cj, b)] ecc[F][k]
+    const int64_t Fe = (J % g.nbx) / g.sd + g.ncx * (((J / g.nbx) % g.nby) / g.sd +
+                                                      g.ncy * ((J / (g.nbx * g.nby)) / g.sd));
+    const ElemCoord fe = elem_coord(g, Fe);
+    const int cj = child_index(g, fe, J);
+    double s = rc0[J * LC + b];
+    double acc = 0.0;
+    for (int k = 0; k < g.lcc; ++k)
+      acc += Rcc[((int64_t)Fe * g.lcc + k) * q + cj * LC + b] * ecc[Fe * g.lcc + k];
+    return s + acc;
+  };
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const int64_t I = child_brick(g, ec, i / LC);
+    r1[i] = rc1_at(I, i % LC);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const int ci = i / LC, a = i % LC;
+    const int64_t I = child_brick(g, ec, ci);
+    double s = 0.0;
+    for (int dir = 0; dir < 7; ++dir) {
+      const int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
+      if (J < 0) continue;
+      const double* blk = Ac + (I * 7 + dir) * LC * LC + a * LC;
+      const int cj = child_index(g, ec, J);
+      for (int b = 0; b < LC; ++b) s += blk[b] * (cj >= 0 ? r1[cj * LC + b] : rc1_at(J, b));
+    }
+    tc[i] = rc[I * LC + a] - s;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const double* W = Winv + ((int64_t)ec.e * q + i) * q;
+    double s = 0.0;
+    for (int j = 0; j < q; ++j) s += W[j] * tc[j];
+    ec_out[child_brick(g, ec, i / LC) * LC + i % LC] = r1[i] + s;
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                          const double* phi, double* Ac, double* Bc, cudaStream_t s) {
+  if (cb == 8)
+    k_coarse_blocks<8><<<(unsigned)g.nb, 512, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+  else
+    k_coarse_blocks<4><<<(unsigned)g.nb, 64, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+}
+
+void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, double* Rcc,
+                     double* cc_evals, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const size_t smem = sizeof(double) * (size_t)(2 * q * q + q + 8);
+  cudaFuncSetAttribute(k_cc_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cc_basis<<<(unsigned)g.ncc, 64, smem, s>>>(g, Ac, Bc, Rcc, cc_evals);
+}
+
+void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
+                            cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const size_t smem = sizeof(double) * (size_t)(q * q + 3 * q + 8);
+  cudaFuncSetAttribute(k_coarse_smoother, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_coarse_smoother<<<(unsigned)g.ncc, 256, smem, s>>>(g, Ac, Winv, status);
+}
+
+void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
+                         cudaStream_t s) {
+  const int64_t n = g.ncc * g.lcc;
+  cudaMemsetAsync(Acc, 0, sizeof(double) * (size_t)(n * n), s);
+  dim3 grid((unsigned)g.ncc, 7);
+  k_acc_assemble<<<grid, g.lcc * g.lcc, 0, s>>>(g, Ac, Rcc, Acc, n);
+}
+
+void launch_coarse_down(const GridParams& g, const int* done, const double* Ac, const double* Winv,
+                        const double* Rcc, const double* rc, double* rc0, double* rcc,
+                        cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const size_t smem = sizeof(double) * (size_t)(2 * q + 32 * g.lcc);
+  k_coarse_down<<<(unsigned)g.ncc, 64, smem, s>>>(g, done, Ac, Winv, Rcc, rc, rc0, rcc);
+}
+
+void launch_coarse_up(const GridParams& g, const int* done, const double* Ac, const double* Winv,
+                      const double* Rcc, const double* rc, const double* rc0, const double* ecc,
+                      double* ec, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const size_t smem = sizeof(double) * (size_t)(2 * q);
+  k_coarse_up<<<(unsigned)g.ncc, 64, smem, s>>>(g, done, Ac, Winv, Rcc, rc, rc0, ecc, ec);
+}
+
+int compiled_lc() { return LC; }
+
+}  // namespace tmg

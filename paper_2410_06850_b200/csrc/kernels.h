@@ -1,0 +1,93 @@
+// Host-visible launchers of the device kernels (one translation unit each).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace tmg {
+
+enum : int {
+  kStatusRunning = 0,
+  kStatusConverged = 1,
+  kStatusMaxIt = 2,
+  kStatusZeroRhs = 3,
+  kStatusIndefinite = 4,
+  kStatusNonFinite = 5,
+};
+
+// Device-resident CG scalars (one per solve context).
+struct PcgState {
+  double bnorm, rnorm, rho, alpha, beta, pq, rtol;
+  int it, maxit, done, status, first;
+  unsigned int ticket[8];
+};
+
+// operator.cu
+void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
+void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
+void launch_conductivity(const double* x, double* kappa, int64_t m, double lo, double hi, int p,
+                         cudaStream_t s);
+void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
+                     double ly, double lz, const double* kappa, const double* source,
+                     uint8_t* dmask, double* rhs, unsigned long long* count, cudaStream_t s);
+void launch_apply(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                  const double* x, double* y, double* dinv, cudaStream_t s);
+
+// setup_fine.cu
+void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                          double* G, int* status, cudaStream_t s);
+int64_t thomas_doubles_per_brick(int cb);
+
+// spectral.cu
+void launch_local_basis(const GridParams& g, int cb, const double* kappa, double* phi,
+                        double* evals, int* iters, double tol, int degree, int max_outer,
+                        cudaStream_t s);
+
+// coarse.cu
+int compiled_lc();
+void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                          const double* phi, double* Ac, double* Bc, cudaStream_t s);
+void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, double* Rcc,
+                     double* cc_evals, cudaStream_t s);
+void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
+                            cudaStream_t s);
+void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
+                         cudaStream_t s);
+void launch_coarse_down(const GridParams& g, const int* done, const double* Ac, const double* Winv,
+                        const double* Rcc, const double* rc, double* rc0, double* rcc,
+                        cudaStream_t s);
+void launch_coarse_up(const GridParams& g, const int* done, const double* Ac, const double* Winv,
+                      const double* Rcc, const double* rc, const double* rc0, const double* ecc,
+                      double* ec, cudaStream_t s);
+
+// dense.cu
+void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
+int64_t dense_inverse_work_doubles(int64_t n);
+void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
+                 cudaStream_t s);
+
+// pcg.cu
+void init_kernel_attributes();
+void launch_init(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                 const double* b, double* x, int has_x0, double* r, PcgState* st, double* partials,
+                 cudaStream_t s);
+void launch_search(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                   const double* z, const double* p_old, double* p, double* q, PcgState* st,
+                   double* partials, cudaStream_t s);
+void launch_update(const GridParams& g, int cb, const double* kappa, const double* Gf, double* x,
+                   const double* p, const double* q, double* r, double* r1, PcgState* st,
+                   double* partials, double* history, int init, cudaStream_t s);
+void launch_restrict(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                     const double* phi, const double* r, const double* r1, double* rc,
+                     const PcgState* st, cudaStream_t s);
+void launch_post(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                 const double* phi, const double* Gf, const double* r, const double* r1,
+                 const double* ec, double* z, PcgState* st, double* partials, int init,
+                 cudaStream_t s);
+void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
+                        const double* q, double* r, double* z, PcgState* st, double* partials,
+                        double* history, int init, cudaStream_t s);
+
+}  // namespace tmg

@@ -1,0 +1,172 @@
+// Fine-grid elementwise / stencil kernels: layout permutation at the C-ABI
+// boundary, SIMP conductivity, Dirichlet face masks, the right-hand side, the
+// matrix-free TPFA apply and the Jacobi diagonal.
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace tmg {
+
+// global x-fastest index of brick-layout slot s
+__device__ __forceinline__ int64_t brick_to_global(const GridParams& g, int cb, int64_t s) {
+  const int c = cb * cb * cb;
+  const int64_t b = s / c;
+  const int l = (int)(s % c);
+  const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
+  const int li = l % cb, lj = (l / cb) % cb, lk = l / (cb * cb);
+  const int64_t i = bi * cb + li, j = bj * cb + lj, k = bk * cb + lk;
+  return i + g.nx * (j + g.ny * k);
+}
+
+__global__ void k_to_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
+                           int64_t m) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x)
+    dst[s] = src[brick_to_global(g, cb, s)];
+}
+
+__global__ void k_from_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
+                             int64_t m) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x)
+    dst[brick_to_global(g, cb, s)] = src[s];
+}
+
+// material.cpp:45-59 — kappa = lo + x^p (hi - lo), repeated multiply
+__global__ void k_conductivity(const double* __restrict__ x, double* kappa, int64_t m, double lo,
+                               double hi, int p) {
+  const double dk = hi - lo;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    double r = 1.0;
+    for (int i = 0; i < p; ++i) r = __dmul_rn(r, x[s]);
+    kappa[s] = __dadd_rn(lo, __dmul_rn(r, dk));
+  }
+}
+
+struct PatchSet {
+  int n;
+  Patch p[kMaxPatches];
+  double lx, ly, lz;
+};
+
+// grid.cpp:61-75 (face-centre containment, inclusive bounds)
+__device__ bool dirichlet_value(const GridParams& g, const PatchSet& ps, int64_t i, int64_t j,
+                                int64_t k, int face, double* value) {
+  bool on = false;
+  switch (face) {
+    case 0: on = i == 0; break;
+    case 1: on = i == g.nx - 1; break;
+    case 2: on = j == 0; break;
+    case 3: on = j == g.ny - 1; break;
+    case 4: on = k == 0; break;
+    default: on = k == g.nz - 1; break;
+  }
+  if (!on) return false;
+  const double cx = __dmul_rn((double)i + 0.5, g.hx);
+  const double cy = __dmul_rn((double)j + 0.5, g.hy);
+  const double cz = __dmul_rn((double)k + 0.5, g.hz);
+  double u, v;
+  if (face <= 1) { u = cy; v = cz; }
+  else if (face <= 3) { u = cx; v = cz; }
+  else { u = cx; v = cy; }
+  for (int q = 0; q < ps.n; ++q) {
+    const Patch& p = ps.p[q];
+    if (p.face != face) continue;
+    if (u >= p.u0 && u <= p.u1 && v >= p.v0 && v <= p.v1) {
+      if (value) *value = p.value;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Per-cell Dirichlet face bits (brick layout) and the rhs
+// b = f*vol + sum_D t_D * T_D in the reference face order (fvm.cpp:63-112).
+__global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __restrict__ kappa,
+                           const double* __restrict__ source, uint8_t* dmask, double* rhs,
+                           int64_t m, unsigned long long* count) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int c = cb * cb * cb;
+    const int64_t b = s / c;
+    const int l = (int)(s % c);
+    const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
+    const int64_t i = bi * cb + l % cb, j = bj * cb + (l / cb) % cb, k = bk * cb + l / (cb * cb);
+    unsigned mask = 0;
+    double bval = source ? __dmul_rn(source[s], g.vol) : 0.0;
+    const bool bnd = i == 0 || j == 0 || k == 0 || i == g.nx - 1 || j == g.ny - 1 || k == g.nz - 1;
+    if (bnd) {
+      for (int f = 0; f < 6; ++f) {
+        double td = 0.0;
+        if (dirichlet_value(g, ps, i, j, k, f, &td)) {
+          mask |= 1u << f;
+          const double t = __dmul_rn(__dmul_rn(2.0, kappa[s]), g.cpl[f >> 1]);
+          bval = __dadd_rn(bval, __dmul_rn(t, td));
+        }
+      }
+      if (mask && count) atomicAdd(count, (unsigned long long)__popc(mask));
+    }
+    dmask[s] = (uint8_t)mask;
+    if (rhs) rhs[s] = bval;
+  }
+}
+
+// y = A x (bitwise SparseOperator::apply), optionally also dinv = 1/diag.
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_apply(GridParams g, const double* __restrict__ kappa,
+                                                       const uint8_t* __restrict__ dmask,
+                                                       const double* __restrict__ x, double* y,
+                                                       double* dinv) {
+  __shared__ double kt[Tile<CB>::N];
+  __shared__ double xt[Tile<CB>::N];
+  constexpr int C = CB * CB * CB;
+  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  load_tile<CB, true>(kappa, kt, g, bc);
+  if (x) load_tile<CB, true>(x, xt, g, bc);
+  __syncthreads();
+  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  const unsigned dm = brick_on_boundary(g, bc) ? dmask[bc.b * C + t] : 0u;
+  const FaceSet fs = cell_faces<CB>(kt, li, lj, lk, g, bc, dm);
+  if (y) y[bc.b * C + t] = apply_row<CB>(fs, xt, li, lj, lk);
+  if (dinv) dinv[bc.b * C + t] = 1.0 / fs.diag;  // solver.cpp:27
+}
+
+static int grid1d(int64_t m) {
+  int64_t b = (m + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s) {
+  const int64_t m = g.nx * g.ny * g.nz;
+  k_to_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, m);
+}
+void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst,
+                       cudaStream_t s) {
+  const int64_t m = g.nx * g.ny * g.nz;
+  k_from_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, m);
+}
+void launch_conductivity(const double* x, double* kappa, int64_t m, double lo, double hi, int p,
+                         cudaStream_t s) {
+  k_conductivity<<<grid1d(m), 256, 0, s>>>(x, kappa, m, lo, hi, p);
+}
+void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
+                     double ly, double lz, const double* kappa, const double* source,
+                     uint8_t* dmask, double* rhs, unsigned long long* count, cudaStream_t s) {
+  PatchSet ps{};
+  ps.n = npatch;
+  for (int i = 0; i < npatch && i < kMaxPatches; ++i) ps.p[i] = patches[i];
+  ps.lx = lx; ps.ly = ly; ps.lz = lz;
+  const int64_t m = g.nx * g.ny * g.nz;
+  k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, m, count);
+}
+void launch_apply(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                  const double* x, double* y, double* dinv, cudaStream_t s) {
+  if (cb == 8)
+    k_apply<8><<<(unsigned)g.nb, 512, 0, s>>>(g, kappa, dmask, x, y, dinv);
+  else
+    k_apply<4><<<(unsigned)g.nb, 64, 0, s>>>(g, kappa, dmask, x, y, dinv);
+}
+
+}  // namespace tmg

@@ -1,0 +1,377 @@
+// Batched local spectral bases, one coarse cell per CTA (north_star item 4).
+//
+// Reference: local_spectral_basis (proj/core/src/coarse_space.cpp:279-304):
+// per coarse cell, the L_c smallest eigenpairs of S_loc phi = lambda M_loc phi
+// with S_loc the TPFA stiffness over faces strictly inside the cell
+// (box_interior_stiffness, :238-277) and M_loc = diag(kappa * vol), solved via
+// B = M^-1/2 S M^-1/2 (generalized_smallest, :203-234) and returned
+// M-orthonormal (phi = M^-1/2 v). The reference uses a dense symmetric
+// eigensolver (:38-56). Here the problem never leaves shared memory: B is
+// applied matrix-free from the cell's face transmissibilities and the lowest
+// eigenvectors are found by Chebyshev-filtered subspace iteration with a block
+// of K = 2 L_c vectors (Rayleigh-Ritz + CholQR each outer step), stopping when
+// every wanted Ritz pair has ||B x - theta x|| <= tol * ||B||. The constant
+// mode (B M^{1/2} 1 = 0) seeds the block.
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace tmg {
+
+__device__ __forceinline__ double hash_uniform(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t z = a * 0x9E3779B97F4A7C15ULL ^ (b + 0x632BE59BD9B4E019ULL) * 0xBF58476D1CE4E5B9ULL ^
+               (c + 0x94D049BB133111EBULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return (double)(z >> 11) * 0x1.0p-53 - 0.5;
+}
+
+// Cyclic Jacobi eigen-decomposition of a K x K symmetric matrix (single thread).
+// a: row-major, destroyed (diag -> eigenvalues). v: eigenvectors in columns.
+template <int K>
+__device__ void jacobi_eig_small(double* a, double* v) {
+  for (int i = 0; i < K; ++i)
+    for (int j = 0; j < K; ++j) v[i * K + j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < K; ++i)
+      for (int j = 0; j < K; ++j) {
+        tot += a[i * K + j] * a[i * K + j];
+        if (i != j) off += a[i * K + j] * a[i * K + j];
+      }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int p = 0; p < K - 1; ++p)
+      for (int q = p + 1; q < K; ++q) {
+        const double apq = a[p * K + q];
+        if (apq == 0.0) continue;
+        const double app = a[p * K + p], aqq = a[q * K + q];
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < K; ++k) {
+          const double akp = a[k * K + p], akq = a[k * K + q];
+          a[k * K + p] = c * akp - s * akq;
+          a[k * K + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < K; ++k) {
+          const double apk = a[p * K + k], aqk = a[q * K + k];
+          a[p * K + k] = c * apk - s * aqk;
+          a[q * K + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < K; ++k) {
+          const double vkp = v[k * K + p], vkq = v[k * K + q];
+          v[k * K + p] = c * vkp - s * vkq;
+          v[k * K + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+}
+
+template <int CB, int K>
+struct ChfsiCtx {
+  static constexpr int C = CB * CB * CB;
+  static constexpr int NW = C / 32;
+};
+
+// y = B x for K vectors held in registers; u smem [K][C].
+template <int CB, int K>
+__device__ __forceinline__ void bmatvec(const double (&x)[K], double (&y)[K], double* u,
+                                        const double* tf, double sl, double sll, int nb[6]) {
+  constexpr int C = CB * CB * CB;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < K; ++k) u[k * C + t] = sl * x[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = sll * u[k * C + t];
+#pragma unroll
+    for (int f = 0; f < 6; ++f)
+      if (nb[f] >= 0) s -= tf[f] * u[k * C + nb[f]];
+    y[k] = sl * s;
+  }
+  __syncthreads();
+}
+
+// Gram matrix G = X^T Y (K x K, symmetric assumed if SYM) -> smem g[K*K]
+template <int CB, int K>
+__device__ __forceinline__ void gram(const double (&x)[K], const double (&y)[K], double* red,
+                                     double* g) {
+  constexpr int NP = K * (K + 1) / 2;
+  double v[NP];
+  int e = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) v[e++] = x[i] * y[j] + (i == j ? 0.0 : 0.0);
+  block_sum_k<CB * CB * CB, NP>(v, red);
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int i = 0; i < K; ++i)
+      for (int j = 0; j <= i; ++j) {
+        g[i * K + j] = v[q];
+        g[j * K + i] = v[q];
+        ++q;
+      }
+  }
+  __syncthreads();
+}
+
+// Symmetrised Gram for Rayleigh-Ritz: H_ij = (x_i . y_j + x_j . y_i) / 2
+template <int CB, int K>
+__device__ __forceinline__ void gram_sym(const double (&x)[K], const double (&y)[K], double* red,
+                                         double* g) {
+  constexpr int NP = K * (K + 1) / 2;
+  double v[NP];
+  int e = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) v[e++] = 0.5 * (x[i] * y[j] + x[j] * y[i]);
+  block_sum_k<CB * CB * CB, NP>(v, red);
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int i = 0; i < K; ++i)
+      for (int j = 0; j <= i; ++j) {
+        g[i * K + j] = v[q];
+        g[j * K + i] = v[q];
+        ++q;
+      }
+  }
+  __syncthreads();
+}
+
+// X <- X R^{-1} where G = R^T R (Cholesky of the Gram matrix in smem).
+// Returns false if G is not numerically positive definite.
+template <int K>
+__device__ __forceinline__ bool cholqr_apply(double (&x)[K], const double* g, double* rsm,
+                                             int* okflag) {
+  if (threadIdx.x == 0) {
+    // R upper: G = R^T R
+    double R[K * K];
+    bool ok = true;
+    double gmax = 0.0;
+    for (int i = 0; i < K; ++i) gmax = fmax(gmax, g[i * K + i]);
+    for (int i = 0; i < K && ok; ++i) {
+      for (int j = i; j < K; ++j) {
+        double s = g[i * K + j];
+        for (int k = 0; k < i; ++k) s -= R[k * K + i] * R[k * K + j];
+        if (j == i) {
+          if (!(s > 1e-28 * gmax)) { ok = false; break; }
+          R[i * K + i] = sqrt(s);
+        } else {
+          R[i * K + j] = s / R[i * K + i];
+        }
+      }
+    }
+    for (int i = 0; i < K * K; ++i) rsm[i] = ok ? R[i] : 0.0;
+    *okflag = ok;
+  }
+  __syncthreads();
+  const bool ok = *okflag;
+  if (ok) {
+    // row vector x (1 x K) times R^{-1}: solve y R = x, forward over columns
+    double y[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double s = x[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) s -= y[k] * rsm[k * K + j];
+      y[j] = s / rsm[j * K + j];
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[j] = y[j];
+  }
+  __syncthreads();
+  return ok;
+}
+
+template <int CB, int K>
+__global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
+                                                             const double* __restrict__ kappa,
+                                                             double* phi, double* evals,
+                                                             int* iters_out, double tol,
+                                                             int degree, int max_outer) {
+  constexpr int C = CB * CB * CB;
+  constexpr int NW = C / 32;
+  constexpr int NP = K * (K + 1) / 2;
+  extern __shared__ double sm[];
+  double* u = sm;                     // K*C exchange buffer
+  double* kt = u + K * C;             // C
+  double* red = kt + C;               // NP*NW + NP
+  double* gs = red + NP * NW + NP + 8;  // K*K
+  double* qv = gs + K * K;            // K*K
+  double* rsm = qv + K * K;           // K*K
+  double* scal = rsm + K * K;         // 8 scalars
+  __shared__ int okflag;
+  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  const int64_t b = blockIdx.x;
+  kt[t] = kappa[b * C + t];
+  __syncthreads();
+  // interior-face transmissibilities (coarse_space.cpp:264-274)
+  const double cp[3] = {g.cpl[0], g.cpl[1], g.cpl[2]};
+  int nb[6];
+  double tf[6];
+  double sll = 0.0;
+  {
+    const int co[3] = {li, lj, lk};
+    const int st[3] = {1, CB, CB * CB};
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int ax = f >> 1;
+      const bool hi = f & 1;
+      const bool exists = hi ? co[ax] + 1 < CB : co[ax] > 0;
+      nb[f] = exists ? (hi ? t + st[ax] : t - st[ax]) : -1;
+      tf[f] = exists ? face_t(kt[t], kt[nb[f]]) * cp[ax] : 0.0;
+      sll += tf[f];
+    }
+  }
+  const double mass = kt[t] * g.vol;
+  const double sl = 1.0 / sqrt(mass);
+  // Gershgorin bound of B
+  double gr = sl * sll * sl;
+#pragma unroll
+  for (int f = 0; f < 6; ++f)
+    if (nb[f] >= 0) gr += sl * tf[f] / sqrt(kt[nb[f]] * g.vol);
+  for (int o = 16; o > 0; o >>= 1) gr = fmax(gr, __shfl_xor_sync(0xffffffffu, gr, o));
+  if ((t & 31) == 0) red[t >> 5] = gr;
+  __syncthreads();
+  if (t == 0) {
+    double m = 0.0;
+    for (int w = 0; w < NW; ++w) m = fmax(m, red[w]);
+    scal[0] = m;
+  }
+  __syncthreads();
+  const double bmax = scal[0];
+  __syncthreads();
+  // initial block: constant mode in B-space (sqrt(mass)) + pseudo-random
+  double x[K], y[K];
+  x[0] = sqrt(mass);
+#pragma unroll
+  for (int k = 1; k < K; ++k) x[k] = hash_uniform(b, t, k);
+  double theta[K];
+  double a_cut = 0.5 * bmax;
+  int outer = 0;
+  bool converged = false;
+  for (outer = 0; outer <= max_outer; ++outer) {
+    // --- orthonormalise (CholQR twice) ---
+    for (int pass = 0; pass < 2; ++pass) {
+      gram<CB, K>(x, x, red, gs);
+      if (!cholqr_apply<K>(x, gs, rsm, &okflag)) {
+        // rank loss: re-seed the trailing vectors and retry next pass
+#pragma unroll
+        for (int k = 1; k < K; ++k) x[k] += 1e-3 * hash_uniform(b + 7777, t, k + 31 * outer);
+      }
+    }
+    // --- Rayleigh-Ritz ---
+    bmatvec<CB, K>(x, y, u, tf, sl, sll, nb);
+    gram_sym<CB, K>(x, y, red, gs);
+    if (t == 0) {
+      double a[K * K], v[K * K];
+      for (int i = 0; i < K * K; ++i) a[i] = gs[i];
+      jacobi_eig_small<K>(a, v);
+      // sort ascending
+      int ord[K];
+      for (int i = 0; i < K; ++i) ord[i] = i;
+      for (int i = 0; i < K; ++i)
+        for (int j = i + 1; j < K; ++j)
+          if (a[ord[j] * K + ord[j]] < a[ord[i] * K + ord[i]]) {
+            const int tmp = ord[i]; ord[i] = ord[j]; ord[j] = tmp;
+          }
+      for (int c = 0; c < K; ++c) {
+        scal[c] = a[ord[c] * K + ord[c]];
+        for (int r = 0; r < K; ++r) qv[r * K + c] = v[r * K + ord[c]];
+      }
+    }
+    __syncthreads();
+    double xn[K], yn[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      theta[c] = scal[c];
+      double s = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        s += x[r] * qv[r * K + c];
+        s2 += y[r] * qv[r * K + c];
+      }
+      xn[c] = s;
+      yn[c] = s2;
+    }
+    __syncthreads();
+    // residual norms of the wanted pairs
+    double rs[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const double rv = yn[c] - theta[c] * xn[c];
+      rs[c] = rv * rv;
+      x[c] = xn[c];
+    }
+    block_sum_k<C, K>(rs, red);
+    double worst = 0.0;
+    for (int c = 0; c < g.lc; ++c) worst = fmax(worst, sqrt(rs[c]));
+    if (worst <= tol * bmax) { converged = true; break; }
+    if (outer == max_outer) break;
+    // --- Chebyshev filter damping [a_cut, bmax], normalised at 0 ---
+    a_cut = fmin(fmax(theta[K - 1], 1e-6 * bmax), 0.95 * bmax);
+    const double e = 0.5 * (bmax - a_cut), c0 = 0.5 * (bmax + a_cut);
+    const double sigma1 = e / (0.0 - c0);
+    double sigma = sigma1;
+    const double gam = 2.0 / sigma1;
+    double x0[K];
+    bmatvec<CB, K>(x, y, u, tf, sl, sll, nb);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      x0[k] = x[k];
+      y[k] = (y[k] - c0 * x[k]) * (sigma1 / e);
+    }
+    for (int d = 2; d <= degree; ++d) {
+      const double sig2 = 1.0 / (gam - sigma);
+      double by[K];
+      bmatvec<CB, K>(y, by, u, tf, sl, sll, nb);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double ynew = (by[k] - c0 * y[k]) * (2.0 * sig2 / e) - (sigma * sig2) * x0[k];
+        x0[k] = y[k];
+        y[k] = ynew;
+      }
+      sigma = sig2;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) x[k] = y[k];
+  }
+  // sign convention: sum of each vector >= 0
+  double sg[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) sg[k] = x[k] * sl;
+  block_sum_k<C, K>(sg, red);
+  for (int a = 0; a < g.lc; ++a) {
+    const double sgn = sg[a] < 0.0 ? -1.0 : 1.0;
+    phi[(b * g.lc + a) * C + t] = sgn * sl * x[a];
+  }
+  if (t == 0) {
+    for (int a = 0; a < g.lc; ++a) evals[b * g.lc + a] = theta[a];
+    iters_out[b] = converged ? outer : -outer - 1;
+  }
+}
+
+size_t local_basis_smem(int cb, int K) {
+  const int C = cb * cb * cb, NW = C / 32, NP = K * (K + 1) / 2;
+  return sizeof(double) * (size_t)(K * C + C + NP * NW + NP + 8 + 3 * K * K + K + 8);
+}
+
+void launch_local_basis(const GridParams& g, int cb, const double* kappa, double* phi,
+                        double* evals, int* iters, double tol, int degree, int max_outer,
+                        cudaStream_t s) {
+  const size_t smem = local_basis_smem(cb, 8);
+  if (cb == 8) {
+    cudaFuncSetAttribute(k_local_basis<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_local_basis<8, 8><<<(unsigned)g.nb, 512, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+                                                         max_outer);
+  } else {
+    cudaFuncSetAttribute(k_local_basis<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_local_basis<4, 8><<<(unsigned)g.nb, 64, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+                                                        max_outer);
+  }
+}
+
+}  // namespace tmg

@@ -1,0 +1,107 @@
+"""Seeded synthetic inputs with the BASELINE.json configs' shapes.
+
+No public dataset is involved: BASELINE.json's designs are generated here
+(SURVEY.md §0 M4, §8(d)). The generator reuses the reference's LCG
+(Lcg64, proj/core/include/topmg/rng.hpp:13-29; default seed 20240501,
+config.hpp:56) and its top-k tie rule (rng.cpp:39-51), with BASELINE's
+radius-r box filter in place of the reference's 7-point averaging. The
+operation order (separable window sums x, y, z in increasing index order,
+division by count_x*count_y*count_z) is fixed so that the oracle's C
+restatement (oracle/topmg_oracle.c: orc_box_filter_design) produces
+bit-identical fields.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+_A = np.uint64(6364136223846793005)
+_C = np.uint64(1442695040888963407)
+
+
+def lcg_uniforms(count: int, seed: int) -> np.ndarray:
+    """Lcg64(seed).next_uniform() x count (rng.hpp:17-25), vectorised by
+    jump-ahead in blocks."""
+    B = 4096
+    # A_k = a^k, C_k = c (a^{k-1} + ... + 1), k = 1..B  (mod 2^64)
+    ak = np.empty(B, dtype=np.uint64)
+    ck = np.empty(B, dtype=np.uint64)
+    a, c = np.uint64(1), np.uint64(0)
+    with np.errstate(over="ignore"):
+        for k in range(B):
+            a = a * _A
+            c = c * _A + _C
+            ak[k] = a
+            ck[k] = c
+        out = np.empty(count, dtype=np.float64)
+        s = np.uint64(seed)
+        for start in range(0, count, B):
+            n = min(B, count - start)
+            states = ak[:n] * s + ck[:n]
+            out[start:start + n] = (states >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+            s = states[n - 1]
+    return out
+
+
+def _window_sum(f: np.ndarray, axis: int, r: int) -> np.ndarray:
+    n = f.shape[axis]
+    out = np.zeros_like(f)
+    for d in range(-r, r + 1):
+        # out[i] += f[i + d] for valid i + d, in increasing d (= increasing index)
+        lo_dst, hi_dst = max(0, -d), min(n, n - d)
+        if hi_dst <= lo_dst:
+            continue
+        dst = [slice(None)] * 3
+        src = [slice(None)] * 3
+        dst[axis] = slice(lo_dst, hi_dst)
+        src[axis] = slice(lo_dst + d, hi_dst + d)
+        out[tuple(dst)] += f[tuple(src)]
+    return out
+
+
+def _counts(n: int, r: int) -> np.ndarray:
+    i = np.arange(n)
+    return (np.minimum(i + r, n - 1) - np.maximum(i - r, 0) + 1).astype(np.float64)
+
+
+def binarize_top(field: np.ndarray, vf: float) -> np.ndarray:
+    """ceil(vf*M) largest values -> 1, ties by lower index (rng.cpp:39-51)."""
+    m = field.size
+    solid = min(m, int(np.ceil(vf * m)))
+    order = np.lexsort((np.arange(m), -field))
+    rho = np.zeros(m)
+    rho[order[:solid]] = 1.0
+    return rho
+
+
+def box_filter_design(n, vf: float, seed: int = 20240501, passes: int = 3,
+                      radius: int = 2) -> np.ndarray:
+    """BASELINE.json configs[0]/[1] density: uniform noise, `passes` box means
+    of radius `radius`, thresholded to volume fraction vf. Returns rho in
+    {0, 1}, x-fastest cell order."""
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    f = lcg_uniforms(nx * ny * nz, seed).reshape(nz, ny, nx)  # [k][j][i]
+    cx, cy, cz = _counts(nx, radius), _counts(ny, radius), _counts(nz, radius)
+    denom = (cx[None, None, :] * cy[None, :, None]) * cz[:, None, None]
+    for _ in range(passes):
+        t = _window_sum(f, 2, radius)
+        t = _window_sum(t, 1, radius)
+        t = _window_sum(t, 0, radius)
+        f = t / denom
+    return binarize_top(f.ravel(), vf)
+
+
+def conductivity(rho: np.ndarray, kappa_lo: float, kappa_hi: float = 1.0, p: int = 3):
+    """SIMP kappa = lo + rho^p (hi - lo) by repeated multiplication
+    (material.cpp:45-59)."""
+    r = np.ones_like(rho)
+    for _ in range(p):
+        r = r * rho
+    return kappa_lo + r * (kappa_hi - kappa_lo)
+
+
+# BASELINE.json configs (SURVEY.md §8 size / hierarchy tables)
+CONFIGS = {
+    0: dict(n=64, vf=0.3, passes=3, radius=2, kmin=1e-3, ncc=4, sd=2),
+    1: dict(n=128, vf=0.3, passes=3, radius=2, kmin=1e-6, ncc=8, sd=2),
+    3: dict(n=512, vf=0.2, passes=3, radius=4, kmin=1e-6, ncc=8, sd=8),
+}

@@ -1,0 +1,368 @@
+"""Python front-end over the C ABI (include/topmg_b200.h).
+
+Mirrors the reference's solver interface (proj/core/include/topmg/solver.hpp)
+so the tests read like the reference's: ``GridSpec``, ``BoundarySpec``,
+``MmgOptions``, ``PrecondKind``, ``make_preconditioner`` and ``pcg`` with the
+same argument meaning and the same error classes (``ConfigError``,
+``SolverError``, ``ValueError`` for std::invalid_argument). All compute runs in
+``libtopmg_b200.so``; there is no CPU fallback — importing the native library
+fails loudly when it has not been built.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtopmg_b200.so")
+
+TMG_OK, TMG_ECONFIG, TMG_ESOLVER, TMG_EARG, TMG_ECUDA, TMG_ENOTSUP = range(6)
+
+
+class ConfigError(RuntimeError):
+    """topmg::ConfigError (grid.hpp:16-19)."""
+
+
+class SolverError(RuntimeError):
+    """topmg::SolverError (grid.hpp:21-24)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NotSupportedError(RuntimeError):
+    pass
+
+
+class _Grid(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
+                ("ncc", C.c_int64 * 3), ("sd", C.c_int64)]
+
+
+class _Patch(C.Structure):
+    _fields_ = [("face", C.c_int), ("u0", C.c_double), ("v0", C.c_double),
+                ("u1", C.c_double), ("v1", C.c_double), ("value", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("kind", C.c_int), ("num_local_basis", C.c_int64),
+                ("num_cc_basis", C.c_int64), ("smoother_sweeps", C.c_int),
+                ("eig_tol", C.c_double), ("eig_degree", C.c_int), ("eig_max_outer", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("status", C.c_int),
+                ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
+                ("final_relative_residual", C.c_double)]
+
+
+_lib = None
+_DP = C.POINTER(C.c_double)
+
+
+def native():
+    """Load libtopmg_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C {_HERE}` or "
+                "`python -c 'import __graft_entry__; __graft_entry__.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.tmg_last_error.restype = C.c_char_p
+        L.tmg_last_error.argtypes = [C.c_void_p]
+        L.tmg_device_bytes.restype = C.c_int64
+        L.tmg_stream.restype = C.c_void_p
+        L.tmg_destroy.argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = (
+    "tmg_create", "tmg_destroy", "tmg_last_error", "tmg_set_conductivity", "tmg_set_design",
+    "tmg_assemble_rhs", "tmg_setup", "tmg_pcg", "tmg_apply_operator",
+    "tmg_apply_preconditioner", "tmg_upload_rhs", "tmg_upload_x0", "tmg_solve_resident",
+    "tmg_download_solution", "tmg_get_local_bases", "tmg_get_coarse_operator",
+    "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
+    "tmg_stream",
+)
+
+
+def _raise(code: int, msg: str):
+    if code == TMG_OK:
+        return
+    cls = {TMG_ECONFIG: ConfigError, TMG_ESOLVER: SolverError, TMG_EARG: ValueError,
+           TMG_ECUDA: CudaError, TMG_ENOTSUP: NotSupportedError}.get(code, RuntimeError)
+    raise cls(msg)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_DP)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ------------------------------------------------------------------ inputs
+
+@dataclass
+class GridSpec:
+    """GridSpec (grid.hpp:30-55)."""
+    nx: int
+    ny: int
+    nz: int
+    lx: float = 1.0
+    ly: float = 1.0
+    lz: float = 1.0
+
+    def num_cells(self):
+        return self.nx * self.ny * self.nz
+
+
+@dataclass
+class DirichletPatch:
+    face: int
+    u0: float
+    v0: float
+    u1: float
+    v1: float
+    value: float = 0.0
+
+
+@dataclass
+class BoundarySpec:
+    """BoundarySpec (grid.hpp:70-91)."""
+    patches: List[DirichletPatch] = field(default_factory=list)
+
+    @staticmethod
+    def bottom_center_patch(lx: float, ly: float, side: float, value: float) -> "BoundarySpec":
+        # grid.cpp:107-119
+        return BoundarySpec([DirichletPatch(4, 0.5 * (lx - side), 0.5 * (ly - side),
+                                            0.5 * (lx + side), 0.5 * (ly + side), value)])
+
+    def _c(self):
+        arr = (_Patch * max(1, len(self.patches)))()
+        for i, p in enumerate(self.patches):
+            arr[i] = _Patch(p.face, p.u0, p.v0, p.u1, p.v1, p.value)
+        return arr, len(self.patches)
+
+
+class PrecondKind:
+    """PrecondKind (solver.hpp:160)."""
+    NONE, JACOBI, BLOCK_JACOBI, TWO_GRID, MMG = range(5)
+    _names = {"none": 0, "jacobi": 1, "block_jacobi": 2, "two_grid": 3, "mmg": 4}
+
+    @classmethod
+    def parse(cls, name: str) -> int:
+        # parse_precond_kind (solver.cpp:422-429)
+        if name not in cls._names:
+            raise ConfigError("unknown preconditioner kind: " + name)
+        return cls._names[name]
+
+
+@dataclass
+class MmgOptions:
+    """MmgOptions (solver.hpp:141-146)."""
+    num_local_basis: int = 4
+    num_cc_basis: int = 8
+    smoother_sweeps: int = 1
+    eig_tol: float = 0.0
+    eig_degree: int = 0
+    eig_max_outer: int = 0
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (solver.hpp:15-22)."""
+    preconditioner: str = ""
+    iterations: int = 0
+    converged: bool = False
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    setup_seconds: float = 0.0
+    solve_seconds: float = 0.0
+    status: int = 0
+    final_relative_residual: float = 0.0
+
+
+@dataclass
+class PcgResult:
+    x: np.ndarray
+    report: SolveReport
+
+
+class Context:
+    """One GPU solve context: grid hierarchy + problem + preconditioner."""
+
+    def __init__(self, grid: GridSpec, ncc: Sequence[int] | int, sd: int, device: int = 0):
+        L = native()
+        ncc3 = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
+        self._g = _Grid(grid.nx, grid.ny, grid.nz, grid.lx, grid.ly, grid.lz,
+                        (C.c_int64 * 3)(*ncc3), sd)
+        self.grid = grid
+        self.ncc = ncc3
+        self.sd = sd
+        ptr = C.c_void_p()
+        rc = L.tmg_create(C.byref(self._g), C.c_int(device), C.byref(ptr))
+        if rc:
+            _raise(rc, L.tmg_last_error(None).decode())
+        self._p = ptr
+        self.kind_name = None
+
+    def close(self):
+        if getattr(self, "_p", None):
+            native().tmg_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc:
+            _raise(rc, native().tmg_last_error(self._p).decode())
+
+    # problem
+    def set_conductivity(self, kappa, boundary: BoundarySpec):
+        k = _f64(kappa)
+        parr, n = boundary._c()
+        self._check(native().tmg_set_conductivity(self._p, _ptr(k), parr, C.c_int(n)))
+
+    def set_design(self, rho, kappa_lo, kappa_hi=1.0, p=3, boundary: BoundarySpec = None):
+        r = _f64(rho)
+        parr, n = boundary._c()
+        self._check(native().tmg_set_design(self._p, _ptr(r), C.c_double(kappa_lo),
+                                            C.c_double(kappa_hi), C.c_int(p), parr, C.c_int(n)))
+
+    def assemble_rhs(self, source=None):
+        out = np.empty(self.grid.num_cells())
+        sp = _ptr(_f64(source)) if source is not None else None
+        self._check(native().tmg_assemble_rhs(self._p, sp, _ptr(out)))
+        return out
+
+    # preconditioner
+    def setup(self, kind: int | str, opts: MmgOptions = MmgOptions()):
+        if isinstance(kind, str):
+            self.kind_name = kind
+            kind = PrecondKind.parse(kind)
+        else:
+            self.kind_name = [k for k, v in PrecondKind._names.items() if v == kind][0]
+        o = _Opts(kind, opts.num_local_basis, opts.num_cc_basis, opts.smoother_sweeps,
+                  opts.eig_tol, opts.eig_degree, opts.eig_max_outer)
+        self._check(native().tmg_setup(self._p, C.byref(o)))
+
+    # operators
+    def apply_operator(self, x):
+        xx = _f64(x)
+        y = np.empty_like(xx)
+        self._check(native().tmg_apply_operator(self._p, _ptr(xx), _ptr(y)))
+        return y
+
+    def apply_preconditioner(self, r):
+        rr = _f64(r)
+        z = np.empty_like(rr)
+        self._check(native().tmg_apply_preconditioner(self._p, _ptr(rr), _ptr(z)))
+        return z
+
+    def pcg(self, b, rtol=1e-6, max_iterations=10000, x0=None) -> PcgResult:
+        bb = _f64(b)
+        if bb.size != self.grid.num_cells():
+            raise ValueError("pcg: rhs size mismatch")
+        if x0 is not None and np.asarray(x0).size != self.grid.num_cells():
+            raise ValueError("pcg: initial guess size mismatch")
+        x = np.empty_like(bb)
+        hist = np.zeros(max(1, max_iterations))
+        rep = _Report()
+        x0p = _ptr(_f64(x0)) if x0 is not None else None
+        self._check(native().tmg_pcg(self._p, _ptr(bb), x0p, C.c_double(rtol),
+                                     C.c_int(max_iterations), _ptr(x), _ptr(hist),
+                                     C.byref(rep)))
+        return PcgResult(x, self._report(rep, hist))
+
+    def _report(self, rep, hist=None):
+        return SolveReport(self.kind_name or "", rep.iterations, bool(rep.converged),
+                           hist[:rep.iterations].copy() if hist is not None else np.zeros(0),
+                           rep.setup_seconds, rep.solve_seconds, rep.status,
+                           rep.final_relative_residual)
+
+    # resident (bench)
+    def upload_rhs(self, b):
+        self._check(native().tmg_upload_rhs(self._p, _ptr(_f64(b))))
+
+    def solve_resident(self, rtol, max_iterations, use_x0=False) -> SolveReport:
+        rep = _Report()
+        self._check(native().tmg_solve_resident(self._p, C.c_double(rtol),
+                                                C.c_int(max_iterations), C.c_int(int(use_x0)),
+                                                C.byref(rep)))
+        return self._report(rep)
+
+    def download_solution(self):
+        x = np.empty(self.grid.num_cells())
+        self._check(native().tmg_download_solution(self._p, _ptr(x)))
+        return x
+
+    # introspection
+    def sizes(self):
+        s = (C.c_int64 * 6)()
+        self._check(native().tmg_get_sizes(self._p, s))
+        return dict(zip(["M", "m_c", "n_c", "m_cc", "n_cc", "cells_per_coarse"], list(s)))
+
+    def local_bases(self):
+        s = self.sizes()
+        lc = s["n_c"] // s["m_c"]
+        phi = np.empty(s["n_c"] * s["cells_per_coarse"])
+        ev = np.empty(s["n_c"])
+        it = np.empty(s["m_c"], dtype=np.int32)
+        self._check(native().tmg_get_local_bases(self._p, _ptr(phi), _ptr(ev),
+                                                 it.ctypes.data_as(C.POINTER(C.c_int))))
+        return phi.reshape(s["m_c"], lc, s["cells_per_coarse"]), ev.reshape(s["m_c"], lc), it
+
+    def coarse_operator(self):
+        n = self.sizes()["n_c"]
+        a = np.empty((n, n))
+        self._check(native().tmg_get_coarse_operator(self._p, _ptr(a)))
+        return a
+
+    def cc_restriction(self):
+        s = self.sizes()
+        a = np.empty((s["n_cc"], s["n_c"]))
+        self._check(native().tmg_get_cc_restriction(self._p, _ptr(a)))
+        return a
+
+    def profile_solve(self, rtol, max_iterations):
+        ms = (C.c_double * 9)()
+        cnt = (C.c_int * 9)()
+        self._check(native().tmg_profile_solve(self._p, C.c_double(rtol),
+                                               C.c_int(max_iterations), ms, cnt))
+        names = ["search", "update", "restrict", "coarse_down", "gemv", "coarse_up", "post",
+                 "jacobi_step", "init"]
+        return {n: (ms[i], cnt[i]) for i, n in enumerate(names)}
+
+    def device_bytes(self):
+        return native().tmg_device_bytes(self._p)
+
+    def stream(self):
+        return native().tmg_stream(self._p)
+
+
+def make_preconditioner(kind, grid: GridSpec, kappa, boundary: BoundarySpec, ncc, sd,
+                        opts: MmgOptions = MmgOptions(), device: int = 0) -> Context:
+    """make_preconditioner (solver.cpp:462-481) on the GPU: returns a context
+    holding A (matrix-free from kappa) and the set-up preconditioner."""
+    ctx = Context(grid, ncc, sd, device)
+    ctx.set_conductivity(kappa, boundary)
+    ctx.setup(kind, opts)
+    return ctx
+
+
+def pcg(ctx: Context, b, rtol=1e-6, max_iterations=10000, x0=None) -> PcgResult:
+    """topmg::pcg (solver.cpp:483-575) with the context's operator and preconditioner."""
+    return ctx.pcg(b, rtol=rtol, max_iterations=max_iterations, x0=x0)
