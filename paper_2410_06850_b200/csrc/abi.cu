@@ -33,6 +33,7 @@ struct tmg_ctx {
   std::string err;
   // problem
   double* kappa = nullptr;
+  double* coef = nullptr;  // 4 x M operator coefficients (Tx+, Ty+, Tz+, diag)
   uint8_t* dmask = nullptr;
   bool have_problem = false;
   std::vector<Patch> patches;
@@ -55,7 +56,8 @@ struct tmg_ctx {
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
          *r1 = nullptr, *stage = nullptr;
   double* pbuf[2] = {nullptr, nullptr};  // ping-pong search directions
-  double *rc = nullptr, *rc0 = nullptr, *rcc = nullptr, *ecc = nullptr, *ec = nullptr;
+  double *rc = nullptr, *rc0 = nullptr, *rcc = nullptr, *ecc = nullptr, *ec = nullptr,
+         *rc1 = nullptr, *tc = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
   double* history = nullptr;
@@ -115,7 +117,8 @@ void free_setup(tmg_ctx* c) {
   for (void** pp : {(void**)&c->dinv, (void**)&c->phi, (void**)&c->evals, (void**)&c->eig_iters,
                     (void**)&c->Gf, (void**)&c->Ac, (void**)&c->Bc, (void**)&c->Rcc,
                     (void**)&c->cc_evals, (void**)&c->Winv, (void**)&c->Acc, (void**)&c->rc,
-                    (void**)&c->rc0, (void**)&c->rcc, (void**)&c->ecc, (void**)&c->ec}) {
+                    (void**)&c->rc0, (void**)&c->rcc, (void**)&c->ecc, (void**)&c->ec,
+                    (void**)&c->rc1, (void**)&c->tc}) {
     dfree(c, *pp);
     *pp = nullptr;
   }
@@ -176,6 +179,8 @@ int finish_problem(tmg_ctx* c) {
               "assemble_system: no Dirichlet face on the boundary, the system would be singular");
       throw Fail{TMG_ECONFIG};
     }
+    launch_coefficients(c->g, c->cb, c->kappa, c->dmask, c->coef, c->stream);
+    CK(cudaGetLastError());
     c->have_problem = true;
     free_setup(c);
   });
@@ -199,13 +204,12 @@ void download_global(tmg_ctx* c, const double* dev_brick, double* host) {
 // ---------------------------------------------------------------- V-cycle
 void enqueue_vcycle(tmg_ctx* c, int init, PcgState* st, cudaStream_t s, const double* p) {
   const GridParams& g = c->g;
-  launch_update(g, c->cb, c->kappa, c->Gf, c->x, p, c->q, c->r, c->r1, st, c->partials,
+  launch_update(g, c->cb, c->coef, c->Gf, c->x, p, c->q, c->r, c->r1, st, c->partials,
                 c->history, init, s);
-  launch_restrict(g, c->cb, c->kappa, c->dmask, c->phi, c->r, c->r1, c->rc, st, s);
-  launch_coarse_down(g, &st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->rcc, s);
-  launch_gemv(&st->done, c->Acc, c->n_cc, c->rcc, c->ecc, s);
-  launch_coarse_up(g, &st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->ecc, c->ec, s);
-  launch_post(g, c->cb, c->kappa, c->dmask, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, st,
+  launch_restrict(g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, st, s);
+  launch_coarse_cycle(g, &st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0,
+                      c->rcc, c->ecc, c->rc1, c->tc, c->ec, s);
+  launch_post(g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, st,
               c->partials, init, s);
 }
 
@@ -213,7 +217,7 @@ void enqueue_vcycle(tmg_ctx* c, int init, PcgState* st, cudaStream_t s, const do
 void enqueue_iteration(tmg_ctx* c, cudaStream_t s, int par) {
   const double* pold = c->pbuf[par];
   double* pnew = c->pbuf[par ^ 1];
-  launch_search(c->g, c->cb, c->kappa, c->dmask, c->z, pold, pnew, c->q, c->st, c->partials, s);
+  launch_search(c->g, c->cb, c->coef, c->z, pold, pnew, c->q, c->st, c->partials, s);
   if (c->kind == TMG_PRECOND_MMG) {
     enqueue_vcycle(c, 0, c->st, s, pnew);
   } else {
@@ -257,6 +261,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   PcgState init{};
   init.rtol = rtol;
   init.maxit = maxit;
+  init.hist_cap = c->hist_cap;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -284,19 +289,17 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     cudaEventDestroy(b);
   };
   timed(8, [&] {
-    launch_init(c->g, c->cb, c->kappa, c->dmask, c->b, c->x, use_x0, c->r, c->st, c->partials,
+    launch_init(c->g, c->cb, c->coef, c->b, c->x, use_x0, c->r, c->st, c->partials,
                 c->stream);
   });
   if (c->kind == TMG_PRECOND_MMG) {
     if (!prof) {
       enqueue_vcycle(c, 1, c->st, c->stream, c->pbuf[0]);
     } else {
-      timed(1, [&] { launch_update(c->g, c->cb, c->kappa, c->Gf, c->x, c->p, c->q, c->r, c->r1, c->st, c->partials, c->history, 1, c->stream); });
-      timed(2, [&] { launch_restrict(c->g, c->cb, c->kappa, c->dmask, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-      timed(3, [&] { launch_coarse_down(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->rcc, c->stream); });
-      timed(4, [&] { launch_gemv(&c->st->done, c->Acc, c->n_cc, c->rcc, c->ecc, c->stream); });
-      timed(5, [&] { launch_coarse_up(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->ecc, c->ec, c->stream); });
-      timed(6, [&] { launch_post(c->g, c->cb, c->kappa, c->dmask, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 1, c->stream); });
+      timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, c->p, c->q, c->r, c->r1, c->st, c->partials, c->history, 1, c->stream); });
+      timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
+      timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
+      timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 1, c->stream); });
     }
   } else {
     timed(7, [&] {
@@ -342,14 +345,12 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       const double* pold = c->pbuf[par];
       double* pnew = c->pbuf[par ^ 1];
       par ^= 1;
-      timed(0, [&] { launch_search(c->g, c->cb, c->kappa, c->dmask, c->z, pold, pnew, c->q, c->st, c->partials, c->stream); });
+      timed(0, [&] { launch_search(c->g, c->cb, c->coef, c->z, pold, pnew, c->q, c->st, c->partials, c->stream); });
       if (c->kind == TMG_PRECOND_MMG) {
-        timed(1, [&] { launch_update(c->g, c->cb, c->kappa, c->Gf, c->x, pnew, c->q, c->r, c->r1, c->st, c->partials, c->history, 0, c->stream); });
-        timed(2, [&] { launch_restrict(c->g, c->cb, c->kappa, c->dmask, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-        timed(3, [&] { launch_coarse_down(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->rcc, c->stream); });
-        timed(4, [&] { launch_gemv(&c->st->done, c->Acc, c->n_cc, c->rcc, c->ecc, c->stream); });
-        timed(5, [&] { launch_coarse_up(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->rc, c->rc0, c->ecc, c->ec, c->stream); });
-        timed(6, [&] { launch_post(c->g, c->cb, c->kappa, c->dmask, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 0, c->stream); });
+        timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, pnew, c->q, c->r, c->r1, c->st, c->partials, c->history, 0, c->stream); });
+        timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
+        timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
+        timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 0, c->stream); });
       } else {
         timed(7, [&] {
           launch_jacobi_step(c->g, c->cb, c->kind == TMG_PRECOND_JACOBI ? c->dinv : nullptr,
@@ -455,6 +456,7 @@ int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
     init_kernel_attributes();
     c->kappa = dalloc<double>(c, c->M);
     c->dmask = dalloc<uint8_t>(c, c->M);
+    c->coef = dalloc<double>(c, 4 * c->M);
     for (double** v : {&c->b, &c->x, &c->r, &c->p, &c->q, &c->z, &c->r1, &c->stage})
       *v = dalloc<double>(c, c->M);
     c->pbuf[0] = c->p;
@@ -585,7 +587,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     CK(cudaMemsetAsync(c->d_status, 0, 4 * sizeof(int), c->stream));
     if (kind == TMG_PRECOND_JACOBI) {
       c->dinv = dalloc<double>(c, c->M);
-      launch_apply(g, c->cb, c->kappa, c->dmask, nullptr, nullptr, c->dinv, c->stream);
+      launch_apply(g, c->cb, c->coef, nullptr, nullptr, c->dinv, c->stream);
     } else if (kind == TMG_PRECOND_MMG) {
       g.lc = (int)o->num_local_basis;
       g.lcc = (int)o->num_cc_basis;
@@ -605,6 +607,8 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       c->rc = dalloc<double>(c, g.nb * g.lc);
       c->rc0 = dalloc<double>(c, g.nb * g.lc);
       c->ec = dalloc<double>(c, g.nb * g.lc);
+      c->rc1 = dalloc<double>(c, g.nb * g.lc);
+      c->tc = dalloc<double>(c, g.nb * g.lc);
       c->rcc = dalloc<double>(c, c->n_cc);
       c->ecc = dalloc<double>(c, c->n_cc);
       const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
@@ -716,7 +720,7 @@ int tmg_apply_operator(tmg_ctx* c, const double* x, double* y) {
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     upload_global(c, x, c->p);
-    launch_apply(c->g, c->cb, c->kappa, c->dmask, c->p, c->q, nullptr, c->stream);
+    launch_apply(c->g, c->cb, c->coef, c->p, c->q, nullptr, c->stream);
     CK(cudaGetLastError());
     download_global(c, c->q, y);
   });
@@ -731,6 +735,7 @@ int tmg_apply_preconditioner(tmg_ctx* c, const double* rin, double* zout) {
     PcgState init{};
     init.rtol = 0.0;
     init.maxit = 1;
+    init.hist_cap = c->hist_cap;
     CK(cudaMemcpyAsync(c->st, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     upload_global(c, rin, c->r);
     if (c->kind == TMG_PRECOND_MMG) {

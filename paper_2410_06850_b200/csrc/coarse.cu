@@ -27,21 +27,23 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
                                                                const double* __restrict__ phi,
                                                                double* Ac, double* Bc) {
   constexpr int C = CB * CB * CB, NW = C / 32;
-  __shared__ double kt[Tile<CB>::N];
+  __shared__ StencilSmem<CB> ss;
   __shared__ double ph[LC][C];
   __shared__ double red[LC * LC * NW + LC * LC + 8];
   const BrickCoord bc = brick_coord(g, blockIdx.x);
-  load_tile<CB, true>(kappa, kt, g, bc);
+  load_tile<CB, true>(kappa, ss.kt, g, bc);
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   double f[LC];
 #pragma unroll
   for (int a = 0; a < LC; ++a) {
-    f[a] = phi[(bc.b * LC + a) * C + t];
+    f[a] = phi[((size_t)bc.b * LC + a) * C + t];
     ph[a][t] = f[a];
   }
   __syncthreads();
-  const unsigned dm = brick_on_boundary(g, bc) ? dmask[bc.b * C + t] : 0u;
-  const FaceSet fs = cell_faces<CB>(kt, li, lj, lk, g, bc, dm);
+  tile_faces<CB>(ss.kt, ss.fx, ss.fy, ss.fz, g, bc);
+  __syncthreads();
+  const unsigned dm = brick_on_boundary(g, bc) ? dmask[bofs(bc.b, C) + t] : 0u;
+  const FaceSet fs = cell_faces<CB>(ss.fx, ss.fy, ss.fz, ss.kt[Tile<CB>::idx(li, lj, lk)], li, lj, lk, g, bc, dm);
   // --- self block: sum_l d_l f_a f_b - sum_{+x,+y,+z in brick} T (f_a(l) f_b(j) + f_a(j) f_b(l))
   {
     double v[LC * LC];
@@ -62,15 +64,12 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
         for (int b = 0; b < LC; ++b) v[a * LC + b] -= T * (f[a] * ph[b][j] + ph[a][j] * f[b]);
     }
     block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Ac[(bc.b * 7 + 0) * LC * LC + t] = v[t];
+    if (t < LC * LC) Ac[((size_t)bc.b * 7 + 0) * LC * LC + t] = v[t];
   }
   // --- face blocks: -T_lj f_a(l) phi_J,b(j) over the CB^2 face pairs
-  const int64_t nbr[6] = {bc.bi > 0 ? bc.b - 1 : -1,
-                          bc.bi + 1 < g.nbx ? bc.b + 1 : -1,
-                          bc.bj > 0 ? bc.b - g.nbx : -1,
-                          bc.bj + 1 < g.nby ? bc.b + g.nbx : -1,
-                          bc.bk > 0 ? bc.b - g.nbx * g.nby : -1,
-                          bc.bk + 1 < g.nbz ? bc.b + g.nbx * g.nby : -1};
+  int nbr[6];
+#pragma unroll
+  for (int f6 = 0; f6 < 6; ++f6) nbr[f6] = nbr_brick(g, bc, f6);
   const int co[3] = {li, lj, lk};
   for (int fc = 0; fc < 6; ++fc) {
     double v[LC * LC];
@@ -86,17 +85,17 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
       const double T = fs.t[fc];
 #pragma unroll
       for (int b = 0; b < LC; ++b) {
-        const double pj = phi[(nbr[fc] * LC + b) * C + lj2];
+        const double pj = phi[((size_t)nbr[fc] * LC + b) * C + lj2];
 #pragma unroll
         for (int a = 0; a < LC; ++a) v[a * LC + b] = -T * f[a] * pj;
       }
     }
     block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Ac[(bc.b * 7 + 1 + fc) * LC * LC + t] = v[t];
+    if (t < LC * LC) Ac[((size_t)bc.b * 7 + 1 + fc) * LC * LC + t] = v[t];
   }
   // --- cc-boundary correction: faces leaving the cc element + Dirichlet terms
   {
-    const int64_t bco[3] = {bc.bi, bc.bj, bc.bk};
+    const int bco[3] = {bc.bi, bc.bj, bc.bk};
     double e = 0.0;
 #pragma unroll
     for (int fc = 0; fc < 6; ++fc) {
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
 #pragma unroll
       for (int b = 0; b < LC; ++b) v[a * LC + b] = e * f[a] * f[b];
     block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Bc[bc.b * LC * LC + t] = v[t];
+    if (t < LC * LC) Bc[(size_t)bc.b * LC * LC + t] = v[t];
   }
 }
 
@@ -372,120 +371,119 @@ __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
 
 // ------------------------------------------------ coarse part of the V-cycle
 
-// C12: rc0 = Winv rc (per element), wc = rc - A_c rc0, rcc = R_cc wc.
-// rc0 at neighbouring elements is recomputed from their Winv rows.
-__global__ void k_coarse_down(GridParams g, const int* __restrict__ done,
-                              const double* __restrict__ Ac, const double* __restrict__ Winv,
-                              const double* __restrict__ Rcc, const double* __restrict__ rc,
-                              double* rc0, double* rcc) {
-  if (*done) return;
-  extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
-  double* r0 = sm;       // q: rc0 of this element
-  double* wc = r0 + q;   // q
-  // (rcc reduction is done by one thread per output, see below)
-  const ElemCoord ec = elem_coord(g, blockIdx.x);
-  for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    const int64_t gi = child_brick(g, ec, i / LC) * LC + i % LC;
-    (void)gi;
-    const double* W = Winv + ((int64_t)ec.e * q + i) * q;
-    double s = 0.0;
-    for (int j = 0; j < q; ++j) s += W[j] * rc[child_brick(g, ec, j / LC) * LC + j % LC];
-    r0[i] = s;
-    rc0[child_brick(g, ec, i / LC) * LC + i % LC] = s;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    const int ci = i / LC, a = i % LC;
-    const int64_t I = child_brick(g, ec, ci);
-    double s = 0.0;
-    for (int dir = 0; dir < 7; ++dir) {
-      const int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
-      if (J < 0) continue;
-      const double* blk = Ac + (I * 7 + dir) * LC * LC + a * LC;
-      const int cj = child_index(g, ec, J);
-      double xj[LC];
-      if (cj >= 0) {
-        for (int b = 0; b < LC; ++b) xj[b] = r0[cj * LC + b];
-      } else {
-        // neighbour element: recompute its rc0 rows for brick J
-        const int64_t Fe = (J % g.nbx) / g.sd + g.ncx * (((J / g.nbx) % g.nby) / g.sd +
-                                                          g.ncy * ((J / (g.nbx * g.nby)) / g.sd));
-        const ElemCoord fe = elem_coord(g, Fe);
-        const int cjf = child_index(g, fe, J);
-        for (int b = 0; b < LC; ++b) {
-          const double* W = Winv + ((int64_t)Fe * q + cjf * LC + b) * q;
-          double t = 0.0;
-          for (int j = 0; j < q; ++j) t += W[j] * rc[child_brick(g, fe, j / LC) * LC + j % LC];
-          xj[b] = t;
-        }
-      }
-      for (int b = 0; b < LC; ++b) s += blk[b] * xj[b];
-    }
-    wc[i] = rc[I * LC + a] - s;
-  }
-  __syncthreads();
-  // rcc_(E,b) = sum_i R[E][b][i] wc_i   (deterministic: thread b sums in order)
-  for (int b = threadIdx.x; b < g.lcc; b += blockDim.x) {
-    const double* R = Rcc + ((int64_t)ec.e * g.lcc + b) * q;
-    double s = 0.0;
-    for (int i = 0; i < q; ++i) s += R[i] * wc[i];
-    rcc[ec.e * g.lcc + b] = s;
-  }
-
-  (void)nch;
+// One CTA (q threads, q = sd^3 * L_c) per cc element; thread i owns the
+// element-local coarse dof i = child*L_c + a. 32-bit index math throughout.
+struct ElemDofs {
+  int brick;  // coarse cell (brick) of this dof
+  int a;      // basis index within the coarse cell
+};
+__device__ __forceinline__ ElemDofs elem_dof(const GridParams& g, int e, int i) {
+  const int ncx = (int)g.ncx, ncy = (int)g.ncy, sd = g.sd;
+  const int ei = e % ncx, ej = (e / ncx) % ncy, ek = e / (ncx * ncy);
+  const int ci = i / LC;
+  const int di = ci % sd, dj = (ci / sd) % sd, dk = ci / (sd * sd);
+  ElemDofs d;
+  d.brick = (ei * sd + di) + (int)g.nbx * ((ej * sd + dj) + (int)g.nby * (ek * sd + dk));
+  d.a = i % LC;
+  return d;
 }
 
-// C45: rc1 = rc0 + R_cc^T ecc (recomputed at neighbouring elements' cells),
-// tc = rc - A_c rc1, ec = rc1 + Winv tc.
-__global__ void k_coarse_up(GridParams g, const int* __restrict__ done,
-                            const double* __restrict__ Ac, const double* __restrict__ Winv,
-                            const double* __restrict__ Rcc, const double* __restrict__ rc,
-                            const double* __restrict__ rc0, const double* __restrict__ ecc,
-                            double* ec_out) {
+// (A_c x)_(I,a) for a global coarse vector x (block 7-point, Ac[I][dir][a][:]).
+__device__ __forceinline__ double coarse_apply_row(const GridParams& g, const double* __restrict__ Ac,
+                                                   const double* __restrict__ x, int I, int a) {
+  const int nbx = (int)g.nbx, nby = (int)g.nby, nbz = (int)g.nbz;
+  const int bi = I % nbx, bj = (I / nbx) % nby, bk = I / (nbx * nby);
+  const int nb[7] = {I, bi > 0 ? I - 1 : -1, bi + 1 < nbx ? I + 1 : -1,
+                     bj > 0 ? I - nbx : -1, bj + 1 < nby ? I + nbx : -1,
+                     bk > 0 ? I - nbx * nby : -1, bk + 1 < nbz ? I + nbx * nby : -1};
+  double s = 0.0;
+#pragma unroll
+  for (int dir = 0; dir < 7; ++dir) {
+    if (nb[dir] < 0) continue;
+    const double* blk = Ac + ((size_t)I * 7 + dir) * LC * LC + a * LC;
+    const double* xv = x + (size_t)nb[dir] * LC;
+#pragma unroll
+    for (int b = 0; b < LC; ++b) s = fma(blk[b], xv[b], s);
+  }
+  return s;
+}
+
+// out_E = add_E + Winv_E in_E  (coarse_blocks_by_cc smoother, one sweep from 0:
+// solver.cpp:221-243). Winv is symmetric: column i read coalesced.
+__global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
+                                const double* __restrict__ Winv, const double* __restrict__ in,
+                                const double* __restrict__ add, double* out) {
   if (*done) return;
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC;
-  double* r1 = sm;      // q
-  double* tc = r1 + q;  // q
-  const ElemCoord ec = elem_coord(g, blockIdx.x);
-  auto rc1_at = [&](int64_t J, int b) -> double {
-    // rc1 of coarse dof (J, b): rc0 + sum_k R[F][k][(cj, b)] ecc[F][k]
-    const int64_t Fe = (J % g.nbx) / g.sd + g.ncx * (((J / g.nbx) % g.nby) / g.sd +
-                                                      g.ncy * ((J / (g.nbx * g.nby)) / g.sd));
-    const ElemCoord fe = elem_coord(g, Fe);
-    const int cj = child_index(g, fe, J);
-    double s = rc0[J * LC + b];
-    double acc = 0.0;
-    for (int k = 0; k < g.lcc; ++k)
-      acc += Rcc[((int64_t)Fe * g.lcc + k) * q + cj * LC + b] * ecc[Fe * g.lcc + k];
-    return s + acc;
-  };
+  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  double* xin = sm;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    const int64_t I = child_brick(g, ec, i / LC);
-    r1[i] = rc1_at(I, i % LC);
+    const ElemDofs d = elem_dof(g, e, i);
+    xin[i] = in[(size_t)d.brick * LC + d.a];
   }
   __syncthreads();
+  const double* W = Winv + (size_t)e * q * q;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    const int ci = i / LC, a = i % LC;
-    const int64_t I = child_brick(g, ec, ci);
-    double s = 0.0;
-    for (int dir = 0; dir < 7; ++dir) {
-      const int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
-      if (J < 0) continue;
-      const double* blk = Ac + (I * 7 + dir) * LC * LC + a * LC;
-      const int cj = child_index(g, ec, J);
-      for (int b = 0; b < LC; ++b) s += blk[b] * (cj >= 0 ? r1[cj * LC + b] : rc1_at(J, b));
+    double s0 = 0.0, s1 = 0.0;
+    int j = 0;
+    for (; j + 1 < q; j += 2) {
+      s0 = fma(W[(size_t)j * q + i], xin[j], s0);
+      s1 = fma(W[(size_t)(j + 1) * q + i], xin[j + 1], s1);
     }
-    tc[i] = rc[I * LC + a] - s;
+    if (j < q) s0 = fma(W[(size_t)j * q + i], xin[j], s0);
+    const ElemDofs d = elem_dof(g, e, i);
+    const size_t gi = (size_t)d.brick * LC + d.a;
+    out[gi] = (add ? add[gi] : 0.0) + (s0 + s1);
+  }
+}
+
+// wc = rc - A_c rc0 on the element's dofs; rcc_(E,b) = R_cc[E][b] . wc
+// (solver.cpp:297-301).
+__global__ void k_coarse_restrict(GridParams g, const int* __restrict__ done,
+                                  const double* __restrict__ Ac, const double* __restrict__ Rcc,
+                                  const double* __restrict__ rc, const double* __restrict__ rc0,
+                                  double* rcc) {
+  if (*done) return;
+  extern __shared__ double sm[];
+  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  double* wc = sm;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const ElemDofs d = elem_dof(g, e, i);
+    wc[i] = rc[(size_t)d.brick * LC + d.a] - coarse_apply_row(g, Ac, rc0, d.brick, d.a);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < q; i += blockDim.x) {
-    const double* W = Winv + ((int64_t)ec.e * q + i) * q;
+  for (int b = threadIdx.x; b < g.lcc; b += blockDim.x) {
+    const double* R = Rcc + ((size_t)e * g.lcc + b) * q;
     double s = 0.0;
-    for (int j = 0; j < q; ++j) s += W[j] * tc[j];
-    ec_out[child_brick(g, ec, i / LC) * LC + i % LC] = r1[i] + s;
+    for (int i = 0; i < q; ++i) s = fma(R[i], wc[i], s);
+    rcc[(size_t)e * g.lcc + b] = s;
   }
+}
+
+// rc1 = rc0 + R_cc^T ecc on the element's dofs (solver.cpp:307-309).
+__global__ void k_coarse_prolong(GridParams g, const int* __restrict__ done,
+                                 const double* __restrict__ Rcc, const double* __restrict__ rc0,
+                                 const double* __restrict__ ecc, double* rc1) {
+  if (*done) return;
+  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const ElemDofs d = elem_dof(g, e, i);
+    double s = 0.0;
+    for (int b = 0; b < g.lcc; ++b)
+      s = fma(Rcc[((size_t)e * g.lcc + b) * q + i], ecc[(size_t)e * g.lcc + b], s);
+    const size_t gi = (size_t)d.brick * LC + d.a;
+    rc1[gi] = rc0[gi] + s;
+  }
+}
+
+// tc = rc - A_c rc1 (any dof) — thread per coarse dof.
+__global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
+                               const double* __restrict__ Ac, const double* __restrict__ rc,
+                               const double* __restrict__ x, double* out, int n) {
+  if (*done) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = rc[k] - coarse_apply_row(g, Ac, x, k / LC, k % LC);
 }
 
 // ------------------------------------------------------------- launchers
@@ -522,20 +520,23 @@ void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rc
   k_acc_assemble<<<grid, g.lcc * g.lcc, 0, s>>>(g, Ac, Rcc, Acc, n);
 }
 
-void launch_coarse_down(const GridParams& g, const int* done, const double* Ac, const double* Winv,
-                        const double* Rcc, const double* rc, double* rc0, double* rcc,
-                        cudaStream_t s) {
+// Coarse part of one V-cycle (solver.cpp:292-319): rc -> ec.
+//  rc0 = S_c(rc); rcc = R_cc (rc - A_c rc0); ecc = A_cc^-1 rcc;
+//  rc1 = rc0 + R_cc^T ecc; ec = rc1 + S_c(rc - A_c rc1).
+void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
+                         const double* Winv, const double* Rcc, const double* Acc_inv,
+                         int64_t n_cc, const double* rc, double* rc0, double* rcc, double* ecc,
+                         double* rc1, double* tc, double* ec, cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
-  const size_t smem = sizeof(double) * (size_t)(2 * q + 32 * g.lcc);
-  k_coarse_down<<<(unsigned)g.ncc, 64, smem, s>>>(g, done, Ac, Winv, Rcc, rc, rc0, rcc);
-}
-
-void launch_coarse_up(const GridParams& g, const int* done, const double* Ac, const double* Winv,
-                      const double* Rcc, const double* rc, const double* rc0, const double* ecc,
-                      double* ec, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
-  const size_t smem = sizeof(double) * (size_t)(2 * q);
-  k_coarse_up<<<(unsigned)g.ncc, 64, smem, s>>>(g, done, Ac, Winv, Rcc, rc, rc0, ecc, ec);
+  const int nt = (q + 31) / 32 * 32;
+  const int nc = (int)(g.nb * LC);
+  const size_t sm = sizeof(double) * (size_t)q;
+  k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, rc, nullptr, rc0);
+  k_coarse_restrict<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
+  launch_gemv(done, Acc_inv, n_cc, rcc, ecc, s);
+  k_coarse_prolong<<<(unsigned)g.ncc, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
+  k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, rc1, tc, nc);
+  k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);
 }
 
 int compiled_lc() { return LC; }

@@ -20,7 +20,7 @@ enum : int {
 // Device-resident CG scalars (one per solve context).
 struct PcgState {
   double bnorm, rnorm, rho, alpha, beta, pq, rtol;
-  int it, maxit, done, status, first;
+  int it, maxit, done, status, first, hist_cap;
   unsigned int ticket[8];
 };
 
@@ -32,8 +32,8 @@ void launch_conductivity(const double* x, double* kappa, int64_t m, double lo, d
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
                      double ly, double lz, const double* kappa, const double* source,
                      uint8_t* dmask, double* rhs, unsigned long long* count, cudaStream_t s);
-void launch_apply(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                  const double* x, double* y, double* dinv, cudaStream_t s);
+void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
+                  double* dinv, cudaStream_t s);
 
 // setup_fine.cu
 void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
@@ -55,12 +55,10 @@ void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv,
                             cudaStream_t s);
 void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
                          cudaStream_t s);
-void launch_coarse_down(const GridParams& g, const int* done, const double* Ac, const double* Winv,
-                        const double* Rcc, const double* rc, double* rc0, double* rcc,
-                        cudaStream_t s);
-void launch_coarse_up(const GridParams& g, const int* done, const double* Ac, const double* Winv,
-                      const double* Rcc, const double* rc, const double* rc0, const double* ecc,
-                      double* ec, cudaStream_t s);
+void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
+                         const double* Winv, const double* Rcc, const double* Acc_inv,
+                         int64_t n_cc, const double* rc, double* rc0, double* rcc, double* ecc,
+                         double* rc1, double* tc, double* ec, cudaStream_t s);
 
 // dense.cu
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
@@ -70,22 +68,22 @@ void launch_gemv(const int* done, const double* A, int64_t n, const double* x, d
 
 // pcg.cu
 void init_kernel_attributes();
-void launch_init(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                 const double* b, double* x, int has_x0, double* r, PcgState* st, double* partials,
-                 cudaStream_t s);
-void launch_search(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                   const double* z, const double* p_old, double* p, double* q, PcgState* st,
-                   double* partials, cudaStream_t s);
-void launch_update(const GridParams& g, int cb, const double* kappa, const double* Gf, double* x,
+void launch_coefficients(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                         double* coef, cudaStream_t s);
+void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
+                 int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s);
+void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
+                   const double* p_old, double* p, double* q, PcgState* st, double* partials,
+                   cudaStream_t s);
+void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s);
-void launch_restrict(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                     const double* phi, const double* r, const double* r1, double* rc,
-                     const PcgState* st, cudaStream_t s);
-void launch_post(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                 const double* phi, const double* Gf, const double* r, const double* r1,
-                 const double* ec, double* z, PcgState* st, double* partials, int init,
-                 cudaStream_t s);
+void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
+                     const double* r, const double* r1, double* rc, const PcgState* st,
+                     cudaStream_t s);
+void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
+                 const double* Gf, const double* r, const double* r1, const double* ec, double* z,
+                 PcgState* st, double* partials, int init, cudaStream_t s);
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, cudaStream_t s);

@@ -111,24 +111,23 @@ __global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __re
   }
 }
 
-// y = A x (bitwise SparseOperator::apply), optionally also dinv = 1/diag.
+// y = A x from the precomputed coefficients (bitwise SparseOperator::apply),
+// optionally dinv = 1/diag (JacobiPreconditioner, solver.cpp:21-29).
 template <int CB>
-__global__ void __launch_bounds__(CB * CB * CB) k_apply(GridParams g, const double* __restrict__ kappa,
-                                                       const uint8_t* __restrict__ dmask,
-                                                       const double* __restrict__ x, double* y,
-                                                       double* dinv) {
-  __shared__ double kt[Tile<CB>::N];
+__global__ void __launch_bounds__(CB * CB * CB) k_apply(GridParams g, const double* __restrict__ coef,
+                                                       int64_t M, const double* __restrict__ x,
+                                                       double* y, double* dinv) {
+  __shared__ CoefSmem<CB> cs;
   __shared__ double xt[Tile<CB>::N];
   constexpr int C = CB * CB * CB;
   const BrickCoord bc = brick_coord(g, blockIdx.x);
-  load_tile<CB, true>(kappa, kt, g, bc);
+  load_coefs<CB>(coef, M, cs, g, bc);
   if (x) load_tile<CB, true>(x, xt, g, bc);
   __syncthreads();
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
-  const unsigned dm = brick_on_boundary(g, bc) ? dmask[bc.b * C + t] : 0u;
-  const FaceSet fs = cell_faces<CB>(kt, li, lj, lk, g, bc, dm);
-  if (y) y[bc.b * C + t] = apply_row<CB>(fs, xt, li, lj, lk);
-  if (dinv) dinv[bc.b * C + t] = 1.0 / fs.diag;  // solver.cpp:27
+  const size_t s = bofs(bc.b, C) + t;
+  if (y) y[s] = apply_coef<CB>(cs, xt, li, lj, lk);
+  if (dinv) dinv[s] = 1.0 / cs.dg[t];  // solver.cpp:27
 }
 
 static int grid1d(int64_t m) {
@@ -161,12 +160,13 @@ void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npat
   const int64_t m = g.nx * g.ny * g.nz;
   k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, m, count);
 }
-void launch_apply(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                  const double* x, double* y, double* dinv, cudaStream_t s) {
+void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
+                  double* dinv, cudaStream_t s) {
+  const int64_t M = g.nx * g.ny * g.nz;
   if (cb == 8)
-    k_apply<8><<<(unsigned)g.nb, 512, 0, s>>>(g, kappa, dmask, x, y, dinv);
+    k_apply<8><<<(unsigned)g.nb, 512, 0, s>>>(g, coef, M, x, y, dinv);
   else
-    k_apply<4><<<(unsigned)g.nb, 64, 0, s>>>(g, kappa, dmask, x, y, dinv);
+    k_apply<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, x, y, dinv);
 }
 
 }  // namespace tmg

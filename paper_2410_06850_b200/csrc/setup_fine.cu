@@ -12,12 +12,15 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
                                                                const double* __restrict__ kappa,
                                                                const uint8_t* __restrict__ dmask,
                                                                double* G, int* status) {
-  constexpr int P = Thomas<CB>::P, PP = Thomas<CB>::PP, C = CB * CB * CB;
+  constexpr int P = Thomas<CB>::P, C = CB * CB * CB;
   extern __shared__ double sm[];
   double* S = sm;                  // P*P  current Schur complement -> inverse
   double* Gprev = S + P * P;       // P*P  previous plane inverse
   double* kt = Gprev + P * P;      // tile
-  double* piv = kt + Tile<CB>::N;  // C
+  double* fx = kt + Tile<CB>::N;   // 3 face arrays
+  double* fy = fx + Tile<CB>::NF;
+  double* fz = fy + Tile<CB>::NF;
+  double* piv = fz + Tile<CB>::NF; // C
   double* col = piv + C;           // P
   double* rowp = col + P;          // P
   double* dg = rowp + P;           // C  diagonal of A
@@ -28,10 +31,12 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
   const BrickCoord bc = brick_coord(g, blockIdx.x);
   load_tile<CB, true>(kappa, kt, g, bc);
   __syncthreads();
+  tile_faces<CB>(kt, fx, fy, fz, g, bc);
+  __syncthreads();
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   {
-    const unsigned dm = brick_on_boundary(g, bc) ? dmask[bc.b * C + t] : 0u;
-    const FaceSet fs = cell_faces<CB>(kt, li, lj, lk, g, bc, dm);
+    const unsigned dm = brick_on_boundary(g, bc) ? dmask[bofs(bc.b, C) + t] : 0u;
+    const FaceSet fs = cell_faces<CB>(fx, fy, fz, kt[Tile<CB>::idx(li, lj, lk)], li, lj, lk, g, bc, dm);
     dg[t] = fs.diag;
     tx[t] = li + 1 < CB ? fs.t[1] : 0.0;
     ty[t] = lj + 1 < CB ? fs.t[3] : 0.0;
@@ -84,13 +89,13 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
       Gprev[e] = 0.5 * (S[e] + S[j * P + i]);
     }
     __syncthreads();
-    for (int e = t; e < PP; e += C) {
-      // unpack e -> (i, j), i >= j
-      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > e) --i;
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      const int j = e - i * (i + 1) / 2;
-      Gout[(size_t)k * PP + e] = Gprev[i * P + j];
+    // lower block-triangle of 8 x 8 blocks, block (I, J <= I) at I(I+1)/2 + J
+    for (int e = t; e < Thomas<CB>::PLANE; e += C) {
+      const int blk = e / 64, rr = (e % 64) / 8, cc = e % 8;
+      int I = 0;
+      while ((I + 1) * (I + 2) / 2 <= blk) ++I;
+      const int J = blk - I * (I + 1) / 2;
+      Gout[(size_t)k * Thomas<CB>::PLANE + blk * 64 + swz(rr, cc)] = Gprev[(8 * I + rr) * P + 8 * J + cc];
     }
     __syncthreads();
   }
@@ -110,7 +115,8 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
 
 size_t thomas_smem_bytes(int cb) {
   const int P = cb * cb, C = cb * cb * cb, N = (cb + 2) * (cb + 2) * (cb + 2);
-  return sizeof(double) * (size_t)(2 * P * P + N + C + 2 * P + 4 * C);
+  const int NF = (cb + 1) * cb * cb;
+  return sizeof(double) * (size_t)(2 * P * P + N + 3 * NF + C + 2 * P + 4 * C);
 }
 
 void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
@@ -126,8 +132,7 @@ void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, cons
 }
 
 int64_t thomas_doubles_per_brick(int cb) {
-  const int P = cb * cb;
-  return (int64_t)cb * (P * (P + 1) / 2);
+  return cb == 8 ? Thomas<8>::PER_BRICK : Thomas<4>::PER_BRICK;
 }
 
 }  // namespace tmg

@@ -8,79 +8,232 @@
 // each brick's block is factorised as a block-tridiagonal matrix over its CB
 // z-planes (CB^2 cells each): S_0 = A_0, S_k = A_k - B_k S_{k-1}^{-1} B_k with
 // B_k = diag(-T_z) the plane coupling, and the Schur inverses G_k = S_k^{-1}
-// are stored densely (packed symmetric). One solve is then 2*CB-1 dense
-// CB^2 x CB^2 mat-vecs — the same arithmetic as the LDL^T solve, reorganised
-// into wide parallel steps. The pivots of the in-place Gauss-Jordan sweeps are
-// the LDL^T pivots of A_II in natural order; the reference's singular-pivot
-// rule (d_i > 1e-14 max|d|, solver.cpp:86-92) is applied to them.
+// are stored densely. One solve is 2*CB-1 dense CB^2 x CB^2 mat-vecs — the
+// same arithmetic as the LDL^T solve, reorganised into wide parallel steps.
+// The pivots of the Gauss-Jordan sweeps are the LDL^T pivots of A_II in natural
+// order; the reference's singular-pivot rule (d_i > 1e-14 max|d|,
+// solver.cpp:86-92) is applied to them.
+//
+// Storage of one plane: the lower block-triangle of 8 x 8 blocks (I, J <= I),
+// block index I(I+1)/2 + J, rows swizzled in 16-byte chunks (swz); diagonal
+// blocks are kept whole. 36 blocks = 2304 doubles (18 KiB) per plane at
+// CB = 8. Planes stream global -> shared through a ring of kSlots TMA bulk
+// copies (cp.async.bulk + mbarrier complete_tx) issued kSlots plane-steps
+// ahead. Each mat-vec thread owns one row of one block: it applies the row to
+// w (row product, y_I) and — for off-diagonal blocks — its transpose (column
+// products, y_J, reduce-scattered across the block's 8 lanes with shuffles).
+// Every output row then has exactly NBK partial sums, added in a fixed order.
 #pragma once
 #include "stencil.cuh"
+#include "tma.cuh"
 
 namespace tmg {
 
 template <int CB>
 struct Thomas {
-  static constexpr int P = CB * CB;              // cells per plane
-  static constexpr int PP = P * (P + 1) / 2;     // packed symmetric plane
-  static constexpr int PER_BRICK = CB * PP;      // doubles per brick
-  static constexpr int TPR = CB;                 // threads per mat-vec row
-  __device__ static __forceinline__ int pidx(int i, int j) {
-    return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i;
+  static constexpr int P = CB * CB;                 // cells per plane
+  static constexpr int NBK = P / 8;                 // 8-row block rows per plane
+  static constexpr int NBLK = NBK * (NBK + 1) / 2;  // stored blocks per plane
+  static constexpr int PLANE = NBLK * 64;           // doubles per plane
+  static constexpr int PER_BRICK = CB * PLANE;      // doubles per brick
+  static constexpr int NL = 2 * CB - 1;             // plane mat-vecs per solve
+  static constexpr int MV = NBLK * 8;               // mat-vec threads
+  static constexpr int NT = (MV + 31) / 32 * 32;    // CTA size of the solve kernels
+  __host__ __device__ static constexpr int plane_of(int n) { return n < CB ? n : 2 * CB - 2 - n; }
+  // storage offset of element (i, j), i, j < P (any order: symmetric)
+  __host__ __device__ static constexpr int off(int i, int j) {
+    return (i / 8 >= j / 8) ? (((i / 8) * (i / 8 + 1) / 2 + j / 8) * 64 + (i % 8) * 8 + j % 8)
+                            : (((j / 8) * (j / 8 + 1) / 2 + i / 8) * 64 + (j % 8) * 8 + i % 8);
   }
 };
 
-// y_i = sum_j G(i,j) w_j over one plane; G packed in smem, w in smem.
-// Thread layout: row i = tid / TPR, lane-group sum over j = s, s+TPR, ...
-// Returns the row value in the TPR threads of row i (all lanes of the group).
-template <int CB>
-__device__ __forceinline__ double plane_matvec(const double* Gp, const double* w) {
-  constexpr int P = Thomas<CB>::P, TPR = Thomas<CB>::TPR;
-  const int i = threadIdx.x / TPR, s = threadIdx.x % TPR;
-  double acc = 0.0;
-#pragma unroll
-  for (int j = s; j < P; j += TPR) acc = fma(Gp[Thomas<CB>::pidx(i, j)], w[j], acc);
-#pragma unroll
-  for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc;
+// Swizzle inside an 8 x 8 block row: 16-byte chunk q (columns 2q, 2q+1) of
+// row r is stored at chunk position (q + r/2) mod 4, so the 8 rows of a block
+// read by one quarter-warp hit 8 distinct 16-byte bank groups.
+__host__ __device__ constexpr int swz(int r, int c) {
+  return r * 8 + 2 * (((c >> 1) + (r >> 1)) & 3) + (c & 1);
 }
 
-// Exact block solve x = A_II^{-1} t for one brick.
-//  t   : smem, C values (brick order, plane k = t[k*P .. k*P+P))
-//  tz  : smem, C values; tz[l] = T_z between cell l and the cell one plane below
-//        (0 for lk = 0)
-//  u   : smem scratch, C values;  x : smem output, C values (may alias t)
-//  gbuf: smem, PP values
-//  G   : global, this brick's CB planes of packed inverses
+#ifndef TMG_SLOTS
+#define TMG_SLOTS 2
+#endif
+constexpr int kSlots = TMG_SLOTS;  // TMA ring depth (planes in flight per CTA)
+
 template <int CB>
-__device__ __forceinline__ void thomas_solve(const double* __restrict__ G, const double* t,
-                                             const double* tz, double* u, double* x, double* gbuf,
-                                             double* w) {
-  constexpr int P = Thomas<CB>::P, PP = Thomas<CB>::PP, C = CB * CB * CB, TPR = Thomas<CB>::TPR;
-  const int tid = threadIdx.x;
-  const int row = tid / TPR, sub = tid % TPR;
-  // forward: w_k = t_k + Tz_k * u_{k-1};  u_k = G_k w_k
-  for (int k = 0; k < CB; ++k) {
-    for (int e = tid; e < PP; e += C) gbuf[e] = __ldg(G + (size_t)k * PP + e);
-    if (tid < P) {
-      const int l = k * P + tid;
-      w[tid] = k == 0 ? t[l] : fma(tz[l], u[l - P], t[l]);
-    }
-    __syncthreads();
-    const double y = plane_matvec<CB>(gbuf, w);
-    if (sub == 0) u[k * P + row] = y;
-    __syncthreads();
+using PlaneSlots = double[kSlots][Thomas<CB>::PLANE];
+
+// Per-solve scratch; the TMA plane slots live separately (16-byte aligned,
+// caller-owned) so kernels can alias them with data dead before the solve.
+template <int CB>
+struct ThomasSmem {
+  double (*slots)[Thomas<CB>::PLANE];
+  double part[CB * CB][Thomas<CB>::NBK + 1];
+  double u[CB * CB * CB];
+  double w2[2][CB * CB];
+  uint64_t bars[kSlots];
+};
+
+// 8-lane reduce-scatter: lane r (of an aligned group of 8) returns sum over the
+// group's lanes of b[r].
+__device__ __forceinline__ double reduce_scatter8(double (&b)[8], int r) {
+  const bool h4 = r & 4, h2 = r & 2, h1 = r & 1;
+  double c4[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double send = h4 ? b[k] : b[k + 4];
+    const double keep = h4 ? b[k + 4] : b[k];
+    c4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
   }
-  // backward: x_{K-1} = u_{K-1};  x_k = u_k - G_k (B_{k+1} x_{k+1}),  B = -Tz
-  if (tid < P) x[(CB - 1) * P + tid] = u[(CB - 1) * P + tid];
-  for (int k = CB - 2; k >= 0; --k) {
-    for (int e = tid; e < PP; e += C) gbuf[e] = __ldg(G + (size_t)k * PP + e);
-    if (tid < P) {
-      const int l = (k + 1) * P + tid;
-      w[tid] = -tz[l] * x[l];
+  double c2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double send = h2 ? c4[k] : c4[k + 2];
+    const double keep = h2 ? c4[k + 2] : c4[k];
+    c2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  const double send = h1 ? c2[0] : c2[1];
+  const double keep = h1 ? c2[1] : c2[0];
+  return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+template <int CB>
+struct MvRole {
+  int I, J, r, blk;
+  bool active;
+};
+
+template <int CB>
+__device__ __forceinline__ MvRole<CB> mv_role() {
+  MvRole<CB> m;
+  const int tid = threadIdx.x;
+  m.active = tid < Thomas<CB>::MV;
+  m.blk = m.active ? tid / 8 : 0;
+  m.r = tid % 8;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= m.blk) ++I;
+  m.I = I;
+  m.J = m.blk - I * (I + 1) / 2;
+  return m;
+}
+
+// One plane mat-vec step: partial products into part[][].
+template <int CB>
+__device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp, const double* w,
+                                            const MvRole<CB>& m) {
+  // whole warps take part (the shuffles below need every lane)
+  if ((int)(threadIdx.x >> 5) >= (Thomas<CB>::MV + 31) / 32) return;
+  const bool off_diag = m.active && m.J < m.I;
+  double gv[8];
+  const double* row = Gp + m.blk * 64;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 v = *reinterpret_cast<const double2*>(row + swz(m.r, 2 * q));
+    gv[2 * q] = m.active ? v.x : 0.0;
+    gv[2 * q + 1] = m.active ? v.y : 0.0;
+  }
+  double a0 = 0.0, a1 = 0.0;  // two chains halve the dependent-FMA latency
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) {
+    a0 = fma(gv[c], w[8 * m.J + c], a0);
+    a1 = fma(gv[c + 1], w[8 * m.J + c + 1], a1);
+  }
+  if (m.active) sm.part[8 * m.I + m.r][m.J] = a0 + a1;
+  const double wr = w[8 * m.I + m.r];
+  double b[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) b[c] = off_diag ? gv[c] * wr : 0.0;
+  const double cs = reduce_scatter8(b, m.r);
+  if (off_diag) sm.part[8 * m.J + m.r][m.I] = cs;
+}
+
+template <int CB>
+__device__ __forceinline__ void thomas_init(ThomasSmem<CB>& sm) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) mbar_init(&sm.bars[s], 1);
+    fence_barrier_init();
+  }
+}
+
+// Issue the first kSlots plane loads of a solve (thread 0). Call after
+// thomas_init + __syncthreads, as early as possible in the kernel.
+template <int CB>
+__device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double* __restrict__ G) {
+  // resident mode (kSlots >= CB): all CB planes stay in shared memory and the
+  // backward sweep reuses them; otherwise a ring refilled kSlots steps ahead.
+  constexpr int NPRE = kSlots >= CB ? CB : kSlots;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int n = 0; n < NPRE && n < Thomas<CB>::NL; ++n) {
+      mbar_arrive_expect_tx(&sm.bars[n], Thomas<CB>::PLANE * sizeof(double));
+      bulk_g2s(sm.slots[n], G + (size_t)Thomas<CB>::plane_of(n) * Thomas<CB>::PLANE,
+               Thomas<CB>::PLANE * sizeof(double), &sm.bars[n]);
     }
+  }
+}
+
+// Exact block solve x = A_II^{-1} t for one brick (after thomas_prefetch).
+//  t  : smem, C values (plane k = t[k*P .. k*P+P)); x may alias t
+//  tz : smem, C values; tz[l] = T_z between cell l and the cell one plane below
+// Starts and ends with a __syncthreads.
+template <int CB>
+__device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* __restrict__ G,
+                                             const double* t, const double* tz, double* x) {
+  constexpr int P = Thomas<CB>::P, NL = Thomas<CB>::NL, NBK = Thomas<CB>::NBK;
+  const int tid = threadIdx.x;
+  const MvRole<CB> m = mv_role<CB>();
+  constexpr bool resident = kSlots >= CB;
+  auto slot_of = [](int n) { return resident ? Thomas<CB>::plane_of(n) : n % kSlots; };
+  auto parity_of = [](int n) { return resident ? 0u : (uint32_t)((n / kSlots) & 1); };
+  // The last warp issues the TMA refills and waits for the next plane before
+  // each step's closing barrier, which then publishes "plane ready" to all.
+  const bool waiter = tid >= (int)blockDim.x - 32;
+  const bool issuer = tid == (int)blockDim.x - 32;
+  if (waiter) mbar_wait(&sm.bars[slot_of(0)], parity_of(0));
+  if (tid < P) sm.w2[0][tid] = t[tid];
+  __syncthreads();
+#pragma unroll 1
+  for (int n = 0; n < NL; ++n) {
+    const int slot = slot_of(n);
+    mv_partials<CB>(sm, sm.slots[slot], sm.w2[n & 1], m);
     __syncthreads();
-    const double y = plane_matvec<CB>(gbuf, w);
-    if (sub == 0) x[k * P + row] = u[k * P + row] - y;
+    // slot consumed by every thread: refill it with the plane kSlots steps ahead
+    if (!resident && issuer && n + kSlots < NL) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&sm.bars[slot], Thomas<CB>::PLANE * sizeof(double));
+      bulk_g2s(sm.slots[slot], G + (size_t)Thomas<CB>::plane_of(n + kSlots) * Thomas<CB>::PLANE,
+               Thomas<CB>::PLANE * sizeof(double), &sm.bars[slot]);
+    }
+    if (tid < P) {
+      double pr[NBK];
+#pragma unroll
+      for (int s = 0; s < NBK; ++s) pr[s] = sm.part[tid][s];
+#pragma unroll
+      for (int w = 1; w < NBK; w *= 2)  // fixed pairwise tree
+#pragma unroll
+        for (int s = 0; s + w < NBK; s += 2 * w) pr[s] += pr[s + w];
+      const double acc = pr[0];
+      double* wn = sm.w2[(n + 1) & 1];
+      const int row = tid;
+      if (n < CB) {  // forward: u_k = G_k w_k ; w_{k+1} = t_{k+1} + Tz_{k+1} u_k
+        const int l = n * P + row;
+        sm.u[l] = acc;
+        if (n + 1 < CB) {
+          wn[row] = fma(tz[l + P], acc, t[l + P]);
+        } else {  // x_{K-1} = u_{K-1};  first backward w = -Tz_{K-1} x_{K-1}
+          x[l] = acc;
+          wn[row] = -tz[l] * acc;
+        }
+      } else {  // backward plane k: x_k = u_k - G_k (B_{k+1} x_{k+1})
+        const int k = Thomas<CB>::plane_of(n);
+        const int l = k * P + row;
+        const double xv = sm.u[l] - acc;
+        x[l] = xv;
+        if (k > 0) wn[row] = -tz[l] * xv;
+      }
+    }
+    if (waiter && n + 1 < NL && (!resident || n + 1 < CB))
+      mbar_wait(&sm.bars[slot_of(n + 1)], parity_of(n + 1));
     __syncthreads();
   }
 }

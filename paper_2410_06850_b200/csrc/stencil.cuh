@@ -5,12 +5,12 @@
 // face, 2 k_c * area/h per Dirichlet boundary face on the diagonal, nothing on
 // Neumann faces. It is never materialised: each CTA stages the conductivity and
 // the input vector of its brick plus a one-cell face halo in shared memory and
-// recomputes the face transmissibilities in registers. The diagonal is summed
-// in the reference's face order (x-lo, x-hi, y-lo, y-hi, z-lo, z-hi,
-// fvm.cpp:71-112) and the row product in its sorted-column order
-// (z-lo, y-lo, x-lo, diag, x-hi, y-hi, z-hi; sparse.cpp:76-83) without FMA
-// contraction, so y = A x is bitwise equal to SparseOperator::apply on the
-// assembled CSR.
+// computes every face transmissibility of the tile once (3 per cell) into
+// shared face arrays. The diagonal is summed in the reference's face order
+// (x-lo, x-hi, y-lo, y-hi, z-lo, z-hi, fvm.cpp:71-112) and the row product in
+// its sorted-column order (z-lo, y-lo, x-lo, diag, x-hi, y-hi, z-hi;
+// sparse.cpp:76-83) without FMA contraction, so y = A x is bitwise equal to
+// SparseOperator::apply on the assembled CSR.
 #pragma once
 #include "common.cuh"
 
@@ -21,65 +21,104 @@ struct Tile {
   static constexpr int E = CB + 2;
   static constexpr int N = E * E * E;
   static constexpr int C = CB * CB * CB;
+  static constexpr int NF = (CB + 1) * CB * CB;  // faces per axis in a tile
   __device__ static __forceinline__ int idx(int i, int j, int k) {
     return (i + 1) + E * ((j + 1) + E * (k + 1));
   }
+  // face between tile cells (i,j,k) and (i+1,j,k), i in [-1, CB-1]; likewise y, z
+  __device__ static __forceinline__ int fxi(int i, int j, int k) { return (i + 1) + (CB + 1) * (j + CB * k); }
+  __device__ static __forceinline__ int fyi(int i, int j, int k) { return (j + 1) + (CB + 1) * (i + CB * k); }
+  __device__ static __forceinline__ int fzi(int i, int j, int k) { return (k + 1) + (CB + 1) * (i + CB * j); }
 };
 
 struct BrickCoord {
-  int64_t bi, bj, bk, b;
+  int bi, bj, bk, b;
 };
 
-__device__ __forceinline__ BrickCoord brick_coord(const GridParams& g, int64_t b) {
+__device__ __forceinline__ BrickCoord brick_coord(const GridParams& g, int b) {
   BrickCoord c;
+  const int nbx = (int)g.nbx, nby = (int)g.nby;
   c.b = b;
-  c.bi = b % g.nbx;
-  c.bj = (b / g.nbx) % g.nby;
-  c.bk = b / (g.nbx * g.nby);
+  c.bi = b % nbx;
+  c.bj = (b / nbx) % nby;
+  c.bk = b / (nbx * nby);
   return c;
 }
 
+__device__ __forceinline__ size_t bofs(int b, int C) { return (size_t)b * (size_t)C; }
+
+// Neighbour brick across face f (0 x-lo .. 5 z-hi) or -1.
+__device__ __forceinline__ int nbr_brick(const GridParams& g, const BrickCoord& bc, int f) {
+  const int nbx = (int)g.nbx, nby = (int)g.nby, nbz = (int)g.nbz;
+  switch (f) {
+    case 0: return bc.bi > 0 ? bc.b - 1 : -1;
+    case 1: return bc.bi + 1 < nbx ? bc.b + 1 : -1;
+    case 2: return bc.bj > 0 ? bc.b - nbx : -1;
+    case 3: return bc.bj + 1 < nby ? bc.b + nbx : -1;
+    case 4: return bc.bk > 0 ? bc.b - nbx * nby : -1;
+    default: return bc.bk + 1 < nbz ? bc.b + nbx * nby : -1;
+  }
+}
+
+// Halo slot s in [0, 6*CB^2): face f = s / CB^2; returns the tile index and the
+// neighbour-local cell index.
+template <int CB>
+__device__ __forceinline__ void halo_slot(int s, int& f, int& tidx, int& nl) {
+  constexpr int F = CB * CB;
+  f = s / F;
+  const int q = s % F, u = q % CB, w = q / CB;
+  switch (f) {
+    case 0: tidx = Tile<CB>::idx(-1, u, w); nl = (CB - 1) + CB * (u + CB * w); break;
+    case 1: tidx = Tile<CB>::idx(CB, u, w); nl = 0 + CB * (u + CB * w); break;
+    case 2: tidx = Tile<CB>::idx(u, -1, w); nl = u + CB * ((CB - 1) + CB * w); break;
+    case 3: tidx = Tile<CB>::idx(u, CB, w); nl = u + CB * (0 + CB * w); break;
+    case 4: tidx = Tile<CB>::idx(u, w, -1); nl = u + CB * (w + CB * (CB - 1)); break;
+    default: tidx = Tile<CB>::idx(u, w, CB); nl = u + CB * (w + CB * 0); break;
+  }
+}
+
 // Load v's brick values into tile interior; if HALO, also the six face layers
-// from the neighbouring bricks (0 outside the domain). Caller syncs.
+// from the neighbouring bricks (0 outside the domain). Any CTA size (cells are
+// strided by blockDim.x). Caller syncs.
 template <int CB, bool HALO>
 __device__ __forceinline__ void load_tile(const double* __restrict__ v, double* tile,
                                           const GridParams& g, const BrickCoord& bc) {
   constexpr int C = CB * CB * CB;
-  constexpr int F = CB * CB;
-  const int t = threadIdx.x;
-  {
-    const int li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
-    tile[Tile<CB>::idx(li, lj, lk)] = __ldg(v + bc.b * C + t);
-  }
+  for (int t = threadIdx.x; t < C; t += blockDim.x)
+    tile[Tile<CB>::idx(t % CB, (t / CB) % CB, t / (CB * CB))] = __ldg(v + bofs(bc.b, C) + t);
   if (HALO) {
-    for (int s = t; s < 6 * F; s += C) {
-      const int f = s / F, q = s % F;
-      const int u = q % CB, w = q / CB;
-      int64_t nbrick = -1;
-      int li = 0, lj = 0, lk = 0, ti = 0, tj = 0, tk = 0;
-      switch (f) {
-        case 0:  // x-lo halo: neighbour bi-1, its li = CB-1
-          if (bc.bi > 0) nbrick = bc.b - 1;
-          li = CB - 1; lj = u; lk = w; ti = -1; tj = u; tk = w; break;
-        case 1:
-          if (bc.bi + 1 < g.nbx) nbrick = bc.b + 1;
-          li = 0; lj = u; lk = w; ti = CB; tj = u; tk = w; break;
-        case 2:
-          if (bc.bj > 0) nbrick = bc.b - g.nbx;
-          li = u; lj = CB - 1; lk = w; ti = u; tj = -1; tk = w; break;
-        case 3:
-          if (bc.bj + 1 < g.nby) nbrick = bc.b + g.nbx;
-          li = u; lj = 0; lk = w; ti = u; tj = CB; tk = w; break;
-        case 4:
-          if (bc.bk > 0) nbrick = bc.b - g.nbx * g.nby;
-          li = u; lj = w; lk = CB - 1; ti = u; tj = w; tk = -1; break;
-        default:
-          if (bc.bk + 1 < g.nbz) nbrick = bc.b + g.nbx * g.nby;
-          li = u; lj = w; lk = 0; ti = u; tj = w; tk = CB; break;
-      }
-      tile[Tile<CB>::idx(ti, tj, tk)] =
-          nbrick >= 0 ? __ldg(v + nbrick * C + (li + CB * (lj + CB * lk))) : 0.0;
+    for (int s = threadIdx.x; s < 6 * CB * CB; s += blockDim.x) {
+      int f, ti, nl;
+      halo_slot<CB>(s, f, ti, nl);
+      const int nb = nbr_brick(g, bc, f);
+      tile[ti] = nb >= 0 ? __ldg(v + bofs(nb, C) + nl) : 0.0;
     }
+  }
+}
+
+// All face transmissibilities of the tile (faces touching at least one
+// interior cell); 0 where a face cell lies outside the domain.
+template <int CB>
+__device__ __forceinline__ void tile_faces(const double* kt, double* fx, double* fy, double* fz,
+                                           const GridParams& g, const BrickCoord& bc) {
+  constexpr int NF = Tile<CB>::NF;
+  constexpr int C = CB * CB * CB;
+  for (int s = threadIdx.x; s < 3 * NF; s += C) {
+    const int ax = s / NF, r = s % NF;
+    const int a = r % (CB + 1) - 1, u = (r / (CB + 1)) % CB, w = r / ((CB + 1) * CB);
+    int i0, j0, k0, i1, j1, k1, ga;
+    int64_t n;
+    if (ax == 0) { i0 = a; j0 = u; k0 = w; i1 = a + 1; j1 = u; k1 = w; ga = bc.bi * CB + a; n = g.nx; }
+    else if (ax == 1) { i0 = u; j0 = a; k0 = w; i1 = u; j1 = a + 1; k1 = w; ga = bc.bj * CB + a; n = g.ny; }
+    else { i0 = u; j0 = w; k0 = a; i1 = u; j1 = w; k1 = a + 1; ga = bc.bk * CB + a; n = g.nz; }
+    double T = 0.0;
+    if (ga >= 0 && ga + 1 < n) {
+      // low cell first: face_transmissibility(k[low], k[high]) — both reference
+      // call sites evaluate this product order (fvm.cpp:73-76, 91-94)
+      T = __dmul_rn(face_t(kt[Tile<CB>::idx(i0, j0, k0)], kt[Tile<CB>::idx(i1, j1, k1)]),
+                    g.cpl[ax]);
+    }
+    (ax == 0 ? fx : ax == 1 ? fy : fz)[r] = T;
   }
 }
 
@@ -92,33 +131,28 @@ struct FaceSet {
 };
 
 template <int CB>
-__device__ __forceinline__ FaceSet cell_faces(const double* kt, int li, int lj, int lk,
+__device__ __forceinline__ FaceSet cell_faces(const double* fx, const double* fy, const double* fz,
+                                              double kc, int li, int lj, int lk,
                                               const GridParams& g, const BrickCoord& bc,
                                               unsigned dmask) {
-  constexpr int E = Tile<CB>::E;
-  const int ti = Tile<CB>::idx(li, lj, lk);
-  const double kc = kt[ti];
-  const int64_t gi = bc.bi * CB + li, gj = bc.bj * CB + lj, gk = bc.bk * CB + lk;
+  const int gi = bc.bi * CB + li, gj = bc.bj * CB + lj, gk = bc.bk * CB + lk;
   const bool has[6] = {gi > 0, gi < g.nx - 1, gj > 0, gj < g.ny - 1, gk > 0, gk < g.nz - 1};
-  const int off[6] = {-1, 1, -E, E, -E * E, E * E};
+  const double ft[6] = {fx[Tile<CB>::fxi(li - 1, lj, lk)], fx[Tile<CB>::fxi(li, lj, lk)],
+                        fy[Tile<CB>::fyi(li, lj - 1, lk)], fy[Tile<CB>::fyi(li, lj, lk)],
+                        fz[Tile<CB>::fzi(li, lj, lk - 1)], fz[Tile<CB>::fzi(li, lj, lk)]};
   FaceSet fs;
   fs.nbmask = 0;
   double diag = 0.0;
 #pragma unroll
   for (int f = 0; f < 6; ++f) {
-    const double cp = g.cpl[f >> 1];
-    double t;
+    double t = 0.0;
     if (has[f]) {
-      const double kn = kt[ti + off[f]];
-      // low side: face_transmissibility(k[nb], k[c]); high: (k[c], k[nb])
-      t = (f & 1) ? __dmul_rn(face_t(kc, kn), cp) : __dmul_rn(face_t(kn, kc), cp);
+      t = ft[f];
       fs.nbmask |= 1 << f;
       diag = __dadd_rn(diag, t);
     } else if (dmask & (1u << f)) {
-      t = __dmul_rn(__dmul_rn(2.0, kc), cp);
+      t = __dmul_rn(__dmul_rn(2.0, kc), g.cpl[f >> 1]);
       diag = __dadd_rn(diag, t);
-    } else {
-      t = 0.0;
     }
     fs.t[f] = t;
   }
@@ -146,6 +180,69 @@ __device__ __forceinline__ double apply_row(const FaceSet& fs, const double* xt,
 __device__ __forceinline__ bool brick_on_boundary(const GridParams& g, const BrickCoord& bc) {
   return bc.bi == 0 || bc.bj == 0 || bc.bk == 0 || bc.bi == g.nbx - 1 || bc.bj == g.nby - 1 ||
          bc.bk == g.nbz - 1;
+}
+
+// Shared-memory scratch of one stencil tile: kappa tile + three face arrays.
+template <int CB>
+struct StencilSmem {
+  double kt[Tile<CB>::N];
+  double fx[Tile<CB>::NF], fy[Tile<CB>::NF], fz[Tile<CB>::NF];
+};
+
+// ------------------------------------------------ precomputed coefficients
+//
+// The solve phase applies A from four per-cell coefficient arrays computed
+// once at set-up with the reference's exact expressions (k_coefficients):
+//   coef[0] = T to the +x neighbour (0 if none), coef[1] = +y, coef[2] = +z,
+//   coef[3] = diagonal (faces summed in reference order, Dirichlet included).
+// A tile needs each axis' coefficients for its cells plus the low halo layer.
+template <int CB>
+struct CoefSmem {
+  double fx[Tile<CB>::NF], fy[Tile<CB>::NF], fz[Tile<CB>::NF];
+  double dg[CB * CB * CB];
+};
+
+template <int CB>
+__device__ __forceinline__ void load_coefs(const double* __restrict__ coef, int64_t M, CoefSmem<CB>& cs,
+                                           const GridParams& g, const BrickCoord& bc) {
+  constexpr int C = CB * CB * CB;
+  for (int t = threadIdx.x; t < C; t += blockDim.x) {
+    const int li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+    const size_t s = bofs(bc.b, C) + t;
+    cs.fx[Tile<CB>::fxi(li, lj, lk)] = __ldg(coef + s);
+    cs.fy[Tile<CB>::fyi(li, lj, lk)] = __ldg(coef + M + s);
+    cs.fz[Tile<CB>::fzi(li, lj, lk)] = __ldg(coef + 2 * M + s);
+    cs.dg[t] = __ldg(coef + 3 * M + s);
+  }
+  // low halo layers: the +axis coefficient of the neighbouring brick's top layer
+  for (int h = threadIdx.x; h < 3 * CB * CB; h += blockDim.x) {
+    const int ax = h / (CB * CB), q = h % (CB * CB), u = q % CB, w = q / CB;
+    const int nb = nbr_brick(g, bc, 2 * ax);
+    int nl, fi;
+    if (ax == 0) { nl = (CB - 1) + CB * (u + CB * w); fi = Tile<CB>::fxi(-1, u, w); }
+    else if (ax == 1) { nl = u + CB * ((CB - 1) + CB * w); fi = Tile<CB>::fyi(u, -1, w); }
+    else { nl = u + CB * (w + CB * (CB - 1)); fi = Tile<CB>::fzi(u, w, -1); }
+    const double v = nb >= 0 ? __ldg(coef + (size_t)ax * M + bofs(nb, C) + nl) : 0.0;
+    (ax == 0 ? cs.fx : ax == 1 ? cs.fy : cs.fz)[fi] = v;
+  }
+}
+
+// (A x)_c, branch-free: missing neighbours have T = 0 and a 0 halo value, so
+// their -0 terms leave the sum bitwise unchanged; order and rounding are those
+// of SparseOperator::apply on the assembled row (sparse.cpp:76-83).
+template <int CB>
+__device__ __forceinline__ double apply_coef(const CoefSmem<CB>& cs, const double* xt, int li, int lj,
+                                             int lk) {
+  constexpr int E = Tile<CB>::E;
+  const int ti = Tile<CB>::idx(li, lj, lk);
+  double s = __dadd_rn(0.0, __dmul_rn(-cs.fz[Tile<CB>::fzi(li, lj, lk - 1)], xt[ti - E * E]));
+  s = __dadd_rn(s, __dmul_rn(-cs.fy[Tile<CB>::fyi(li, lj - 1, lk)], xt[ti - E]));
+  s = __dadd_rn(s, __dmul_rn(-cs.fx[Tile<CB>::fxi(li - 1, lj, lk)], xt[ti - 1]));
+  s = __dadd_rn(s, __dmul_rn(cs.dg[li + CB * (lj + CB * lk)], xt[ti]));
+  s = __dadd_rn(s, __dmul_rn(-cs.fx[Tile<CB>::fxi(li, lj, lk)], xt[ti + 1]));
+  s = __dadd_rn(s, __dmul_rn(-cs.fy[Tile<CB>::fyi(li, lj, lk)], xt[ti + E]));
+  s = __dadd_rn(s, __dmul_rn(-cs.fz[Tile<CB>::fzi(li, lj, lk)], xt[ti + E * E]));
+  return s;
 }
 
 }  // namespace tmg

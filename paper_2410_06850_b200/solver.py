@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtopmg_b200.so")
+LIB_PATH = os.environ.get("TMG_LIB", os.path.join(_HERE, "libtopmg_b200.so"))
 
 TMG_OK, TMG_ECONFIG, TMG_ESOLVER, TMG_EARG, TMG_ECUDA, TMG_ENOTSUP = range(6)
 
@@ -342,7 +342,7 @@ class Context:
         cnt = (C.c_int * 9)()
         self._check(native().tmg_profile_solve(self._p, C.c_double(rtol),
                                                C.c_int(max_iterations), ms, cnt))
-        names = ["search", "update", "restrict", "coarse_down", "gemv", "coarse_up", "post",
+        names = ["search", "update", "restrict", "coarse", "unused4", "unused5", "post",
                  "jacobi_step", "init"]
         return {n: (ms[i], cnt[i]) for i, n in enumerate(names)}
 
