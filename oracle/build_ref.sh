@@ -1,0 +1,35 @@
+#!/usr/bin/env bash
+# ORACLE — test infrastructure only.
+# Compiles the reference's own proj/core sources, unmodified and where they lie
+# under /root/reference, together with the Eigen-API subset shim
+# (oracle/eigen_shim) and the C harness (oracle/ref_harness.cpp) into
+# oracle/_ref/libtopmg_ref.so. No reference source is copied into the repo and
+# the reference's own CMake build is not used. The output is git-ignored but
+# travels to the GPU box with the working tree.
+set -euo pipefail
+HERE="$(cd "$(dirname "${BASH_SOURCE[0]}")" && pwd)"
+REF="${TOPMG_REFERENCE:-/root/reference}/proj/core"
+OUT="$HERE/_ref"
+if [ ! -d "$REF/src" ]; then
+  echo "build_ref.sh: reference sources not found at $REF" >&2
+  exit 1
+fi
+mkdir -p "$OUT/obj"
+CXX=/usr/bin/g++
+CC=/usr/bin/gcc
+# x86-64-v2: portable to the GPU box host; no FMA contraction (matches the
+# oracle restatement's rounding of dot products).
+FLAGS="-O2 -march=x86-64-v2 -fPIC -pthread"
+SRCS="grid material fvm sparse solver coarse_space parallel rng"
+pids=()
+for s in $SRCS; do
+  $CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$REF/src/$s.cpp" -o "$OUT/obj/$s.o" &
+  pids+=($!)
+done
+$CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$HERE/ref_harness.cpp" -o "$OUT/obj/ref_harness.o" &
+pids+=($!)
+$CC -std=c11 $FLAGS -c "$HERE/dense_la.c" -o "$OUT/obj/dense_la.o" &
+pids+=($!)
+for p in "${pids[@]}"; do wait "$p"; done
+$CXX -shared -pthread -o "$OUT/libtopmg_ref.so" "$OUT"/obj/*.o -lm
+echo "built $OUT/libtopmg_ref.so"

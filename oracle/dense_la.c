@@ -468,3 +468,39 @@ void dla_env_ldlt_solve(int64_t n, const int64_t* first, const int64_t* rowptr,
     for (int64_t kk = first[i]; kk < i; ++kk) x[kk] -= ri[kk - first[i]] * xi;
   }
 }
+
+/* All eigenvalues (ascending) of the symmetric n x n row-major `a` (destroyed)
+ * plus eigenvectors for the k smallest (v: n x k row-major). Used by the
+ * Eigen shim: the reference reads only leading eigenvector columns. */
+int dla_syev_partial(int n, int k, double* a, double* w_all, double* v) {
+  if (n <= 0) return 0;
+  if (k > n) k = n;
+  double* acopy = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);
+  memcpy(acopy, a, sizeof(double) * (size_t)n * (size_t)n);
+  double* d = (double*)malloc(sizeof(double) * (size_t)n);
+  double* e = (double*)malloc(sizeof(double) * (size_t)n);
+  tridiagonalize(n, acopy, d, e, NULL, 0);
+  int rc = tql_rows(n, d, e, NULL);
+  if (rc == 0) {
+    /* ascending insertion sort of the eigenvalues */
+    for (int i = 1; i < n; ++i) {
+      const double x = d[i];
+      int j = i - 1;
+      while (j >= 0 && d[j] > x) {
+        d[j + 1] = d[j];
+        --j;
+      }
+      d[j + 1] = x;
+    }
+    memcpy(w_all, d, sizeof(double) * (size_t)n);
+    if (k > 0) {
+      double* wk = (double*)malloc(sizeof(double) * (size_t)k);
+      rc = dla_syev_smallest(n, k, a, wk, v);
+      free(wk);
+    }
+  }
+  free(acopy);
+  free(d);
+  free(e);
+  return rc;
+}

@@ -13,6 +13,9 @@ int dla_syev_all(int n, double* a, double* w, double* v);
 /* The k smallest eigenpairs. w: k ascending; v: n x k row-major. */
 int dla_syev_smallest(int n, int k, double* a, double* w, double* v);
 
+/* All eigenvalues ascending + the k smallest eigenvectors (v: n x k). */
+int dla_syev_partial(int n, int k, double* a, double* w_all, double* v);
+
 /* Envelope LDL^T (no pivoting) of an SPD matrix; row i holds columns
  * [first[i], i] at vals[rowptr[i]..]. Returns -1 (bad_index set) when a pivot
  * fails d_i > 1e-14 * max|d| (the rule of proj/core/src/solver.cpp:86-92). */

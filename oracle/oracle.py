@@ -252,3 +252,110 @@ def syev_all(a):
     if rc:
         raise OracleError(rc, "eigensolver failed")
     return w, v
+
+
+# --------------------------------------------------------------------------
+# The reference itself (oracle/_ref/libtopmg_ref.so, built by build_ref.sh)
+# --------------------------------------------------------------------------
+
+REF_PATH = os.path.join(HERE, "_ref", "libtopmg_ref.so")
+
+
+def ref_available():
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _REF
+    if _REF is None:
+        R = C.CDLL(REF_PATH)
+        R.ref_last_error.restype = C.c_char_p
+        R.ref_ctx_create.restype = C.c_void_p
+        R.ref_ctx_create.argtypes = [I64, I64, I64, DP, C.c_int, DP, C.c_int, C.c_int, C.c_int,
+                                     I64, I64, C.c_int, DP]
+        R.ref_ctx_pcg.argtypes = [C.c_void_p, C.c_double, C.c_int, DP, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), DP]
+        R.ref_ctx_destroy.argtypes = [C.c_void_p]
+        R.ref_num_threads.restype = C.c_int
+        _REF = R
+    return _REF
+
+
+def _ref_check(rc):
+    if rc != 0:
+        raise OracleError(rc, ref().ref_last_error().decode())
+
+
+def _patch_array(patches):
+    a = np.zeros(6 * max(1, len(patches)))
+    for i, p in enumerate(patches):
+        a[6 * i:6 * i + 6] = p
+    return a
+
+
+def ref_frozen_bench_design(n, vstar, seed=20240501, passes=2):
+    out = np.empty(n ** 3)
+    ref().ref_frozen_bench_design(I64(n), I64(n), I64(n), C.c_double(vstar), C.c_uint64(seed),
+                                  C.c_int(passes), _d(out))
+    return out
+
+
+def ref_conductivity(x, lo, hi=1.0, p=3):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _ref_check(ref().ref_conductivity(I64(x.size), _d(x), C.c_double(lo), C.c_double(hi),
+                                      C.c_int(p), _d(out)))
+    return out
+
+
+def ref_assemble(n, kappa, source, patches, l=(1.0, 1.0, 1.0)):
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    m = nx * ny * nz
+    off = np.empty(m + 1, dtype=np.int64)
+    col = np.empty(7 * m, dtype=np.int64)
+    val = np.empty(7 * m)
+    rhs = np.empty(m)
+    pa = _patch_array(patches)
+    _ref_check(ref().ref_assemble(I64(nx), I64(ny), I64(nz), C.c_double(l[0]), C.c_double(l[1]),
+                                  C.c_double(l[2]), _d(np.ascontiguousarray(kappa, np.float64)),
+                                  _d(np.ascontiguousarray(source, np.float64)), C.c_int(len(patches)),
+                                  _d(pa), off.ctypes.data_as(IP), col.ctypes.data_as(IP), _d(val),
+                                  _d(rhs)))
+    import scipy.sparse as sp
+    nnz = off[-1]
+    return sp.csr_matrix((val[:nnz], col[:nnz], off), shape=(m, m)), rhs
+
+
+def ref_local_basis(n, ncc, sd, kappa, cid, count):
+    cpc = n // (ncc * sd)
+    vals = np.empty(count)
+    vecs = np.empty(count * cpc ** 3)
+    _ref_check(ref().ref_local_basis(I64(n), I64(n), I64(n), I64(ncc), I64(sd),
+                                     _d(np.ascontiguousarray(kappa, np.float64)), I64(cid),
+                                     I64(count), _d(vals), _d(vecs)))
+    return vals, vecs.reshape(count, cpc ** 3)
+
+
+def ref_solve(n, ncc, sd, kappa, rhs, patches, kind="mmg", fine_blocks=None,
+              coarse_blocks=None, lc=4, lcc=8, sweeps=1, rtol=1e-8, maxit=10000, x0=None):
+    """Reference make_preconditioner/build_hierarchy_operators + pcg. Blocks:
+    None = make_preconditioner default; 'cc' / 'point' / 'cell'."""
+    m = n ** 3
+    x = np.empty(m)
+    hist = np.zeros(max(1, maxit))
+    it = C.c_int()
+    conv = C.c_int()
+    ts = C.c_double()
+    tv = C.c_double()
+    pa = _patch_array(patches)
+    fb = -1 if fine_blocks is None else BLOCKS[fine_blocks]
+    cb = -1 if coarse_blocks is None else BLOCKS[coarse_blocks]
+    x0p = _d(np.ascontiguousarray(x0, np.float64)) if x0 is not None else None
+    _ref_check(ref().ref_solve(I64(n), I64(ncc), I64(sd),
+                               _d(np.ascontiguousarray(kappa, np.float64)),
+                               _d(np.ascontiguousarray(rhs, np.float64)), C.c_int(len(patches)),
+                               _d(pa), C.c_int(KIND[kind]), C.c_int(fb), C.c_int(cb), I64(lc),
+                               I64(lcc), C.c_int(sweeps), C.c_double(rtol), C.c_int(maxit), x0p,
+                               _d(x), C.byref(it), C.byref(conv), _d(hist), C.byref(ts),
+                               C.byref(tv)))
+    return PcgResult(x, it.value, bool(conv.value), hist[:it.value].copy(), tv.value), ts.value

@@ -1,0 +1,267 @@
+// ORACLE — test infrastructure only.
+//
+// C entry points over the reference's own proj/core code (compiled unmodified
+// from /root/reference by oracle/build_ref.sh into oracle/_ref/libtopmg_ref.so)
+// so tests and bench.py's reference arm can run the reference solver on the
+// same inputs as the GPU path. Nothing here re-implements reference logic: it
+// only marshals arrays and builds the block partitions through the reference's
+// public HierarchicalGrid API.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "topmg/coarse_space.hpp"
+#include "topmg/fvm.hpp"
+#include "topmg/grid.hpp"
+#include "topmg/material.hpp"
+#include "topmg/parallel.hpp"
+#include "topmg/rng.hpp"
+#include "topmg/solver.hpp"
+#include "topmg/sparse.hpp"
+
+using namespace topmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+  g_err = e.what();
+  return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigError& e) {
+    return fail(e, 1);
+  } catch (const SolverError& e) {
+    return fail(e, 2);
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 3);
+  } catch (const std::exception& e) {
+    return fail(e, 4);
+  }
+}
+
+BoundarySpec make_bc(int npatch, const double* patches) {
+  BoundarySpec bc;
+  for (int i = 0; i < npatch; ++i) {
+    DirichletPatch p;
+    p.face = static_cast<Face>(static_cast<int>(patches[6 * i + 0]));
+    p.u0 = patches[6 * i + 1];
+    p.v0 = patches[6 * i + 2];
+    p.u1 = patches[6 * i + 3];
+    p.v1 = patches[6 * i + 4];
+    p.value = patches[6 * i + 5];
+    bc.patches.push_back(p);
+  }
+  return bc;
+}
+
+std::vector<std::vector<index_t>> blocks(const HierarchicalGrid& h, int kind, index_t lc,
+                                         bool coarse) {
+  // kind: 0 = per cc element (reference default), 1 = point, 2 = per coarse cell
+  std::vector<std::vector<index_t>> out;
+  if (!coarse) {
+    if (kind == 0) {
+      for (index_t e = 0; e < h.num_coarse_coarse(); ++e) out.push_back(h.cells_of_coarse_coarse(e));
+    } else if (kind == 1) {
+      for (index_t c = 0; c < h.spec.num_cells(); ++c) out.push_back({c});
+    } else {
+      for (index_t e = 0; e < h.num_coarse(); ++e) out.push_back(h.cells_of_coarse(e));
+    }
+  } else {
+    if (kind == 0) {
+      for (index_t e = 0; e < h.num_coarse_coarse(); ++e) {
+        std::vector<index_t> rows;
+        for (index_t child : h.coarse_children(e))
+          for (index_t j = 0; j < lc; ++j) rows.push_back(child * lc + j);
+        out.push_back(rows);
+      }
+    } else {
+      for (index_t e = 0; e < h.num_coarse(); ++e) {
+        std::vector<index_t> rows;
+        for (index_t j = 0; j < lc; ++j) rows.push_back(e * lc + j);
+        out.push_back(rows);
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_set_num_threads(int n) { set_num_threads(n); }
+int ref_num_threads() { return num_threads(); }
+
+void ref_frozen_bench_design(int64_t nx, int64_t ny, int64_t nz, double vstar, uint64_t seed,
+                             int passes, double* rho) {
+  const GridSpec g(nx, ny, nz);
+  const DesignField d = frozen_bench_design(g, vstar, seed, passes);
+  std::memcpy(rho, d.values.data(), sizeof(double) * d.values.size());
+}
+
+int ref_conductivity(int64_t n, const double* x, double lo, double hi, int p, double* kappa) {
+  return guarded([&] {
+    const GridSpec g(n, 1, 1);
+    const DesignField d(g, std::vector<double>(x, x + n));
+    const MaterialModel m(lo, hi, 1.0, p);
+    const std::vector<double> k = conductivity(d, m);
+    std::memcpy(kappa, k.data(), sizeof(double) * k.size());
+  });
+}
+
+// assemble_system: writes rhs (M) and the CSR arrays (capacity 7M).
+int ref_assemble(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                 const double* kappa, const double* source, int npatch, const double* patches,
+                 int64_t* offsets, int64_t* cols, double* vals, double* rhs) {
+  return guarded([&] {
+    const GridSpec g(nx, ny, nz, lx, ly, lz);
+    const index_t m = g.num_cells();
+    const AssembledSystem sys =
+        assemble_system(g, std::vector<double>(kappa, kappa + m),
+                        std::vector<double>(source, source + m), make_bc(npatch, patches));
+    std::memcpy(offsets, sys.matrix.row_offsets().data(), sizeof(int64_t) * (m + 1));
+    std::memcpy(cols, sys.matrix.col_indices().data(), sizeof(int64_t) * sys.matrix.nnz());
+    std::memcpy(vals, sys.matrix.values().data(), sizeof(double) * sys.matrix.nnz());
+    std::memcpy(rhs, sys.rhs.data(), sizeof(double) * m);
+  });
+}
+
+int ref_local_basis(int64_t nx, int64_t ny, int64_t nz, int64_t ncc, int64_t sd,
+                    const double* kappa, int64_t coarse_id, int64_t count, double* values,
+                    double* vectors) {
+  return guarded([&] {
+    const GridSpec g(nx, ny, nz);
+    const HierarchicalGrid h = build_hierarchy(g, {ncc, ncc, ncc}, sd);
+    const LocalSpectralBasis b = local_spectral_basis(
+        h, std::vector<double>(kappa, kappa + g.num_cells()), coarse_id, count);
+    std::memcpy(values, b.eigenvalues.data(), sizeof(double) * b.eigenvalues.size());
+    std::memcpy(vectors, b.vectors.data(), sizeof(double) * b.vectors.size());
+  });
+}
+
+// Full reference solve: assemble, make_preconditioner (kind 0 none, 1 jacobi,
+// 2 block_jacobi, 3 two_grid, 4 mmg) or — when fine_blocks/coarse_blocks >= 0
+// with kind 4 — build_coarse_spaces + build_hierarchy_operators with the given
+// partitions, then pcg. Returns iterations etc.; solve/setup seconds from the
+// reference's own timers (bench.cpp:54-59, solver.cpp:494,570-573).
+int ref_solve(int64_t n, int64_t ncc, int64_t sd, const double* kappa, const double* rhs_in,
+              int npatch, const double* patches, int kind, int fine_blocks, int coarse_blocks,
+              int64_t lc, int64_t lcc, int sweeps, double rtol, int maxit, const double* x0,
+              double* x_out, int* iterations, int* converged, double* history,
+              double* setup_seconds, double* solve_seconds) {
+  return guarded([&] {
+    const GridSpec g(n, n, n);
+    const index_t m = g.num_cells();
+    const HierarchicalGrid h = build_hierarchy(g, {ncc, ncc, ncc}, sd);
+    const std::vector<double> kap(kappa, kappa + m);
+    const AssembledSystem sys =
+        assemble_system(g, kap, std::vector<double>(m, 0.0), make_bc(npatch, patches));
+    const std::vector<double> b(rhs_in, rhs_in + m);
+    MmgOptions opts;
+    opts.num_local_basis = lc;
+    opts.num_cc_basis = lcc;
+    opts.smoother_sweeps = sweeps;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::unique_ptr<Preconditioner> pre;
+    if (kind == 4 && fine_blocks >= 0) {
+      CoarseSpaces cs = build_coarse_spaces(h, kap, lc, lcc);
+      pre = std::make_unique<MultiscaleHierarchy>(build_hierarchy_operators(
+          sys.matrix, std::move(cs.restriction_c), std::move(cs.restriction_cc),
+          blocks(h, fine_blocks, lc, false), blocks(h, coarse_blocks, lc, true), sweeps));
+    } else {
+      static const PrecondKind kinds[] = {PrecondKind::None, PrecondKind::Jacobi,
+                                          PrecondKind::BlockJacobi, PrecondKind::TwoGrid,
+                                          PrecondKind::Mmg};
+      pre = make_preconditioner(kinds[kind], sys, h, opts);
+    }
+    *setup_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    PcgOptions po;
+    po.rtol = rtol;
+    po.max_iterations = maxit;
+    std::vector<double> xx0;
+    if (x0) xx0.assign(x0, x0 + m);
+    const PcgResult r = pcg(sys.matrix, b, *pre, po, xx0);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * m);
+    *iterations = r.report.iterations;
+    *converged = r.report.converged ? 1 : 0;
+    if (history)
+      std::memcpy(history, r.report.residual_history.data(),
+                  sizeof(double) * r.report.residual_history.size());
+    *solve_seconds = r.report.solve_seconds;
+  });
+}
+
+// The reference solve as a reusable object (bench.py's reference arm times
+// repeated pcg() calls against one set-up).
+struct RefCtx {
+  AssembledSystem sys;
+  std::unique_ptr<Preconditioner> pre;
+};
+
+void* ref_ctx_create(int64_t n, int64_t ncc, int64_t sd, const double* kappa, int npatch,
+                     const double* patches, int kind, int fine_blocks, int coarse_blocks,
+                     int64_t lc, int64_t lcc, int sweeps, double* setup_seconds) {
+  RefCtx* c = new RefCtx;
+  const int rc = guarded([&] {
+    const GridSpec g(n, n, n);
+    const index_t m = g.num_cells();
+    const HierarchicalGrid h = build_hierarchy(g, {ncc, ncc, ncc}, sd);
+    const std::vector<double> kap(kappa, kappa + m);
+    c->sys = assemble_system(g, kap, std::vector<double>(m, 1.0), make_bc(npatch, patches));
+    MmgOptions opts;
+    opts.num_local_basis = lc;
+    opts.num_cc_basis = lcc;
+    opts.smoother_sweeps = sweeps;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (kind == 4 && fine_blocks >= 0) {
+      CoarseSpaces cs = build_coarse_spaces(h, kap, lc, lcc);
+      c->pre = std::make_unique<MultiscaleHierarchy>(build_hierarchy_operators(
+          c->sys.matrix, std::move(cs.restriction_c), std::move(cs.restriction_cc),
+          blocks(h, fine_blocks, lc, false), blocks(h, coarse_blocks, lc, true), sweeps));
+    } else {
+      static const PrecondKind kinds[] = {PrecondKind::None, PrecondKind::Jacobi,
+                                          PrecondKind::BlockJacobi, PrecondKind::TwoGrid,
+                                          PrecondKind::Mmg};
+      c->pre = make_preconditioner(kinds[kind], c->sys, h, opts);
+    }
+    *setup_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  if (rc) {
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+int ref_ctx_pcg(void* ctx, double rtol, int maxit, double* x_out, int* iterations,
+                int* converged, double* solve_seconds) {
+  RefCtx* c = static_cast<RefCtx*>(ctx);
+  return guarded([&] {
+    PcgOptions po;
+    po.rtol = rtol;
+    po.max_iterations = maxit;
+    const PcgResult r = pcg(c->sys.matrix, c->sys.rhs, *c->pre, po);
+    if (x_out) std::memcpy(x_out, r.x.data(), sizeof(double) * r.x.size());
+    *iterations = r.report.iterations;
+    *converged = r.report.converged ? 1 : 0;
+    *solve_seconds = r.report.solve_seconds;
+  });
+}
+
+void ref_ctx_destroy(void* ctx) { delete static_cast<RefCtx*>(ctx); }
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports exactly the
+entry points include/topmg_b200.h declares, and validates configurations the
+way the reference does before any device work."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "topmg_b200.h")
+PKG = os.path.join(ROOT, "paper_2410_06850_b200")
+
+from paper_2410_06850_b200 import (BoundarySpec, ConfigError, Context, GridSpec,  # noqa: E402
+                                   NotSupportedError, PrecondKind, native, solver)
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(tmg_\w+)\s*\(", text, re.M)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    lib = native()
+    decl = declared_symbols()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), name
+    nm = subprocess.run(["nm", "-D", "--defined-only", solver.LIB_PATH], capture_output=True,
+                        text=True).stdout
+    exported = sorted(set(re.findall(r"\bT (tmg_\w+)", nm)))
+    assert exported == decl
+    assert set(solver.EXPORTED_SYMBOLS) == set(decl)
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", solver.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_product_does_not_use_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                for bad in ("import oracle", "from oracle", "liboracle", "libtopmg_ref",
+                            "#include \"topmg_oracle", "dense_la"):
+                    assert bad not in text, (f, bad)
+
+
+def test_create_rejects_nondivisible_hierarchy():
+    # build_hierarchy (grid.cpp:205-213): axis not divisible by ncc*sd -> ConfigError
+    with pytest.raises(ConfigError, match="not divisible"):
+        Context(GridSpec(30, 32, 32), 2, 2)
+
+
+def test_create_rejects_bad_grid():
+    with pytest.raises(ConfigError):
+        Context(GridSpec(0, 8, 8), 1, 1)
+    with pytest.raises(ConfigError):
+        Context(GridSpec(8, 8, 8, lx=-1.0), 1, 1)
+    with pytest.raises(ConfigError):
+        Context(GridSpec(8, 8, 8), 0, 1)
+
+
+def test_create_rejects_unsupported_coarse_cell_shape():
+    # the GPU path builds cubic 4^3 / 8^3 coarse cells
+    with pytest.raises(NotSupportedError):
+        Context(GridSpec(12, 12, 12), 1, 2)
+
+
+def test_precond_kind_parse():
+    assert PrecondKind.parse("mmg") == PrecondKind.MMG
+    assert PrecondKind.parse("jacobi") == PrecondKind.JACOBI
+    with pytest.raises(ConfigError, match="unknown preconditioner kind"):
+        PrecondKind.parse("amg")
+
+
+def test_bottom_center_patch_matches_reference_formula():
+    bc = BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0)
+    p = bc.patches[0]
+    assert (p.face, p.u0, p.v0, p.u1, p.v1) == (4, 0.4, 0.4, 0.6, 0.6)
+
+
+def test_inputs_config_table():
+    from paper_2410_06850_b200 import inputs
+    c1 = inputs.CONFIGS[1]
+    assert c1["n"] % (c1["ncc"] * c1["sd"]) == 0
+    assert c1["n"] // (c1["ncc"] * c1["sd"]) == 8
+
+
+def test_header_documents_reference_interfaces():
+    text = open(HEADER).read()
+    for ref in ["solver.cpp:483-575", "solver.cpp:462-481", "fvm.cpp:33-51", "sparse.cpp:71-84",
+                "grid.cpp:196-218"]:
+        assert ref in text, ref

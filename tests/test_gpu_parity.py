@@ -1,0 +1,419 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the oracle's
+restatement of the reference and against golden fixtures produced by the
+reference itself. Bars (BASELINE.json north_star): FP64, same stopping rule,
+relative solution error <= 1e-6, PCG iteration count within 10%; the TPFA
+apply and the rhs assembly are bitwise."""
+import glob
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+import oracle as O
+from paper_2410_06850_b200 import (BoundarySpec, ConfigError, Context, DirichletPatch, GridSpec,
+                                   MmgOptions, NotSupportedError, SolverError, inputs,
+                                   make_preconditioner, pcg)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+BC = BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0)
+PATCH = O.bottom_center_patch()
+
+
+def problem(n, kmin, vf=0.3, radius=2):
+    rho = inputs.box_filter_design(n, vf, radius=radius)
+    return rho, inputs.conductivity(rho, kmin)
+
+
+def ctx_for(n, ncc, sd, kappa, bc=BC, grid=None):
+    c = Context(grid or GridSpec(n, n, n), ncc, sd)
+    c.set_conductivity(kappa, bc)
+    return c
+
+
+def iters_close(a, b):
+    return abs(a - b) <= max(1, int(0.1 * b))
+
+
+# ------------------------------------------------------------- operator, rhs
+
+@pytest.mark.parametrize("dims,l,ncc,sd", [((16, 16, 16), (1, 1, 1), 2, 2),
+                                           ((32, 32, 32), (1, 1, 1), 2, 2),
+                                           ((16, 8, 24), (2.0, 1.0, 1.5), (2, 1, 3), 2),
+                                           ((64, 64, 64), (1, 1, 1), 4, 2)])
+def test_apply_and_rhs_bitwise(dims, l, ncc, sd):
+    nx, ny, nz = dims
+    m = nx * ny * nz
+    rng = np.random.default_rng(m)
+    kappa = 10.0 ** rng.uniform(-6, 0, m)
+    source = rng.random(m)
+    patches = [(4, 0.2 * l[0], 0.3 * l[1], 0.7 * l[0], 0.6 * l[1], 3.0),
+               (1, 0.0, 0.0, 0.5 * l[1], 0.5 * l[2], -1.0)]
+    bc = BoundarySpec([DirichletPatch(*p) for p in patches])
+    s = O.System(O.grid(dims, l), kappa, source, patches)
+    c = ctx_for(None, ncc, sd, kappa, bc, GridSpec(nx, ny, nz, *l))
+    x = rng.standard_normal(m)
+    np.testing.assert_array_equal(c.apply_operator(x), s.apply(x))
+    np.testing.assert_array_equal(c.assemble_rhs(source), s.rhs)
+
+
+def test_set_design_conductivity_bitwise():
+    n = 16
+    rho = np.random.default_rng(2).random(n ** 3)
+    kappa = O.conductivity(rho, 1e-3, 1.0, 3)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    c = Context(GridSpec(n, n, n), 2, 2)
+    c.set_design(rho, 1e-3, 1.0, 3, BC)
+    x = np.random.default_rng(3).standard_normal(n ** 3)
+    np.testing.assert_array_equal(c.apply_operator(x), s.apply(x))
+
+
+# ----------------------------------------------------------------- PCG parity
+
+@pytest.mark.parametrize("n,kmin", [(16, 1e-3), (32, 1e-6)])
+def test_jacobi_pcg_vs_oracle(n, kmin):
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    ref = O.pcg(s, s.rhs, O.Precond("jacobi", s), rtol=1e-8, max_iterations=20000)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("jacobi")
+    r = c.pcg(s.rhs, rtol=1e-8, max_iterations=20000)
+    assert r.report.converged and iters_close(r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (16, 2, 2, 1e-6), (32, 2, 2, 1e-3),
+                                           (32, 2, 2, 1e-6), (64, 4, 2, 1e-3)])
+def test_mmg_pcg_vs_oracle(n, ncc, sd, kmin):
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond("mmg", s, O.hierarchy(O.grid(n), ncc, sd), fine_blocks="cell",
+                  coarse_blocks="cc")
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg")
+    r = c.pcg(s.rhs, rtol=1e-8)
+    assert r.report.converged
+    assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+    k = min(len(r.report.residual_history), len(ref.residual_history))
+    np.testing.assert_allclose(r.report.residual_history[:k // 2], ref.residual_history[:k // 2],
+                               rtol=1e-3)
+
+
+def _golden():
+    return sorted(p for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if "local_basis" not in p)
+
+
+@pytest.mark.parametrize("path", _golden(), ids=lambda p: os.path.basename(p)[:-4])
+def test_pcg_vs_reference_golden(path):
+    z = np.load(path)
+    n, ncc, sd = int(z["n"]), int(z["ncc"]), int(z["sd"])
+    kind = str(z["kind"])
+    fb = str(z["fine_blocks"])
+    rho = inputs.box_filter_design(n, float(z["vf"]), passes=int(z["passes"]),
+                                   radius=int(z["radius"]))
+    kappa = inputs.conductivity(rho, float(z["kmin"]))
+    c = ctx_for(n, ncc, sd, kappa)
+    b = c.assemble_rhs(np.ones(n ** 3))
+    np.testing.assert_array_equal(b, z["rhs"])
+    np.testing.assert_array_equal(c.apply_operator(z["apply_in"]), z["apply_out"])
+    c.setup(kind)
+    r = c.pcg(b, rtol=float(z["rtol"]), max_iterations=20000)
+    assert r.report.converged
+    ref_it = int(z["iterations"])
+    rel = np.linalg.norm(r.x - z["x"]) / np.linalg.norm(z["x"])
+    assert rel <= 1e-6, rel
+    if kind == "jacobi" or fb == "cell":
+        # the GPU builds exactly these preconditioners
+        assert iters_close(r.report.iterations, ref_it), (r.report.iterations, ref_it)
+    else:
+        # reference-default MMG (exact smoothing per cc element): informational bound
+        assert r.report.iterations <= 2 * ref_it + 2
+
+
+# --------------------------------------------------------- set-up components
+
+def _rc_from_gpu(c, n, ncc, sd):
+    phi, ev, it = c.local_bases()
+    m_c, lc, cells = phi.shape
+    cpc = n // (ncc * sd)
+    nbx = n // cpc
+    rows, cols, vals = [], [], []
+    for I in range(m_c):
+        bi, bj, bk = I % nbx, (I // nbx) % nbx, I // (nbx * nbx)
+        loc = np.arange(cells)
+        gi = bi * cpc + loc % cpc
+        gj = bj * cpc + (loc // cpc) % cpc
+        gk = bk * cpc + loc // (cpc * cpc)
+        gid = gi + n * (gj + n * gk)
+        for a in range(lc):
+            rows.append(np.full(cells, I * lc + a))
+            cols.append(gid)
+            vals.append(phi[I, a])
+    Rc = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                       shape=(m_c * lc, n ** 3))
+    return Rc, ev, it
+
+
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (32, 2, 2, 1e-6)])
+def test_local_bases_vs_oracle(n, ncc, sd, kmin):
+    _, kappa = problem(n, kmin)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg")
+    phi, ev, it = c.local_bases()
+    assert (it >= 0).all(), "local eigensolver did not converge"
+    h = O.hierarchy(O.grid(n), ncc, sd)
+    vol = 1.0 / n ** 3
+    cpc = n // (ncc * sd)
+    nbx = n // cpc
+    for I in range(0, phi.shape[0], max(1, phi.shape[0] // 16)):
+        vals, vecs = O.local_basis(h, kappa, I, 8)
+        scale = max(abs(vals).max(), 1.0)
+        np.testing.assert_allclose(ev[I], vals[:4], atol=1e-7 * scale)
+        bi, bj, bk = I % nbx, (I // nbx) % nbx, I // (nbx * nbx)
+        loc = np.arange(cpc ** 3)
+        gid = (bi * cpc + loc % cpc) + n * ((bj * cpc + (loc // cpc) % cpc) + n * (bk * cpc + loc // cpc ** 2))
+        mass = kappa[gid] * vol
+        G = phi[I] @ (mass[:, None] * phi[I].T)  # M-orthonormal
+        np.testing.assert_allclose(G, np.eye(4), atol=1e-9)
+        if vals[4] - vals[3] > 1e-3 * scale:  # well separated cut: spans must agree
+            qa = np.linalg.qr((np.sqrt(mass)[:, None] * phi[I].T))[0]
+            qb = np.linalg.qr((np.sqrt(mass)[:, None] * vecs[:4].T))[0]
+            np.testing.assert_allclose(np.linalg.svd(qa.T @ qb)[1], 1.0, atol=1e-7)
+
+
+def test_coarse_operator_is_galerkin_product():
+    n, ncc, sd = 32, 2, 2
+    _, kappa = problem(n, 1e-6)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg")
+    A = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH).matrix
+    Rc, _, _ = _rc_from_gpu(c, n, ncc, sd)
+    Ac_ref = (Rc @ A @ Rc.T).toarray()
+    Ac = c.coarse_operator()
+    np.testing.assert_allclose(Ac, Ac_ref, atol=1e-11 * abs(Ac_ref).max())
+
+
+def _numpy_vcycle(A, Rc, Rcc, fine_blocks, coarse_blocks, r):
+    """MultiscaleHierarchy::apply (solver.cpp:272-334) with exact block solves."""
+    Ac = (Rc @ A @ Rc.T).toarray()
+    Acc = Rcc @ Ac @ Rcc.T
+    Ad = A.tocsr()
+
+    def smooth(M, blocks, v):
+        z = np.zeros_like(v)
+        for b in blocks:
+            sub = M[np.ix_(b, b)] if isinstance(M, np.ndarray) else Ad[b][:, b].toarray()
+            z[b] = sla.solve(sub, v[b], assume_a="pos")
+        return z
+
+    r1 = smooth(A, fine_blocks, r)
+    rc = Rc @ (r - Ad @ r1)
+    rc0 = smooth(Ac, coarse_blocks, rc)
+    rcc = Rcc @ (rc - Ac @ rc0)
+    ecc = sla.solve(Acc, rcc, assume_a="pos")
+    rc1 = rc0 + Rcc.T @ ecc
+    ec = rc1 + smooth(Ac, coarse_blocks, rc - Ac @ rc1)
+    r2 = r1 + Rc.T @ ec
+    return r2 + smooth(A, fine_blocks, r - Ad @ r2)
+
+
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (32, 2, 2, 1e-6)])
+def test_vcycle_matches_numpy_reference(n, ncc, sd, kmin):
+    _, kappa = problem(n, kmin)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg")
+    A = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH).matrix
+    Rc, _, _ = _rc_from_gpu(c, n, ncc, sd)
+    Rcc = c.cc_restriction()
+    h = O.hierarchy(O.grid(n), ncc, sd)
+    cpc = n // (ncc * sd)
+    nbx = n // cpc
+    lc = 4
+    fine = []
+    for I in range(nbx ** 3):
+        bi, bj, bk = I % nbx, (I // nbx) % nbx, I // (nbx * nbx)
+        loc = np.arange(cpc ** 3)
+        fine.append((bi * cpc + loc % cpc) + n * ((bj * cpc + (loc // cpc) % cpc)
+                                                  + n * (bk * cpc + loc // cpc ** 2)))
+    coarse = []
+    for e in range(ncc ** 3):
+        ei, ej, ek = e % ncc, (e // ncc) % ncc, e // (ncc * ncc)
+        rows = []
+        for dk in range(sd):
+            for dj in range(sd):
+                for di in range(sd):
+                    I = (ei * sd + di) + nbx * ((ej * sd + dj) + nbx * (ek * sd + dk))
+                    rows.extend(range(I * lc, I * lc + lc))
+        coarse.append(np.array(rows))
+    r = np.random.default_rng(11).standard_normal(n ** 3)
+    z_ref = _numpy_vcycle(A, Rc, Rcc, fine, coarse, r)
+    z = c.apply_preconditioner(r)
+    assert np.linalg.norm(z - z_ref) <= 1e-8 * np.linalg.norm(z_ref)
+
+
+def test_preconditioner_symmetric_positive_definite():
+    n = 32
+    _, kappa = problem(n, 1e-6)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("mmg")
+    rng = np.random.default_rng(4)
+    r1, r2 = rng.standard_normal((2, n ** 3))
+    a, b = c.apply_preconditioner(r1) @ r2, r1 @ c.apply_preconditioner(r2)
+    assert abs(a - b) <= 1e-9 * abs(a)
+    assert r1 @ c.apply_preconditioner(r1) > 0
+    # linearity
+    z = c.apply_preconditioner(2.0 * r1 - 3.0 * r2)
+    np.testing.assert_allclose(z, 2.0 * c.apply_preconditioner(r1) - 3.0 * c.apply_preconditioner(r2),
+                               atol=1e-10 * abs(z).max())
+
+
+# ------------------------------------------------------------------- edges
+
+def test_zero_rhs_returns_zero():
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("mmg")
+    r = c.pcg(np.zeros(n ** 3), x0=np.ones(n ** 3))  # solver.cpp:506-513
+    assert r.report.converged and r.report.iterations == 0
+    assert not r.x.any()
+
+
+def test_exact_initial_guess_zero_iterations():
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("mmg")
+    b = c.assemble_rhs(np.ones(n ** 3))
+    x = c.pcg(b, rtol=1e-12).x
+    r = c.pcg(b, rtol=1e-6, x0=x)  # solver.cpp:523-531
+    assert r.report.converged and r.report.iterations == 0
+    np.testing.assert_array_equal(r.x, x)
+
+
+@pytest.mark.parametrize("maxit", [0, 1, 3, 5])
+def test_max_iterations_not_converged(maxit):
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("mmg")
+    b = c.assemble_rhs(np.ones(n ** 3))
+    r = c.pcg(b, rtol=1e-14, max_iterations=maxit)  # solver.hpp:179-182
+    assert not r.report.converged and r.report.iterations == maxit
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    ref = O.pcg(s, s.rhs, O.Precond("mmg", s, O.hierarchy(O.grid(n), 2, 2), fine_blocks="cell",
+                                    coarse_blocks="cc"), rtol=1e-14, max_iterations=maxit)
+    if maxit:
+        np.testing.assert_allclose(r.report.residual_history, ref.residual_history, rtol=1e-6)
+        assert np.linalg.norm(r.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
+
+
+def test_warm_start_interpolated_coarse_solution():
+    # north_star item 7: x0 = piecewise-constant prolongation of the 16^3
+    # solution (interpolate_design, grid.cpp:220-241) for the 32^3 solve
+    lo, hi = 16, 32
+    _, k_lo = problem(lo, 1e-3)
+    rho_hi = np.zeros(hi ** 3)
+    O.lib().orc_interpolate_design(O._d(inputs.box_filter_design(lo, 0.3)), O.Grid(lo, lo, lo, 1, 1, 1),
+                                   O.Grid(hi, hi, hi, 1, 1, 1), O._d(rho_hi))
+    k_hi = inputs.conductivity(rho_hi, 1e-3)
+    c_lo = ctx_for(lo, 2, 2, k_lo)
+    c_lo.setup("mmg")
+    x_lo = c_lo.pcg(c_lo.assemble_rhs(np.ones(lo ** 3)), rtol=1e-10).x
+    x0 = np.empty(hi ** 3)
+    O.lib().orc_interpolate_design(O._d(x_lo), O.Grid(lo, lo, lo, 1, 1, 1), O.Grid(hi, hi, hi, 1, 1, 1),
+                                   O._d(x0))
+    c = ctx_for(hi, 2, 2, k_hi)
+    c.setup("mmg")
+    b = c.assemble_rhs(np.ones(hi ** 3))
+    cold = c.pcg(b, rtol=1e-8)
+    warm = c.pcg(b, rtol=1e-8, x0=x0)
+    assert warm.report.converged and warm.report.iterations < cold.report.iterations
+    s = O.System(O.grid(hi), k_hi, np.ones(hi ** 3), PATCH)
+    ref = O.pcg(s, s.rhs, O.Precond("mmg", s, O.hierarchy(O.grid(hi), 2, 2), fine_blocks="cell",
+                                    coarse_blocks="cc"), rtol=1e-8, x0=x0)
+    assert iters_close(warm.report.iterations, ref.iterations)
+    assert np.linalg.norm(warm.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
+def test_configuration_errors():
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    c = Context(GridSpec(n, n, n), 2, 2)
+    with pytest.raises(ConfigError, match="no Dirichlet"):
+        c.set_conductivity(kappa, BoundarySpec([]))
+    bad = kappa.copy()
+    bad[7] = 0.0
+    with pytest.raises(ConfigError, match="positive"):
+        c.set_conductivity(bad, BC)
+    with pytest.raises(ConfigError, match="overlapping"):
+        c.set_conductivity(kappa, BoundarySpec([DirichletPatch(4, 0, 0, 0.5, 0.5),
+                                                DirichletPatch(4, 0.4, 0.4, 0.6, 0.6)]))
+    with pytest.raises(ConfigError, match="outside"):
+        c.set_conductivity(kappa, BoundarySpec([DirichletPatch(4, 0, 0, 1.5, 0.5)]))
+    with pytest.raises(ConfigError, match="MaterialModel"):
+        c.set_design(np.zeros(n ** 3), 0.0, 1.0, 3, BC)
+    with pytest.raises(ValueError, match="no problem"):
+        c.setup("mmg")
+    c.set_conductivity(kappa, BC)
+    with pytest.raises(ValueError, match="more eigenvectors"):
+        c.setup("mmg", MmgOptions(num_cc_basis=33))
+    with pytest.raises(NotSupportedError):
+        c.setup("two_grid")
+    with pytest.raises(ValueError, match="no preconditioner"):
+        c.pcg(np.ones(n ** 3))
+    c.setup("jacobi")
+    with pytest.raises(ValueError, match="size mismatch"):
+        c.pcg(np.ones(10))
+
+
+def test_solves_are_deterministic():
+    n = 32
+    _, kappa = problem(n, 1e-6)
+    c = ctx_for(n, 2, 2, kappa)
+    c.setup("mmg")
+    b = c.assemble_rhs(np.ones(n ** 3))
+    a1, a2 = c.pcg(b, rtol=1e-8), c.pcg(b, rtol=1e-8)
+    np.testing.assert_array_equal(a1.x, a2.x)
+    np.testing.assert_array_equal(a1.report.residual_history, a2.report.residual_history)
+
+
+def test_reference_style_api():
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    ctx = make_preconditioner("mmg", GridSpec(n, n, n), kappa, BC, 2, 2)
+    b = ctx.assemble_rhs(np.ones(n ** 3))
+    r = pcg(ctx, b, rtol=1e-8)
+    assert r.report.converged and r.report.preconditioner == "mmg"
+    assert np.linalg.norm(b - ctx.apply_operator(r.x)) <= 1.01e-8 * np.linalg.norm(b)
+
+
+# ------------------------------------------------- full-size properties
+
+@pytest.mark.slow
+def test_config1_full_size_properties():
+    # BASELINE configs[1]: 128^3, kmin 1e-6, rtol 1e-8 — too large for the
+    # oracle; size-independent checks only.
+    cfg = inputs.CONFIGS[1]
+    n = cfg["n"]
+    _, kappa = problem(n, cfg["kmin"])
+    c = ctx_for(n, cfg["ncc"], cfg["sd"], kappa)
+    c.setup("mmg")
+    b = c.assemble_rhs(np.ones(n ** 3))
+    r = c.pcg(b, rtol=1e-8)
+    assert r.report.converged and 15 <= r.report.iterations <= 80
+    true_rel = np.linalg.norm(b - c.apply_operator(r.x)) / np.linalg.norm(b)
+    assert true_rel <= 1.05e-8
+    hist = r.report.residual_history
+    assert hist[-1] <= 1e-8 and (hist[-2] > 1e-8)
+    # recurrence residual tracks the true residual
+    assert abs(true_rel - hist[-1]) <= 0.05 * hist[-1]
+    rng = np.random.default_rng(9)
+    r1, r2 = rng.standard_normal((2, n ** 3))
+    a, bb = c.apply_preconditioner(r1) @ r2, r1 @ c.apply_preconditioner(r2)
+    assert abs(a - bb) <= 1e-9 * abs(a)
