@@ -359,3 +359,12 @@ def ref_solve(n, ncc, sd, kappa, rhs, patches, kind="mmg", fine_blocks=None,
                                _d(x), C.byref(it), C.byref(conv), _d(hist), C.byref(ts),
                                C.byref(tv)))
     return PcgResult(x, it.value, bool(conv.value), hist[:it.value].copy(), tv.value), ts.value
+
+
+def interpolate_design(values_lo, n_lo, n_hi):
+    """interpolate_design (grid.cpp:220-241): piecewise-constant prolongation."""
+    v = np.ascontiguousarray(values_lo, dtype=np.float64)
+    glo, ghi = grid(n_lo), grid(n_hi)
+    out = np.empty(ghi.nx * ghi.ny * ghi.nz)
+    _check(lib().orc_interpolate_design(_d(v), C.byref(glo), C.byref(ghi), _d(out)))
+    return out

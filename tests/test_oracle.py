@@ -243,3 +243,11 @@ def test_live_reference_warm_start_x0():
     o = O.pcg(s, s.rhs, O.Precond("jacobi", s), rtol=1e-8, x0=x0)
     assert r.iterations == o.iterations
     np.testing.assert_array_equal(r.x, o.x)
+
+
+def test_interpolate_design_mean_preserving():
+    # grid.cpp:220-241: piecewise-constant prolongation preserves the mean
+    lo = np.random.default_rng(2).random(8 ** 3)
+    hi = O.interpolate_design(lo, 8, 16)
+    assert hi.size == 16 ** 3 and abs(hi.mean() - lo.mean()) < 1e-15
+    assert hi[0] == lo[0] and hi[1] == lo[0] and hi[2] == lo[1]
