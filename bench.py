@@ -1,0 +1,353 @@
+"""Benchmark: FP64 PCG + multiscale-MG solve throughput on B200.
+
+Workload (BASELINE.json configs[1], the single-GPU configuration the metric is
+quoted on): 128^3 cells, seeded box-filter design (vf 0.3, 3 passes, radius 2),
+SIMP p = 3, kmin = 1e-6, unit source, T = 0 on the centred 0.2 x 0.2 patch of
+z = 0, PCG to ||r||/||b|| <= 1e-8 with the multiscale V-cycle (L_c = 4,
+L_cc = 8, c = 8, sd = 2, ncc = 8). One step = one full PCG solve from x0 = 0
+on the resident system. value = DoF * iterations / solve time (MDoF*iter/s),
+summed over ranks (N independent replicas: the brick-decomposed multi-GPU solve
+is not built yet).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the reference's own CPU implementation of the path
+(oracle/_ref: proj/core compiled unmodified) on the same
+config with all host threads; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCG solve MDoF*iter/s (FP64, rtol 1e-8, multiscale-MG V-cycle)"
+UNIT = "MDoF*iter/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+RTOL = 1e-8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iters", type=int, default=8,
+                    help="PCG iterations per reference step (bounded sample)")
+    return ap.parse_args()
+
+
+def workload(cfg_id):
+    from paper_2410_06850_b200 import inputs
+    cfg = dict(inputs.CONFIGS[cfg_id])
+    rho = inputs.box_filter_design(cfg["n"], cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
+    kappa = inputs.conductivity(rho, cfg["kmin"])
+    return cfg, kappa
+
+
+def config_json(cfg, cfg_id, extra=None):
+    n = cfg["n"]
+    d = {"workload": f"BASELINE configs[{cfg_id}]: {n}^3 cells, kmin={cfg['kmin']:g}, "
+                     f"MMG-PCG rtol={RTOL:g}",
+         "cells": n ** 3, "kmin": cfg["kmin"], "rtol": RTOL,
+         "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} "
+                      f"L_c=4 L_cc=8 nu=1",
+         "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
+         "l2": "no flush: one solve streams ~1.7 GB/iteration through the 126 MB L2"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks and throttle reasons
+    during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clocks_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- reference
+
+def reference_context(cfg, kappa):
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # bench's reference / cpu-baseline leg only
+    R = O.ref()
+    R.ref_set_num_threads(0)
+    pa = O._patch_array(O.bottom_center_patch())
+    ts = C.c_double()
+    ctx = R.ref_ctx_create(cfg["n"], cfg["ncc"], cfg["sd"], O._d(kappa), 1, O._d(pa), 4,
+                           O.BLOCKS["cell"], O.BLOCKS["cc"], 4, 8, 1, C.byref(ts))
+    if not ctx:
+        raise RuntimeError(R.ref_last_error().decode())
+    return O, R, ctx, ts.value, R.ref_num_threads()
+
+
+def reference_steps(O, R, ctx, n, steps, iters):
+    import ctypes as C
+    it, cv, sv = C.c_int(), C.c_int(), C.c_double()
+    tot_it, tot_s = 0, 0.0
+    for _ in range(steps):
+        rc = R.ref_ctx_pcg(ctx, C.c_double(RTOL), C.c_int(iters), None, C.byref(it), C.byref(cv),
+                           C.byref(sv))
+        if rc:
+            raise RuntimeError(R.ref_last_error().decode())
+        tot_it += it.value
+        tot_s += sv.value
+    return tot_it, tot_s
+
+
+def cpu_baseline(cfg, kappa, iters):
+    O, R, ctx, setup_s, threads = reference_context(cfg, kappa)
+    try:
+        its, secs = reference_steps(O, R, ctx, cfg["n"], 1, iters)
+    finally:
+        R.ref_ctx_destroy(ctx)
+    return {"value": cfg["n"] ** 3 * its / secs / 1e6, "unit": UNIT, "cores": threads,
+            "kind": "reference",
+            "sample": f"reference proj/core (oracle/_ref) on {cfg['n']}^3 configs[1]: "
+                      f"set-up ({setup_s:.1f} s, untimed) + one PCG of {its} iterations",
+            "setup_seconds": setup_s}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, kappa = workload(args.config)
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtopmg_ref.so")):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopmg_ref.so not built "
+                          "(run bash oracle/build_ref.sh where /root/reference exists)"}))
+        return 0
+    O, R, ctx, setup_s, threads = reference_context(cfg, kappa)
+    try:
+        reference_steps(O, R, ctx, cfg["n"], args.warmup, args.ref_iters)
+        t0 = time.perf_counter()
+        its, secs = reference_steps(O, R, ctx, cfg["n"], args.steps, args.ref_iters)
+        wall = time.perf_counter() - t0
+    finally:
+        R.ref_ctx_destroy(ctx)
+    value = cfg["n"] ** 3 * its / secs / 1e6
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[1])",
+            "config": config_json(cfg, args.config, {"reference_setup_seconds": setup_s,
+                                                     "iterations_per_step": its // args.steps}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{args.steps} steps x {args.ref_iters} PCG iterations "
+                                       f"of the reference on {cfg['n']}^3 (set-up untimed)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# -------------------------------------------------------------------- ours
+
+# Algorithmic bytes per fine cell of the two block-solve kernels (DESIGN.md
+# §Roofline): streams that must move between HBM and the SMs once per launch.
+#  k_post  : r1 8 + Phi 32 + r 8 + coef 32 + G 288 + z 8          = 376
+#  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8    = 352
+KERNEL_BYTES_PER_CELL = {"post": 376, "update": 352, "search": 64, "restrict": 88}
+ITER_BYTES_PER_CELL = 64 + 352 + 88 + 376  # + coarse levels (~0.1%)
+
+
+def ncu_traffic(kernel):
+    path = os.path.join(ROOT, "profiles", "ncu_summary_latest.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec
+    cfg, kappa = workload(args.config)
+    n = cfg["n"]
+    M = n ** 3
+    ctx = Context(GridSpec(n, n, n), cfg["ncc"], cfg["sd"], device=local)
+    ctx.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0))
+    b = ctx.assemble_rhs(np.ones(M))
+    t0 = time.perf_counter()
+    ctx.setup("mmg")
+    setup_wall = time.perf_counter() - t0
+    ctx.upload_rhs(b)
+    for _ in range(max(3, args.warmup)):
+        rep = ctx.solve_resident(RTOL, 10000)
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.kernel_launches()
+    torch.cuda.synchronize()
+    barrier()
+    its = []
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            rep = ctx.solve_resident(RTOL, 10000)
+            its.append(rep.iterations)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    iters = int(np.mean(its))
+    value = world * M * iters / (ms * 1e-3) / 1e6
+
+    # e2e through the C ABI with pinned host buffers (H2D b, solve, D2H x)
+    b_pin = torch.from_numpy(b).pin_memory().numpy()
+    x_pin = torch.empty(M, dtype=torch.float64).pin_memory().numpy()
+    ctx.pcg(b_pin, rtol=RTOL, out=x_pin)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_its = 0
+    for _ in range(args.steps):
+        e2e_its += ctx.pcg(b_pin, rtol=RTOL, out=x_pin).report.iterations
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * M * (e2e_its / args.steps) / e2e_s / 1e6
+    true_rel = float(np.linalg.norm(b - ctx.apply_operator(x_pin)) / np.linalg.norm(b))
+
+    # per-kernel CUDA-event times during one live solve (roofline)
+    prof = ctx.profile_solve(RTOL, 10000)
+    per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+    dominant = max(("post", "update", "search", "restrict"), key=lambda k: prof[k][0])
+    peak = None
+    peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    try:
+        with open(PEAKS) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+            peak_src = "measured MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak = 6650.0
+    bytes_launch = KERNEL_BYTES_PER_CELL[dominant] * M
+    achieved = bytes_launch / (per[dominant] * 1e-3) / 1e9
+    iter_achieved = ITER_BYTES_PER_CELL * M * iters / (ms * 1e-3) / 1e9
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded box-filter design, BASELINE configs[1])",
+        "config": config_json(cfg, args.config, {
+            "iterations": iters, "setup_ms": 1e3 * rep.setup_seconds,
+            "setup_wall_ms": 1e3 * setup_wall,
+            "time_to_solution_ms": 1e3 * rep.setup_seconds + ms,
+            "true_relative_residual": true_rel,
+            "parallelism": "replicas" if world > 1 else "single-gpu",
+            "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items() if v},
+            "iteration_hbm_gbs_algorithmic": iter_achieved,
+            "device_bytes": ctx.device_bytes()}),
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dominant),
+                     "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * M,
+                "d2h_bytes_per_step": 8 * M},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg, kappa, args.ref_iters)
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

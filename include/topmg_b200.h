@@ -151,6 +151,9 @@ int tmg_profile_solve(tmg_ctx* ctx, double rtol, int max_iterations, double* ms_
                       int* count);
 /* Bytes of device memory held by the context. */
 int64_t tmg_device_bytes(const tmg_ctx* ctx);
+/* Kernels enqueued by this context's solves so far (graph nodes included,
+ * kernels that exit early after convergence included). */
+int64_t tmg_kernel_launches(const tmg_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for external event timing. */
 void* tmg_stream(tmg_ctx* ctx);
 

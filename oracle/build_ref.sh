@@ -30,6 +30,8 @@ $CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$HERE/ref_harne
 pids+=($!)
 $CC -std=c11 $FLAGS -c "$HERE/dense_la.c" -o "$OUT/obj/dense_la.o" &
 pids+=($!)
+$CC -std=c11 $FLAGS -c "$HERE/lapack_glue.c" -o "$OUT/obj/lapack_glue.o" &
+pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
-$CXX -shared -pthread -o "$OUT/libtopmg_ref.so" "$OUT"/obj/*.o -lm
+$CXX -shared -pthread -o "$OUT/libtopmg_ref.so" "$OUT"/obj/*.o -lm -ldl
 echo "built $OUT/libtopmg_ref.so"

@@ -68,6 +68,8 @@ struct tmg_ctx {
   // graph
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
+  int64_t graph_kernels = 0;  // kernel nodes in one captured chunk
+  int64_t launches = 0;       // kernels enqueued by solves (incl. graph nodes)
   int64_t bytes = 0;
   std::vector<void*> allocs;
   double setup_seconds = 0.0;
@@ -236,6 +238,9 @@ void build_graph(tmg_ctx* c, int chunk) {
   // chunk is even so every graph launch starts from pbuf[0]
   for (int i = 0; i < chunk; ++i) enqueue_iteration(c, c->stream, i & 1);
   CK(cudaStreamEndCapture(c->stream, &graph));
+  size_t nodes = 0;
+  CK(cudaGraphGetNodes(graph, nullptr, &nodes));
+  c->graph_kernels = (int64_t)nodes;
   CK(cudaGraphInstantiate(&c->graph, graph, 0));
   cudaGraphDestroy(graph);
   c->graph_chunk = chunk;
@@ -292,6 +297,8 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     launch_init(c->g, c->cb, c->coef, c->b, c->x, use_x0, c->r, c->st, c->partials,
                 c->stream);
   });
+  c->launches += 1;                                          // init
+  c->launches += c->kind == TMG_PRECOND_MMG ? c->graph_kernels / c->graph_chunk - 1 : 1;
   if (c->kind == TMG_PRECOND_MMG) {
     if (!prof) {
       enqueue_vcycle(c, 1, c->st, c->stream, c->pbuf[0]);
@@ -321,6 +328,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       int launched = 0;
       auto launch_chunk = [&](int sl) {
         CK(cudaGraphLaunch(c->graph, c->stream));
+        c->launches += c->graph_kernels;
         CK(cudaMemcpyAsync(&hs[sl], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(ev[sl], c->stream));
         launched += c->graph_chunk;
@@ -842,6 +850,8 @@ int tmg_profile_solve(tmg_ctx* c, double rtol, int maxit, double* ms_total, int*
 }
 
 int64_t tmg_device_bytes(const tmg_ctx* c) { return c ? c->bytes : 0; }
+
+int64_t tmg_kernel_launches(const tmg_ctx* c) { return c ? c->launches : 0; }
 
 void* tmg_stream(tmg_ctx* c) { return c ? (void*)c->stream : nullptr; }
 

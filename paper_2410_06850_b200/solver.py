@@ -78,6 +78,7 @@ def native():
         L.tmg_last_error.restype = C.c_char_p
         L.tmg_last_error.argtypes = [C.c_void_p]
         L.tmg_device_bytes.restype = C.c_int64
+        L.tmg_kernel_launches.restype = C.c_int64
         L.tmg_stream.restype = C.c_void_p
         L.tmg_destroy.argtypes = [C.c_void_p]
         _lib = L
@@ -90,7 +91,7 @@ EXPORTED_SYMBOLS = (
     "tmg_apply_preconditioner", "tmg_upload_rhs", "tmg_upload_x0", "tmg_solve_resident",
     "tmg_download_solution", "tmg_get_local_bases", "tmg_get_coarse_operator",
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
-    "tmg_stream",
+    "tmg_stream", "tmg_kernel_launches",
 )
 
 
@@ -272,13 +273,13 @@ class Context:
         self._check(native().tmg_apply_preconditioner(self._p, _ptr(rr), _ptr(z)))
         return z
 
-    def pcg(self, b, rtol=1e-6, max_iterations=10000, x0=None) -> PcgResult:
+    def pcg(self, b, rtol=1e-6, max_iterations=10000, x0=None, out=None) -> PcgResult:
         bb = _f64(b)
         if bb.size != self.grid.num_cells():
             raise ValueError("pcg: rhs size mismatch")
         if x0 is not None and np.asarray(x0).size != self.grid.num_cells():
             raise ValueError("pcg: initial guess size mismatch")
-        x = np.empty_like(bb)
+        x = np.empty_like(bb) if out is None else out
         hist = np.zeros(max(1, max_iterations))
         rep = _Report()
         x0p = _ptr(_f64(x0)) if x0 is not None else None
@@ -345,6 +346,9 @@ class Context:
         names = ["search", "update", "restrict", "coarse", "unused4", "unused5", "post",
                  "jacobi_step", "init"]
         return {n: (ms[i], cnt[i]) for i, n in enumerate(names)}
+
+    def kernel_launches(self):
+        return native().tmg_kernel_launches(self._p)
 
     def device_bytes(self):
         return native().tmg_device_bytes(self._p)
