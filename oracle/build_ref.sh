@@ -35,3 +35,11 @@ pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
 $CXX -shared -pthread -o "$OUT/libtopmg_ref.so" "$OUT"/obj/*.o -lm -ldl
 echo "built $OUT/libtopmg_ref.so"
+# integration demo of include/topmg_b200.hpp inside the reference code base
+if [ -f "$HERE/../paper_2410_06850_b200/libtopmg_b200.so" ]; then
+  $CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/../include" "$HERE/adapter_demo.cpp" \
+    "$OUT"/obj/{grid,material,fvm,sparse,solver,coarse_space,parallel,rng,dense_la,lapack_glue}.o \
+    -L"$HERE/../paper_2410_06850_b200" -ltopmg_b200 -Wl,-rpath,'$ORIGIN/../../paper_2410_06850_b200' \
+    -ldl -o "$OUT/adapter_demo"
+  echo "built $OUT/adapter_demo"
+fi

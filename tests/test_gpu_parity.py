@@ -418,3 +418,15 @@ def test_config1_full_size_properties():
     r1, r2 = rng.standard_normal((2, n ** 3))
     a, bb = c.apply_preconditioner(r1) @ r2, r1 @ c.apply_preconditioner(r2)
     assert abs(a - bb) <= 1e-9 * abs(a)
+
+
+def test_cpp_dropin_adapter_inside_reference():
+    # include/topmg_b200.hpp compiled into the reference's own code base
+    # (oracle/adapter_demo.cpp, built by oracle/build_ref.sh)
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "adapter_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_demo not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ADAPTER OK" in out.stdout
