@@ -50,7 +50,9 @@ struct tmg_ctx {
   double* Rcc = nullptr;
   double* cc_evals = nullptr;
   double* Winv = nullptr;
-  double* Acc = nullptr;
+  double* Acc = nullptr;   // dense A_cc^-1 (set-up only)
+  double* AccT = nullptr;  // its lower 64x64 tiles (per-cycle GEMV)
+  double* symvP = nullptr; // GEMV partials
   int64_t n_cc = 0;
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
@@ -118,7 +120,7 @@ void dfree(tmg_ctx* c, void* p) {
 void free_setup(tmg_ctx* c) {
   for (void** pp : {(void**)&c->dinv, (void**)&c->phi, (void**)&c->evals, (void**)&c->eig_iters,
                     (void**)&c->Gf, (void**)&c->Ac, (void**)&c->Bc, (void**)&c->Rcc,
-                    (void**)&c->cc_evals, (void**)&c->Winv, (void**)&c->Acc, (void**)&c->rc,
+                    (void**)&c->cc_evals, (void**)&c->Winv, (void**)&c->Acc, (void**)&c->AccT, (void**)&c->symvP, (void**)&c->rc,
                     (void**)&c->rc0, (void**)&c->rcc, (void**)&c->ecc, (void**)&c->ec,
                     (void**)&c->rc1, (void**)&c->tc}) {
     dfree(c, *pp);
@@ -209,7 +211,7 @@ void enqueue_vcycle(tmg_ctx* c, int init, PcgState* st, cudaStream_t s, const do
   launch_update(g, c->cb, c->coef, c->Gf, c->x, p, c->q, c->r, c->r1, st, c->partials,
                 c->history, init, s);
   launch_restrict(g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, st, s);
-  launch_coarse_cycle(g, &st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0,
+  launch_coarse_cycle(g, &st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0,
                       c->rcc, c->ecc, c->rc1, c->tc, c->ec, s);
   launch_post(g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, st,
               c->partials, init, s);
@@ -305,7 +307,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     } else {
       timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, c->p, c->q, c->r, c->r1, c->st, c->partials, c->history, 1, c->stream); });
       timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-      timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
+      timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
       timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 1, c->stream); });
     }
   } else {
@@ -357,7 +359,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       if (c->kind == TMG_PRECOND_MMG) {
         timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, pnew, c->q, c->r, c->r1, c->st, c->partials, c->history, 0, c->stream); });
         timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-        timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->Acc, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
+        timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
         timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 0, c->stream); });
       } else {
         timed(7, [&] {
@@ -638,8 +640,14 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       double* work = dalloc<double>(c, dense_inverse_work_doubles(c->n_cc));
       dense_spd_inverse(c->Acc, c->n_cc, work, c->d_status + 2, c->stream);
       CK(cudaGetLastError());
+      c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
+      c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
+      pack_sym_tiles(c->Acc, c->n_cc, c->AccT, c->stream);
+      CK(cudaGetLastError());
       CK(cudaStreamSynchronize(c->stream));
       dfree(c, work);
+      dfree(c, c->Acc);
+      c->Acc = nullptr;
     }
     CK(cudaEventRecord(e1, c->stream));
     CK(cudaStreamSynchronize(c->stream));

@@ -524,16 +524,17 @@ void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rc
 //  rc0 = S_c(rc); rcc = R_cc (rc - A_c rc0); ecc = A_cc^-1 rcc;
 //  rc1 = rc0 + R_cc^T ecc; ec = rc1 + S_c(rc - A_c rc1).
 void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
-                         const double* Winv, const double* Rcc, const double* Acc_inv,
-                         int64_t n_cc, const double* rc, double* rc0, double* rcc, double* ecc,
-                         double* rc1, double* tc, double* ec, cudaStream_t s) {
+                         const double* Winv, const double* Rcc, const double* Acc_tiles,
+                         double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
+                         double* rcc, double* ecc, double* rc1, double* tc, double* ec,
+                         cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
   const int nt = (q + 31) / 32 * 32;
   const int nc = (int)(g.nb * LC);
   const size_t sm = sizeof(double) * (size_t)q;
   k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, rc, nullptr, rc0);
   k_coarse_restrict<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
-  launch_gemv(done, Acc_inv, n_cc, rcc, ecc, s);
+  launch_symv(done, Acc_tiles, n_cc, rcc, symv_partials, ecc, s);
   k_coarse_prolong<<<(unsigned)g.ncc, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
   k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, rc1, tc, nc);
   k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);

@@ -56,14 +56,20 @@ void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv,
 void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
                          cudaStream_t s);
 void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
-                         const double* Winv, const double* Rcc, const double* Acc_inv,
-                         int64_t n_cc, const double* rc, double* rc0, double* rcc, double* ecc,
-                         double* rc1, double* tc, double* ec, cudaStream_t s);
+                         const double* Winv, const double* Rcc, const double* Acc_tiles,
+                         double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
+                         double* rcc, double* ecc, double* rc1, double* tc, double* ec,
+                         cudaStream_t s);
 
 // dense.cu
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
 int64_t dense_inverse_work_doubles(int64_t n);
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
+                 cudaStream_t s);
+int64_t sym_tiles_doubles(int64_t n);
+int64_t sym_partials_doubles(int64_t n);
+void pack_sym_tiles(const double* A, int64_t n, double* T, cudaStream_t s);
+void launch_symv(const int* done, const double* T, int64_t n, const double* x, double* P, double* y,
                  cudaStream_t s);
 
 // pcg.cu

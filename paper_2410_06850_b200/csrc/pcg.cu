@@ -110,23 +110,29 @@ __global__ void __launch_bounds__(CB * CB * CB, 3) k_search(GridParams g, const 
   __shared__ double zt[Tile<CB>::N];
   __shared__ double red[80];
   __shared__ int flag;
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   const bool first = st->first;
   const double beta = st->beta;
-  load_coefs<CB>(coef, M, cs, g, bc);
-  load_tile<CB, true>(z, zt, g, bc);
-  if (!first) load_tile<CB, true>(p_old, pt, g, bc);
-  __syncthreads();
-  // p = z + beta p over the whole tile (solver.cpp:565-567)
-  for (int e = t; e < Tile<CB>::N; e += C) pt[e] = first ? zt[e] : zt[e] + beta * pt[e];
-  __syncthreads();
-  const size_t s = bofs(bc.b, C) + t;
-  const double pv = pt[Tile<CB>::idx(li, lj, lk)];
-  const double qv = apply_coef<CB>(cs, pt, li, lj, lk);  // solver.cpp:540
-  p[s] = pv;
-  q[s] = qv;
-  double v[1] = {pv * qv};
+  double pq = 0.0;
+  // persistent: the grid covers the SMs, each CTA walks bricks b, b + grid, ...
+  for (int b = blockIdx.x; b < g.nb; b += gridDim.x) {
+    const BrickCoord bc = brick_coord(g, b);
+    load_coefs<CB>(coef, M, cs, g, bc);
+    load_tile<CB, true>(z, zt, g, bc);
+    if (!first) load_tile<CB, true>(p_old, pt, g, bc);
+    __syncthreads();
+    // p = z + beta p over the whole tile (solver.cpp:565-567)
+    for (int e = t; e < Tile<CB>::N; e += C) pt[e] = first ? zt[e] : zt[e] + beta * pt[e];
+    __syncthreads();
+    const size_t s = bofs(bc.b, C) + t;
+    const double pv = pt[Tile<CB>::idx(li, lj, lk)];
+    const double qv = apply_coef<CB>(cs, pt, li, lj, lk);  // solver.cpp:540
+    p[s] = pv;
+    q[s] = qv;
+    pq += pv * qv;
+    __syncthreads();
+  }
+  double v[1] = {pq};
   block_sum_k<C, 1>(v, red);
   double tot[1];
   if (grid_reduce_last_k<1>(v, partials, &st->ticket[1], tot, &flag, red) && t == 0) {
@@ -391,6 +397,22 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
 
 // ---------------------------------------------------------------- launchers
 
+// Grid for a persistent kernel: every resident CTA slot of every SM, capped
+// at the number of bricks.
+template <typename K>
+static unsigned persist_grid(K kernel, int threads, size_t smem, int64_t nb) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  const int64_t n = (int64_t)sms * (per > 0 ? per : 1);
+  return (unsigned)(n < nb ? n : nb);
+}
+
 size_t update_smem(int cb) { return cb == 8 ? sizeof(UpdateSmem<8>) : sizeof(UpdateSmem<4>); }
 size_t post_smem(int cb) { return cb == 8 ? sizeof(PostSmem<8>) : sizeof(PostSmem<4>); }
 
@@ -422,8 +444,8 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s) {
   const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_search<8><<<(unsigned)g.nb, 512, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
-  else k_search<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  if (cb == 8) k_search<8><<<persist_grid(k_search<8>, 512, 0, g.nb), 512, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  else k_search<4><<<persist_grid(k_search<4>, 64, 0, g.nb), 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,

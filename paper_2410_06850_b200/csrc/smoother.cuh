@@ -66,11 +66,11 @@ using PlaneSlots = double[kSlots][Thomas<CB>::PLANE];
 // caller-owned) so kernels can alias them with data dead before the solve.
 template <int CB>
 struct ThomasSmem {
-  double (*slots)[Thomas<CB>::PLANE];
+  alignas(16) double w2[2][CB * CB];  // read as double2 broadcasts
   double part[CB * CB][Thomas<CB>::NBK + 1];
   double u[CB * CB * CB];
-  double w2[2][CB * CB];
   uint64_t bars[kSlots];
+  double (*slots)[Thomas<CB>::PLANE];
 };
 
 // 8-lane reduce-scatter: lane r (of an aligned group of 8) returns sum over the
@@ -134,8 +134,9 @@ __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp
   double a0 = 0.0, a1 = 0.0;  // two chains halve the dependent-FMA latency
 #pragma unroll
   for (int c = 0; c < 8; c += 2) {
-    a0 = fma(gv[c], w[8 * m.J + c], a0);
-    a1 = fma(gv[c + 1], w[8 * m.J + c + 1], a1);
+    const double2 wv = *reinterpret_cast<const double2*>(w + 8 * m.J + c);  // broadcast
+    a0 = fma(gv[c], wv.x, a0);
+    a1 = fma(gv[c + 1], wv.y, a1);
   }
   if (m.active) sm.part[8 * m.I + m.r][m.J] = a0 + a1;
   const double wr = w[8 * m.I + m.r];
