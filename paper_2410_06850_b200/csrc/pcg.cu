@@ -96,54 +96,52 @@ __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const doubl
 }
 
 // --------------------------------------------------------------- K1 search
+constexpr int kStencilThreads = 256;  // CTA size of the stencil kernels (2 cells/thread at CB = 8)
+
 template <int CB>
-__global__ void __launch_bounds__(CB * CB * CB, 3) k_search(GridParams g, const double* __restrict__ coef,
-                                                           int64_t M, const double* __restrict__ z,
-                                                           const double* __restrict__ p_old, double* p,
-                                                           double* q, PcgState* st, double* partials) {
+__global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, const double* __restrict__ coef,
+                                                              int64_t M, const double* __restrict__ z,
+                                                              const double* __restrict__ p_old, double* p,
+                                                              double* q, PcgState* st, double* partials) {
   // p_old and p are distinct buffers: neighbouring CTAs read p_old's halo while
   // this CTA writes the new search direction.
   if (st->done) return;
-  constexpr int C = CB * CB * CB;
+  constexpr int C = CB * CB * CB, NT = kStencilThreads < C ? kStencilThreads : C;
+  constexpr int KPT = C / NT;
   __shared__ CoefSmem<CB> cs;
   __shared__ double pt[Tile<CB>::N];
-  __shared__ double zt[Tile<CB>::N];
   __shared__ double red[80];
   __shared__ int flag;
-  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  const int t = threadIdx.x;
   const bool first = st->first;
   const double beta = st->beta;
+  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  load_coefs<CB>(coef, M, cs, g, bc);
+  load_tile_axpy<CB>(z, p_old, beta, first, pt, g, bc);  // p = z + beta p (solver.cpp:565-567)
+  __syncthreads();
   double pq = 0.0;
-  // persistent: the grid covers the SMs, each CTA walks bricks b, b + grid, ...
-  for (int b = blockIdx.x; b < g.nb; b += gridDim.x) {
-    const BrickCoord bc = brick_coord(g, b);
-    load_coefs<CB>(coef, M, cs, g, bc);
-    load_tile<CB, true>(z, zt, g, bc);
-    if (!first) load_tile<CB, true>(p_old, pt, g, bc);
-    __syncthreads();
-    // p = z + beta p over the whole tile (solver.cpp:565-567)
-    for (int e = t; e < Tile<CB>::N; e += C) pt[e] = first ? zt[e] : zt[e] + beta * pt[e];
-    __syncthreads();
-    const size_t s = bofs(bc.b, C) + t;
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int c = t + k * NT, li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+    const size_t s = bofs(bc.b, C) + c;
     const double pv = pt[Tile<CB>::idx(li, lj, lk)];
     const double qv = apply_coef<CB>(cs, pt, li, lj, lk);  // solver.cpp:540
     p[s] = pv;
     q[s] = qv;
     pq += pv * qv;
-    __syncthreads();
   }
   double v[1] = {pq};
-  block_sum_k<C, 1>(v, red);
+  block_sum_k<NT, 1>(v, red);
   double tot[1];
   if (grid_reduce_last_k<1>(v, partials, &st->ticket[1], tot, &flag, red) && t == 0) {
-    const double pq = tot[0];
-    st->pq = pq;
+    const double pqt = tot[0];
+    st->pq = pqt;
     st->first = 0;
-    if (!(pq > 0.0)) {  // solver.cpp:541-548
+    if (!(pqt > 0.0)) {  // solver.cpp:541-548
       st->status = kStatusIndefinite;
       st->done = 1;
     } else {
-      st->alpha = st->rho / pq;  // :549
+      st->alpha = st->rho / pqt;  // :549
     }
   }
 }
@@ -224,31 +222,39 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, cons
 
 // ------------------------------------------------------------ K3 restrict
 template <int CB>
-__global__ void __launch_bounds__(CB * CB * CB, 3) k_restrict(GridParams g, const double* __restrict__ coef,
-                                                             int64_t M, const double* __restrict__ phi,
-                                                             const double* __restrict__ r,
-                                                             const double* __restrict__ r1, double* rc,
-                                                             const PcgState* st) {
+__global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, const double* __restrict__ coef,
+                                                                int64_t M, const double* __restrict__ phi,
+                                                                const double* __restrict__ r,
+                                                                const double* __restrict__ r1, double* rc,
+                                                                const PcgState* st) {
   if (st->done) return;
-  constexpr int C = CB * CB * CB;
+  constexpr int C = CB * CB * CB, NT = kStencilThreads < C ? kStencilThreads : C;
+  constexpr int KPT = C / NT;
   __shared__ CoefSmem<CB> cs;
   __shared__ double xt[Tile<CB>::N];
-  __shared__ double red[LCP * (C / 32) + LCP + 8];
+  __shared__ double red[LCP * (NT / 32) + LCP + 8];
   const BrickCoord bc = brick_coord(g, blockIdx.x);
-  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  const int t = threadIdx.x;
   load_coefs<CB>(coef, M, cs, g, bc);
   load_tile<CB, true>(r1, xt, g, bc);
-  const size_t s = bofs(bc.b, C) + t;
-  const double rv = r[s];
-  double ph[LCP];
+  double rv[KPT], ph[KPT][LCP];
 #pragma unroll
-  for (int a = 0; a < LCP; ++a) ph[a] = phi[((size_t)bc.b * LCP + a) * C + t];
+  for (int k = 0; k < KPT; ++k) {
+    const int c = t + k * NT;
+    rv[k] = r[bofs(bc.b, C) + c];
+#pragma unroll
+    for (int a = 0; a < LCP; ++a) ph[k][a] = phi[((size_t)bc.b * LCP + a) * C + c];
+  }
   __syncthreads();
-  const double wv = rv - apply_coef<CB>(cs, xt, li, lj, lk);  // solver.cpp:285-288
-  double v[LCP];
+  double v[LCP] = {};
 #pragma unroll
-  for (int a = 0; a < LCP; ++a) v[a] = ph[a] * wv;  // :289
-  block_sum_k<C, LCP>(v, red);
+  for (int k = 0; k < KPT; ++k) {
+    const int c = t + k * NT, li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+    const double wv = rv[k] - apply_coef<CB>(cs, xt, li, lj, lk);  // solver.cpp:285-288
+#pragma unroll
+    for (int a = 0; a < LCP; ++a) v[a] = fma(ph[k][a], wv, v[a]);  // :289
+  }
+  block_sum_k<NT, LCP>(v, red);
   if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
 }
 
@@ -270,7 +276,7 @@ struct PostSmem {
 };
 
 template <int CB>
-__global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_post(GridParams g, const double* __restrict__ coef,
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const double* __restrict__ coef,
                                                            int64_t M, const double* __restrict__ phi,
                                                            const double* __restrict__ Gf,
                                                            const double* __restrict__ r,
@@ -444,8 +450,8 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s) {
   const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_search<8><<<persist_grid(k_search<8>, 512, 0, g.nb), 512, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
-  else k_search<4><<<persist_grid(k_search<4>, 64, 0, g.nb), 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  if (cb == 8) k_search<8><<<(unsigned)g.nb, kStencilThreads, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  else k_search<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,
@@ -458,7 +464,7 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
   const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_restrict<8><<<(unsigned)g.nb, 512, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
+  if (cb == 8) k_restrict<8><<<(unsigned)g.nb, kStencilThreads, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
   else k_restrict<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,

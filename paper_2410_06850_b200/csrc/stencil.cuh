@@ -96,6 +96,33 @@ __device__ __forceinline__ void load_tile(const double* __restrict__ v, double* 
   }
 }
 
+// tile = z + beta * p_old (or z when `first`) over the brick and its face
+// halo, loaded straight from the two vectors (solver.cpp:565-567).
+template <int CB>
+__device__ __forceinline__ void load_tile_axpy(const double* __restrict__ z,
+                                               const double* __restrict__ p_old, double beta,
+                                               bool first, double* tile, const GridParams& g,
+                                               const BrickCoord& bc) {
+  constexpr int C = CB * CB * CB;
+  for (int t = threadIdx.x; t < C; t += blockDim.x) {
+    const size_t s = bofs(bc.b, C) + t;
+    const double zv = __ldg(z + s);
+    tile[Tile<CB>::idx(t % CB, (t / CB) % CB, t / (CB * CB))] = first ? zv : zv + beta * __ldg(p_old + s);
+  }
+  for (int h = threadIdx.x; h < 6 * CB * CB; h += blockDim.x) {
+    int f, ti, nl;
+    halo_slot<CB>(h, f, ti, nl);
+    const int nb = nbr_brick(g, bc, f);
+    double v = 0.0;
+    if (nb >= 0) {
+      const size_t s = bofs(nb, C) + nl;
+      const double zv = __ldg(z + s);
+      v = first ? zv : zv + beta * __ldg(p_old + s);
+    }
+    tile[ti] = v;
+  }
+}
+
 // All face transmissibilities of the tile (faces touching at least one
 // interior cell); 0 where a face cell lies outside the domain.
 template <int CB>
