@@ -206,7 +206,7 @@ __device__ void warp_jacobi(double* M, double* V, int q) {
       off += __shfl_xor_sync(0xffffffffu, off, o);
       tot += __shfl_xor_sync(0xffffffffu, tot, o);
     }
-    if (off <= 1e-30 * tot || off == 0.0) break;
+    if (off <= 1e-26 * tot || off == 0.0) break;
     for (int p = 0; p < q - 1; ++p)
       for (int qq = p + 1; qq < q; ++qq) {
         const double apq = M[p * q + qq];

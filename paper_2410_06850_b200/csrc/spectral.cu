@@ -67,6 +67,58 @@ __device__ void jacobi_eig_small(double* a, double* v) {
   }
 }
 
+// Warp-parallel cyclic Jacobi on a K x K symmetric matrix in shared memory
+// (lane r < K owns row/column r); eigenvectors accumulate in V (columns).
+// Called by one full warp.
+template <int K>
+__device__ void warp_jacobi_small(double* a, double* v) {
+  const int lane = threadIdx.x & 31;
+  if (lane < K)
+    for (int c = 0; c < K; ++c) v[lane * K + c] = lane == c ? 1.0 : 0.0;
+  __syncwarp();
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    if (lane < K)
+      for (int c = 0; c < K; ++c) {
+        const double x = a[lane * K + c] * a[lane * K + c];
+        tot += x;
+        if (c != lane) off += x;
+      }
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    // off-diagonal mass below ~1e-13 of the total: the Ritz values and
+    // vectors are converged far beyond what the subspace iteration needs
+    if (off <= 1e-26 * tot || off == 0.0) break;
+    for (int p = 0; p < K - 1; ++p)
+      for (int q = p + 1; q < K; ++q) {
+        const double apq = a[p * K + q];
+        const double app = a[p * K + p], aqq = a[q * K + q];
+        if (fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq)) || apq == 0.0) continue;
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), sn = tt * c;
+        __syncwarp();
+        if (lane < K) {  // columns p, q of row `lane`; eigenvector columns
+          const double akp = a[lane * K + p], akq = a[lane * K + q];
+          a[lane * K + p] = c * akp - sn * akq;
+          a[lane * K + q] = sn * akp + c * akq;
+          const double vkp = v[lane * K + p], vkq = v[lane * K + q];
+          v[lane * K + p] = c * vkp - sn * vkq;
+          v[lane * K + q] = sn * vkp + c * vkq;
+        }
+        __syncwarp();
+        if (lane < K) {  // rows p, q at column `lane`
+          const double apk = a[p * K + lane], aqk = a[q * K + lane];
+          a[p * K + lane] = c * apk - sn * aqk;
+          a[q * K + lane] = sn * apk + c * aqk;
+        }
+        __syncwarp();
+      }
+  }
+}
+
 template <int CB, int K>
 struct ChfsiCtx {
   static constexpr int C = CB * CB * CB;
@@ -93,94 +145,77 @@ __device__ __forceinline__ void bmatvec(const double (&x)[K], double (&y)[K], do
   __syncthreads();
 }
 
-// Gram matrix G = X^T Y (K x K, symmetric assumed if SYM) -> smem g[K*K]
-template <int CB, int K>
-__device__ __forceinline__ void gram(const double (&x)[K], const double (&y)[K], double* red,
-                                     double* g) {
-  constexpr int NP = K * (K + 1) / 2;
-  double v[NP];
-  int e = 0;
-#pragma unroll
-  for (int i = 0; i < K; ++i)
-#pragma unroll
-    for (int j = 0; j <= i; ++j) v[e++] = x[i] * y[j] + (i == j ? 0.0 : 0.0);
-  block_sum_k<CB * CB * CB, NP>(v, red);
-  if (threadIdx.x == 0) {
-    int q = 0;
-    for (int i = 0; i < K; ++i)
-      for (int j = 0; j <= i; ++j) {
-        g[i * K + j] = v[q];
-        g[j * K + i] = v[q];
-        ++q;
-      }
-  }
-  __syncthreads();
-}
-
-// Symmetrised Gram for Rayleigh-Ritz: H_ij = (x_i . y_j + x_j . y_i) / 2
+// Gram matrix G_ij = (x_i . y_j + x_j . y_i) / 2 (K x K, symmetric) -> smem g,
+// reduced in chunks of K+1 sums to bound register pressure.
 template <int CB, int K>
 __device__ __forceinline__ void gram_sym(const double (&x)[K], const double (&y)[K], double* red,
                                          double* g) {
   constexpr int NP = K * (K + 1) / 2;
-  double v[NP];
-  int e = 0;
+  constexpr int CH = K + 1;
+  static_assert(NP % CH == 0, "chunking");
 #pragma unroll
-  for (int i = 0; i < K; ++i)
+  for (int c0 = 0; c0 < NP; c0 += CH) {
+    double v[CH];
 #pragma unroll
-    for (int j = 0; j <= i; ++j) v[e++] = 0.5 * (x[i] * y[j] + x[j] * y[i]);
-  block_sum_k<CB * CB * CB, NP>(v, red);
-  if (threadIdx.x == 0) {
-    int q = 0;
-    for (int i = 0; i < K; ++i)
-      for (int j = 0; j <= i; ++j) {
-        g[i * K + j] = v[q];
-        g[j * K + i] = v[q];
-        ++q;
-      }
+    for (int e = 0; e < CH; ++e) {
+      // unrank e + c0 -> (i, j), j <= i
+      int idx = c0 + e, i = 0;
+      while ((i + 1) * (i + 2) / 2 <= idx) ++i;
+      const int j = idx - i * (i + 1) / 2;
+      v[e] = 0.5 * (x[i] * y[j] + x[j] * y[i]);
+    }
+    block_sum_k<CB * CB * CB, CH>(v, red);
+    if (threadIdx.x < CH) {
+      int idx = c0 + threadIdx.x, i = 0;
+      while ((i + 1) * (i + 2) / 2 <= idx) ++i;
+      const int j = idx - i * (i + 1) / 2;
+      g[i * K + j] = v[threadIdx.x];
+      g[j * K + i] = v[threadIdx.x];
+    }
   }
   __syncthreads();
 }
 
-// X <- X R^{-1} where G = R^T R (Cholesky of the Gram matrix in smem).
+template <int CB, int K>
+__device__ __forceinline__ void gram(const double (&x)[K], double* red, double* g) {
+  gram_sym<CB, K>(x, x, red, g);
+}
+
+// X <- X R^{-1} where G = R^T R (Cholesky of the Gram matrix, kept in smem).
 // Returns false if G is not numerically positive definite.
 template <int K>
 __device__ __forceinline__ bool cholqr_apply(double (&x)[K], const double* g, double* rsm,
                                              int* okflag) {
   if (threadIdx.x == 0) {
-    // R upper: G = R^T R
-    double R[K * K];
     bool ok = true;
     double gmax = 0.0;
     for (int i = 0; i < K; ++i) gmax = fmax(gmax, g[i * K + i]);
+    for (int i = 0; i < K * K; ++i) rsm[i] = 0.0;
     for (int i = 0; i < K && ok; ++i) {
       for (int j = i; j < K; ++j) {
         double s = g[i * K + j];
-        for (int k = 0; k < i; ++k) s -= R[k * K + i] * R[k * K + j];
+        for (int k = 0; k < i; ++k) s -= rsm[k * K + i] * rsm[k * K + j];
         if (j == i) {
           if (!(s > 1e-28 * gmax)) { ok = false; break; }
-          R[i * K + i] = sqrt(s);
+          rsm[i * K + i] = sqrt(s);
         } else {
-          R[i * K + j] = s / R[i * K + i];
+          rsm[i * K + j] = s / rsm[i * K + i];
         }
       }
     }
-    for (int i = 0; i < K * K; ++i) rsm[i] = ok ? R[i] : 0.0;
     *okflag = ok;
   }
   __syncthreads();
   const bool ok = *okflag;
   if (ok) {
-    // row vector x (1 x K) times R^{-1}: solve y R = x, forward over columns
-    double y[K];
+    // row vector x (1 x K) times R^{-1}: solve y R = x, in place
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       double s = x[j];
 #pragma unroll
-      for (int k = 0; k < j; ++k) s -= y[k] * rsm[k * K + j];
-      y[j] = s / rsm[j * K + j];
+      for (int k = 0; k < j; ++k) s -= x[k] * rsm[k * K + j];
+      x[j] = s / rsm[j * K + j];
     }
-#pragma unroll
-    for (int j = 0; j < K; ++j) x[j] = y[j];
   }
   __syncthreads();
   return ok;
@@ -256,7 +291,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   for (outer = 0; outer <= max_outer; ++outer) {
     // --- orthonormalise (CholQR twice) ---
     for (int pass = 0; pass < 2; ++pass) {
-      gram<CB, K>(x, x, red, gs);
+      gram<CB, K>(x, red, gs);
       if (!cholqr_apply<K>(x, gs, rsm, &okflag)) {
         // rank loss: re-seed the trailing vectors and retry next pass
 #pragma unroll
@@ -266,21 +301,20 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
     // --- Rayleigh-Ritz ---
     bmatvec<CB, K>(x, y, u, tf, sl, sll, nb);
     gram_sym<CB, K>(x, y, red, gs);
-    if (t == 0) {
-      double a[K * K], v[K * K];
-      for (int i = 0; i < K * K; ++i) a[i] = gs[i];
-      jacobi_eig_small<K>(a, v);
-      // sort ascending
-      int ord[K];
-      for (int i = 0; i < K; ++i) ord[i] = i;
-      for (int i = 0; i < K; ++i)
-        for (int j = i + 1; j < K; ++j)
-          if (a[ord[j] * K + ord[j]] < a[ord[i] * K + ord[i]]) {
-            const int tmp = ord[i]; ord[i] = ord[j]; ord[j] = tmp;
-          }
-      for (int c = 0; c < K; ++c) {
-        scal[c] = a[ord[c] * K + ord[c]];
-        for (int r = 0; r < K; ++r) qv[r * K + c] = v[r * K + ord[c]];
+    if (t < 32) {
+      warp_jacobi_small<K>(gs, rsm);  // gs -> eigenvalues on its diagonal, rsm = vectors
+      if (t == 0) {
+        int ord[K];  // ascending
+        for (int i = 0; i < K; ++i) ord[i] = i;
+        for (int i = 0; i < K; ++i)
+          for (int j = i + 1; j < K; ++j)
+            if (gs[ord[j] * K + ord[j]] < gs[ord[i] * K + ord[i]]) {
+              const int tmp = ord[i]; ord[i] = ord[j]; ord[j] = tmp;
+            }
+        for (int c = 0; c < K; ++c) {
+          scal[c] = gs[ord[c] * K + ord[c]];
+          for (int r = 0; r < K; ++r) qv[r * K + c] = rsm[r * K + ord[c]];
+        }
       }
     }
     __syncthreads();
