@@ -621,30 +621,56 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       c->tc = dalloc<double>(c, g.nb * g.lc);
       c->rcc = dalloc<double>(c, c->n_cc);
       c->ecc = dalloc<double>(c, c->n_cc);
+      // TMG_SETUP_PROFILE=1: per-phase device times on stderr (diagnostics only)
+      const bool sprof = getenv("TMG_SETUP_PROFILE") != nullptr;
+      cudaEvent_t ph[10];
+      int nph = 0;
+      const char* phname[10];
+      auto mark = [&](const char* name) {
+        if (!sprof) return;
+        CK(cudaEventCreate(&ph[nph]));
+        CK(cudaEventRecord(ph[nph], c->stream));
+        phname[nph++] = name;
+      };
+      mark("alloc");
       const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
       const int degree = o->eig_degree > 0 ? o->eig_degree : 16;
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
       launch_local_basis(g, c->cb, c->kappa, c->phi, c->evals, c->eig_iters, tol, degree, max_outer,
                          c->stream);
       CK(cudaGetLastError());
+      mark("local_basis");
       launch_coarse_blocks(g, c->cb, c->kappa, c->dmask, c->phi, c->Ac, c->Bc, c->stream);
       CK(cudaGetLastError());
+      mark("coarse_blocks");
       launch_cc_basis(g, c->Ac, c->Bc, c->Rcc, c->cc_evals, c->stream);
       CK(cudaGetLastError());
+      mark("cc_basis");
       launch_coarse_smoother(g, c->Ac, c->Winv, c->d_status + 1, c->stream);
       CK(cudaGetLastError());
+      mark("coarse_smoother");
       launch_thomas_factor(g, c->cb, c->kappa, c->dmask, c->Gf, c->d_status, c->stream);
       CK(cudaGetLastError());
+      mark("thomas_factor");
       launch_acc_assemble(g, c->Ac, c->Rcc, c->Acc, c->stream);
       CK(cudaGetLastError());
+      mark("acc_assemble");
       double* work = dalloc<double>(c, dense_inverse_work_doubles(c->n_cc));
       dense_spd_inverse(c->Acc, c->n_cc, work, c->d_status + 2, c->stream);
       CK(cudaGetLastError());
+      mark("acc_inverse");
       c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
       c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
       pack_sym_tiles(c->Acc, c->n_cc, c->AccT, c->stream);
       CK(cudaGetLastError());
+      mark("pack_tiles");
       CK(cudaStreamSynchronize(c->stream));
+      for (int i = 1; i < nph; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ph[i - 1], ph[i]));
+        fprintf(stderr, "[setup] %-16s %9.3f ms\n", phname[i], t);
+      }
+      for (int i = 0; i < nph; ++i) cudaEventDestroy(ph[i]);
       dfree(c, work);
       dfree(c, c->Acc);
       c->Acc = nullptr;

@@ -92,9 +92,8 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
     // lower block-triangle of 8 x 8 blocks, block (I, J <= I) at I(I+1)/2 + J
     for (int e = t; e < Thomas<CB>::PLANE; e += C) {
       const int blk = e / 64, rr = (e % 64) / 8, cc = e % 8;
-      int I = 0;
-      while ((I + 1) * (I + 2) / 2 <= blk) ++I;
-      const int J = blk - I * (I + 1) / 2;
+      int I, J;
+      block_of<CB>(blk, I, J);
       Gout[(size_t)k * Thomas<CB>::PLANE + blk * 64 + swz(rr, cc)] = Gprev[(8 * I + rr) * P + 8 * J + cc];
     }
     __syncthreads();

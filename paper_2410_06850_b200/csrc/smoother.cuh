@@ -47,6 +47,25 @@ struct Thomas {
   }
 };
 
+// Storage / thread order of the 36 stored 8x8 blocks (I, J <= I) of a CB = 8
+// plane, encoded 8*I + J. Chosen (offline search) so that the 4 blocks of each
+// warp touch w and part[][] with the fewest shared-memory wavefronts: at most
+// two distinct J (and I) per 64-byte bank half, I+J parities balanced 2/2.
+static __constant__ unsigned char kBlockOrder8[36] = {44, 33, 41, 36, 60, 51, 59, 52, 17, 18, 25, 9, 26, 50, 63, 58, 24, 27, 16, 0, 57, 62, 54, 49, 45, 8, 32, 40, 61, 56, 53, 48, 34, 43, 42, 35};
+
+template <int CB>
+__device__ __forceinline__ void block_of(int blk, int& I, int& J) {
+  if constexpr (CB == 8) {
+    const int v = kBlockOrder8[blk];
+    I = v >> 3;
+    J = v & 7;
+  } else {  // row-major lower block triangle
+    I = 0;
+    while ((I + 1) * (I + 2) / 2 <= blk) ++I;
+    J = blk - I * (I + 1) / 2;
+  }
+}
+
 // Swizzle inside an 8 x 8 block row: 16-byte chunk q (columns 2q, 2q+1) of
 // row r is stored at chunk position (q + r/2) mod 4, so the 8 rows of a block
 // read by one quarter-warp hit 8 distinct 16-byte bank groups.
@@ -67,11 +86,30 @@ using PlaneSlots = double[kSlots][Thomas<CB>::PLANE];
 template <int CB>
 struct ThomasSmem {
   alignas(16) double w2[2][CB * CB];  // read as double2 broadcasts
-  double part[CB * CB][Thomas<CB>::NBK + 1];
+  // part[s][row]: contribution of block column s to a row (8-double pad keeps
+  // the stores of a warp's 4 blocks in distinct bank halves by I+J parity)
+  double part[Thomas<CB>::NBK][CB * CB + 8];
   double u[CB * CB * CB];
   uint64_t bars[kSlots];
   double (*slots)[Thomas<CB>::PLANE];
 };
+
+template <int CB>
+struct MvRole {
+  int I, J, r, blk;
+  bool active;
+};
+
+template <int CB>
+__device__ __forceinline__ MvRole<CB> mv_role() {
+  MvRole<CB> m;
+  const int tid = threadIdx.x;
+  m.active = tid < Thomas<CB>::MV;
+  m.blk = m.active ? tid / 8 : 0;
+  m.r = tid % 8;
+  block_of<CB>(m.blk, m.I, m.J);
+  return m;
+}
 
 // 8-lane reduce-scatter: lane r (of an aligned group of 8) returns sum over the
 // group's lanes of b[r].
@@ -96,26 +134,6 @@ __device__ __forceinline__ double reduce_scatter8(double (&b)[8], int r) {
   return keep + __shfl_xor_sync(0xffffffffu, send, 1);
 }
 
-template <int CB>
-struct MvRole {
-  int I, J, r, blk;
-  bool active;
-};
-
-template <int CB>
-__device__ __forceinline__ MvRole<CB> mv_role() {
-  MvRole<CB> m;
-  const int tid = threadIdx.x;
-  m.active = tid < Thomas<CB>::MV;
-  m.blk = m.active ? tid / 8 : 0;
-  m.r = tid % 8;
-  int I = 0;
-  while ((I + 1) * (I + 2) / 2 <= m.blk) ++I;
-  m.I = I;
-  m.J = m.blk - I * (I + 1) / 2;
-  return m;
-}
-
 // One plane mat-vec step: partial products into part[][].
 template <int CB>
 __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp, const double* w,
@@ -124,12 +142,15 @@ __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp
   if ((int)(threadIdx.x >> 5) >= (Thomas<CB>::MV + 31) / 32) return;
   const bool off_diag = m.active && m.J < m.I;
   double gv[8];
-  const double* row = Gp + m.blk * 64;
+  const uint32_t row = smem_u32(Gp + m.blk * 64);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const double2 v = *reinterpret_cast<const double2*>(row + swz(m.r, 2 * q));
-    gv[2 * q] = m.active ? v.x : 0.0;
-    gv[2 * q + 1] = m.active ? v.y : 0.0;
+    double2 v;  // explicit ld.shared: the slot pointer is opaque to the compiler
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "r"(row + (uint32_t)(swz(m.r, 2 * q) * sizeof(double))));
+    gv[2 * q] = v.x;
+    gv[2 * q + 1] = v.y;
   }
   double a0 = 0.0, a1 = 0.0;  // two chains halve the dependent-FMA latency
 #pragma unroll
@@ -138,13 +159,14 @@ __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp
     a0 = fma(gv[c], wv.x, a0);
     a1 = fma(gv[c + 1], wv.y, a1);
   }
-  if (m.active) sm.part[8 * m.I + m.r][m.J] = a0 + a1;
-  const double wr = w[8 * m.I + m.r];
+  if (m.active) sm.part[m.J][8 * m.I + m.r] = a0 + a1;
+  // transposed block; diagonal blocks (and idle lanes) contribute zeros
+  const double wr = off_diag ? w[8 * m.I + m.r] : 0.0;
   double b[8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) b[c] = off_diag ? gv[c] * wr : 0.0;
+  for (int c = 0; c < 8; ++c) b[c] = gv[c] * wr;
   const double cs = reduce_scatter8(b, m.r);
-  if (off_diag) sm.part[8 * m.J + m.r][m.I] = cs;
+  if (off_diag) sm.part[m.I][8 * m.J + m.r] = cs;
 }
 
 template <int CB>
@@ -208,7 +230,7 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
     if (tid < P) {
       double pr[NBK];
 #pragma unroll
-      for (int s = 0; s < NBK; ++s) pr[s] = sm.part[tid][s];
+      for (int s = 0; s < NBK; ++s) pr[s] = sm.part[s][tid];
 #pragma unroll
       for (int w = 1; w < NBK; w *= 2)  // fixed pairwise tree
 #pragma unroll

@@ -12,6 +12,7 @@ ap.add_argument("--sd", type=int, default=2)
 ap.add_argument("--kmin", type=float, default=1e-6)
 ap.add_argument("--kind", default="mmg")
 ap.add_argument("--solves", type=int, default=2)
+ap.add_argument("--setups", type=int, default=1)
 a = ap.parse_args()
 n = a.n
 rho = inputs.box_filter_design(n, 0.3)
@@ -19,7 +20,11 @@ kappa = inputs.conductivity(rho, a.kmin)
 ctx = Context(GridSpec(n, n, n), a.ncc, a.sd)
 ctx.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))
 b = ctx.assemble_rhs(np.ones(n ** 3))
-ctx.setup(a.kind)
+import time
+for _ in range(a.setups):
+    t0 = time.perf_counter()
+    ctx.setup(a.kind)
+    print("setup wall ms %.2f" % ((time.perf_counter() - t0) * 1e3))
 ctx.upload_rhs(b)
 for _ in range(a.solves):
     rep = ctx.solve_resident(1e-8, 5000)
