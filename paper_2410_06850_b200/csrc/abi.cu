@@ -8,6 +8,7 @@
 #include <cstring>
 #include <functional>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/topmg_b200.h"
@@ -74,6 +75,10 @@ struct tmg_ctx {
   int64_t launches = 0;       // kernels enqueued by solves (incl. graph nodes)
   int64_t bytes = 0;
   std::vector<void*> allocs;
+  // released buffers kept for reuse (re-setup with the same sizes allocates
+  // nothing); byte size of every live or pooled buffer
+  std::vector<std::pair<void*, size_t>> pool;
+  std::unordered_map<void*, size_t> sizes;
   double setup_seconds = 0.0;
 };
 
@@ -104,17 +109,27 @@ template <typename T>
 T* dalloc(tmg_ctx* c, int64_t n) {
   void* p = nullptr;
   const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(n, 1);
+  for (size_t i = 0; i < c->pool.size(); ++i)
+    if (c->pool[i].second == bytes) {
+      p = c->pool[i].first;
+      c->pool.erase(c->pool.begin() + (std::ptrdiff_t)i);
+      c->allocs.push_back(p);
+      return (T*)p;
+    }
   CK(cudaMalloc(&p, bytes));
   c->allocs.push_back(p);
+  c->sizes[p] = bytes;
   c->bytes += (int64_t)bytes;
   return (T*)p;
 }
 
+// release to the context's pool (freed for real in tmg_destroy)
 void dfree(tmg_ctx* c, void* p) {
   if (!p) return;
   auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
-  if (it != c->allocs.end()) c->allocs.erase(it);
-  cudaFree(p);
+  if (it == c->allocs.end()) return;
+  c->allocs.erase(it);
+  c->pool.emplace_back(p, c->sizes[p]);
 }
 
 void free_setup(tmg_ctx* c) {
@@ -492,6 +507,7 @@ void tmg_destroy(tmg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
+  for (auto& pb : c->pool) cudaFree(pb.first);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -634,7 +650,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       };
       mark("alloc");
       const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
-      const int degree = o->eig_degree > 0 ? o->eig_degree : 16;
+      const int degree = o->eig_degree > 0 ? o->eig_degree : 32;
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
       launch_local_basis(g, c->cb, c->kappa, c->phi, c->evals, c->eig_iters, tol, degree, max_outer,
                          c->stream);

@@ -145,40 +145,50 @@ __device__ __forceinline__ void bmatvec(const double (&x)[K], double (&y)[K], do
   __syncthreads();
 }
 
-// Gram matrix G_ij = (x_i . y_j + x_j . y_i) / 2 (K x K, symmetric) -> smem g,
-// reduced in chunks of K+1 sums to bound register pressure.
-template <int CB, int K>
-__device__ __forceinline__ void gram_sym(const double (&x)[K], const double (&y)[K], double* red,
-                                         double* g) {
-  constexpr int NP = K * (K + 1) / 2;
-  constexpr int CH = K + 1;
-  static_assert(NP % CH == 0, "chunking");
-#pragma unroll
-  for (int c0 = 0; c0 < NP; c0 += CH) {
-    double v[CH];
-#pragma unroll
-    for (int e = 0; e < CH; ++e) {
-      // unrank e + c0 -> (i, j), j <= i
-      int idx = c0 + e, i = 0;
-      while ((i + 1) * (i + 2) / 2 <= idx) ++i;
-      const int j = idx - i * (i + 1) / 2;
-      v[e] = 0.5 * (x[i] * y[j] + x[j] * y[i]);
-    }
-    block_sum_k<CB * CB * CB, CH>(v, red);
-    if (threadIdx.x < CH) {
-      int idx = c0 + threadIdx.x, i = 0;
-      while ((i + 1) * (i + 2) / 2 <= idx) ++i;
-      const int j = idx - i * (i + 1) / 2;
-      g[i * K + j] = v[threadIdx.x];
-      g[j * K + i] = v[threadIdx.x];
-    }
-  }
-  __syncthreads();
+// FP64 tensor-core Gram: G = (X^T Y + Y^T X) / 2 for K = 8 vectors over the
+// C cells (thread t owns cell t). X and Y are staged in smem as [K][C + 4]
+// (the pad puts the 8 vectors' 4-cell runs in distinct bank quarters), each
+// warp accumulates its 32 cells with 8 mma.m8n8k4 (A fragment X^T[v][c] =
+// B fragment layout), and the 16 (or 2) warp partials are summed in a fixed
+// order, symmetrising on the way. Ends with g in smem after a barrier.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
 template <int CB, int K>
-__device__ __forceinline__ void gram(const double (&x)[K], double* red, double* g) {
-  gram_sym<CB, K>(x, x, red, g);
+__device__ __forceinline__ void gram_mma(const double (&x)[K], const double (&y)[K], bool same,
+                                         double* xs, double* ys, double* red, double* g) {
+  static_assert(K == 8, "mma.m8n8k4 Gram is built for K = 8");
+  constexpr int C = CB * CB * CB, CS = C + 4, NW = C / 32;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    xs[k * CS + t] = x[k];
+    if (!same) ys[k * CS + t] = y[k];
+  }
+  __syncthreads();
+  const double* yb = same ? xs : ys;
+  double acc[2] = {0.0, 0.0};
+  const int off = (lane >> 2) * CS + 32 * w + (lane & 3);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) dmma_8x8x4(acc, xs[off + 4 * s], yb[off + 4 * s]);
+  // acc = rows lane/4, cols 2*(lane%4) + {0, 1} of this warp's X^T Y
+  red[w * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[0];
+  red[w * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[1];
+  __syncthreads();
+  if (t < 64) {
+    const int i = t >> 3, j = t & 7;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int v = 0; v < NW; ++v) {
+      a += red[v * 64 + i * 8 + j];
+      b += red[v * 64 + j * 8 + i];
+    }
+    g[t] = 0.5 * (a + b);
+  }
+  __syncthreads();
 }
 
 // X <- X R^{-1} where G = R^T R (Cholesky of the Gram matrix, kept in smem).
@@ -233,11 +243,13 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   extern __shared__ double sm[];
   double* u = sm;                     // K*C exchange buffer
   double* kt = u + K * C;             // C
-  double* red = kt + C;               // NP*NW + NP
-  double* gs = red + NP * NW + NP + 8;  // K*K
+  double* red = kt + C;               // max(NP*NW + NP + 8, 64*NW)
+  double* gs = red + (NP * NW + NP + 8 > 64 * NW ? NP * NW + NP + 8 : 64 * NW);  // K*K
   double* qv = gs + K * K;            // K*K
   double* rsm = qv + K * K;           // K*K
-  double* scal = rsm + K * K;         // 8 scalars
+  double* scal = rsm + K * K;         // K + 8 scalars
+  double* xs = scal + K + 8;          // K*(C+4) Gram staging
+  double* ys = xs + K * (C + 4);      // K*(C+4)
   __shared__ int okflag;
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   const int64_t b = blockIdx.x;
@@ -291,7 +303,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   for (outer = 0; outer <= max_outer; ++outer) {
     // --- orthonormalise (CholQR twice) ---
     for (int pass = 0; pass < 2; ++pass) {
-      gram<CB, K>(x, red, gs);
+      gram_mma<CB, K>(x, x, true, xs, ys, red, gs);
       if (!cholqr_apply<K>(x, gs, rsm, &okflag)) {
         // rank loss: re-seed the trailing vectors and retry next pass
 #pragma unroll
@@ -300,7 +312,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
     }
     // --- Rayleigh-Ritz ---
     bmatvec<CB, K>(x, y, u, tf, sl, sll, nb);
-    gram_sym<CB, K>(x, y, red, gs);
+    gram_mma<CB, K>(x, y, false, xs, ys, red, gs);
     if (t < 32) {
       warp_jacobi_small<K>(gs, rsm);  // gs -> eigenvalues on its diagonal, rsm = vectors
       if (t == 0) {
@@ -333,16 +345,15 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
     }
     __syncthreads();
     // residual norms of the wanted pairs
-    double rs[K];
+    double rv[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      const double rv = yn[c] - theta[c] * xn[c];
-      rs[c] = rv * rv;
+      rv[c] = yn[c] - theta[c] * xn[c];
       x[c] = xn[c];
     }
-    block_sum_k<C, K>(rs, red);
+    gram_mma<CB, K>(rv, rv, true, xs, ys, red, rsm);  // diagonal = squared residual norms
     double worst = 0.0;
-    for (int c = 0; c < g.lc; ++c) worst = fmax(worst, sqrt(rs[c]));
+    for (int c = 0; c < g.lc; ++c) worst = fmax(worst, sqrt(fmax(rsm[c * K + c], 0.0)));
     if (worst <= tol * bmax) { converged = true; break; }
     if (outer == max_outer) break;
     // --- Chebyshev filter damping [a_cut, bmax], normalised at 0 ---
@@ -390,7 +401,8 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
 
 size_t local_basis_smem(int cb, int K) {
   const int C = cb * cb * cb, NW = C / 32, NP = K * (K + 1) / 2;
-  return sizeof(double) * (size_t)(K * C + C + NP * NW + NP + 8 + 3 * K * K + K + 8);
+  const int red = NP * NW + NP + 8 > 64 * NW ? NP * NW + NP + 8 : 64 * NW;
+  return sizeof(double) * (size_t)(K * C + C + red + 3 * K * K + K + 8 + 2 * K * (C + 4));
 }
 
 void launch_local_basis(const GridParams& g, int cb, const double* kappa, double* phi,

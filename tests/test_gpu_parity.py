@@ -254,11 +254,15 @@ def test_vcycle_matches_numpy_reference(n, ncc, sd, kmin):
     z_ref = _numpy_vcycle(A, Rc, Rcc, fine, coarse, r)
     z = c.apply_preconditioner(r)
     # The GPU applies explicit inverses (A_cc^-1, the plane Schur inverses, the
-    # coarse block inverses) where the numpy reference factorises: the
-    # difference scales with cond(A_II), ~1e7 at contrast 1e6. PCG parity
-    # (iterations, solution) is checked separately and is unaffected.
-    tol = 1e-9 if kmin >= 1e-3 else 2e-6
-    assert np.linalg.norm(z - z_ref) <= tol * np.linalg.norm(z_ref)
+    # coarse block inverses) where the numpy reference factorises, so the two
+    # agree to the forward-error scale eps * cond of the worst-conditioned
+    # solve, A_cc (cond ~1e10 at contrast 1e6). PCG parity (iterations,
+    # solution) is checked separately and is unaffected.
+    Acc = Rcc @ (Rc @ A @ Rc.T).toarray() @ Rcc.T
+    cond = np.linalg.cond(Acc)
+    tol = max(1e-9, 100 * np.finfo(float).eps * cond)
+    err = np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref)
+    assert err <= tol, (err, cond)
 
 
 def test_preconditioner_symmetric_positive_definite():

@@ -4,7 +4,7 @@ from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs, MmgOp
 for n,ncc,kmin in [(128,8,1e-6),(64,4,1e-3)]:
     rho=inputs.box_filter_design(n,0.3); kap=inputs.conductivity(rho,kmin)
     c=Context(GridSpec(n,n,n),ncc,2); c.set_conductivity(kap,BoundarySpec.bottom_center_patch(1,1,0.2,0))
-    for deg in [8,16,32]:
+    for deg in [16,24,32,48]:
         c.setup("mmg", MmgOptions(eig_degree=deg))
         t=time.time(); c.setup("mmg", MmgOptions(eig_degree=deg)); 
         phi,ev,it=c.local_bases()
