@@ -12,109 +12,207 @@
 
 namespace tmg {
 
-constexpr int NB = 32;
+constexpr int NB = 64;  // Gauss-Jordan pivot block
 
-// Invert the pivot block A[K,K] (nbk x nbk) into Dinv (NB x NB), record pivots.
-__global__ void k_gj_diag(const double* __restrict__ A, int64_t n, int64_t k0, int nbk,
-                          double* Dinv, double* pivots) {
-  __shared__ double M[NB * NB];
+// Invert the pivot block A[K,K] (nbk x nbk, nbk <= NB) into Dinv, record the
+// pivots. 1024 threads, each owning fixed elements of the (NB x NB) block.
+__global__ void __launch_bounds__(1024) k_gj_diag(const double* __restrict__ A, int64_t n,
+                                                  int64_t k0, int nbk, double* Dinv,
+                                                  double* pivots) {
+  constexpr int PER = NB * NB / 1024;
+  __shared__ double M[NB][NB + 1];
   __shared__ double col[NB], rowp[NB];
-  for (int e = threadIdx.x; e < nbk * nbk; e += blockDim.x) {
-    const int i = e / nbk, j = e % nbk;
-    M[e] = A[(k0 + i) * n + k0 + j];
+  const int t = threadIdx.x;
+  int ei[PER], ej[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    ei[q] = (t + 1024 * q) / NB;
+    ej[q] = (t + 1024 * q) % NB;
+    const bool in = ei[q] < nbk && ej[q] < nbk;
+    // identity padding keeps the padded pivots harmless
+    M[ei[q]][ej[q]] = in ? A[(k0 + ei[q]) * n + k0 + ej[q]] : (ei[q] == ej[q] ? 1.0 : 0.0);
   }
   __syncthreads();
   for (int p = 0; p < nbk; ++p) {
-    const double pv = M[p * nbk + p];
-    if (threadIdx.x < nbk) {
-      col[threadIdx.x] = M[threadIdx.x * nbk + p];
-      rowp[threadIdx.x] = M[p * nbk + threadIdx.x];
+    if (t < NB) {
+      col[t] = M[t][p];
+      rowp[t] = M[p][t];
     }
-    if (threadIdx.x == 0) pivots[k0 + p] = pv;
     __syncthreads();
+    const double pv = rowp[p];
+    if (t == 0) pivots[k0 + p] = pv;
     const double inv = 1.0 / pv;
-    for (int e = threadIdx.x; e < nbk * nbk; e += blockDim.x) {
-      const int i = e / nbk, j = e % nbk;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = ei[q], j = ej[q];
       double v;
       if (i == p && j == p) v = inv;
       else if (i == p) v = rowp[j] * inv;
       else if (j == p) v = -col[i] * inv;
-      else v = M[e] - col[i] * (rowp[j] * inv);
-      M[e] = v;
+      else v = M[i][j] - col[i] * (rowp[j] * inv);
+      M[i][j] = v;
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < nbk * nbk; e += blockDim.x) Dinv[e] = M[e];
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if (ei[q] < nbk && ej[q] < nbk) Dinv[ei[q] * nbk + ej[q]] = M[ei[q]][ej[q]];
 }
 
-// Pn[r][j] = sum_c Dinv[r][c] A[k0+c][j]  (row panel, new);  Cold[i][c] = A[i][k0+c]
-__global__ void k_gj_panels(const double* __restrict__ A, int64_t n, int64_t k0, int nbk,
-                            const double* __restrict__ Dinv, double* Pn, double* Cold) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  double a[NB];
-  for (int c = 0; c < nbk; ++c) a[c] = A[(k0 + c) * n + j];
-  for (int r = 0; r < nbk; ++r) {
-    double s = 0.0;
-    for (int c = 0; c < nbk; ++c) s += Dinv[r * nbk + c] * a[c];
-    Pn[r * n + j] = s;
-  }
-  // by symmetry of the current iterate's structure we still copy the column explicitly
-  for (int c = 0; c < nbk; ++c) Cold[j * NB + c] = A[j * n + k0 + c];
-}
-
-// A <- swept(A) given Dinv, Pn (new row panel), Cold (old column panel).
-// 64 x 64 tiles, 256 threads, 4 x 4 per thread.
-__global__ void __launch_bounds__(256) k_gj_update(double* A, int64_t n, int64_t k0, int nbk,
-                                                   const double* __restrict__ Dinv,
-                                                   const double* __restrict__ Pn,
-                                                   const double* __restrict__ Cold) {
-  __shared__ double Cs[64][NB + 1];
-  __shared__ double Ps[NB][64 + 1];
-  __shared__ double Ds[NB][NB + 1];
-  const int64_t i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  for (int e = threadIdx.x; e < 64 * NB; e += 256) {
-    const int r = e / NB, c = e % NB;
-    const int64_t i = i0 + r;
-    Cs[r][c] = (i < n && c < nbk) ? Cold[i * NB + c] : 0.0;
-  }
-  for (int e = threadIdx.x; e < NB * 64; e += 256) {
-    const int r = e / 64, c = e % 64;
-    const int64_t j = j0 + c;
-    Ps[r][c] = (j < n && r < nbk) ? Pn[r * n + j] : 0.0;
-  }
-  for (int e = threadIdx.x; e < NB * NB; e += 256) {
+// Pn[r][j] = sum_c Dinv[r][c] A[k0+c][j] (new pivot rows); Cold[i][c] = A[i][k0+c]
+// (old pivot columns, ld NB, zero padded past nbk). CTA = 32 columns x 8 row
+// groups of NB/8 rows.
+__global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A, int64_t n,
+                                                   int64_t k0, int nbk,
+                                                   const double* __restrict__ Dinv, double* Pn,
+                                                   double* Cold) {
+  __shared__ double Ds[NB][NB];  // read as warp broadcasts
+  __shared__ double As[NB][32];
+  const int t = threadIdx.x, jx = t & 31, ry = t >> 5;
+  const int64_t j = blockIdx.x * 32LL + jx;
+  for (int e = t; e < NB * NB; e += 256) {
     const int r = e / NB, c = e % NB;
     Ds[r][c] = (r < nbk && c < nbk) ? Dinv[r * nbk + c] : 0.0;
   }
+  for (int c = ry; c < NB; c += 8) As[c][jx] = (c < nbk && j < n) ? A[(k0 + c) * n + j] : 0.0;
   __syncthreads();
-  for (int a = 0; a < 4; ++a) {
-    const int r = ty + 16 * a;
-    const int64_t i = i0 + r;
+  if (j < n) {
+    constexpr int RG = NB / 8;
+    double acc[RG];
+#pragma unroll
+    for (int q = 0; q < RG; ++q) acc[q] = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < NB; ++c) {
+      const double a = As[c][jx];
+#pragma unroll
+      for (int q = 0; q < RG; ++q) acc[q] = fma(Ds[ry * RG + q][c], a, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RG; ++q) Pn[(ry * RG + q) * n + j] = acc[q];
+  }
+  // Cold: this CTA's 32 rows i = j-range, NB columns each
+  for (int e = t; e < 32 * NB; e += 256) {
+    const int64_t i = blockIdx.x * 32LL + e / NB;
+    const int c = e % NB;
+    if (i < n) Cold[i * NB + c] = c < nbk ? A[i * n + k0 + c] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Trailing update A -= Cold * Pn on FP64 tensor cores (mma.m8n8k4, DMMA).
+// 128 x 64 output tile per CTA (2 CTAs per SM), 8 warps of 32 x 32; both panels are
+// staged whole in shared memory (padded so each fragment load is 2
+// wavefronts) while the C tile is prefetched into L2 by bulk prefetches. The
+// pivot rows/columns get overwritten by k_gj_fix afterwards.
+constexpr int GT = 128;              // output tile rows
+constexpr int GN = 64;               // output tile columns
+constexpr int AS_LD = NB + 4;        // smem row stride of the Cold panel
+constexpr int BS_LD = GN + 8;        // smem row stride of the Pn panel
+constexpr size_t kGemmSmem = sizeof(double) * (size_t)(GT * AS_LD + NB * BS_LD);
+
+__global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
+                                                    const double* __restrict__ Cold,
+                                                    const double* __restrict__ Pn) {
+  extern __shared__ __align__(16) double smg[];
+  double* As = smg;
+  double* Bs = smg + GT * AS_LD;
+  const int64_t i0 = (int64_t)blockIdx.y * GT, j0 = (int64_t)blockIdx.x * GN;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t < GT && i0 + t < n) {
+    const int64_t cols = (n - j0) < GN ? (n - j0) : GN;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A + (i0 + t) * n + j0),
+                 "r"((unsigned)(cols * sizeof(double)))
+                 : "memory");
+  }
+  // both operand panels arrive by TMA bulk copies (one per panel row) on one
+  // mbarrier; rows past n are zero-filled by the threads instead
+  __shared__ uint64_t bar;
+  const int rows_a = (int)((n - i0) < GT ? (n - i0) : GT);
+  const int cols_b = (int)((n - j0) < GN ? (n - j0) : GN);
+  if (t == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (t == 0)
+    mbar_arrive_expect_tx(&bar, (uint32_t)(sizeof(double) * (rows_a * NB + NB * cols_b)));
+  __syncwarp();
+  if (w == 0) {
+    for (int r = lane; r < rows_a; r += 32)
+      bulk_g2s(As + r * AS_LD, Cold + (i0 + r) * NB, NB * sizeof(double), &bar);
+    for (int r = lane; r < NB; r += 32)
+      bulk_g2s(Bs + r * BS_LD, Pn + r * n + j0, (uint32_t)(cols_b * sizeof(double)), &bar);
+  }
+  for (int e = rows_a * AS_LD + t; e < GT * AS_LD; e += 256) As[e] = 0.0;
+  if (cols_b < GN)
+    for (int e = t; e < NB * GN; e += 256)
+      if (e % GN >= cols_b) Bs[(e / GN) * BS_LD + e % GN] = 0.0;
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const int wm = w & 3, wn = w >> 2;  // warp tile rows 32 wm.., cols 32 wn..
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  const double* ap = As + (32 * wm + (lane >> 2)) * AS_LD + (lane & 3);
+  const double* bp = Bs + (lane & 3) * BS_LD + 32 * wn + (lane >> 2);
+#pragma unroll 2
+  for (int k = 0; k < NB; k += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = ap[mi * 8 * AS_LD + k];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = bp[k * BS_LD + 8 * ni];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_m8n8k4(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int64_t i = i0 + 32 * wm + 8 * mi + (lane >> 2);
     if (i >= n) continue;
-    const bool iK = i >= k0 && i < k0 + nbk;
-    for (int b = 0; b < 4; ++b) {
-      const int c = tx + 16 * b;
-      const int64_t j = j0 + c;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int64_t j = j0 + 32 * wn + 8 * ni + 2 * (lane & 3);
       if (j >= n) continue;
-      const bool jK = j >= k0 && j < k0 + nbk;
-      double v;
-      if (iK && jK) {
-        v = Ds[i - k0][j - k0];
-      } else if (iK) {
-        v = Ps[i - k0][c];
-      } else if (jK) {
-        // -A_iK Dinv
-        double s = 0.0;
-        for (int q = 0; q < nbk; ++q) s += Cs[r][q] * Ds[q][j - k0];
-        v = -s;
-      } else {
-        double s = 0.0;
-        for (int q = 0; q < nbk; ++q) s += Cs[r][q] * Ps[q][c];
-        v = A[i * n + j] - s;
-      }
-      A[i * n + j] = v;
+      double2* cp = reinterpret_cast<double2*>(A + i * n + j);
+      double2 c = *cp;
+      c.x -= acc[mi][ni][0];
+      c.y -= acc[mi][ni][1];
+      *cp = c;
+    }
+  }
+}
+
+// Pivot rows <- Pn, pivot block <- Dinv, pivot columns <- -Cold Dinv.
+__global__ void __launch_bounds__(256) k_gj_fix(double* A, int64_t n, int64_t k0, int nbk,
+                                                const double* __restrict__ Dinv,
+                                                const double* __restrict__ Pn,
+                                                const double* __restrict__ Cold) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n * nbk) return;
+  // rows: e -> (r, j)
+  {
+    const int r = (int)(e / n);
+    const int64_t j = e % n;
+    const bool jK = j >= k0 && j < k0 + nbk;
+    A[(k0 + r) * n + j] = jK ? Dinv[r * nbk + (j - k0)] : Pn[r * n + j];
+  }
+  // columns: e -> (i, c)
+  {
+    const int64_t i = e / nbk;
+    const int c = (int)(e % nbk);
+    if (i < k0 || i >= k0 + nbk) {
+      double s = 0.0;
+      for (int q = 0; q < nbk; ++q) s = fma(Cold[i * NB + q], Dinv[q * nbk + c], s);
+      A[i * n + k0 + c] = -s;
     }
   }
 }
@@ -333,12 +431,14 @@ void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStre
   double* Pn = Dinv + NB * NB;
   double* Cold = Pn + (int64_t)NB * n;
   double* piv = Cold + n * NB;
+  cudaFuncSetAttribute(k_gj_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  const dim3 grid((unsigned)((n + GN - 1) / GN), (unsigned)((n + GT - 1) / GT));
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int nbk = (int)((n - k0) < NB ? (n - k0) : NB);
-    k_gj_diag<<<1, 256, 0, s>>>(A, n, k0, nbk, Dinv, piv);
-    k_gj_panels<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
-    dim3 grid((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
-    k_gj_update<<<grid, 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
+    k_gj_diag<<<1, 1024, 0, s>>>(A, n, k0, nbk, Dinv, piv);
+    k_gj_panels<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
+    k_gj_gemm<<<grid, 256, kGemmSmem, s>>>(A, n, Cold, Pn);
+    k_gj_fix<<<(unsigned)((n * nbk + 255) / 256), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
   }
   k_symmetrize<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(A, n);
   k_pivot_check<<<1, 1024, 0, s>>>(piv, n, status);
