@@ -475,6 +475,12 @@ int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
   g.vol = g.hx * g.hy * g.hz;
   g.lc = 4;
   g.lcc = 8;
+  g.b0 = 0;
+  g.nbo = g.nb;
+  g.e0 = 0;
+  g.neo = g.ncc;
+  g.mst = c->M;
+  g.dist = 0;
   const int rc = guard(c, [&] {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -553,7 +559,7 @@ int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,
   rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
     upload_global(c, rho, c->r);  // r as scratch for rho (brick layout)
-    launch_conductivity(c->r, c->kappa, c->M, lo, hi, p, c->stream);
+    launch_conductivity(c->g, c->cb, c->r, c->kappa, lo, hi, p, c->stream);
     CK(cudaGetLastError());
   });
   if (rc) return rc;

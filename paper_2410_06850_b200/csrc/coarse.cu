@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
   __shared__ StencilSmem<CB> ss;
   __shared__ double ph[LC][C];
   __shared__ double red[LC * LC * NW + LC * LC + 8];
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_tile<CB, true>(kappa, ss.kt, g, bc);
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   double f[LC];
@@ -242,7 +242,7 @@ __global__ void k_cc_basis(GridParams g, const double* __restrict__ Ac,
   const int q = g.sd * g.sd * g.sd * LC;
   double* M = sm;
   double* V = M + q * q;
-  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   build_elem_matrix(g, ec, Ac, Bc, true, M, q);
   if (threadIdx.x < 32) warp_jacobi(M, V, q);
   __syncthreads();
@@ -255,11 +255,11 @@ __global__ void k_cc_basis(GridParams g, const double* __restrict__ Ac,
       for (int i = 0; i < q; ++i)
         if (!used[i] && (best < 0 || M[i * q + i] < M[best * q + best])) best = i;
       used[best] = 1;
-      cc_evals[blockIdx.x * g.lcc + k] = M[best * q + best];
+      cc_evals[ec.e * g.lcc + k] = M[best * q + best];
       double s = 0.0;
       for (int r = 0; r < q; ++r) s += V[r * q + best];
       const double sg = s < 0.0 ? -1.0 : 1.0;
-      for (int r = 0; r < q; ++r) Rcc[((int64_t)blockIdx.x * g.lcc + k) * q + r] = sg * V[r * q + best];
+      for (int r = 0; r < q; ++r) Rcc[((int64_t)ec.e * g.lcc + k) * q + r] = sg * V[r * q + best];
     }
   }
 }
@@ -320,11 +320,11 @@ __global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, d
   double* col = M + q * q;
   double* rowp = col + q;
   double* pivs = rowp + q;
-  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   build_elem_matrix(g, ec, Ac, nullptr, false, M, q);
   const bool ok = smem_gj_inverse(M, q, col, rowp, pivs);
   if (!ok && threadIdx.x == 0) atomicExch(status, 2);
-  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Winv[(int64_t)blockIdx.x * q * q + e] = M[e];
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Winv[(int64_t)ec.e * q * q + e] = M[e];
 }
 
 // A_cc block (E, F) for F in {E, 6 face neighbours}: sum over coupled child
@@ -333,7 +333,7 @@ __global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, d
 __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
                                const double* __restrict__ Rcc, double* Acc, int64_t ldacc) {
   const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
-  const ElemCoord ec = elem_coord(g, blockIdx.x);
+  const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   const int fdir = blockIdx.y;  // 0 self, 1..6 faces
   int64_t F = ec.e;
   if (fdir > 0) {
@@ -415,7 +415,7 @@ __global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
                                 const double* __restrict__ add, double* out) {
   if (*done) return;
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
   double* xin = sm;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
@@ -445,7 +445,7 @@ __global__ void k_coarse_restrict(GridParams g, const int* __restrict__ done,
                                   double* rcc) {
   if (*done) return;
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
   double* wc = sm;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
@@ -465,7 +465,7 @@ __global__ void k_coarse_prolong(GridParams g, const int* __restrict__ done,
                                  const double* __restrict__ Rcc, const double* __restrict__ rc0,
                                  const double* __restrict__ ecc, double* rc1) {
   if (*done) return;
-  const int q = g.sd * g.sd * g.sd * LC, e = blockIdx.x;
+  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
     double s = 0.0;
@@ -481,8 +481,8 @@ __global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
                                const double* __restrict__ Ac, const double* __restrict__ rc,
                                const double* __restrict__ x, double* out, int n) {
   if (*done) return;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
+  const int64_t k = g.b0 * LC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= g.b0 * LC + n) return;
   out[k] = rc[k] - coarse_apply_row(g, Ac, x, k / LC, k % LC);
 }
 
@@ -491,9 +491,9 @@ __global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
 void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                           const double* phi, double* Ac, double* Bc, cudaStream_t s) {
   if (cb == 8)
-    k_coarse_blocks<8><<<(unsigned)g.nb, 512, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+    k_coarse_blocks<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
   else
-    k_coarse_blocks<4><<<(unsigned)g.nb, 64, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+    k_coarse_blocks<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
 }
 
 void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, double* Rcc,
@@ -501,7 +501,7 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
   const int q = g.sd * g.sd * g.sd * LC;
   const size_t smem = sizeof(double) * (size_t)(2 * q * q + q + 8);
   cudaFuncSetAttribute(k_cc_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cc_basis<<<(unsigned)g.ncc, 64, smem, s>>>(g, Ac, Bc, Rcc, cc_evals);
+  k_cc_basis<<<(unsigned)g.neo, 64, smem, s>>>(g, Ac, Bc, Rcc, cc_evals);
 }
 
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
@@ -509,14 +509,15 @@ void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv,
   const int q = g.sd * g.sd * g.sd * LC;
   const size_t smem = sizeof(double) * (size_t)(q * q + 3 * q + 8);
   cudaFuncSetAttribute(k_coarse_smoother, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_coarse_smoother<<<(unsigned)g.ncc, 256, smem, s>>>(g, Ac, Winv, status);
+  k_coarse_smoother<<<(unsigned)g.neo, 256, smem, s>>>(g, Ac, Winv, status);
 }
 
 void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
                          cudaStream_t s) {
   const int64_t n = g.ncc * g.lcc;
-  cudaMemsetAsync(Acc, 0, sizeof(double) * (size_t)(n * n), s);
-  dim3 grid((unsigned)g.ncc, 7);
+  // this context's rows of the global n x n matrix
+  cudaMemsetAsync(Acc + g.e0 * g.lcc * n, 0, sizeof(double) * (size_t)(g.neo * g.lcc * n), s);
+  dim3 grid((unsigned)g.neo, 7);
   k_acc_assemble<<<grid, g.lcc * g.lcc, 0, s>>>(g, Ac, Rcc, Acc, n);
 }
 
@@ -530,14 +531,14 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
   const int nt = (q + 31) / 32 * 32;
-  const int nc = (int)(g.nb * LC);
+  const int nc = (int)(g.nbo * LC);
   const size_t sm = sizeof(double) * (size_t)q;
-  k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, rc, nullptr, rc0);
-  k_coarse_restrict<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
+  k_coarse_smooth<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Winv, rc, nullptr, rc0);
+  k_coarse_restrict<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
   launch_symv(done, Acc_tiles, n_cc, rcc, symv_partials, ecc, s);
-  k_coarse_prolong<<<(unsigned)g.ncc, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
+  k_coarse_prolong<<<(unsigned)g.neo, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
   k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, rc1, tc, nc);
-  k_coarse_smooth<<<(unsigned)g.ncc, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);
+  k_coarse_smooth<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);
 }
 
 int compiled_lc() { return LC; }

@@ -34,6 +34,13 @@ struct GridParams {
   double cpl[3];             // area/h per axis (fvm.cpp:23-26)
   double vol;                // cell volume
   double hx, hy, hz;
+  // Partition: this context owns bricks [b0, b0 + nbo) and
+  // cc elements [e0, e0 + neo) -- whole z-layers of cc elements. Kernels index
+  // global bricks/elements; device arrays are windows of the global arrays
+  // (own layers plus one ghost brick layer per neighbouring slab). mst is the
+  // stored cells per fine vector (component stride of coef).
+  int64_t b0, nbo, e0, neo, mst;
+  int dist;  // 1: reductions finish in k_finalize after the cross-slab sum
 };
 
 __device__ __forceinline__ double face_t(double kl, double kr) {

@@ -27,8 +27,8 @@ struct PcgState {
 // operator.cu
 void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
 void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
-void launch_conductivity(const double* x, double* kappa, int64_t m, double lo, double hi, int p,
-                         cudaStream_t s);
+void launch_conductivity(const GridParams& g, int cb, const double* x, double* kappa, double lo,
+                         double hi, int p, cudaStream_t s);
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
                      double ly, double lz, const double* kappa, const double* source,
                      uint8_t* dmask, double* rhs, unsigned long long* count, cudaStream_t s);

@@ -17,25 +17,26 @@ __device__ __forceinline__ int64_t brick_to_global(const GridParams& g, int cb, 
   return i + g.nx * (j + g.ny * k);
 }
 
+// src/dst: x-fastest cells of this context's z-slab (global index - xoff).
 __global__ void k_to_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
-                           int64_t m) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+                           int64_t s0, int64_t m, int64_t xoff) {
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x)
-    dst[s] = src[brick_to_global(g, cb, s)];
+    dst[s] = src[brick_to_global(g, cb, s) - xoff];
 }
 
 __global__ void k_from_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
-                             int64_t m) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+                             int64_t s0, int64_t m, int64_t xoff) {
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x)
-    dst[brick_to_global(g, cb, s)] = src[s];
+    dst[brick_to_global(g, cb, s) - xoff] = src[s];
 }
 
 // material.cpp:45-59 — kappa = lo + x^p (hi - lo), repeated multiply
-__global__ void k_conductivity(const double* __restrict__ x, double* kappa, int64_t m, double lo,
-                               double hi, int p) {
+__global__ void k_conductivity(const double* __restrict__ x, double* kappa, int64_t s0, int64_t m,
+                               double lo, double hi, int p) {
   const double dk = hi - lo;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x) {
     double r = 1.0;
     for (int i = 0; i < p; ++i) r = __dmul_rn(r, x[s]);
@@ -84,8 +85,8 @@ __device__ bool dirichlet_value(const GridParams& g, const PatchSet& ps, int64_t
 // b = f*vol + sum_D t_D * T_D in the reference face order (fvm.cpp:63-112).
 __global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __restrict__ kappa,
                            const double* __restrict__ source, uint8_t* dmask, double* rhs,
-                           int64_t m, unsigned long long* count) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+                           int64_t s0, int64_t m, unsigned long long* count) {
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int c = cb * cb * cb;
     const int64_t b = s / c;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_apply(GridParams g, const doub
   __shared__ CoefSmem<CB> cs;
   __shared__ double xt[Tile<CB>::N];
   constexpr int C = CB * CB * CB;
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_coefs<CB>(coef, M, cs, g, bc);
   if (x) load_tile<CB, true>(x, xt, g, bc);
   __syncthreads();
@@ -137,18 +138,24 @@ static int grid1d(int64_t m) {
   return (int)b;
 }
 
+// own cells of the context: brick-layout [b0*C, (b0+nbo)*C); x-fastest slab
+// arrays start at global cell (b0 / (nbx*nby)) * cb * nx * ny
+static int64_t slab_xoff(const GridParams& g, int cb) {
+  return (g.b0 / (g.nbx * g.nby)) * cb * g.nx * g.ny;
+}
 void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s) {
-  const int64_t m = g.nx * g.ny * g.nz;
-  k_to_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, m);
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_to_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, g.b0 * C, m, slab_xoff(g, cb));
 }
 void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst,
                        cudaStream_t s) {
-  const int64_t m = g.nx * g.ny * g.nz;
-  k_from_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, m);
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_from_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, g.b0 * C, m, slab_xoff(g, cb));
 }
-void launch_conductivity(const double* x, double* kappa, int64_t m, double lo, double hi, int p,
-                         cudaStream_t s) {
-  k_conductivity<<<grid1d(m), 256, 0, s>>>(x, kappa, m, lo, hi, p);
+void launch_conductivity(const GridParams& g, int cb, const double* x, double* kappa, double lo,
+                         double hi, int p, cudaStream_t s) {
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_conductivity<<<grid1d(m), 256, 0, s>>>(x, kappa, g.b0 * C, m, lo, hi, p);
 }
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
                      double ly, double lz, const double* kappa, const double* source,
@@ -157,16 +164,16 @@ void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npat
   ps.n = npatch;
   for (int i = 0; i < npatch && i < kMaxPatches; ++i) ps.p[i] = patches[i];
   ps.lx = lx; ps.ly = ly; ps.lz = lz;
-  const int64_t m = g.nx * g.ny * g.nz;
-  k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, m, count);
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, g.b0 * C, m, count);
 }
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
+  const int64_t M = g.mst;
   if (cb == 8)
-    k_apply<8><<<(unsigned)g.nb, 512, 0, s>>>(g, coef, M, x, y, dinv);
+    k_apply<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, x, y, dinv);
   else
-    k_apply<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, x, y, dinv);
+    k_apply<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, x, y, dinv);
 }
 
 }  // namespace tmg

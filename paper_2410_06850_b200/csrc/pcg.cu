@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coefficients(GridParams g,
                                                               double* coef, int64_t M) {
   constexpr int C = CB * CB * CB;
   __shared__ StencilSmem<CB> ss;
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_tile<CB, true>(kappa, ss.kt, g, bc);
   __syncthreads();
   tile_faces<CB>(ss.kt, ss.fx, ss.fy, ss.fz, g, bc);
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const doubl
   __shared__ double xt[Tile<CB>::N];
   __shared__ double red[80];
   __shared__ int flag;
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   const size_t s = bofs(bc.b, C) + t;
   const double bv = b[s];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, con
   const int t = threadIdx.x;
   const bool first = st->first;
   const double beta = st->beta;
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_coefs<CB>(coef, M, cs, g, bc);
   load_tile_axpy<CB>(z, p_old, beta, first, pt, g, bc);  // p = z + beta p (solver.cpp:565-567)
   __syncthreads();
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, cons
   constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
-  const int b = blockIdx.x;
+  const int b = (int)(blockIdx.x + g.b0);
   const double* G = Gf + (size_t)b * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
   __shared__ CoefSmem<CB> cs;
   __shared__ double xt[Tile<CB>::N];
   __shared__ double red[LCP * (NT / 32) + LCP + 8];
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const int t = threadIdx.x;
   load_coefs<CB>(coef, M, cs, g, bc);
   load_tile<CB, true>(r1, xt, g, bc);
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   constexpr int C = CB * CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
   PostSmem<CB>& sm = *reinterpret_cast<PostSmem<CB>*>(smraw);
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const double* G = Gf + (size_t)bc.b * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.u.slots;
   thomas_init<CB>(sm.th);
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
   __shared__ double red[80];
   __shared__ int flag;
   const int t = threadIdx.x;
-  const size_t s = bofs(blockIdx.x, C) + t;
+  const size_t s = bofs((int)(blockIdx.x + g.b0), C) + t;
   double rv = r[s];
   if (!init) {
     const double alpha = st->alpha;
@@ -436,49 +436,49 @@ void init_kernel_attributes() {
 
 void launch_coefficients(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                          double* coef, cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_coefficients<8><<<(unsigned)g.nb, 512, 0, s>>>(g, kappa, dmask, coef, M);
-  else k_coefficients<4><<<(unsigned)g.nb, 64, 0, s>>>(g, kappa, dmask, coef, M);
+  const int64_t M = g.mst;
+  if (cb == 8) k_coefficients<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, coef, M);
+  else k_coefficients<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, coef, M);
 }
 void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
                  int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_init<8><<<(unsigned)g.nb, 512, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
-  else k_init<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
+  const int64_t M = g.mst;
+  if (cb == 8) k_init<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
+  else k_init<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
 }
 void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_search<8><<<(unsigned)g.nb, kStencilThreads, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
-  else k_search<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  const int64_t M = g.mst;
+  if (cb == 8) k_search<8><<<(unsigned)g.nbo, kStencilThreads, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  else k_search<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_update<8><<<(unsigned)g.nb, Thomas<8>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
-  else k_update<4><<<(unsigned)g.nb, Thomas<4>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
+  const int64_t M = g.mst;
+  if (cb == 8) k_update<8><<<(unsigned)g.nbo, Thomas<8>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
+  else k_update<4><<<(unsigned)g.nbo, Thomas<4>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
 }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_restrict<8><<<(unsigned)g.nb, kStencilThreads, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
-  else k_restrict<4><<<(unsigned)g.nb, 64, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
+  const int64_t M = g.mst;
+  if (cb == 8) k_restrict<8><<<(unsigned)g.nbo, kStencilThreads, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
+  else k_restrict<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s) {
-  const int64_t M = g.nx * g.ny * g.nz;
-  if (cb == 8) k_post<8><<<(unsigned)g.nb, Thomas<8>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
-  else k_post<4><<<(unsigned)g.nb, Thomas<4>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  const int64_t M = g.mst;
+  if (cb == 8) k_post<8><<<(unsigned)g.nbo, Thomas<8>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  else k_post<4><<<(unsigned)g.nbo, Thomas<4>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, cudaStream_t s) {
-  if (cb == 8) k_jacobi_step<8><<<(unsigned)g.nb, 512, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
-  else k_jacobi_step<4><<<(unsigned)g.nb, 64, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
+  if (cb == 8) k_jacobi_step<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
+  else k_jacobi_step<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
 }
 
 }  // namespace tmg

@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
   double* ty = tx + C;             // C
   double* tzb = ty + C;            // C  T to the cell one plane below (0 for lk=0)
   __shared__ double red[64];
-  const BrickCoord bc = brick_coord(g, blockIdx.x);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_tile<CB, true>(kappa, kt, g, bc);
   __syncthreads();
   tile_faces<CB>(kt, fx, fy, fz, g, bc);
@@ -123,10 +123,10 @@ void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, cons
   const size_t smem = thomas_smem_bytes(cb);
   if (cb == 8) {
     cudaFuncSetAttribute(k_thomas_factor<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<8><<<(unsigned)g.nb, 512, smem, s>>>(g, kappa, dmask, G, status);
+    k_thomas_factor<8><<<(unsigned)g.nbo, 512, smem, s>>>(g, kappa, dmask, G, status);
   } else {
     cudaFuncSetAttribute(k_thomas_factor<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<4><<<(unsigned)g.nb, 64, smem, s>>>(g, kappa, dmask, G, status);
+    k_thomas_factor<4><<<(unsigned)g.nbo, 64, smem, s>>>(g, kappa, dmask, G, status);
   }
 }
 

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   double* ys = xs + K * (C + 4);      // K*(C+4)
   __shared__ int okflag;
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
-  const int64_t b = blockIdx.x;
+  const int64_t b = blockIdx.x + g.b0;
   kt[t] = kappa[b * C + t];
   __syncthreads();
   // interior-face transmissibilities (coarse_space.cpp:264-274)
@@ -411,11 +411,11 @@ void launch_local_basis(const GridParams& g, int cb, const double* kappa, double
   const size_t smem = local_basis_smem(cb, 8);
   if (cb == 8) {
     cudaFuncSetAttribute(k_local_basis<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_local_basis<8, 8><<<(unsigned)g.nb, 512, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+    k_local_basis<8, 8><<<(unsigned)g.nbo, 512, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
                                                          max_outer);
   } else {
     cudaFuncSetAttribute(k_local_basis<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_local_basis<4, 8><<<(unsigned)g.nb, 64, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+    k_local_basis<4, 8><<<(unsigned)g.nbo, 64, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
                                                         max_outer);
   }
 }
