@@ -89,6 +89,31 @@ typedef struct {
  * on non-divisible axes) and allocates the context on CUDA device `device`. */
 int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out);
 void tmg_destroy(tmg_ctx* ctx);
+
+/* Partitioned solves; no reference counterpart (the
+ * reference is shared-memory only). The grid is split along z into slabs of
+ * whole cc-element layers (the slab count must divide ncc[2]); a slab keeps
+ * one ghost brick layer per neighbour, refreshed by halo exchanges, and the
+ * CG dot products / the coarse-coarse right-hand side are reduced across
+ * slabs. Iteration counts match the single-slab solve (the smoother blocks
+ * never straddle slabs); dot products differ only in summation order.
+ *
+ * tmg_create_slabs: `nslabs` slabs in one process on one device, exchanged
+ *   by device copies (the partitioned data path on a single GPU). Host arrays
+ *   stay global.
+ * tmg_create_dist: slab `rank` of `nranks`, one process per GPU, exchanges
+ *   and reductions over NCCL. `nccl_id` = the bytes of tmg_nccl_unique_id()
+ *   made on rank 0 and broadcast by the caller. Every host array passed to
+ *   this context is the rank's own slab: cells x-fastest with z in
+ *   [out[0], out[1]) of tmg_partition(). */
+int tmg_create_slabs(const tmg_grid* grid, int device, int nslabs, tmg_ctx** out);
+int tmg_nccl_unique_id(void* id, int bytes); /* bytes >= 128 */
+int tmg_create_dist(const tmg_grid* grid, int device, int rank, int nranks, const void* nccl_id,
+                    tmg_ctx** out);
+/* Host-only: slab `rank` of `nranks`. out[10] = {first fine z, end fine z,
+ * first brick, bricks, first cc element, cc elements, first x-fastest cell,
+ * cells, has neighbour below, has neighbour above}. */
+int tmg_partition(const tmg_grid* grid, int nranks, int rank, int64_t* out);
 /* Message of the last failed call on this context (or of tmg_create when ctx
  * is NULL). */
 const char* tmg_last_error(const tmg_ctx* ctx);

@@ -1,15 +1,32 @@
 // C-ABI implementation: context, set-up orchestration and the PCG driver.
 // See include/topmg_b200.h for the reference interface each entry replaces.
+//
+// A context holds one or more z-slabs of the grid:
+//  * tmg_create            one slab = the whole grid (single GPU);
+//  * tmg_create_slabs      S slabs in this process on one GPU (the partitioned
+//                          path with in-process ghost copies — how the
+//                          multi-GPU data path is exercised on one device);
+//  * tmg_create_dist       one slab per process/GPU, ghosts and reductions
+//                          over NCCL (NVLink/NVSwitch).
+// A slab owns whole z-layers of cc elements. Its device arrays are windows of
+// the global brick-layout arrays: the own bricks plus one ghost brick layer
+// per neighbouring slab, addressed through "virtual global" base pointers so
+// the kernels index global bricks unchanged. Ghost layers are contiguous
+// (bricks are z-slowest), so a halo exchange is one send/recv (or one device
+// copy) per neighbour and array, with no packing.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
+
+#include <nccl.h>
 
 #include "../../include/topmg_b200.h"
 #include "kernels.h"
@@ -22,25 +39,44 @@ thread_local std::string g_create_error;
 struct Fail {
   int code;
 };
+
+// Partition of the cc-element z-layers over `total` slabs.
+struct Part {
+  int64_t cz0, cz1;  // coarse-cell z layers [cz0, cz1)
+  int64_t b0, nbo, e0, neo;
+  int lo, hi;        // ghost layers below / above
+};
+
+Part partition(const GridParams& g, int slab, int total) {
+  Part p{};
+  const int64_t per = g.ncz / total;  // cc layers per slab
+  const int64_t ccz0 = per * slab, ccz1 = per * (slab + 1);
+  p.cz0 = ccz0 * g.sd;
+  p.cz1 = ccz1 * g.sd;
+  const int64_t L = g.nbx * g.nby, Le = g.ncx * g.ncy;
+  p.b0 = p.cz0 * L;
+  p.nbo = (p.cz1 - p.cz0) * L;
+  p.e0 = ccz0 * Le;
+  p.neo = (ccz1 - ccz0) * Le;
+  p.lo = slab > 0;
+  p.hi = slab + 1 < total;
+  return p;
+}
 }  // namespace
 
-struct tmg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  tmg_grid grid{};
+struct Slab {
+  int id = 0;  // global slab index (= rank for NCCL contexts)
   GridParams g{};
-  int cb = 0;
-  int64_t M = 0;
-  std::string err;
-  // problem
+  int lo = 0, hi = 0;
+  int64_t L = 0, Le = 0;      // bricks / cc elements per z-layer
+  int64_t bs0 = 0, nbs = 0;   // stored bricks (incl. ghost layers)
+  int64_t es0 = 0, nes = 0;   // stored cc elements (incl. ghost layers)
+  int64_t xoff = 0, xcells = 0;  // x-fastest cells of the slab: global offset, count
+  // problem (virtual global pointers)
   double* kappa = nullptr;
-  double* coef = nullptr;  // 4 x M operator coefficients (Tx+, Ty+, Tz+, diag)
+  double* coef = nullptr;  // 4 x mst operator coefficients (Tx+, Ty+, Tz+, diag)
   uint8_t* dmask = nullptr;
-  bool have_problem = false;
-  std::vector<Patch> patches;
   // preconditioner
-  int kind = -1;
-  bool have_setup = false;
   double* dinv = nullptr;
   double* phi = nullptr;
   double* evals = nullptr;
@@ -51,27 +87,51 @@ struct tmg_ctx {
   double* Rcc = nullptr;
   double* cc_evals = nullptr;
   double* Winv = nullptr;
-  double* Acc = nullptr;   // dense A_cc^-1 (set-up only)
-  double* AccT = nullptr;  // its lower 64x64 tiles (per-cycle GEMV)
-  double* symvP = nullptr; // GEMV partials
-  int64_t n_cc = 0;
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
          *r1 = nullptr, *stage = nullptr;
   double* pbuf[2] = {nullptr, nullptr};  // ping-pong search directions
-  double *rc = nullptr, *rc0 = nullptr, *rcc = nullptr, *ecc = nullptr, *ec = nullptr,
-         *rc1 = nullptr, *tc = nullptr;
+  double *rc = nullptr, *rc0 = nullptr, *ec = nullptr, *rc1 = nullptr, *tc = nullptr;
   PcgState* st = nullptr;
   double* partials = nullptr;
   double* history = nullptr;
-  int hist_cap = 0;
   int* d_status = nullptr;
   unsigned long long* d_count = nullptr;
+};
+
+struct tmg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  tmg_grid grid{};
+  GridParams g{};  // global grid (b0 = 0, nbo = nb, ...)
+  int cb = 0;
+  int64_t M = 0;   // global cells
+  std::string err;
+  // partition
+  int total = 1;                 // slabs over all processes
+  ncclComm_t comm = nullptr;     // NCCL contexts only
+  std::vector<Slab> slabs;       // slabs held by this process
+  bool dist() const { return total > 1; }
+  bool nccl() const { return comm != nullptr; }
+  // problem
+  bool have_problem = false;
+  std::vector<Patch> patches;
+  // preconditioner
+  int kind = -1;
+  bool have_setup = false;
+  int lc = 4, lcc = 8;
+  int64_t n_cc = 0;
+  double* AccT = nullptr;   // single slab: lower 64x64 tiles of A_cc^-1
+  double* symvP = nullptr;  // single slab: GEMV partials
+  double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
+  double *rcc = nullptr, *ecc = nullptr;  // full-length cc vectors (one per process)
+  int hist_cap = 0;
   PcgState* h_state = nullptr;  // pinned, 2 slots
   // graph
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
   int64_t graph_kernels = 0;  // kernel nodes in one captured chunk
+  int64_t kcount = 0;         // kernels enqueued (running count)
   int64_t launches = 0;       // kernels enqueued by solves (incl. graph nodes)
   int64_t bytes = 0;
   std::vector<void*> allocs;
@@ -79,6 +139,7 @@ struct tmg_ctx {
   // nothing); byte size of every live or pooled buffer
   std::vector<std::pair<void*, size_t>> pool;
   std::unordered_map<void*, size_t> sizes;
+  std::unordered_map<void*, void*> virt;  // windowed pointer -> allocation
   double setup_seconds = 0.0;
 };
 
@@ -105,6 +166,16 @@ int set_err(tmg_ctx* c, int code, const char* fmt, ...) {
     }                                                                                     \
   } while (0)
 
+#define NK(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      set_err(c, TMG_ECUDA, "NCCL error %s at %s:%d", ncclGetErrorString(r_), __FILE__, \
+              __LINE__);                                                                \
+      throw Fail{TMG_ECUDA};                                                            \
+    }                                                                                   \
+  } while (0)
+
 template <typename T>
 T* dalloc(tmg_ctx* c, int64_t n) {
   void* p = nullptr;
@@ -123,24 +194,66 @@ T* dalloc(tmg_ctx* c, int64_t n) {
   return (T*)p;
 }
 
+// windowed allocation: `units` stored, first stored global unit `first`
+template <typename T>
+T* walloc(tmg_ctx* c, int64_t units, int64_t per, int64_t first) {
+  T* a = dalloc<T>(c, units * per);
+  T* v = a - first * per;
+  c->virt[(void*)v] = (void*)a;
+  return v;
+}
+template <typename T>
+T* ghosted(tmg_ctx* c, const Slab& s, int64_t per) { return walloc<T>(c, s.nbs, per, s.bs0); }
+template <typename T>
+T* owned(tmg_ctx* c, const Slab& s, int64_t per) { return walloc<T>(c, s.g.nbo, per, s.g.b0); }
+template <typename T>
+T* owned_e(tmg_ctx* c, const Slab& s, int64_t per) { return walloc<T>(c, s.g.neo, per, s.g.e0); }
+template <typename T>
+T* ghosted_e(tmg_ctx* c, const Slab& s, int64_t per) { return walloc<T>(c, s.nes, per, s.es0); }
+
 // release to the context's pool (freed for real in tmg_destroy)
 void dfree(tmg_ctx* c, void* p) {
   if (!p) return;
+  auto v = c->virt.find(p);
+  if (v != c->virt.end()) {
+    p = v->second;
+    c->virt.erase(v);
+  }
   auto it = std::find(c->allocs.begin(), c->allocs.end(), p);
   if (it == c->allocs.end()) return;
   c->allocs.erase(it);
   c->pool.emplace_back(p, c->sizes[p]);
 }
 
+template <typename T>
+void dfree_null(tmg_ctx* c, T*& p) {
+  dfree(c, (void*)p);
+  p = nullptr;
+}
+
 void free_setup(tmg_ctx* c) {
-  for (void** pp : {(void**)&c->dinv, (void**)&c->phi, (void**)&c->evals, (void**)&c->eig_iters,
-                    (void**)&c->Gf, (void**)&c->Ac, (void**)&c->Bc, (void**)&c->Rcc,
-                    (void**)&c->cc_evals, (void**)&c->Winv, (void**)&c->Acc, (void**)&c->AccT, (void**)&c->symvP, (void**)&c->rc,
-                    (void**)&c->rc0, (void**)&c->rcc, (void**)&c->ecc, (void**)&c->ec,
-                    (void**)&c->rc1, (void**)&c->tc}) {
-    dfree(c, *pp);
-    *pp = nullptr;
+  for (Slab& s : c->slabs) {
+    dfree_null(c, s.dinv);
+    dfree_null(c, s.phi);
+    dfree_null(c, s.evals);
+    dfree_null(c, s.eig_iters);
+    dfree_null(c, s.Gf);
+    dfree_null(c, s.Ac);
+    dfree_null(c, s.Bc);
+    dfree_null(c, s.Rcc);
+    dfree_null(c, s.cc_evals);
+    dfree_null(c, s.Winv);
+    dfree_null(c, s.rc);
+    dfree_null(c, s.rc0);
+    dfree_null(c, s.ec);
+    dfree_null(c, s.rc1);
+    dfree_null(c, s.tc);
   }
+  dfree_null(c, c->AccT);
+  dfree_null(c, c->symvP);
+  dfree_null(c, c->Ainv);
+  dfree_null(c, c->rcc);
+  dfree_null(c, c->ecc);
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
@@ -183,65 +296,241 @@ int validate_patches(tmg_ctx* c, const tmg_patch* p, int np) {
   return TMG_OK;
 }
 
-// device kappa (brick layout) is in c->kappa; build mask, count faces
+// cells of the host arrays this context reads/writes (NCCL: the own slab)
+int64_t host_cells(const tmg_ctx* c) { return c->nccl() ? c->slabs[0].xcells : c->M; }
+
+int64_t cells_per_brick(const tmg_ctx* c) { return (int64_t)c->cb * c->cb * c->cb; }
+
+// ------------------------------------------------------- ghost exchanges
+//
+// Fill the ghost layers of a windowed array: unit = brick (elem = false) or
+// cc element (elem = true), `bytes` per unit. get(s) returns slab s's
+// windowed base pointer.
+void exchange(tmg_ctx* c, const std::function<void*(Slab&)>& get, size_t bytes, bool elem) {
+  if (!c->dist()) return;
+  cudaStream_t st = c->stream;
+  auto unit = [&](Slab& s, int64_t u) { return (char*)get(s) + (int64_t)bytes * u; };
+  if (!c->nccl()) {
+    for (size_t k = 0; k < c->slabs.size(); ++k) {
+      Slab& s = c->slabs[k];
+      const int64_t u0 = elem ? s.g.e0 : s.g.b0, nu = elem ? s.g.neo : s.g.nbo;
+      const int64_t Lu = elem ? s.Le : s.L;
+      const size_t lb = (size_t)Lu * bytes;
+      if (s.lo)
+        CK(cudaMemcpyAsync(unit(s, u0 - Lu), unit(c->slabs[k - 1], u0 - Lu), lb,
+                           cudaMemcpyDeviceToDevice, st));
+      if (s.hi)
+        CK(cudaMemcpyAsync(unit(s, u0 + nu), unit(c->slabs[k + 1], u0 + nu), lb,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    return;
+  }
+  Slab& s = c->slabs[0];
+  const int64_t u0 = elem ? s.g.e0 : s.g.b0, nu = elem ? s.g.neo : s.g.nbo;
+  const int64_t Lu = elem ? s.Le : s.L;
+  const size_t lb = (size_t)Lu * bytes;
+  NK(ncclGroupStart());
+  if (s.lo) {
+    NK(ncclSend(unit(s, u0), lb, ncclChar, s.id - 1, c->comm, st));
+    NK(ncclRecv(unit(s, u0 - Lu), lb, ncclChar, s.id - 1, c->comm, st));
+  }
+  if (s.hi) {
+    NK(ncclSend(unit(s, u0 + nu - Lu), lb, ncclChar, s.id + 1, c->comm, st));
+    NK(ncclRecv(unit(s, u0 + nu), lb, ncclChar, s.id + 1, c->comm, st));
+  }
+  NK(ncclGroupEnd());
+}
+
+#define XCH(member, per_unit_bytes, elem) \
+  exchange(c, [&](Slab& s_) { return (void*)s_.member; }, (per_unit_bytes), (elem))
+
+void exchange_coef(tmg_ctx* c) {
+  const int64_t C = cells_per_brick(c);
+  for (int k = 0; k < 4; ++k)
+    exchange(c, [&](Slab& s) { return (void*)(s.coef + (size_t)k * s.g.mst); },
+             sizeof(double) * (size_t)C, false);
+}
+
+// cross-slab sum of PcgState::loc[which..] and the scalar update on every slab
+void reduce_finalize(tmg_ctx* c, int which, int init) {
+  const int nv = (which == kRedInit || which == kRedJacobi) ? 2 : 1;
+  if (c->nccl())
+    NK(ncclAllReduce(c->slabs[0].st->loc + which, c->slabs[0].st->loc + which, nv, ncclDouble,
+                     ncclSum, c->comm, c->stream));
+  FinArgs a{};
+  a.ns = (int)c->slabs.size();
+  for (int j = 0; j < a.ns; ++j) {
+    a.st[j] = c->slabs[j].st;
+    a.hist[j] = c->slabs[j].history;
+  }
+  launch_finalize(a, which, init, c->stream);
+  ++c->kcount;
+}
+
+// ------------------------------------------------------ host <-> device
+void upload(tmg_ctx* c, const double* host, const std::function<double*(Slab&)>& dst) {
+  for (Slab& s : c->slabs) {
+    const double* h = host + (c->nccl() ? 0 : s.xoff);
+    CK(cudaMemcpyAsync(s.stage, h, sizeof(double) * (size_t)s.xcells, cudaMemcpyHostToDevice,
+                       c->stream));
+    launch_to_brick(s.g, c->cb, s.stage, dst(s), c->stream);
+    CK(cudaGetLastError());
+  }
+}
+
+void download(tmg_ctx* c, const std::function<double*(Slab&)>& src, double* host) {
+  for (Slab& s : c->slabs) {
+    launch_from_brick(s.g, c->cb, src(s), s.stage, c->stream);
+    CK(cudaGetLastError());
+    double* h = host + (c->nccl() ? 0 : s.xoff);
+    CK(cudaMemcpyAsync(h, s.stage, sizeof(double) * (size_t)s.xcells, cudaMemcpyDeviceToHost,
+                       c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+#define UP(host, member) upload(c, (host), [&](Slab& s_) { return s_.member; })
+#define DOWN(member, host) download(c, [&](Slab& s_) { return s_.member; }, (host))
+
+// device kappa (brick layout) is in s.kappa: ghosts, Dirichlet mask, faces,
+// coefficients
 int finish_problem(tmg_ctx* c) {
   return guard(c, [&] {
-    CK(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), c->stream));
-    launch_boundary(c->g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx, c->grid.ly,
-                    c->grid.lz, c->kappa, nullptr, c->dmask, nullptr, c->d_count, c->stream);
-    CK(cudaGetLastError());
+    const int64_t C = cells_per_brick(c);
+    XCH(kappa, sizeof(double) * C, false);
+    for (Slab& s : c->slabs) {
+      CK(cudaMemsetAsync(s.d_count, 0, sizeof(unsigned long long), c->stream));
+      launch_boundary(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                      c->grid.ly, c->grid.lz, s.kappa, nullptr, s.dmask, nullptr, s.d_count,
+                      c->stream);
+      CK(cudaGetLastError());
+    }
+    if (c->nccl())
+      NK(ncclAllReduce(c->slabs[0].d_count, c->slabs[0].d_count, 1, ncclUint64, ncclSum, c->comm,
+                       c->stream));
     unsigned long long cnt = 0;
-    CK(cudaMemcpyAsync(&cnt, c->d_count, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    for (Slab& s : c->slabs) {
+      unsigned long long v = 0;
+      CK(cudaMemcpyAsync(&v, s.d_count, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cnt += v;
+    }
     if (cnt == 0) {
       set_err(c, TMG_ECONFIG,
               "assemble_system: no Dirichlet face on the boundary, the system would be singular");
       throw Fail{TMG_ECONFIG};
     }
-    launch_coefficients(c->g, c->cb, c->kappa, c->dmask, c->coef, c->stream);
-    CK(cudaGetLastError());
+    XCH(dmask, C, false);
+    for (Slab& s : c->slabs) {
+      launch_coefficients(s.g, c->cb, s.kappa, s.dmask, s.coef, c->stream);
+      CK(cudaGetLastError());
+    }
+    exchange_coef(c);
     c->have_problem = true;
     free_setup(c);
   });
 }
 
-void upload_global(tmg_ctx* c, const double* host, double* dev_brick) {
-  CK(cudaMemcpyAsync(c->stage, host, sizeof(double) * (size_t)c->M, cudaMemcpyHostToDevice,
-                     c->stream));
-  launch_to_brick(c->g, c->cb, c->stage, dev_brick, c->stream);
-  CK(cudaGetLastError());
-}
-
-void download_global(tmg_ctx* c, const double* dev_brick, double* host) {
-  launch_from_brick(c->g, c->cb, dev_brick, c->stage, c->stream);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(host, c->stage, sizeof(double) * (size_t)c->M, cudaMemcpyDeviceToHost,
-                     c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-}
-
 // ---------------------------------------------------------------- V-cycle
-void enqueue_vcycle(tmg_ctx* c, int init, PcgState* st, cudaStream_t s, const double* p) {
-  const GridParams& g = c->g;
-  launch_update(g, c->cb, c->coef, c->Gf, c->x, p, c->q, c->r, c->r1, st, c->partials,
-                c->history, init, s);
-  launch_restrict(g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, st, s);
-  launch_coarse_cycle(g, &st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0,
-                      c->rcc, c->ecc, c->rc1, c->tc, c->ec, s);
-  launch_post(g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, st,
-              c->partials, init, s);
+#define KL(n_kernels, call)     \
+  do {                          \
+    call;                       \
+    c->kcount += (n_kernels);   \
+  } while (0)
+
+// single slab: the fused path (device-side scalars, symmetric tiled A_cc GEMV)
+void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
+  Slab& s = c->slabs[0];
+  const GridParams& g = s.g;
+  cudaStream_t st = c->stream;
+  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.st, s.partials,
+                      s.history, init, st));
+  KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  KL(7, launch_coarse_cycle(g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc,
+                            s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, st));
+  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
+                    st));
+}
+
+// partitioned: the same kernels per slab, ghost exchanges and cross-slab
+// reductions between them (SURVEY.md §8(e) "collectives per PCG iteration")
+void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
+  cudaStream_t st = c->stream;
+  const int64_t C = cells_per_brick(c);
+  const size_t cvec = sizeof(double) * (size_t)c->lc;
+  for (Slab& s : c->slabs)
+    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.st,
+                        s.partials, s.history, init, st));
+  if (!init) reduce_finalize(c, kRedUpdate, 0);
+  XCH(r1, sizeof(double) * C, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  // coarse level (solver.cpp:292-319)
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.rc, nullptr, s.rc0, st));
+  XCH(rc0, cvec, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_restrict(s.g, &s.st->done, s.Ac, s.Rcc, s.rc, s.rc0, c->rcc, st));
+  if (c->nccl()) {
+    const Slab& s = c->slabs[0];
+    const int64_t own = s.g.neo * c->lcc;
+    NK(ncclAllGather(c->rcc + s.g.e0 * c->lcc, c->rcc, (size_t)own, ncclDouble, c->comm, st));
+  }
+  for (Slab& s : c->slabs)
+    KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
+                           c->rcc, c->ecc, st));
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_prolong(s.g, &s.st->done, s.Rcc, s.rc0, c->ecc, s.rc1, st));
+  XCH(rc1, cvec, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_resid(s.g, &s.st->done, s.Ac, s.rc, s.rc1, s.tc, st));
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.tc, s.rc1, s.ec, st));
+  XCH(ec, cvec, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
+                      init, st));
+  reduce_finalize(c, kRedPost, init);
+  XCH(z, sizeof(double) * C, false);
+}
+
+void enqueue_jacobi(tmg_ctx* c, int init, int par_new) {
+  const int64_t C = cells_per_brick(c);
+  for (Slab& s : c->slabs)
+    KL(1, launch_jacobi_step(s.g, c->cb, c->kind == TMG_PRECOND_JACOBI ? s.dinv : nullptr, s.x,
+                             s.pbuf[par_new], s.q, s.r, s.z, s.st, s.partials, s.history, init,
+                             c->stream));
+  if (c->dist()) {
+    reduce_finalize(c, kRedJacobi, init);
+    XCH(z, sizeof(double) * C, false);
+  }
+}
+
+// first application (x0 residual already in r): z = M^-1 r, rho = r.z
+void enqueue_precond_init(tmg_ctx* c) {
+  if (c->kind == TMG_PRECOND_MMG) {
+    if (c->dist()) enqueue_vcycle_dist(c, 1, 0);
+    else enqueue_vcycle_single(c, 1, c->slabs[0].pbuf[0]);
+  } else {
+    enqueue_jacobi(c, 1, 0);
+  }
 }
 
 // Iteration with parity `par`: reads p from pbuf[par], writes pbuf[par ^ 1].
-void enqueue_iteration(tmg_ctx* c, cudaStream_t s, int par) {
-  const double* pold = c->pbuf[par];
-  double* pnew = c->pbuf[par ^ 1];
-  launch_search(c->g, c->cb, c->coef, c->z, pold, pnew, c->q, c->st, c->partials, s);
+void enqueue_iteration(tmg_ctx* c, int par) {
+  const int64_t C = cells_per_brick(c);
+  for (Slab& s : c->slabs)
+    KL(1, launch_search(s.g, c->cb, s.coef, s.z, s.pbuf[par], s.pbuf[par ^ 1], s.q, s.st,
+                        s.partials, c->stream));
+  if (c->dist()) {
+    reduce_finalize(c, kRedSearch, 0);
+    exchange(c, [&](Slab& s) { return (void*)s.pbuf[par ^ 1]; }, sizeof(double) * C, false);
+  }
   if (c->kind == TMG_PRECOND_MMG) {
-    enqueue_vcycle(c, 0, c->st, s, pnew);
+    if (c->dist()) enqueue_vcycle_dist(c, 0, par ^ 1);
+    else enqueue_vcycle_single(c, 0, c->slabs[0].pbuf[par ^ 1]);
   } else {
-    launch_jacobi_step(c->g, c->cb, c->kind == TMG_PRECOND_JACOBI ? c->dinv : nullptr, c->x, pnew,
-                       c->q, c->r, c->z, c->st, c->partials, c->history, 0, s);
+    enqueue_jacobi(c, 0, par ^ 1);
   }
 }
 
@@ -251,13 +540,13 @@ void build_graph(tmg_ctx* c, int chunk) {
     c->graph = nullptr;
   }
   cudaGraph_t graph;
+  const int64_t k0 = c->kcount;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   // chunk is even so every graph launch starts from pbuf[0]
-  for (int i = 0; i < chunk; ++i) enqueue_iteration(c, c->stream, i & 1);
+  for (int i = 0; i < chunk; ++i) enqueue_iteration(c, i & 1);
   CK(cudaStreamEndCapture(c->stream, &graph));
-  size_t nodes = 0;
-  CK(cudaGraphGetNodes(graph, nullptr, &nodes));
-  c->graph_kernels = (int64_t)nodes;
+  c->graph_kernels = c->kcount - k0;
+  c->kcount = k0;
   CK(cudaGraphInstantiate(&c->graph, graph, 0));
   cudaGraphDestroy(graph);
   c->graph_chunk = chunk;
@@ -265,14 +554,25 @@ void build_graph(tmg_ctx* c, int chunk) {
 
 void ensure_history(tmg_ctx* c, int maxit) {
   if (maxit <= c->hist_cap) return;
-  dfree(c, c->history);
-  c->history = dalloc<double>(c, maxit);
+  for (Slab& s : c->slabs) {
+    dfree_null(c, s.history);
+    s.history = dalloc<double>(c, maxit);
+  }
   c->hist_cap = maxit;
-  // the captured graph holds the history pointer
+  // the captured graph holds the history pointers
   if (c->graph) build_graph(c, c->graph_chunk);
 }
 
-// Runs the device solve on resident c->b (and c->x if use_x0).
+void init_states(tmg_ctx* c, double rtol, int maxit) {
+  PcgState init{};
+  init.rtol = rtol;
+  init.maxit = maxit;
+  init.hist_cap = c->hist_cap;
+  for (Slab& s : c->slabs)
+    CK(cudaMemcpyAsync(s.st, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+}
+
+// Runs the device solve on resident b (and x if use_x0).
 void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* rep,
                   double* ms_total, int* counts) {
   if (!c->have_setup) {
@@ -280,17 +580,14 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     throw Fail{TMG_EARG};
   }
   ensure_history(c, std::max(maxit, 1));
-  PcgState init{};
-  init.rtol = rtol;
-  init.maxit = maxit;
-  init.hist_cap = c->hist_cap;
+  const int64_t C = cells_per_brick(c);
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
-  CK(cudaMemcpyAsync(c->st, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
-  const bool prof = ms_total != nullptr;
-  std::vector<cudaEvent_t> evs;
+  init_states(c, rtol, maxit);
+  const bool prof = ms_total != nullptr && !c->dist();
+  Slab& s0 = c->slabs[0];
   auto timed = [&](int slot, const std::function<void()>& launch) {
     if (!prof) {
       launch();
@@ -310,33 +607,32 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   };
+  const int64_t k_before = c->kcount;
+  if (use_x0) XCH(x, sizeof(double) * C, false);
   timed(8, [&] {
-    launch_init(c->g, c->cb, c->coef, c->b, c->x, use_x0, c->r, c->st, c->partials,
-                c->stream);
+    for (Slab& s : c->slabs)
+      KL(1, launch_init(s.g, c->cb, s.coef, s.b, s.x, use_x0, s.r, s.st, s.partials, c->stream));
+    if (c->dist()) reduce_finalize(c, kRedInit, 0);
   });
-  c->launches += 1;                                          // init
-  c->launches += c->kind == TMG_PRECOND_MMG ? c->graph_kernels / c->graph_chunk - 1 : 1;
-  if (c->kind == TMG_PRECOND_MMG) {
-    if (!prof) {
-      enqueue_vcycle(c, 1, c->st, c->stream, c->pbuf[0]);
-    } else {
-      timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, c->p, c->q, c->r, c->r1, c->st, c->partials, c->history, 1, c->stream); });
-      timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-      timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
-      timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 1, c->stream); });
-    }
+  if (!prof) {
+    enqueue_precond_init(c);
+  } else if (c->kind == TMG_PRECOND_MMG) {
+    Slab& s = s0;
+    const GridParams& g = s.g;
+    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
+    timed(2, [&] { KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
+    timed(3, [&] { KL(7, launch_coarse_cycle(g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream)); });
+    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
-    timed(7, [&] {
-      launch_jacobi_step(c->g, c->cb, c->kind == TMG_PRECOND_JACOBI ? c->dinv : nullptr, c->x,
-                         c->p, c->q, c->r, c->z, c->st, c->partials, c->history, 1, c->stream);
-    });
+    timed(7, [&] { enqueue_jacobi(c, 1, 0); });
   }
   CK(cudaGetLastError());
+  c->launches += c->kcount - k_before;
   PcgState* hs = c->h_state;
   if (!prof) {
     // chunked graph launches; the next chunk is enqueued before the previous
     // one's state is polled, so the GPU never idles on the host.
-    CK(cudaMemcpyAsync(&hs[0], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&hs[0], s0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (!hs[0].done && maxit > 0) {
       cudaEvent_t ev[2];
@@ -346,7 +642,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       auto launch_chunk = [&](int sl) {
         CK(cudaGraphLaunch(c->graph, c->stream));
         c->launches += c->graph_kernels;
-        CK(cudaMemcpyAsync(&hs[sl], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&hs[sl], s0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaEventRecord(ev[sl], c->stream));
         launched += c->graph_chunk;
       };
@@ -364,30 +660,29 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       cudaEventDestroy(ev[1]);
     }
   } else {
-    CK(cudaMemcpy(&hs[0], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+    Slab& s = s0;
+    CK(cudaMemcpy(&hs[0], s.st, sizeof(PcgState), cudaMemcpyDeviceToHost));
     int guard_it = 0, par = 0;
     while (!hs[0].done && maxit > 0 && guard_it++ <= maxit) {
-      const double* pold = c->pbuf[par];
-      double* pnew = c->pbuf[par ^ 1];
+      const double* pold = s.pbuf[par];
+      double* pnew = s.pbuf[par ^ 1];
       par ^= 1;
-      timed(0, [&] { launch_search(c->g, c->cb, c->coef, c->z, pold, pnew, c->q, c->st, c->partials, c->stream); });
+      const int64_t kb = c->kcount;
+      timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
       if (c->kind == TMG_PRECOND_MMG) {
-        timed(1, [&] { launch_update(c->g, c->cb, c->coef, c->Gf, c->x, pnew, c->q, c->r, c->r1, c->st, c->partials, c->history, 0, c->stream); });
-        timed(2, [&] { launch_restrict(c->g, c->cb, c->coef, c->phi, c->r, c->r1, c->rc, c->st, c->stream); });
-        timed(3, [&] { launch_coarse_cycle(c->g, &c->st->done, c->Ac, c->Winv, c->Rcc, c->AccT, c->symvP, c->n_cc, c->rc, c->rc0, c->rcc, c->ecc, c->rc1, c->tc, c->ec, c->stream); });
-        timed(6, [&] { launch_post(c->g, c->cb, c->coef, c->phi, c->Gf, c->r, c->r1, c->ec, c->z, c->st, c->partials, 0, c->stream); });
+        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
+        timed(2, [&] { KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
+        timed(3, [&] { KL(7, launch_coarse_cycle(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream)); });
+        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
-        timed(7, [&] {
-          launch_jacobi_step(c->g, c->cb, c->kind == TMG_PRECOND_JACOBI ? c->dinv : nullptr,
-                             c->x, pnew, c->q, c->r, c->z, c->st, c->partials, c->history, 0,
-                             c->stream);
-        });
+        timed(7, [&] { enqueue_jacobi(c, 0, par); });
       }
-      CK(cudaMemcpy(&hs[0], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+      c->launches += c->kcount - kb;
+      CK(cudaMemcpy(&hs[0], s.st, sizeof(PcgState), cudaMemcpyDeviceToHost));
     }
   }
   CK(cudaEventRecord(e1, c->stream));
-  CK(cudaMemcpyAsync(&hs[0], c->st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&hs[0], s0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());
   float ms = 0.f;
@@ -397,7 +692,8 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   PcgState& f = hs[0];
   if (!f.done && maxit == 0) f.status = kStatusMaxIt;
   if (f.status == kStatusZeroRhs) {
-    CK(cudaMemsetAsync(c->x, 0, sizeof(double) * (size_t)c->M, c->stream));  // solver.cpp:506-513
+    for (Slab& s : c->slabs)  // solver.cpp:506-513
+      CK(cudaMemsetAsync(s.x + s.g.b0 * C, 0, sizeof(double) * (size_t)(s.g.nbo * C), c->stream));
   }
   if (rep) {
     rep->iterations = f.it;
@@ -419,19 +715,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   }
 }
 
-}  // namespace
-
-// =================================================================== C ABI
-
-extern "C" {
-
-const char* tmg_last_error(const tmg_ctx* ctx) {
-  return ctx ? ctx->err.c_str() : g_create_error.c_str();
-}
-
-int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
-  if (!grid || !out) return set_err(nullptr, TMG_EARG, "tmg_create: null argument");
-  *out = nullptr;
+int check_grid(const tmg_grid* grid, int64_t* cpc_out) {
   const tmg_grid& G = *grid;
   if (G.nx <= 0 || G.ny <= 0 || G.nz <= 0)
     return set_err(nullptr, TMG_ECONFIG, "GridSpec: cell counts must be positive");
@@ -454,14 +738,14 @@ int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
     return set_err(nullptr, TMG_ENOTSUP,
                    "GPU path builds cubic coarse cells of 4^3 or 8^3 fine cells (got %lldx%lldx%lld)",
                    (long long)cpc[0], (long long)cpc[1], (long long)cpc[2]);
-  tmg_ctx* c = new tmg_ctx;
-  c->grid = G;
-  c->device = device;
-  c->cb = (int)cpc[0];
-  c->M = G.nx * G.ny * G.nz;
-  GridParams& g = c->g;
+  *cpc_out = cpc[0];
+  return TMG_OK;
+}
+
+GridParams global_params(const tmg_grid& G, int cb) {
+  GridParams g{};
   g.nx = G.nx; g.ny = G.ny; g.nz = G.nz;
-  g.nbx = G.nx / c->cb; g.nby = G.ny / c->cb; g.nbz = G.nz / c->cb;
+  g.nbx = G.nx / cb; g.nby = G.ny / cb; g.nbz = G.nz / cb;
   g.nb = g.nbx * g.nby * g.nbz;
   g.ncx = G.ncc[0]; g.ncy = G.ncc[1]; g.ncz = G.ncc[2];
   g.ncc = g.ncx * g.ncy * g.ncz;
@@ -479,25 +763,96 @@ int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
   g.nbo = g.nb;
   g.e0 = 0;
   g.neo = g.ncc;
-  g.mst = c->M;
+  g.mst = G.nx * G.ny * G.nz;
   g.dist = 0;
-  const int rc = guard(c, [&] {
+  return g;
+}
+
+int check_partition(const tmg_grid* grid, int total) {
+  if (total < 1 || total > kMaxSlabs)
+    return set_err(nullptr, TMG_EARG, "partition: 1..%d slabs (got %d)", kMaxSlabs, total);
+  if (grid->ncc[2] % total != 0)
+    return set_err(nullptr, TMG_ECONFIG,
+                   "partition: %d slabs must divide the %lld cc-element layers along z", total,
+                   (long long)grid->ncc[2]);
+  return TMG_OK;
+}
+
+// create a context holding slabs [first, first + count) of `total`
+int create_impl(const tmg_grid* grid, int device, int first, int count, int total,
+                const void* nccl_id, tmg_ctx** out) {
+  if (!grid || !out) return set_err(nullptr, TMG_EARG, "tmg_create: null argument");
+  *out = nullptr;
+  int64_t cb = 0;
+  int rc = check_grid(grid, &cb);
+  if (rc) return rc;
+  rc = check_partition(grid, total);
+  if (rc) return rc;
+  if (count < 1 || first < 0 || first + count > total)
+    return set_err(nullptr, TMG_EARG, "partition: bad slab range %d+%d of %d", first, count, total);
+  tmg_ctx* c = new tmg_ctx;
+  c->grid = *grid;
+  c->device = device;
+  c->cb = (int)cb;
+  c->M = grid->nx * grid->ny * grid->nz;
+  c->g = global_params(*grid, c->cb);
+  c->total = total;
+  const int64_t C = cells_per_brick(c);
+  rc = guard(c, [&] {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     init_kernel_attributes();
-    c->kappa = dalloc<double>(c, c->M);
-    c->dmask = dalloc<uint8_t>(c, c->M);
-    c->coef = dalloc<double>(c, 4 * c->M);
-    for (double** v : {&c->b, &c->x, &c->r, &c->p, &c->q, &c->z, &c->r1, &c->stage})
-      *v = dalloc<double>(c, c->M);
-    c->pbuf[0] = c->p;
-    c->pbuf[1] = dalloc<double>(c, c->M);
-    c->st = dalloc<PcgState>(c, 1);
-    c->partials = dalloc<double>(c, 4 * g.nb + 64);
-    c->d_status = dalloc<int>(c, 4);
-    c->d_count = dalloc<unsigned long long>(c, 1);
-    CK(cudaMemset(c->st, 0, sizeof(PcgState)));
+    if (nccl_id) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof id);
+      NK(ncclCommInitRank(&c->comm, total, id, first));
+    }
+    c->slabs.resize((size_t)count);
+    for (int k = 0; k < count; ++k) {
+      Slab& s = c->slabs[(size_t)k];
+      s.id = first + k;
+      const Part p = partition(c->g, s.id, total);
+      s.g = c->g;
+      s.g.b0 = p.b0;
+      s.g.nbo = p.nbo;
+      s.g.e0 = p.e0;
+      s.g.neo = p.neo;
+      s.g.dist = total > 1;
+      s.lo = p.lo;
+      s.hi = p.hi;
+      s.L = c->g.nbx * c->g.nby;
+      s.Le = c->g.ncx * c->g.ncy;
+      s.bs0 = p.b0 - p.lo * s.L;
+      s.nbs = p.nbo + (p.lo + p.hi) * s.L;
+      s.es0 = p.e0 - p.lo * s.Le;
+      s.nes = p.neo + (p.lo + p.hi) * s.Le;
+      s.xoff = p.cz0 * c->cb * c->g.nx * c->g.ny;
+      s.xcells = (p.cz1 - p.cz0) * c->cb * c->g.nx * c->g.ny;
+      s.g.mst = s.nbs * C;
+      s.kappa = ghosted<double>(c, s, C);
+      s.dmask = ghosted<uint8_t>(c, s, C);
+      {
+        double* a = dalloc<double>(c, 4 * s.g.mst);
+        s.coef = a - s.bs0 * C;
+        c->virt[(void*)s.coef] = (void*)a;
+      }
+      for (double** v : {&s.b, &s.x, &s.r, &s.q, &s.z, &s.r1}) *v = ghosted<double>(c, s, C);
+      s.pbuf[0] = ghosted<double>(c, s, C);
+      s.pbuf[1] = ghosted<double>(c, s, C);
+      s.p = s.pbuf[0];
+      s.stage = dalloc<double>(c, s.xcells);
+      s.st = dalloc<PcgState>(c, 1);
+      s.partials = dalloc<double>(c, 4 * s.g.nbo + 64);
+      s.d_status = dalloc<int>(c, 4);
+      s.d_count = dalloc<unsigned long long>(c, 1);
+      CK(cudaMemset(s.st, 0, sizeof(PcgState)));
+      CK(cudaMemset(s.d_status, 0, 4 * sizeof(int)));
+      // ghost cells of vectors read before their first exchange stay finite
+      for (double* v : {s.b, s.x, s.r, s.q, s.z, s.r1, s.pbuf[0], s.pbuf[1], s.kappa})
+        CK(cudaMemset(v + s.bs0 * C, 0, sizeof(double) * (size_t)(s.nbs * C)));
+    }
     CK(cudaMallocHost(&c->h_state, 2 * sizeof(PcgState)));
+    CK(cudaDeviceSynchronize());
   });
   if (rc) {
     g_create_error = c->err;
@@ -508,10 +863,71 @@ int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
   return TMG_OK;
 }
 
+bool single(const tmg_ctx* c) { return !c->dist(); }
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* tmg_last_error(const tmg_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out) {
+  return create_impl(grid, device, 0, 1, 1, nullptr, out);
+}
+
+int tmg_create_slabs(const tmg_grid* grid, int device, int nslabs, tmg_ctx** out) {
+  return create_impl(grid, device, 0, nslabs, nslabs, nullptr, out);
+}
+
+int tmg_nccl_unique_id(void* id, int bytes) {
+  if (!id || bytes < (int)sizeof(ncclUniqueId))
+    return set_err(nullptr, TMG_EARG, "tmg_nccl_unique_id: need %d bytes", (int)sizeof(ncclUniqueId));
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess)
+    return set_err(nullptr, TMG_ECUDA, "ncclGetUniqueId failed");
+  std::memcpy(id, &u, sizeof u);
+  return TMG_OK;
+}
+
+int tmg_create_dist(const tmg_grid* grid, int device, int rank, int nranks, const void* nccl_id,
+                    tmg_ctx** out) {
+  if (nranks > 1 && !nccl_id) return set_err(nullptr, TMG_EARG, "tmg_create_dist: null NCCL id");
+  return create_impl(grid, device, rank, 1, nranks, nranks > 1 ? nccl_id : nullptr, out);
+}
+
+int tmg_partition(const tmg_grid* grid, int nranks, int rank, int64_t* out) {
+  if (!grid || !out) return set_err(nullptr, TMG_EARG, "tmg_partition: null argument");
+  int64_t cb = 0;
+  int rc = check_grid(grid, &cb);
+  if (rc) return rc;
+  rc = check_partition(grid, nranks);
+  if (rc) return rc;
+  if (rank < 0 || rank >= nranks)
+    return set_err(nullptr, TMG_EARG, "tmg_partition: bad rank %d of %d", rank, nranks);
+  const GridParams g = global_params(*grid, (int)cb);
+  const Part p = partition(g, rank, nranks);
+  out[0] = p.cz0 * cb;                          // first fine z layer
+  out[1] = p.cz1 * cb;                          // end fine z layer
+  out[2] = p.b0;                                // first owned brick
+  out[3] = p.nbo;                               // owned bricks
+  out[4] = p.e0;                                // first owned cc element
+  out[5] = p.neo;                               // owned cc elements
+  out[6] = p.cz0 * cb * g.nx * g.ny;            // first x-fastest cell
+  out[7] = (p.cz1 - p.cz0) * cb * g.nx * g.ny;  // cells
+  out[8] = p.lo;                                // neighbour below
+  out[9] = p.hi;                                // neighbour above
+  return TMG_OK;
+}
+
 void tmg_destroy(tmg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& pb : c->pool) cudaFree(pb.first);
   if (c->h_state) cudaFreeHost(c->h_state);
@@ -521,7 +937,8 @@ void tmg_destroy(tmg_ctx* c) {
 
 int tmg_set_conductivity(tmg_ctx* c, const double* kappa, const tmg_patch* patches, int np) {
   if (!c || !kappa) return set_err(c, TMG_EARG, "tmg_set_conductivity: null argument");
-  for (int64_t i = 0; i < c->M; ++i)
+  const int64_t n = host_cells(c);
+  for (int64_t i = 0; i < n; ++i)
     if (!(kappa[i] > 0.0))  // fvm.cpp:42-44
       return set_err(c, TMG_ECONFIG, "assemble_system: conductivity must be positive");
   int rc = validate_patches(c, patches, np);
@@ -532,7 +949,7 @@ int tmg_set_conductivity(tmg_ctx* c, const double* kappa, const tmg_patch* patch
                                patches[i].v1, patches[i].value});
   rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, kappa, c->kappa);
+    UP(kappa, kappa);
   });
   if (rc) return rc;
   return finish_problem(c);
@@ -544,7 +961,8 @@ int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,
   if (!(lo > 0.0) || !(hi > lo))  // material.cpp:11-12
     return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
   if (p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
-  for (int64_t i = 0; i < c->M; ++i) {
+  const int64_t n = host_cells(c);
+  for (int64_t i = 0; i < n; ++i) {
     double r = 1.0;
     for (int k = 0; k < p; ++k) r *= rho[i];
     if (!(lo + r * (hi - lo) > 0.0))
@@ -558,9 +976,11 @@ int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,
                                patches[i].v1, patches[i].value});
   rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, rho, c->r);  // r as scratch for rho (brick layout)
-    launch_conductivity(c->g, c->cb, c->r, c->kappa, lo, hi, p, c->stream);
-    CK(cudaGetLastError());
+    UP(rho, r);  // r as scratch for rho (brick layout)
+    for (Slab& s : c->slabs) {
+      launch_conductivity(s.g, c->cb, s.r, s.kappa, lo, hi, p, c->stream);
+      CK(cudaGetLastError());
+    }
   });
   if (rc) return rc;
   return finish_problem(c);
@@ -571,15 +991,14 @@ int tmg_assemble_rhs(tmg_ctx* c, const double* source, double* rhs_out) {
   if (!c->have_problem) return set_err(c, TMG_EARG, "tmg_assemble_rhs: no problem set");
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    double* src = nullptr;
-    if (source) {
-      upload_global(c, source, c->q);
-      src = c->q;
+    if (source) UP(source, q);
+    for (Slab& s : c->slabs) {
+      launch_boundary(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                      c->grid.ly, c->grid.lz, s.kappa, source ? s.q : nullptr, s.dmask, s.z,
+                      nullptr, c->stream);
+      CK(cudaGetLastError());
     }
-    launch_boundary(c->g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
-                    c->grid.ly, c->grid.lz, c->kappa, src, c->dmask, c->z, nullptr, c->stream);
-    CK(cudaGetLastError());
-    download_global(c, c->z, rhs_out);
+    DOWN(z, rhs_out);
   });
 }
 
@@ -615,39 +1034,46 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, c->stream));
-    GridParams& g = c->g;
-    CK(cudaMemsetAsync(c->d_status, 0, 4 * sizeof(int), c->stream));
+    const int64_t C = cells_per_brick(c);
+    for (Slab& s : c->slabs) CK(cudaMemsetAsync(s.d_status, 0, 4 * sizeof(int), c->stream));
     if (kind == TMG_PRECOND_JACOBI) {
-      c->dinv = dalloc<double>(c, c->M);
-      launch_apply(g, c->cb, c->coef, nullptr, nullptr, c->dinv, c->stream);
+      for (Slab& s : c->slabs) {
+        s.dinv = owned<double>(c, s, C);
+        launch_apply(s.g, c->cb, s.coef, nullptr, nullptr, s.dinv, c->stream);
+        CK(cudaGetLastError());
+      }
     } else if (kind == TMG_PRECOND_MMG) {
-      g.lc = (int)o->num_local_basis;
-      g.lcc = (int)o->num_cc_basis;
-      const int64_t C = (int64_t)c->cb * c->cb * c->cb;
-      const int64_t q = (int64_t)g.sd * g.sd * g.sd * g.lc;
-      c->phi = dalloc<double>(c, g.nb * g.lc * C);
-      c->evals = dalloc<double>(c, g.nb * g.lc);
-      c->eig_iters = dalloc<int>(c, g.nb);
-      c->Gf = dalloc<double>(c, g.nb * thomas_doubles_per_brick(c->cb));
-      c->Ac = dalloc<double>(c, g.nb * 7 * g.lc * g.lc);
-      c->Bc = dalloc<double>(c, g.nb * g.lc * g.lc);
-      c->Rcc = dalloc<double>(c, g.ncc * g.lcc * q);
-      c->cc_evals = dalloc<double>(c, g.ncc * g.lcc);
-      c->Winv = dalloc<double>(c, g.ncc * q * q);
-      c->n_cc = g.ncc * g.lcc;
-      c->Acc = dalloc<double>(c, c->n_cc * c->n_cc);
-      c->rc = dalloc<double>(c, g.nb * g.lc);
-      c->rc0 = dalloc<double>(c, g.nb * g.lc);
-      c->ec = dalloc<double>(c, g.nb * g.lc);
-      c->rc1 = dalloc<double>(c, g.nb * g.lc);
-      c->tc = dalloc<double>(c, g.nb * g.lc);
+      c->lc = (int)o->num_local_basis;
+      c->lcc = (int)o->num_cc_basis;
+      c->g.lc = c->lc;
+      c->g.lcc = c->lcc;
+      const int64_t q = (int64_t)c->g.sd * c->g.sd * c->g.sd * c->lc;
+      const int lc = c->lc, lcc = c->lcc;
+      for (Slab& s : c->slabs) {
+        s.g.lc = lc;
+        s.g.lcc = lcc;
+        s.phi = ghosted<double>(c, s, lc * C);
+        s.evals = owned<double>(c, s, lc);
+        s.eig_iters = owned<int>(c, s, 1);
+        s.Gf = owned<double>(c, s, thomas_doubles_per_brick(c->cb));
+        s.Ac = owned<double>(c, s, 7 * lc * lc);
+        s.Bc = owned<double>(c, s, lc * lc);
+        s.Rcc = ghosted_e<double>(c, s, lcc * q);
+        s.cc_evals = owned_e<double>(c, s, lcc);
+        s.Winv = owned_e<double>(c, s, q * q);
+        for (double** v : {&s.rc, &s.rc0, &s.ec, &s.rc1, &s.tc}) {
+          *v = ghosted<double>(c, s, lc);
+          CK(cudaMemsetAsync(*v + s.bs0 * lc, 0, sizeof(double) * (size_t)(s.nbs * lc), c->stream));
+        }
+      }
+      c->n_cc = c->g.ncc * lcc;
       c->rcc = dalloc<double>(c, c->n_cc);
       c->ecc = dalloc<double>(c, c->n_cc);
       // TMG_SETUP_PROFILE=1: per-phase device times on stderr (diagnostics only)
       const bool sprof = getenv("TMG_SETUP_PROFILE") != nullptr;
-      cudaEvent_t ph[10];
+      cudaEvent_t ph[12];
       int nph = 0;
-      const char* phname[10];
+      const char* phname[12];
       auto mark = [&](const char* name) {
         if (!sprof) return;
         CK(cudaEventCreate(&ph[nph]));
@@ -658,34 +1084,54 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
       const int degree = o->eig_degree > 0 ? o->eig_degree : 32;
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
-      launch_local_basis(g, c->cb, c->kappa, c->phi, c->evals, c->eig_iters, tol, degree, max_outer,
-                         c->stream);
+      for (Slab& s : c->slabs)
+        launch_local_basis(s.g, c->cb, s.kappa, s.phi, s.evals, s.eig_iters, tol, degree,
+                           max_outer, c->stream);
       CK(cudaGetLastError());
+      XCH(phi, sizeof(double) * lc * C, false);
       mark("local_basis");
-      launch_coarse_blocks(g, c->cb, c->kappa, c->dmask, c->phi, c->Ac, c->Bc, c->stream);
+      for (Slab& s : c->slabs)
+        launch_coarse_blocks(s.g, c->cb, s.kappa, s.dmask, s.phi, s.Ac, s.Bc, c->stream);
       CK(cudaGetLastError());
       mark("coarse_blocks");
-      launch_cc_basis(g, c->Ac, c->Bc, c->Rcc, c->cc_evals, c->stream);
+      for (Slab& s : c->slabs) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
       CK(cudaGetLastError());
+      XCH(Rcc, sizeof(double) * lcc * q, true);
       mark("cc_basis");
-      launch_coarse_smoother(g, c->Ac, c->Winv, c->d_status + 1, c->stream);
+      for (Slab& s : c->slabs)
+        launch_coarse_smoother(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
       CK(cudaGetLastError());
       mark("coarse_smoother");
-      launch_thomas_factor(g, c->cb, c->kappa, c->dmask, c->Gf, c->d_status, c->stream);
+      for (Slab& s : c->slabs)
+        launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.Gf, s.d_status, c->stream);
       CK(cudaGetLastError());
       mark("thomas_factor");
-      launch_acc_assemble(g, c->Ac, c->Rcc, c->Acc, c->stream);
+      // A_cc: every slab assembles its rows of the one dense matrix
+      double* Acc = dalloc<double>(c, c->n_cc * c->n_cc);
+      for (Slab& s : c->slabs) launch_acc_assemble(s.g, s.Ac, s.Rcc, Acc, c->stream);
       CK(cudaGetLastError());
+      if (c->nccl()) {
+        const Slab& s = c->slabs[0];
+        const int64_t rows = s.g.neo * lcc;
+        NK(ncclAllGather(Acc + s.g.e0 * lcc * c->n_cc, Acc, (size_t)(rows * c->n_cc), ncclDouble,
+                         c->comm, c->stream));
+      }
       mark("acc_assemble");
       double* work = dalloc<double>(c, dense_inverse_work_doubles(c->n_cc));
-      dense_spd_inverse(c->Acc, c->n_cc, work, c->d_status + 2, c->stream);
+      dense_spd_inverse(Acc, c->n_cc, work, c->slabs[0].d_status + 2, c->stream);
       CK(cudaGetLastError());
       mark("acc_inverse");
-      c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
-      c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
-      pack_sym_tiles(c->Acc, c->n_cc, c->AccT, c->stream);
-      CK(cudaGetLastError());
-      mark("pack_tiles");
+      if (!c->dist()) {
+        c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
+        c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
+        pack_sym_tiles(Acc, c->n_cc, c->AccT, c->stream);
+        CK(cudaGetLastError());
+        mark("pack_tiles");
+        CK(cudaStreamSynchronize(c->stream));
+        dfree(c, Acc);
+      } else {
+        c->Ainv = Acc;  // row blocks applied per slab (launch_gemv_rows)
+      }
       CK(cudaStreamSynchronize(c->stream));
       for (int i = 1; i < nph; ++i) {
         float t = 0.f;
@@ -694,8 +1140,6 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       }
       for (int i = 0; i < nph; ++i) cudaEventDestroy(ph[i]);
       dfree(c, work);
-      dfree(c, c->Acc);
-      c->Acc = nullptr;
     }
     CK(cudaEventRecord(e1, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -705,20 +1149,22 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     c->setup_seconds = 1e-3 * ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    int status[4];
-    CK(cudaMemcpy(status, c->d_status, sizeof status, cudaMemcpyDeviceToHost));
-    if (status[0]) {
-      set_err(c, TMG_ESOLVER,
-              "BlockJacobiSmoother: singular block: DirectSolver: matrix numerically singular");
-      throw Fail{TMG_ESOLVER};
-    }
-    if (status[1]) {
-      set_err(c, TMG_ESOLVER, "BlockJacobiSmoother: singular block (coarse level)");
-      throw Fail{TMG_ESOLVER};
-    }
-    if (status[2]) {
-      set_err(c, TMG_ESOLVER, "DirectSolver: matrix numerically singular (A_cc)");
-      throw Fail{TMG_ESOLVER};
+    for (Slab& s : c->slabs) {
+      int status[4];
+      CK(cudaMemcpy(status, s.d_status, sizeof status, cudaMemcpyDeviceToHost));
+      if (status[0]) {
+        set_err(c, TMG_ESOLVER,
+                "BlockJacobiSmoother: singular block: DirectSolver: matrix numerically singular");
+        throw Fail{TMG_ESOLVER};
+      }
+      if (status[1]) {
+        set_err(c, TMG_ESOLVER, "BlockJacobiSmoother: singular block (coarse level)");
+        throw Fail{TMG_ESOLVER};
+      }
+      if (status[2]) {
+        set_err(c, TMG_ESOLVER, "DirectSolver: matrix numerically singular (A_cc)");
+        throw Fail{TMG_ESOLVER};
+      }
     }
     c->kind = kind;
     c->have_setup = true;
@@ -730,7 +1176,7 @@ int tmg_upload_rhs(tmg_ctx* c, const double* b) {
   if (!c || !b) return set_err(c, TMG_EARG, "tmg_upload_rhs: null argument");
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, b, c->b);
+    UP(b, b);
   });
 }
 
@@ -738,7 +1184,7 @@ int tmg_upload_x0(tmg_ctx* c, const double* x0) {
   if (!c || !x0) return set_err(c, TMG_EARG, "tmg_upload_x0: null argument");
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, x0, c->x);
+    UP(x0, x);
   });
 }
 
@@ -755,7 +1201,7 @@ int tmg_download_solution(tmg_ctx* c, double* x) {
   if (!c || !x) return set_err(c, TMG_EARG, "tmg_download_solution: null argument");
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    download_global(c, c->x, x);
+    DOWN(x, x);
   });
 }
 
@@ -766,12 +1212,12 @@ int tmg_pcg(tmg_ctx* c, const double* b, const double* x0, double rtol, int maxi
   tmg_report local{};
   const int rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, b, c->b);
-    if (x0) upload_global(c, x0, c->x);
+    UP(b, b);
+    if (x0) UP(x0, x);
     solve_device(c, rtol, maxit, x0 ? 1 : 0, &local, nullptr, nullptr);
-    download_global(c, c->x, x_out);
+    DOWN(x, x_out);
     if (history && local.iterations > 0)
-      CK(cudaMemcpy(history, c->history, sizeof(double) * (size_t)local.iterations,
+      CK(cudaMemcpy(history, c->slabs[0].history, sizeof(double) * (size_t)local.iterations,
                     cudaMemcpyDeviceToHost));
   });
   if (rep) *rep = local;
@@ -783,10 +1229,13 @@ int tmg_apply_operator(tmg_ctx* c, const double* x, double* y) {
   if (!c->have_problem) return set_err(c, TMG_EARG, "apply: no problem set");
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    upload_global(c, x, c->p);
-    launch_apply(c->g, c->cb, c->coef, c->p, c->q, nullptr, c->stream);
-    CK(cudaGetLastError());
-    download_global(c, c->q, y);
+    UP(x, p);
+    XCH(p, sizeof(double) * cells_per_brick(c), false);
+    for (Slab& s : c->slabs) {
+      launch_apply(s.g, c->cb, s.coef, s.p, s.q, nullptr, c->stream);
+      CK(cudaGetLastError());
+    }
+    DOWN(q, y);
   });
 }
 
@@ -796,59 +1245,53 @@ int tmg_apply_preconditioner(tmg_ctx* c, const double* rin, double* zout) {
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     ensure_history(c, 1);
-    PcgState init{};
-    init.rtol = 0.0;
-    init.maxit = 1;
-    init.hist_cap = c->hist_cap;
-    CK(cudaMemcpyAsync(c->st, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
-    upload_global(c, rin, c->r);
-    if (c->kind == TMG_PRECOND_MMG) {
-      enqueue_vcycle(c, 1, c->st, c->stream, c->p);
-    } else {
-      launch_jacobi_step(c->g, c->cb, c->kind == TMG_PRECOND_JACOBI ? c->dinv : nullptr, c->x,
-                         c->p, c->q, c->r, c->z, c->st, c->partials, c->history, 1, c->stream);
-    }
+    init_states(c, 0.0, 1);
+    UP(rin, r);
+    enqueue_precond_init(c);
     CK(cudaGetLastError());
-    download_global(c, c->z, zout);
+    DOWN(z, zout);
   });
 }
 
 int tmg_get_sizes(tmg_ctx* c, int64_t* s) {
   if (!c || !s) return set_err(c, TMG_EARG, "null argument");
-  const int64_t C = (int64_t)c->cb * c->cb * c->cb;
   s[0] = c->M;
   s[1] = c->g.nb;
-  s[2] = c->g.nb * c->g.lc;
+  s[2] = c->g.nb * c->lc;
   s[3] = c->g.ncc;
-  s[4] = c->g.ncc * c->g.lcc;
-  s[5] = C;
+  s[4] = c->g.ncc * c->lcc;
+  s[5] = cells_per_brick(c);
   return TMG_OK;
 }
 
 int tmg_get_local_bases(tmg_ctx* c, double* phi, double* evals, int* iters) {
   if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG)
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
+  if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {
-    const int64_t C = (int64_t)c->cb * c->cb * c->cb;
+    const Slab& s = c->slabs[0];
+    const int64_t C = cells_per_brick(c);
     if (phi)
-      CK(cudaMemcpy(phi, c->phi, sizeof(double) * (size_t)(c->g.nb * c->g.lc * C),
+      CK(cudaMemcpy(phi, s.phi, sizeof(double) * (size_t)(c->g.nb * c->lc * C),
                     cudaMemcpyDeviceToHost));
     if (evals)
-      CK(cudaMemcpy(evals, c->evals, sizeof(double) * (size_t)(c->g.nb * c->g.lc),
+      CK(cudaMemcpy(evals, s.evals, sizeof(double) * (size_t)(c->g.nb * c->lc),
                     cudaMemcpyDeviceToHost));
     if (iters)
-      CK(cudaMemcpy(iters, c->eig_iters, sizeof(int) * (size_t)c->g.nb, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(iters, s.eig_iters, sizeof(int) * (size_t)c->g.nb, cudaMemcpyDeviceToHost));
   });
 }
 
 int tmg_get_coarse_operator(tmg_ctx* c, double* ac) {
   if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG || !ac)
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
+  if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {
     const GridParams& g = c->g;
-    const int L = g.lc;
+    const int L = c->lc;
     std::vector<double> blk((size_t)(g.nb * 7 * L * L));
-    CK(cudaMemcpy(blk.data(), c->Ac, sizeof(double) * blk.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(blk.data(), c->slabs[0].Ac, sizeof(double) * blk.size(),
+                  cudaMemcpyDeviceToHost));
     const int64_t nc = g.nb * L;
     std::fill(ac, ac + nc * nc, 0.0);
     for (int64_t I = 0; I < g.nb; ++I) {
@@ -873,20 +1316,22 @@ int tmg_get_coarse_operator(tmg_ctx* c, double* ac) {
 int tmg_get_cc_restriction(tmg_ctx* c, double* rcc) {
   if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG || !rcc)
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
+  if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {
     const GridParams& g = c->g;
-    const int64_t q = (int64_t)g.sd * g.sd * g.sd * g.lc, nc = g.nb * g.lc;
-    std::vector<double> R((size_t)(g.ncc * g.lcc * q));
-    CK(cudaMemcpy(R.data(), c->Rcc, sizeof(double) * R.size(), cudaMemcpyDeviceToHost));
-    std::fill(rcc, rcc + g.ncc * g.lcc * nc, 0.0);
+    const int64_t q = (int64_t)g.sd * g.sd * g.sd * c->lc, nc = g.nb * c->lc;
+    std::vector<double> R((size_t)(g.ncc * c->lcc * q));
+    CK(cudaMemcpy(R.data(), c->slabs[0].Rcc, sizeof(double) * R.size(), cudaMemcpyDeviceToHost));
+    std::fill(rcc, rcc + g.ncc * c->lcc * nc, 0.0);
     for (int64_t e = 0; e < g.ncc; ++e) {
       const int64_t ei = e % g.ncx, ej = (e / g.ncx) % g.ncy, ek = e / (g.ncx * g.ncy);
       for (int64_t ch = 0; ch < (int64_t)g.sd * g.sd * g.sd; ++ch) {
         const int64_t di = ch % g.sd, dj = (ch / g.sd) % g.sd, dk = ch / (g.sd * g.sd);
         const int64_t I = (ei * g.sd + di) + g.nbx * ((ej * g.sd + dj) + g.nby * (ek * g.sd + dk));
-        for (int k = 0; k < g.lcc; ++k)
-          for (int a = 0; a < g.lc; ++a)
-            rcc[(e * g.lcc + k) * nc + I * g.lc + a] = R[(size_t)((e * g.lcc + k) * q + ch * g.lc + a)];
+        for (int k = 0; k < c->lcc; ++k)
+          for (int a = 0; a < c->lc; ++a)
+            rcc[(e * c->lcc + k) * nc + I * c->lc + a] =
+                R[(size_t)((e * c->lcc + k) * q + ch * c->lc + a)];
       }
     }
   });
@@ -894,6 +1339,8 @@ int tmg_get_cc_restriction(tmg_ctx* c, double* rcc) {
 
 int tmg_profile_solve(tmg_ctx* c, double rtol, int maxit, double* ms_total, int* count) {
   if (!c || !ms_total || !count) return set_err(c, TMG_EARG, "null argument");
+  if (!single(c))
+    return set_err(c, TMG_ENOTSUP, "per-kernel profiling needs a single-slab context");
   for (int i = 0; i < 9; ++i) {
     ms_total[i] = 0.0;
     count[i] = 0;

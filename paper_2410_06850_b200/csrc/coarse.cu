@@ -541,6 +541,30 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
   k_coarse_smooth<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);
 }
 
+// Phase launchers of the same cycle for partitioned solves (ghost exchanges
+// and the A_cc row-block GEMV go between them).
+void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
+                          const double* in, const double* add, double* out, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  k_coarse_smooth<<<(unsigned)g.neo, nt, sizeof(double) * (size_t)q, s>>>(g, done, Winv, in, add, out);
+}
+void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
+                            const double* Rcc, const double* rc, const double* rc0, double* rcc,
+                            cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  k_coarse_restrict<<<(unsigned)g.neo, nt, sizeof(double) * (size_t)q, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
+}
+void launch_coarse_prolong(const GridParams& g, const int* done, const double* Rcc,
+                           const double* rc0, const double* ecc, double* rc1, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  k_coarse_prolong<<<(unsigned)g.neo, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
+}
+void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac, const double* rc,
+                         const double* x, double* out, cudaStream_t s) {
+  const int nc = (int)(g.nbo * LC);
+  k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, x, out, nc);
+}
+
 int compiled_lc() { return LC; }
 
 }  // namespace tmg

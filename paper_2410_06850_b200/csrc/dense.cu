@@ -248,24 +248,25 @@ __global__ void k_pivot_check(const double* pivots, int64_t n, int* status) {
 
 // y = A x, one warp per row, fixed-order lane-strided sums (deterministic).
 __global__ void __launch_bounds__(256) k_gemv(const int* __restrict__ done,
-                                              const double* __restrict__ A, int64_t n,
-                                              const double* __restrict__ x, double* y) {
+                                              const double* __restrict__ A, int64_t nrows,
+                                              int64_t ncols, const double* __restrict__ x,
+                                              double* y) {
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const double* a = A + row * n;
+  if (row >= nrows) return;
+  const double* a = A + row * ncols;
   double s = 0.0;
-  if ((n & 1) == 0) {
+  if ((ncols & 1) == 0) {
     const double2* a2 = reinterpret_cast<const double2*>(a);
     const double2* x2 = reinterpret_cast<const double2*>(x);
-    for (int64_t j = lane; j < n / 2; j += 32) {
+    for (int64_t j = lane; j < ncols / 2; j += 32) {
       const double2 av = __ldg(a2 + j), xv = __ldg(x2 + j);
       s = fma(av.x, xv.x, s);
       s = fma(av.y, xv.y, s);
     }
   } else {
-    for (int64_t j = lane; j < n; j += 32) s = fma(__ldg(a + j), __ldg(x + j), s);
+    for (int64_t j = lane; j < ncols; j += 32) s = fma(__ldg(a + j), __ldg(x + j), s);
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) y[row] = s;
@@ -448,7 +449,13 @@ int64_t dense_inverse_work_doubles(int64_t n) { return NB * NB + 2 * (int64_t)NB
 
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
                  cudaStream_t s) {
-  k_gemv<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(done, A, n, x, y);
+  k_gemv<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(done, A, n, n, x, y);
+}
+
+void launch_gemv_rows(const int* done, const double* A, int64_t n, int64_t row0, int64_t nrows,
+                      const double* x, double* y, cudaStream_t s) {
+  // rows of A and y shifted so the kernel's row r is global row row0 + r
+  k_gemv<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(done, A + row0 * n, nrows, n, x, y + row0);
 }
 
 }  // namespace tmg

@@ -22,6 +22,19 @@ struct PcgState {
   double bnorm, rnorm, rho, alpha, beta, pq, rtol;
   int it, maxit, done, status, first, hist_cap;
   unsigned int ticket[8];
+  // partitioned solves (GridParams::dist): each reduction kernel leaves its
+  // local total here; the cross-slab sum (in-process or NCCL all-reduce)
+  // overwrites it and k_finalize applies the same scalar logic.
+  double loc[8];
+};
+
+// PcgState::loc slots and k_finalize selectors
+enum : int { kRedInit = 0, kRedSearch = 2, kRedUpdate = 3, kRedPost = 4, kRedJacobi = 5 };
+constexpr int kMaxSlabs = 64;
+struct FinArgs {
+  PcgState* st[kMaxSlabs];
+  double* hist[kMaxSlabs];
+  int ns;
 };
 
 // operator.cu
@@ -61,11 +74,24 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
                          cudaStream_t s);
 
+void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
+                          const double* in, const double* add, double* out, cudaStream_t s);
+void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
+                            const double* Rcc, const double* rc, const double* rc0, double* rcc,
+                            cudaStream_t s);
+void launch_coarse_prolong(const GridParams& g, const int* done, const double* Rcc,
+                           const double* rc0, const double* ecc, double* rc1, cudaStream_t s);
+void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac, const double* rc,
+                         const double* x, double* out, cudaStream_t s);
+
 // dense.cu
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
 int64_t dense_inverse_work_doubles(int64_t n);
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
                  cudaStream_t s);
+// rows [row0, row0 + nrows) of y = A x (A n x n, row-major)
+void launch_gemv_rows(const int* done, const double* A, int64_t n, int64_t row0, int64_t nrows,
+                      const double* x, double* y, cudaStream_t s);
 int64_t sym_tiles_doubles(int64_t n);
 int64_t sym_partials_doubles(int64_t n);
 void pack_sym_tiles(const double* A, int64_t n, double* T, cudaStream_t s);
@@ -90,6 +116,9 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s);
+// sum PcgState::loc[which..] over the slabs in a fixed order and finish the
+// reduction on every slab (partitioned solves)
+void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s);
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, cudaStream_t s);

@@ -47,6 +47,104 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coefficients(GridParams g,
   coef[3 * M + s] = fs.diag;
 }
 
+// ------------------------------------------------- scalar logic of pcg()
+// (shared by the in-kernel last-block path and k_finalize)
+__device__ __forceinline__ void fin_init(PcgState* st, double bb, double rr) {
+  const double bnorm = sqrt(bb), rnorm = sqrt(rr);
+  st->bnorm = bnorm;
+  st->rnorm = rnorm;
+  st->it = 0;
+  st->first = 0;
+  if (bnorm == 0.0) {  // solver.cpp:506-513
+    st->status = kStatusZeroRhs;
+    st->done = 1;
+  } else if (rnorm / bnorm <= st->rtol) {  // :523-531
+    st->status = kStatusConverged;
+    st->done = 1;
+  } else {
+    st->status = kStatusRunning;
+    st->done = 0;
+  }
+}
+
+__device__ __forceinline__ void fin_search(PcgState* st, double pqt) {
+  st->pq = pqt;
+  st->first = 0;
+  if (!(pqt > 0.0)) {  // solver.cpp:541-548
+    st->status = kStatusIndefinite;
+    st->done = 1;
+  } else {
+    st->alpha = st->rho / pqt;  // :549
+  }
+}
+
+__device__ __forceinline__ void finish_rr(PcgState* st, double rr, double* history) {
+  const int it = st->it + 1;
+  const double rel = sqrt(rr) / st->bnorm;
+  st->it = it;
+  st->rnorm = sqrt(rr);
+  if (it - 1 < st->hist_cap) history[it - 1] = rel;  // solver.cpp:555
+  if (!is_finite(rel)) {
+    st->status = kStatusNonFinite;
+    st->done = 1;
+  } else if (rel <= st->rtol) {  // solver.cpp:557-560
+    st->status = kStatusConverged;
+    st->done = 1;
+  } else if (it >= st->maxit) {
+    st->status = kStatusMaxIt;
+    st->done = 1;
+  }
+}
+
+__device__ __forceinline__ void fin_post(PcgState* st, double rz, int init) {
+  if (init) {
+    st->rho = rz;  // solver.cpp:537
+    st->beta = 0.0;
+    st->first = 1;
+  } else {
+    st->beta = rz / st->rho;  // :562-564
+    st->rho = rz;
+  }
+}
+
+__device__ __forceinline__ void fin_jacobi(PcgState* st, double rr, double rz, int init,
+                                           double* history) {
+  if (init) {
+    st->rho = rz;
+    st->beta = 0.0;
+    st->first = 1;
+  } else {
+    finish_rr(st, rr, history);
+    if (!st->done) {
+      st->beta = rz / st->rho;
+      st->rho = rz;
+    }
+  }
+}
+
+__global__ void k_finalize(FinArgs a, int which, int init) {
+  if (threadIdx.x != 0) return;
+  if (which != kRedInit && a.st[0]->done) return;  // every slab holds the same flag
+  const int nv = (which == kRedInit || which == kRedJacobi) ? 2 : 1;
+  double tot[2] = {0.0, 0.0};
+  for (int j = 0; j < a.ns; ++j)
+    for (int v = 0; v < nv; ++v) tot[v] += a.st[j]->loc[which + v];
+  for (int j = 0; j < a.ns; ++j) {
+    PcgState* st = a.st[j];
+    switch (which) {
+      case kRedInit: fin_init(st, tot[0], tot[1]); break;
+      case kRedSearch: fin_search(st, tot[0]); break;
+      case kRedUpdate: finish_rr(st, tot[0], a.hist[j]); break;
+      case kRedPost: fin_post(st, tot[0], init); break;
+      default: fin_jacobi(st, tot[0], tot[1], init, a.hist[j]); break;
+    }
+  }
+}
+
+void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s) {
+  k_finalize<<<1, 32, 0, s>>>(a, which, init);
+}
+
 // ------------------------------------------------------------------ K0 init
 template <int CB>
 __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const double* __restrict__ coef,
@@ -77,20 +175,11 @@ __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const doubl
   block_sum_k<C, 2>(v, red);
   double tot[2];
   if (grid_reduce_last_k<2>(v, partials, &st->ticket[0], tot, &flag, red) && t == 0) {
-    const double bnorm = sqrt(tot[0]), rnorm = sqrt(tot[1]);
-    st->bnorm = bnorm;
-    st->rnorm = rnorm;
-    st->it = 0;
-    st->first = 0;
-    if (bnorm == 0.0) {  // solver.cpp:506-513
-      st->status = kStatusZeroRhs;
-      st->done = 1;
-    } else if (rnorm / bnorm <= st->rtol) {  // :523-531
-      st->status = kStatusConverged;
-      st->done = 1;
+    if (g.dist) {
+      st->loc[kRedInit] = tot[0];
+      st->loc[kRedInit + 1] = tot[1];
     } else {
-      st->status = kStatusRunning;
-      st->done = 0;
+      fin_init(st, tot[0], tot[1]);
     }
   }
 }
@@ -134,37 +223,12 @@ __global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, con
   block_sum_k<NT, 1>(v, red);
   double tot[1];
   if (grid_reduce_last_k<1>(v, partials, &st->ticket[1], tot, &flag, red) && t == 0) {
-    const double pqt = tot[0];
-    st->pq = pqt;
-    st->first = 0;
-    if (!(pqt > 0.0)) {  // solver.cpp:541-548
-      st->status = kStatusIndefinite;
-      st->done = 1;
-    } else {
-      st->alpha = st->rho / pqt;  // :549
-    }
+    if (g.dist) st->loc[kRedSearch] = tot[0];
+    else fin_search(st, tot[0]);
   }
 }
 
 // ------------------------------------------------- K2 update + pre-smooth
-__device__ __forceinline__ void finish_rr(PcgState* st, double rr, double* history) {
-  const int it = st->it + 1;
-  const double rel = sqrt(rr) / st->bnorm;
-  st->it = it;
-  st->rnorm = sqrt(rr);
-  if (it - 1 < st->hist_cap) history[it - 1] = rel;  // solver.cpp:555
-  if (!is_finite(rel)) {
-    st->status = kStatusNonFinite;
-    st->done = 1;
-  } else if (rel <= st->rtol) {  // solver.cpp:557-560
-    st->status = kStatusConverged;
-    st->done = 1;
-  } else if (it >= st->maxit) {
-    st->status = kStatusMaxIt;
-    st->done = 1;
-  }
-}
-
 template <int CB>
 struct UpdateSmem {
   double slots[kSlots][Thomas<CB>::PLANE];
@@ -215,8 +279,10 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, cons
     double v[1] = {rr};
     block_sum_k<NT, 1>(v, sm.red);
     double tot[1];
-    if (grid_reduce_last_k<1>(v, partials, &st->ticket[2], tot, &sm.flag, sm.red) && t == 0)
-      finish_rr(st, tot[0], history);  // :554-560
+    if (grid_reduce_last_k<1>(v, partials, &st->ticket[2], tot, &sm.flag, sm.red) && t == 0) {
+      if (g.dist) st->loc[kRedUpdate] = tot[0];
+      else finish_rr(st, tot[0], history);  // :554-560
+    }
   }
 }
 
@@ -348,15 +414,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   block_sum_k<NT, 1>(v, sm.red);
   double tot[1];
   if (grid_reduce_last_k<1>(v, partials, &st->ticket[3], tot, &sm.flag, sm.red) && t == 0) {
-    const double rz = tot[0];
-    if (init) {
-      st->rho = rz;  // solver.cpp:537
-      st->beta = 0.0;
-      st->first = 1;
-    } else {
-      st->beta = rz / st->rho;  // :562-564
-      st->rho = rz;
-    }
+    if (g.dist) st->loc[kRedPost] = tot[0];
+    else fin_post(st, tot[0], init);
   }
 }
 
@@ -387,16 +446,11 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
   block_sum_k<C, 2>(v, red);
   double tot[2];
   if (grid_reduce_last_k<2>(v, partials, &st->ticket[4], tot, &flag, red) && t == 0) {
-    if (init) {
-      st->rho = tot[1];
-      st->beta = 0.0;
-      st->first = 1;
+    if (g.dist) {
+      st->loc[kRedJacobi] = tot[0];
+      st->loc[kRedJacobi + 1] = tot[1];
     } else {
-      finish_rr(st, tot[0], history);
-      if (!st->done) {
-        st->beta = tot[1] / st->rho;
-        st->rho = tot[1];
-      }
+      fin_jacobi(st, tot[0], tot[1], init, history);
     }
   }
 }

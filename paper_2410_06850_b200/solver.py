@@ -91,7 +91,8 @@ EXPORTED_SYMBOLS = (
     "tmg_apply_preconditioner", "tmg_upload_rhs", "tmg_upload_x0", "tmg_solve_resident",
     "tmg_download_solution", "tmg_get_local_bases", "tmg_get_coarse_operator",
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
-    "tmg_stream", "tmg_kernel_launches",
+    "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
+    "tmg_create_dist", "tmg_partition",
 )
 
 
@@ -198,10 +199,36 @@ class PcgResult:
     report: SolveReport
 
 
+def partition(grid: GridSpec, ncc, sd: int, nranks: int, rank: int) -> dict:
+    """Slab `rank` of `nranks` (tmg_partition; host-only, no GPU needed)."""
+    L = native()
+    ncc3 = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
+    g = _Grid(grid.nx, grid.ny, grid.nz, grid.lx, grid.ly, grid.lz, (C.c_int64 * 3)(*ncc3), sd)
+    out = (C.c_int64 * 10)()
+    rc = L.tmg_partition(C.byref(g), C.c_int(nranks), C.c_int(rank), out)
+    if rc:
+        _raise(rc, L.tmg_last_error(None).decode())
+    keys = ("z0", "z1", "brick0", "bricks", "elem0", "elems", "cell0", "cells", "lo", "hi")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
+def nccl_unique_id() -> bytes:
+    """NCCL unique id for tmg_create_dist (make on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    rc = native().tmg_nccl_unique_id(buf, C.c_int(128))
+    if rc:
+        _raise(rc, native().tmg_last_error(None).decode())
+    return buf.raw
+
+
 class Context:
     """One GPU solve context: grid hierarchy + problem + preconditioner."""
 
-    def __init__(self, grid: GridSpec, ncc: Sequence[int] | int, sd: int, device: int = 0):
+    def __init__(self, grid: GridSpec, ncc: Sequence[int] | int, sd: int, device: int = 0,
+                 slabs: int = 1, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
+        """slabs > 1: the grid split into z-slabs inside this process (one GPU);
+        nranks > 1: this process holds slab `rank` and talks NCCL to the others
+        (host arrays are then the rank's own slab, see partition())."""
         L = native()
         ncc3 = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
         self._g = _Grid(grid.nx, grid.ny, grid.nz, grid.lx, grid.ly, grid.lz,
@@ -209,12 +236,27 @@ class Context:
         self.grid = grid
         self.ncc = ncc3
         self.sd = sd
+        self.slabs = slabs
+        self.rank, self.nranks = rank, nranks
         ptr = C.c_void_p()
-        rc = L.tmg_create(C.byref(self._g), C.c_int(device), C.byref(ptr))
+        if nranks > 1:
+            if slabs != 1:
+                raise ValueError("a distributed context holds one slab per rank")
+            idb = C.create_string_buffer(bytes(nccl_id), 128)
+            rc = L.tmg_create_dist(C.byref(self._g), C.c_int(device), C.c_int(rank),
+                                   C.c_int(nranks), idb, C.byref(ptr))
+        elif slabs > 1:
+            rc = L.tmg_create_slabs(C.byref(self._g), C.c_int(device), C.c_int(slabs),
+                                    C.byref(ptr))
+        else:
+            rc = L.tmg_create(C.byref(self._g), C.c_int(device), C.byref(ptr))
         if rc:
             _raise(rc, L.tmg_last_error(None).decode())
         self._p = ptr
         self.kind_name = None
+        # cells of every host array this context takes or returns
+        self.cells = (partition(grid, ncc3, sd, nranks, rank)["cells"] if nranks > 1
+                      else grid.num_cells())
 
     def close(self):
         if getattr(self, "_p", None):
@@ -244,7 +286,7 @@ class Context:
                                             C.c_double(kappa_hi), C.c_int(p), parr, C.c_int(n)))
 
     def assemble_rhs(self, source=None):
-        out = np.empty(self.grid.num_cells())
+        out = np.empty(self.cells)
         sp = _ptr(_f64(source)) if source is not None else None
         self._check(native().tmg_assemble_rhs(self._p, sp, _ptr(out)))
         return out
@@ -275,9 +317,9 @@ class Context:
 
     def pcg(self, b, rtol=1e-6, max_iterations=10000, x0=None, out=None) -> PcgResult:
         bb = _f64(b)
-        if bb.size != self.grid.num_cells():
+        if bb.size != self.cells:
             raise ValueError("pcg: rhs size mismatch")
-        if x0 is not None and np.asarray(x0).size != self.grid.num_cells():
+        if x0 is not None and np.asarray(x0).size != self.cells:
             raise ValueError("pcg: initial guess size mismatch")
         x = np.empty_like(bb) if out is None else out
         hist = np.zeros(max(1, max_iterations))
@@ -306,7 +348,7 @@ class Context:
         return self._report(rep)
 
     def download_solution(self):
-        x = np.empty(self.grid.num_cells())
+        x = np.empty(self.cells)
         self._check(native().tmg_download_solution(self._p, _ptr(x)))
         return x
 

@@ -1,0 +1,103 @@
+"""Partitioned (multi-slab) data path on one GPU.
+
+tmg_create_slabs splits the grid into z-slabs of whole cc-element layers with
+ghost brick layers, halo exchanges, cross-slab CG reductions, and a row-block
+A_cc^-1 GEMV per slab: everything the NCCL (one slab per GPU) path runs except
+the transport. The smoother blocks never straddle slabs, so the partitioned
+solve is the same algorithm as the single-slab one: the operator must agree
+bit for bit, the preconditioner and the PCG result up to summation order.
+"""
+import numpy as np
+import pytest
+
+from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs
+
+pytestmark = pytest.mark.gpu
+
+PATCH = BoundarySpec.bottom_center_patch(1, 1, 0.2, 0)
+
+
+def _ctx(n, ncc, sd, kappa, slabs, kind="mmg"):
+    c = Context(GridSpec(n, n, n), ncc, sd, slabs=slabs)
+    c.set_conductivity(kappa, PATCH)
+    c.setup(kind)
+    return c
+
+
+def _problem(n, kmin, seed=7):
+    """BASELINE-style design (seeded box-filtered field, volume fraction 0.3)."""
+    return inputs.conductivity(inputs.box_filter_design(n, 0.3, seed=seed), kmin)
+
+
+@pytest.mark.parametrize("n,ncc,sd,slabs", [(32, 4, 2, 2), (32, 4, 2, 4), (64, 4, 2, 2),
+                                            (64, 4, 2, 4), (64, 8, 1, 8)])
+def test_slab_operator_bitwise(n, ncc, sd, slabs):
+    kappa = _problem(n, 1e-3)
+    a = Context(GridSpec(n, n, n), ncc, sd)
+    a.set_conductivity(kappa, PATCH)
+    b = Context(GridSpec(n, n, n), ncc, sd, slabs=slabs)
+    b.set_conductivity(kappa, PATCH)
+    x = np.random.default_rng(1).standard_normal(n ** 3)
+    np.testing.assert_array_equal(a.apply_operator(x), b.apply_operator(x))
+    np.testing.assert_array_equal(a.assemble_rhs(np.ones(n ** 3)), b.assemble_rhs(np.ones(n ** 3)))
+
+
+@pytest.mark.parametrize("n,ncc,sd,slabs,kmin", [(32, 4, 2, 2, 1e-3), (32, 4, 2, 4, 1e-6),
+                                                 (64, 4, 2, 4, 1e-3), (128, 8, 2, 8, 1e-6)])
+def test_slab_preconditioner_matches_single(n, ncc, sd, slabs, kmin):
+    kappa = _problem(n, kmin)
+    a = _ctx(n, ncc, sd, kappa, 1)
+    b = _ctx(n, ncc, sd, kappa, slabs)
+    r = np.random.default_rng(3).standard_normal(n ** 3)
+    za, zb = a.apply_preconditioner(r), b.apply_preconditioner(r)
+    # same blocks and bases; only the A_cc^-1 GEMV sums in another order
+    assert np.linalg.norm(za - zb) <= 1e-9 * np.linalg.norm(za)
+
+
+@pytest.mark.parametrize("n,ncc,sd,slabs,kmin", [(32, 4, 2, 2, 1e-3), (64, 4, 2, 4, 1e-6),
+                                                 (128, 8, 2, 8, 1e-6)])
+def test_slab_pcg_matches_single(n, ncc, sd, slabs, kmin):
+    kappa = _problem(n, kmin)
+    a = _ctx(n, ncc, sd, kappa, 1)
+    b = _ctx(n, ncc, sd, kappa, slabs)
+    rhs = a.assemble_rhs(np.ones(n ** 3))
+    ra, rb = a.pcg(rhs, rtol=1e-8), b.pcg(rhs, rtol=1e-8)
+    assert ra.report.converged and rb.report.converged
+    assert abs(ra.report.iterations - rb.report.iterations) <= 1
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-8 * np.linalg.norm(ra.x)
+
+
+def test_slab_pcg_configs0_matches_single_and_warm_start():
+    n = 64
+    rho = inputs.box_filter_design(n, 0.3)
+    kappa = inputs.conductivity(rho, 1e-3)
+    a = _ctx(n, 4, 2, kappa, 1)
+    b = _ctx(n, 4, 2, kappa, 4)
+    rhs = a.assemble_rhs(np.ones(n ** 3))
+    ra, rb = a.pcg(rhs, rtol=1e-8), b.pcg(rhs, rtol=1e-8)
+    assert ra.report.iterations == rb.report.iterations
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-9 * np.linalg.norm(ra.x)
+    # warm start from a perturbed solution: fewer iterations, same answer
+    x0 = ra.x * (1 + 1e-3 * np.random.default_rng(5).standard_normal(n ** 3))
+    wa, wb = a.pcg(rhs, rtol=1e-8, x0=x0), b.pcg(rhs, rtol=1e-8, x0=x0)
+    assert wa.report.iterations == wb.report.iterations < ra.report.iterations
+    assert np.linalg.norm(wa.x - wb.x) <= 1e-9 * np.linalg.norm(wa.x)
+
+
+@pytest.mark.parametrize("kind", ["jacobi", "none"])
+def test_slab_baseline_preconditioners(kind):
+    n = 32
+    kappa = _problem(n, 1e-2)
+    a = _ctx(n, 4, 2, kappa, 1, kind)
+    b = _ctx(n, 4, 2, kappa, 4, kind)
+    rhs = a.assemble_rhs(np.ones(n ** 3))
+    ra, rb = a.pcg(rhs, rtol=1e-6, max_iterations=5000), b.pcg(rhs, rtol=1e-6, max_iterations=5000)
+    # hundreds of CG steps: summation-order drift moves the count by < 2 %
+    assert abs(ra.report.iterations - rb.report.iterations) <= max(1, 0.02 * ra.report.iterations)
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-6 * np.linalg.norm(ra.x)
+
+
+def test_slab_count_must_divide_cc_layers():
+    from paper_2410_06850_b200 import ConfigError
+    with pytest.raises(ConfigError):
+        Context(GridSpec(32, 32, 32), 4, 2, slabs=3)
