@@ -5,9 +5,10 @@ quoted on): 128^3 cells, seeded box-filter design (vf 0.3, 3 passes, radius 2),
 SIMP p = 3, kmin = 1e-6, unit source, T = 0 on the centred 0.2 x 0.2 patch of
 z = 0, PCG to ||r||/||b|| <= 1e-8 with the multiscale V-cycle (L_c = 4,
 L_cc = 8, c = 8, sd = 2, ncc = 8). One step = one full PCG solve from x0 = 0
-on the resident system. value = DoF * iterations / solve time (MDoF*iter/s),
-summed over ranks (N independent replicas: the brick-decomposed multi-GPU solve
-is not built yet).
+on the resident system. value = DoF * iterations / solve time (MDoF*iter/s).
+With N > 1 ranks (torchrun) the solve is partitioned: one configs[1] slab of
+128^3 cells per GPU stacked along z (weak scaling), ghost exchanges and CG
+reductions over NCCL, time = max over ranks, value = all DoF of the job.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
@@ -49,23 +50,35 @@ def parse():
     return ap.parse_args()
 
 
-def workload(cfg_id):
+def workload(cfg_id, world=1):
+    """configs[cfg_id] design; with world > 1 the weak-scaling grid of the
+    partitioned runs: world slabs of n^3 cells stacked along z."""
     from paper_2410_06850_b200 import inputs
     cfg = dict(inputs.CONFIGS[cfg_id])
-    rho = inputs.box_filter_design(cfg["n"], cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
+    n = cfg["n"]
+    shape = n if world == 1 else (n, n, n * world)
+    rho = inputs.box_filter_design(shape, cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
     kappa = inputs.conductivity(rho, cfg["kmin"])
     return cfg, kappa
 
 
-def config_json(cfg, cfg_id, extra=None):
+def config_json(cfg, cfg_id, extra=None, world=1):
     n = cfg["n"]
-    d = {"workload": f"BASELINE configs[{cfg_id}]: {n}^3 cells, kmin={cfg['kmin']:g}, "
-                     f"MMG-PCG rtol={RTOL:g}",
-         "cells": n ** 3, "kmin": cfg["kmin"], "rtol": RTOL,
-         "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} "
-                      f"L_c=4 L_cc=8 nu=1",
-         "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
-         "l2": "no flush: one solve streams ~1.7 GB/iteration through the 126 MB L2"}
+    if world == 1:
+        d = {"workload": f"BASELINE configs[{cfg_id}]: {n}^3 cells, kmin={cfg['kmin']:g}, "
+                         f"MMG-PCG rtol={RTOL:g}",
+             "cells": n ** 3,
+             "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} "
+                          f"L_c=4 L_cc=8 nu=1"}
+    else:
+        d = {"workload": f"{world} x BASELINE configs[{cfg_id}] slabs: {n}x{n}x{n * world} cells, "
+                         f"kmin={cfg['kmin']:g}, MMG-PCG rtol={RTOL:g}",
+             "cells": n ** 3 * world,
+             "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} "
+                          f"ncc={cfg['ncc']}x{cfg['ncc']}x{cfg['ncc'] * world} L_c=4 L_cc=8 nu=1"}
+    d.update({"kmin": cfg["kmin"], "rtol": RTOL,
+              "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
+              "l2": "no flush: one solve streams ~1.7 GB/iteration per GPU through the 126 MB L2"})
     if extra:
         d.update(extra)
     return d
@@ -126,7 +139,9 @@ class ClockSampler:
 
 # --------------------------------------------------------------- reference
 
-def reference_context(cfg, kappa):
+def reference_context(cfg, kappa, world=1):
+    """The reference (proj/core, oracle/_ref) on the bench workload: configs[1]
+    for N = 1, the N-slab elongated grid of the partitioned runs for N > 1."""
     import ctypes as C
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O  # bench's reference / cpu-baseline leg only
@@ -134,8 +149,10 @@ def reference_context(cfg, kappa):
     R.ref_set_num_threads(0)
     pa = O._patch_array(O.bottom_center_patch())
     ts = C.c_double()
-    ctx = R.ref_ctx_create(cfg["n"], cfg["ncc"], cfg["sd"], O._d(kappa), 1, O._d(pa), 4,
-                           O.BLOCKS["cell"], O.BLOCKS["cc"], 4, 8, 1, C.byref(ts))
+    n = cfg["n"]
+    ctx = R.ref_ctx_create_grid(n, n, n * world, 1.0, 1.0, float(world), cfg["ncc"], cfg["ncc"],
+                                cfg["ncc"] * world, cfg["sd"], O._d(kappa), 1, O._d(pa), 4,
+                                O.BLOCKS["cell"], O.BLOCKS["cc"], 4, 8, 1, C.byref(ts))
     if not ctx:
         raise RuntimeError(R.ref_last_error().decode())
     return O, R, ctx, ts.value, R.ref_num_threads()
@@ -170,14 +187,15 @@ def cpu_baseline(cfg, kappa, iters):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    cfg, kappa = workload(args.config)
+    cfg, kappa = workload(args.config, world)
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtopmg_ref.so")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopmg_ref.so not built "
                           "(run bash oracle/build_ref.sh where /root/reference exists)"}))
         return 0
-    O, R, ctx, setup_s, threads = reference_context(cfg, kappa)
+    O, R, ctx, setup_s, threads = reference_context(cfg, kappa, world)
     try:
         reference_steps(O, R, ctx, cfg["n"], args.warmup, args.ref_iters)
         t0 = time.perf_counter()
@@ -185,16 +203,17 @@ def run_reference(args):
         wall = time.perf_counter() - t0
     finally:
         R.ref_ctx_destroy(ctx)
-    value = cfg["n"] ** 3 * its / secs / 1e6
+    value = kappa.size * its / secs / 1e6
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[1])",
             "config": config_json(cfg, args.config, {"reference_setup_seconds": setup_s,
-                                                     "iterations_per_step": its // args.steps}),
+                                                     "iterations_per_step": its // args.steps},
+                                  world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{args.steps} steps x {args.ref_iters} PCG iterations "
-                                       f"of the reference on {cfg['n']}^3 (set-up untimed)"},
+                                       f"of the reference on {kappa.size} cells (set-up untimed)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -235,16 +254,45 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec
-    cfg, kappa = workload(args.config)
-    n = cfg["n"]
-    M = n ** 3
-    ctx = Context(GridSpec(n, n, n), cfg["ncc"], cfg["sd"], device=local)
-    ctx.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0))
-    b = ctx.assemble_rhs(np.ones(M))
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs
+    from paper_2410_06850_b200 import dist as D
+    n = inputs.CONFIGS[args.config]["n"]
+    patch = BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0)
+    cfg, kappa = workload(args.config, world)
+    if world == 1:
+        grid = GridSpec(n, n, n)
+        ctx = Context(grid, cfg["ncc"], cfg["sd"], device=local)
+        kappa_local = kappa
+    else:
+        # weak scaling: one configs[1] slab (n^3 cells) per GPU, stacked along z
+        # into an n x n x (n * world) grid with cubic cells (lz = world); the
+        # design is the same generator on the whole grid.
+        grid = GridSpec(n, n, n * world, 1.0, 1.0, float(world))
+        ncc = (cfg["ncc"], cfg["ncc"], cfg["ncc"] * world)
+        ctx = D.dist_context(grid, ncc, cfg["sd"], dist, local)
+        kappa_local = D.slab(kappa, D.partition(grid, ncc, cfg["sd"], world, rank))
+    M_local = ctx.cells
+    M = grid.num_cells()
+    ctx.set_conductivity(kappa_local, patch)
+    b = ctx.assemble_rhs(np.ones(M_local))
+    barrier()
     t0 = time.perf_counter()
     ctx.setup("mmg")
-    setup_wall = time.perf_counter() - t0
+    setup_wall = max_over_ranks(time.perf_counter() - t0)
     ctx.upload_rhs(b)
     for _ in range(max(3, args.warmup)):
         rep = ctx.solve_resident(RTOL, 10000)
@@ -263,17 +311,13 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     launches = ctx.kernel_launches() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     iters = int(np.mean(its))
-    value = world * M * iters / (ms * 1e-3) / 1e6
+    value = M * iters / (ms * 1e-3) / 1e6
 
     # e2e through the C ABI with pinned host buffers (H2D b, solve, D2H x)
     b_pin = torch.from_numpy(b).pin_memory().numpy()
-    x_pin = torch.empty(M, dtype=torch.float64).pin_memory().numpy()
+    x_pin = torch.empty(M_local, dtype=torch.float64).pin_memory().numpy()
     ctx.pcg(b_pin, rtol=RTOL, out=x_pin)
     torch.cuda.synchronize()
     barrier()
@@ -281,18 +325,12 @@ def run_ours(args):
     e2e_its = 0
     for _ in range(args.steps):
         e2e_its += ctx.pcg(b_pin, rtol=RTOL, out=x_pin).report.iterations
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * M * (e2e_its / args.steps) / e2e_s / 1e6
-    true_rel = float(np.linalg.norm(b - ctx.apply_operator(x_pin)) / np.linalg.norm(b))
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    e2e_value = M * (e2e_its / args.steps) / e2e_s / 1e6
+    res2 = sum_over_ranks(float(np.sum((b - ctx.apply_operator(x_pin)) ** 2)))
+    b2 = sum_over_ranks(float(np.sum(b ** 2)))
+    true_rel = float(np.sqrt(res2 / b2))
 
-    # per-kernel CUDA-event times during one live solve (roofline)
-    prof = ctx.profile_solve(RTOL, 10000)
-    per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
-    dominant = max(("post", "update", "search", "restrict"), key=lambda k: prof[k][0])
     peak = None
     peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
     try:
@@ -301,33 +339,49 @@ def run_ours(args):
             peak_src = "measured MEASURED_PEAKS.json hbm_gbs"
     except Exception:
         peak = 6650.0
-    bytes_launch = KERNEL_BYTES_PER_CELL[dominant] * M
-    achieved = bytes_launch / (per[dominant] * 1e-3) / 1e9
-    iter_achieved = ITER_BYTES_PER_CELL * M * iters / (ms * 1e-3) / 1e9
+    iter_achieved = ITER_BYTES_PER_CELL * M_local * iters / (ms * 1e-3) / 1e9  # per GPU
+    if world == 1:
+        # per-kernel CUDA-event times during one live solve (roofline)
+        prof = ctx.profile_solve(RTOL, 10000)
+        per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+        dominant = max(("post", "update", "search", "restrict"), key=lambda k: prof[k][0])
+        bytes_launch = KERNEL_BYTES_PER_CELL[dominant] * M
+        achieved = bytes_launch / (per[dominant] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dominant),
+                "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src}
+    else:
+        per = {}
+        roof = {"bound": "hbm", "kernel": "whole iteration, per GPU (incl. exchanges)",
+                "achieved": iter_achieved, "peak": peak, "unit": "GB/s",
+                "frac": iter_achieved / peak, "traffic": None,
+                "algorithmic_bytes_per_launch": ITER_BYTES_PER_CELL * M_local,
+                "peak_source": peak_src}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
+    extra = {
+        "iterations": iters, "setup_ms": 1e3 * rep.setup_seconds,
+        "setup_wall_ms": 1e3 * setup_wall,
+        "time_to_solution_ms": 1e3 * rep.setup_seconds + ms,
+        "true_relative_residual": true_rel,
+        "parallelism": f"z-slabs x{world} over NCCL (one {n}^3 slab per GPU)" if world > 1
+                       else "single-gpu",
+        "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items() if v},
+        "iteration_hbm_gbs_algorithmic_per_gpu": iter_achieved,
+        "device_bytes": ctx.device_bytes()}
+    cj = config_json(cfg, args.config, extra, world)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded box-filter design, BASELINE configs[1])",
-        "config": config_json(cfg, args.config, {
-            "iterations": iters, "setup_ms": 1e3 * rep.setup_seconds,
-            "setup_wall_ms": 1e3 * setup_wall,
-            "time_to_solution_ms": 1e3 * rep.setup_seconds + ms,
-            "true_relative_residual": true_rel,
-            "parallelism": "replicas" if world > 1 else "single-gpu",
-            "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items() if v},
-            "iteration_hbm_gbs_algorithmic": iter_achieved,
-            "device_bytes": ctx.device_bytes()}),
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dominant),
-                     "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * M,
-                "d2h_bytes_per_step": 8 * M},
+        "config": cj,
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * M_local,
+                "d2h_bytes_per_step": 8 * M_local},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

@@ -273,6 +273,10 @@ def ref():
         R.ref_ctx_create.restype = C.c_void_p
         R.ref_ctx_create.argtypes = [I64, I64, I64, DP, C.c_int, DP, C.c_int, C.c_int, C.c_int,
                                      I64, I64, C.c_int, DP]
+        R.ref_ctx_create_grid.restype = C.c_void_p
+        R.ref_ctx_create_grid.argtypes = [I64, I64, I64, C.c_double, C.c_double, C.c_double,
+                                          I64, I64, I64, I64, DP, C.c_int, DP, C.c_int, C.c_int,
+                                          C.c_int, I64, I64, C.c_int, DP]
         R.ref_ctx_pcg.argtypes = [C.c_void_p, C.c_double, C.c_int, DP, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), DP]
         R.ref_ctx_destroy.argtypes = [C.c_void_p]

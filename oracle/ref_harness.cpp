@@ -211,14 +211,18 @@ struct RefCtx {
   std::unique_ptr<Preconditioner> pre;
 };
 
-void* ref_ctx_create(int64_t n, int64_t ncc, int64_t sd, const double* kappa, int npatch,
-                     const double* patches, int kind, int fine_blocks, int coarse_blocks,
-                     int64_t lc, int64_t lcc, int sweeps, double* setup_seconds) {
+// Any box grid: (nx, ny, nz) cells on [0,lx]x[0,ly]x[0,lz], ncx x ncy x ncz
+// cc elements (the multi-GPU benchmark's elongated weak-scaling grid).
+void* ref_ctx_create_grid(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                          int64_t ncx, int64_t ncy, int64_t ncz, int64_t sd, const double* kappa,
+                          int npatch, const double* patches, int kind, int fine_blocks,
+                          int coarse_blocks, int64_t lc, int64_t lcc, int sweeps,
+                          double* setup_seconds) {
   RefCtx* c = new RefCtx;
   const int rc = guarded([&] {
-    const GridSpec g(n, n, n);
+    const GridSpec g(nx, ny, nz, lx, ly, lz);
     const index_t m = g.num_cells();
-    const HierarchicalGrid h = build_hierarchy(g, {ncc, ncc, ncc}, sd);
+    const HierarchicalGrid h = build_hierarchy(g, {ncx, ncy, ncz}, sd);
     const std::vector<double> kap(kappa, kappa + m);
     c->sys = assemble_system(g, kap, std::vector<double>(m, 1.0), make_bc(npatch, patches));
     MmgOptions opts;
@@ -245,6 +249,13 @@ void* ref_ctx_create(int64_t n, int64_t ncc, int64_t sd, const double* kappa, in
     return nullptr;
   }
   return c;
+}
+
+void* ref_ctx_create(int64_t n, int64_t ncc, int64_t sd, const double* kappa, int npatch,
+                     const double* patches, int kind, int fine_blocks, int coarse_blocks,
+                     int64_t lc, int64_t lcc, int sweeps, double* setup_seconds) {
+  return ref_ctx_create_grid(n, n, n, 1.0, 1.0, 1.0, ncc, ncc, ncc, sd, kappa, npatch, patches,
+                             kind, fine_blocks, coarse_blocks, lc, lcc, sweeps, setup_seconds);
 }
 
 int ref_ctx_pcg(void* ctx, double rtol, int maxit, double* x_out, int* iterations,

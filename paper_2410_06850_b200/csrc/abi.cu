@@ -111,7 +111,11 @@ struct tmg_ctx {
   int total = 1;                 // slabs over all processes
   ncclComm_t comm = nullptr;     // NCCL contexts only
   std::vector<Slab> slabs;       // slabs held by this process
-  bool dist() const { return total > 1; }
+  // TMG_FORCE_DIST=1 (diagnostics): a one-slab context runs the partitioned
+  // path over a one-rank NCCL communicator (all-reduce, all-gather, captured
+  // NCCL calls), which is all of the NCCL transport but the halo send/recv
+  bool force_dist = false;
+  bool dist() const { return total > 1 || force_dist; }
   bool nccl() const { return comm != nullptr; }
   // problem
   bool have_problem = false;
@@ -806,6 +810,11 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof id);
       NK(ncclCommInitRank(&c->comm, total, id, first));
+    } else if (total == 1 && getenv("TMG_FORCE_DIST") && atoi(getenv("TMG_FORCE_DIST")) > 0) {
+      ncclUniqueId id;
+      NK(ncclGetUniqueId(&id));
+      NK(ncclCommInitRank(&c->comm, 1, id, 0));
+      c->force_dist = true;
     }
     c->slabs.resize((size_t)count);
     for (int k = 0; k < count; ++k) {
@@ -817,7 +826,7 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
       s.g.nbo = p.nbo;
       s.g.e0 = p.e0;
       s.g.neo = p.neo;
-      s.g.dist = total > 1;
+      s.g.dist = c->dist();
       s.lo = p.lo;
       s.hi = p.hi;
       s.L = c->g.nbx * c->g.nby;

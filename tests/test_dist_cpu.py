@@ -1,0 +1,101 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 4).
+
+The GPU data path of a partitioned solve is covered on one device by
+tests/test_gpu_slabs.py (same kernels, ghost layers and reductions; device
+copies instead of NCCL). Here real processes check what the NCCL transport
+relies on: the partition every rank computes independently is one consistent
+cover of the grid, the halo plan pairs every send with the matching receive
+and delivers exactly the neighbour's boundary layer, the NCCL id reaches all
+ranks, and the slabs of a global array reassemble it.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2410_06850_b200 import GridSpec
+from paper_2410_06850_b200 import dist as D
+
+GRID = GridSpec(64, 64, 64)
+NCC, SD = 4, 2  # 4 cc layers of 16 cells; coarse cells of 8^3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        part = D.partition(GRID, NCC, SD, world, rank)
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+        # one consistent cover of z, bricks, cc elements and cells
+        assert parts[0]["z0"] == 0 and parts[-1]["z1"] == GRID.nz
+        for a, b in zip(parts, parts[1:]):
+            assert a["z1"] == b["z0"]
+            assert a["brick0"] + a["bricks"] == b["brick0"]
+            assert a["elem0"] + a["elems"] == b["elem0"]
+            assert a["cell0"] + a["cells"] == b["cell0"]
+        assert sum(p["cells"] for p in parts) == GRID.num_cells()
+        assert [p["lo"] for p in parts] == [0] + [1] * (world - 1)
+        assert [p["hi"] for p in parts] == [1] * (world - 1) + [0]
+        # halo exchange following the library's plan: bricks hold their
+        # global index; ghosts start at -1 and must end as the neighbour's ids
+        L = (GRID.nx // 8) * (GRID.ny // 8)
+        lo_b = part["brick0"] - part["lo"] * L
+        n_st = part["bricks"] + (part["lo"] + part["hi"]) * L
+        win = -np.ones(n_st, dtype=np.int64)
+        win[part["brick0"] - lo_b:part["brick0"] - lo_b + part["bricks"]] = np.arange(
+            part["brick0"], part["brick0"] + part["bricks"])
+        reqs, recv = [], []
+        for peer, (s0, s1), (r0, r1) in D.halo_plan(part, rank, L):
+            send = torch.from_numpy(win[s0 - lo_b:s1 - lo_b].copy())
+            buf = torch.empty(r1 - r0, dtype=torch.int64)
+            reqs += [dist.isend(send, peer), dist.irecv(buf, peer)]
+            recv.append((r0, buf))
+        for q in reqs:
+            q.wait()
+        for r0, buf in recv:
+            win[r0 - lo_b:r0 - lo_b + len(buf)] = buf.numpy()
+        np.testing.assert_array_equal(win, np.arange(lo_b, lo_b + n_st))
+        # NCCL unique id hand-off (host-only call)
+        nid = D.broadcast_nccl_id(dist)
+        ids = [None] * world
+        dist.all_gather_object(ids, nid)
+        assert len(nid) == 128 and all(i == ids[0] for i in ids)
+        # slabs of a global array reassemble it
+        g = np.arange(GRID.num_cells(), dtype=np.float64)
+        pieces = [None] * world
+        dist.all_gather_object(pieces, D.slab(g, part))
+        np.testing.assert_array_equal(np.concatenate(pieces), g)
+        out[rank] = 1
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partition_and_halo_plan_gloo(world):
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+                       start_method="spawn")
+    assert sorted(out.keys()) == list(range(world))
+
+
+def test_partition_errors():
+    from paper_2410_06850_b200 import ConfigError
+    with pytest.raises(ConfigError):
+        D.partition(GRID, NCC, SD, 3, 0)  # 3 does not divide 4 cc layers
+    with pytest.raises(ValueError):
+        D.partition(GRID, NCC, SD, 2, 2)  # rank out of range

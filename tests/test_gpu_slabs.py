@@ -101,3 +101,36 @@ def test_slab_count_must_divide_cc_layers():
     from paper_2410_06850_b200 import ConfigError
     with pytest.raises(ConfigError):
         Context(GridSpec(32, 32, 32), 4, 2, slabs=3)
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL transport on a one-rank communicator (TMG_FORCE_DIST=1): the
+    partitioned path with all-reduce / all-gather and NCCL calls captured in
+    the iteration graph must reproduce the single-GPU solve."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, numpy as np\n"
+        "from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs\n"
+        "n = 64\n"
+        "k = inputs.conductivity(inputs.box_filter_design(n, 0.3), 1e-3)\n"
+        "c = Context(GridSpec(n, n, n), 4, 2)\n"
+        "c.set_conductivity(k, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))\n"
+        "c.setup('mmg')\n"
+        "b = c.assemble_rhs(np.ones(n ** 3))\n"
+        "r = c.pcg(b, rtol=1e-8)\n"
+        "z = c.apply_preconditioner(b)\n"
+        "print(json.dumps([r.report.iterations, r.x[::997].tolist(), z[::991].tolist()]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for force in ("0", "1"):
+        env = dict(os.environ, TMG_FORCE_DIST=force, PYTHONPATH=root)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[force] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert out["0"][0] == out["1"][0]
+    np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-9)
+    np.testing.assert_allclose(out["1"][2], out["0"][2], rtol=1e-9, atol=1e-12)
