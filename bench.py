@@ -234,7 +234,7 @@ def ncu_traffic(kernel):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["kernels"][kernel]["dram_bytes_per_launch"]
+        return d["kernels"]["k_" + kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 

@@ -13,11 +13,12 @@ ap.add_argument("--kmin", type=float, default=1e-6)
 ap.add_argument("--kind", default="mmg")
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--setups", type=int, default=1)
+ap.add_argument("--slabs", type=int, default=1)
 a = ap.parse_args()
 n = a.n
 rho = inputs.box_filter_design(n, 0.3)
 kappa = inputs.conductivity(rho, a.kmin)
-ctx = Context(GridSpec(n, n, n), a.ncc, a.sd)
+ctx = Context(GridSpec(n, n, n), a.ncc, a.sd, slabs=a.slabs)
 ctx.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))
 b = ctx.assemble_rhs(np.ones(n ** 3))
 import time
@@ -29,7 +30,7 @@ ctx.upload_rhs(b)
 for _ in range(a.solves):
     rep = ctx.solve_resident(1e-8, 5000)
 print("iterations", rep.iterations, "solve ms", rep.solve_seconds * 1e3)
-if os.environ.get("TMG_PROFILE"):
+if os.environ.get("TMG_PROFILE") and a.slabs == 1:
     prof = ctx.profile_solve(1e-8, 5000)
     for k, (ms, cnt) in prof.items():
         if cnt:

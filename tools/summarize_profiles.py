@@ -1,6 +1,6 @@
 """Summarise ncu output into profiles/ (committed evidence).
 
-    python tools/summarize_profiles.py <round-tag> <launches.csv> <full.ncu-rep>
+    python tools/summarize_profiles.py <round-tag> <launches.csv> <full.ncu-rep> [more.ncu-rep ...]
 
 Writes profiles/<tag>_launches.md (per-kernel launch count, time share from the
 cold-cache serialised launch list), profiles/<tag>_ncu_full.md (DRAM bytes,
@@ -28,14 +28,19 @@ def launches(path):
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[start]
     ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
-    agg = defaultdict(lambda: [0, 0.0])
+    ui = hdr.index("Metric Unit") if "Metric Unit" in hdr else None
+    agg = defaultdict(lambda: [0, 0.0])  # launches, ns
     for r in rows[start + 1:]:
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         k = short(r[ki])
         agg[k][0] += 1
-        agg[k][1] += float(r[vi].replace(",", ""))
+        agg[k][1] += float(r[vi].replace(",", "")) * TSCALE_NS.get(r[ui] if ui is not None else "nsecond", 1)
     return agg
+
+
+TSCALE_NS = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+             "second": 1e9, "s": 1e9}
 
 
 def full(path):
@@ -51,7 +56,7 @@ def full(path):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = g("dram__bytes_read.sum") * scale.get(u("dram__bytes_read.sum"), 1)
         wr = g("dram__bytes_write.sum") * scale.get(u("dram__bytes_write.sum"), 1)
-        tus = g("gpu__time_duration.sum") * (1e-3 if u("gpu__time_duration.sum") == "nsecond" else 1)
+        tus = g("gpu__time_duration.sum") * TSCALE_NS.get(u("gpu__time_duration.sum"), 1e3) * 1e-3
         st = sorted(((hdr[i].replace("smsp__average_warps_issue_stalled_", "").replace(
             "_per_issue_active.ratio", ""), float(r[i])) for i in range(len(hdr))
             if hdr[i].startswith("smsp__average_warps_issue_stalled_")
@@ -70,21 +75,25 @@ def full(path):
 
 
 def main():
-    tag, lpath, fpath = sys.argv[1:4]
+    tag, lpath, fpaths = sys.argv[1], sys.argv[2], sys.argv[3:]
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     agg = launches(lpath)
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(prof, f"{tag}_launches.md"), "w") as f:
         f.write(f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)\n\n")
-        f.write("Command: `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` (BASELINE configs[1], "
-                "128^3). Cold-cache, serialised per-launch times: compare shares, not absolutes.\n\n")
+        f.write("Command: `python bench.py --steps 1 --warmup 3 --no-cpu-baseline` (BASELINE configs[1], "
+                "128^3: set-up + 5 solves). Cold-cache, serialised per-launch times: compare shares, "
+                "not absolutes.\n\n")
         f.write("| kernel | launches | total us | share |\n|---|---:|---:|---:|\n")
         for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"| {k} | {n} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |\n")
-    fr = full(fpath)
+    fr = {}
+    for fp in fpaths:
+        for k, v in full(fp).items():
+            fr.setdefault(k, v)
     with open(os.path.join(prof, f"{tag}_ncu_full.md"), "w") as f:
-        f.write(f"# {tag}: ncu --set full (one launch per kernel, 128^3 solve)\n\n")
+        f.write(f"# {tag}: ncu --set full (one launch per kernel, 128^3: solve and set-up kernels)\n\n")
         f.write("| kernel | us | DRAM MB/launch | achieved GB/s | DRAM % peak | warps active % | regs | top stalls |\n")
         f.write("|---|---:|---:|---:|---:|---:|---:|---|\n")
         for k, v in fr.items():
