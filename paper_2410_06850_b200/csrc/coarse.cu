@@ -413,6 +413,8 @@ __device__ __forceinline__ double coarse_apply_row(const GridParams& g, const do
 __global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
                                 const double* __restrict__ Winv, const double* __restrict__ in,
                                 const double* __restrict__ add, double* out) {
+  pdl_trigger();
+  pdl_wait();
   if (*done) return;
   extern __shared__ double sm[];
   const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
@@ -443,6 +445,8 @@ __global__ void k_coarse_restrict(GridParams g, const int* __restrict__ done,
                                   const double* __restrict__ Ac, const double* __restrict__ Rcc,
                                   const double* __restrict__ rc, const double* __restrict__ rc0,
                                   double* rcc) {
+  pdl_trigger();
+  pdl_wait();
   if (*done) return;
   extern __shared__ double sm[];
   const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
@@ -464,6 +468,8 @@ __global__ void k_coarse_restrict(GridParams g, const int* __restrict__ done,
 __global__ void k_coarse_prolong(GridParams g, const int* __restrict__ done,
                                  const double* __restrict__ Rcc, const double* __restrict__ rc0,
                                  const double* __restrict__ ecc, double* rc1) {
+  pdl_trigger();
+  pdl_wait();
   if (*done) return;
   const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
@@ -480,6 +486,8 @@ __global__ void k_coarse_prolong(GridParams g, const int* __restrict__ done,
 __global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
                                const double* __restrict__ Ac, const double* __restrict__ rc,
                                const double* __restrict__ x, double* out, int n) {
+  pdl_trigger();
+  pdl_wait();
   if (*done) return;
   const int64_t k = g.b0 * LC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= g.b0 * LC + n) return;
@@ -533,12 +541,15 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
   const int nt = (q + 31) / 32 * 32;
   const int nc = (int)(g.nbo * LC);
   const size_t sm = sizeof(double) * (size_t)q;
-  k_coarse_smooth<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Winv, rc, nullptr, rc0);
-  k_coarse_restrict<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
+  const double* nul = nullptr;
+  launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Winv, rc, nul, rc0);
+  launch_pdl(k_coarse_restrict, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Ac, Rcc, rc, rc0,
+             rcc);
   launch_symv(done, Acc_tiles, n_cc, rcc, symv_partials, ecc, s);
-  k_coarse_prolong<<<(unsigned)g.neo, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
-  k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, rc1, tc, nc);
-  k_coarse_smooth<<<(unsigned)g.neo, nt, sm, s>>>(g, done, Winv, tc, rc1, ec);
+  launch_pdl(k_coarse_prolong, dim3((unsigned)g.neo), dim3(nt), 0, s, g, done, Rcc, rc0, ecc, rc1);
+  launch_pdl(k_coarse_resid, dim3((unsigned)((nc + 255) / 256)), dim3(256), 0, s, g, done, Ac, rc,
+             rc1, tc, nc);
+  launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Winv, tc, rc1, ec);
 }
 
 // Phase launchers of the same cycle for partitioned solves (ghost exchanges
@@ -546,23 +557,26 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
 void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
                           const double* in, const double* add, double* out, cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
-  k_coarse_smooth<<<(unsigned)g.neo, nt, sizeof(double) * (size_t)q, s>>>(g, done, Winv, in, add, out);
+  launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
+             done, Winv, in, add, out);
 }
 void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
                             const double* Rcc, const double* rc, const double* rc0, double* rcc,
                             cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
-  k_coarse_restrict<<<(unsigned)g.neo, nt, sizeof(double) * (size_t)q, s>>>(g, done, Ac, Rcc, rc, rc0, rcc);
+  launch_pdl(k_coarse_restrict, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
+             done, Ac, Rcc, rc, rc0, rcc);
 }
 void launch_coarse_prolong(const GridParams& g, const int* done, const double* Rcc,
                            const double* rc0, const double* ecc, double* rc1, cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
-  k_coarse_prolong<<<(unsigned)g.neo, nt, 0, s>>>(g, done, Rcc, rc0, ecc, rc1);
+  launch_pdl(k_coarse_prolong, dim3((unsigned)g.neo), dim3(nt), 0, s, g, done, Rcc, rc0, ecc, rc1);
 }
 void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac, const double* rc,
                          const double* x, double* out, cudaStream_t s) {
   const int nc = (int)(g.nbo * LC);
-  k_coarse_resid<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(g, done, Ac, rc, x, out, nc);
+  launch_pdl(k_coarse_resid, dim3((unsigned)((nc + 255) / 256)), dim3(256), 0, s, g, done, Ac, rc,
+             x, out, nc);
 }
 
 int compiled_lc() { return LC; }

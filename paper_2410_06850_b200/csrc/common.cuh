@@ -43,6 +43,23 @@ struct GridParams {
   int dist;  // 1: reductions finish in k_finalize after the cross-slab sum
 };
 
+// ------------------------------------------ programmatic dependent launch
+// Iteration kernels are launched with PDL (launch_pdl): each CTA lets the next
+// kernel in the stream be scheduled as soon as it starts (pdl_trigger), so the
+// next kernel's CTAs fill SMs freed by this kernel's tail and run their
+// prologue (barrier init, constant-data TMA/L2 prefetch) early; pdl_wait()
+// blocks until the previous kernel has completed and its writes are visible,
+// and must precede the first read of anything that kernel produced.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// L2 prefetch of constant data (no shared-memory side effects)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ double face_t(double kl, double kr) {
   // fvm.cpp:9-14: 2*kl*kr/(kl+kr) — no contraction, bitwise with the reference
   return __ddiv_rn(__dmul_rn(__dmul_rn(2.0, kl), kr), __dadd_rn(kl, kr));

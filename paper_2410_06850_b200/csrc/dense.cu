@@ -251,6 +251,8 @@ __global__ void __launch_bounds__(256) k_gemv(const int* __restrict__ done,
                                               const double* __restrict__ A, int64_t nrows,
                                               int64_t ncols, const double* __restrict__ x,
                                               double* y) {
+  pdl_trigger();
+  pdl_wait();
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -296,44 +298,57 @@ __global__ void k_pack_sym_tiles(const double* __restrict__ A, int64_t n, double
 }
 
 // Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...; each
-// 32 KB tile arrives by TMA bulk copy into a 2-deep shared ring.
+// 32 KB tile arrives by TMA bulk copy into a kSymvSlots-deep shared ring
+// (128 KB in flight per SM: enough for one SM's share of HBM bandwidth at
+// loaded latency).
+#ifndef TMG_SYMV_SLOTS
+#define TMG_SYMV_SLOTS 2
+#endif
+constexpr int kSymvSlots = TMG_SYMV_SLOTS;
 __global__ void __launch_bounds__(256) k_symv_tiles(const int* __restrict__ done,
                                                     const double* __restrict__ T, int64_t n,
                                                     const double* __restrict__ x, double* P) {
-  if (done && *done) return;
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char smraw[];
-  double* ring = reinterpret_cast<double*>(smraw);  // 2 x TS*TS
+  double* ring = reinterpret_cast<double*>(smraw);  // kSymvSlots x TS*TS
   const int64_t nt = (n + TS - 1) / TS;
-  double* xs = ring + 2 * TS * TS;                  // all of x, zero padded to nt*TS
-  __shared__ uint64_t bars[2];
+  double* xs = ring + kSymvSlots * TS * TS;         // all of x, zero padded to nt*TS
+  __shared__ uint64_t bars[kSymvSlots];
   __shared__ double colp[4][TS];
   const int64_t ntiles = nt * (nt + 1) / 2;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   constexpr uint32_t kTileBytes = TS * TS * sizeof(double);
   if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int k = 0; k < kSymvSlots; ++k) mbar_init(&bars[k], 1);
     fence_barrier_init();
   }
-  for (int64_t k = t; k < nt * TS; k += blockDim.x) xs[k] = k < n ? x[k] : 0.0;
   __syncthreads();
   auto issue = [&](int64_t tile, int slot) {
     mbar_arrive_expect_tx(&bars[slot], kTileBytes);
     bulk_g2s(ring + slot * TS * TS, T + tile * TS * TS, kTileBytes, &bars[slot]);
   };
   int64_t tile = blockIdx.x;
-  if (t == 0) {
-    if (tile < ntiles) issue(tile, 0);
-    if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+  // the tiles are constant: start streaming them before the dependency wait
+  if (t == 0)
+    for (int k = 0; k < kSymvSlots; ++k)
+      if (tile + k * (int64_t)gridDim.x < ntiles) issue(tile + k * gridDim.x, k);
+  pdl_wait();
+  if (done && *done) {
+    if (t == 0)  // drain the issued copies before exiting
+      for (int k = 0; k < kSymvSlots; ++k)
+        if (tile + k * (int64_t)gridDim.x < ntiles) mbar_wait(&bars[k], 0);
+    return;
   }
+  for (int64_t k = t; k < nt * TS; k += blockDim.x) xs[k] = k < n ? x[k] : 0.0;
+  __syncthreads();
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int slot = it & 1;
+    const int slot = it % kSymvSlots;
     int64_t I = 0;
     while ((I + 1) * (I + 2) / 2 <= tile) ++I;
     const int64_t J = tile - I * (I + 1) / 2;
     const double* xi = xs + I * TS;
     const double* xj = xs + J * TS;
-    mbar_wait(&bars[slot], (uint32_t)((it >> 1) & 1));
+    mbar_wait(&bars[slot], (uint32_t)((it / kSymvSlots) & 1));
     __syncthreads();
     const double* A = ring + slot * TS * TS;
     // row products: warp w owns rows 8w..8w+7; lane l covers columns l, l+32
@@ -375,9 +390,9 @@ __global__ void __launch_bounds__(256) k_symv_tiles(const int* __restrict__ done
     }
     __syncthreads();  // ring slot and xi/xj/colp consumed
     if (I != J && t < TS) P[(J * nt + I) * TS + t] = (colp[0][t] + colp[1][t]) + (colp[2][t] + colp[3][t]);
-    if (t == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) {
+    if (t == 0 && tile + kSymvSlots * (int64_t)gridDim.x < ntiles) {
       fence_proxy_async_smem();
-      issue(tile + 2 * gridDim.x, slot);
+      issue(tile + kSymvSlots * gridDim.x, slot);
     }
     __syncthreads();
   }
@@ -385,6 +400,8 @@ __global__ void __launch_bounds__(256) k_symv_tiles(const int* __restrict__ done
 
 __global__ void k_symv_reduce(const int* __restrict__ done, const double* __restrict__ P,
                               int64_t n, double* y) {
+  pdl_trigger();
+  pdl_wait();
   if (done && *done) return;
   const int64_t nt = (n + TS - 1) / TS;
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -418,12 +435,18 @@ void launch_symv(const int* done, const double* T, int64_t n, const double* x, d
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(double) * (size_t)(2 * TS * TS + nt * TS);
+  const size_t smem = sizeof(double) * (size_t)(kSymvSlots * TS * TS + nt * TS);
   cudaFuncSetAttribute(k_symv_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_symv_tiles, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
   const int64_t ntiles = nt * (nt + 1) / 2;
-  const unsigned grid = (unsigned)(ntiles < 2 * sms ? ntiles : 2 * sms);
-  k_symv_tiles<<<grid, 256, smem, s>>>(done, T, n, x, P);
-  k_symv_reduce<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(done, P, n, y);
+  const int64_t slots = (int64_t)per_sm * sms;
+  const unsigned grid = (unsigned)(ntiles < slots ? ntiles : slots);
+  launch_pdl(k_symv_tiles, dim3(grid), dim3(256), smem, s, done, T, n, x, P);
+  launch_pdl(k_symv_reduce, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, s, done, P, n, y);
 }
 
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s) {
@@ -455,7 +478,8 @@ void launch_gemv(const int* done, const double* A, int64_t n, const double* x, d
 void launch_gemv_rows(const int* done, const double* A, int64_t n, int64_t row0, int64_t nrows,
                       const double* x, double* y, cudaStream_t s) {
   // rows of A and y shifted so the kernel's row r is global row row0 + r
-  k_gemv<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(done, A + row0 * n, nrows, n, x, y + row0);
+  launch_pdl(k_gemv, dim3((unsigned)((nrows + 7) / 8)), dim3(256), 0, s, done, A + row0 * n, nrows,
+             n, x, y + row0);
 }
 
 }  // namespace tmg

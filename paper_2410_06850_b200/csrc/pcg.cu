@@ -123,6 +123,8 @@ __device__ __forceinline__ void fin_jacobi(PcgState* st, double rr, double rz, i
 }
 
 __global__ void k_finalize(FinArgs a, int which, int init) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x != 0) return;
   if (which != kRedInit && a.st[0]->done) return;  // every slab holds the same flag
   const int nv = (which == kRedInit || which == kRedJacobi) ? 2 : 1;
@@ -142,7 +144,7 @@ __global__ void k_finalize(FinArgs a, int which, int init) {
 }
 
 void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s) {
-  k_finalize<<<1, 32, 0, s>>>(a, which, init);
+  launch_pdl(k_finalize, dim3(1), dim3(32), 0, s, a, which, init);
 }
 
 // ------------------------------------------------------------------ K0 init
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, con
                                                               double* q, PcgState* st, double* partials) {
   // p_old and p are distinct buffers: neighbouring CTAs read p_old's halo while
   // this CTA writes the new search direction.
-  if (st->done) return;
+  pdl_trigger();
   constexpr int C = CB * CB * CB, NT = kStencilThreads < C ? kStencilThreads : C;
   constexpr int KPT = C / NT;
   __shared__ CoefSmem<CB> cs;
@@ -202,10 +204,12 @@ __global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, con
   __shared__ double red[80];
   __shared__ int flag;
   const int t = threadIdx.x;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  load_coefs<CB>(coef, M, cs, g, bc);  // constant: before the dependency wait
+  pdl_wait();
+  if (st->done) return;
   const bool first = st->first;
   const double beta = st->beta;
-  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
-  load_coefs<CB>(coef, M, cs, g, bc);
   load_tile_axpy<CB>(z, p_old, beta, first, pt, g, bc);  // p = z + beta p (solver.cpp:565-567)
   __syncthreads();
   double pq = 0.0;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, cons
                                                              const double* __restrict__ q, double* r,
                                                              double* r1, PcgState* st, double* partials,
                                                              double* history, int init) {
-  if (st->done) return;
+  pdl_trigger();
   constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
@@ -257,7 +261,12 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, cons
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
-  thomas_prefetch<CB>(sm.th, G);
+  thomas_prefetch<CB>(sm.th, G);  // G is constant: stream it before the wait
+  pdl_wait();
+  if (st->done) {
+    thomas_drain<CB>(sm.th);  // no bulk copy may land after the CTA exits
+    return;
+  }
   const int t = threadIdx.x;
   const double alpha = init ? 0.0 : st->alpha;
   double rr = 0.0;
@@ -293,6 +302,8 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
                                                                 const double* __restrict__ r,
                                                                 const double* __restrict__ r1, double* rc,
                                                                 const PcgState* st) {
+  pdl_trigger();
+  pdl_wait();
   if (st->done) return;
   constexpr int C = CB * CB * CB, NT = kStencilThreads < C ? kStencilThreads : C;
   constexpr int KPT = C / NT;
@@ -349,12 +360,16 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
                                                            const double* __restrict__ r1,
                                                            const double* __restrict__ ec, double* z,
                                                            PcgState* st, double* partials, int init) {
-  if (st->done) return;
+  pdl_trigger();
   constexpr int C = CB * CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
   PostSmem<CB>& sm = *reinterpret_cast<PostSmem<CB>*>(smraw);
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const double* G = Gf + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  if (threadIdx.x == 0)  // warm L2 with the first G planes (constant) before the wait
+    prefetch_l2(G, (uint32_t)(2 * Thomas<CB>::PLANE * sizeof(double)));
+  pdl_wait();
+  if (st->done) return;
   sm.th.slots = sm.u.slots;
   thomas_init<CB>(sm.th);
   const int t = threadIdx.x;
@@ -427,6 +442,8 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
                                                              double* z, PcgState* st,
                                                              double* partials, double* history,
                                                              int init) {
+  pdl_trigger();
+  pdl_wait();
   if (st->done) return;
   constexpr int C = CB * CB * CB;
   __shared__ double red[80];
@@ -504,35 +521,35 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) k_search<8><<<(unsigned)g.nbo, kStencilThreads, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
-  else k_search<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, z, p_old, p, q, st, partials);
+  if (cb == 8) launch_pdl(k_search<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, z, p_old, p, q, st, partials);
+  else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) k_update<8><<<(unsigned)g.nbo, Thomas<8>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
-  else k_update<4><<<(unsigned)g.nbo, Thomas<4>::NT, update_smem(cb), s>>>(g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
+  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
+  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
 }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) k_restrict<8><<<(unsigned)g.nbo, kStencilThreads, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
-  else k_restrict<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, phi, r, r1, rc, st);
+  if (cb == 8) launch_pdl(k_restrict<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
+  else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) k_post<8><<<(unsigned)g.nbo, Thomas<8>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
-  else k_post<4><<<(unsigned)g.nbo, Thomas<4>::NT, post_smem(cb), s>>>(g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  if (cb == 8) launch_pdl(k_post<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  else launch_pdl(k_post<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, cudaStream_t s) {
-  if (cb == 8) k_jacobi_step<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
-  else k_jacobi_step<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, dinv, x, p, q, r, z, st, partials, history, init);
+  if (cb == 8) launch_pdl(k_jacobi_step<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init);
+  else launch_pdl(k_jacobi_step<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init);
 }
 
 }  // namespace tmg

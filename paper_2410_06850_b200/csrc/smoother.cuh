@@ -195,6 +195,15 @@ __device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double
   }
 }
 
+// Wait for the loads thomas_prefetch issued (a CTA that exits early must not
+// leave bulk copies in flight into its shared memory).
+template <int CB>
+__device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm) {
+  constexpr int NPRE = kSlots >= CB ? CB : kSlots;
+  if (threadIdx.x == 0)
+    for (int n = 0; n < NPRE && n < Thomas<CB>::NL; ++n) mbar_wait(&sm.bars[n], 0);
+}
+
 // Exact block solve x = A_II^{-1} t for one brick (after thomas_prefetch).
 //  t  : smem, C values (plane k = t[k*P .. k*P+P)); x may alias t
 //  tz : smem, C values; tz[l] = T_z between cell l and the cell one plane below
