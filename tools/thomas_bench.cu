@@ -1,0 +1,134 @@
+// Microbenchmark of the fine block solve (diagnostics, not part of the
+// library): k_update's thread layout, shared memory and TMA ring over 4096
+// bricks, timed in three modes to separate HBM streaming from the solve's
+// own latency:
+//   0  real: each brick's 8 G planes (forward + backward sweep)
+//   1  L2:   every plane load reads brick 0 / plane 0 (L2-resident)
+//   2  copy: ring only (loads issued and awaited, no mat-vec work)
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//        --expt-relaxed-constexpr -I paper_2410_06850_b200/csrc tools/thomas_bench.cu
+#include <cstdio>
+#include <vector>
+
+#include "smoother.cuh"
+
+using namespace tmg;
+
+constexpr int CB = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __restrict__ Gf,
+                                                            const double* __restrict__ tin,
+                                                            double* xout) {
+  constexpr int C = CB * CB * CB, NT = Thomas<CB>::NT;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  struct Sm {
+    double slots[kSlots][Thomas<CB>::PLANE];
+    ThomasSmem<CB> th;
+    double tv[C];
+    double tz[C];
+  };
+  Sm& sm = *reinterpret_cast<Sm*>(smraw);
+  const int b = blockIdx.x;
+  const double* G = Gf + (MODE == 1 ? 0 : (size_t)b * Thomas<CB>::PER_BRICK);
+  sm.th.slots = sm.slots;
+  thomas_init<CB>(sm.th);
+  __syncthreads();
+  thomas_prefetch<CB>(sm.th, G);
+  for (int c = threadIdx.x; c < C; c += NT) {
+    sm.tv[c] = tin[(size_t)b * C + c];
+    sm.tz[c] = c >= CB * CB ? -0.1 : 0.0;
+  }
+  if (MODE == 2) {
+    // stream the same 15 plane loads through the ring, no compute
+    const bool waiter = threadIdx.x >= (int)blockDim.x - 32;
+    const bool issuer = threadIdx.x == (int)blockDim.x - 32;
+    for (int n = 0; n < Thomas<CB>::NL; ++n) {
+      const int slot = n % kSlots;
+      if (waiter) mbar_wait(&sm.th.bars[slot], (uint32_t)((n / kSlots) & 1));
+      __syncthreads();
+      if (issuer && n + kSlots < Thomas<CB>::NL) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&sm.th.bars[slot], Thomas<CB>::PLANE * sizeof(double));
+        bulk_g2s(sm.slots[slot], G + (size_t)Thomas<CB>::plane_of(n + kSlots) * Thomas<CB>::PLANE,
+                 Thomas<CB>::PLANE * sizeof(double), &sm.th.bars[slot]);
+      }
+      __syncthreads();
+    }
+  } else {
+    thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += NT) xout[(size_t)b * C + c] = sm.tv[c];
+}
+
+template <int MODE>
+float run(const double* G, const double* t, double* x, int nb, size_t smem) {
+  cudaFuncSetAttribute(k_bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, e;
+  cudaEventCreate(&a);
+  cudaEventCreate(&e);
+  for (int w = 0; w < 3; ++w) k_bench<MODE><<<nb, Thomas<CB>::NT, smem>>>(G, t, x);
+  cudaEventRecord(a);
+  const int reps = 20;
+  for (int i = 0; i < reps; ++i) k_bench<MODE><<<nb, Thomas<CB>::NT, smem>>>(G, t, x);
+  cudaEventRecord(e);
+  cudaEventSynchronize(e);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, e);
+  return 1e3f * ms / reps;
+}
+
+__global__ void k_dirty(double* buf, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    buf[i] = v + (double)i;
+}
+
+// time k_bench<0> right after a kernel that leaves `mb` MB of dirty lines
+float run_after_dirty(const double* G, const double* t, double* x, int nb, size_t smem, double* buf,
+                      size_t mb) {
+  cudaEvent_t a, e;
+  cudaEventCreate(&a);
+  cudaEventCreate(&e);
+  float tot = 0.f;
+  const int reps = 20;
+  for (int i = 0; i < reps + 3; ++i) {
+    if (mb) k_dirty<<<148 * 8, 256>>>(buf, mb << 17, (double)i);
+    cudaEventRecord(a);
+    k_bench<0><<<nb, Thomas<CB>::NT, smem>>>(G, t, x);
+    cudaEventRecord(e);
+    cudaEventSynchronize(e);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, e);
+    if (i >= 3) tot += ms;
+  }
+  return 1e3f * tot / reps;
+}
+
+int main() {
+  const int nb = 4096;
+  const size_t per = Thomas<CB>::PER_BRICK, C = CB * CB * CB;
+  std::vector<double> hg(per * nb), ht(C * nb);
+  for (size_t i = 0; i < hg.size(); ++i) hg[i] = 1e-3 * (double)((i * 2654435761u) % 1000) / 1000.0;
+  for (size_t i = 0; i < ht.size(); ++i) ht[i] = 1.0;
+  double *G, *t, *x;
+  cudaMalloc(&G, sizeof(double) * hg.size());
+  cudaMalloc(&t, sizeof(double) * ht.size());
+  cudaMalloc(&x, sizeof(double) * ht.size());
+  cudaMemcpy(G, hg.data(), sizeof(double) * hg.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(t, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice);
+  const size_t smem = sizeof(double) * (kSlots * Thomas<CB>::PLANE + 2 * C) + sizeof(ThomasSmem<CB>) + 256;
+  const double gb = (double)sizeof(double) * per * nb / 1e9;
+  const float t0 = run<0>(G, t, x, nb, smem), t1 = run<1>(G, t, x, nb, smem), t2 = run<2>(G, t, x, nb, smem);
+  printf("threads %d smem %zu KB  G %.0f MB\n", Thomas<CB>::NT, smem >> 10, gb * 1e3);
+  printf("real   %7.1f us  (%.0f GB/s of G)\n", t0, gb / (t0 * 1e-6));
+  printf("L2     %7.1f us\n", t1);
+  printf("copy   %7.1f us  (%.0f GB/s of G)\n", t2, gb / (t2 * 1e-6));
+  double* buf;
+  cudaMalloc(&buf, (size_t)512 << 20);
+  for (size_t mb : {0, 32, 64, 128, 256})
+    printf("after %3zu MB dirty: real %7.1f us\n", mb, run_after_dirty(G, t, x, nb, smem, buf, mb));
+  cudaError_t err = cudaGetLastError();
+  printf("%s\n", cudaGetErrorString(err));
+  return 0;
+}
