@@ -129,6 +129,7 @@ struct tmg_ctx {
   double* symvP = nullptr;  // single slab: GEMV partials
   double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
   double *rcc = nullptr, *ecc = nullptr;  // full-length cc vectors (one per process)
+  unsigned int* gbar = nullptr;           // grid-barrier state of the fused coarse kernel
   int hist_cap = 0;
   PcgState* h_state = nullptr;  // pinned, 2 slots
   // graph
@@ -442,6 +443,17 @@ int finish_problem(tmg_ctx* c) {
     c->kcount += (n_kernels);   \
   } while (0)
 
+// single slab: coarse + coarse-coarse levels as one cooperative kernel
+void enqueue_coarse_single(tmg_ctx* c) {
+  Slab& s = c->slabs[0];
+  if (getenv("TMG_UNFUSED_COARSE") || !coarse_fused_supported(s.g, c->n_cc))
+    KL(7, launch_coarse_cycle(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc,
+                              s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream));
+  else
+    KL(1, launch_coarse_fused(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc,
+                              s.rc, s.rc0, c->rcc, s.rc1, s.ec, c->gbar, c->stream));
+}
+
 // single slab: the fused path (device-side scalars, symmetric tiled A_cc GEMV)
 void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
@@ -450,8 +462,7 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.st, s.partials,
                       s.history, init, st));
   KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
-  KL(7, launch_coarse_cycle(g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc,
-                            s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, st));
+  enqueue_coarse_single(c);
   KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
@@ -625,7 +636,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     const GridParams& g = s.g;
     timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
     timed(2, [&] { KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
-    timed(3, [&] { KL(7, launch_coarse_cycle(g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream)); });
+    timed(3, [&] { enqueue_coarse_single(c); });
     timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_jacobi(c, 1, 0); });
@@ -676,7 +687,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       if (c->kind == TMG_PRECOND_MMG) {
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
-        timed(3, [&] { KL(7, launch_coarse_cycle(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc, s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream)); });
+        timed(3, [&] { enqueue_coarse_single(c); });
         timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_jacobi(c, 0, par); });
@@ -861,6 +872,8 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
         CK(cudaMemset(v + s.bs0 * C, 0, sizeof(double) * (size_t)(s.nbs * C)));
     }
     CK(cudaMallocHost(&c->h_state, 2 * sizeof(PcgState)));
+    c->gbar = dalloc<unsigned int>(c, 2);
+    CK(cudaMemset(c->gbar, 0, 2 * sizeof(unsigned int)));
     CK(cudaDeviceSynchronize());
   });
   if (rc) {

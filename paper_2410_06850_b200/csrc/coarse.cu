@@ -13,6 +13,7 @@
 // level and is assembled densely for the direct solve.
 #include "kernels.h"
 #include "stencil.cuh"
+#include "symv.cuh"
 
 namespace tmg {
 
@@ -408,6 +409,28 @@ __device__ __forceinline__ double coarse_apply_row(const GridParams& g, const do
   return s;
 }
 
+// coarse_apply_row reading x through L2 only (x written by other CTAs of the
+// same cooperative grid)
+__device__ __forceinline__ double coarse_apply_row_cg(const GridParams& g,
+                                                      const double* __restrict__ Ac,
+                                                      const double* x, int I, int a) {
+  const int nbx = (int)g.nbx, nby = (int)g.nby, nbz = (int)g.nbz;
+  const int bi = I % nbx, bj = (I / nbx) % nby, bk = I / (nbx * nby);
+  const int nb[7] = {I, bi > 0 ? I - 1 : -1, bi + 1 < nbx ? I + 1 : -1,
+                     bj > 0 ? I - nbx : -1, bj + 1 < nby ? I + nbx : -1,
+                     bk > 0 ? I - nbx * nby : -1, bk + 1 < nbz ? I + nbx * nby : -1};
+  double s = 0.0;
+#pragma unroll
+  for (int dir = 0; dir < 7; ++dir) {
+    if (nb[dir] < 0) continue;
+    const double* blk = Ac + ((size_t)I * 7 + dir) * LC * LC + a * LC;
+    const double* xv = x + (size_t)nb[dir] * LC;
+#pragma unroll
+    for (int b = 0; b < LC; ++b) s = fma(blk[b], __ldcg(xv + b), s);
+  }
+  return s;
+}
+
 // out_E = add_E + Winv_E in_E  (coarse_blocks_by_cc smoother, one sweep from 0:
 // solver.cpp:221-243). Winv is symmetric: column i read coalesced.
 __global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
@@ -494,7 +517,189 @@ __global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
   out[k] = rc[k] - coarse_apply_row(g, Ac, x, k / LC, k % LC);
 }
 
+// ---------------------------------------- fused coarse level (one kernel)
+//
+// The whole coarse part of one V-cycle for a single-slab context as one
+// cooperative persistent kernel: one warp per cc element (q = sd^3 L_c <= 32
+// dofs, lane i = dof i), four grid barriers between the phases that need
+// other elements' results, and the symmetric tiled A_cc^-1 GEMV in the middle
+// (its constant tiles start streaming at kernel entry). Replaces seven
+// launch-latency-bound kernels (launch_coarse_cycle).
+//   1  rc0 = W rc                      (solver.cpp:292-296)
+//   2  rcc = R_cc (rc - A_c rc0)       (:297-301)
+//   3  P   = tiles of A_cc^-1 . rcc    (:304)
+//   4  ecc = sum_J P; rc1 = rc0 + R_cc^T ecc   (:307-309)
+//   5  ec  = rc1 + W (rc - A_c rc1)    (:311-319)
+// Grid-wide barrier for a co-resident (cooperative) grid: arrive on a global
+// counter; the last CTA resets it and bumps the generation every other CTA
+// waits on. Data other CTAs wrote before the barrier is read afterwards with
+// L2-only loads (__ldcg), so no L1 invalidation is needed.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int my = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == my) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int Q, int LCC>
+__global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int* __restrict__ done,
+                                                        const double* __restrict__ Ac,
+                                                        const double* __restrict__ Winv,
+                                                        const double* __restrict__ Rcc,
+                                                        const double* __restrict__ T, int64_t n,
+                                                        double* P, const double* __restrict__ rc,
+                                                        double* rc0, double* rcc, double* rc1,
+                                                        double* ec, unsigned int* bar) {
+  static_assert(Q == 32, "one lane per element dof");
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>(smraw);
+  double* xs = ring + kSymvSlots * TS * TS;
+  __shared__ SymvSmem ss;
+  symv_begin(ss, ring, T, n);  // constant tiles stream while phases 1-2 run
+  pdl_wait();
+  if (*done) {  // same flag for every CTA: no barrier is left half-entered
+    symv_drain(ss, n);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  // element e -> warp (e / gridDim.x) of CTA (e % gridDim.x): spread over every SM
+  const int64_t w0 = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t e_end = g.e0 + g.neo;
+  // every phase first issues all of its loads (one round trip), then computes
+  // 1: rc0 = W rc
+  for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
+    const ElemDofs d = elem_dof(g, (int)e, lane);
+    const size_t gi = (size_t)d.brick * LC + d.a;
+    const double* W = Winv + (size_t)e * Q * Q;
+    double wcol[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) wcol[j] = W[(size_t)j * Q + lane];  // W symmetric: column = row
+    const double xin = rc[gi];
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < Q; j += 2) {
+      s0 = fma(wcol[j], __shfl_sync(0xffffffffu, xin, j), s0);
+      s1 = fma(wcol[j + 1], __shfl_sync(0xffffffffu, xin, j + 1), s1);
+    }
+    rc0[gi] = s0 + s1;
+  }
+  grid_barrier(bar);
+  // 2: rcc = R_cc (rc - A_c rc0)
+  for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
+    const ElemDofs d = elem_dof(g, (int)e, lane);
+    double rr[LCC];
+#pragma unroll
+    for (int b = 0; b < LCC; ++b) rr[b] = Rcc[((size_t)e * LCC + b) * Q + lane];
+    const double wc = rc[(size_t)d.brick * LC + d.a] - coarse_apply_row_cg(g, Ac, rc0, d.brick, d.a);
+#pragma unroll
+    for (int b = 0; b < LCC; ++b) {
+      const double v = warp_sum(rr[b] * wc);
+      if (lane == b) rcc[(size_t)e * LCC + b] = v;
+    }
+  }
+  grid_barrier(bar);
+  // 3: tile partials of A_cc^-1 rcc
+  symv_run(ss, ring, xs, T, n, rcc, P);
+  grid_barrier(bar);
+  // 4: ecc rows of the element (fixed-order sums over the nt tile columns), rc1
+  const int64_t nt = (n + TS - 1) / TS;
+  for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
+    const ElemDofs d = elem_dof(g, (int)e, lane);
+    const size_t gi = (size_t)d.brick * LC + d.a;
+    double rr[LCC], pv[LCC][2];
+#pragma unroll
+    for (int b = 0; b < LCC; ++b) {
+      rr[b] = Rcc[((size_t)e * LCC + b) * Q + lane];
+      const int64_t row = e * LCC + b, I = row / TS, r = row % TS;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t J = lane + 32 * h;
+        pv[b][h] = J < nt ? __ldcg(P + (I * nt + J) * TS + r) : 0.0;
+      }
+    }
+    const double r0v = __ldcg(rc0 + gi);
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < LCC; ++b) s = fma(rr[b], warp_sum(pv[b][0] + pv[b][1]), s);
+    rc1[gi] = r0v + s;
+    if (nt > 64) __trap();  // two tile columns per lane (n_cc <= 4096)
+  }
+  grid_barrier(bar);
+  // 5: ec = rc1 + W (rc - A_c rc1)
+  for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
+    const ElemDofs d = elem_dof(g, (int)e, lane);
+    const size_t gi = (size_t)d.brick * LC + d.a;
+    const double* W = Winv + (size_t)e * Q * Q;
+    double wcol[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) wcol[j] = W[(size_t)j * Q + lane];
+    const double tcv = rc[gi] - coarse_apply_row_cg(g, Ac, rc1, d.brick, d.a);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < Q; j += 2) {
+      s0 = fma(wcol[j], __shfl_sync(0xffffffffu, tcv, j), s0);
+      s1 = fma(wcol[j + 1], __shfl_sync(0xffffffffu, tcv, j + 1), s1);
+    }
+    ec[gi] = __ldcg(rc1 + gi) + (s0 + s1);
+  }
+}
+
+// true when launch_coarse_fused handles the hierarchy (q = 32, L_cc = 8, n_cc <= 4096)
+bool coarse_fused_supported(const GridParams& g, int64_t n_cc) {
+  return g.sd * g.sd * g.sd * LC == 32 && g.lcc == 8 && n_cc <= 64 * TS;
+}
+
 // ------------------------------------------------------------- launchers
+
+void launch_coarse_fused(const GridParams& g, const int* done, const double* Ac,
+                         const double* Winv, const double* Rcc, const double* Acc_tiles,
+                         double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
+                         double* rcc, double* rc1, double* ec, unsigned int* bar,
+                         cudaStream_t s) {
+  const size_t smem = symv_dyn_smem(n_cc);
+  static int grid = 0;
+  static size_t grid_smem = 0;
+  if (!grid || grid_smem != smem) {
+    cudaFuncSetAttribute(k_coarse_fused<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_fused<32, 8>, 256, smem);
+    grid = (per < 1 ? 1 : per) * sms;
+    grid_smem = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_coarse_fused<32, 8>, g, done, Ac, Winv, Rcc, Acc_tiles, n_cc, symv_partials,
+                     rc, rc0, rcc, rc1, ec, bar);
+}
 
 void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                           const double* phi, double* Ac, double* Bc, cudaStream_t s) {

@@ -9,6 +9,7 @@
 // GEMV — a single wide kernel instead of two latency-bound triangular solves.
 #include "kernels.h"
 #include "tma.cuh"
+#include "symv.cuh"
 
 namespace tmg {
 
@@ -275,126 +276,31 @@ __global__ void __launch_bounds__(256) k_gemv(const int* __restrict__ done,
 }
 
 // ------------------------------------------------ symmetric tiled GEMV
-//
-// A_cc^-1 is symmetric: only its lower block-triangle of 64 x 64 tiles is kept
-// (tile (I, J <= I) at I(I+1)/2 + J, row-major, zero padded), halving the
-// bytes streamed per V-cycle. Pass 1: one CTA per tile computes the tile's
-// row products (contribution to y_I) and, off the diagonal, its column
-// products (contribution to y_J) into a partial buffer P[I][J][64]; pass 2
-// sums the nt partials of every output in a fixed order (deterministic).
-constexpr int TS = 64;
-
-__global__ void k_pack_sym_tiles(const double* __restrict__ A, int64_t n, double* T) {
-  const int64_t nt = (n + TS - 1) / TS;
-  const int64_t tile = blockIdx.x;
-  int64_t I = 0;
-  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
-  const int64_t J = tile - I * (I + 1) / 2;
-  (void)nt;
-  for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) {
-    const int64_t r = I * TS + e / TS, c = J * TS + e % TS;
-    T[tile * TS * TS + e] = (r < n && c < n) ? A[r * n + c] : 0.0;
-  }
-}
-
-// Persistent: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...; each
-// 32 KB tile arrives by TMA bulk copy into a kSymvSlots-deep shared ring
-// (128 KB in flight per SM: enough for one SM's share of HBM bandwidth at
-// loaded latency).
-#ifndef TMG_SYMV_SLOTS
-#define TMG_SYMV_SLOTS 2
-#endif
-constexpr int kSymvSlots = TMG_SYMV_SLOTS;
+// (symv.cuh). Persistent: one or two CTAs per SM.
 __global__ void __launch_bounds__(256) k_symv_tiles(const int* __restrict__ done,
                                                     const double* __restrict__ T, int64_t n,
                                                     const double* __restrict__ x, double* P) {
   pdl_trigger();
   extern __shared__ __align__(128) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);  // kSymvSlots x TS*TS
-  const int64_t nt = (n + TS - 1) / TS;
   double* xs = ring + kSymvSlots * TS * TS;         // all of x, zero padded to nt*TS
-  __shared__ uint64_t bars[kSymvSlots];
-  __shared__ double colp[4][TS];
-  const int64_t ntiles = nt * (nt + 1) / 2;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  constexpr uint32_t kTileBytes = TS * TS * sizeof(double);
-  if (t == 0) {
-    for (int k = 0; k < kSymvSlots; ++k) mbar_init(&bars[k], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int64_t tile, int slot) {
-    mbar_arrive_expect_tx(&bars[slot], kTileBytes);
-    bulk_g2s(ring + slot * TS * TS, T + tile * TS * TS, kTileBytes, &bars[slot]);
-  };
-  int64_t tile = blockIdx.x;
-  // the tiles are constant: start streaming them before the dependency wait
-  if (t == 0)
-    for (int k = 0; k < kSymvSlots; ++k)
-      if (tile + k * (int64_t)gridDim.x < ntiles) issue(tile + k * gridDim.x, k);
+  __shared__ SymvSmem ss;
+  symv_begin(ss, ring, T, n);  // constant tiles: before the dependency wait
   pdl_wait();
   if (done && *done) {
-    if (t == 0)  // drain the issued copies before exiting
-      for (int k = 0; k < kSymvSlots; ++k)
-        if (tile + k * (int64_t)gridDim.x < ntiles) mbar_wait(&bars[k], 0);
+    symv_drain(ss, n);
     return;
   }
-  for (int64_t k = t; k < nt * TS; k += blockDim.x) xs[k] = k < n ? x[k] : 0.0;
-  __syncthreads();
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int slot = it % kSymvSlots;
-    int64_t I = 0;
-    while ((I + 1) * (I + 2) / 2 <= tile) ++I;
-    const int64_t J = tile - I * (I + 1) / 2;
-    const double* xi = xs + I * TS;
-    const double* xj = xs + J * TS;
-    mbar_wait(&bars[slot], (uint32_t)((it / kSymvSlots) & 1));
-    __syncthreads();
-    const double* A = ring + slot * TS * TS;
-    // row products: warp w owns rows 8w..8w+7; lane l covers columns l, l+32
-    {
-      double pr[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double* row = A + (8 * warp + k) * TS;
-        pr[k] = fma(row[lane], xj[lane], row[lane + 32] * xj[lane + 32]);
-      }
-      // reduce-scatter over 32 lanes: 8 -> 4 -> 2 -> 1 values, then 2 more folds
-      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-      double c4[4], c2[2];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        c4[k] = (b16 ? pr[k + 4] : pr[k]) + __shfl_xor_sync(0xffffffffu, b16 ? pr[k] : pr[k + 4], 16);
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        c2[k] = (b8 ? c4[k + 2] : c4[k]) + __shfl_xor_sync(0xffffffffu, b8 ? c4[k] : c4[k + 2], 8);
-      double c1 = (b4 ? c2[1] : c2[0]) + __shfl_xor_sync(0xffffffffu, b4 ? c2[0] : c2[1], 4);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, 2);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, 1);
-      // lane with bits (b16 b8 b4) holds row 8w + 4*b16 + 2*b8 + b4
-      if ((lane & 3) == 0) {
-        const int k = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
-        P[(I * nt + J) * TS + 8 * warp + k] = c1;
-      }
-    }
-    // column products (off-diagonal tiles): thread (group g, column c)
-    if (I != J) {
-      const int c = t & (TS - 1), gq = t >> 6;
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int r = 0; r < 16; r += 2) {
-        s0 = fma(A[(16 * gq + r) * TS + c], xi[16 * gq + r], s0);
-        s1 = fma(A[(16 * gq + r + 1) * TS + c], xi[16 * gq + r + 1], s1);
-      }
-      colp[gq][c] = s0 + s1;
-    }
-    __syncthreads();  // ring slot and xi/xj/colp consumed
-    if (I != J && t < TS) P[(J * nt + I) * TS + t] = (colp[0][t] + colp[1][t]) + (colp[2][t] + colp[3][t]);
-    if (t == 0 && tile + kSymvSlots * (int64_t)gridDim.x < ntiles) {
-      fence_proxy_async_smem();
-      issue(tile + kSymvSlots * gridDim.x, slot);
-    }
-    __syncthreads();
+  symv_run(ss, ring, xs, T, n, x, P);
+}
+
+__global__ void k_pack_sym_tiles(const double* __restrict__ A, int64_t n, double* T) {
+  const int64_t tile = blockIdx.x;
+  int64_t I, J;
+  symv_tile_ij(tile, I, J);
+  for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) {
+    const int64_t r = I * TS + e / TS, c = J * TS + e % TS;
+    T[tile * TS * TS + e] = (r < n && c < n) ? A[r * n + c] : 0.0;
   }
 }
 
@@ -435,7 +341,7 @@ void launch_symv(const int* done, const double* T, int64_t n, const double* x, d
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(double) * (size_t)(kSymvSlots * TS * TS + nt * TS);
+  const size_t smem = symv_dyn_smem(n);
   cudaFuncSetAttribute(k_symv_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   static int per_sm = 0;
   if (!per_sm) {

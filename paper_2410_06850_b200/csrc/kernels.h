@@ -98,6 +98,13 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
                          cudaStream_t s);
 
+// the same cycle as one cooperative kernel (single slab; q = 32, L_cc = 8)
+bool coarse_fused_supported(const GridParams& g, int64_t n_cc);
+void launch_coarse_fused(const GridParams& g, const int* done, const double* Ac,
+                         const double* Winv, const double* Rcc, const double* Acc_tiles,
+                         double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
+                         double* rcc, double* rc1, double* ec, unsigned int* bar,
+                         cudaStream_t s);
 void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
                           const double* in, const double* add, double* out, cudaStream_t s);
 void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
