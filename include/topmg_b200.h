@@ -129,6 +129,18 @@ int tmg_set_conductivity(tmg_ctx* ctx, const double* kappa, const tmg_patch* pat
  * conductivity (material.cpp:8-15,45-59). */
 int tmg_set_design(tmg_ctx* ctx, const double* rho, double kappa_lo, double kappa_hi, int p,
                    const tmg_patch* patches, int npatches);
+/* interpolate_design (grid.cpp:220-241) on the device: piecewise-constant
+ * prolongation of a field on a coarser grid n_lo[3] (x-fastest; every axis
+ * an integer factor of the context's grid, else TMG_ECONFIG).
+ * tmg_set_x0_interpolated: into the resident x, the warm start of the next
+ *   tmg_solve_resident(..., use_x0 = 1) (a coarse solve's T as initial guess).
+ * tmg_set_design_interpolated: prolongs rho, then as tmg_set_design (the
+ *   continuation step of optimize, optim.cpp:288-295). */
+int tmg_set_x0_interpolated(tmg_ctx* ctx, const double* x_lo, const int64_t* n_lo);
+int tmg_set_design_interpolated(tmg_ctx* ctx, const double* rho_lo, const int64_t* n_lo,
+                                double kappa_lo, double kappa_hi, int p,
+                                const tmg_patch* patches, int npatches);
+
 /* The rhs of assemble_system (fvm.cpp:63-112): f*vol + Dirichlet terms.
  * source may be NULL (f = 0). */
 int tmg_assemble_rhs(tmg_ctx* ctx, const double* source, double* rhs_out);

@@ -1008,6 +1008,69 @@ int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,
   return finish_problem(c);
 }
 
+// interpolate_design's checks (grid.cpp:223-231); uploads the coarse field
+int interp_prepare(tmg_ctx* c, const double* lo, const int64_t* nlo, double** dlo) {
+  if (!c || !lo || !nlo) return set_err(c, TMG_EARG, "interpolate_design: null argument");
+  const int64_t nhi[3] = {c->grid.nx, c->grid.ny, c->grid.nz};
+  for (int a = 0; a < 3; ++a)
+    if (nlo[a] <= 0 || nhi[a] % nlo[a] != 0)
+      return set_err(c, TMG_ECONFIG, "interpolate_design: non-integer refinement factor");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    const int64_t m = nlo[0] * nlo[1] * nlo[2];
+    *dlo = dalloc<double>(c, m);
+    CK(cudaMemcpyAsync(*dlo, lo, sizeof(double) * (size_t)m, cudaMemcpyHostToDevice, c->stream));
+  });
+}
+
+int tmg_set_x0_interpolated(tmg_ctx* c, const double* x_lo, const int64_t* n_lo) {
+  double* dlo = nullptr;
+  int rc = interp_prepare(c, x_lo, n_lo, &dlo);
+  if (rc) return rc;
+  rc = guard(c, [&] {
+    for (Slab& s : c->slabs) {
+      launch_interpolate(s.g, c->cb, dlo, n_lo, s.x, c->stream);
+      CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+  dfree(c, dlo);
+  return rc;
+}
+
+int tmg_set_design_interpolated(tmg_ctx* c, const double* rho_lo, const int64_t* n_lo, double lo,
+                                double hi, int p, const tmg_patch* patches, int np) {
+  if (!(lo > 0.0) || !(hi > lo))  // material.cpp:11-12
+    return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
+  if (p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
+  int rc = validate_patches(c, patches, np);
+  if (rc) return rc;
+  const int64_t m = n_lo ? n_lo[0] * n_lo[1] * n_lo[2] : 0;
+  for (int64_t i = 0; rho_lo && i < m; ++i) {
+    double r = 1.0;
+    for (int k = 0; k < p; ++k) r *= rho_lo[i];
+    if (!(lo + r * (hi - lo) > 0.0))
+      return set_err(c, TMG_ECONFIG, "assemble_system: conductivity must be positive");
+  }
+  double* dlo = nullptr;
+  rc = interp_prepare(c, rho_lo, n_lo, &dlo);
+  if (rc) return rc;
+  c->patches.clear();
+  for (int i = 0; i < np; ++i)
+    c->patches.push_back(Patch{patches[i].face, patches[i].u0, patches[i].v0, patches[i].u1,
+                               patches[i].v1, patches[i].value});
+  rc = guard(c, [&] {
+    for (Slab& s : c->slabs) {
+      launch_interpolate(s.g, c->cb, dlo, n_lo, s.r, c->stream);  // r as scratch for rho
+      launch_conductivity(s.g, c->cb, s.r, s.kappa, lo, hi, p, c->stream);
+      CK(cudaGetLastError());
+    }
+  });
+  dfree(c, dlo);
+  if (rc) return rc;
+  return finish_problem(c);
+}
+
 int tmg_assemble_rhs(tmg_ctx* c, const double* source, double* rhs_out) {
   if (!c || !rhs_out) return set_err(c, TMG_EARG, "tmg_assemble_rhs: null argument");
   if (!c->have_problem) return set_err(c, TMG_EARG, "tmg_assemble_rhs: no problem set");

@@ -64,6 +64,9 @@ struct FinArgs {
 // operator.cu
 void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
 void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s);
+// interpolate_design (grid.cpp:220-241) into the own cells of dst
+void launch_interpolate(const GridParams& g, int cb, const double* lo, const int64_t* nlo,
+                        double* dst, cudaStream_t s);
 void launch_conductivity(const GridParams& g, int cb, const double* x, double* kappa, double lo,
                          double hi, int p, cudaStream_t s);
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,

@@ -32,6 +32,20 @@ __global__ void k_from_brick(GridParams g, int cb, const double* __restrict__ sr
     dst[brick_to_global(g, cb, s) - xoff] = src[s];
 }
 
+// interpolate_design (grid.cpp:220-241): piecewise-constant prolongation of a
+// field on an (nxl, nyl, nzl) grid by integer factors, into this context's
+// own cells (brick layout).
+__global__ void k_interpolate(GridParams g, int cb, const double* __restrict__ lo, int64_t nxl,
+                              int64_t nyl, int64_t fx, int64_t fy, int64_t fz, double* dst,
+                              int64_t s0, int64_t m) {
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gx = brick_to_global(g, cb, s);
+    const int64_t i = gx % g.nx, j = (gx / g.nx) % g.ny, k = gx / (g.nx * g.ny);
+    dst[s] = lo[(i / fx) + nxl * ((j / fy) + nyl * (k / fz))];
+  }
+}
+
 // material.cpp:45-59 — kappa = lo + x^p (hi - lo), repeated multiply
 __global__ void k_conductivity(const double* __restrict__ x, double* kappa, int64_t s0, int64_t m,
                                double lo, double hi, int p) {
@@ -151,6 +165,12 @@ void launch_from_brick(const GridParams& g, int cb, const double* src, double* d
                        cudaStream_t s) {
   const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
   k_from_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, g.b0 * C, m, slab_xoff(g, cb));
+}
+void launch_interpolate(const GridParams& g, int cb, const double* lo, const int64_t* nlo,
+                        double* dst, cudaStream_t s) {
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_interpolate<<<grid1d(m), 256, 0, s>>>(g, cb, lo, nlo[0], nlo[1], g.nx / nlo[0], g.ny / nlo[1],
+                                          g.nz / nlo[2], dst, g.b0 * C, m);
 }
 void launch_conductivity(const GridParams& g, int cb, const double* x, double* kappa, double lo,
                          double hi, int p, cudaStream_t s) {

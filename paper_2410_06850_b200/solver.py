@@ -92,7 +92,7 @@ EXPORTED_SYMBOLS = (
     "tmg_download_solution", "tmg_get_local_bases", "tmg_get_coarse_operator",
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
     "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
-    "tmg_create_dist", "tmg_partition",
+    "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
 )
 
 
@@ -284,6 +284,24 @@ class Context:
         parr, n = boundary._c()
         self._check(native().tmg_set_design(self._p, _ptr(r), C.c_double(kappa_lo),
                                             C.c_double(kappa_hi), C.c_int(p), parr, C.c_int(n)))
+
+    def set_design_interpolated(self, rho_lo, shape_lo, kappa_lo, kappa_hi=1.0, p=3,
+                                boundary: BoundarySpec = None):
+        """interpolate_design (grid.cpp:220-241) of a coarser design on the
+        device, then set_design."""
+        r = _f64(rho_lo)
+        n = (C.c_int64 * 3)(*shape_lo)
+        parr, npat = boundary._c()
+        self._check(native().tmg_set_design_interpolated(
+            self._p, _ptr(r), n, C.c_double(kappa_lo), C.c_double(kappa_hi), C.c_int(p), parr,
+            C.c_int(npat)))
+
+    def set_x0_interpolated(self, x_lo, shape_lo):
+        """Warm start for solve_resident(use_x0=True): a coarser grid's field
+        prolonged on the device (interpolate_design semantics)."""
+        xx = _f64(x_lo)
+        n = (C.c_int64 * 3)(*shape_lo)
+        self._check(native().tmg_set_x0_interpolated(self._p, _ptr(xx), n))
 
     def assemble_rhs(self, source=None):
         out = np.empty(self.cells)
