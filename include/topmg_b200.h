@@ -141,6 +141,14 @@ int tmg_set_design_interpolated(tmg_ctx* ctx, const double* rho_lo, const int64_
                                 double kappa_lo, double kappa_hi, int p,
                                 const tmg_patch* patches, int npatches);
 
+/* sensitivity (optim.cpp:21-84) on the device: the adjoint gradient of the
+ * mean temperature per cell for design rho, state t and adjoint u (the LS2
+ * solution with rhs adjoint_rhs = 1/M, optim.cpp:16-19), with the
+ * MaterialModel (kappa_lo, kappa_hi, f0, p) and the context's conductivity
+ * and Dirichlet patches. Bitwise equal to the reference. */
+int tmg_sensitivity(tmg_ctx* ctx, const double* rho, double kappa_lo, double kappa_hi, double f0,
+                    int p, const double* t, const double* u, double* grad);
+
 /* The rhs of assemble_system (fvm.cpp:63-112): f*vol + Dirichlet terms.
  * source may be NULL (f = 0). */
 int tmg_assemble_rhs(tmg_ctx* ctx, const double* source, double* rhs_out);

@@ -277,12 +277,96 @@ def ref():
         R.ref_ctx_create_grid.argtypes = [I64, I64, I64, C.c_double, C.c_double, C.c_double,
                                           I64, I64, I64, I64, DP, C.c_int, DP, C.c_int, C.c_int,
                                           C.c_int, I64, I64, C.c_int, DP]
+        R.ref_sensitivity.argtypes = [I64, I64, I64, C.c_double, C.c_double, C.c_double, DP,
+                                      C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, DP,
+                                      DP, DP, DP]
         R.ref_ctx_pcg.argtypes = [C.c_void_p, C.c_double, C.c_int, DP, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), DP]
         R.ref_ctx_destroy.argtypes = [C.c_void_p]
         R.ref_num_threads.restype = C.c_int
         _REF = R
     return _REF
+
+
+def sensitivity(n, rho, t, u, kappa_lo, kappa_hi=1.0, f0=1.0, p=3, patches=None,
+                extent=(1.0, 1.0, 1.0)):
+    """Restatement of topmg::sensitivity (optim.cpp:21-84) in numpy, same
+    operation order (elementwise, no contraction)."""
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    hx, hy, hz = extent[0] / nx, extent[1] / ny, extent[2] / nz
+    vol = hx * hy * hz
+    cpl = (hy * hz / hx, hx * hz / hy, hx * hy / hz)
+    rho3 = np.asarray(rho, dtype=float).reshape(nz, ny, nx)
+    t3 = np.asarray(t, dtype=float).reshape(nz, ny, nx)
+    u3 = np.asarray(u, dtype=float).reshape(nz, ny, nx)
+    # material.cpp:45-74 (int_pow by repeated multiply)
+    xp = np.ones_like(rho3)
+    for _ in range(p):
+        xp = xp * rho3
+    kap = kappa_lo + xp * (kappa_hi - kappa_lo)
+    xp1 = np.ones_like(rho3)
+    if p >= 2:
+        for _ in range(p - 1):
+            xp1 = xp1 * rho3
+    dk = float(p) * xp1 * (kappa_hi - kappa_lo)
+    dsrc = -float(p) * xp1 * f0
+    val = u3 * dsrc * vol
+    on = dk != 0.0
+    patches = patches if patches is not None else bottom_center_patch()
+    for a in range(3):
+        ax = 2 - a  # array axis of coordinate a
+        n_a = (nx, ny, nz)[a]
+        for side in (0, 1):
+            sl_c = [slice(None)] * 3
+            sl_n = [slice(None)] * 3
+            if side == 0:
+                sl_c[ax], sl_n[ax] = slice(1, n_a), slice(0, n_a - 1)
+            else:
+                sl_c[ax], sl_n[ax] = slice(0, n_a - 1), slice(1, n_a)
+            sc, sn = tuple(sl_c), tuple(sl_n)
+            kc, kn = kap[sc], kap[sn]
+            kf = 2.0 * kc * kn / (kc + kn)
+            ratio = kf / kc
+            dt = 0.5 * ratio * ratio * dk[sc] * cpl[a]
+            term = dt * (u3[sc] - u3[sn]) * (t3[sc] - t3[sn])
+            v = val[sc]
+            val[sc] = np.where(on[sc], v - term, v)
+        for side in (0, 1):
+            face = 2 * a + side
+            sl = [slice(None)] * 3
+            sl[ax] = slice(0, 1) if side == 0 else slice(n_a - 1, n_a)
+            sl = tuple(sl)
+            # boundary-face centres of the layer (grid.cpp:61-75)
+            k_i, j_i, i_i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+            cx, cy, cz = (i_i[sl] + 0.5) * hx, (j_i[sl] + 0.5) * hy, (k_i[sl] + 0.5) * hz
+            uu, vv = ((cy, cz), (cx, cz), (cx, cy))[a]
+            td = np.zeros(uu.shape)
+            hit = np.zeros(uu.shape, dtype=bool)
+            for (f, u0, v0, u1, v1, value) in patches:
+                if f != face:
+                    continue
+                m = (~hit) & (uu >= u0) & (uu <= u1) & (vv >= v0) & (vv <= v1)
+                td[m] = value
+                hit |= m
+            dtd = 2.0 * cpl[a] * dk[sl]
+            add = dtd * u3[sl] * (td - t3[sl])
+            val[sl] = np.where(hit & on[sl], val[sl] + add, val[sl])
+    return val.ravel()
+
+
+def ref_sensitivity(n, rho, t, u, kappa_lo, kappa_hi=1.0, f0=1.0, p=3, patches=None,
+                    extent=(1.0, 1.0, 1.0)):
+    """topmg::sensitivity (optim.cpp:21-84) of the compiled reference."""
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    patches = patches if patches is not None else bottom_center_patch()
+    pa = _patch_array(patches)
+    out = np.empty(nx * ny * nz)
+    R = ref()
+    _ref_check(R.ref_sensitivity(nx, ny, nz, *extent, _d(np.ascontiguousarray(rho, dtype=float)),
+                                 kappa_lo, kappa_hi, f0, p, len(patches), _d(pa),
+                                 _d(np.ascontiguousarray(t, dtype=float)),
+                                 _d(np.ascontiguousarray(u, dtype=float)), _d(out)))
+    return out
 
 
 def _ref_check(rc):

@@ -17,6 +17,7 @@
 #include "topmg/fvm.hpp"
 #include "topmg/grid.hpp"
 #include "topmg/material.hpp"
+#include "topmg/optim.hpp"
 #include "topmg/parallel.hpp"
 #include "topmg/rng.hpp"
 #include "topmg/solver.hpp"
@@ -274,5 +275,23 @@ int ref_ctx_pcg(void* ctx, double rtol, int maxit, double* x_out, int* iteration
 }
 
 void ref_ctx_destroy(void* ctx) { delete static_cast<RefCtx*>(ctx); }
+
+// topmg::sensitivity (optim.cpp:21-84) on a design rho with MaterialModel
+// (klo, khi, f0, p), state t and adjoint u.
+int ref_sensitivity(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                    const double* rho, double klo, double khi, double f0, int p, int npatch,
+                    const double* patches, const double* t, const double* u, double* grad) {
+  return guarded([&] {
+    const GridSpec g(nx, ny, nz, lx, ly, lz);
+    const index_t m = g.num_cells();
+    const DesignField x(g, std::vector<double>(rho, rho + m));
+    const MaterialModel mm(klo, khi, f0, p);
+    const AssembledSystem sys =
+        assemble_system(g, conductivity(x, mm), heat_source(x, mm), make_bc(npatch, patches));
+    const std::vector<double> gr =
+        sensitivity(x, mm, sys, std::vector<double>(t, t + m), std::vector<double>(u, u + m));
+    std::copy(gr.begin(), gr.end(), grad);
+  });
+}
 
 }  // extern "C"

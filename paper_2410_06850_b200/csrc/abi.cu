@@ -1071,6 +1071,32 @@ int tmg_set_design_interpolated(tmg_ctx* c, const double* rho_lo, const int64_t*
   return finish_problem(c);
 }
 
+int tmg_sensitivity(tmg_ctx* c, const double* rho, double kappa_lo, double kappa_hi, double f0,
+                    int p, const double* t, const double* u, double* grad) {
+  if (!c || !rho || !t || !u || !grad) return set_err(c, TMG_EARG, "sensitivity: null argument");
+  if (!c->have_problem) return set_err(c, TMG_EARG, "sensitivity: no problem set");
+  if (!(kappa_lo > 0.0) || !(kappa_hi > kappa_lo))  // material.cpp:11-12
+    return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
+  if (f0 < 0.0) return set_err(c, TMG_ECONFIG, "MaterialModel: f0 must be nonnegative");
+  if (p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    const int64_t C = cells_per_brick(c);
+    UP(rho, r);
+    UP(t, pbuf[0]);
+    UP(u, pbuf[1]);
+    exchange(c, [&](Slab& s) { return (void*)s.pbuf[0]; }, sizeof(double) * C, false);
+    exchange(c, [&](Slab& s) { return (void*)s.pbuf[1]; }, sizeof(double) * C, false);
+    for (Slab& s : c->slabs) {
+      launch_sensitivity(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                         c->grid.ly, c->grid.lz, s.r, s.kappa, s.pbuf[0], s.pbuf[1], kappa_lo,
+                         kappa_hi, f0, p, s.q, c->stream);
+      CK(cudaGetLastError());
+    }
+    DOWN(q, grad);
+  });
+}
+
 int tmg_assemble_rhs(tmg_ctx* c, const double* source, double* rhs_out) {
   if (!c || !rhs_out) return set_err(c, TMG_EARG, "tmg_assemble_rhs: null argument");
   if (!c->have_problem) return set_err(c, TMG_EARG, "tmg_assemble_rhs: no problem set");

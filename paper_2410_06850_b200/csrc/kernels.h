@@ -72,6 +72,11 @@ void launch_conductivity(const GridParams& g, int cb, const double* x, double* k
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
                      double ly, double lz, const double* kappa, const double* source,
                      uint8_t* dmask, double* rhs, unsigned long long* count, cudaStream_t s);
+// sensitivity (optim.cpp:21-84) into grad (own cells; t and u ghosts filled)
+void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
+                        double ly, double lz, const double* rho, const double* kappa,
+                        const double* t, const double* u, double kappa_lo, double kappa_hi,
+                        double f0, int p, double* grad, cudaStream_t s);
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s);
 

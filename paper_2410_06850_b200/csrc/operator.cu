@@ -126,6 +126,67 @@ __global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __re
   }
 }
 
+// sensitivity (optim.cpp:21-84): adjoint gradient of the mean temperature per
+// cell, face by face, in the reference's operation order (no contraction:
+// bitwise). rho = design x, t = state, u = adjoint (brick layout, ghosts of
+// t and u filled), kappa = the system's conductivity.
+__global__ void k_sensitivity(GridParams g, int cb, PatchSet ps, const double* __restrict__ rho,
+                              const double* __restrict__ kappa, const double* __restrict__ t,
+                              const double* __restrict__ u, double kappa_lo, double kappa_hi,
+                              double f0, int p, double* grad, int64_t s0, int64_t m) {
+  const int64_t C = (int64_t)cb * cb * cb;
+  const double dkm = __dsub_rn(kappa_hi, kappa_lo), pd = (double)p;
+  for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = s / C;
+    const int l = (int)(s % C);
+    const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
+    const int li = l % cb, lj = (l / cb) % cb, lk = l / (cb * cb);
+    const int64_t ijk[3] = {bi * cb + li, bj * cb + lj, bk * cb + lk};
+    const int64_t n_axis[3] = {g.nx, g.ny, g.nz};
+    // material_derivatives (material.cpp:61-74)
+    double xp1 = 1.0;
+    if (p >= 2)
+      for (int q = 0; q < p - 1; ++q) xp1 = __dmul_rn(xp1, rho[s]);
+    const double dk = __dmul_rn(__dmul_rn(pd, xp1), dkm);
+    const double dsrc = __dmul_rn(__dmul_rn(-pd, xp1), f0);
+    const double uc = u[s], tc = t[s];
+    double value = __dmul_rn(__dmul_rn(uc, dsrc), g.vol);
+    if (dk != 0.0) {
+      const double kc = kappa[s];
+      const int st_in[3] = {1, cb, cb * cb};
+      const int64_t st_b[3] = {1, g.nbx, g.nbx * g.nby};
+      const int lc3[3] = {li, lj, lk};
+      for (int a = 0; a < 3; ++a) {
+        for (int side = 0; side < 2; ++side) {
+          const bool exists = side == 0 ? ijk[a] > 0 : ijk[a] < n_axis[a] - 1;
+          if (!exists) continue;
+          // neighbour's storage index: inside the brick or across its face
+          int64_t ns;
+          if (side == 0)
+            ns = lc3[a] > 0 ? s - st_in[a] : (b - st_b[a]) * C + (l + (cb - 1) * st_in[a]);
+          else
+            ns = lc3[a] < cb - 1 ? s + st_in[a] : (b + st_b[a]) * C + (l - (cb - 1) * st_in[a]);
+          const double kf = face_t(kc, kappa[ns]);
+          const double ratio = __ddiv_rn(kf, kc);
+          const double dt =
+              __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.5, ratio), ratio), dk), g.cpl[a]);
+          value = __dsub_rn(value, __dmul_rn(__dmul_rn(dt, __dsub_rn(uc, u[ns])),
+                                             __dsub_rn(tc, t[ns])));
+        }
+        for (int side = 0; side < 2; ++side) {
+          double td = 0.0;
+          if (dirichlet_value(g, ps, ijk[0], ijk[1], ijk[2], 2 * a + side, &td)) {
+            const double dt = __dmul_rn(__dmul_rn(2.0, g.cpl[a]), dk);
+            value = __dadd_rn(value, __dmul_rn(__dmul_rn(dt, uc), __dsub_rn(td, tc)));
+          }
+        }
+      }
+    }
+    grad[s] = value;
+  }
+}
+
 // y = A x from the precomputed coefficients (bitwise SparseOperator::apply),
 // optionally dinv = 1/diag (JacobiPreconditioner, solver.cpp:21-29).
 template <int CB>
@@ -186,6 +247,18 @@ void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npat
   ps.lx = lx; ps.ly = ly; ps.lz = lz;
   const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
   k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, g.b0 * C, m, count);
+}
+void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
+                        double ly, double lz, const double* rho, const double* kappa,
+                        const double* t, const double* u, double kappa_lo, double kappa_hi,
+                        double f0, int p, double* grad, cudaStream_t s) {
+  PatchSet ps{};
+  ps.n = npatch;
+  for (int i = 0; i < npatch && i < kMaxPatches; ++i) ps.p[i] = patches[i];
+  ps.lx = lx; ps.ly = ly; ps.lz = lz;
+  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  k_sensitivity<<<grid1d(m), 256, 0, s>>>(g, cb, ps, rho, kappa, t, u, kappa_lo, kappa_hi, f0, p,
+                                          grad, g.b0 * C, m);
 }
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s) {

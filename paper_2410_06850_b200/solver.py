@@ -93,6 +93,7 @@ EXPORTED_SYMBOLS = (
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
     "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
+    "tmg_sensitivity",
 )
 
 
@@ -302,6 +303,15 @@ class Context:
         xx = _f64(x_lo)
         n = (C.c_int64 * 3)(*shape_lo)
         self._check(native().tmg_set_x0_interpolated(self._p, _ptr(xx), n))
+
+    def sensitivity(self, rho, t, u, kappa_lo, kappa_hi=1.0, f0=1.0, p=3):
+        """sensitivity (optim.cpp:21-84) on the device: d(mean T)/d rho."""
+        r, tt, uu = _f64(rho), _f64(t), _f64(u)
+        out = np.empty(self.cells)
+        self._check(native().tmg_sensitivity(self._p, _ptr(r), C.c_double(kappa_lo),
+                                             C.c_double(kappa_hi), C.c_double(f0), C.c_int(p),
+                                             _ptr(tt), _ptr(uu), _ptr(out)))
+        return out
 
     def assemble_rhs(self, source=None):
         out = np.empty(self.cells)

@@ -478,3 +478,22 @@ def test_device_interpolation_slabs():
         outs.append(c.download_solution())
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[0], O.interpolate_design(x_lo, lo, (n, n, n)))
+
+
+@pytest.mark.parametrize("n,p,f0,slabs", [(16, 3, 1.0, 1), (32, 3, 1.0, 2), ((16, 24, 32), 1, 0.5, 1)])
+def test_device_sensitivity_bitwise_vs_reference(n, p, f0, slabs):
+    # sensitivity (optim.cpp:21-84) on the device
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    m = nx * ny * nz
+    rng = np.random.default_rng(40)
+    rho = rng.random(m)
+    rho[rng.random(m) < 0.2] = 0.0
+    t, u = rng.standard_normal(m), rng.standard_normal(m)
+    patches = [(4, 0.2, 0.2, 0.8, 0.8, 1.5), (1, 0.0, 0.0, 0.5, 1.0, -0.5)]
+    bc = BoundarySpec([DirichletPatch(*q) for q in patches])
+    ncc = (nx // 8, ny // 8, nz // 8) if slabs == 1 else 2
+    c = Context(GridSpec(nx, ny, nz), ncc, 2 if slabs > 1 else 1, slabs=slabs) if slabs > 1 \
+        else Context(GridSpec(nx, ny, nz), ncc, 1)
+    c.set_design(rho, 1e-3, 1.0, p, bc)
+    g = c.sensitivity(rho, t, u, 1e-3, 1.0, f0, p)
+    np.testing.assert_array_equal(g, O.ref_sensitivity(n, rho, t, u, 1e-3, 1.0, f0, p, patches))

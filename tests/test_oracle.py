@@ -251,3 +251,49 @@ def test_interpolate_design_mean_preserving():
     hi = O.interpolate_design(lo, 8, 16)
     assert hi.size == 16 ** 3 and abs(hi.mean() - lo.mean()) < 1e-15
     assert hi[0] == lo[0] and hi[1] == lo[0] and hi[2] == lo[1]
+
+
+# ---------------------------------------------------------- sensitivity (§8(f))
+
+@needs_ref
+@pytest.mark.parametrize("n,p,f0", [(8, 3, 1.0), ((6, 8, 10), 1, 0.5), (12, 2, 0.0)])
+def test_sensitivity_restatement_bitwise_vs_reference(n, p, f0):
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    m = nx * ny * nz
+    rng = np.random.default_rng(30)
+    rho = rng.random(m)
+    rho[rng.random(m) < 0.2] = 0.0  # dk == 0 cells (p >= 2)
+    t, u = rng.standard_normal(m), rng.standard_normal(m)
+    patches = [(4, 0.2, 0.2, 0.8, 0.8, 1.5), (1, 0.0, 0.0, 0.5, 1.0, -0.5)]
+    ref = O.ref_sensitivity(n, rho, t, u, 1e-3, 1.0, f0, p, patches)
+    mine = O.sensitivity(n, rho, t, u, 1e-3, 1.0, f0, p, patches)
+    np.testing.assert_array_equal(mine, ref)
+
+
+@needs_ref
+def test_sensitivity_matches_finite_differences():
+    """d(mean T)/d rho_c from the adjoint formula vs central differences of
+    the exactly solved system (grid 6^3, dense solves)."""
+    n, klo, f0, p = 6, 1e-2, 1.0, 3
+    m = n ** 3
+    rng = np.random.default_rng(31)
+    rho = 0.2 + 0.6 * rng.random(m)
+    patches = O.bottom_center_patch(side=0.5)
+
+    def mean_t(r):
+        kap = inputs.conductivity(r, klo)
+        src = f0 * (1.0 - r ** p)  # heat_source (material.cpp:52-58)
+        s = O.System(O.grid(n), kap, src, patches)
+        A = s.matrix.toarray()
+        return np.linalg.solve(A, s.rhs), A
+
+    t, A = mean_t(rho)
+    u = np.linalg.solve(A.T, np.full(m, 1.0 / m))  # adjoint_rhs (optim.cpp:16-19)
+    grad = O.ref_sensitivity(n, rho, t, u, klo, 1.0, f0, p, patches)
+    for c in rng.choice(m, 6, replace=False):
+        h = 1e-6
+        rp, rm = rho.copy(), rho.copy()
+        rp[c] += h
+        rm[c] -= h
+        fd = (mean_t(rp)[0].mean() - mean_t(rm)[0].mean()) / (2 * h)
+        assert abs(fd - grad[c]) <= 1e-5 * abs(grad[c]) + 1e-12
