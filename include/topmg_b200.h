@@ -153,6 +153,44 @@ int tmg_sensitivity(tmg_ctx* ctx, const double* rho, double kappa_lo, double kap
  * source may be NULL (f = 0). */
 int tmg_assemble_rhs(tmg_ctx* ctx, const double* source, double* rhs_out);
 
+/* SIMP design loop on the device (BASELINE configs[2]) ------
+ * One design iteration = density filter (linear hat, radius rmin cells) ->
+ * kappa = MaterialModel(kappa_lo, kappa_hi, p) -> make_preconditioner ->
+ * state solve LS1 (source f = `source` per cell) and adjoint solve LS2
+ * (rhs 1/M, optim.cpp:16-19), each warm-started from its previous solution ->
+ * sensitivity (optim.cpp:21-84, design-independent source) -> filter
+ * transpose -> optimality-criteria update (move limit `move`, bisection on
+ * the volume multiplier for mean(filtered x) = volfrac). The filter and OC
+ * rules are builder-defined (the reference's outer loop uses MMA,
+ * optim.cpp:121-345). Single-slab contexts; the problem's patches are those
+ * of the last tmg_set_conductivity / tmg_set_design call. */
+typedef struct {
+  double volfrac;    /* target mean of the filtered design */
+  double rmin;       /* filter radius in cells (configs[2]: 1.5) */
+  double move;       /* OC move limit (configs[2]: 0.2) */
+  double kappa_lo, kappa_hi;
+  int p;             /* SIMP penalisation */
+  double source;     /* uniform heat source f */
+  double rtol;       /* PCG tolerance of LS1 / LS2 */
+  int maxit;
+} tmg_simp_options;
+
+typedef struct {
+  int iteration;
+  double cost;       /* mean temperature of LS1 (mean_temperature, optim.cpp:10-14) */
+  double volume;     /* mean filtered design before the update */
+  double change;     /* ||x_new - x||_inf */
+  int ls1_iterations, ls2_iterations;
+  double setup_seconds, ls1_seconds, ls2_seconds, step_seconds;
+} tmg_simp_report;
+
+/* rho0 = initial design (x-fastest, NULL -> uniform volfrac). */
+int tmg_simp_init(tmg_ctx* ctx, const tmg_simp_options* opts, const tmg_mmg_options* mmg,
+                  const double* rho0);
+int tmg_simp_step(tmg_ctx* ctx, tmg_simp_report* report);
+/* filtered design ("physical" densities) and the last state solution */
+int tmg_simp_download(tmg_ctx* ctx, double* xphys, double* temperature);
+
 /* Preconditioner set-up: make_preconditioner (solver.cpp:462-481). */
 int tmg_setup(tmg_ctx* ctx, const tmg_mmg_options* opts);
 

@@ -146,6 +146,16 @@ struct tmg_ctx {
   std::unordered_map<void*, size_t> sizes;
   std::unordered_map<void*, void*> virt;  // windowed pointer -> allocation
   double setup_seconds = 0.0;
+  // SIMP design loop (tmg_simp_*): x-fastest design arrays + warm starts
+  struct Simp {
+    bool on = false;
+    tmg_simp_options o{};
+    tmg_mmg_options mmg{};
+    int iter = 0;
+    double *x = nullptr, *xphys = nullptr, *xnew = nullptr, *dc = nullptr, *dv = nullptr,
+           *W = nullptr, *tmp = nullptr, *part = nullptr, *scal = nullptr;
+    double *T = nullptr, *U = nullptr;  // previous state / adjoint (brick layout)
+  } simp;
 };
 
 namespace {
@@ -889,6 +899,8 @@ bool single(const tmg_ctx* c) { return !c->dist(); }
 
 }  // namespace
 
+extern "C" int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o);
+
 // =================================================================== C ABI
 
 extern "C" {
@@ -1094,6 +1106,155 @@ int tmg_sensitivity(tmg_ctx* c, const double* rho, double kappa_lo, double kappa
       CK(cudaGetLastError());
     }
     DOWN(q, grad);
+  });
+}
+
+int tmg_simp_init(tmg_ctx* c, const tmg_simp_options* o, const tmg_mmg_options* mmg,
+                  const double* rho0) {
+  if (!c || !o || !mmg) return set_err(c, TMG_EARG, "tmg_simp_init: null argument");
+  if (c->dist()) return set_err(c, TMG_ENOTSUP, "the SIMP loop runs on single-slab contexts");
+  if (!c->have_problem)
+    return set_err(c, TMG_EARG, "tmg_simp_init: set a problem (patches) first");
+  if (!(o->volfrac > 0.0 && o->volfrac <= 1.0) || !(o->rmin >= 1.0) || !(o->move > 0.0))
+    return set_err(c, TMG_ECONFIG, "simp: need 0 < volfrac <= 1, rmin >= 1, move > 0");
+  if (!(o->kappa_lo > 0.0) || !(o->kappa_hi > o->kappa_lo) || o->p < 1)
+    return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi, p >= 1");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    auto& S = c->simp;
+    const int64_t M = c->M;
+    const tmg_grid& G = c->grid;
+    for (double** v : {&S.x, &S.xphys, &S.xnew, &S.dc, &S.dv, &S.W, &S.tmp, &S.T, &S.U})
+      if (!*v) *v = dalloc<double>(c, M);
+    if (!S.part) S.part = dalloc<double>(c, sum_partials_doubles());
+    if (!S.scal) S.scal = dalloc<double>(c, 4);
+    S.o = *o;
+    S.mmg = *mmg;
+    S.iter = 0;
+    if (rho0)
+      CK(cudaMemcpyAsync(S.x, rho0, sizeof(double) * (size_t)M, cudaMemcpyHostToDevice,
+                         c->stream));
+    else
+      launch_fill(S.x, M, o->volfrac, c->stream);
+    launch_density_filter(G.nx, G.ny, G.nz, o->rmin, nullptr, nullptr, S.W, 0, c->stream);
+    launch_fill(S.tmp, M, 1.0 / (double)M, c->stream);  // d mean(x~) / d x~
+    launch_density_filter(G.nx, G.ny, G.nz, o->rmin, S.tmp, S.W, S.dv, 2, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    S.on = true;
+  });
+}
+
+int tmg_simp_step(tmg_ctx* c, tmg_simp_report* rep) {
+  if (!c) return set_err(c, TMG_EARG, "null context");
+  if (!c->simp.on) return set_err(c, TMG_EARG, "tmg_simp_step: call tmg_simp_init first");
+  auto& S = c->simp;
+  const auto t0 = std::chrono::steady_clock::now();
+  tmg_simp_report r{};
+  r.iteration = S.iter;
+  const tmg_grid& G = c->grid;
+  const int64_t M = c->M;
+  auto host_scalar = [&](double* d) {
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, d, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return v;
+  };
+  int rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    Slab& s = c->slabs[0];
+    // 1. physical densities and conductivity
+    launch_density_filter(G.nx, G.ny, G.nz, S.o.rmin, S.x, S.W, S.xphys, 1, c->stream);
+    launch_to_brick(s.g, c->cb, S.xphys, s.r, c->stream);
+    launch_conductivity(s.g, c->cb, s.r, s.kappa, S.o.kappa_lo, S.o.kappa_hi, S.o.p, c->stream);
+    CK(cudaGetLastError());
+    launch_sum(S.xphys, M, S.part, S.scal, c->stream);
+    r.volume = host_scalar(S.scal) / (double)M;
+  });
+  if (rc) return rc;
+  if ((rc = finish_problem(c))) return rc;  // mask, faces, coefficients
+  if ((rc = tmg_setup(c, &S.mmg))) return rc;
+  r.setup_seconds = c->setup_seconds;
+  rc = guard(c, [&] {
+    Slab& s = c->slabs[0];
+    const size_t bytes = sizeof(double) * (size_t)M;
+    // 2. state LS1: b = f vol + Dirichlet lift (fvm.cpp:63-112)
+    launch_fill(s.q, M, S.o.source, c->stream);
+    launch_boundary(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                    c->grid.ly, c->grid.lz, s.kappa, s.q, s.dmask, s.b, nullptr, c->stream);
+    if (S.iter > 0) CK(cudaMemcpyAsync(s.x, S.T, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    tmg_report a{};
+    solve_device(c, S.o.rtol, S.o.maxit, S.iter > 0, &a, nullptr, nullptr);
+    if (!a.converged) {
+      set_err(c, TMG_ESOLVER, "simp: state solve did not converge (%d iterations)", a.iterations);
+      throw Fail{TMG_ESOLVER};
+    }
+    r.ls1_iterations = a.iterations;
+    r.ls1_seconds = a.solve_seconds;
+    CK(cudaMemcpyAsync(S.T, s.x, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    launch_sum(S.T, M, S.part, S.scal, c->stream);
+    r.cost = host_scalar(S.scal) / (double)M;
+    // 3. adjoint LS2: rhs = 1/M (adjoint_rhs, optim.cpp:16-19)
+    launch_fill(s.b, M, 1.0 / (double)M, c->stream);
+    if (S.iter > 0) CK(cudaMemcpyAsync(s.x, S.U, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    solve_device(c, S.o.rtol, S.o.maxit, S.iter > 0, &a, nullptr, nullptr);
+    if (!a.converged) {
+      set_err(c, TMG_ESOLVER, "simp: adjoint solve did not converge (%d iterations)",
+              a.iterations);
+      throw Fail{TMG_ESOLVER};
+    }
+    r.ls2_iterations = a.iterations;
+    r.ls2_seconds = a.solve_seconds;
+    CK(cudaMemcpyAsync(S.U, s.x, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    // 4. sensitivity w.r.t. the physical densities (design-independent source);
+    // the solves used s.r, so the densities go to brick layout again (S.xnew
+    // is free until the OC update)
+    launch_to_brick(s.g, c->cb, S.xphys, S.xnew, c->stream);
+    launch_sensitivity(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                       c->grid.ly, c->grid.lz, S.xnew, s.kappa, S.T, S.U, S.o.kappa_lo,
+                       S.o.kappa_hi, 0.0, S.o.p, s.q, c->stream);
+    launch_from_brick(s.g, c->cb, s.q, S.tmp, c->stream);
+    launch_density_filter(G.nx, G.ny, G.nz, S.o.rmin, S.tmp, S.W, S.dc, 2, c->stream);
+    CK(cudaGetLastError());
+    // 5. OC update: bisection (in log space) on the volume multiplier
+    double lo = 1e-40, hi = 1e40;
+    for (int it = 0; it < 200 && hi / lo > 1.0 + 1e-10; ++it) {
+      const double mid = std::sqrt(lo * hi);
+      launch_oc_candidate(S.x, S.dc, S.dv, mid, S.o.move, 0.0, M, S.xnew, c->stream);
+      launch_density_filter(G.nx, G.ny, G.nz, S.o.rmin, S.xnew, S.W, S.tmp, 1, c->stream);
+      launch_sum(S.tmp, M, S.part, S.scal, c->stream);
+      if (host_scalar(S.scal) / (double)M > S.o.volfrac) lo = mid;
+      else hi = mid;
+    }
+    launch_oc_candidate(S.x, S.dc, S.dv, hi, S.o.move, 0.0, M, S.xnew, c->stream);
+    launch_maxdiff(S.xnew, S.x, M, S.part, S.scal, c->stream);
+    r.change = host_scalar(S.scal);
+    std::swap(S.x, S.xnew);
+    CK(cudaGetLastError());
+  });
+  if (rc) return rc;
+  ++S.iter;
+  r.step_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (rep) *rep = r;
+  return TMG_OK;
+}
+
+int tmg_simp_download(tmg_ctx* c, double* xphys, double* temperature) {
+  if (!c || !c->simp.on) return set_err(c, TMG_EARG, "tmg_simp_download: no SIMP loop");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    auto& S = c->simp;
+    const size_t bytes = sizeof(double) * (size_t)c->M;
+    if (xphys) {
+      launch_density_filter(c->grid.nx, c->grid.ny, c->grid.nz, S.o.rmin, S.x, S.W, S.tmp, 1,
+                            c->stream);
+      CK(cudaMemcpyAsync(xphys, S.tmp, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (temperature) {
+      launch_from_brick(c->slabs[0].g, c->cb, S.T, S.xnew, c->stream);
+      CK(cudaMemcpyAsync(temperature, S.xnew, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
   });
 }
 

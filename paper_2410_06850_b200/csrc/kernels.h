@@ -137,6 +137,17 @@ void pack_sym_tiles(const double* A, int64_t n, double* T, cudaStream_t s);
 void launch_symv(const int* done, const double* T, int64_t n, const double* x, double* P, double* y,
                  cudaStream_t s);
 
+// simp.cu (x-fastest design arrays)
+void launch_density_filter(int64_t nx, int64_t ny, int64_t nz, double r, const double* in,
+                           const double* W, double* out, int mode, cudaStream_t s);
+void launch_oc_candidate(const double* x, const double* dc, const double* dv, double lam,
+                         double mv, double xmin, int64_t m, double* xnew, cudaStream_t s);
+void launch_sum(const double* v, int64_t m, double* part, double* out, cudaStream_t s);
+void launch_maxdiff(const double* a, const double* b, int64_t m, double* part, double* out,
+                    cudaStream_t s);
+int64_t sum_partials_doubles();
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+
 // pcg.cu
 void init_kernel_attributes();
 void launch_coefficients(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,

@@ -62,6 +62,19 @@ class _Report(C.Structure):
                 ("final_relative_residual", C.c_double)]
 
 
+class _SimpOpts(C.Structure):
+    _fields_ = [("volfrac", C.c_double), ("rmin", C.c_double), ("move", C.c_double),
+                ("kappa_lo", C.c_double), ("kappa_hi", C.c_double), ("p", C.c_int),
+                ("source", C.c_double), ("rtol", C.c_double), ("maxit", C.c_int)]
+
+
+class _SimpReport(C.Structure):
+    _fields_ = [("iteration", C.c_int), ("cost", C.c_double), ("volume", C.c_double),
+                ("change", C.c_double), ("ls1_iterations", C.c_int), ("ls2_iterations", C.c_int),
+                ("setup_seconds", C.c_double), ("ls1_seconds", C.c_double),
+                ("ls2_seconds", C.c_double), ("step_seconds", C.c_double)]
+
+
 _lib = None
 _DP = C.POINTER(C.c_double)
 
@@ -93,7 +106,7 @@ EXPORTED_SYMBOLS = (
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
     "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
-    "tmg_sensitivity",
+    "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
 )
 
 
@@ -312,6 +325,26 @@ class Context:
                                              C.c_double(kappa_hi), C.c_double(f0), C.c_int(p),
                                              _ptr(tt), _ptr(uu), _ptr(out)))
         return out
+
+    # SIMP design loop (BASELINE configs[2]; include/topmg_b200.h tmg_simp_*)
+    def simp_init(self, volfrac=0.3, rmin=1.5, move=0.2, kappa_lo=1e-6, kappa_hi=1.0, p=3,
+                  source=1.0, rtol=1e-8, maxit=10000, rho0=None, mmg: MmgOptions = MmgOptions()):
+        o = _SimpOpts(volfrac, rmin, move, kappa_lo, kappa_hi, p, source, rtol, maxit)
+        m = _Opts(PrecondKind.parse("mmg"), mmg.num_local_basis, mmg.num_cc_basis,
+                  mmg.smoother_sweeps, mmg.eig_tol, mmg.eig_degree, mmg.eig_max_outer)
+        r0 = _ptr(_f64(rho0)) if rho0 is not None else None
+        self._check(native().tmg_simp_init(self._p, C.byref(o), C.byref(m), r0))
+
+    def simp_step(self) -> dict:
+        r = _SimpReport()
+        self._check(native().tmg_simp_step(self._p, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in _SimpReport._fields_}
+
+    def simp_download(self):
+        """(filtered design, last state solution), x-fastest."""
+        xp, t = np.empty(self.cells), np.empty(self.cells)
+        self._check(native().tmg_simp_download(self._p, _ptr(xp), _ptr(t)))
+        return xp, t
 
     def assemble_rhs(self, source=None):
         out = np.empty(self.cells)
