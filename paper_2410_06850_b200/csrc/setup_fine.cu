@@ -5,25 +5,25 @@
 
 namespace tmg {
 
-// One CTA per brick, C = CB^3 threads. Dynamic smem: 2 full P x P matrices +
-// kappa tile + C pivots + P scratch x2.
+// One CTA per brick, NTF threads (256 at CB = 8: three CTAs per SM). Dynamic
+// smem: 2 full P x P matrices + kappa tile + C pivots + P scratch x2.
 template <int CB>
-__global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
+constexpr int factor_threads() { return CB == 8 ? 256 : CB * CB * CB; }
+
+template <int CB>
+__global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridParams g,
                                                                const double* __restrict__ kappa,
                                                                const uint8_t* __restrict__ dmask,
                                                                double* G, int* status) {
-  constexpr int P = Thomas<CB>::P, C = CB * CB * CB;
+  constexpr int P = Thomas<CB>::P, C = CB * CB * CB, NTF = factor_threads<CB>();
+  constexpr int GP = P + 1;        // padded row stride of Gprev (conflict-free transpose)
   extern __shared__ double sm[];
-  double* S = sm;                  // P*P  current Schur complement -> inverse
-  double* Gprev = S + P * P;       // P*P  previous plane inverse
-  double* kt = Gprev + P * P;      // tile
-  double* fx = kt + Tile<CB>::N;   // 3 face arrays
+  double* Gprev = sm;              // P*GP  previous plane inverse
+  double* kt = Gprev + P * GP;     // tile (prologue only)
+  double* fx = kt + Tile<CB>::N;   // 3 face arrays (prologue only)
   double* fy = fx + Tile<CB>::NF;
   double* fz = fy + Tile<CB>::NF;
-  double* piv = fz + Tile<CB>::NF; // C
-  double* col = piv + C;           // P
-  double* rowp = col + P;          // P
-  double* dg = rowp + P;           // C  diagonal of A
+  double* dg = fz + Tile<CB>::NF;  // C  diagonal of A
   double* tx = dg + C;             // C  T to +x neighbour in brick (0 if none)
   double* ty = tx + C;             // C
   double* tzb = ty + C;            // C  T to the cell one plane below (0 for lk=0)
@@ -33,89 +33,168 @@ __global__ void __launch_bounds__(CB * CB * CB) k_thomas_factor(GridParams g,
   __syncthreads();
   tile_faces<CB>(kt, fx, fy, fz, g, bc);
   __syncthreads();
-  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
-  {
-    const unsigned dm = brick_on_boundary(g, bc) ? dmask[bofs(bc.b, C) + t] : 0u;
+  const int t = threadIdx.x;
+  for (int c = t; c < C; c += NTF) {
+    const int li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+    const unsigned dm = brick_on_boundary(g, bc) ? dmask[bofs(bc.b, C) + c] : 0u;
     const FaceSet fs = cell_faces<CB>(fx, fy, fz, kt[Tile<CB>::idx(li, lj, lk)], li, lj, lk, g, bc, dm);
-    dg[t] = fs.diag;
-    tx[t] = li + 1 < CB ? fs.t[1] : 0.0;
-    ty[t] = lj + 1 < CB ? fs.t[3] : 0.0;
-    tzb[t] = lk > 0 ? fs.t[4] : 0.0;
+    dg[c] = fs.diag;
+    tx[c] = li + 1 < CB ? fs.t[1] : 0.0;
+    ty[c] = lj + 1 < CB ? fs.t[3] : 0.0;
+    tzb[c] = lk > 0 ? fs.t[4] : 0.0;
   }
   __syncthreads();
   double* Gout = G + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  // Register-resident Gauss-Jordan. Warp w owns columns [CW*w, CW*w + CW) of
+  // all P rows, lane l the rows l + 32 h (h < RH): per pivot the generic
+  // update is one multiply and one FMA per entry, and the pivot column's
+  // special case is warp-uniform (one warp). Pivot row, pivot column and
+  // 1/pivot go through shared memory (double-buffered, one barrier per pivot).
+  constexpr int NW = NTF / 32;
+  constexpr int CW = P / NW;        // columns per warp (8 at CB = 8)
+  constexpr int RH = P > 32 ? P / 32 : 1;  // rows per lane (2 at CB = 8)
+  static_assert(CW % 2 == 0 && CW * NW == P && (P >= 32 ? RH * 32 == P : true), "layout");
+  constexpr int NE = CW * RH;
+  const int lane = t & 31, wq = t >> 5, c0 = CW * wq;
+  const bool lane_active = lane < P;  // P < 32 (CB = 4): lanes >= P idle
+  double pmin = 1e300, pmax = 0.0;    // this thread's pivots
+  __shared__ alignas(16) double rowbuf[2][P];
+  __shared__ double colbuf[2][P];
+  __shared__ double invbuf[2];
   for (int k = 0; k < CB; ++k) {
-    // S = A_k - B_k Gprev B_k, B_k = diag(-tz)
-    for (int e = t; e < P * P; e += C) {
-      const int i = e / P, j = e % P;
-      const int ci = k * P + i, cj = k * P + j;
-      double v = 0.0;
-      if (i == j) v = dg[ci];
-      else {
-        const int ii = i % CB, ij = i / CB, ji = j % CB, jj = j / CB;
-        if (ij == jj && ji == ii + 1) v = -tx[ci];
-        else if (ij == jj && ii == ji + 1) v = -tx[cj];
-        else if (ii == ji && jj == ij + 1) v = -ty[ci];
-        else if (ii == ji && ij == jj + 1) v = -ty[cj];
+    // S = A_k - B_k Gprev B_k, B_k = diag(-tz) (own entries, in registers)
+    double v[RH][CW];
+#pragma unroll
+    for (int h = 0; h < RH; ++h) {
+      const int ri = lane_active ? lane + 32 * h : 0;
+      const int ci = k * P + ri;
+#pragma unroll
+      for (int q = 0; q < CW; ++q) {
+        const int j = c0 + q, cj = k * P + j;
+        double a = 0.0;
+        if (ri == j) a = dg[ci];
+        else {
+          const int ii = ri % CB, ij = ri / CB, ji = j % CB, jj = j / CB;
+          if (ij == jj && ji == ii + 1) a = -tx[ci];
+          else if (ij == jj && ii == ji + 1) a = -tx[cj];
+          else if (ii == ji && jj == ij + 1) a = -ty[ci];
+          else if (ii == ji && ij == jj + 1) a = -ty[cj];
+        }
+        if (k > 0) a -= tzb[ci] * Gprev[ri * GP + j] * tzb[cj];
+        v[h][q] = a;
       }
-      if (k > 0) v -= tzb[ci] * Gprev[e] * tzb[cj];
-      S[e] = v;
+    }
+    __syncthreads();  // every thread has read Gprev
+    // in-place Gauss-Jordan sweep inversion (SPD, no pivoting)
+#pragma unroll 1
+    for (int p = 0; p < P; ++p) {
+      const int b = p & 1, pr = p & 31, ph = p >> 5, pq = p - c0;
+      const bool colw = pq >= 0 && pq < CW;  // this warp owns column p
+      if (lane_active) {
+        // publish row p (owner lane pr, row slot ph) and column p (warp p / CW)
+        if (lane == pr) {
+#pragma unroll
+          for (int h = 0; h < RH; ++h)
+            if (h == ph) {
+#pragma unroll
+              for (int q = 0; q < CW; q += 2)
+                *reinterpret_cast<double2*>(&rowbuf[b][c0 + q]) = make_double2(v[h][q], v[h][q + 1]);
+            }
+        }
+        if (colw) {
+#pragma unroll
+          for (int h = 0; h < RH; ++h) {
+            double cv = v[h][0];
+#pragma unroll
+            for (int q = 1; q < CW; ++q) cv = (q == pq) ? v[h][q] : cv;
+            colbuf[b][lane + 32 * h] = cv;
+            if (lane == pr && h == ph) {
+              invbuf[b] = 1.0 / cv;
+              pmin = fmin(pmin, cv);  // the LDL^T pivots of A_II (natural order)
+              pmax = fmax(pmax, fabs(cv));
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (lane_active) {
+        const double inv = invbuf[b];
+        double rji[CW];
+#pragma unroll
+        for (int q = 0; q < CW; q += 2) {
+          const double2 r2 = *reinterpret_cast<const double2*>(&rowbuf[b][c0 + q]);
+          rji[q] = r2.x * inv;
+          rji[q + 1] = r2.y * inv;
+        }
+#pragma unroll
+        for (int h = 0; h < RH; ++h) {
+          const double cvi = colbuf[b][lane + 32 * h];
+#pragma unroll
+          for (int q = 0; q < CW; ++q) v[h][q] = fma(-cvi, rji[q], v[h][q]);
+          if (colw) {  // pivot column: -c_i / pivot
+#pragma unroll
+            for (int q = 0; q < CW; ++q)
+              if (q == pq) v[h][q] = -cvi * inv;
+          }
+          if (lane == pr && h == ph) {  // pivot row: r_j / pivot, pivot: 1 / pivot
+#pragma unroll
+            for (int q = 0; q < CW; ++q) v[h][q] = (q == pq) ? inv : rji[q];
+          }
+        }
+      }
+    }
+    // symmetrise in place, store packed, keep the full copy for the next plane
+    if (lane_active) {
+#pragma unroll
+      for (int h = 0; h < RH; ++h)
+#pragma unroll
+        for (int q = 0; q < CW; ++q) Gprev[(lane + 32 * h) * GP + c0 + q] = v[h][q];
     }
     __syncthreads();
-    // in-place Gauss-Jordan sweep inversion (SPD, no pivoting)
-    for (int p = 0; p < P; ++p) {
-      const double pv = S[p * P + p];
-      if (t < P) {
-        col[t] = S[t * P + p];
-        rowp[t] = S[p * P + t];
-      }
-      if (t == 0) piv[k * P + p] = pv;
-      __syncthreads();
-      const double inv = 1.0 / pv;
-      for (int e = t; e < P * P; e += C) {
-        const int i = e / P, j = e % P;
-        double v;
-        if (i == p && j == p) v = inv;
-        else if (i == p) v = rowp[j] * inv;
-        else if (j == p) v = -col[i] * inv;
-        else v = S[e] - col[i] * (rowp[j] * inv);
-        S[e] = v;
-      }
-      __syncthreads();
-    }
-    // symmetrise, store packed, keep full copy for the next plane
-    for (int e = t; e < P * P; e += C) {
+    for (int e = t; e < P * P; e += NTF) {
       const int i = e / P, j = e % P;
-      Gprev[e] = 0.5 * (S[e] + S[j * P + i]);
+      if (i < j) {
+        const double m = 0.5 * (Gprev[i * GP + j] + Gprev[j * GP + i]);
+        Gprev[i * GP + j] = m;
+        Gprev[j * GP + i] = m;
+      }
     }
     __syncthreads();
     // lower block-triangle of 8 x 8 blocks, block (I, J <= I) at I(I+1)/2 + J
-    for (int e = t; e < Thomas<CB>::PLANE; e += C) {
+    for (int e = t; e < Thomas<CB>::PLANE; e += NTF) {
       const int blk = e / 64, rr = (e % 64) / 8, cc = e % 8;
       int I, J;
       block_of<CB>(blk, I, J);
-      Gout[(size_t)k * Thomas<CB>::PLANE + blk * 64 + swz(rr, cc)] = Gprev[(8 * I + rr) * P + 8 * J + cc];
+      Gout[(size_t)k * Thomas<CB>::PLANE + blk * 64 + swz(rr, cc)] = Gprev[(8 * I + rr) * GP + 8 * J + cc];
     }
     __syncthreads();
   }
-  // reference singular-pivot rule over the block's pivots (solver.cpp:86-92)
-  double mx = fabs(piv[t]);
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((t & 31) == 0) red[t >> 5] = mx;
-  __syncthreads();
-  if (t == 0) {
-    double m = 0.0;
-    for (int w = 0; w < C / 32 || w == 0; ++w) m = fmax(m, red[w]);
-    red[32] = m;
+  // reference singular-pivot rule over the block's pivots (solver.cpp:86-92):
+  // every d > 1e-14 max|d|  <=>  min d > 1e-14 max|d|
+  double mx = pmax, mn = pmin;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if ((t & 31) == 0) {
+    red[t >> 5] = mx;
+    red[32 + (t >> 5)] = mn;
   }
   __syncthreads();
-  if (!(piv[t] > 1e-14 * red[32])) atomicExch(status, 1);
+  if (t == 0) {
+    double m = 0.0, n = 1e300;
+    for (int w = 0; w < NTF / 32 || w == 0; ++w) {
+      m = fmax(m, red[w]);
+      n = fmin(n, red[32 + w]);
+    }
+    if (!(n > 1e-14 * m)) atomicExch(status, 1);
+  }
 }
 
 size_t thomas_smem_bytes(int cb) {
   const int P = cb * cb, C = cb * cb * cb, N = (cb + 2) * (cb + 2) * (cb + 2);
   const int NF = (cb + 1) * cb * cb;
-  return sizeof(double) * (size_t)(2 * P * P + N + 3 * NF + C + 2 * P + 4 * C);
+  return sizeof(double) * (size_t)(P * (P + 1) + N + 3 * NF + 4 * C);
 }
 
 void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
@@ -123,10 +202,12 @@ void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, cons
   const size_t smem = thomas_smem_bytes(cb);
   if (cb == 8) {
     cudaFuncSetAttribute(k_thomas_factor<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<8><<<(unsigned)g.nbo, 512, smem, s>>>(g, kappa, dmask, G, status);
+    k_thomas_factor<8><<<(unsigned)g.nbo, factor_threads<8>(), smem, s>>>(g, kappa, dmask, G,
+                                                                          status);
   } else {
     cudaFuncSetAttribute(k_thomas_factor<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<4><<<(unsigned)g.nbo, 64, smem, s>>>(g, kappa, dmask, G, status);
+    k_thomas_factor<4><<<(unsigned)g.nbo, factor_threads<4>(), smem, s>>>(g, kappa, dmask, G,
+                                                                          status);
   }
 }
 

@@ -130,7 +130,7 @@ __device__ __forceinline__ void tile_faces(const double* kt, double* fx, double*
                                            const GridParams& g, const BrickCoord& bc) {
   constexpr int NF = Tile<CB>::NF;
   constexpr int C = CB * CB * CB;
-  for (int s = threadIdx.x; s < 3 * NF; s += C) {
+  for (int s = threadIdx.x; s < 3 * NF; s += blockDim.x) {
     const int ax = s / NF, r = s % NF;
     const int a = r % (CB + 1) - 1, u = (r / (CB + 1)) % CB, w = r / ((CB + 1) * CB);
     int i0, j0, k0, i1, j1, k1, ga;
