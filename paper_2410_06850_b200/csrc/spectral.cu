@@ -67,11 +67,17 @@ __device__ void jacobi_eig_small(double* a, double* v) {
   }
 }
 
-// Warp-parallel cyclic Jacobi on a K x K symmetric matrix in shared memory
-// (lane r < K owns row/column r); eigenvectors accumulate in V (columns).
-// Called by one full warp.
+// Warp-parallel Jacobi on a K x K symmetric matrix in shared memory (K even),
+// round-robin ("tournament") ordering: a sweep is K-1 rounds of K/2 disjoint
+// rotations; lane g < K/2 computes rotation g of a round, then lanes r < K
+// apply all of them to row / column r. Eigenvectors accumulate in V
+// (columns). Called by one full warp.
 template <int K>
 __device__ void warp_jacobi_small(double* a, double* v) {
+  static_assert(K % 2 == 0 && K <= 32, "round-robin Jacobi");
+  constexpr int NP = K / 2;
+  __shared__ double rot_c[NP], rot_s[NP];
+  __shared__ int rot_p[NP], rot_q[NP];
   const int lane = threadIdx.x & 31;
   if (lane < K)
     for (int c = 0; c < K; ++c) v[lane * K + c] = lane == c ? 1.0 : 0.0;
@@ -91,16 +97,41 @@ __device__ void warp_jacobi_small(double* a, double* v) {
     // off-diagonal mass below ~1e-13 of the total: the Ritz values and
     // vectors are converged far beyond what the subspace iteration needs
     if (off <= 1e-26 * tot || off == 0.0) break;
-    for (int p = 0; p < K - 1; ++p)
-      for (int q = p + 1; q < K; ++q) {
+    for (int round = 0; round < K - 1; ++round) {
+      if (lane < NP) {  // circle method: player K-1 fixed, the others rotate
+        int p, q;
+        if (lane == 0) {
+          p = round;
+          q = K - 1;
+        } else {
+          p = (round + lane) % (K - 1);
+          q = (round - lane + (K - 1)) % (K - 1);
+        }
+        if (p > q) {
+          const int tmp = p;
+          p = q;
+          q = tmp;
+        }
         const double apq = a[p * K + q];
         const double app = a[p * K + p], aqq = a[q * K + q];
-        if (fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq)) || apq == 0.0) continue;
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(tt * tt + 1.0), sn = tt * c;
-        __syncwarp();
-        if (lane < K) {  // columns p, q of row `lane`; eigenvector columns
+        double c = 1.0, sn = 0.0;
+        if (!(fabs(apq) <= 1e-16 * sqrt(fabs(app * aqq)) || apq == 0.0)) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(tt * tt + 1.0);
+          sn = tt * c;
+        }
+        rot_c[lane] = c;
+        rot_s[lane] = sn;
+        rot_p[lane] = p;
+        rot_q[lane] = q;
+      }
+      __syncwarp();
+      if (lane < K) {  // columns p, q of row `lane` (all pairs are disjoint)
+#pragma unroll
+        for (int g = 0; g < NP; ++g) {
+          const int p = rot_p[g], q = rot_q[g];
+          const double c = rot_c[g], sn = rot_s[g];
           const double akp = a[lane * K + p], akq = a[lane * K + q];
           a[lane * K + p] = c * akp - sn * akq;
           a[lane * K + q] = sn * akp + c * akq;
@@ -108,14 +139,20 @@ __device__ void warp_jacobi_small(double* a, double* v) {
           v[lane * K + p] = c * vkp - sn * vkq;
           v[lane * K + q] = sn * vkp + c * vkq;
         }
-        __syncwarp();
-        if (lane < K) {  // rows p, q at column `lane`
+      }
+      __syncwarp();
+      if (lane < K) {  // rows p, q at column `lane`
+#pragma unroll
+        for (int g = 0; g < NP; ++g) {
+          const int p = rot_p[g], q = rot_q[g];
+          const double c = rot_c[g], sn = rot_s[g];
           const double apk = a[p * K + lane], aqk = a[q * K + lane];
           a[p * K + lane] = c * apk - sn * aqk;
           a[q * K + lane] = sn * apk + c * aqk;
         }
-        __syncwarp();
       }
+      __syncwarp();
+    }
   }
 }
 
@@ -192,28 +229,34 @@ __device__ __forceinline__ void gram_mma(const double (&x)[K], const double (&y)
 }
 
 // X <- X R^{-1} where G = R^T R (Cholesky of the Gram matrix, kept in smem).
-// Returns false if G is not numerically positive definite.
+// Warp 0 factorises (lane j owns column j, right-looking updates through
+// shuffles); every thread then applies R^{-1} to its row of X. Returns false
+// if G is not numerically positive definite.
 template <int K>
 __device__ __forceinline__ bool cholqr_apply(double (&x)[K], const double* g, double* rsm,
                                              int* okflag) {
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double a[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) a[i] = lane < K ? g[i * K + lane] : 0.0;
+    double gmax = lane < K ? g[lane * K + lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
     bool ok = true;
-    double gmax = 0.0;
-    for (int i = 0; i < K; ++i) gmax = fmax(gmax, g[i * K + i]);
-    for (int i = 0; i < K * K; ++i) rsm[i] = 0.0;
-    for (int i = 0; i < K && ok; ++i) {
-      for (int j = i; j < K; ++j) {
-        double s = g[i * K + j];
-        for (int k = 0; k < i; ++k) s -= rsm[k * K + i] * rsm[k * K + j];
-        if (j == i) {
-          if (!(s > 1e-28 * gmax)) { ok = false; break; }
-          rsm[i * K + i] = sqrt(s);
-        } else {
-          rsm[i * K + j] = s / rsm[i * K + i];
-        }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double d = __shfl_sync(0xffffffffu, a[k], k);  // A_kk (column k, row k)
+      ok = ok && (d > 1e-28 * gmax);
+      const double rkk = ok ? sqrt(d) : 1.0;
+      const double rkj = lane >= k && lane < K ? a[k] / rkk : 0.0;  // R_kj
+      if (lane < K) rsm[k * K + lane] = lane >= k ? rkj : 0.0;
+#pragma unroll
+      for (int i = k + 1; i < K; ++i) {
+        const double rki = __shfl_sync(0xffffffffu, rkj, i);
+        if (lane > k) a[i] -= rki * rkj;
       }
     }
-    *okflag = ok;
+    if (lane == 0) *okflag = ok;
   }
   __syncthreads();
   const bool ok = *okflag;
