@@ -10,54 +10,44 @@
 #include "kernels.h"
 #include "tma.cuh"
 #include "symv.cuh"
+#include "gj.cuh"
 
 namespace tmg {
 
 constexpr int NB = 64;  // Gauss-Jordan pivot block
 
-// Invert the pivot block A[K,K] (nbk x nbk, nbk <= NB) into Dinv, record the
-// pivots. 1024 threads, each owning fixed elements of the (NB x NB) block.
-__global__ void __launch_bounds__(1024) k_gj_diag(const double* __restrict__ A, int64_t n,
-                                                  int64_t k0, int nbk, double* Dinv,
-                                                  double* pivots) {
-  constexpr int PER = NB * NB / 1024;
-  __shared__ double M[NB][NB + 1];
-  __shared__ double col[NB], rowp[NB];
-  const int t = threadIdx.x;
-  int ei[PER], ej[PER];
+// Invert the pivot block A[K,K] (nbk x nbk, nbk <= NB, identity-padded to NB)
+// into Dinv and record the pivots: one CTA, register-resident Gauss-Jordan
+// (gj.cuh).
+constexpr int kDiagThreads = 256;
+__global__ void __launch_bounds__(kDiagThreads) k_gj_diag(const double* __restrict__ A, int64_t n,
+                                                          int64_t k0, int nbk, double* Dinv,
+                                                          double* pivots) {
+  using L = GjLayout<NB, kDiagThreads>;
+  constexpr int CW = L::CW, RH = L::RH;
+  __shared__ GjSmem<NB> gjs;
+  const int lane = threadIdx.x & 31, c0 = CW * (threadIdx.x >> 5);
+  double v[RH][CW];
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    ei[q] = (t + 1024 * q) / NB;
-    ej[q] = (t + 1024 * q) % NB;
-    const bool in = ei[q] < nbk && ej[q] < nbk;
-    // identity padding keeps the padded pivots harmless
-    M[ei[q]][ej[q]] = in ? A[(k0 + ei[q]) * n + k0 + ej[q]] : (ei[q] == ej[q] ? 1.0 : 0.0);
-  }
-  __syncthreads();
-  for (int p = 0; p < nbk; ++p) {
-    if (t < NB) {
-      col[t] = M[t][p];
-      rowp[t] = M[p][t];
+  for (int h = 0; h < RH; ++h) {
+    const int i = lane + 32 * h;
+#pragma unroll
+    for (int q = 0; q < CW; ++q) {
+      const int j = c0 + q;
+      v[h][q] = (i < nbk && j < nbk) ? A[(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
     }
-    __syncthreads();
-    const double pv = rowp[p];
-    if (t == 0) pivots[k0 + p] = pv;
-    const double inv = 1.0 / pv;
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int i = ei[q], j = ej[q];
-      double v;
-      if (i == p && j == p) v = inv;
-      else if (i == p) v = rowp[j] * inv;
-      else if (j == p) v = -col[i] * inv;
-      else v = M[i][j] - col[i] * (rowp[j] * inv);
-      M[i][j] = v;
-    }
-    __syncthreads();
   }
+  double pmin = 1e300, pmax = 0.0;
+  gj_invert<NB, kDiagThreads>(v, gjs, pmin, pmax, pivots + k0);
 #pragma unroll
-  for (int q = 0; q < PER; ++q)
-    if (ei[q] < nbk && ej[q] < nbk) Dinv[ei[q] * nbk + ej[q]] = M[ei[q]][ej[q]];
+  for (int h = 0; h < RH; ++h) {
+    const int i = lane + 32 * h;
+#pragma unroll
+    for (int q = 0; q < CW; ++q) {
+      const int j = c0 + q;
+      if (i < nbk && j < nbk) Dinv[i * nbk + j] = v[h][q];
+    }
+  }
 }
 
 // Pn[r][j] = sum_c Dinv[r][c] A[k0+c][j] (new pivot rows); Cold[i][c] = A[i][k0+c]
@@ -365,7 +355,7 @@ void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStre
   const dim3 grid((unsigned)((n + GN - 1) / GN), (unsigned)((n + GT - 1) / GT));
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int nbk = (int)((n - k0) < NB ? (n - k0) : NB);
-    k_gj_diag<<<1, 1024, 0, s>>>(A, n, k0, nbk, Dinv, piv);
+    k_gj_diag<<<1, kDiagThreads, 0, s>>>(A, n, k0, nbk, Dinv, piv);
     k_gj_panels<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
     k_gj_gemm<<<grid, 256, kGemmSmem, s>>>(A, n, Cold, Pn);
     k_gj_fix<<<(unsigned)((n * nbk + 255) / 256), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
@@ -374,7 +364,8 @@ void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStre
   k_pivot_check<<<1, 1024, 0, s>>>(piv, n, status);
 }
 
-int64_t dense_inverse_work_doubles(int64_t n) { return NB * NB + 2 * (int64_t)NB * n + n; }
+// (+ NB: the identity-padded last pivot block writes NB pivots)
+int64_t dense_inverse_work_doubles(int64_t n) { return NB * NB + 2 * (int64_t)NB * n + n + NB; }
 
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
                  cudaStream_t s) {

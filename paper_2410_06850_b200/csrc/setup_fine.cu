@@ -2,6 +2,7 @@
 // packed inverses G_k of the plane Schur complements of A_II.
 #include "kernels.h"
 #include "smoother.cuh"
+#include "gj.cuh"
 
 namespace tmg {
 
@@ -45,22 +46,13 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
   }
   __syncthreads();
   double* Gout = G + (size_t)bc.b * Thomas<CB>::PER_BRICK;
-  // Register-resident Gauss-Jordan. Warp w owns columns [CW*w, CW*w + CW) of
-  // all P rows, lane l the rows l + 32 h (h < RH): per pivot the generic
-  // update is one multiply and one FMA per entry, and the pivot column's
-  // special case is warp-uniform (one warp). Pivot row, pivot column and
-  // 1/pivot go through shared memory (double-buffered, one barrier per pivot).
-  constexpr int NW = NTF / 32;
-  constexpr int CW = P / NW;        // columns per warp (8 at CB = 8)
-  constexpr int RH = P > 32 ? P / 32 : 1;  // rows per lane (2 at CB = 8)
-  static_assert(CW % 2 == 0 && CW * NW == P && (P >= 32 ? RH * 32 == P : true), "layout");
-  constexpr int NE = CW * RH;
-  const int lane = t & 31, wq = t >> 5, c0 = CW * wq;
+  // Register-resident Gauss-Jordan per plane (gj.cuh)
+  using L = GjLayout<P, NTF>;
+  constexpr int CW = L::CW, RH = L::RH;
+  const int lane = t & 31, c0 = CW * (t >> 5);
   const bool lane_active = lane < P;  // P < 32 (CB = 4): lanes >= P idle
   double pmin = 1e300, pmax = 0.0;    // this thread's pivots
-  __shared__ alignas(16) double rowbuf[2][P];
-  __shared__ double colbuf[2][P];
-  __shared__ double invbuf[2];
+  __shared__ GjSmem<P> gjs;
   for (int k = 0; k < CB; ++k) {
     // S = A_k - B_k Gprev B_k, B_k = diag(-tz) (own entries, in registers)
     double v[RH][CW];
@@ -85,64 +77,7 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
       }
     }
     __syncthreads();  // every thread has read Gprev
-    // in-place Gauss-Jordan sweep inversion (SPD, no pivoting)
-#pragma unroll 1
-    for (int p = 0; p < P; ++p) {
-      const int b = p & 1, pr = p & 31, ph = p >> 5, pq = p - c0;
-      const bool colw = pq >= 0 && pq < CW;  // this warp owns column p
-      if (lane_active) {
-        // publish row p (owner lane pr, row slot ph) and column p (warp p / CW)
-        if (lane == pr) {
-#pragma unroll
-          for (int h = 0; h < RH; ++h)
-            if (h == ph) {
-#pragma unroll
-              for (int q = 0; q < CW; q += 2)
-                *reinterpret_cast<double2*>(&rowbuf[b][c0 + q]) = make_double2(v[h][q], v[h][q + 1]);
-            }
-        }
-        if (colw) {
-#pragma unroll
-          for (int h = 0; h < RH; ++h) {
-            double cv = v[h][0];
-#pragma unroll
-            for (int q = 1; q < CW; ++q) cv = (q == pq) ? v[h][q] : cv;
-            colbuf[b][lane + 32 * h] = cv;
-            if (lane == pr && h == ph) {
-              invbuf[b] = 1.0 / cv;
-              pmin = fmin(pmin, cv);  // the LDL^T pivots of A_II (natural order)
-              pmax = fmax(pmax, fabs(cv));
-            }
-          }
-        }
-      }
-      __syncthreads();
-      if (lane_active) {
-        const double inv = invbuf[b];
-        double rji[CW];
-#pragma unroll
-        for (int q = 0; q < CW; q += 2) {
-          const double2 r2 = *reinterpret_cast<const double2*>(&rowbuf[b][c0 + q]);
-          rji[q] = r2.x * inv;
-          rji[q + 1] = r2.y * inv;
-        }
-#pragma unroll
-        for (int h = 0; h < RH; ++h) {
-          const double cvi = colbuf[b][lane + 32 * h];
-#pragma unroll
-          for (int q = 0; q < CW; ++q) v[h][q] = fma(-cvi, rji[q], v[h][q]);
-          if (colw) {  // pivot column: -c_i / pivot
-#pragma unroll
-            for (int q = 0; q < CW; ++q)
-              if (q == pq) v[h][q] = -cvi * inv;
-          }
-          if (lane == pr && h == ph) {  // pivot row: r_j / pivot, pivot: 1 / pivot
-#pragma unroll
-            for (int q = 0; q < CW; ++q) v[h][q] = (q == pq) ? inv : rji[q];
-          }
-        }
-      }
-    }
+    gj_invert<P, NTF>(v, gjs, pmin, pmax);  // the LDL^T pivots of A_II (natural order)
     // symmetrise in place, store packed, keep the full copy for the next plane
     if (lane_active) {
 #pragma unroll
