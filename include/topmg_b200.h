@@ -71,6 +71,8 @@ typedef struct {
   double eig_tol;      /* residual tolerance relative to ||B||, 0 -> 1e-11 */
   int eig_degree;      /* Chebyshev filter degree, 0 -> 32 */
   int eig_max_outer;   /* filter/Rayleigh-Ritz rounds, 0 -> 60 */
+  int warm_start;      /* 1: start the local eigensolver from the previous set-up's
+                          bases (same context; a design iteration's re-set-up) */
 } tmg_mmg_options;
 
 /* SolveReport (solver.hpp:15-22). */

@@ -79,6 +79,7 @@ struct Slab {
   // preconditioner
   double* dinv = nullptr;
   double* phi = nullptr;
+  double* phi_keep = nullptr;  // last set-up's bases (warm start of the next one)
   double* evals = nullptr;
   int* eig_iters = nullptr;
   double* Gf = nullptr;
@@ -124,6 +125,7 @@ struct tmg_ctx {
   int kind = -1;
   bool have_setup = false;
   int lc = 4, lcc = 8;
+  int lc_keep = 0;  // L_c of the kept bases
   int64_t n_cc = 0;
   double* AccT = nullptr;   // single slab: lower 64x64 tiles of A_cc^-1
   double* symvP = nullptr;  // single slab: GEMV partials
@@ -249,7 +251,12 @@ void dfree_null(tmg_ctx* c, T*& p) {
 void free_setup(tmg_ctx* c) {
   for (Slab& s : c->slabs) {
     dfree_null(c, s.dinv);
-    dfree_null(c, s.phi);
+    if (s.phi) {  // kept for a warm-started re-set-up (tmg_mmg_options.warm_start)
+      dfree_null(c, s.phi_keep);
+      s.phi_keep = s.phi;
+      s.phi = nullptr;
+      c->lc_keep = c->lc;
+    }
     dfree_null(c, s.evals);
     dfree_null(c, s.eig_iters);
     dfree_null(c, s.Gf);
@@ -1173,7 +1180,9 @@ int tmg_simp_step(tmg_ctx* c, tmg_simp_report* rep) {
   });
   if (rc) return rc;
   if ((rc = finish_problem(c))) return rc;  // mask, faces, coefficients
-  if ((rc = tmg_setup(c, &S.mmg))) return rc;
+  tmg_mmg_options mo = S.mmg;
+  mo.warm_start = S.iter > 0;  // consecutive designs differ little
+  if ((rc = tmg_setup(c, &mo))) return rc;
   r.setup_seconds = c->setup_seconds;
   rc = guard(c, [&] {
     Slab& s = c->slabs[0];
@@ -1301,7 +1310,15 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
   }
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
-    free_setup(c);
+    free_setup(c);  // the current bases (if any) move to phi_keep
+    // warm start: the last set-up's bases seed the local eigensolver
+    std::vector<double*> phi_prev(c->slabs.size(), nullptr);
+    const bool warm = kind == TMG_PRECOND_MMG && o->warm_start && c->lc_keep == (int)o->num_local_basis;
+    for (size_t k = 0; k < c->slabs.size(); ++k) {
+      phi_prev[k] = warm ? c->slabs[k].phi_keep : nullptr;
+      if (!warm) dfree_null(c, c->slabs[k].phi_keep);
+      c->slabs[k].phi_keep = nullptr;
+    }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1356,10 +1373,13 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
       const int degree = o->eig_degree > 0 ? o->eig_degree : 32;
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
-      for (Slab& s : c->slabs)
-        launch_local_basis(s.g, c->cb, s.kappa, s.phi, s.evals, s.eig_iters, tol, degree,
-                           max_outer, c->stream);
+      for (size_t k = 0; k < c->slabs.size(); ++k) {
+        Slab& s = c->slabs[k];
+        launch_local_basis(s.g, c->cb, s.kappa, phi_prev[k], s.phi, s.evals, s.eig_iters, tol,
+                           degree, max_outer, c->stream);
+      }
       CK(cudaGetLastError());
+      for (double*& pp : phi_prev) dfree_null(c, pp);  // stream-ordered reuse only
       XCH(phi, sizeof(double) * lc * C, false);
       mark("local_basis");
       for (Slab& s : c->slabs)

@@ -86,9 +86,10 @@ void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, cons
 int64_t thomas_doubles_per_brick(int cb);
 
 // spectral.cu
-void launch_local_basis(const GridParams& g, int cb, const double* kappa, double* phi,
-                        double* evals, int* iters, double tol, int degree, int max_outer,
-                        cudaStream_t s);
+// phi0: previous bases as the initial block (warm start) or nullptr
+void launch_local_basis(const GridParams& g, int cb, const double* kappa, const double* phi0,
+                        double* phi, double* evals, int* iters, double tol, int degree,
+                        int max_outer, cudaStream_t s);
 
 // coarse.cu
 int compiled_lc();

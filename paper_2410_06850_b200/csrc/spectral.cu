@@ -277,6 +277,7 @@ __device__ __forceinline__ bool cholqr_apply(double (&x)[K], const double* g, do
 template <int CB, int K>
 __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
                                                              const double* __restrict__ kappa,
+                                                             const double* __restrict__ phi0,
                                                              double* phi, double* evals,
                                                              int* iters_out, double tol,
                                                              int degree, int max_outer) {
@@ -334,16 +335,29 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   __syncthreads();
   const double bmax = scal[0];
   __syncthreads();
-  // initial block: constant mode in B-space (sqrt(mass)) + pseudo-random
+  // initial block: constant mode in B-space (sqrt(mass)) + pseudo-random, or
+  // (warm start) the previous set-up's M-orthonormal bases mapped to the
+  // B metric, x = M^{1/2} phi, completed by pseudo-random vectors
+  // A warm start that has not converged after kWarmOuter rounds restarts once
+  // from the cold block (a stagnating seed costs at most kWarmOuter rounds).
+  constexpr int kWarmOuter = 20;
   double x[K], y[K];
+  double theta[K];
+  double a_cut = 0.0;
+  int outer = 0, outer_total = 0;
+  bool converged = false;
+  for (int attempt = 0; attempt < (phi0 ? 2 : 1) && !converged; ++attempt) {
+  const bool warm = phi0 && attempt == 0;
   x[0] = sqrt(mass);
 #pragma unroll
   for (int k = 1; k < K; ++k) x[k] = hash_uniform(b, t, k);
-  double theta[K];
-  double a_cut = 0.5 * bmax;
-  int outer = 0;
-  bool converged = false;
-  for (outer = 0; outer <= max_outer; ++outer) {
+  if (warm) {
+    const double sm_ = sqrt(mass);
+    for (int k = 0; k < g.lc && k < K; ++k) x[k] = sm_ * phi0[(b * g.lc + k) * C + t];
+  }
+  a_cut = 0.5 * bmax;
+  const int outer_cap = warm && kWarmOuter < max_outer ? kWarmOuter : max_outer;
+  for (outer = 0; outer <= outer_cap; ++outer) {
     // --- orthonormalise (CholQR twice) ---
     for (int pass = 0; pass < 2; ++pass) {
       gram_mma<CB, K>(x, x, true, xs, ys, red, gs);
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
     double worst = 0.0;
     for (int c = 0; c < g.lc; ++c) worst = fmax(worst, sqrt(fmax(rsm[c * K + c], 0.0)));
     if (worst <= tol * bmax) { converged = true; break; }
-    if (outer == max_outer) break;
+    if (outer == outer_cap) break;
     // --- Chebyshev filter damping [a_cut, bmax], normalised at 0 ---
     a_cut = fmin(fmax(theta[K - 1], 1e-6 * bmax), 0.95 * bmax);
     const double e = 0.5 * (bmax - a_cut), c0 = 0.5 * (bmax + a_cut);
@@ -427,6 +441,8 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
 #pragma unroll
     for (int k = 0; k < K; ++k) x[k] = y[k];
   }
+  outer_total += outer;
+  }  // attempt
   // sign convention: sum of each vector >= 0
   double sg[K];
 #pragma unroll
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   }
   if (t == 0) {
     for (int a = 0; a < g.lc; ++a) evals[b * g.lc + a] = theta[a];
-    iters_out[b] = converged ? outer : -outer - 1;
+    iters_out[b] = converged ? outer_total : -outer_total - 1;
   }
 }
 
@@ -448,17 +464,17 @@ size_t local_basis_smem(int cb, int K) {
   return sizeof(double) * (size_t)(K * C + C + red + 3 * K * K + K + 8 + 2 * K * (C + 4));
 }
 
-void launch_local_basis(const GridParams& g, int cb, const double* kappa, double* phi,
-                        double* evals, int* iters, double tol, int degree, int max_outer,
-                        cudaStream_t s) {
+void launch_local_basis(const GridParams& g, int cb, const double* kappa, const double* phi0,
+                        double* phi, double* evals, int* iters, double tol, int degree,
+                        int max_outer, cudaStream_t s) {
   const size_t smem = local_basis_smem(cb, 8);
   if (cb == 8) {
     cudaFuncSetAttribute(k_local_basis<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_local_basis<8, 8><<<(unsigned)g.nbo, 512, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+    k_local_basis<8, 8><<<(unsigned)g.nbo, 512, smem, s>>>(g, kappa, phi0, phi, evals, iters, tol, degree,
                                                          max_outer);
   } else {
     cudaFuncSetAttribute(k_local_basis<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_local_basis<4, 8><<<(unsigned)g.nbo, 64, smem, s>>>(g, kappa, phi, evals, iters, tol, degree,
+    k_local_basis<4, 8><<<(unsigned)g.nbo, 64, smem, s>>>(g, kappa, phi0, phi, evals, iters, tol, degree,
                                                         max_outer);
   }
 }

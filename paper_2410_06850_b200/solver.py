@@ -53,7 +53,8 @@ class _Patch(C.Structure):
 class _Opts(C.Structure):
     _fields_ = [("kind", C.c_int), ("num_local_basis", C.c_int64),
                 ("num_cc_basis", C.c_int64), ("smoother_sweeps", C.c_int),
-                ("eig_tol", C.c_double), ("eig_degree", C.c_int), ("eig_max_outer", C.c_int)]
+                ("eig_tol", C.c_double), ("eig_degree", C.c_int), ("eig_max_outer", C.c_int),
+                ("warm_start", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -192,6 +193,7 @@ class MmgOptions:
     eig_tol: float = 0.0
     eig_degree: int = 0
     eig_max_outer: int = 0
+    warm_start: bool = False  # start the local eigensolver from the previous set-up's bases
 
 
 @dataclass
@@ -331,7 +333,8 @@ class Context:
                   source=1.0, rtol=1e-8, maxit=10000, rho0=None, mmg: MmgOptions = MmgOptions()):
         o = _SimpOpts(volfrac, rmin, move, kappa_lo, kappa_hi, p, source, rtol, maxit)
         m = _Opts(PrecondKind.parse("mmg"), mmg.num_local_basis, mmg.num_cc_basis,
-                  mmg.smoother_sweeps, mmg.eig_tol, mmg.eig_degree, mmg.eig_max_outer)
+                  mmg.smoother_sweeps, mmg.eig_tol, mmg.eig_degree, mmg.eig_max_outer,
+                  int(mmg.warm_start))
         r0 = _ptr(_f64(rho0)) if rho0 is not None else None
         self._check(native().tmg_simp_init(self._p, C.byref(o), C.byref(m), r0))
 
@@ -360,7 +363,7 @@ class Context:
         else:
             self.kind_name = [k for k, v in PrecondKind._names.items() if v == kind][0]
         o = _Opts(kind, opts.num_local_basis, opts.num_cc_basis, opts.smoother_sweeps,
-                  opts.eig_tol, opts.eig_degree, opts.eig_max_outer)
+                  opts.eig_tol, opts.eig_degree, opts.eig_max_outer, int(opts.warm_start))
         self._check(native().tmg_setup(self._p, C.byref(o)))
 
     # operators

@@ -497,3 +497,27 @@ def test_device_sensitivity_bitwise_vs_reference(n, p, f0, slabs):
     c.set_design(rho, 1e-3, 1.0, p, bc)
     g = c.sensitivity(rho, t, u, 1e-3, 1.0, f0, p)
     np.testing.assert_array_equal(g, O.ref_sensitivity(n, rho, t, u, 1e-3, 1.0, f0, p, patches))
+
+
+def test_warm_started_setup_matches_cold():
+    # SIMP re-set-up (tmg_mmg_options.warm_start): the local eigensolver starts
+    # from the previous bases; the hierarchy converges to the same spans
+    n = 32
+    rho = inputs.box_filter_design(n, 0.3)
+    rng = np.random.default_rng(60)
+    rho2 = np.clip(rho + 0.05 * rng.standard_normal(n ** 3), 0.0, 1.0)
+    k2 = inputs.conductivity(rho2, 1e-6)
+    warm = ctx_for(n, 2, 2, inputs.conductivity(rho, 1e-6))
+    warm.setup("mmg")
+    warm.set_conductivity(k2, BC)
+    warm.setup("mmg", MmgOptions(warm_start=True))
+    _, _, it_w = warm.local_bases()
+    cold = ctx_for(n, 2, 2, k2)
+    cold.setup("mmg")
+    _, _, it_c = cold.local_bases()
+    # every brick converges (a stagnating seed restarts cold) to the same spans
+    assert (it_w >= 0).all() and (it_c >= 0).all()
+    b = cold.assemble_rhs(np.ones(n ** 3))
+    rw, rc = warm.pcg(b, rtol=1e-8), cold.pcg(b, rtol=1e-8)
+    assert abs(rw.report.iterations - rc.report.iterations) <= 1
+    assert np.linalg.norm(rw.x - rc.x) <= 1e-6 * np.linalg.norm(rc.x)
