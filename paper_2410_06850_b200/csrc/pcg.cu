@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const doubl
 constexpr int kStencilThreads = 256;  // CTA size of the stencil kernels (2 cells/thread at CB = 8)
 
 template <int CB>
-__global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, const double* __restrict__ coef,
+#ifndef TMG_SEARCH_MINB
+#define TMG_SEARCH_MINB 8
+#endif
+__global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(GridParams g, const double* __restrict__ coef,
                                                               int64_t M, const double* __restrict__ z,
                                                               const double* __restrict__ p_old, double* p,
                                                               double* q, PcgState* st, double* partials) {
@@ -205,12 +208,12 @@ __global__ void __launch_bounds__(kStencilThreads, 8) k_search(GridParams g, con
   __shared__ int flag;
   const int t = threadIdx.x;
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
-  load_coefs<CB>(coef, M, cs, g, bc);  // constant: before the dependency wait
   pdl_wait();
   if (st->done) return;
   const bool first = st->first;
   const double beta = st->beta;
-  load_tile_axpy<CB>(z, p_old, beta, first, pt, g, bc);  // p = z + beta p (solver.cpp:565-567)
+  // coefficients + p = z + beta p over the tile (solver.cpp:565-567)
+  load_coefs_tile_axpy<CB, NT>(coef, M, cs, z, p_old, beta, first, pt, g, bc);
   __syncthreads();
   double pq = 0.0;
 #pragma unroll

@@ -254,6 +254,94 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ coef, int6
   }
 }
 
+// load_coefs + load_tile_axpy for a CTA of exactly NT threads: every global
+// load of a thread is issued before the first shared-memory store, so ~16
+// loads per thread are in flight instead of the few of a load/store loop.
+template <int CB, int NT>
+__device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ coef, int64_t M,
+                                                     CoefSmem<CB>& cs, const double* __restrict__ z,
+                                                     const double* __restrict__ p_old, double beta,
+                                                     bool first, double* tile,
+                                                     const GridParams& g, const BrickCoord& bc) {
+  constexpr int C = CB * CB * CB, F = CB * CB;
+  constexpr int KO = (C + NT - 1) / NT;          // own cells per thread
+  constexpr int KH = (6 * F + NT - 1) / NT;      // halo cells per thread
+  constexpr int KC = (3 * F + NT - 1) / NT;      // coefficient halo entries per thread
+  const int t = threadIdx.x;
+  double cf[KO][4], zo[KO], po[KO], zh[KH], ph[KH], ch[KC];
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int c = t + k * NT;
+    if (c < C) {
+      const size_t s = bofs(bc.b, C) + c;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) cf[k][a] = __ldg(coef + (size_t)a * M + s);
+      zo[k] = __ldg(z + s);
+      po[k] = first ? 0.0 : __ldg(p_old + s);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KH; ++k) {
+    const int h = t + k * NT;
+    zh[k] = 0.0;
+    ph[k] = 0.0;
+    if (h < 6 * F) {
+      int f, ti, nl;
+      halo_slot<CB>(h, f, ti, nl);
+      const int nb = nbr_brick(g, bc, f);
+      if (nb >= 0) {
+        const size_t s = bofs(nb, C) + nl;
+        zh[k] = __ldg(z + s);
+        ph[k] = first ? 0.0 : __ldg(p_old + s);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int h = t + k * NT;
+    ch[k] = 0.0;
+    if (h < 3 * F) {
+      const int ax = h / F, q = h % F, u = q % CB, w = q / CB;
+      const int nb = nbr_brick(g, bc, 2 * ax);
+      const int nl = ax == 0 ? (CB - 1) + CB * (u + CB * w)
+                             : ax == 1 ? u + CB * ((CB - 1) + CB * w) : u + CB * (w + CB * (CB - 1));
+      if (nb >= 0) ch[k] = __ldg(coef + (size_t)ax * M + bofs(nb, C) + nl);
+    }
+  }
+  // stores
+#pragma unroll
+  for (int k = 0; k < KO; ++k) {
+    const int c = t + k * NT;
+    if (c < C) {
+      const int li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+      cs.fx[Tile<CB>::fxi(li, lj, lk)] = cf[k][0];
+      cs.fy[Tile<CB>::fyi(li, lj, lk)] = cf[k][1];
+      cs.fz[Tile<CB>::fzi(li, lj, lk)] = cf[k][2];
+      cs.dg[c] = cf[k][3];
+      tile[Tile<CB>::idx(li, lj, lk)] = first ? zo[k] : zo[k] + beta * po[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KH; ++k) {
+    const int h = t + k * NT;
+    if (h < 6 * F) {
+      int f, ti, nl;
+      halo_slot<CB>(h, f, ti, nl);
+      tile[ti] = first ? zh[k] : zh[k] + beta * ph[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int h = t + k * NT;
+    if (h < 3 * F) {
+      const int ax = h / F, q = h % F, u = q % CB, w = q / CB;
+      const int fi = ax == 0 ? Tile<CB>::fxi(-1, u, w)
+                             : ax == 1 ? Tile<CB>::fyi(u, -1, w) : Tile<CB>::fzi(u, w, -1);
+      (ax == 0 ? cs.fx : ax == 1 ? cs.fy : cs.fz)[fi] = ch[k];
+    }
+  }
+}
+
 // (A x)_c, branch-free: missing neighbours have T = 0 and a 0 halo value, so
 // their -0 terms leave the sum bitwise unchanged; order and rounding are those
 // of SparseOperator::apply on the assembled row (sparse.cpp:76-83).
