@@ -1,4 +1,9 @@
 // Coarsest-level direct solve (north_star item 6).
+// The Gauss-Jordan sweeps keep only the lower triangle: for SPD A every sweep
+// preserves A_ij = s_i s_j A_ji with s = -1 on processed pivot blocks, so the
+// pivot row/column panels are rebuilt from lower entries, the trailing
+// update skips tiles above the diagonal (half the DMMA work), and the final
+// pass mirrors the symmetric inverse.
 //
 // Reference: DirectSolver (proj/core/src/solver.cpp:60-126) factorises A_cc
 // with LDL^T once per set-up and solves once per V-cycle (:304). Here the SPD
@@ -34,7 +39,8 @@ __global__ void __launch_bounds__(kDiagThreads) k_gj_diag(const double* __restri
 #pragma unroll
     for (int q = 0; q < CW; ++q) {
       const int j = c0 + q;
-      v[h][q] = (i < nbk && j < nbk) ? A[(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
+      v[h][q] = (i < nbk && j < nbk) ? (j <= i ? A[(k0 + i) * n + k0 + j] : A[(k0 + j) * n + k0 + i])
+                                     : (i == j ? 1.0 : 0.0);
     }
   }
   double pmin = 1e300, pmax = 0.0;
@@ -65,7 +71,12 @@ __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A,
     const int r = e / NB, c = e % NB;
     Ds[r][c] = (r < nbk && c < nbk) ? Dinv[r * nbk + c] : 0.0;
   }
-  for (int c = ry; c < NB; c += 8) As[c][jx] = (c < nbk && j < n) ? A[(k0 + c) * n + j] : 0.0;
+  // A_{K,j} from the lower triangle: below the diagonal directly, above it
+  // (j > row, both unprocessed: symmetric) from the mirror entry
+  for (int c = ry; c < NB; c += 8) {
+    const int64_t r = k0 + c;
+    As[c][jx] = (c < nbk && j < n) ? (j <= r ? A[r * n + j] : A[j * n + r]) : 0.0;
+  }
   __syncthreads();
   if (j < n) {
     constexpr int RG = NB / 8;
@@ -81,11 +92,16 @@ __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A,
 #pragma unroll
     for (int q = 0; q < RG; ++q) Pn[(ry * RG + q) * n + j] = acc[q];
   }
-  // Cold: this CTA's 32 rows i = j-range, NB columns each
+  // Cold: this CTA's 32 rows i = j-range, NB columns each; A_{i,K} from the
+  // lower triangle (processed rows i < k0 carry the sign of the sweep:
+  // A_iK = -A_Ki^T)
   for (int e = t; e < 32 * NB; e += 256) {
     const int64_t i = blockIdx.x * 32LL + e / NB;
     const int c = e % NB;
-    if (i < n) Cold[i * NB + c] = c < nbk ? A[i * n + k0 + c] : 0.0;
+    const int64_t col = k0 + c;
+    double v = 0.0;
+    if (i < n && c < nbk) v = i >= col ? A[i * n + col] : (i >= k0 ? A[col * n + i] : -A[col * n + i]);
+    if (i < n) Cold[i * NB + c] = v;
   }
 }
 
@@ -113,6 +129,7 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
   double* As = smg;
   double* Bs = smg + GT * AS_LD;
   const int64_t i0 = (int64_t)blockIdx.y * GT, j0 = (int64_t)blockIdx.x * GN;
+  if (i0 + GT - 1 < j0) return;  // strictly above the diagonal: not maintained
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   if (t < GT && i0 + t < n) {
     const int64_t cols = (n - j0) < GN ? (n - j0) : GN;
@@ -189,18 +206,18 @@ __global__ void __launch_bounds__(256) k_gj_fix(double* A, int64_t n, int64_t k0
                                                 const double* __restrict__ Cold) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * nbk) return;
-  // rows: e -> (r, j)
+  // rows: e -> (r, j); the lower triangle only (j < k0 + nbk)
   {
     const int r = (int)(e / n);
     const int64_t j = e % n;
     const bool jK = j >= k0 && j < k0 + nbk;
-    A[(k0 + r) * n + j] = jK ? Dinv[r * nbk + (j - k0)] : Pn[r * n + j];
+    if (j < k0 + nbk) A[(k0 + r) * n + j] = jK ? Dinv[r * nbk + (j - k0)] : Pn[r * n + j];
   }
-  // columns: e -> (i, c)
+  // columns: e -> (i, c); below the pivot block only
   {
     const int64_t i = e / nbk;
     const int c = (int)(e % nbk);
-    if (i < k0 || i >= k0 + nbk) {
+    if (i >= k0 + nbk) {
       double s = 0.0;
       for (int q = 0; q < nbk; ++q) s = fma(Cold[i * NB + q], Dinv[q * nbk + c], s);
       A[i * n + k0 + c] = -s;
@@ -212,11 +229,7 @@ __global__ void k_symmetrize(double* A, int64_t n) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * n) return;
   const int64_t i = e / n, j = e % n;
-  if (i < j) {
-    const double s = 0.5 * (A[i * n + j] + A[j * n + i]);
-    A[i * n + j] = s;
-    A[j * n + i] = s;
-  }
+  if (i < j) A[i * n + j] = A[j * n + i];  // the sweeps kept the lower triangle
 }
 
 __global__ void k_pivot_check(const double* pivots, int64_t n, int* status) {
