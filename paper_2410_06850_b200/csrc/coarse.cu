@@ -188,10 +188,15 @@ __device__ void build_elem_matrix(const GridParams& g, const ElemCoord& ec, cons
   __syncthreads();
 }
 
-// Warp-parallel cyclic Jacobi on q x q (q <= 64) symmetric M in smem;
+// Warp-parallel Jacobi on q x q (q even, q <= 64) symmetric M in smem;
 // V (q x q) eigenvectors in columns. Lanes own rows r = lane, lane+32.
 __device__ void warp_jacobi(double* M, double* V, int q) {
-  const int lane = threadIdx.x & 31;
+  // round-robin ("tournament") ordering: a sweep is q-1 rounds of q/2
+  // disjoint rotations (q even, q <= 64); lane g computes rotation g of the
+  // round, then every lane applies all of them to its rows / columns.
+  __shared__ double rc[32], rs[32];
+  __shared__ int rp[32], rq[32];
+  const int lane = threadIdx.x & 31, np = q / 2;
   for (int r = lane; r < q; r += 32)
     for (int c = 0; c < q; ++c) V[r * q + c] = r == c ? 1.0 : 0.0;
   __syncwarp();
@@ -208,31 +213,58 @@ __device__ void warp_jacobi(double* M, double* V, int q) {
       tot += __shfl_xor_sync(0xffffffffu, tot, o);
     }
     if (off <= 1e-26 * tot || off == 0.0) break;
-    for (int p = 0; p < q - 1; ++p)
-      for (int qq = p + 1; qq < q; ++qq) {
+    for (int round = 0; round < q - 1; ++round) {
+      if (lane < np) {  // circle method: player q-1 fixed
+        int p, qq;
+        if (lane == 0) {
+          p = round;
+          qq = q - 1;
+        } else {
+          p = (round + lane) % (q - 1);
+          qq = (round - lane + (q - 1)) % (q - 1);
+        }
+        if (p > qq) {
+          const int tmp = p;
+          p = qq;
+          qq = tmp;
+        }
         const double apq = M[p * q + qq];
         const double app = M[p * q + p], aqq = M[qq * q + qq];
-        if (fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq))) continue;
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
-        __syncwarp();
-        for (int r = lane; r < q; r += 32) {
-          const double akp = M[r * q + p], akq = M[r * q + qq];
-          M[r * q + p] = c * akp - s * akq;
-          M[r * q + qq] = s * akp + c * akq;
-          const double vkp = V[r * q + p], vkq = V[r * q + qq];
-          V[r * q + p] = c * vkp - s * vkq;
-          V[r * q + qq] = s * vkp + c * vkq;
+        double c = 1.0, sn = 0.0;
+        if (!(fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq)))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(tt * tt + 1.0);
+          sn = tt * c;
         }
-        __syncwarp();
-        for (int r = lane; r < q; r += 32) {
-          const double apk = M[p * q + r], aqk = M[qq * q + r];
-          M[p * q + r] = c * apk - s * aqk;
-          M[qq * q + r] = s * apk + c * aqk;
-        }
-        __syncwarp();
+        rc[lane] = c;
+        rs[lane] = sn;
+        rp[lane] = p;
+        rq[lane] = qq;
       }
+      __syncwarp();
+      for (int r = lane; r < q; r += 32)  // columns p, qq of row r (pairs disjoint)
+        for (int g = 0; g < np; ++g) {
+          const int p = rp[g], qq = rq[g];
+          const double c = rc[g], sn = rs[g];
+          const double akp = M[r * q + p], akq = M[r * q + qq];
+          M[r * q + p] = c * akp - sn * akq;
+          M[r * q + qq] = sn * akp + c * akq;
+          const double vkp = V[r * q + p], vkq = V[r * q + qq];
+          V[r * q + p] = c * vkp - sn * vkq;
+          V[r * q + qq] = sn * vkp + c * vkq;
+        }
+      __syncwarp();
+      for (int r = lane; r < q; r += 32)  // rows p, qq at column r
+        for (int g = 0; g < np; ++g) {
+          const int p = rp[g], qq = rq[g];
+          const double c = rc[g], sn = rs[g];
+          const double apk = M[p * q + r], aqk = M[qq * q + r];
+          M[p * q + r] = c * apk - sn * aqk;
+          M[qq * q + r] = sn * apk + c * aqk;
+        }
+      __syncwarp();
+    }
   }
 }
 
