@@ -291,7 +291,11 @@ def run_ours(args):
     b = ctx.assemble_rhs(np.ones(M_local))
     barrier()
     t0 = time.perf_counter()
-    ctx.setup("mmg")
+    ctx.setup("mmg")  # first set-up: includes module loading and allocations
+    setup_cold_wall = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    t0 = time.perf_counter()
+    ctx.setup("mmg")  # re-set-up (a design iteration's cost; buffers pooled)
     setup_wall = max_over_ranks(time.perf_counter() - t0)
     ctx.upload_rhs(b)
     for _ in range(max(3, args.warmup)):
@@ -364,7 +368,7 @@ def run_ours(args):
         return 0
     extra = {
         "iterations": iters, "setup_ms": 1e3 * rep.setup_seconds,
-        "setup_wall_ms": 1e3 * setup_wall,
+        "setup_wall_ms": 1e3 * setup_wall, "setup_cold_wall_ms": 1e3 * setup_cold_wall,
         "time_to_solution_ms": 1e3 * rep.setup_seconds + ms,
         "true_relative_residual": true_rel,
         "parallelism": f"z-slabs x{world} over NCCL (one {n}^3 slab per GPU)" if world > 1
