@@ -26,15 +26,23 @@ struct SymvSmem {
   double colp[4][TS];
 };
 
-// dynamic shared memory of a CTA that runs the GEMV: ring + all of x
+// x is staged in shared memory up to this many unknowns; larger systems read
+// it from global memory (L2-resident) tile by tile
+constexpr int64_t kSymvStageMax = 12288;
+__host__ __device__ inline bool symv_staged(int64_t n) { return n <= kSymvStageMax; }
+
+// dynamic shared memory of a CTA that runs the GEMV: ring (+ all of x)
 inline size_t symv_dyn_smem(int64_t n) {
   const int64_t nt = (n + TS - 1) / TS;
-  return sizeof(double) * (size_t)(kSymvSlots * TS * TS + nt * TS);
+  return sizeof(double) * (size_t)(kSymvSlots * TS * TS + (symv_staged(n) ? nt * TS : 0));
 }
 
+// lower-triangle tile index -> (I, J <= I): closed-form triangular root,
+// corrected by one step either way against rounding
 __device__ __forceinline__ void symv_tile_ij(int64_t tile, int64_t& I, int64_t& J) {
-  I = 0;
-  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  I = (int64_t)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+  if (I * (I + 1) / 2 > tile) --I;
+  if ((I + 1) * (I + 2) / 2 <= tile) ++I;
   J = tile - I * (I + 1) / 2;
 }
 
@@ -73,15 +81,31 @@ __device__ __forceinline__ void symv_run(SymvSmem& ss, double* ring, double* xs,
                                          const double* __restrict__ x, double* P) {
   const int64_t nt = (n + TS - 1) / TS, ntiles = nt * (nt + 1) / 2;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int64_t k = t; k < nt * TS; k += blockDim.x) xs[k] = k < n ? __ldcg(x + k) : 0.0;
+  const bool staged = symv_staged(n);
+  if (staged)
+    for (int64_t k = t; k < nt * TS; k += blockDim.x) xs[k] = k < n ? __ldcg(x + k) : 0.0;
+  // large systems: a per-tile copy of the two x segments (the last tile row
+  // is zero padded past n)
+  __shared__ double xseg[2][TS];
   __syncthreads();
   int64_t tile = blockIdx.x;
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     const int slot = it % kSymvSlots;
     int64_t I, J;
     symv_tile_ij(tile, I, J);
-    const double* xi = xs + I * TS;
-    const double* xj = xs + J * TS;
+    const double* xi;
+    const double* xj;
+    if (staged) {
+      xi = xs + I * TS;
+      xj = xs + J * TS;
+    } else {
+      if (t < 2 * TS) {
+        const int64_t k = (t < TS ? I : J) * TS + (t % TS);
+        xseg[t / TS][t % TS] = k < n ? __ldcg(x + k) : 0.0;
+      }
+      xi = xseg[0];
+      xj = xseg[1];
+    }
     mbar_wait(&ss.bars[slot], (uint32_t)((it / kSymvSlots) & 1));
     __syncthreads();
     const double* A = ring + slot * TS * TS;

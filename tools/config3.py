@@ -1,0 +1,62 @@
+"""BASELINE configs[3] on one B200: 512^3 cells (~1.34e8 DoF), seeded box-filter
+design (vf 0.2, radius 4, 3 passes), kmin 1e-6, MMG-PCG to rtol 1e-8.
+
+Hierarchy: c = 8, sd = 2, ncc = 32 (the GPU cc eigensolver handles
+sd^3 L_c <= 64), L_c = 4 and a small L_cc so that the dense A_cc^-1 fits
+(n_cc = 32768 L_cc: 8.6 GB at L_cc = 1). SURVEY.md suggests sd = 8 / ncc = 8
+(n_cc = 4096), which needs the block-sparse coarse smoother and cc
+eigensolver listed as next steps in DESIGN.md §8.
+
+    python tools/config3.py [--n 512] [--lcc 1] [--solves 2] [--out file.json]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, R)
+from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=512)
+ap.add_argument("--lcc", type=int, default=1)
+ap.add_argument("--solves", type=int, default=2)
+ap.add_argument("--out", default=None)
+a = ap.parse_args()
+n = a.n
+t0 = time.perf_counter()
+rho = inputs.box_filter_design(n, 0.2, passes=3, radius=4)
+kappa = inputs.conductivity(rho, 1e-6)
+del rho
+t_gen = time.perf_counter() - t0
+ncc = n // 16
+c = Context(GridSpec(n, n, n), ncc, 2)
+c.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))
+b = c.assemble_rhs(np.ones(n ** 3))
+del kappa
+t0 = time.perf_counter()
+c.setup("mmg", MmgOptions(num_cc_basis=a.lcc))
+t_setup = time.perf_counter() - t0
+c.upload_rhs(b)
+reps = [c.solve_resident(1e-8, 20000) for _ in range(a.solves)]
+rep = reps[-1]
+x = c.download_solution()
+true_rel = float(np.linalg.norm(b - c.apply_operator(x)) / np.linalg.norm(b))
+out = {
+    "workload": f"BASELINE configs[3]-style: {n}^3 cells, vf 0.2, radius 4, kmin 1e-6, rtol 1e-8",
+    "hierarchy": f"c=8 sd=2 ncc={ncc} L_c=4 L_cc={a.lcc} (n_cc={ncc ** 3 * a.lcc})",
+    "cells": n ** 3, "iterations": rep.iterations, "converged": rep.converged,
+    "solve_s": rep.solve_seconds, "setup_s": t_setup,
+    "mdof_iter_per_s": n ** 3 * rep.iterations / rep.solve_seconds / 1e6,
+    "ms_per_iteration": 1e3 * rep.solve_seconds / rep.iterations,
+    "true_relative_residual": true_rel, "device_gb": c.device_bytes() / 1e9,
+    "design_generation_s": t_gen,
+}
+print(json.dumps(out))
+if a.out:
+    with open(a.out, "w") as f:
+        json.dump(out, f, indent=1)

@@ -3,7 +3,7 @@ import argparse, os, sys
 import numpy as np
 R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, R)
-from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs
+from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, inputs
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=128)
@@ -14,6 +14,7 @@ ap.add_argument("--kind", default="mmg")
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--setups", type=int, default=1)
 ap.add_argument("--slabs", type=int, default=1)
+ap.add_argument("--lcc", type=int, default=8)
 a = ap.parse_args()
 n = a.n
 rho = inputs.box_filter_design(n, 0.3)
@@ -24,7 +25,7 @@ b = ctx.assemble_rhs(np.ones(n ** 3))
 import time
 for _ in range(a.setups):
     t0 = time.perf_counter()
-    ctx.setup(a.kind)
+    ctx.setup(a.kind, MmgOptions(num_cc_basis=a.lcc))
     print("setup wall ms %.2f" % ((time.perf_counter() - t0) * 1e3))
 ctx.upload_rhs(b)
 for _ in range(a.solves):
