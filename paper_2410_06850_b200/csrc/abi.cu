@@ -1302,9 +1302,11 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       return set_err(c, TMG_EARG,
                      "coarse_coarse_basis: more eigenvectors than coarse basis functions");
     if (o->num_cc_basis < 1) return set_err(c, TMG_EARG, "num_cc_basis must be >= 1");
-    if (q > 64)
-      return set_err(c, TMG_ENOTSUP, "GPU coarse-coarse eigensolver handles sd^3*L_c <= 64 (got %lld)",
-                     (long long)q);
+    if (q > 64 && !coarse_large_supported((int)q, (int)o->num_cc_basis))
+      return set_err(c, TMG_ENOTSUP,
+                     "GPU coarse level handles sd^3*L_c <= 64, or a multiple of 64 up to 256 with "
+                     "num_cc_basis <= 12 (got %lld, %lld)",
+                     (long long)q, (long long)o->num_cc_basis);
     if (o->smoother_sweeps != 1)
       return set_err(c, TMG_ENOTSUP, "GPU smoother is built for smoother_sweeps = 1");
   }
@@ -1386,12 +1388,31 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         launch_coarse_blocks(s.g, c->cb, s.kappa, s.dmask, s.phi, s.Ac, s.Bc, c->stream);
       CK(cudaGetLastError());
       mark("coarse_blocks");
-      for (Slab& s : c->slabs) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
+      int* cc_iters = nullptr;
+      if (sprof && q > 64) {
+        cc_iters = dalloc<int>(c, 1);
+        CK(cudaMemsetAsync(cc_iters, 0, sizeof(int), c->stream));
+      }
+      for (Slab& s : c->slabs) {
+        if (q <= 64) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
+        else  // Winv's storage holds the shifted inverses until the smoother overwrites it
+          launch_cc_basis_large(s.g, s.Ac, s.Bc, s.Winv, s.Rcc, s.cc_evals, s.d_status + 3,
+                                cc_iters, 1e-12, 100, c->stream);
+      }
+      if (cc_iters) {
+        int it = 0;
+        CK(cudaMemcpyAsync(&it, cc_iters, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        fprintf(stderr, "[setup] cc subspace iterations (max over elements): %d\n", it);
+        dfree(c, cc_iters);
+      }
       CK(cudaGetLastError());
       XCH(Rcc, sizeof(double) * lcc * q, true);
       mark("cc_basis");
-      for (Slab& s : c->slabs)
-        launch_coarse_smoother(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
+      for (Slab& s : c->slabs) {
+        if (q <= 64) launch_coarse_smoother(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
+        else launch_coarse_smoother_large(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
+      }
       CK(cudaGetLastError());
       mark("coarse_smoother");
       for (Slab& s : c->slabs)

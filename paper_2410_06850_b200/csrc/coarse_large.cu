@@ -1,0 +1,530 @@
+// Coarse level for large cc elements (q = sd^3 L_c > 64, e.g. sd = 4: q = 256;
+// the 512^3 / 1024^3 hierarchies of SURVEY.md §8). The element matrices no
+// longer fit in shared memory, so they live in global memory (L2-resident per
+// CTA) and are inverted by a batched blocked Gauss-Jordan with 64 x 64 pivot
+// blocks (register-resident pivot inversion, gj.cuh); the cc eigenproblem is
+// solved by subspace iteration on a shifted inverse with Rayleigh-Ritz on the
+// projected stiffness (coarse_coarse_basis, coarse_space.cpp:343-406).
+#include "coarse_elem.cuh"
+#include "gj.cuh"
+
+namespace tmg {
+
+namespace {
+constexpr int GB = 64;        // pivot block
+constexpr int GJT = 256;      // threads of the batched inverse (one column each, q <= 256)
+constexpr int KS = 16;        // subspace width of the cc eigensolver (L_cc <= KS - 4)
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double m = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+  return m;
+}
+}  // namespace
+
+// Element matrix of A_c restricted to the cc element (couplings between its
+// children only), optionally minus the boundary terms Bc (the projected
+// stiffness of the cc eigenproblem) plus shift_rel * max_i M_ii * I;
+// symmetrised. One CTA per element, out[e - e0][q][q].
+__global__ void k_elem_matrix(GridParams g, const double* __restrict__ Ac,
+                              const double* __restrict__ Bc, double shift_rel, double* out) {
+  __shared__ double red[32];
+  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
+  const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
+  double* M = out + (int64_t)blockIdx.x * q * q;
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) M[e] = 0.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < nch * 7 * LC * LC; e += blockDim.x) {
+    const int ci = e / (7 * LC * LC), rem = e % (7 * LC * LC);
+    const int dir = rem / (LC * LC), ab = rem % (LC * LC), a = ab / LC, b = ab % LC;
+    const int64_t I = child_brick(g, ec, ci);
+    int cj;
+    if (dir == 0) cj = ci;
+    else {
+      const int64_t J = brick_nbr(g, I, dir - 1);
+      cj = J >= 0 ? child_index(g, ec, J) : -1;
+    }
+    if (cj < 0) continue;
+    double v = Ac[(I * 7 + dir) * LC * LC + ab];
+    if (dir == 0 && Bc) v -= Bc[I * LC * LC + ab];
+    M[(ci * LC + a) * q + cj * LC + b] += v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int i = e / q, j = e % q;
+    if (i < j) {
+      const double s = 0.5 * (M[i * q + j] + M[j * q + i]);
+      M[i * q + j] = s;
+      M[j * q + i] = s;
+    }
+  }
+  if (shift_rel == 0.0) return;
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) mx = fmax(mx, M[i * q + i]);
+  mx = block_max(mx, red);
+  for (int i = threadIdx.x; i < q; i += blockDim.x) M[i * q + i] += shift_rel * mx;
+}
+
+// In-place inverse of each SPD q x q matrix (q a multiple of 64, q <= 256):
+// blocked Gauss-Jordan sweeps with 64 x 64 pivot blocks. Thread j owns column
+// j: the trailing update A_ij -= Cold_i . Pn_j reads the old pivot columns
+// Cold (q x 64, shared memory) and keeps its own new pivot-row entries Pn_j
+// (64 values) in registers. Pivots checked with the reference's rule
+// (solver.cpp:86-92); status = 2 on failure. Symmetrised on exit.
+__global__ void __launch_bounds__(GJT, 1) k_batched_gj(double* A, int q, int* status) {
+  extern __shared__ __align__(16) double smg[];
+  double* Cold = smg;              // q x GB
+  double* Ds = Cold + q * GB;      // GB x GB
+  double* Dt = Ds + GB * GB;       // its transpose
+  __shared__ GjSmem<GB> gjs;
+  __shared__ double red[2][GJT / 32];
+  double* M = A + (int64_t)blockIdx.x * q * q;
+  const int t = threadIdx.x, lane = t & 31;
+  using L = GjLayout<GB, GJT>;
+  constexpr int CW = L::CW, RH = L::RH;
+  const int c0 = CW * (t >> 5);
+  double pmin = 1e300, pmax = 0.0;
+  for (int K = 0; K < q / GB; ++K) {
+    const int k0 = K * GB;
+    // (a) pivot block inverse (register-resident)
+    double v[RH][CW];
+#pragma unroll
+    for (int h = 0; h < RH; ++h)
+#pragma unroll
+      for (int qq = 0; qq < CW; ++qq) v[h][qq] = M[(k0 + lane + 32 * h) * q + k0 + c0 + qq];
+    gj_invert<GB, GJT>(v, gjs, pmin, pmax);
+#pragma unroll
+    for (int h = 0; h < RH; ++h)
+#pragma unroll
+      for (int qq = 0; qq < CW; ++qq) Ds[(lane + 32 * h) * GB + c0 + qq] = v[h][qq];
+    // (b) old pivot columns; D^-1 transposed for the pivot-row product
+    for (int e = t; e < q * GB; e += GJT) Cold[e] = M[(e / GB) * q + k0 + e % GB];
+    for (int e = t; e < GB * GB; e += GJT) Dt[e] = Ds[(e % GB) * GB + e / GB];
+    __syncthreads();
+    // (c) new pivot row entries of column j: Pn_j = D^-1 A_{K, j}
+    const int j = t;
+    const bool jcol = j < q;
+    double pn[GB];
+#pragma unroll
+    for (int r = 0; r < GB; ++r) pn[r] = 0.0;
+    if (jcol) {
+      for (int k = 0; k < GB; ++k) {
+        const double a = M[(int64_t)(k0 + k) * q + j];
+        const double2* dk = reinterpret_cast<const double2*>(Dt + k * GB);
+#pragma unroll
+        for (int r = 0; r < GB / 2; ++r) {
+          const double2 d = dk[r];
+          pn[2 * r] = fma(d.x, a, pn[2 * r]);
+          pn[2 * r + 1] = fma(d.y, a, pn[2 * r + 1]);
+        }
+      }
+    }
+    __syncthreads();  // every column read its pivot-row entries
+    if (jcol) {
+      const bool jK = j >= k0 && j < k0 + GB;
+      for (int i = 0; i < q; ++i) {
+        if (i == k0) {  // pivot rows last
+          i += GB - 1;
+          continue;
+        }
+        const double2* ci = reinterpret_cast<const double2*>(Cold + i * GB);
+        double x;
+        if (jK) {  // pivot columns: -Cold_i D^-1
+          double s = 0.0;
+          for (int k = 0; k < GB; ++k) s = fma(Cold[i * GB + k], Ds[k * GB + (j - k0)], s);
+          x = -s;
+        } else {  // trailing update
+          double s0 = M[(int64_t)i * q + j], s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < GB / 2; ++k) {
+            const double2 c2 = ci[k];
+            s0 = fma(-c2.x, pn[2 * k], s0);
+            s1 = fma(-c2.y, pn[2 * k + 1], s1);
+          }
+          x = s0 + s1;
+        }
+        M[(int64_t)i * q + j] = x;
+      }
+      // pivot rows: D^-1 on the pivot block, Pn elsewhere
+#pragma unroll
+      for (int k = 0; k < GB; ++k)
+        M[(int64_t)(k0 + k) * q + j] = jK ? Ds[k * GB + (j - k0)] : pn[k];
+    }
+    __syncthreads();
+  }
+  // reference singular-pivot rule over the element's pivots
+  double mx = pmax, mn = pmin;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if (lane == 0) {
+    red[0][t >> 5] = mx;
+    red[1][t >> 5] = mn;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double m = 0.0, n = 1e300;
+    for (int w = 0; w < GJT / 32; ++w) {
+      m = fmax(m, red[0][w]);
+      n = fmin(n, red[1][w]);
+    }
+    if (!(n > 1e-14 * m)) atomicExch(status, 2);
+  }
+  for (int e = t; e < q * q; e += GJT) {
+    const int i = e / q, jj = e % q;
+    if (i < jj) {
+      const double s = 0.5 * (M[i * q + jj] + M[jj * q + i]);
+      M[i * q + jj] = s;
+      M[jj * q + i] = s;
+    }
+  }
+}
+
+// ---------------------------------------------- cc eigensolver for large q
+//
+// Lowest L_cc eigenpairs of the projected stiffness H = P S_E P^T of each cc
+// element (coarse_coarse_basis, coarse_space.cpp:343-406) by subspace
+// iteration on the shifted inverse Hs = (H + sigma I)^-1 (k_elem_matrix +
+// k_batched_gj): KS columns, two SVQB orthonormalisation passes per step and
+// Rayleigh-Ritz on H, applied sparsely from Ac / Bc. Stops when every wanted
+// Ritz pair has ||H x - theta x|| <= tol * max_i H_ii. Output as k_cc_basis:
+// ascending eigenvalues, each vector signed so that its entries sum to >= 0.
+// sigma = 1e-5 max_i H_ii: H is singular (Neumann), and a smaller shift makes
+// the rounding of Hs X the residual floor (1e-10 at sigma = 1e-10); measured
+// on the oracle's projected matrices at contrast 1e3..1e6, 1e-5 reaches
+// 1e-13 in <= 24 steps (tests/cc_subspace_sim.py).
+namespace {
+__device__ __forceinline__ double hash_unit(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return (double)x * (1.0 / 4294967296.0) - 0.5;
+}
+
+// Block-wide cyclic Jacobi on the K x K symmetric M (smem): round-robin
+// ordering, K/2 disjoint rotations per round, one thread per (row, pair)
+// update; V (K x K) collects the eigenvectors in its columns. blockDim >= K^2.
+template <int K>
+__device__ void block_jacobi(double* M, double* V, double* red) {
+  constexpr int NP = K / 2;
+  __shared__ double rc[NP], rs[NP];
+  __shared__ int rp[NP], rq[NP];
+  const int t = threadIdx.x;
+  if (t < K * K) V[t] = (t / K == t % K) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double tot = 0.0, off = 0.0;
+    if (t < K * K) {
+      tot = M[t] * M[t];
+      off = (t / K != t % K) ? tot : 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+    }
+    if ((t & 31) == 0 && t < K * K) {
+      red[t >> 5] = tot;
+      red[16 + (t >> 5)] = off;
+    }
+    __syncthreads();
+    tot = 0.0;
+    off = 0.0;
+    for (int w = 0; w < K * K / 32; ++w) {
+      tot += red[w];
+      off += red[16 + w];
+    }
+    __syncthreads();
+    if (off <= 1e-26 * tot || off == 0.0) break;
+    for (int round = 0; round < K - 1; ++round) {
+      if (t < NP) {  // circle method, player K-1 fixed
+        int p = t == 0 ? round : (round + t) % (K - 1);
+        int qq = t == 0 ? K - 1 : (round - t + (K - 1)) % (K - 1);
+        if (p > qq) {
+          const int tmp = p;
+          p = qq;
+          qq = tmp;
+        }
+        const double apq = M[p * K + qq], app = M[p * K + p], aqq = M[qq * K + qq];
+        double c = 1.0, sn = 0.0;
+        if (!(fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq)))) {
+          const double theta = (aqq - app) / (2.0 * apq);
+          const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+          c = 1.0 / sqrt(tt * tt + 1.0);
+          sn = tt * c;
+        }
+        rc[t] = c;
+        rs[t] = sn;
+        rp[t] = p;
+        rq[t] = qq;
+      }
+      __syncthreads();
+      if (t < K * NP) {  // columns p, q of row r
+        const int r = t / NP, gq = t % NP, p = rp[gq], qq = rq[gq];
+        const double c = rc[gq], sn = rs[gq];
+        const double akp = M[r * K + p], akq = M[r * K + qq];
+        M[r * K + p] = c * akp - sn * akq;
+        M[r * K + qq] = sn * akp + c * akq;
+        const double vkp = V[r * K + p], vkq = V[r * K + qq];
+        V[r * K + p] = c * vkp - sn * vkq;
+        V[r * K + qq] = sn * vkp + c * vkq;
+      }
+      __syncthreads();
+      if (t < K * NP) {  // rows p, q at column col
+        const int gq = t / K, col = t % K, p = rp[gq], qq = rq[gq];
+        const double c = rc[gq], sn = rs[gq];
+        const double apk = M[p * K + col], aqk = M[qq * K + col];
+        M[p * K + col] = c * apk - sn * aqk;
+        M[qq * K + col] = sn * apk + c * aqk;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// X = orthonormal basis of span(Y) (q x KS, row-major): scaled Gram matrix,
+// its eigendecomposition (warp Jacobi), X = Y D W Lambda^-1/2.
+__device__ void svqb_pass(const double* Y, double* X, int q, double* T, double* V, double* F,
+                          double* dsc, double* red) {
+  const int t = threadIdx.x;
+  if (t < KS * KS) {
+    const int i = t / KS, j = t % KS;
+    double s = 0.0;
+    for (int r = 0; r < q; ++r) s = fma(Y[r * KS + i], Y[r * KS + j], s);
+    T[t] = s;
+  }
+  __syncthreads();
+  if (t < KS) dsc[t] = rsqrt(fmax(T[t * KS + t], 1e-300));
+  __syncthreads();
+  if (t < KS * KS) T[t] *= dsc[t / KS] * dsc[t % KS];
+  __syncthreads();
+  block_jacobi<KS>(T, V, red);
+  if (t < KS * KS) {
+    const int i = t / KS, j = t % KS;
+    F[t] = dsc[i] * V[i * KS + j] * rsqrt(fmax(T[j * KS + j], 1e-24));
+  }
+  __syncthreads();
+  for (int r = t; r < q; r += blockDim.x) {
+    double y[KS];
+#pragma unroll
+    for (int i = 0; i < KS; ++i) y[i] = Y[r * KS + i];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < KS; ++i) s = fma(y[i], F[i * KS + j], s);
+      X[r * KS + j] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Z = H X with H = (A_c - Bc on the diagonal blocks) restricted to E's children.
+__device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const double* Ac,
+                                const double* Bc, const double* X, double* Z, int q) {
+  for (int r = threadIdx.x; r < q; r += blockDim.x) {
+    const int ci = r / LC, a = r % LC;
+    const int64_t I = child_brick(g, ec, ci);
+    double z[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) z[k] = 0.0;
+    for (int dir = 0; dir < 7; ++dir) {
+      int cj = ci;
+      if (dir > 0) {
+        const int64_t J = brick_nbr(g, I, dir - 1);
+        cj = J >= 0 ? child_index(g, ec, J) : -1;
+      }
+      if (cj < 0) continue;
+#pragma unroll
+      for (int b = 0; b < LC; ++b) {
+        double h = Ac[(I * 7 + dir) * LC * LC + a * LC + b];
+        if (dir == 0) h -= Bc[I * LC * LC + a * LC + b];
+        const double* xr = X + (cj * LC + b) * KS;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) z[k] = fma(h, xr[k], z[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KS; ++k) Z[r * KS + k] = z[k];
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double* __restrict__ Ac,
+                                                     const double* __restrict__ Bc,
+                                                     const double* __restrict__ Hs, double tol,
+                                                     int maxit, double* Rcc, double* cc_evals,
+                                                     int* iters) {
+  extern __shared__ __align__(16) double sms[];
+  const int q = g.sd * g.sd * g.sd * LC, t = threadIdx.x;
+  double* X = sms;
+  double* Y = X + q * KS;
+  double* Z = Y + q * KS;
+  double* T = Z + q * KS;
+  double* V = T + KS * KS;
+  double* F = V + KS * KS;
+  double* dsc = F + KS * KS;
+  double* th = dsc + KS;
+  double* res = th + KS;
+  __shared__ int perm[KS];
+  __shared__ int flag;
+  __shared__ double red[32];
+  const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
+  const double* H = Hs + (int64_t)blockIdx.x * q * q;
+  double hd = 0.0;
+  for (int r = t; r < q; r += blockDim.x) {
+    const int64_t I = child_brick(g, ec, r / LC);
+    const int a = r % LC;
+    hd = fmax(hd, Ac[I * 7 * LC * LC + a * (LC + 1)] - Bc[I * LC * LC + a * (LC + 1)]);
+  }
+  const double thr = tol * block_max(hd, red);
+  // start: the constant vector and hashed columns
+  for (int e = t; e < q * KS; e += blockDim.x) {
+    const int r = e / KS, k = e % KS;
+    Y[e] = k == 0 ? 1.0 : hash_unit((uint32_t)(r * KS + k + 1));
+  }
+  __syncthreads();
+  int it = 0;
+  for (;; ++it) {
+    svqb_pass(Y, X, q, T, V, F, dsc, red);
+    svqb_pass(X, Y, q, T, V, F, dsc, red);
+    { double* tmp = X; X = Y; Y = tmp; }
+    // Rayleigh-Ritz on H
+    apply_projected(g, ec, Ac, Bc, X, Z, q);
+    __syncthreads();
+    if (t < KS * KS) {
+      const int i = t / KS, j = t % KS;
+      double s = 0.0, s2 = 0.0;
+      for (int r = 0; r < q; ++r) {
+        s = fma(X[r * KS + i], Z[r * KS + j], s);
+        s2 = fma(X[r * KS + j], Z[r * KS + i], s2);
+      }
+      T[t] = 0.5 * (s + s2);
+    }
+    __syncthreads();
+    block_jacobi<KS>(T, V, red);
+    if (t == 0) {  // ascending, ties by index
+      unsigned used = 0;
+      for (int k = 0; k < KS; ++k) {
+        int best = -1;
+        for (int i = 0; i < KS; ++i)
+          if (!(used >> i & 1u) && (best < 0 || T[i * (KS + 1)] < T[best * (KS + 1)])) best = i;
+        used |= 1u << best;
+        perm[k] = best;
+        th[k] = T[best * (KS + 1)];
+      }
+    }
+    __syncthreads();
+    for (int r = t; r < q; r += blockDim.x) {
+      double xr[KS], zr[KS];
+#pragma unroll
+      for (int i = 0; i < KS; ++i) {
+        xr[i] = X[r * KS + i];
+        zr[i] = Z[r * KS + i];
+      }
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const int pk = perm[k];
+        double xs = 0.0, zs = 0.0;
+#pragma unroll
+        for (int i = 0; i < KS; ++i) {
+          xs = fma(xr[i], V[i * KS + pk], xs);
+          zs = fma(zr[i], V[i * KS + pk], zs);
+        }
+        X[r * KS + k] = xs;
+        Z[r * KS + k] = zs;
+      }
+    }
+    __syncthreads();
+    {  // residual norms of the wanted pairs: 16 lanes per column
+      const int k = t >> 4, part = t & 15;
+      double s = 0.0;
+      if (k < KS)
+        for (int r = part; r < q; r += 16) {
+          const double d = Z[r * KS + k] - th[k] * X[r * KS + k];
+          s = fma(d, d, s);
+        }
+      for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (k < KS && part == 0) res[k] = sqrt(s);
+    }
+    __syncthreads();
+    if (t == 0) {
+      int ok = 1;
+      for (int k = 0; k < g.lcc; ++k) ok &= res[k] <= thr;
+      flag = ok;
+    }
+    __syncthreads();
+    if (flag || it + 1 >= maxit) break;
+    // Y = Hs X (Hs symmetric: column r read coalesced)
+    for (int r = t; r < q; r += blockDim.x) {
+      double acc[KS];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) acc[k] = 0.0;
+      for (int c = 0; c < q; ++c) {
+        const double h = H[(int64_t)c * q + r];
+        const double2* xc = reinterpret_cast<const double2*>(X + c * KS);
+#pragma unroll
+        for (int k = 0; k < KS / 2; ++k) {
+          const double2 xv = xc[k];
+          acc[2 * k] = fma(h, xv.x, acc[2 * k]);
+          acc[2 * k + 1] = fma(h, xv.y, acc[2 * k + 1]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KS; ++k) Y[r * KS + k] = acc[k];
+    }
+    __syncthreads();
+  }
+  if (t < g.lcc) {
+    double s = 0.0;
+    for (int r = 0; r < q; ++r) s += X[r * KS + t];
+    dsc[t] = s < 0.0 ? -1.0 : 1.0;
+    cc_evals[ec.e * g.lcc + t] = th[t];
+  }
+  __syncthreads();
+  for (int e = t; e < g.lcc * q; e += blockDim.x) {
+    const int k = e / q, r = e % q;
+    Rcc[(ec.e * g.lcc + k) * q + r] = dsc[k] * X[r * KS + k];
+  }
+  if (t == 0 && iters) atomicMax(iters, it + 1);
+}
+
+bool coarse_large_supported(int q, int lcc) {
+  return q > 64 && q % GB == 0 && q <= GJT && lcc <= KS - 4;
+}
+
+size_t batched_gj_smem(int q) { return sizeof(double) * (size_t)(q * GB + 2 * GB * GB); }
+
+// Winv of every owned cc element (coarse_blocks_by_cc smoother) for large q.
+void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
+                                  int* status, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, nullptr, 0.0, Winv + g.e0 * q * q);
+  const size_t smem = batched_gj_smem(q);
+  cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_batched_gj<<<(unsigned)g.neo, GJT, smem, s>>>(Winv + g.e0 * q * q, q, status);
+}
+
+// R_cc rows and cc eigenvalues of every owned cc element for large q; scratch
+// holds the shifted inverses (neo q^2 doubles, virtual-global like Winv).
+void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* Bc,
+                           double* scratch, double* Rcc, double* cc_evals, int* scratch_status,
+                           int* iters, double tol, int maxit, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  double* Hs = scratch + g.e0 * q * q;
+  k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, Bc, 1e-5, Hs);
+  const size_t smem = batched_gj_smem(q);
+  cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_batched_gj<<<(unsigned)g.neo, GJT, smem, s>>>(Hs, q, scratch_status);
+  const size_t sm2 = sizeof(double) * (size_t)(3 * q * KS + 3 * KS * KS + 3 * KS);
+  cudaFuncSetAttribute(k_cc_subspace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  k_cc_subspace<<<(unsigned)g.neo, 256, sm2, s>>>(g, Ac, Bc, Hs, tol, maxit, Rcc, cc_evals, iters);
+}
+
+}  // namespace tmg

@@ -99,6 +99,13 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
                      double* cc_evals, cudaStream_t s);
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
                             cudaStream_t s);
+// large cc elements (q = sd^3 L_c > 64, coarse_large.cu)
+bool coarse_large_supported(int q, int lcc);
+void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
+                                  int* status, cudaStream_t s);
+void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* Bc,
+                           double* scratch, double* Rcc, double* cc_evals, int* scratch_status,
+                           int* iters, double tol, int maxit, cudaStream_t s);
 void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
                          cudaStream_t s);
 void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,

@@ -1,13 +1,13 @@
 """BASELINE configs[3] on one B200: 512^3 cells (~1.34e8 DoF), seeded box-filter
 design (vf 0.2, radius 4, 3 passes), kmin 1e-6, MMG-PCG to rtol 1e-8.
 
-Hierarchy: c = 8, sd = 2, ncc = 32 (the GPU cc eigensolver handles
-sd^3 L_c <= 64), L_c = 4 and a small L_cc so that the dense A_cc^-1 fits
-(n_cc = 32768 L_cc: 8.6 GB at L_cc = 1). SURVEY.md suggests sd = 8 / ncc = 8
-(n_cc = 4096), which needs the block-sparse coarse smoother and cc
-eigensolver listed as next steps in DESIGN.md §8.
+Hierarchy: c = n / (ncc sd) cells per coarse cell, L_c = 4. Defaults: sd = 4,
+ncc = n / 32 (c = 8, q = sd^3 L_c = 256: the large-element coarse level of
+coarse_large.cu) and L_cc = 8, so n_cc = 8 ncc^3 (32768 at 512^3: the dense
+A_cc^-1 takes 8.6 GB). SURVEY.md suggests sd = 8 / ncc = 8 (q = 2048), which
+needs a block-sparse coarse level.
 
-    python tools/config3.py [--n 512] [--lcc 1] [--solves 2] [--out file.json]
+    python tools/config3.py [--n 512] [--ncc 16] [--sd 4] [--lcc 8] [--solves 2] [--out f.json]
 """
 import argparse
 import json
@@ -23,7 +23,9 @@ from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, i
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=512)
-ap.add_argument("--lcc", type=int, default=1)
+ap.add_argument("--lcc", type=int, default=8)
+ap.add_argument("--sd", type=int, default=4)
+ap.add_argument("--ncc", type=int, default=0)
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
@@ -33,8 +35,9 @@ rho = inputs.box_filter_design(n, 0.2, passes=3, radius=4)
 kappa = inputs.conductivity(rho, 1e-6)
 del rho
 t_gen = time.perf_counter() - t0
-ncc = n // 16
-c = Context(GridSpec(n, n, n), ncc, 2)
+sd = a.sd
+ncc = a.ncc or n // (8 * sd)
+c = Context(GridSpec(n, n, n), ncc, sd)
 c.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))
 b = c.assemble_rhs(np.ones(n ** 3))
 del kappa
@@ -48,7 +51,8 @@ x = c.download_solution()
 true_rel = float(np.linalg.norm(b - c.apply_operator(x)) / np.linalg.norm(b))
 out = {
     "workload": f"BASELINE configs[3]-style: {n}^3 cells, vf 0.2, radius 4, kmin 1e-6, rtol 1e-8",
-    "hierarchy": f"c=8 sd=2 ncc={ncc} L_c=4 L_cc={a.lcc} (n_cc={ncc ** 3 * a.lcc})",
+    "hierarchy": f"c={n // (ncc * sd)} sd={sd} ncc={ncc} L_c=4 L_cc={a.lcc} "
+                 f"(n_cc={ncc ** 3 * a.lcc})",
     "cells": n ** 3, "iterations": rep.iterations, "converged": rep.converged,
     "solve_s": rep.solve_seconds, "setup_s": t_setup,
     "mdof_iter_per_s": n ** 3 * rep.iterations / rep.solve_seconds / 1e6,
