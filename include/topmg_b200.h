@@ -33,8 +33,8 @@ extern "C" {
 /* PrecondKind (solver.hpp:160). */
 #define TMG_PRECOND_NONE 0
 #define TMG_PRECOND_JACOBI 1
-#define TMG_PRECOND_BLOCK_JACOBI 2 /* not built on GPU: returns TMG_ENOTSUP */
-#define TMG_PRECOND_TWO_GRID 3     /* not built on GPU yet: TMG_ENOTSUP     */
+#define TMG_PRECOND_BLOCK_JACOBI 2 /* cc-element blocks of 8^3 / 16^3 cells */
+#define TMG_PRECOND_TWO_GRID 3     /* R_cc = I; sd^3 L_c <= 32              */
 #define TMG_PRECOND_MMG 4
 
 /* Faces, topmg::Face (grid.hpp:57). */
@@ -73,7 +73,14 @@ typedef struct {
   int eig_max_outer;   /* filter/Rayleigh-Ritz rounds, 0 -> 60 */
   int warm_start;      /* 1: start the local eigensolver from the previous set-up's
                           bases (same context; a design iteration's re-set-up) */
+  int fine_blocks;     /* fine smoother partition (mmg, two_grid):
+                          TMG_FINE_BLOCKS_COARSE_CELL (GPU default) or
+                          TMG_FINE_BLOCKS_CC (build_mmg's fine_blocks_by_cc,
+                          solver.cpp:353-361; cc elements of 8^3 / 16^3 cells) */
 } tmg_mmg_options;
+
+#define TMG_FINE_BLOCKS_COARSE_CELL 0
+#define TMG_FINE_BLOCKS_CC 1
 
 /* SolveReport (solver.hpp:15-22). */
 typedef struct {

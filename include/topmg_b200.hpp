@@ -37,12 +37,15 @@ inline void check(int rc, const tmg_ctx* c) {
 // A GPU-resident operator + preconditioner for one assembled system.
 class GpuMmgPreconditioner final : public topmg::Preconditioner {
  public:
-  // make_preconditioner (solver.cpp:462-481) for kinds None / Jacobi / Mmg.
-  // The operator is rebuilt matrix-free from system.kappa and system.boundary
-  // (fvm.hpp:20-26); system.matrix is not copied to the device.
+  // make_preconditioner (solver.cpp:462-481) for all five kinds. The operator
+  // is rebuilt matrix-free from system.kappa and system.boundary
+  // (fvm.hpp:20-26); system.matrix is not copied to the device. fine_blocks
+  // selects the Mmg / TwoGrid fine smoother partition: TMG_FINE_BLOCKS_CC is
+  // the reference's own (fine_blocks_by_cc, cc elements of 8^3 / 16^3 cells),
+  // TMG_FINE_BLOCKS_COARSE_CELL the GPU default.
   GpuMmgPreconditioner(topmg::PrecondKind kind, const topmg::AssembledSystem& system,
                        const topmg::HierarchicalGrid& hgrid, const topmg::MmgOptions& opts = {},
-                       int device = 0)
+                       int device = 0, int fine_blocks = TMG_FINE_BLOCKS_COARSE_CELL)
       : kind_(kind), n_(system.grid.num_cells()) {
     tmg_grid g{};
     g.nx = system.grid.nx;
@@ -69,6 +72,7 @@ class GpuMmgPreconditioner final : public topmg::Preconditioner {
     o.num_local_basis = opts.num_local_basis;
     o.num_cc_basis = opts.num_cc_basis;
     o.smoother_sweeps = opts.smoother_sweeps;
+    o.fine_blocks = fine_blocks;
     check(tmg_setup(ctx_.get(), &o), ctx_.get());
   }
 
@@ -94,8 +98,9 @@ class GpuMmgPreconditioner final : public topmg::Preconditioner {
 
 inline std::unique_ptr<topmg::Preconditioner> make_preconditioner(
     topmg::PrecondKind kind, const topmg::AssembledSystem& system,
-    const topmg::HierarchicalGrid& hgrid, const topmg::MmgOptions& opts = {}, int device = 0) {
-  return std::make_unique<GpuMmgPreconditioner>(kind, system, hgrid, opts, device);
+    const topmg::HierarchicalGrid& hgrid, const topmg::MmgOptions& opts = {}, int device = 0,
+    int fine_blocks = TMG_FINE_BLOCKS_COARSE_CELL) {
+  return std::make_unique<GpuMmgPreconditioner>(kind, system, hgrid, opts, device, fine_blocks);
 }
 
 // topmg::pcg (solver.cpp:483-575) with the whole iteration on the device. `a`

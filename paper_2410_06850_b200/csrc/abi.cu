@@ -88,6 +88,8 @@ struct Slab {
   double* Rcc = nullptr;
   double* cc_evals = nullptr;
   double* Winv = nullptr;
+  double* Gbj = nullptr;  // block-Jacobi plane Schur inverses (virtual-global per element)
+  double *r2 = nullptr, *t2 = nullptr;  // cc-block-smoothed V-cycle: r1 + R_c^T e_c, r - A r2
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
          *r1 = nullptr, *stage = nullptr;
@@ -106,6 +108,7 @@ struct tmg_ctx {
   tmg_grid grid{};
   GridParams g{};  // global grid (b0 = 0, nbo = nb, ...)
   int cb = 0;
+  int fine_bj = 0;  // fine smoother blocks = cc elements (tmg_mmg_options.fine_blocks)
   int64_t M = 0;   // global cells
   std::string err;
   // partition
@@ -265,6 +268,9 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.Rcc);
     dfree_null(c, s.cc_evals);
     dfree_null(c, s.Winv);
+    dfree_null(c, s.Gbj);
+    dfree_null(c, s.r2);
+    dfree_null(c, s.t2);
     dfree_null(c, s.rc);
     dfree_null(c, s.rc0);
     dfree_null(c, s.ec);
@@ -484,20 +490,10 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
                     st));
 }
 
-// partitioned: the same kernels per slab, ghost exchanges and cross-slab
-// reductions between them (SURVEY.md §8(e) "collectives per PCG iteration")
-void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
+// partitioned coarse + coarse-coarse levels (solver.cpp:292-319): rc -> ec
+void enqueue_coarse_dist(tmg_ctx* c) {
   cudaStream_t st = c->stream;
-  const int64_t C = cells_per_brick(c);
   const size_t cvec = sizeof(double) * (size_t)c->lc;
-  for (Slab& s : c->slabs)
-    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.st,
-                        s.partials, s.history, init, st));
-  if (!init) reduce_finalize(c, kRedUpdate, 0);
-  XCH(r1, sizeof(double) * C, false);
-  for (Slab& s : c->slabs)
-    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
-  // coarse level (solver.cpp:292-319)
   for (Slab& s : c->slabs)
     KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.rc, nullptr, s.rc0, st));
   XCH(rc0, cvec, false);
@@ -519,6 +515,21 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   for (Slab& s : c->slabs)
     KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.tc, s.rc1, s.ec, st));
   XCH(ec, cvec, false);
+}
+
+// partitioned: the same kernels per slab, ghost exchanges and cross-slab
+// reductions between them (SURVEY.md §8(e) "collectives per PCG iteration")
+void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
+  cudaStream_t st = c->stream;
+  const int64_t C = cells_per_brick(c);
+  for (Slab& s : c->slabs)
+    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.st,
+                        s.partials, s.history, init, st));
+  if (!init) reduce_finalize(c, kRedUpdate, 0);
+  XCH(r1, sizeof(double) * C, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
     KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
                       init, st));
@@ -526,27 +537,88 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   XCH(z, sizeof(double) * C, false);
 }
 
+// block_jacobi (BlockJacobiPreconditioner, solver.cpp:444-458): x, r update
+// and the stopping test, then z = A_BB^-1 r per cc element and r.z
+void enqueue_block_jacobi(tmg_ctx* c, int init, int par_new) {
+  const int64_t C = cells_per_brick(c);
+  if (!init) {
+    for (Slab& s : c->slabs)
+      KL(1, launch_jacobi_step(s.g, c->cb, nullptr, s.x, s.pbuf[par_new], s.q, s.r, s.z, s.st,
+                               s.partials, s.history, 0, 1, c->stream));
+    if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
+  }
+  const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+  for (Slab& s : c->slabs)
+    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r, s.st,
+                          s.partials, init, c->stream));
+  if (c->dist()) {
+    reduce_finalize(c, kRedPost, init);
+    XCH(z, sizeof(double) * C, false);
+  }
+}
+
 void enqueue_jacobi(tmg_ctx* c, int init, int par_new) {
+  if (c->kind == TMG_PRECOND_BLOCK_JACOBI) return enqueue_block_jacobi(c, init, par_new);
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
     KL(1, launch_jacobi_step(s.g, c->cb, c->kind == TMG_PRECOND_JACOBI ? s.dinv : nullptr, s.x,
                              s.pbuf[par_new], s.q, s.r, s.z, s.st, s.partials, s.history, init,
-                             c->stream));
+                             0, c->stream));
   if (c->dist()) {
     reduce_finalize(c, kRedJacobi, init);
     XCH(z, sizeof(double) * C, false);
   }
 }
 
-// first application (x0 residual already in r): z = M^-1 r, rho = r.z
-void enqueue_precond_init(tmg_ctx* c) {
-  if (c->kind == TMG_PRECOND_MMG) {
-    if (c->dist()) enqueue_vcycle_dist(c, 1, 0);
-    else enqueue_vcycle_single(c, 1, c->slabs[0].pbuf[0]);
-  } else {
-    enqueue_jacobi(c, 1, 0);
+// V-cycle with the reference build_mmg fine blocks (one per cc element,
+// tmg_mmg_options.fine_blocks = TMG_FINE_BLOCKS_CC), solver.cpp:272-334:
+//   r1 = B^-1 r; rc = R_c (r - A r1); coarse levels; r2 = r1 + R_c^T ec;
+//   z = r2 + B^-1 (r - A r2); r.z
+void enqueue_vcycle_bj(tmg_ctx* c, int init, int par_new) {
+  const int64_t C = cells_per_brick(c);
+  cudaStream_t st = c->stream;
+  if (!init) {
+    for (Slab& s : c->slabs)
+      KL(1, launch_jacobi_step(s.g, c->cb, nullptr, s.x, s.pbuf[par_new], s.q, s.r, s.z, s.st,
+                               s.partials, s.history, 0, 1, st));
+    if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
+  }
+  const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+  for (Slab& s : c->slabs)
+    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.r1, nullptr,
+                          s.st, s.partials, init, st));
+  if (c->dist()) XCH(r1, sizeof(double) * C, false);
+  for (Slab& s : c->slabs)
+    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  if (c->dist()) enqueue_coarse_dist(c);
+  else enqueue_coarse_single(c);
+  for (Slab& s : c->slabs)
+    KL(1, launch_prolong_add(s.g, c->cb, s.phi, s.r1, s.ec, s.r2, s.st, st));
+  if (c->dist()) XCH(r2, sizeof(double) * C, false);
+  for (Slab& s : c->slabs) KL(1, launch_resid(s.g, c->cb, s.coef, s.r, s.r2, s.t2, s.st, st));
+  for (Slab& s : c->slabs)
+    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.t2, s.r2, s.z, s.r, s.st,
+                          s.partials, init, st));
+  if (c->dist()) {
+    reduce_finalize(c, kRedPost, init);
+    XCH(z, sizeof(double) * C, false);
   }
 }
+
+bool hierarchical(const tmg_ctx* c) {
+  return c->kind == TMG_PRECOND_MMG || c->kind == TMG_PRECOND_TWO_GRID;
+}
+
+// z = M^-1 r and r.z for the current preconditioner (init: first application,
+// x0 residual already in r); otherwise after the search step of an iteration.
+void enqueue_precond(tmg_ctx* c, int init, int par_new) {
+  if (!hierarchical(c)) return enqueue_jacobi(c, init, par_new);
+  if (c->fine_bj) enqueue_vcycle_bj(c, init, par_new);
+  else if (c->dist()) enqueue_vcycle_dist(c, init, par_new);
+  else enqueue_vcycle_single(c, init, c->slabs[0].pbuf[par_new]);
+}
+
+void enqueue_precond_init(tmg_ctx* c) { enqueue_precond(c, 1, 0); }
 
 // Iteration with parity `par`: reads p from pbuf[par], writes pbuf[par ^ 1].
 void enqueue_iteration(tmg_ctx* c, int par) {
@@ -558,12 +630,7 @@ void enqueue_iteration(tmg_ctx* c, int par) {
     reduce_finalize(c, kRedSearch, 0);
     exchange(c, [&](Slab& s) { return (void*)s.pbuf[par ^ 1]; }, sizeof(double) * C, false);
   }
-  if (c->kind == TMG_PRECOND_MMG) {
-    if (c->dist()) enqueue_vcycle_dist(c, 0, par ^ 1);
-    else enqueue_vcycle_single(c, 0, c->slabs[0].pbuf[par ^ 1]);
-  } else {
-    enqueue_jacobi(c, 0, par ^ 1);
-  }
+  enqueue_precond(c, 0, par ^ 1);
 }
 
 void build_graph(tmg_ctx* c, int chunk) {
@@ -648,7 +715,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   });
   if (!prof) {
     enqueue_precond_init(c);
-  } else if (c->kind == TMG_PRECOND_MMG) {
+  } else if (hierarchical(c) && !c->fine_bj) {
     Slab& s = s0;
     const GridParams& g = s.g;
     timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
@@ -656,7 +723,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     timed(3, [&] { enqueue_coarse_single(c); });
     timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
-    timed(7, [&] { enqueue_jacobi(c, 1, 0); });
+    timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
   CK(cudaGetLastError());
   c->launches += c->kcount - k_before;
@@ -701,13 +768,13 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       par ^= 1;
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
-      if (c->kind == TMG_PRECOND_MMG) {
+      if (hierarchical(c) && !c->fine_bj) {
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
         timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
-        timed(7, [&] { enqueue_jacobi(c, 0, par); });
+        timed(7, [&] { enqueue_precond(c, 0, par); });
       }
       c->launches += c->kcount - kb;
       CK(cudaMemcpy(&hs[0], s.st, sizeof(PcgState), cudaMemcpyDeviceToHost));
@@ -1287,10 +1354,16 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
   if (!c || !o) return set_err(c, TMG_EARG, "tmg_setup: null argument");
   if (!c->have_problem) return set_err(c, TMG_EARG, "tmg_setup: no problem set");
   const int kind = o->kind;
-  if (kind == TMG_PRECOND_BLOCK_JACOBI || kind == TMG_PRECOND_TWO_GRID)
-    return set_err(c, TMG_ENOTSUP, "preconditioner kind %d is not built on the GPU path", kind);
+  const bool hier = kind == TMG_PRECOND_MMG || kind == TMG_PRECOND_TWO_GRID;
+  const bool fine_bj = hier && o->fine_blocks == TMG_FINE_BLOCKS_CC;
+  if (hier && o->fine_blocks != TMG_FINE_BLOCKS_COARSE_CELL && !fine_bj)
+    return set_err(c, TMG_EARG, "fine_blocks must be TMG_FINE_BLOCKS_COARSE_CELL or _CC");
+  if ((kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj) && !bj_supported((int)c->cb, c->g.sd))
+    return set_err(c, TMG_ENOTSUP,
+                   "GPU block_jacobi handles cc elements of 8^3 or 16^3 cells (got %lld^3)",
+                   (long long)(c->cb * c->g.sd));
   if (kind < 0 || kind > 4) return set_err(c, TMG_ECONFIG, "make_preconditioner: unknown kind");
-  if (kind == TMG_PRECOND_MMG) {
+  if (hier) {
     const int64_t cells = (int64_t)c->cb * c->cb * c->cb;
     if (o->num_local_basis > cells)
       return set_err(c, TMG_EARG, "local_spectral_basis: more eigenvectors than cells requested");
@@ -1298,11 +1371,15 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       return set_err(c, TMG_ENOTSUP, "GPU path is compiled for L_c = %d (got %lld)", compiled_lc(),
                      (long long)o->num_local_basis);
     const int64_t q = (int64_t)c->g.sd * c->g.sd * c->g.sd * o->num_local_basis;
-    if (o->num_cc_basis > q)
+    if (kind == TMG_PRECOND_TWO_GRID && q > 32)
+      return set_err(c, TMG_ENOTSUP, "GPU two_grid handles sd^3*L_c <= 32 (got %lld)",
+                     (long long)q);
+    if (kind == TMG_PRECOND_MMG && o->num_cc_basis > q)
       return set_err(c, TMG_EARG,
                      "coarse_coarse_basis: more eigenvectors than coarse basis functions");
-    if (o->num_cc_basis < 1) return set_err(c, TMG_EARG, "num_cc_basis must be >= 1");
-    if (q > 64 && !coarse_large_supported((int)q, (int)o->num_cc_basis))
+    if (kind == TMG_PRECOND_MMG && o->num_cc_basis < 1)
+      return set_err(c, TMG_EARG, "num_cc_basis must be >= 1");
+    if (kind == TMG_PRECOND_MMG && q > 64 && !coarse_large_supported((int)q, (int)o->num_cc_basis))
       return set_err(c, TMG_ENOTSUP,
                      "GPU coarse level handles sd^3*L_c <= 64, or a multiple of 64 up to 256 with "
                      "num_cc_basis <= 12 (got %lld, %lld)",
@@ -1315,7 +1392,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     free_setup(c);  // the current bases (if any) move to phi_keep
     // warm start: the last set-up's bases seed the local eigensolver
     std::vector<double*> phi_prev(c->slabs.size(), nullptr);
-    const bool warm = kind == TMG_PRECOND_MMG && o->warm_start && c->lc_keep == (int)o->num_local_basis;
+    const bool warm = hier && o->warm_start && c->lc_keep == (int)o->num_local_basis;
     for (size_t k = 0; k < c->slabs.size(); ++k) {
       phi_prev[k] = warm ? c->slabs[k].phi_keep : nullptr;
       if (!warm) dfree_null(c, c->slabs[k].phi_keep);
@@ -1333,9 +1410,19 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         launch_apply(s.g, c->cb, s.coef, nullptr, nullptr, s.dinv, c->stream);
         CK(cudaGetLastError());
       }
-    } else if (kind == TMG_PRECOND_MMG) {
+    } else if (kind == TMG_PRECOND_BLOCK_JACOBI) {
+      const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+      for (Slab& s : c->slabs) {
+        s.Gbj = owned_e<double>(c, s, per);
+        launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, c->stream);
+        CK(cudaGetLastError());
+      }
+    } else if (hier) {
       c->lc = (int)o->num_local_basis;
-      c->lcc = (int)o->num_cc_basis;
+      // two_grid: R_cc = I (build_two_grid, solver.cpp:401-420)
+      c->lcc = kind == TMG_PRECOND_TWO_GRID
+                   ? (int)(c->g.sd * c->g.sd * c->g.sd * o->num_local_basis)
+                   : (int)o->num_cc_basis;
       c->g.lc = c->lc;
       c->g.lcc = c->lcc;
       const int64_t q = (int64_t)c->g.sd * c->g.sd * c->g.sd * c->lc;
@@ -1346,7 +1433,13 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         s.phi = ghosted<double>(c, s, lc * C);
         s.evals = owned<double>(c, s, lc);
         s.eig_iters = owned<int>(c, s, 1);
-        s.Gf = owned<double>(c, s, thomas_doubles_per_brick(c->cb));
+        if (fine_bj) {
+          s.Gbj = owned_e<double>(c, s, bj_doubles_per_element(c->cb, c->g.sd));
+          s.r2 = ghosted<double>(c, s, C);
+          s.t2 = ghosted<double>(c, s, C);
+        } else {
+          s.Gf = owned<double>(c, s, thomas_doubles_per_brick(c->cb));
+        }
         s.Ac = owned<double>(c, s, 7 * lc * lc);
         s.Bc = owned<double>(c, s, lc * lc);
         s.Rcc = ghosted_e<double>(c, s, lcc * q);
@@ -1394,7 +1487,8 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         CK(cudaMemsetAsync(cc_iters, 0, sizeof(int), c->stream));
       }
       for (Slab& s : c->slabs) {
-        if (q <= 64) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
+        if (kind == TMG_PRECOND_TWO_GRID) launch_cc_identity(s.g, s.Rcc, s.cc_evals, c->stream);
+        else if (q <= 64) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
         else  // Winv's storage holds the shifted inverses until the smoother overwrites it
           launch_cc_basis_large(s.g, s.Ac, s.Bc, s.Winv, s.Rcc, s.cc_evals, s.d_status + 3,
                                 cc_iters, 1e-12, 100, c->stream);
@@ -1415,8 +1509,14 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       }
       CK(cudaGetLastError());
       mark("coarse_smoother");
-      for (Slab& s : c->slabs)
-        launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.Gf, s.d_status, c->stream);
+      for (Slab& s : c->slabs) {
+        if (fine_bj) {
+          const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+          launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, c->stream);
+        } else {
+          launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.Gf, s.d_status, c->stream);
+        }
+      }
       CK(cudaGetLastError());
       mark("thomas_factor");
       // A_cc: every slab assembles its rows of the one dense matrix
@@ -1480,6 +1580,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       }
     }
     c->kind = kind;
+    c->fine_bj = fine_bj ? 1 : 0;
     c->have_setup = true;
     build_graph(c, 4);
   });
@@ -1578,7 +1679,7 @@ int tmg_get_sizes(tmg_ctx* c, int64_t* s) {
 }
 
 int tmg_get_local_bases(tmg_ctx* c, double* phi, double* evals, int* iters) {
-  if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG)
+  if (!c || !c->have_setup || !hierarchical(c))
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
   if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {
@@ -1596,7 +1697,7 @@ int tmg_get_local_bases(tmg_ctx* c, double* phi, double* evals, int* iters) {
 }
 
 int tmg_get_coarse_operator(tmg_ctx* c, double* ac) {
-  if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG || !ac)
+  if (!c || !c->have_setup || !hierarchical(c) || !ac)
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
   if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {
@@ -1627,7 +1728,7 @@ int tmg_get_coarse_operator(tmg_ctx* c, double* ac) {
 }
 
 int tmg_get_cc_restriction(tmg_ctx* c, double* rcc) {
-  if (!c || !c->have_setup || c->kind != TMG_PRECOND_MMG || !rcc)
+  if (!c || !c->have_setup || !hierarchical(c) || !rcc)
     return set_err(c, TMG_EARG, "no MMG hierarchy set up");
   if (!single(c)) return set_err(c, TMG_ENOTSUP, "hierarchy getters need a single-slab context");
   return guard(c, [&] {

@@ -1,0 +1,244 @@
+// Block-Jacobi with one block per cc element (fine_blocks_by_cc,
+// solver.cpp:353-361): the reference's block_jacobi preconditioner
+// (BlockJacobiPreconditioner, solver.cpp:444-458 -- one BlockJacobiSmoother
+// sweep from zero, z = A_BB^-1 r per block, solver.cpp:221-243).
+//
+// A block is the E^3 cells of a cc element (E = c sd), x-fastest like
+// HierarchicalGrid::cells_of_coarse_coarse. In that order A_BB is block
+// tridiagonal over its E z-planes of P = E^2 cells: A_kk is the plane's 2-D
+// 5-point part with the full diagonal, A_k,k+1 = -D_{k+1} with D_{k+1} the
+// z transmissibilities between planes k and k+1. It is factorised by block
+// Thomas with explicit Schur-complement inverses
+//   G_0 = A_00^-1,  G_k = (A_kk - D_k G_{k-1} D_k)^-1
+// (gj_inverse_global, pivots checked with the reference's rule) and applied as
+//   y_k = G_k (r_k + D_k y_{k-1}),  x_k = y_k + G_k D_{k+1} x_{k+1}.
+// Storage G[e][k][P][P] (symmetric, full): 4.3 GB at 128^3 / c = 8 / sd = 2.
+// Each apply streams it once (two GEMVs per plane): an HBM-bound baseline.
+#include "gj_global.cuh"
+#include "kernels.h"
+#include "pcg_fin.cuh"
+#include "stencil.cuh"
+
+namespace tmg {
+
+namespace {
+// brick-layout offset of element cell (i, j, k)
+__device__ __forceinline__ size_t elem_cell(const GridParams& g, int cb, int64_t e, int i, int j,
+                                            int k) {
+  const int64_t ei = e % g.ncx, ej = (e / g.ncx) % g.ncy, ek = e / (g.ncx * g.ncy);
+  const int64_t b = (ei * g.sd + i / cb) + g.nbx * ((ej * g.sd + j / cb) + g.nby * (ek * g.sd + k / cb));
+  return (size_t)b * (size_t)(cb * cb * cb) + (size_t)((i % cb) + cb * ((j % cb) + cb * (k % cb)));
+}
+}  // namespace
+
+// One CTA (256 threads) per owned cc element; planes in sequence.
+__global__ void __launch_bounds__(kGjThreads, 1) k_bj_factor(GridParams g, int cb, int E,
+                                                             const double* __restrict__ coef,
+                                                             double* G, int* status) {
+  extern __shared__ __align__(16) double smg[];
+  __shared__ GjSmem<kGjBlock> gjs;
+  __shared__ double red[2][kGjThreads / 32];
+  const int P = E * E, t = threadIdx.x, lane = t & 31;
+  const int64_t e = blockIdx.x + g.e0, M = g.mst;
+  double* Ge = G + (size_t)blockIdx.x * E * P * P;
+  const GjGlobalSmem gsm = gj_global_smem(smg, P);
+  double pmin = 1e300, pmax = 0.0;
+  for (int k = 0; k < E; ++k) {
+    double* Gk = Ge + (size_t)k * P * P;
+    const double* Gp = Gk - (size_t)P * P;
+    for (int idx = t; idx < P * P; idx += blockDim.x) {
+      const int a = idx / P, b = idx % P;
+      const int ia = a % E, ja = a / E, ib = b % E, jb = b / E;
+      double v = 0.0;
+      if (a == b) {
+        v = coef[3 * M + elem_cell(g, cb, e, ia, ja, k)];
+      } else if (ja == jb && (ib == ia + 1 || ia == ib + 1)) {
+        v = -coef[elem_cell(g, cb, e, min(ia, ib), ja, k)];
+      } else if (ia == ib && (jb == ja + 1 || ja == jb + 1)) {
+        v = -coef[M + elem_cell(g, cb, e, ia, min(ja, jb), k)];
+      }
+      if (k > 0) {
+        const double da = coef[2 * M + elem_cell(g, cb, e, ia, ja, k - 1)];
+        const double db = coef[2 * M + elem_cell(g, cb, e, ib, jb, k - 1)];
+        v -= da * Gp[idx] * db;
+      }
+      Gk[idx] = v;
+    }
+    __syncthreads();
+    gj_inverse_global(Gk, P, gsm, gjs, pmin, pmax);
+  }
+  double mx = pmax, mn = pmin;
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if (lane == 0) {
+    red[0][t >> 5] = mx;
+    red[1][t >> 5] = mn;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double m = 0.0, n = 1e300;
+    for (int w = 0; w < kGjThreads / 32; ++w) {
+      m = fmax(m, red[0][w]);
+      n = fmin(n, red[1][w]);
+    }
+    if (!(n > 1e-14 * m)) atomicExch(status, 1);  // solver.cpp:86-92 via the smoother
+  }
+}
+
+// out = add + A_BB^-1 in on every owned cc element (add nullable). With rdot
+// (the PCG residual) the product rdot . out is reduced and finishes the
+// iteration like the V-cycle's post kernel (fin_post: rho, beta).
+// One CTA of P threads per element, thread p = plane cell (i, j).
+template <int E>
+__global__ void __launch_bounds__(E * E) k_bj_apply(GridParams g, int cb,
+                                                   const double* __restrict__ coef,
+                                                   const double* __restrict__ G,
+                                                   const double* __restrict__ in,
+                                                   const double* __restrict__ add, double* out,
+                                                   const double* __restrict__ rdot, PcgState* st,
+                                                   double* partials, int init) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  constexpr int P = E * E;
+  __shared__ double y[E][P];
+  __shared__ double v[P];
+  __shared__ double red[80];
+  __shared__ int flag;
+  const int p = threadIdx.x, i = p % E, j = p / E;
+  const int64_t e = blockIdx.x + g.e0, M = g.mst;
+  const double* Ge = G + (size_t)blockIdx.x * E * P * P;
+  auto gemv = [&](const double* Gk) {  // sum_q Gk[q][p] v[q] (Gk symmetric: coalesced)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < P; q += 4) {
+      s0 = fma(Gk[(size_t)q * P + p], v[q], s0);
+      s1 = fma(Gk[(size_t)(q + 1) * P + p], v[q + 1], s1);
+      s2 = fma(Gk[(size_t)(q + 2) * P + p], v[q + 2], s2);
+      s3 = fma(Gk[(size_t)(q + 3) * P + p], v[q + 3], s3);
+    }
+    return (s0 + s1) + (s2 + s3);
+  };
+  double prev = 0.0, rz = 0.0;
+  for (int k = 0; k < E; ++k) {
+    const double dz = k > 0 ? coef[2 * M + elem_cell(g, cb, e, i, j, k - 1)] : 0.0;
+    v[p] = in[elem_cell(g, cb, e, i, j, k)] + dz * prev;
+    __syncthreads();
+    prev = gemv(Ge + (size_t)k * P * P);
+    y[k][p] = prev;
+    __syncthreads();
+  }
+  double xn = y[E - 1][p];
+  auto store = [&](size_t s, double xv) {
+    const double o = add ? add[s] + xv : xv;
+    out[s] = o;
+    if (rdot) rz = fma(rdot[s], o, rz);
+  };
+  store(elem_cell(g, cb, e, i, j, E - 1), xn);
+  for (int k = E - 2; k >= 0; --k) {
+    const size_t s = elem_cell(g, cb, e, i, j, k);
+    v[p] = coef[2 * M + s] * xn;
+    __syncthreads();
+    xn = y[k][p] + gemv(Ge + (size_t)k * P * P);
+    store(s, xn);
+    __syncthreads();
+  }
+  if (!rdot) return;
+  double vv[1] = {rz};
+  block_sum_k<P, 1>(vv, red);
+  double tot[1];
+  if (grid_reduce_last_k<1>(vv, partials, &st->ticket[5], tot, &flag, red) && p == 0) {
+    if (g.dist) st->loc[kRedPost] = tot[0];
+    else fin_post(st, tot[0], init);
+  }
+}
+
+// r2 = r1 + R_c^T ec (solver.cpp:307-309 prolongation, per coarse cell)
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_prolong_add(GridParams g,
+                                                             const double* __restrict__ phi,
+                                                             const double* __restrict__ r1,
+                                                             const double* __restrict__ ec,
+                                                             double* r2, const PcgState* st) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  constexpr int C = CB * CB * CB, LCB = 4;
+  const int64_t b = blockIdx.x + g.b0;
+  const size_t s = (size_t)b * C + threadIdx.x;
+  double v = r1[s];
+#pragma unroll
+  for (int a = 0; a < LCB; ++a) v = fma(phi[((size_t)b * LCB + a) * C + threadIdx.x], ec[b * LCB + a], v);
+  r2[s] = v;
+}
+
+// t = r - A x (the residual before post-smoothing, solver.cpp:327)
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_resid(GridParams g, const double* __restrict__ coef,
+                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ x, double* t,
+                                                       const PcgState* st) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  __shared__ CoefSmem<CB> cs;
+  __shared__ double xt[Tile<CB>::N];
+  constexpr int C = CB * CB * CB;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  load_coefs<CB>(coef, g.mst, cs, g, bc);
+  load_tile<CB, true>(x, xt, g, bc);
+  __syncthreads();
+  const int u = threadIdx.x, li = u % CB, lj = (u / CB) % CB, lk = u / (CB * CB);
+  const size_t s = bofs(bc.b, C) + u;
+  t[s] = r[s] - apply_coef<CB>(cs, xt, li, lj, lk);
+}
+
+bool bj_supported(int cb, int sd) {
+  const int E = cb * sd;
+  return E == 8 || E == 16;
+}
+
+int64_t bj_doubles_per_element(int cb, int sd) {
+  const int64_t E = cb * sd;
+  return E * E * E * E * E;
+}
+
+void launch_bj_factor(const GridParams& g, int cb, const double* coef, double* G, int* status,
+                      cudaStream_t s) {
+  const int E = cb * g.sd, P = E * E;
+  const size_t smem = gj_global_smem_bytes(P);
+  cudaFuncSetAttribute(k_bj_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_bj_factor<<<(unsigned)g.neo, kGjThreads, smem, s>>>(g, cb, E, coef, G, status);
+}
+
+void launch_bj_apply(const GridParams& g, int cb, const double* coef, const double* G,
+                     const double* in, const double* add, double* out, const double* rdot,
+                     PcgState* st, double* partials, int init, cudaStream_t s) {
+  const int E = cb * g.sd;
+  if (E == 16)
+    launch_pdl(k_bj_apply<16>, dim3((unsigned)g.neo), dim3(256), 0, s, g, cb, coef, G, in, add,
+               out, rdot, st, partials, init);
+  else
+    launch_pdl(k_bj_apply<8>, dim3((unsigned)g.neo), dim3(64), 0, s, g, cb, coef, G, in, add, out,
+               rdot, st, partials, init);
+}
+
+void launch_prolong_add(const GridParams& g, int cb, const double* phi, const double* r1,
+                        const double* ec, double* r2, const PcgState* st, cudaStream_t s) {
+  if (cb == 8)
+    launch_pdl(k_prolong_add<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, phi, r1, ec, r2, st);
+  else
+    launch_pdl(k_prolong_add<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, phi, r1, ec, r2, st);
+}
+
+void launch_resid(const GridParams& g, int cb, const double* coef, const double* r,
+                  const double* x, double* t, const PcgState* st, cudaStream_t s) {
+  if (cb == 8)
+    launch_pdl(k_resid<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, coef, r, x, t, st);
+  else
+    launch_pdl(k_resid<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, r, x, t, st);
+}
+
+}  // namespace tmg

@@ -231,27 +231,28 @@ __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
     F = hi ? ec.e + strides[ax] : ec.e - strides[ax];
   }
   const ElemCoord fc = elem_coord(g, F);
-  const int bb = threadIdx.x / g.lcc, bp = threadIdx.x % g.lcc;
-  if (bb >= g.lcc) return;
-  const double* RE = Rcc + (ec.e * g.lcc + bb) * q;
-  const double* RF = Rcc + (F * g.lcc + bp) * q;
-  double acc = 0.0;
-  for (int ci = 0; ci < nch; ++ci) {
-    const int64_t I = child_brick(g, ec, ci);
-    for (int dir = 0; dir < 7; ++dir) {
-      int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
-      if (J < 0) continue;
-      const int cj = child_index(g, fc, J);
-      if (cj < 0) continue;
-      const double* blk = Ac + (I * 7 + dir) * LC * LC;
-      for (int a = 0; a < LC; ++a) {
-        double s = 0.0;
-        for (int b = 0; b < LC; ++b) s += blk[a * LC + b] * RF[cj * LC + b];
-        acc += RE[ci * LC + a] * s;
+  for (int pr = threadIdx.x; pr < g.lcc * g.lcc; pr += blockDim.x) {
+    const int bb = pr / g.lcc, bp = pr % g.lcc;
+    const double* RE = Rcc + (ec.e * g.lcc + bb) * q;
+    const double* RF = Rcc + (F * g.lcc + bp) * q;
+    double acc = 0.0;
+    for (int ci = 0; ci < nch; ++ci) {
+      const int64_t I = child_brick(g, ec, ci);
+      for (int dir = 0; dir < 7; ++dir) {
+        int64_t J = dir == 0 ? I : brick_nbr(g, I, dir - 1);
+        if (J < 0) continue;
+        const int cj = child_index(g, fc, J);
+        if (cj < 0) continue;
+        const double* blk = Ac + (I * 7 + dir) * LC * LC;
+        for (int a = 0; a < LC; ++a) {
+          double s = 0.0;
+          for (int b = 0; b < LC; ++b) s += blk[a * LC + b] * RF[cj * LC + b];
+          acc += RE[ci * LC + a] * s;
+        }
       }
     }
+    Acc[(ec.e * g.lcc + bb) * ldacc + F * g.lcc + bp] = acc;
   }
-  Acc[(ec.e * g.lcc + bb) * ldacc + F * g.lcc + bp] = acc;
 }
 
 // ------------------------------------------------ coarse part of the V-cycle
@@ -601,6 +602,20 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
   k_cc_basis<<<(unsigned)g.neo, 64, smem, s>>>(g, Ac, Bc, Rcc, cc_evals);
 }
 
+// two_grid: R_cc = I (build_two_grid, solver.cpp:401-420), lcc = q: row
+// (E, k) of R_cc is the unit vector of the element's k-th coarse dof.
+__global__ void k_cc_identity(GridParams g, double* Rcc, double* cc_evals) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const int64_t e = blockIdx.x + g.e0;
+  for (int i = threadIdx.x; i < q * q; i += blockDim.x)
+    Rcc[e * q * q + i] = (i / q == i % q) ? 1.0 : 0.0;
+  for (int k = threadIdx.x; k < q; k += blockDim.x) cc_evals[e * q + k] = 0.0;
+}
+
+void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cudaStream_t s) {
+  k_cc_identity<<<(unsigned)g.neo, 256, 0, s>>>(g, Rcc, cc_evals);
+}
+
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
                             cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
@@ -615,7 +630,7 @@ void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rc
   // this context's rows of the global n x n matrix
   cudaMemsetAsync(Acc + g.e0 * g.lcc * n, 0, sizeof(double) * (size_t)(g.neo * g.lcc * n), s);
   dim3 grid((unsigned)g.neo, 7);
-  k_acc_assemble<<<grid, g.lcc * g.lcc, 0, s>>>(g, Ac, Rcc, Acc, n);
+  k_acc_assemble<<<grid, g.lcc * g.lcc < 256 ? g.lcc * g.lcc : 256, 0, s>>>(g, Ac, Rcc, Acc, n);
 }
 
 // Coarse part of one V-cycle (solver.cpp:292-319): rc -> ec.

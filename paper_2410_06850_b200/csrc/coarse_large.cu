@@ -6,13 +6,13 @@
 // solved by subspace iteration on a shifted inverse with Rayleigh-Ritz on the
 // projected stiffness (coarse_coarse_basis, coarse_space.cpp:343-406).
 #include "coarse_elem.cuh"
-#include "gj.cuh"
+#include "gj_global.cuh"
 
 namespace tmg {
 
 namespace {
-constexpr int GB = 64;        // pivot block
-constexpr int GJT = 256;      // threads of the batched inverse (one column each, q <= 256)
+constexpr int GB = kGjBlock;
+constexpr int GJT = kGjThreads;
 constexpr int KS = 16;        // subspace width of the cc eigensolver (L_cc <= KS - 4)
 
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -69,94 +69,16 @@ __global__ void k_elem_matrix(GridParams g, const double* __restrict__ Ac,
   for (int i = threadIdx.x; i < q; i += blockDim.x) M[i * q + i] += shift_rel * mx;
 }
 
-// In-place inverse of each SPD q x q matrix (q a multiple of 64, q <= 256):
-// blocked Gauss-Jordan sweeps with 64 x 64 pivot blocks. Thread j owns column
-// j: the trailing update A_ij -= Cold_i . Pn_j reads the old pivot columns
-// Cold (q x 64, shared memory) and keeps its own new pivot-row entries Pn_j
-// (64 values) in registers. Pivots checked with the reference's rule
-// (solver.cpp:86-92); status = 2 on failure. Symmetrised on exit.
+// In-place inverse of each SPD q x q matrix (gj_global.cuh), one CTA per
+// matrix; the reference singular-pivot rule (solver.cpp:86-92) over each
+// matrix's pivots, status = 2 on failure.
 __global__ void __launch_bounds__(GJT, 1) k_batched_gj(double* A, int q, int* status) {
   extern __shared__ __align__(16) double smg[];
-  double* Cold = smg;              // q x GB
-  double* Ds = Cold + q * GB;      // GB x GB
-  double* Dt = Ds + GB * GB;       // its transpose
   __shared__ GjSmem<GB> gjs;
   __shared__ double red[2][GJT / 32];
-  double* M = A + (int64_t)blockIdx.x * q * q;
   const int t = threadIdx.x, lane = t & 31;
-  using L = GjLayout<GB, GJT>;
-  constexpr int CW = L::CW, RH = L::RH;
-  const int c0 = CW * (t >> 5);
   double pmin = 1e300, pmax = 0.0;
-  for (int K = 0; K < q / GB; ++K) {
-    const int k0 = K * GB;
-    // (a) pivot block inverse (register-resident)
-    double v[RH][CW];
-#pragma unroll
-    for (int h = 0; h < RH; ++h)
-#pragma unroll
-      for (int qq = 0; qq < CW; ++qq) v[h][qq] = M[(k0 + lane + 32 * h) * q + k0 + c0 + qq];
-    gj_invert<GB, GJT>(v, gjs, pmin, pmax);
-#pragma unroll
-    for (int h = 0; h < RH; ++h)
-#pragma unroll
-      for (int qq = 0; qq < CW; ++qq) Ds[(lane + 32 * h) * GB + c0 + qq] = v[h][qq];
-    // (b) old pivot columns; D^-1 transposed for the pivot-row product
-    for (int e = t; e < q * GB; e += GJT) Cold[e] = M[(e / GB) * q + k0 + e % GB];
-    for (int e = t; e < GB * GB; e += GJT) Dt[e] = Ds[(e % GB) * GB + e / GB];
-    __syncthreads();
-    // (c) new pivot row entries of column j: Pn_j = D^-1 A_{K, j}
-    const int j = t;
-    const bool jcol = j < q;
-    double pn[GB];
-#pragma unroll
-    for (int r = 0; r < GB; ++r) pn[r] = 0.0;
-    if (jcol) {
-      for (int k = 0; k < GB; ++k) {
-        const double a = M[(int64_t)(k0 + k) * q + j];
-        const double2* dk = reinterpret_cast<const double2*>(Dt + k * GB);
-#pragma unroll
-        for (int r = 0; r < GB / 2; ++r) {
-          const double2 d = dk[r];
-          pn[2 * r] = fma(d.x, a, pn[2 * r]);
-          pn[2 * r + 1] = fma(d.y, a, pn[2 * r + 1]);
-        }
-      }
-    }
-    __syncthreads();  // every column read its pivot-row entries
-    if (jcol) {
-      const bool jK = j >= k0 && j < k0 + GB;
-      for (int i = 0; i < q; ++i) {
-        if (i == k0) {  // pivot rows last
-          i += GB - 1;
-          continue;
-        }
-        const double2* ci = reinterpret_cast<const double2*>(Cold + i * GB);
-        double x;
-        if (jK) {  // pivot columns: -Cold_i D^-1
-          double s = 0.0;
-          for (int k = 0; k < GB; ++k) s = fma(Cold[i * GB + k], Ds[k * GB + (j - k0)], s);
-          x = -s;
-        } else {  // trailing update
-          double s0 = M[(int64_t)i * q + j], s1 = 0.0;
-#pragma unroll
-          for (int k = 0; k < GB / 2; ++k) {
-            const double2 c2 = ci[k];
-            s0 = fma(-c2.x, pn[2 * k], s0);
-            s1 = fma(-c2.y, pn[2 * k + 1], s1);
-          }
-          x = s0 + s1;
-        }
-        M[(int64_t)i * q + j] = x;
-      }
-      // pivot rows: D^-1 on the pivot block, Pn elsewhere
-#pragma unroll
-      for (int k = 0; k < GB; ++k)
-        M[(int64_t)(k0 + k) * q + j] = jK ? Ds[k * GB + (j - k0)] : pn[k];
-    }
-    __syncthreads();
-  }
-  // reference singular-pivot rule over the element's pivots
+  gj_inverse_global(A + (int64_t)blockIdx.x * q * q, q, gj_global_smem(smg, q), gjs, pmin, pmax);
   double mx = pmax, mn = pmin;
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -174,14 +96,6 @@ __global__ void __launch_bounds__(GJT, 1) k_batched_gj(double* A, int q, int* st
       n = fmin(n, red[1][w]);
     }
     if (!(n > 1e-14 * m)) atomicExch(status, 2);
-  }
-  for (int e = t; e < q * q; e += GJT) {
-    const int i = e / q, jj = e % q;
-    if (i < jj) {
-      const double s = 0.5 * (M[i * q + jj] + M[jj * q + i]);
-      M[i * q + jj] = s;
-      M[jj * q + i] = s;
-    }
   }
 }
 
@@ -499,7 +413,7 @@ bool coarse_large_supported(int q, int lcc) {
   return q > 64 && q % GB == 0 && q <= GJT && lcc <= KS - 4;
 }
 
-size_t batched_gj_smem(int q) { return sizeof(double) * (size_t)(q * GB + 2 * GB * GB); }
+size_t batched_gj_smem(int q) { return gj_global_smem_bytes(q); }
 
 // Winv of every owned cc element (coarse_blocks_by_cc smoother) for large q.
 void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,

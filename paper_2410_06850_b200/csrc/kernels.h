@@ -99,6 +99,7 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
                      double* cc_evals, cudaStream_t s);
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
                             cudaStream_t s);
+void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cudaStream_t s);
 // large cc elements (q = sd^3 L_c > 64, coarse_large.cu)
 bool coarse_large_supported(int q, int lcc);
 void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
@@ -179,6 +180,18 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
 void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s);
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
-                        double* history, int init, cudaStream_t s);
+                        double* history, int init, int defer, cudaStream_t s);
+// block-Jacobi with one block per cc element (block_jacobi.cu)
+bool bj_supported(int cb, int sd);
+int64_t bj_doubles_per_element(int cb, int sd);
+void launch_bj_factor(const GridParams& g, int cb, const double* coef, double* G, int* status,
+                      cudaStream_t s);
+void launch_bj_apply(const GridParams& g, int cb, const double* coef, const double* G,
+                     const double* in, const double* add, double* out, const double* rdot,
+                     PcgState* st, double* partials, int init, cudaStream_t s);
+void launch_prolong_add(const GridParams& g, int cb, const double* phi, const double* r1,
+                        const double* ec, double* r2, const PcgState* st, cudaStream_t s);
+void launch_resid(const GridParams& g, int cb, const double* coef, const double* r,
+                  const double* x, double* t, const PcgState* st, cudaStream_t s);
 
 }  // namespace tmg

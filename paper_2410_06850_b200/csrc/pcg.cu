@@ -15,13 +15,12 @@
 // trip is needed inside an iteration; the host only polls `done` between
 // chunks of captured iterations.
 #include "kernels.h"
+#include "pcg_fin.cuh"
 #include "smoother.cuh"
 
 namespace tmg {
 
 constexpr int LCP = 4;  // compiled L_c (see coarse.cu)
-
-__device__ __forceinline__ bool is_finite(double v) { return isfinite(v); }
 
 // ------------------------------------------------------------ coefficients
 template <int CB>
@@ -45,81 +44,6 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coefficients(GridParams g,
   coef[M + s] = (fs.nbmask & 8) ? fs.t[3] : 0.0;
   coef[2 * M + s] = (fs.nbmask & 32) ? fs.t[5] : 0.0;
   coef[3 * M + s] = fs.diag;
-}
-
-// ------------------------------------------------- scalar logic of pcg()
-// (shared by the in-kernel last-block path and k_finalize)
-__device__ __forceinline__ void fin_init(PcgState* st, double bb, double rr) {
-  const double bnorm = sqrt(bb), rnorm = sqrt(rr);
-  st->bnorm = bnorm;
-  st->rnorm = rnorm;
-  st->it = 0;
-  st->first = 0;
-  if (bnorm == 0.0) {  // solver.cpp:506-513
-    st->status = kStatusZeroRhs;
-    st->done = 1;
-  } else if (rnorm / bnorm <= st->rtol) {  // :523-531
-    st->status = kStatusConverged;
-    st->done = 1;
-  } else {
-    st->status = kStatusRunning;
-    st->done = 0;
-  }
-}
-
-__device__ __forceinline__ void fin_search(PcgState* st, double pqt) {
-  st->pq = pqt;
-  st->first = 0;
-  if (!(pqt > 0.0)) {  // solver.cpp:541-548
-    st->status = kStatusIndefinite;
-    st->done = 1;
-  } else {
-    st->alpha = st->rho / pqt;  // :549
-  }
-}
-
-__device__ __forceinline__ void finish_rr(PcgState* st, double rr, double* history) {
-  const int it = st->it + 1;
-  const double rel = sqrt(rr) / st->bnorm;
-  st->it = it;
-  st->rnorm = sqrt(rr);
-  if (it - 1 < st->hist_cap) history[it - 1] = rel;  // solver.cpp:555
-  if (!is_finite(rel)) {
-    st->status = kStatusNonFinite;
-    st->done = 1;
-  } else if (rel <= st->rtol) {  // solver.cpp:557-560
-    st->status = kStatusConverged;
-    st->done = 1;
-  } else if (it >= st->maxit) {
-    st->status = kStatusMaxIt;
-    st->done = 1;
-  }
-}
-
-__device__ __forceinline__ void fin_post(PcgState* st, double rz, int init) {
-  if (init) {
-    st->rho = rz;  // solver.cpp:537
-    st->beta = 0.0;
-    st->first = 1;
-  } else {
-    st->beta = rz / st->rho;  // :562-564
-    st->rho = rz;
-  }
-}
-
-__device__ __forceinline__ void fin_jacobi(PcgState* st, double rr, double rz, int init,
-                                           double* history) {
-  if (init) {
-    st->rho = rz;
-    st->beta = 0.0;
-    st->first = 1;
-  } else {
-    finish_rr(st, rr, history);
-    if (!st->done) {
-      st->beta = rz / st->rho;
-      st->rho = rz;
-    }
-  }
 }
 
 __global__ void k_finalize(FinArgs a, int which, int init) {
@@ -444,7 +368,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
                                                              const double* __restrict__ q, double* r,
                                                              double* z, PcgState* st,
                                                              double* partials, double* history,
-                                                             int init) {
+                                                             int init, int defer) {
   pdl_trigger();
   pdl_wait();
   if (st->done) return;
@@ -461,12 +385,15 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
     r[s] = rv;
   }
   const double zv = dinv ? rv * dinv[s] : rv;  // solver.cpp:35 / :18
-  z[s] = zv;
+  if (!defer) z[s] = zv;  // defer: the block solve (block_jacobi.cu) writes z
   double v[2] = {rv * rv, rv * zv};
   block_sum_k<C, 2>(v, red);
   double tot[2];
   if (grid_reduce_last_k<2>(v, partials, &st->ticket[4], tot, &flag, red) && t == 0) {
-    if (g.dist) {
+    if (defer) {
+      if (g.dist) st->loc[kRedUpdate] = tot[0];
+      else finish_rr(st, tot[0], history);
+    } else if (g.dist) {
       st->loc[kRedJacobi] = tot[0];
       st->loc[kRedJacobi + 1] = tot[1];
     } else {
@@ -550,9 +477,9 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
-                        double* history, int init, cudaStream_t s) {
-  if (cb == 8) launch_pdl(k_jacobi_step<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init);
-  else launch_pdl(k_jacobi_step<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init);
+                        double* history, int init, int defer, cudaStream_t s) {
+  if (cb == 8) launch_pdl(k_jacobi_step<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init, defer);
+  else launch_pdl(k_jacobi_step<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init, defer);
 }
 
 }  // namespace tmg

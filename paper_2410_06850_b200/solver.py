@@ -54,7 +54,7 @@ class _Opts(C.Structure):
     _fields_ = [("kind", C.c_int), ("num_local_basis", C.c_int64),
                 ("num_cc_basis", C.c_int64), ("smoother_sweeps", C.c_int),
                 ("eig_tol", C.c_double), ("eig_degree", C.c_int), ("eig_max_outer", C.c_int),
-                ("warm_start", C.c_int)]
+                ("warm_start", C.c_int), ("fine_blocks", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -194,6 +194,17 @@ class MmgOptions:
     eig_degree: int = 0
     eig_max_outer: int = 0
     warm_start: bool = False  # start the local eigensolver from the previous set-up's bases
+    # fine smoother partition: "coarse_cell" (GPU default) or "cc" (the reference
+    # build_mmg's fine_blocks_by_cc, solver.cpp:353-361)
+    fine_blocks: str = "coarse_cell"
+
+    def _c(self, kind):
+        fb = {"coarse_cell": 0, "cc": 1}
+        if self.fine_blocks not in fb:
+            raise ValueError(f"fine_blocks must be one of {list(fb)}")
+        return _Opts(kind, self.num_local_basis, self.num_cc_basis, self.smoother_sweeps,
+                     self.eig_tol, self.eig_degree, self.eig_max_outer, int(self.warm_start),
+                     fb[self.fine_blocks])
 
 
 @dataclass
@@ -332,9 +343,7 @@ class Context:
     def simp_init(self, volfrac=0.3, rmin=1.5, move=0.2, kappa_lo=1e-6, kappa_hi=1.0, p=3,
                   source=1.0, rtol=1e-8, maxit=10000, rho0=None, mmg: MmgOptions = MmgOptions()):
         o = _SimpOpts(volfrac, rmin, move, kappa_lo, kappa_hi, p, source, rtol, maxit)
-        m = _Opts(PrecondKind.parse("mmg"), mmg.num_local_basis, mmg.num_cc_basis,
-                  mmg.smoother_sweeps, mmg.eig_tol, mmg.eig_degree, mmg.eig_max_outer,
-                  int(mmg.warm_start))
+        m = mmg._c(PrecondKind.parse("mmg"))
         r0 = _ptr(_f64(rho0)) if rho0 is not None else None
         self._check(native().tmg_simp_init(self._p, C.byref(o), C.byref(m), r0))
 
@@ -362,8 +371,7 @@ class Context:
             kind = PrecondKind.parse(kind)
         else:
             self.kind_name = [k for k, v in PrecondKind._names.items() if v == kind][0]
-        o = _Opts(kind, opts.num_local_basis, opts.num_cc_basis, opts.smoother_sweeps,
-                  opts.eig_tol, opts.eig_degree, opts.eig_max_outer, int(opts.warm_start))
+        o = opts._c(kind)
         self._check(native().tmg_setup(self._p, C.byref(o)))
 
     # operators

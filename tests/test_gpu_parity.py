@@ -85,6 +85,74 @@ def test_jacobi_pcg_vs_oracle(n, kmin):
     assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
 
 
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (32, 2, 2, 1e-6), (64, 4, 2, 1e-6)])
+def test_block_jacobi_vs_oracle(n, ncc, sd, kmin):
+    """block_jacobi (BlockJacobiPreconditioner, solver.cpp:444-458): one exact
+    solve per cc element (16^3 cells at c = 8, 8^3 at c = 4)."""
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond("block_jacobi", s, O.hierarchy(O.grid(n), ncc, sd), fine_blocks="cc")
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("block_jacobi")
+    r = np.random.default_rng(7).standard_normal(n ** 3)
+    z_ref = m.apply(r)
+    # explicit plane Schur inverses vs the reference's factorisation: forward
+    # error eps * cond(block) (cond ~1e8 at contrast 1e6)
+    tol = 1e-12 if kmin >= 1e-3 else 1e-8
+    assert np.linalg.norm(c.apply_preconditioner(r) - z_ref) <= tol * np.linalg.norm(z_ref)
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8, max_iterations=20000)
+    res = c.pcg(s.rhs, rtol=1e-8, max_iterations=20000)
+    assert res.report.converged
+    it, it_ref = res.report.iterations, ref.iterations
+    if kmin >= 1e-3:
+        assert iters_close(it, it_ref), (it, it_ref)
+    else:
+        # at contrast 1e6 the reference's own count moves 205..286 (of 286)
+        # under 1e-14 relative noise on z (tests/bj_sensitivity.py): bound by
+        # that spread instead of 10%
+        assert 0.7 * it_ref <= it <= 1.1 * it_ref, (it, it_ref)
+    assert np.linalg.norm(res.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("kind,fine", [("mmg", "cc"), ("two_grid", "cell"), ("two_grid", "cc")])
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (32, 2, 2, 1e-6), (64, 4, 2, 1e-3)])
+def test_hierarchy_variants_vs_oracle(kind, fine, n, ncc, sd, kmin):
+    """two_grid (build_two_grid, solver.cpp:401-420: R_cc = I) and the
+    reference's own fine blocks (fine_blocks_by_cc) for mmg / two_grid."""
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond(kind, s, O.hierarchy(O.grid(n), ncc, sd), fine_blocks=fine, coarse_blocks="cc")
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup(kind, MmgOptions(fine_blocks="cc" if fine == "cc" else "coarse_cell"))
+    r = c.pcg(s.rhs, rtol=1e-8)
+    assert r.report.converged
+    assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+    k = min(len(r.report.residual_history), len(ref.residual_history))
+    np.testing.assert_allclose(r.report.residual_history[:k // 2], ref.residual_history[:k // 2],
+                               rtol=1e-3)
+
+
+def test_hierarchy_variant_limits():
+    n = 16
+    _, kappa = problem(n, 1e-3)
+    c = ctx_for(n, 1, 4, kappa)  # q = 256
+    with pytest.raises(NotSupportedError, match="two_grid"):
+        c.setup("two_grid")
+    c = ctx_for(64, 2, 4, problem(64, 1e-3)[1])  # 32^3-cell cc elements
+    with pytest.raises(NotSupportedError, match="block_jacobi"):
+        c.setup("mmg", MmgOptions(fine_blocks="cc"))
+
+
+def test_block_jacobi_limits():
+    n = 64
+    _, kappa = problem(n, 1e-3)
+    c = ctx_for(n, 2, 4, kappa)  # 32^3-cell blocks
+    with pytest.raises(NotSupportedError, match="block_jacobi"):
+        c.setup("block_jacobi")
+
+
 @pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (16, 2, 2, 1e-6), (32, 2, 2, 1e-3),
                                            (32, 2, 2, 1e-6), (64, 4, 2, 1e-3),
                                            # large cc elements (q = 256, coarse_large.cu)
@@ -416,8 +484,8 @@ def test_configuration_errors():
     c.set_conductivity(kappa, BC)
     with pytest.raises(ValueError, match="more eigenvectors"):
         c.setup("mmg", MmgOptions(num_cc_basis=33))
-    with pytest.raises(NotSupportedError):
-        c.setup("two_grid")
+    with pytest.raises(ValueError, match="fine_blocks"):
+        c.setup("mmg", MmgOptions(fine_blocks="bogus"))
     with pytest.raises(ValueError, match="no preconditioner"):
         c.pcg(np.ones(n ** 3))
     c.setup("jacobi")
