@@ -200,6 +200,47 @@ int tmg_simp_step(tmg_ctx* ctx, tmg_simp_report* report);
 /* filtered design ("physical" densities) and the last state solution */
 int tmg_simp_download(tmg_ctx* ctx, double* xphys, double* temperature);
 
+/* The reference's design loop (topmg::optimize, optim.cpp:240-345) on one
+ * resolution level, resident on the device: per iteration the design's
+ * conductivity and heat source (material.cpp:45-66), a preconditioner set-up
+ * (mmg options as given; the reference rebuilds it from scratch), LS1 and LS2
+ * (adjoint_rhs) from zero, mean temperature, sensitivity (optim.cpp:21-84)
+ * and the single-constraint MMA update (mma_update, :121-220) clamped to
+ * [0, 1]. The level schedule and design prolongation between levels
+ * (interpolate_design, grid.cpp:220-241) stay with the host caller
+ * (paper_2410_06850_b200/optim.py mirrors optimize()). */
+typedef struct {
+  double vstar;                /* OptimConfig::vstar (reference default 0.05) */
+  double move_limit, asy_init, asy_incr, asy_decr; /* MmaOptions: 0.2, 0.5, 1.2, 0.7 */
+  double kappa_lo, kappa_hi, f0; /* MaterialModel */
+  int p;
+  double rtol;                 /* OptimConfig::rtol (1e-6) */
+  int maxit;                   /* OptimConfig::maxit (10000) */
+  int warm_start;              /* 0: as the reference (cold set-up, x0 = 0); 1: warm-started
+                                  local eigensolver and solves from the previous T / U */
+} tmg_optim_options;
+
+/* IterationLog (optim.hpp:74-84) plus the update's ||dx||_inf and multiplier. */
+typedef struct {
+  int iter;
+  double cost, volume;
+  int ls1_iters, ls2_iters;
+  double setup_seconds, ls1_seconds, ls2_seconds;
+  double dx_inf, lambda, step_seconds;
+} tmg_iteration_log;
+
+/* x0: initial design (x-fastest); NULL -> uniform vstar. Resets the MMA
+ * state (MmaState, optim.hpp:35-40). The context's boundary patches are used. */
+int tmg_optim_init(tmg_ctx* ctx, const tmg_optim_options* opts, const tmg_mmg_options* mmg,
+                   const double* x0);
+/* One MMA iteration. A state/adjoint solve that does not converge returns
+ * TMG_ESOLVER with the reference's failure message; the design is unchanged. */
+int tmg_optim_step(tmg_ctx* ctx, tmg_iteration_log* log);
+/* Evaluation solve of the current design (LS1 only): log->cost = final cost. */
+int tmg_optim_evaluate(tmg_ctx* ctx, tmg_iteration_log* log);
+/* current design and the last state solution (x-fastest; either nullable) */
+int tmg_optim_download(tmg_ctx* ctx, double* x, double* temperature);
+
 /* Preconditioner set-up: make_preconditioner (solver.cpp:462-481). */
 int tmg_setup(tmg_ctx* ctx, const tmg_mmg_options* opts);
 

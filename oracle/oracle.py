@@ -283,6 +283,10 @@ def ref():
         R.ref_ctx_pcg.argtypes = [C.c_void_p, C.c_double, C.c_int, DP, C.POINTER(C.c_int),
                                   C.POINTER(C.c_int), DP]
         R.ref_ctx_destroy.argtypes = [C.c_void_p]
+        IP = C.POINTER(C.c_int)
+        R.ref_optimize.argtypes = [C.c_int, C.POINTER(I64), IP, I64, I64, C.c_double, C.c_double,
+                                   C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, DP,
+                                   C.c_double, C.c_int, C.c_int, IP, DP, DP, IP, IP, DP, DP, IP]
         R.ref_num_threads.restype = C.c_int
         _REF = R
     return _REF
@@ -367,6 +371,31 @@ def ref_sensitivity(n, rho, t, u, kappa_lo, kappa_hi=1.0, f0=1.0, p=3, patches=N
                                  _d(np.ascontiguousarray(t, dtype=float)),
                                  _d(np.ascontiguousarray(u, dtype=float)), _d(out)))
     return out
+
+
+def ref_optimize(levels, iters, ncc, sd, vstar=0.05, convergence_dx=0.01, kappa_lo=1e-3,
+                 kappa_hi=1.0, f0=1.0, p=3, patches=None, rtol=1e-6, maxit=10000):
+    """topmg::optimize (optim.cpp:240-345) of the compiled reference on cubic
+    levels; returns (trajectory dict of arrays, final design, final cost, failed)."""
+    patches = patches if patches is not None else bottom_center_patch()
+    pa = _patch_array(patches)
+    nl = len(levels)
+    lv = (I64 * nl)(*levels)
+    it = (C.c_int * nl)(*iters)
+    cap = int(sum(iters)) + 1
+    costs, vols = np.zeros(cap), np.zeros(cap)
+    l1, l2 = np.zeros(cap, dtype=np.int32), np.zeros(cap, dtype=np.int32)
+    nlog, failed = C.c_int(0), C.c_int(0)
+    fc = C.c_double(0.0)
+    x = np.empty(levels[-1] ** 3)
+    IP = C.POINTER(C.c_int)
+    _ref_check(ref().ref_optimize(nl, lv, it, ncc, sd, vstar, convergence_dx, kappa_lo, kappa_hi,
+                                  f0, p, len(patches), _d(pa), rtol, maxit, cap, C.byref(nlog),
+                                  _d(costs), _d(vols), l1.ctypes.data_as(IP),
+                                  l2.ctypes.data_as(IP), _d(x), C.byref(fc), C.byref(failed)))
+    n = nlog.value
+    traj = {"cost": costs[:n], "volume": vols[:n], "ls1": l1[:n], "ls2": l2[:n]}
+    return traj, x, fc.value, bool(failed.value)
 
 
 def _ref_check(rc):

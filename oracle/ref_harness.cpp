@@ -294,4 +294,39 @@ int ref_sensitivity(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, do
   });
 }
 
+// topmg::optimize (optim.cpp:240-345) on cubic levels n_levels[0..nlev) with
+// the reference's Mmg preconditioner and MmaOptions defaults. Up to max_log
+// trajectory entries; x_out receives the final design (finest level).
+int ref_optimize(int nlev, const int64_t* n_levels, const int* iters, int64_t ncc, int64_t sd,
+                 double vstar, double conv_dx, double klo, double khi, double f0, int p,
+                 int npatch, const double* patches, double rtol, int maxit, int max_log,
+                 int* nlog, double* costs, double* volumes, int* ls1, int* ls2, double* x_out,
+                 double* final_cost, int* failed) {
+  return guarded([&] {
+    OptimConfig cfg;
+    cfg.vstar = vstar;
+    cfg.convergence_dx = conv_dx;
+    for (int l = 0; l < nlev; ++l) {
+      cfg.schedule.emplace_back(n_levels[l], n_levels[l], n_levels[l]);
+      cfg.iters_per_level.push_back(iters[l]);
+    }
+    cfg.ncc = {ncc, ncc, ncc};
+    cfg.sd = sd;
+    cfg.rtol = rtol;
+    cfg.maxit = maxit;
+    const OptimizeResult r = optimize(cfg, MaterialModel(klo, khi, f0, p), make_bc(npatch, patches));
+    const int n = static_cast<int>(r.trajectory.size());
+    *nlog = n;
+    for (int i = 0; i < n && i < max_log; ++i) {
+      costs[i] = r.trajectory[i].cost;
+      volumes[i] = r.trajectory[i].volume;
+      ls1[i] = r.trajectory[i].ls1_iters;
+      ls2[i] = r.trajectory[i].ls2_iters;
+    }
+    std::copy(r.design.values.begin(), r.design.values.end(), x_out);
+    *final_cost = r.final_cost;
+    *failed = r.failed ? 1 : 0;
+  });
+}
+
 }  // extern "C"

@@ -7,7 +7,10 @@ reference's solver interface used by the tests and the benchmark.
 from .solver import (BoundarySpec, ConfigError, Context, DirichletPatch, GridSpec, MmgOptions,
                      NotSupportedError, PcgResult, PrecondKind, SolveReport, SolverError,
                      make_preconditioner, native, pcg)
+from .optim import (IterationLog, MaterialModel, MmaOptions, OptimConfig, OptimizeResult,
+                    interpolate_design, optimize)
 
 __all__ = ["BoundarySpec", "ConfigError", "Context", "DirichletPatch", "GridSpec", "MmgOptions",
            "NotSupportedError", "PcgResult", "PrecondKind", "SolveReport", "SolverError",
-           "make_preconditioner", "native", "pcg"]
+           "make_preconditioner", "native", "pcg", "IterationLog", "MaterialModel", "MmaOptions",
+           "OptimConfig", "OptimizeResult", "interpolate_design", "optimize"]

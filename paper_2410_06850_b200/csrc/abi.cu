@@ -161,6 +161,19 @@ struct tmg_ctx {
            *W = nullptr, *tmp = nullptr, *part = nullptr, *scal = nullptr;
     double *T = nullptr, *U = nullptr;  // previous state / adjoint (brick layout)
   } simp;
+  // reference design loop with MMA (tmg_optim_*): x-fastest design arrays
+  struct Optim {
+    bool on = false;
+    tmg_optim_options o{};
+    tmg_mmg_options mmg{};
+    int iter = 0;  // MmaState::iteration
+    double *x = nullptr, *xp = nullptr, *xp2 = nullptr, *xnew = nullptr, *low = nullptr,
+           *upp = nullptr, *grad = nullptr, *xb = nullptr, *part = nullptr, *sp = nullptr,
+           *scal = nullptr;
+    double *T = nullptr, *U = nullptr;  // last state / adjoint (brick layout)
+    unsigned int* bar = nullptr;
+    bool have_T = false;
+  } opt;
 };
 
 namespace {
@@ -1329,6 +1342,201 @@ int tmg_simp_download(tmg_ctx* c, double* xphys, double* temperature) {
     if (temperature) {
       launch_from_brick(c->slabs[0].g, c->cb, S.T, S.xnew, c->stream);
       CK(cudaMemcpyAsync(temperature, S.xnew, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+// ------------------------------------------------ reference design loop (MMA)
+
+int tmg_optim_init(tmg_ctx* c, const tmg_optim_options* o, const tmg_mmg_options* mmg,
+                   const double* x0) {
+  if (!c || !o || !mmg) return set_err(c, TMG_EARG, "tmg_optim_init: null argument");
+  if (c->dist()) return set_err(c, TMG_ENOTSUP, "the design loop runs on single-slab contexts");
+  if (!c->have_problem)
+    return set_err(c, TMG_EARG, "tmg_optim_init: set a problem (patches) first");
+  if (!(o->vstar > 0.0 && o->vstar <= 1.0))
+    return set_err(c, TMG_ECONFIG, "optimize: vstar must lie in (0, 1]");
+  if (!(o->kappa_lo > 0.0) || !(o->kappa_hi > o->kappa_lo))
+    return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
+  if (o->f0 < 0.0) return set_err(c, TMG_ECONFIG, "MaterialModel: f0 must be nonnegative");
+  if (o->p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    auto& O = c->opt;
+    const int64_t M = c->M;
+    for (double** v : {&O.x, &O.xp, &O.xp2, &O.xnew, &O.low, &O.upp, &O.grad, &O.xb, &O.T, &O.U})
+      if (!*v) *v = dalloc<double>(c, M);
+    if (!O.part) O.part = dalloc<double>(c, mma_partials_doubles());
+    if (!O.sp) O.sp = dalloc<double>(c, sum_partials_doubles());
+    if (!O.scal) O.scal = dalloc<double>(c, 8);
+    if (!O.bar) O.bar = dalloc<unsigned int>(c, 2);
+    CK(cudaMemsetAsync(O.bar, 0, 2 * sizeof(unsigned int), c->stream));
+    O.o = *o;
+    O.mmg = *mmg;
+    O.iter = 0;
+    O.have_T = false;
+    if (x0)
+      CK(cudaMemcpyAsync(O.x, x0, sizeof(double) * (size_t)M, cudaMemcpyHostToDevice,
+                         c->stream));
+    else
+      launch_fill(O.x, M, o->vstar, c->stream);  // DesignField(grid, vstar)
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    O.on = true;
+  });
+}
+
+namespace {
+// solve_pair (optim.cpp:248-292) on the current design: conductivity, heat
+// source, set-up, LS1 and (with_adjoint) LS2. Returns TMG_OK or an error code.
+int optim_solve_pair(tmg_ctx* c, bool with_adjoint, tmg_iteration_log* L) {
+  auto& O = c->opt;
+  const int64_t M = c->M;
+  int rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    Slab& s = c->slabs[0];
+    launch_to_brick(s.g, c->cb, O.x, O.xb, c->stream);
+    launch_conductivity(s.g, c->cb, O.xb, s.kappa, O.o.kappa_lo, O.o.kappa_hi, O.o.p, c->stream);
+    CK(cudaGetLastError());
+  });
+  if (rc) return rc;
+  if ((rc = finish_problem(c))) return rc;
+  tmg_mmg_options mo = O.mmg;
+  mo.warm_start = O.o.warm_start && O.iter > 0;
+  if ((rc = tmg_setup(c, &mo))) return rc;
+  L->setup_seconds = c->setup_seconds;
+  const bool warm = O.o.warm_start && O.have_T;
+  return guard(c, [&] {
+    Slab& s = c->slabs[0];
+    const size_t bytes = sizeof(double) * (size_t)M;
+    // LS1: b = f(x) vol + Dirichlet lift (assemble_system, fvm.cpp:63-112)
+    launch_heat_source(s.g, c->cb, O.xb, s.q, O.o.f0, O.o.p, c->stream);
+    launch_boundary(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                    c->grid.ly, c->grid.lz, s.kappa, s.q, s.dmask, s.b, nullptr, c->stream);
+    if (warm) CK(cudaMemcpyAsync(s.x, O.T, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    tmg_report a{};
+    solve_device(c, O.o.rtol, O.o.maxit, warm, &a, nullptr, nullptr);
+    if (!a.converged) {
+      set_err(c, TMG_ESOLVER, "state solve (LS1) did not converge within %d iterations",
+              O.o.maxit);
+      throw Fail{TMG_ESOLVER};
+    }
+    L->ls1_iters = a.iterations;
+    L->ls1_seconds = a.solve_seconds;
+    CK(cudaMemcpyAsync(O.T, s.x, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    launch_sum(O.T, M, O.sp, O.scal, c->stream);
+    double sum = 0.0;
+    CK(cudaMemcpyAsync(&sum, O.scal, sizeof sum, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    L->cost = sum / (double)M;  // mean_temperature (optim.cpp:10-14)
+    if (!with_adjoint) return;
+    // LS2: adjoint_rhs (optim.cpp:16-19)
+    launch_fill(s.b, M, 1.0 / (double)M, c->stream);
+    if (warm) CK(cudaMemcpyAsync(s.x, O.U, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    solve_device(c, O.o.rtol, O.o.maxit, warm, &a, nullptr, nullptr);
+    if (!a.converged) {
+      set_err(c, TMG_ESOLVER, "adjoint solve (LS2) did not converge within %d iterations",
+              O.o.maxit);
+      throw Fail{TMG_ESOLVER};
+    }
+    L->ls2_iters = a.iterations;
+    L->ls2_seconds = a.solve_seconds;
+    CK(cudaMemcpyAsync(O.U, s.x, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    O.have_T = true;
+  });
+}
+}  // namespace
+
+int tmg_optim_step(tmg_ctx* c, tmg_iteration_log* log) {
+  if (!c) return set_err(c, TMG_EARG, "null context");
+  if (!c->opt.on) return set_err(c, TMG_EARG, "tmg_optim_step: call tmg_optim_init first");
+  auto& O = c->opt;
+  const auto t0 = std::chrono::steady_clock::now();
+  tmg_iteration_log L{};
+  L.iter = O.iter + 1;
+  const int64_t M = c->M;
+  auto host = [&](const double* d, int k) {
+    double v[8];
+    CK(cudaMemcpyAsync(v, d, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return std::vector<double>(v, v + k);
+  };
+  int rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    launch_sum(O.x, M, O.sp, O.scal, c->stream);
+    L.volume = host(O.scal, 1)[0] / (double)M;  // DesignField::volume_fraction
+  });
+  if (rc) return rc;
+  if ((rc = optim_solve_pair(c, true, &L))) return rc;
+  rc = guard(c, [&] {
+    Slab& s = c->slabs[0];
+    // sensitivity (optim.cpp:21-84) with the design-dependent source
+    launch_sensitivity(s.g, c->cb, c->patches.data(), (int)c->patches.size(), c->grid.lx,
+                       c->grid.ly, c->grid.lz, O.xb, s.kappa, O.T, O.U, O.o.kappa_lo,
+                       O.o.kappa_hi, O.o.f0, O.o.p, s.q, c->stream);
+    launch_from_brick(s.g, c->cb, s.q, O.grad, c->stream);
+    // MMA update with constraint volume - vstar, gradient 1/M (optim.cpp:308-318)
+    const MmaParams mp{O.o.move_limit, O.o.asy_init, O.o.asy_incr, O.o.asy_decr, 0.0, 1.0,
+                       1.0 / (double)M};
+    launch_mma_asymptotes(O.x, O.xp, O.xp2, O.low, O.upp, M, O.iter, mp, c->stream);
+    launch_mma_dual(O.x, O.grad, O.low, O.upp, M, L.volume - O.o.vstar, mp, O.part, O.bar,
+                    O.scal, c->stream);
+    CK(cudaGetLastError());
+    const std::vector<double> d = host(O.scal, 3);
+    if (d[1] != 0.0) {
+      set_err(c, TMG_ESOLVER, "mma_update: multiplier bisection failed, bracket [%g, %g]",
+              0.5 * d[2], d[2]);
+      throw Fail{TMG_ESOLVER};
+    }
+    L.lambda = d[0];
+    launch_mma_primal(O.x, O.grad, O.low, O.upp, M, O.scal, mp, O.xnew, O.part, O.scal + 3,
+                      c->stream);
+    CK(cudaGetLastError());
+    L.dx_inf = host(O.scal + 3, 1)[0];
+    // MmaState: x_prev2 <- x_prev, x_prev <- x; x <- x_new
+    double* t = O.xp2;
+    O.xp2 = O.xp;
+    O.xp = O.x;
+    O.x = O.xnew;
+    O.xnew = t;
+  });
+  if (rc) return rc;
+  ++O.iter;
+  L.step_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (log) *log = L;
+  return TMG_OK;
+}
+
+int tmg_optim_evaluate(tmg_ctx* c, tmg_iteration_log* log) {
+  if (!c) return set_err(c, TMG_EARG, "null context");
+  if (!c->opt.on) return set_err(c, TMG_EARG, "tmg_optim_evaluate: call tmg_optim_init first");
+  tmg_iteration_log L{};
+  L.iter = c->opt.iter;
+  int rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    launch_sum(c->opt.x, c->M, c->opt.sp, c->opt.scal, c->stream);
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, c->opt.scal, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    L.volume = v / (double)c->M;
+  });
+  if (rc) return rc;
+  if ((rc = optim_solve_pair(c, false, &L))) return rc;
+  if (log) *log = L;
+  return TMG_OK;
+}
+
+int tmg_optim_download(tmg_ctx* c, double* x, double* temperature) {
+  if (!c || !c->opt.on) return set_err(c, TMG_EARG, "tmg_optim_download: no design loop");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    auto& O = c->opt;
+    const size_t bytes = sizeof(double) * (size_t)c->M;
+    if (x) CK(cudaMemcpyAsync(x, O.x, bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (temperature) {
+      launch_from_brick(c->slabs[0].g, c->cb, O.T, O.xnew, c->stream);
+      CK(cudaMemcpyAsync(temperature, O.xnew, bytes, cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
   });

@@ -181,6 +181,23 @@ void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s);
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, int defer, cudaStream_t s);
+// design loop with MMA (optim.cu; MmaOptions, optim.hpp:27-32)
+struct MmaParams {
+  double move, asy_init, asy_incr, asy_decr, xmin, xmax;
+  double cgrad;  // constraint gradient (the reference's vol_grad = 1/M)
+};
+int mma_partials_doubles();
+void launch_heat_source(const GridParams& g, int cb, const double* x, double* f, double f0, int p,
+                        cudaStream_t s);
+void launch_mma_asymptotes(const double* x, const double* xp, const double* xp2, double* low,
+                           double* upp, int64_t n, int iteration, const MmaParams& o,
+                           cudaStream_t s);
+void launch_mma_dual(const double* x, const double* grad, const double* low, const double* upp,
+                     int64_t n, double constraint, const MmaParams& o, double* partials,
+                     unsigned int* bar, double* out, cudaStream_t s);
+void launch_mma_primal(const double* x, const double* grad, const double* low, const double* upp,
+                       int64_t n, const double* lam, const MmaParams& o, double* xnew,
+                       double* partials, double* dx_out, cudaStream_t s);
 // block-Jacobi with one block per cc element (block_jacobi.cu)
 bool bj_supported(int cb, int sd);
 int64_t bj_doubles_per_element(int cb, int sd);

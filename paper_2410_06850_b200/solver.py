@@ -76,6 +76,20 @@ class _SimpReport(C.Structure):
                 ("ls2_seconds", C.c_double), ("step_seconds", C.c_double)]
 
 
+class _OptimOpts(C.Structure):
+    _fields_ = [("vstar", C.c_double), ("move_limit", C.c_double), ("asy_init", C.c_double),
+                ("asy_incr", C.c_double), ("asy_decr", C.c_double), ("kappa_lo", C.c_double),
+                ("kappa_hi", C.c_double), ("f0", C.c_double), ("p", C.c_int),
+                ("rtol", C.c_double), ("maxit", C.c_int), ("warm_start", C.c_int)]
+
+
+class _IterLog(C.Structure):
+    _fields_ = [("iter", C.c_int), ("cost", C.c_double), ("volume", C.c_double),
+                ("ls1_iters", C.c_int), ("ls2_iters", C.c_int), ("setup_seconds", C.c_double),
+                ("ls1_seconds", C.c_double), ("ls2_seconds", C.c_double),
+                ("dx_inf", C.c_double), ("lambda", C.c_double), ("step_seconds", C.c_double)]
+
+
 _lib = None
 _DP = C.POINTER(C.c_double)
 
@@ -108,6 +122,7 @@ EXPORTED_SYMBOLS = (
     "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
+    "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
 )
 
 
@@ -357,6 +372,32 @@ class Context:
         xp, t = np.empty(self.cells), np.empty(self.cells)
         self._check(native().tmg_simp_download(self._p, _ptr(xp), _ptr(t)))
         return xp, t
+
+    # reference design loop (topmg::optimize with MMA, one level; optim.py)
+    def optim_init(self, vstar=0.05, kappa_lo=1e-3, kappa_hi=1.0, f0=1.0, p=3, move_limit=0.2,
+                   asy_init=0.5, asy_incr=1.2, asy_decr=0.7, rtol=1e-6, maxit=10000,
+                   warm_start=False, x0=None, kind="mmg", mmg: MmgOptions = MmgOptions()):
+        o = _OptimOpts(vstar, move_limit, asy_init, asy_incr, asy_decr, kappa_lo, kappa_hi, f0, p,
+                       rtol, maxit, int(warm_start))
+        m = mmg._c(PrecondKind.parse(kind) if isinstance(kind, str) else kind)
+        xp = _ptr(_f64(x0)) if x0 is not None else None
+        self._check(native().tmg_optim_init(self._p, C.byref(o), C.byref(m), xp))
+
+    def optim_step(self) -> dict:
+        r = _IterLog()
+        self._check(native().tmg_optim_step(self._p, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in _IterLog._fields_}
+
+    def optim_evaluate(self) -> dict:
+        r = _IterLog()
+        self._check(native().tmg_optim_evaluate(self._p, C.byref(r)))
+        return {k: getattr(r, k) for k, _ in _IterLog._fields_}
+
+    def optim_download(self):
+        """(design, last state solution), x-fastest."""
+        x, t = np.empty(self.cells), np.empty(self.cells)
+        self._check(native().tmg_optim_download(self._p, _ptr(x), _ptr(t)))
+        return x, t
 
     def assemble_rhs(self, source=None):
         out = np.empty(self.cells)

@@ -297,3 +297,11 @@ def test_sensitivity_matches_finite_differences():
         rm[c] -= h
         fd = (mean_t(rp)[0].mean() - mean_t(rm)[0].mean()) / (2 * h)
         assert abs(fd - grad[c]) <= 1e-5 * abs(grad[c]) + 1e-12
+
+
+def test_interpolate_design_matches_oracle():
+    from paper_2410_06850_b200 import GridSpec, interpolate_design
+    rng = np.random.default_rng(5)
+    lo = rng.random(4 * 6 * 8)
+    hi = interpolate_design(lo, GridSpec(4, 6, 8), GridSpec(8, 12, 24))
+    np.testing.assert_array_equal(hi, O.interpolate_design(lo, (4, 6, 8), (8, 12, 24)))
