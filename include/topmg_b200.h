@@ -136,6 +136,24 @@ int tmg_set_conductivity(tmg_ctx* ctx, const double* kappa, const tmg_patch* pat
                          int npatches);
 /* SIMP design (rho per cell) -> kappa on the device, MaterialModel +
  * conductivity (material.cpp:8-15,45-59). */
+/* Seeded synthetic design (SURVEY.md §8(d) "Synthetic inputs", §8(f) rank 3):
+ * Lcg64(seed) uniforms (rng.hpp:17-25), `passes` box means of radius `radius`
+ * over the clipped (2r+1)^3 window, the ceil(vf M) largest -> 1 with ties by
+ * lower index (rng.cpp:39-51). Bit-identical to inputs.box_filter_design. */
+typedef struct {
+  double vf;
+  uint64_t seed;
+  int passes;
+  int radius;
+} tmg_design_gen;
+
+/* Generates the design on the device (every rank of a partitioned solve
+ * generates the whole field and keeps its slab), then as tmg_set_design.
+ * rho_out (nullable): the whole design, x-fastest, on the host. */
+int tmg_set_design_generated(tmg_ctx* ctx, const tmg_design_gen* gen, double kappa_lo,
+                             double kappa_hi, int p, const tmg_patch* patches, int npatch,
+                             double* rho_out);
+
 int tmg_set_design(tmg_ctx* ctx, const double* rho, double kappa_lo, double kappa_hi, int p,
                    const tmg_patch* patches, int npatches);
 /* interpolate_design (grid.cpp:220-241) on the device: piecewise-constant

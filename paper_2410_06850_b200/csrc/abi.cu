@@ -1076,6 +1076,47 @@ int tmg_set_conductivity(tmg_ctx* c, const double* kappa, const tmg_patch* patch
   return finish_problem(c);
 }
 
+int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, double hi, int p,
+                             const tmg_patch* patches, int np, double* rho_out) {
+  if (!c || !gen) return set_err(c, TMG_EARG, "tmg_set_design_generated: null argument");
+  if (!(lo > 0.0) || !(hi > lo))  // material.cpp:11-12
+    return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
+  if (p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
+  if (!(gen->vf >= 0.0 && gen->vf <= 1.0) || gen->passes < 0 || gen->radius < 0)
+    return set_err(c, TMG_ECONFIG, "design generator: need 0 <= vf <= 1, passes, radius >= 0");
+  int rc = validate_patches(c, patches, np);
+  if (rc) return rc;
+  c->patches.clear();
+  for (int i = 0; i < np; ++i)
+    c->patches.push_back(Patch{patches[i].face, patches[i].u0, patches[i].v0, patches[i].u1,
+                               patches[i].v1, patches[i].value});
+  rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    const tmg_grid& G = c->grid;
+    const int64_t m = G.nx * G.ny * G.nz;  // the whole design (every rank generates it)
+    double* rho = dalloc<double>(c, m);
+    double* f = dalloc<double>(c, m);
+    double* scratch = dalloc<double>(c, (int64_t)(gen_scratch_bytes(m) / sizeof(double)) + 1);
+    launch_box_filter_design(G.nx, G.ny, G.nz, gen->vf, gen->seed, gen->passes, gen->radius, rho,
+                             f, scratch, c->stream);
+    CK(cudaGetLastError());
+    for (Slab& s : c->slabs) {
+      launch_to_brick(s.g, c->cb, rho + s.xoff, s.r, c->stream);
+      launch_conductivity(s.g, c->cb, s.r, s.kappa, lo, hi, p, c->stream);
+      CK(cudaGetLastError());
+    }
+    if (rho_out)
+      CK(cudaMemcpyAsync(rho_out, rho, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost,
+                         c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, rho);
+    dfree(c, f);
+    dfree(c, scratch);
+  });
+  if (rc) return rc;
+  return finish_problem(c);
+}
+
 int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,
                    const tmg_patch* patches, int np) {
   if (!c || !rho) return set_err(c, TMG_EARG, "tmg_set_design: null argument");

@@ -1,0 +1,221 @@
+// Seeded synthetic designs on the device (§8(d)
+// "Synthetic inputs"): bit-identical to paper_2410_06850_b200/inputs.py
+// box_filter_design and the oracle's orc_box_filter_design.
+//   1. u_i = Lcg64(seed).next_uniform(), i = 0..M-1 (rng.hpp:17-25), by
+//      jump-ahead: state_{i+1} = a^{i+1} seed + c (a^i + ... + 1) mod 2^64;
+//   2. `passes` box means of radius r over the clipped (2r+1)^3 window:
+//      window sums along x, then y, then z, each accumulated from 0 in
+//      increasing offset order, then divided by (count_x count_y) count_z;
+//   3. the ceil(vf M) largest values -> 1, ties by lower index (rng.cpp:39-51):
+//      an MSB-first 8-bit radix select of the (order-preserving) bit patterns
+//      of the nonnegative values, then a block-ordered prefix count of the
+//      values equal to the threshold.
+// Host-side generation at 512^3 takes ~37 s; this path is HBM-bound.
+#include "kernels.h"
+
+namespace tmg {
+
+namespace {
+constexpr uint64_t kLcgA = 6364136223846793005ULL, kLcgC = 1442695040888963407ULL;
+constexpr int kGenThreads = 256;
+
+// (A, C) with state_e = A seed + C after e steps
+__device__ __forceinline__ void lcg_jump(uint64_t e, uint64_t& A, uint64_t& C) {
+  uint64_t ra = 1, rc = 0, pa = kLcgA, pc = kLcgC;  // result, power-of-two step
+  while (e) {
+    if (e & 1) {  // apply step (pa, pc) after the current result
+      rc = pa * rc + pc;
+      ra = pa * ra;
+    }
+    pc = pa * pc + pc;  // compose the step with itself
+    pa = pa * pa;
+    e >>= 1;
+  }
+  A = ra;
+  C = rc;
+}
+}  // namespace
+
+// each thread: G consecutive uniforms
+__global__ void k_lcg_uniforms(double* out, int64_t n, uint64_t seed, int G) {
+  const int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * G;
+  if (i0 >= n) return;
+  uint64_t A, C;
+  lcg_jump((uint64_t)i0, A, C);
+  uint64_t st = A * seed + C;  // state after i0 steps
+  for (int g = 0; g < G && i0 + g < n; ++g) {
+    st = kLcgA * st + kLcgC;
+    out[i0 + g] = (double)(st >> 11) * 0x1.0p-53;
+  }
+}
+
+// out = window sum of in along `axis` (0 = x), radius r; with denom, out /=
+// (cx cy) cz of the clipped window (the last axis of a pass)
+__global__ void k_window_sum(const double* __restrict__ in, double* out, int64_t nx, int64_t ny,
+                             int64_t nz, int axis, int r, int divide) {
+  const int64_t m = nx * ny * nz;
+  const int64_t stride = axis == 0 ? 1 : axis == 1 ? nx : nx * ny;
+  const int64_t na = axis == 0 ? nx : axis == 1 ? ny : nz;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = s % nx, j = (s / nx) % ny, k = s / (nx * ny);
+    const int64_t a = axis == 0 ? i : axis == 1 ? j : k;
+    double acc = 0.0;
+    for (int d = -r; d <= r; ++d) {
+      const int64_t b = a + d;
+      if (b < 0 || b >= na) continue;
+      acc += in[s + d * stride];
+    }
+    if (divide) {
+      auto cnt = [r](int64_t c, int64_t n) {
+        const int64_t lo = c - r < 0 ? 0 : c - r, hi = c + r > n - 1 ? n - 1 : c + r;
+        return (double)(hi - lo + 1);
+      };
+      acc = acc / ((cnt(i, nx) * cnt(j, ny)) * cnt(k, nz));
+    }
+    out[s] = acc;
+  }
+}
+
+// radix select: histogram of the digit at `shift` over keys matching prefix
+__global__ void k_radix_hist(const double* __restrict__ f, int64_t m, const uint64_t* sel,
+                             int shift, unsigned long long* hist) {
+  __shared__ unsigned int h[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const uint64_t prefix = sel[0], mask = sel[1];
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = (uint64_t)__double_as_longlong(f[s]);
+    if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (h[b]) atomicAdd(&hist[b], (unsigned long long)h[b]);
+}
+
+// walk the bins from the largest digit; sel = {prefix, mask, k (rank still
+// to take among the keys matching the prefix)}
+__global__ void k_radix_pick(unsigned long long* hist, uint64_t* sel, int shift) {
+  if (threadIdx.x != 0) return;
+  uint64_t k = sel[2], cum = 0;
+  for (int b = 255; b >= 0; --b) {
+    const uint64_t h = hist[b];
+    if (cum + h >= k) {
+      sel[0] |= (uint64_t)b << shift;
+      sel[1] |= (uint64_t)255 << shift;
+      sel[2] = k - cum;
+      break;
+    }
+    cum += h;
+  }
+  for (int b = 0; b < 256; ++b) hist[b] = 0;
+}
+
+// rho = key > threshold; per-chunk counts of keys equal to it
+__global__ void k_mark_greater(const double* __restrict__ f, int64_t m, const uint64_t* sel,
+                               int64_t chunk, double* rho, unsigned long long* eq_count) {
+  __shared__ unsigned int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const uint64_t thr = sel[0];
+  const int64_t a = blockIdx.x * chunk, b = a + chunk < m ? a + chunk : m;
+  unsigned int mine = 0;
+  for (int64_t s = a + threadIdx.x; s < b; s += blockDim.x) {
+    const uint64_t key = (uint64_t)__double_as_longlong(f[s]);
+    rho[s] = key > thr ? 1.0 : 0.0;
+    mine += key == thr;
+  }
+  if (mine) atomicAdd(&cnt, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) eq_count[blockIdx.x] = cnt;
+}
+
+__global__ void k_exclusive_scan(unsigned long long* v, int n) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long s = 0;
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long t = v[i];
+    v[i] = s;
+    s += t;
+  }
+}
+
+// the first k' keys equal to the threshold (lowest indices) -> 1
+__global__ void k_mark_equal(const double* __restrict__ f, int64_t m, const uint64_t* sel,
+                             int64_t chunk, const unsigned long long* eq_base, double* rho) {
+  __shared__ unsigned int wsum[kGenThreads / 32];
+  __shared__ unsigned long long base;
+  const uint64_t thr = sel[0], take = sel[2];
+  if (threadIdx.x == 0) base = eq_base[blockIdx.x];
+  __syncthreads();
+  if (base >= take) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t a = blockIdx.x * chunk, b = a + chunk < m ? a + chunk : m;
+  for (int64_t t0 = a; t0 < b; t0 += blockDim.x) {
+    const int64_t s = t0 + threadIdx.x;
+    const bool eq = s < b && (uint64_t)__double_as_longlong(f[s]) == thr;
+    const unsigned bal = __ballot_sync(0xffffffffu, eq);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    unsigned before = 0, total = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (i < w) before += wsum[i];
+      total += wsum[i];
+    }
+    const unsigned rank = before + __popc(bal & ((1u << lane) - 1u));
+    if (eq && base + rank < take) rho[s] = 1.0;
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    __syncthreads();
+  }
+}
+
+size_t gen_scratch_bytes(int64_t m) {
+  const int64_t chunks = (m + 65535) / 65536;
+  return sizeof(double) * (size_t)m + sizeof(unsigned long long) * (size_t)(256 + chunks) +
+         sizeof(uint64_t) * 4;
+}
+
+// rho (x-fastest, M = nx ny nz doubles) from the seeded generator; scratch of
+// gen_scratch_bytes(M); f is a second M-double work array.
+void launch_box_filter_design(int64_t nx, int64_t ny, int64_t nz, double vf, uint64_t seed,
+                              int passes, int radius, double* rho, double* f, void* scratch,
+                              cudaStream_t s) {
+  const int64_t m = nx * ny * nz;
+  double* t = (double*)scratch;
+  unsigned long long* hist = (unsigned long long*)(t + m);
+  const int64_t chunk = 65536, chunks = (m + chunk - 1) / chunk;
+  unsigned long long* eq = hist + 256;
+  uint64_t* sel = (uint64_t*)(eq + chunks);
+  const int G = 16;
+  const int64_t nthreads = (m + G - 1) / G;
+  k_lcg_uniforms<<<(unsigned)((nthreads + kGenThreads - 1) / kGenThreads), kGenThreads, 0, s>>>(
+      f, m, seed, G);
+  int64_t gb = (m + kGenThreads - 1) / kGenThreads;
+  if (gb > 148 * 64) gb = 148 * 64;
+  for (int p = 0; p < passes; ++p) {
+    k_window_sum<<<(unsigned)gb, kGenThreads, 0, s>>>(f, t, nx, ny, nz, 0, radius, 0);
+    k_window_sum<<<(unsigned)gb, kGenThreads, 0, s>>>(t, rho, nx, ny, nz, 1, radius, 0);
+    k_window_sum<<<(unsigned)gb, kGenThreads, 0, s>>>(rho, f, nx, ny, nz, 2, radius, 1);
+  }
+  // solid = min(M, ceil(vf M)) largest (rng.cpp:39-51)
+  int64_t solid = (int64_t)ceil(vf * (double)m);
+  if (solid > m) solid = m;
+  if (solid <= 0) {
+    cudaMemsetAsync(rho, 0, sizeof(double) * (size_t)m, s);
+    return;
+  }
+  const uint64_t init[3] = {0, 0, (uint64_t)solid};
+  cudaMemcpyAsync(sel, init, sizeof init, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 256, s);
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    k_radix_hist<<<(unsigned)gb, kGenThreads, 0, s>>>(f, m, sel, shift, hist);
+    k_radix_pick<<<1, 32, 0, s>>>(hist, sel, shift);
+  }
+  k_mark_greater<<<(unsigned)chunks, kGenThreads, 0, s>>>(f, m, sel, chunk, rho, eq);
+  k_exclusive_scan<<<1, 32, 0, s>>>(eq, (int)chunks);
+  k_mark_equal<<<(unsigned)chunks, kGenThreads, 0, s>>>(f, m, sel, chunk, eq, rho);
+}
+
+}  // namespace tmg

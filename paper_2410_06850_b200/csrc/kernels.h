@@ -181,6 +181,11 @@ void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s);
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, int defer, cudaStream_t s);
+// seeded designs on the device (gen.cu)
+size_t gen_scratch_bytes(int64_t m);
+void launch_box_filter_design(int64_t nx, int64_t ny, int64_t nz, double vf, uint64_t seed,
+                              int passes, int radius, double* rho, double* f, void* scratch,
+                              cudaStream_t s);
 // design loop with MMA (optim.cu; MmaOptions, optim.hpp:27-32)
 struct MmaParams {
   double move, asy_init, asy_incr, asy_decr, xmin, xmax;

@@ -76,6 +76,11 @@ class _SimpReport(C.Structure):
                 ("ls2_seconds", C.c_double), ("step_seconds", C.c_double)]
 
 
+class _DesignGen(C.Structure):
+    _fields_ = [("vf", C.c_double), ("seed", C.c_uint64), ("passes", C.c_int),
+                ("radius", C.c_int)]
+
+
 class _OptimOpts(C.Structure):
     _fields_ = [("vstar", C.c_double), ("move_limit", C.c_double), ("asy_init", C.c_double),
                 ("asy_incr", C.c_double), ("asy_decr", C.c_double), ("kappa_lo", C.c_double),
@@ -123,6 +128,7 @@ EXPORTED_SYMBOLS = (
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
     "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
+    "tmg_set_design_generated",
 )
 
 
@@ -326,6 +332,19 @@ class Context:
         parr, n = boundary._c()
         self._check(native().tmg_set_design(self._p, _ptr(r), C.c_double(kappa_lo),
                                             C.c_double(kappa_hi), C.c_int(p), parr, C.c_int(n)))
+
+    def set_design_generated(self, vf, kappa_lo, kappa_hi=1.0, p=3,
+                             boundary: BoundarySpec = None, seed=20240501, passes=3, radius=2,
+                             return_rho=False):
+        """inputs.box_filter_design generated on the device (bit-identical),
+        then as set_design. Returns the whole design (x-fastest) if asked."""
+        g = _DesignGen(vf, seed, passes, radius)
+        parr, n = boundary._c()
+        rho = np.empty(self.grid.num_cells()) if return_rho else None
+        self._check(native().tmg_set_design_generated(
+            self._p, C.byref(g), C.c_double(kappa_lo), C.c_double(kappa_hi), C.c_int(p), parr,
+            C.c_int(n), _ptr(rho) if rho is not None else None))
+        return rho
 
     def set_design_interpolated(self, rho_lo, shape_lo, kappa_lo, kappa_hi=1.0, p=3,
                                 boundary: BoundarySpec = None):
