@@ -20,7 +20,7 @@ CC=/usr/bin/gcc
 # x86-64-v2: portable to the GPU box host; no FMA contraction (matches the
 # oracle restatement's rounding of dot products).
 FLAGS="-O2 -march=x86-64-v2 -fPIC -pthread"
-SRCS="grid material fvm sparse solver coarse_space parallel rng optim"
+SRCS="grid material fvm sparse solver coarse_space parallel rng optim io"
 pids=()
 for s in $SRCS; do
   $CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$REF/src/$s.cpp" -o "$OUT/obj/$s.o" &

@@ -16,6 +16,7 @@
 #include "topmg/coarse_space.hpp"
 #include "topmg/fvm.hpp"
 #include "topmg/grid.hpp"
+#include "topmg/io.hpp"
 #include "topmg/material.hpp"
 #include "topmg/optim.hpp"
 #include "topmg/parallel.hpp"
@@ -326,6 +327,53 @@ int ref_optimize(int nlev, const int64_t* n_levels, const int* iters, int64_t nc
     std::copy(r.design.values.begin(), r.design.values.end(), x_out);
     *final_cost = r.final_cost;
     *failed = r.failed ? 1 : 0;
+  });
+}
+
+// io.cpp writers, for byte comparisons with paper_2410_06850_b200/io.py
+int ref_write_vtk(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                  const double* field, const char* name, const char* path) {
+  return guarded([&] {
+    const GridSpec g(nx, ny, nz, lx, ly, lz);
+    write_vtk_cell_scalars(g, std::vector<double>(field, field + g.num_cells()), name, path);
+  });
+}
+
+int ref_write_trajectory(int n, const int* level, const int* iter, const double* cost,
+                         const double* volume, const int* ls1, const int* ls2,
+                         const double* setup, const double* t1, const double* t2,
+                         const char* traj_path, const char* timings_path) {
+  return guarded([&] {
+    std::vector<IterationLog> rows(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      rows[i].level = level[i];
+      rows[i].iter = iter[i];
+      rows[i].cost = cost[i];
+      rows[i].volume = volume[i];
+      rows[i].ls1_iters = ls1[i];
+      rows[i].ls2_iters = ls2[i];
+      rows[i].setup_seconds = setup[i];
+      rows[i].ls1_seconds = t1[i];
+      rows[i].ls2_seconds = t2[i];
+    }
+    write_trajectory_csv(rows, traj_path);
+    write_timings_csv(rows, timings_path);
+  });
+}
+
+int ref_write_bench(int n, const char* const* phase, const char* const* prec, const int* cr,
+                    const int64_t* dof, const int* iters, const double* secs, const char* path) {
+  return guarded([&] {
+    std::vector<BenchRow> rows(static_cast<std::size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      rows[i].phase = phase[i];
+      rows[i].preconditioner = prec[i];
+      rows[i].cr = cr[i];
+      rows[i].dof = dof[i];
+      rows[i].iterations = iters[i];
+      rows[i].seconds = secs[i];
+    }
+    write_bench_csv(rows, path);
   });
 }
 
