@@ -134,3 +134,29 @@ def test_nccl_transport_single_rank():
     assert out["0"][0] == out["1"][0]
     np.testing.assert_allclose(out["1"][1], out["0"][1], rtol=1e-9)
     np.testing.assert_allclose(out["1"][2], out["0"][2], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind,fine", [("block_jacobi", None), ("two_grid", "coarse_cell"),
+                                       ("mmg", "cc"), ("two_grid", "cc")])
+@pytest.mark.parametrize("n,ncc,sd,slabs", [(32, 2, 2, 2), (64, 4, 2, 4)])
+def test_slab_variants_match_single(kind, fine, n, ncc, sd, slabs):
+    """block_jacobi, two_grid and the reference's cc-element fine blocks on
+    slabs (the blocks are whole cc elements, never straddling a slab)."""
+    from paper_2410_06850_b200 import MmgOptions
+    kappa = _problem(n, 1e-3)
+    opts = MmgOptions(fine_blocks=fine) if fine else MmgOptions()
+    ctxs = []
+    for s in (1, slabs):
+        c = Context(GridSpec(n, n, n), ncc, sd, slabs=s)
+        c.set_conductivity(kappa, PATCH)
+        c.setup(kind, opts)
+        ctxs.append(c)
+    a, b = ctxs
+    r = np.random.default_rng(5).standard_normal(n ** 3)
+    za, zb = a.apply_preconditioner(r), b.apply_preconditioner(r)
+    assert np.linalg.norm(za - zb) <= 1e-9 * np.linalg.norm(za)
+    rhs = a.assemble_rhs(np.ones(n ** 3))
+    ra, rb = a.pcg(rhs, rtol=1e-8, max_iterations=5000), b.pcg(rhs, rtol=1e-8, max_iterations=5000)
+    assert ra.report.converged and rb.report.converged
+    assert abs(ra.report.iterations - rb.report.iterations) <= max(1, ra.report.iterations // 50)
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
