@@ -3,11 +3,12 @@ design (vf 0.2, radius 4, 3 passes), kmin 1e-6, MMG-PCG to rtol 1e-8.
 
 Hierarchy: c = n / (ncc sd) cells per coarse cell, L_c = 4. Defaults: sd = 4,
 ncc = n / 32 (c = 8, q = sd^3 L_c = 256: the large-element coarse level of
-coarse_large.cu) and L_cc = 8, so n_cc = 8 ncc^3 (32768 at 512^3: the dense
-A_cc^-1 takes 8.6 GB). SURVEY.md suggests sd = 8 / ncc = 8 (q = 2048), which
+coarse_large.cu) and L_cc = 12, so n_cc = 12 ncc^3 (49152 at 512^3: the
+dense A_cc^-1 takes 19 GB). At 512^3, L_cc = 8 needs 372 iterations and
+L_cc = 12 needs 49 (profiles/r05_config3_512*.json). SURVEY.md suggests sd = 8 / ncc = 8 (q = 2048), which
 needs a block-sparse coarse level.
 
-    python tools/config3.py [--n 512] [--ncc 16] [--sd 4] [--lcc 8] [--solves 2] [--out f.json]
+    python tools/config3.py [--n 512] [--ncc 16] [--sd 4] [--lcc 12] [--solves 2] [--out f.json]
 """
 import argparse
 import json
@@ -23,7 +24,7 @@ from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, i
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=512)
-ap.add_argument("--lcc", type=int, default=8)
+ap.add_argument("--lcc", type=int, default=12)
 ap.add_argument("--sd", type=int, default=4)
 ap.add_argument("--ncc", type=int, default=0)
 ap.add_argument("--solves", type=int, default=2)
