@@ -1630,8 +1630,8 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       return set_err(c, TMG_EARG, "num_cc_basis must be >= 1");
     if (kind == TMG_PRECOND_MMG && q > 64 && !coarse_large_supported((int)q, (int)o->num_cc_basis))
       return set_err(c, TMG_ENOTSUP,
-                     "GPU coarse level handles sd^3*L_c <= 64, or a multiple of 64 up to 256 with "
-                     "num_cc_basis <= 12 (got %lld, %lld)",
+                     "GPU coarse level handles sd^3*L_c <= 64, or a multiple of 64 up to 4096 with "
+                     "num_cc_basis <= 20 (got %lld, %lld)",
                      (long long)q, (long long)o->num_cc_basis);
     if (o->smoother_sweeps != 1)
       return set_err(c, TMG_ENOTSUP, "GPU smoother is built for smoother_sweeps = 1");
@@ -1735,12 +1735,19 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         cc_iters = dalloc<int>(c, 1);
         CK(cudaMemsetAsync(cc_iters, 0, sizeof(int), c->stream));
       }
+      double* large_work = nullptr;
+      if (q > 64) {
+        int64_t wd = 0;
+        for (Slab& s : c->slabs)
+          wd = std::max(wd, coarse_large_work_doubles((int)q, s.g.neo, lcc));
+        if (wd) large_work = dalloc<double>(c, wd);
+      }
       for (Slab& s : c->slabs) {
         if (kind == TMG_PRECOND_TWO_GRID) launch_cc_identity(s.g, s.Rcc, s.cc_evals, c->stream);
         else if (q <= 64) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
         else  // Winv's storage holds the shifted inverses until the smoother overwrites it
-          launch_cc_basis_large(s.g, s.Ac, s.Bc, s.Winv, s.Rcc, s.cc_evals, s.d_status + 3,
-                                cc_iters, 1e-12, 100, c->stream);
+          launch_cc_basis_large(s.g, s.Ac, s.Bc, s.Winv, large_work, s.Rcc, s.cc_evals,
+                                s.d_status + 3, cc_iters, 1e-12, 100, c->stream);
       }
       if (cc_iters) {
         int it = 0;
@@ -1754,8 +1761,9 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       mark("cc_basis");
       for (Slab& s : c->slabs) {
         if (q <= 64) launch_coarse_smoother(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
-        else launch_coarse_smoother_large(s.g, s.Ac, s.Winv, s.d_status + 1, c->stream);
+        else launch_coarse_smoother_large(s.g, s.Ac, s.Winv, large_work, s.d_status + 1, c->stream);
       }
+      dfree_null(c, large_work);
       CK(cudaGetLastError());
       mark("coarse_smoother");
       for (Slab& s : c->slabs) {

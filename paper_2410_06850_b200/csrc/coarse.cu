@@ -642,7 +642,7 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
                          cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
-  const int nt = (q + 31) / 32 * 32;
+  const int nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   const int nc = (int)(g.nbo * LC);
   const size_t sm = sizeof(double) * (size_t)q;
   const double* nul = nullptr;
@@ -660,20 +660,20 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
 // and the A_cc row-block GEMV go between them).
 void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
                           const double* in, const double* add, double* out, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
              done, Winv, in, add, out);
 }
 void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
                             const double* Rcc, const double* rc, const double* rc0, double* rcc,
                             cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_restrict, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
              done, Ac, Rcc, rc, rc0, rcc);
 }
 void launch_coarse_prolong(const GridParams& g, const int* done, const double* Rcc,
                            const double* rc0, const double* ecc, double* rc1, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q + 31) / 32 * 32;
+  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_prolong, dim3((unsigned)g.neo), dim3(nt), 0, s, g, done, Rcc, rc0, ecc, rc1);
 }
 void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac, const double* rc,

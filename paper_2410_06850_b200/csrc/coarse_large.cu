@@ -13,7 +13,6 @@ namespace tmg {
 namespace {
 constexpr int GB = kGjBlock;
 constexpr int GJT = kGjThreads;
-constexpr int KS = 16;        // subspace width of the cc eigensolver (L_cc <= KS - 4)
 
 __device__ __forceinline__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -122,39 +121,38 @@ __device__ __forceinline__ double hash_unit(uint32_t x) {
   return (double)x * (1.0 / 4294967296.0) - 0.5;
 }
 
+// sum over the block of one value per thread (every thread gets the total)
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
 // Block-wide cyclic Jacobi on the K x K symmetric M (smem): round-robin
-// ordering, K/2 disjoint rotations per round, one thread per (row, pair)
-// update; V (K x K) collects the eigenvectors in its columns. blockDim >= K^2.
+// ordering, K/2 disjoint rotations per round, the (row, pair) updates spread
+// over the block; V (K x K) collects the eigenvectors in its columns.
 template <int K>
 __device__ void block_jacobi(double* M, double* V, double* red) {
   constexpr int NP = K / 2;
   __shared__ double rc[NP], rs[NP];
   __shared__ int rp[NP], rq[NP];
-  const int t = threadIdx.x;
-  if (t < K * K) V[t] = (t / K == t % K) ? 1.0 : 0.0;
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int e = t; e < K * K; e += nt) V[e] = (e / K == e % K) ? 1.0 : 0.0;
   __syncthreads();
   for (int sweep = 0; sweep < 30; ++sweep) {
     double tot = 0.0, off = 0.0;
-    if (t < K * K) {
-      tot = M[t] * M[t];
-      off = (t / K != t % K) ? tot : 0.0;
+    for (int e = t; e < K * K; e += nt) {
+      const double v = M[e] * M[e];
+      tot += v;
+      if (e / K != e % K) off += v;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      off += __shfl_xor_sync(0xffffffffu, off, o);
-    }
-    if ((t & 31) == 0 && t < K * K) {
-      red[t >> 5] = tot;
-      red[16 + (t >> 5)] = off;
-    }
-    __syncthreads();
-    tot = 0.0;
-    off = 0.0;
-    for (int w = 0; w < K * K / 32; ++w) {
-      tot += red[w];
-      off += red[16 + w];
-    }
-    __syncthreads();
+    tot = block_sum(tot, red);
+    off = block_sum(off, red);
     if (off <= 1e-26 * tot || off == 0.0) break;
     for (int round = 0; round < K - 1; ++round) {
       if (t < NP) {  // circle method, player K-1 fixed
@@ -179,8 +177,8 @@ __device__ void block_jacobi(double* M, double* V, double* red) {
         rq[t] = qq;
       }
       __syncthreads();
-      if (t < K * NP) {  // columns p, q of row r
-        const int r = t / NP, gq = t % NP, p = rp[gq], qq = rq[gq];
+      for (int e = t; e < K * NP; e += nt) {  // columns p, q of row r
+        const int r = e / NP, gq = e % NP, p = rp[gq], qq = rq[gq];
         const double c = rc[gq], sn = rs[gq];
         const double akp = M[r * K + p], akq = M[r * K + qq];
         M[r * K + p] = c * akp - sn * akq;
@@ -190,8 +188,8 @@ __device__ void block_jacobi(double* M, double* V, double* red) {
         V[r * K + qq] = sn * vkp + c * vkq;
       }
       __syncthreads();
-      if (t < K * NP) {  // rows p, q at column col
-        const int gq = t / K, col = t % K, p = rp[gq], qq = rq[gq];
+      for (int e = t; e < K * NP; e += nt) {  // rows p, q at column col
+        const int gq = e / K, col = e % K, p = rp[gq], qq = rq[gq];
         const double c = rc[gq], sn = rs[gq];
         const double apk = M[p * K + col], aqk = M[qq * K + col];
         M[p * K + col] = c * apk - sn * aqk;
@@ -202,26 +200,37 @@ __device__ void block_jacobi(double* M, double* V, double* red) {
   }
 }
 
+// Gram entries T[i][j] = sum_r A[r][i] B[r][j] (q x KS row-major A, B),
+// (i, j) pairs spread over the block; sym: 0.5 (A^T B + B^T A)
+template <int KS>
+__device__ void gram(const double* A, const double* B, int q, double* T, bool sym) {
+  for (int e = threadIdx.x; e < KS * KS; e += blockDim.x) {
+    const int i = e / KS, j = e % KS;
+    double s = 0.0, s2 = 0.0;
+    for (int r = 0; r < q; ++r) {
+      s = fma(A[r * KS + i], B[r * KS + j], s);
+      if (sym) s2 = fma(A[r * KS + j], B[r * KS + i], s2);
+    }
+    T[e] = sym ? 0.5 * (s + s2) : s;
+  }
+  __syncthreads();
+}
+
 // X = orthonormal basis of span(Y) (q x KS, row-major): scaled Gram matrix,
-// its eigendecomposition (warp Jacobi), X = Y D W Lambda^-1/2.
+// its eigendecomposition, X = Y D W Lambda^-1/2.
+template <int KS>
 __device__ void svqb_pass(const double* Y, double* X, int q, double* T, double* V, double* F,
                           double* dsc, double* red) {
   const int t = threadIdx.x;
-  if (t < KS * KS) {
-    const int i = t / KS, j = t % KS;
-    double s = 0.0;
-    for (int r = 0; r < q; ++r) s = fma(Y[r * KS + i], Y[r * KS + j], s);
-    T[t] = s;
-  }
+  gram<KS>(Y, Y, q, T, false);
+  for (int k = t; k < KS; k += blockDim.x) dsc[k] = rsqrt(fmax(T[k * KS + k], 1e-300));
   __syncthreads();
-  if (t < KS) dsc[t] = rsqrt(fmax(T[t * KS + t], 1e-300));
-  __syncthreads();
-  if (t < KS * KS) T[t] *= dsc[t / KS] * dsc[t % KS];
+  for (int e = t; e < KS * KS; e += blockDim.x) T[e] *= dsc[e / KS] * dsc[e % KS];
   __syncthreads();
   block_jacobi<KS>(T, V, red);
-  if (t < KS * KS) {
-    const int i = t / KS, j = t % KS;
-    F[t] = dsc[i] * V[i * KS + j] * rsqrt(fmax(T[j * KS + j], 1e-24));
+  for (int e = t; e < KS * KS; e += blockDim.x) {
+    const int i = e / KS, j = e % KS;
+    F[e] = dsc[i] * V[i * KS + j] * rsqrt(fmax(T[j * KS + j], 1e-24));
   }
   __syncthreads();
   for (int r = t; r < q; r += blockDim.x) {
@@ -240,6 +249,7 @@ __device__ void svqb_pass(const double* Y, double* X, int q, double* T, double* 
 }
 
 // Z = H X with H = (A_c - Bc on the diagonal blocks) restricted to E's children.
+template <int KS>
 __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const double* Ac,
                                 const double* Bc, const double* X, double* Z, int q) {
   for (int r = threadIdx.x; r < q; r += blockDim.x) {
@@ -270,58 +280,53 @@ __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const 
 }
 }  // namespace
 
+// One CTA (256 threads) per element. X, Y, Z (q x KS each) in shared memory,
+// or in gscr (3 q KS doubles per element) when they do not fit (q > 256).
+template <int KS>
 __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double* __restrict__ Ac,
                                                      const double* __restrict__ Bc,
                                                      const double* __restrict__ Hs, double tol,
                                                      int maxit, double* Rcc, double* cc_evals,
-                                                     int* iters) {
+                                                     int* iters, double* gscr) {
   extern __shared__ __align__(16) double sms[];
-  const int q = g.sd * g.sd * g.sd * LC, t = threadIdx.x;
-  double* X = sms;
-  double* Y = X + q * KS;
-  double* Z = Y + q * KS;
-  double* T = Z + q * KS;
+  const int q = g.sd * g.sd * g.sd * LC, t = threadIdx.x, nt = blockDim.x;
+  double* T = sms;
   double* V = T + KS * KS;
   double* F = V + KS * KS;
   double* dsc = F + KS * KS;
   double* th = dsc + KS;
   double* res = th + KS;
+  double* vec = gscr ? gscr + (size_t)blockIdx.x * 3 * q * KS : res + KS;
+  double* X = vec;
+  double* Y = X + q * KS;
+  double* Z = Y + q * KS;
   __shared__ int perm[KS];
   __shared__ int flag;
   __shared__ double red[32];
   const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   const double* H = Hs + (int64_t)blockIdx.x * q * q;
   double hd = 0.0;
-  for (int r = t; r < q; r += blockDim.x) {
+  for (int r = t; r < q; r += nt) {
     const int64_t I = child_brick(g, ec, r / LC);
     const int a = r % LC;
     hd = fmax(hd, Ac[I * 7 * LC * LC + a * (LC + 1)] - Bc[I * LC * LC + a * (LC + 1)]);
   }
   const double thr = tol * block_max(hd, red);
   // start: the constant vector and hashed columns
-  for (int e = t; e < q * KS; e += blockDim.x) {
+  for (int e = t; e < q * KS; e += nt) {
     const int r = e / KS, k = e % KS;
     Y[e] = k == 0 ? 1.0 : hash_unit((uint32_t)(r * KS + k + 1));
   }
   __syncthreads();
   int it = 0;
   for (;; ++it) {
-    svqb_pass(Y, X, q, T, V, F, dsc, red);
-    svqb_pass(X, Y, q, T, V, F, dsc, red);
+    svqb_pass<KS>(Y, X, q, T, V, F, dsc, red);
+    svqb_pass<KS>(X, Y, q, T, V, F, dsc, red);
     { double* tmp = X; X = Y; Y = tmp; }
     // Rayleigh-Ritz on H
-    apply_projected(g, ec, Ac, Bc, X, Z, q);
+    apply_projected<KS>(g, ec, Ac, Bc, X, Z, q);
     __syncthreads();
-    if (t < KS * KS) {
-      const int i = t / KS, j = t % KS;
-      double s = 0.0, s2 = 0.0;
-      for (int r = 0; r < q; ++r) {
-        s = fma(X[r * KS + i], Z[r * KS + j], s);
-        s2 = fma(X[r * KS + j], Z[r * KS + i], s2);
-      }
-      T[t] = 0.5 * (s + s2);
-    }
-    __syncthreads();
+    gram<KS>(X, Z, q, T, true);
     block_jacobi<KS>(T, V, red);
     if (t == 0) {  // ascending, ties by index
       unsigned used = 0;
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
       }
     }
     __syncthreads();
-    for (int r = t; r < q; r += blockDim.x) {
+    for (int r = t; r < q; r += nt) {
       double xr[KS], zr[KS];
 #pragma unroll
       for (int i = 0; i < KS; ++i) {
@@ -356,8 +361,9 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
       }
     }
     __syncthreads();
-    {  // residual norms of the wanted pairs: 16 lanes per column
-      const int k = t >> 4, part = t & 15;
+    // residual norms of the wanted pairs: 16 lanes per column
+    for (int k0 = 0; k0 < KS; k0 += nt >> 4) {
+      const int k = k0 + (t >> 4), part = t & 15;
       double s = 0.0;
       if (k < KS)
         for (int r = part; r < q; r += 16) {
@@ -376,7 +382,7 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
     __syncthreads();
     if (flag || it + 1 >= maxit) break;
     // Y = Hs X (Hs symmetric: column r read coalesced)
-    for (int r = t; r < q; r += blockDim.x) {
+    for (int r = t; r < q; r += nt) {
       double acc[KS];
 #pragma unroll
       for (int k = 0; k < KS; ++k) acc[k] = 0.0;
@@ -395,50 +401,87 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
     }
     __syncthreads();
   }
-  if (t < g.lcc) {
+  for (int k = t; k < g.lcc; k += nt) {
     double s = 0.0;
-    for (int r = 0; r < q; ++r) s += X[r * KS + t];
-    dsc[t] = s < 0.0 ? -1.0 : 1.0;
-    cc_evals[ec.e * g.lcc + t] = th[t];
+    for (int r = 0; r < q; ++r) s += X[r * KS + k];
+    dsc[k] = s < 0.0 ? -1.0 : 1.0;
+    cc_evals[ec.e * g.lcc + k] = th[k];
   }
   __syncthreads();
-  for (int e = t; e < g.lcc * q; e += blockDim.x) {
+  for (int e = t; e < g.lcc * q; e += nt) {
     const int k = e / q, r = e % q;
     Rcc[(ec.e * g.lcc + k) * q + r] = dsc[k] * X[r * KS + k];
   }
   if (t == 0 && iters) atomicMax(iters, it + 1);
 }
 
+// q <= 256: one CTA per element (k_batched_gj); larger q (sd = 8: 2048) with
+// the tensor-core blocked Gauss-Jordan batched over the elements (dense.cu).
+// L_cc <= 12: 16 subspace columns, <= 20: 24.
 bool coarse_large_supported(int q, int lcc) {
-  return q > 64 && q % GB == 0 && q <= GJT && lcc <= KS - 4;
+  return q > 64 && q % GB == 0 && q <= 4096 && lcc <= 20;
+}
+
+static int subspace_width(int lcc) { return lcc <= 12 ? 16 : 24; }
+
+static bool subspace_in_smem(int q, int ks) { return q <= 256 && 3 * q * ks * 8 <= 160 * 1024; }
+
+// scratch doubles the large-q set-up needs besides Winv's storage
+int64_t coarse_large_work_doubles(int q, int64_t neo, int lcc) {
+  if (q <= 256 && subspace_in_smem(q, subspace_width(lcc))) return 0;
+  const int64_t inv = q > 256 ? neo * dense_inverse_work_doubles(q) : 0;
+  const int64_t sub = neo * 3 * (int64_t)q * subspace_width(lcc);
+  return inv > sub ? inv : sub;
 }
 
 size_t batched_gj_smem(int q) { return gj_global_smem_bytes(q); }
 
+static void invert_elements(double* A, int q, int64_t neo, double* work, int* status,
+                            cudaStream_t s) {
+  if (q <= GJT) {
+    const size_t smem = batched_gj_smem(q);
+    cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_batched_gj<<<(unsigned)neo, GJT, smem, s>>>(A, q, status);
+  } else {
+    dense_spd_inverse_batched(A, q, neo, work, status, s);
+  }
+}
+
 // Winv of every owned cc element (coarse_blocks_by_cc smoother) for large q.
 void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
-                                  int* status, cudaStream_t s) {
+                                  double* work, int* status, cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
   k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, nullptr, 0.0, Winv + g.e0 * q * q);
-  const size_t smem = batched_gj_smem(q);
-  cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_batched_gj<<<(unsigned)g.neo, GJT, smem, s>>>(Winv + g.e0 * q * q, q, status);
+  invert_elements(Winv + g.e0 * q * q, q, g.neo, work, status, s);
+}
+
+template <int KS>
+static void launch_subspace(const GridParams& g, const double* Ac, const double* Bc,
+                            const double* Hs, double tol, int maxit, double* Rcc, double* cc_evals,
+                            int* iters, double* work, cudaStream_t s) {
+  const int q = g.sd * g.sd * g.sd * LC;
+  const bool in_smem = subspace_in_smem(q, KS);
+  const size_t sm2 = sizeof(double) * (size_t)((in_smem ? 3 * q * KS : 0) + 3 * KS * KS + 3 * KS);
+  cudaFuncSetAttribute(k_cc_subspace<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  k_cc_subspace<KS><<<(unsigned)g.neo, 256, sm2, s>>>(g, Ac, Bc, Hs, tol, maxit, Rcc, cc_evals,
+                                                      iters, in_smem ? nullptr : work);
 }
 
 // R_cc rows and cc eigenvalues of every owned cc element for large q; scratch
-// holds the shifted inverses (neo q^2 doubles, virtual-global like Winv).
+// holds the shifted inverses (neo q^2 doubles, virtual-global like Winv),
+// work coarse_large_work_doubles().
 void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* Bc,
-                           double* scratch, double* Rcc, double* cc_evals, int* scratch_status,
-                           int* iters, double tol, int maxit, cudaStream_t s) {
+                           double* scratch, double* work, double* Rcc, double* cc_evals,
+                           int* scratch_status, int* iters, double tol, int maxit,
+                           cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
   double* Hs = scratch + g.e0 * q * q;
   k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, Bc, 1e-5, Hs);
-  const size_t smem = batched_gj_smem(q);
-  cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_batched_gj<<<(unsigned)g.neo, GJT, smem, s>>>(Hs, q, scratch_status);
-  const size_t sm2 = sizeof(double) * (size_t)(3 * q * KS + 3 * KS * KS + 3 * KS);
-  cudaFuncSetAttribute(k_cc_subspace, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-  k_cc_subspace<<<(unsigned)g.neo, 256, sm2, s>>>(g, Ac, Bc, Hs, tol, maxit, Rcc, cc_evals, iters);
+  invert_elements(Hs, q, g.neo, work, scratch_status, s);
+  if (subspace_width(g.lcc) == 16)
+    launch_subspace<16>(g, Ac, Bc, Hs, tol, maxit, Rcc, cc_evals, iters, work, s);
+  else
+    launch_subspace<24>(g, Ac, Bc, Hs, tol, maxit, Rcc, cc_evals, iters, work, s);
 }
 
 }  // namespace tmg

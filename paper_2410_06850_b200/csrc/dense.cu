@@ -25,9 +25,15 @@ constexpr int NB = 64;  // Gauss-Jordan pivot block
 // into Dinv and record the pivots: one CTA, register-resident Gauss-Jordan
 // (gj.cuh).
 constexpr int kDiagThreads = 256;
+// Batched calls (dense_spd_inverse_batched): matrix blockIdx.z at A + z sA,
+// its work (Dinv, Pn, Cold, pivots) at + z sW; single calls pass 0 strides.
 __global__ void __launch_bounds__(kDiagThreads) k_gj_diag(const double* __restrict__ A, int64_t n,
                                                           int64_t k0, int nbk, double* Dinv,
-                                                          double* pivots) {
+                                                          double* pivots, int64_t sA,
+                                                          int64_t sW) {
+  A += blockIdx.z * sA;
+  Dinv += blockIdx.z * sW;
+  pivots += blockIdx.z * sW;
   using L = GjLayout<NB, kDiagThreads>;
   constexpr int CW = L::CW, RH = L::RH;
   __shared__ GjSmem<NB> gjs;
@@ -62,7 +68,11 @@ __global__ void __launch_bounds__(kDiagThreads) k_gj_diag(const double* __restri
 __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A, int64_t n,
                                                    int64_t k0, int nbk,
                                                    const double* __restrict__ Dinv, double* Pn,
-                                                   double* Cold) {
+                                                   double* Cold, int64_t sA, int64_t sW) {
+  A += blockIdx.z * sA;
+  Dinv += blockIdx.z * sW;
+  Pn += blockIdx.z * sW;
+  Cold += blockIdx.z * sW;
   __shared__ double Ds[NB][NB];  // read as warp broadcasts
   __shared__ double As[NB][32];
   const int t = threadIdx.x, jx = t & 31, ry = t >> 5;
@@ -124,7 +134,11 @@ constexpr size_t kGemmSmem = sizeof(double) * (size_t)(GT * AS_LD + NB * BS_LD);
 
 __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
                                                     const double* __restrict__ Cold,
-                                                    const double* __restrict__ Pn) {
+                                                    const double* __restrict__ Pn, int64_t sA,
+                                                    int64_t sW) {
+  A += blockIdx.z * sA;
+  Cold += blockIdx.z * sW;
+  Pn += blockIdx.z * sW;
   extern __shared__ __align__(16) double smg[];
   double* As = smg;
   double* Bs = smg + GT * AS_LD;
@@ -203,7 +217,12 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
 __global__ void __launch_bounds__(256) k_gj_fix(double* A, int64_t n, int64_t k0, int nbk,
                                                 const double* __restrict__ Dinv,
                                                 const double* __restrict__ Pn,
-                                                const double* __restrict__ Cold) {
+                                                const double* __restrict__ Cold, int64_t sA,
+                                                int64_t sW) {
+  A += blockIdx.z * sA;
+  Dinv += blockIdx.z * sW;
+  Pn += blockIdx.z * sW;
+  Cold += blockIdx.z * sW;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * nbk) return;
   // rows: e -> (r, j); the lower triangle only (j < k0 + nbk)
@@ -225,14 +244,16 @@ __global__ void __launch_bounds__(256) k_gj_fix(double* A, int64_t n, int64_t k0
   }
 }
 
-__global__ void k_symmetrize(double* A, int64_t n) {
+__global__ void k_symmetrize(double* A, int64_t n, int64_t sA) {
+  A += blockIdx.z * sA;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= n * n) return;
   const int64_t i = e / n, j = e % n;
   if (i < j) A[i * n + j] = A[j * n + i];  // the sweeps kept the lower triangle
 }
 
-__global__ void k_pivot_check(const double* pivots, int64_t n, int* status) {
+__global__ void k_pivot_check(const double* pivots, int64_t n, int* status, int64_t sW) {
+  pivots += blockIdx.z * sW;
   __shared__ double red[32];
   double mx = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, fabs(pivots[i]));
@@ -358,23 +379,39 @@ void launch_symv(const int* done, const double* T, int64_t n, const double* x, d
   launch_pdl(k_symv_reduce, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, s, done, P, n, y);
 }
 
-void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s) {
-  // work: NB*NB (Dinv) + NB*n (Pn) + n*NB (Cold) + n (pivots)
+// work per matrix: NB*NB (Dinv) + NB*n (Pn) + n*NB (Cold) + n + NB (pivots)
+static void gj_inverse_impl(double* A, int64_t n, int64_t batch, int64_t sA, double* work,
+                            int64_t sW, int* status, cudaStream_t s) {
   double* Dinv = work;
   double* Pn = Dinv + NB * NB;
   double* Cold = Pn + (int64_t)NB * n;
   double* piv = Cold + n * NB;
+  const unsigned B = (unsigned)batch;
   cudaFuncSetAttribute(k_gj_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-  const dim3 grid((unsigned)((n + GN - 1) / GN), (unsigned)((n + GT - 1) / GT));
+  const dim3 grid((unsigned)((n + GN - 1) / GN), (unsigned)((n + GT - 1) / GT), B);
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
     const int nbk = (int)((n - k0) < NB ? (n - k0) : NB);
-    k_gj_diag<<<1, kDiagThreads, 0, s>>>(A, n, k0, nbk, Dinv, piv);
-    k_gj_panels<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
-    k_gj_gemm<<<grid, 256, kGemmSmem, s>>>(A, n, Cold, Pn);
-    k_gj_fix<<<(unsigned)((n * nbk + 255) / 256), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn, Cold);
+    k_gj_diag<<<dim3(1, 1, B), kDiagThreads, 0, s>>>(A, n, k0, nbk, Dinv, piv, sA, sW);
+    k_gj_panels<<<dim3((unsigned)((n + 31) / 32), 1, B), 256, 0, s>>>(A, n, k0, nbk, Dinv, Pn,
+                                                                      Cold, sA, sW);
+    k_gj_gemm<<<grid, 256, kGemmSmem, s>>>(A, n, Cold, Pn, sA, sW);
+    k_gj_fix<<<dim3((unsigned)((n * nbk + 255) / 256), 1, B), 256, 0, s>>>(A, n, k0, nbk, Dinv,
+                                                                            Pn, Cold, sA, sW);
   }
-  k_symmetrize<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(A, n);
-  k_pivot_check<<<1, 1024, 0, s>>>(piv, n, status);
+  k_symmetrize<<<dim3((unsigned)((n * n + 255) / 256), 1, B), 256, 0, s>>>(A, n, sA);
+  k_pivot_check<<<dim3(1, 1, B), 1024, 0, s>>>(piv, n, status, sW);
+}
+
+void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s) {
+  gj_inverse_impl(A, n, 1, 0, work, 0, status, s);
+}
+
+// batch SPD matrices of order n at A + b n^2, each inverted in place (same
+// blocked Gauss-Jordan, the batch on gridDim.z); work: batch *
+// dense_inverse_work_doubles(n). A singular pivot sets *status = 3.
+void dense_spd_inverse_batched(double* A, int64_t n, int64_t batch, double* work, int* status,
+                               cudaStream_t s) {
+  gj_inverse_impl(A, n, batch, n * n, work, dense_inverse_work_doubles(n), status, s);
 }
 
 // (+ NB: the identity-padded last pivot block writes NB pivots)

@@ -102,11 +102,13 @@ void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv,
 void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cudaStream_t s);
 // large cc elements (q = sd^3 L_c > 64, coarse_large.cu)
 bool coarse_large_supported(int q, int lcc);
+int64_t coarse_large_work_doubles(int q, int64_t neo, int lcc);
 void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
-                                  int* status, cudaStream_t s);
+                                  double* work, int* status, cudaStream_t s);
 void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* Bc,
-                           double* scratch, double* Rcc, double* cc_evals, int* scratch_status,
-                           int* iters, double tol, int maxit, cudaStream_t s);
+                           double* scratch, double* work, double* Rcc, double* cc_evals,
+                           int* scratch_status, int* iters, double tol, int maxit,
+                           cudaStream_t s);
 void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rcc, double* Acc,
                          cudaStream_t s);
 void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
@@ -135,6 +137,8 @@ void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac,
 // dense.cu
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
 int64_t dense_inverse_work_doubles(int64_t n);
+void dense_spd_inverse_batched(double* A, int64_t n, int64_t batch, double* work, int* status,
+                               cudaStream_t s);
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
                  cudaStream_t s);
 // rows [row0, row0 + nrows) of y = A x (A n x n, row-major)

@@ -366,12 +366,36 @@ def test_cc_basis_large_q_matches_oracle(n, ncc, sd, kmin):
         assert sv.min() >= 1 - 1e-8, (e, sv)
 
 
+@pytest.mark.parametrize("n,ncc,sd,lcc,kmin", [(32, 1, 8, 8, 1e-3), (32, 1, 8, 16, 1e-6),
+                                                (64, 2, 4, 16, 1e-6), (64, 2, 4, 20, 1e-3)])
+def test_large_q_wide_subspace_vs_oracle(n, ncc, sd, lcc, kmin):
+    """sd = 8 (q = 2048: tensor-core batched inverses, subspace vectors in
+    global memory) and L_cc up to 20 (24 subspace columns) against the oracle
+    with the same hierarchy."""
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond("mmg", s, O.hierarchy(O.grid(n), ncc, sd), lcc=lcc, fine_blocks="cell",
+                  coarse_blocks="cc")
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg", MmgOptions(num_cc_basis=lcc))
+    r = c.pcg(s.rhs, rtol=1e-8)
+    assert r.report.converged
+    assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+    # R_cc rows orthonormal per element
+    Rcc = c.cc_restriction()
+    for e in range(ncc ** 3):
+        blk = slice(e * lcc, (e + 1) * lcc)
+        np.testing.assert_allclose(Rcc[blk] @ Rcc[blk].T, np.eye(lcc), atol=1e-10)
+
+
 def test_large_q_limits():
     n = 32
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 1, 4, kappa)
     with pytest.raises(NotSupportedError, match="num_cc_basis"):
-        c.setup("mmg", MmgOptions(num_cc_basis=13))
+        c.setup("mmg", MmgOptions(num_cc_basis=21))
     c.setup("mmg", MmgOptions(num_cc_basis=12))
     r = c.pcg(np.ones(n ** 3), rtol=1e-8)
     assert r.report.converged
