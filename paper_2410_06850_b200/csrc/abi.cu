@@ -131,6 +131,9 @@ struct tmg_ctx {
   int lc_keep = 0;  // L_c of the kept bases
   int64_t n_cc = 0;
   double* AccT = nullptr;   // single slab: lower 64x64 tiles of A_cc^-1
+  double* accP = nullptr;   // single slab, plane-Thomas A_cc solve: tiles + couplings + work
+  bool acc_planes = false;
+  AccPlanesRef planes{};
   double* symvP = nullptr;  // single slab: GEMV partials
   double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
   double *rcc = nullptr, *ecc = nullptr;  // full-length cc vectors (one per process)
@@ -291,6 +294,8 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.tc);
   }
   dfree_null(c, c->AccT);
+  dfree_null(c, c->accP);
+  c->acc_planes = false;
   dfree_null(c, c->symvP);
   dfree_null(c, c->Ainv);
   dfree_null(c, c->rcc);
@@ -482,9 +487,13 @@ int finish_problem(tmg_ctx* c) {
 // single slab: coarse + coarse-coarse levels as one cooperative kernel
 void enqueue_coarse_single(tmg_ctx* c) {
   Slab& s = c->slabs[0];
-  if (getenv("TMG_UNFUSED_COARSE") || !coarse_fused_supported(s.g, c->n_cc))
+  if (c->acc_planes)
+    KL(5 + acc_planes_solve_kernels(s.g),
+       launch_coarse_cycle(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, nullptr, c->symvP, c->n_cc,
+                           s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, &c->planes, c->stream));
+  else if (getenv("TMG_UNFUSED_COARSE") || !coarse_fused_supported(s.g, c->n_cc))
     KL(7, launch_coarse_cycle(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc,
-                              s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, c->stream));
+                              s.rc, s.rc0, c->rcc, c->ecc, s.rc1, s.tc, s.ec, nullptr, c->stream));
   else
     KL(1, launch_coarse_fused(s.g, &s.st->done, s.Ac, s.Winv, s.Rcc, c->AccT, c->symvP, c->n_cc,
                               s.rc, s.rc0, c->rcc, s.rc1, s.ec, c->gbar, c->stream));
@@ -1776,31 +1785,61 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       }
       CK(cudaGetLastError());
       mark("thomas_factor");
-      // A_cc: every slab assembles its rows of the one dense matrix
-      double* Acc = dalloc<double>(c, c->n_cc * c->n_cc);
-      for (Slab& s : c->slabs) launch_acc_assemble(s.g, s.Ac, s.Rcc, Acc, c->stream);
-      CK(cudaGetLastError());
-      if (c->nccl()) {
-        const Slab& s = c->slabs[0];
-        const int64_t rows = s.g.neo * lcc;
-        NK(ncclAllGather(Acc + s.g.e0 * lcc * c->n_cc, Acc, (size_t)(rows * c->n_cc), ncclDouble,
-                         c->comm, c->stream));
-      }
-      mark("acc_assemble");
-      double* work = dalloc<double>(c, dense_inverse_work_doubles(c->n_cc));
-      dense_spd_inverse(Acc, c->n_cc, work, c->slabs[0].d_status + 2, c->stream);
-      CK(cudaGetLastError());
-      mark("acc_inverse");
-      if (!c->dist()) {
-        c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
-        c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
-        pack_sym_tiles(Acc, c->n_cc, c->AccT, c->stream);
+      // A_cc. Single slab with several cc-element z-planes and a large n_cc
+      // (or TMG_ACC_PLANES=1): block Thomas over the planes (acc_planes.cu);
+      // otherwise the dense inverse (replicated row blocks when partitioned).
+      const char* ap = getenv("TMG_ACC_PLANES");
+      const bool planes = !c->dist() && c->g.ncz >= 2 &&
+                          (ap ? ap[0] == '1' : c->n_cc > 16384);
+      double* work = nullptr;
+      if (planes) {
+        const GridParams& g0 = c->slabs[0].g;
+        const int64_t P = g0.ncx * g0.ncy * lcc;
+        double* Gd = dalloc<double>(c, g0.ncz * P * P);
+        c->accP = dalloc<double>(c, acc_planes_doubles(g0));
+        const int64_t ts = sym_tiles_doubles(P);
+        double* T = c->accP;
+        double* C = T + g0.ncz * ts;
+        double* wv = C + g0.ncc * lcc * lcc;
+        launch_acc_assemble_planes(g0, c->slabs[0].Ac, c->slabs[0].Rcc, Gd, C, c->stream);
         CK(cudaGetLastError());
-        mark("pack_tiles");
+        mark("acc_assemble");
+        work = dalloc<double>(c, dense_inverse_work_doubles(P));
+        acc_planes_factor(g0, Gd, C, T, work, c->slabs[0].d_status + 2, c->stream);
+        CK(cudaGetLastError());
+        mark("acc_planes");
+        c->symvP = dalloc<double>(c, sym_partials_doubles(P));
+        c->planes = AccPlanesRef{T, C, wv};
+        c->acc_planes = true;
         CK(cudaStreamSynchronize(c->stream));
-        dfree(c, Acc);
+        dfree(c, Gd);
       } else {
-        c->Ainv = Acc;  // row blocks applied per slab (launch_gemv_rows)
+        // every slab assembles its rows of the one dense matrix
+        double* Acc = dalloc<double>(c, c->n_cc * c->n_cc);
+        for (Slab& s : c->slabs) launch_acc_assemble(s.g, s.Ac, s.Rcc, Acc, c->stream);
+        CK(cudaGetLastError());
+        if (c->nccl()) {
+          const Slab& s = c->slabs[0];
+          const int64_t rows = s.g.neo * lcc;
+          NK(ncclAllGather(Acc + s.g.e0 * lcc * c->n_cc, Acc, (size_t)(rows * c->n_cc),
+                           ncclDouble, c->comm, c->stream));
+        }
+        mark("acc_assemble");
+        work = dalloc<double>(c, dense_inverse_work_doubles(c->n_cc));
+        dense_spd_inverse(Acc, c->n_cc, work, c->slabs[0].d_status + 2, c->stream);
+        CK(cudaGetLastError());
+        mark("acc_inverse");
+        if (!c->dist()) {
+          c->AccT = dalloc<double>(c, sym_tiles_doubles(c->n_cc));
+          c->symvP = dalloc<double>(c, sym_partials_doubles(c->n_cc));
+          pack_sym_tiles(Acc, c->n_cc, c->AccT, c->stream);
+          CK(cudaGetLastError());
+          mark("pack_tiles");
+          CK(cudaStreamSynchronize(c->stream));
+          dfree(c, Acc);
+        } else {
+          c->Ainv = Acc;  // row blocks applied per slab (launch_gemv_rows)
+        }
       }
       CK(cudaStreamSynchronize(c->stream));
       for (int i = 1; i < nph; ++i) {

@@ -215,8 +215,11 @@ __global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, d
 // A_cc block (E, F) for F in {E, 6 face neighbours}: sum over coupled child
 // pairs (I in E, J in F) of R_E[:, I] Ac_IJ R_F[:, J]^T, written into the dense
 // n_cc x n_cc matrix. grid = (m_cc, 7), block = lcc*lcc threads.
+// planar (acc_planes.cu): Acc = ncz dense P x P plane blocks, C = the z-lo
+// coupling blocks [element][L_cc][L_cc]; z-hi couplings are their transposes.
 __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
-                               const double* __restrict__ Rcc, double* Acc, int64_t ldacc) {
+                               const double* __restrict__ Rcc, double* Acc, int64_t ldacc,
+                               double* C, int planar) {
   const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
   const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   const int fdir = blockIdx.y;  // 0 self, 1..6 faces
@@ -231,6 +234,8 @@ __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
     F = hi ? ec.e + strides[ax] : ec.e - strides[ax];
   }
   const ElemCoord fc = elem_coord(g, F);
+  if (planar && fdir == 6) return;
+  const int64_t nxy = g.ncx * g.ncy, P = nxy * g.lcc;
   for (int pr = threadIdx.x; pr < g.lcc * g.lcc; pr += blockDim.x) {
     const int bb = pr / g.lcc, bp = pr % g.lcc;
     const double* RE = Rcc + (ec.e * g.lcc + bb) * q;
@@ -251,7 +256,14 @@ __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
         }
       }
     }
-    Acc[(ec.e * g.lcc + bb) * ldacc + F * g.lcc + bp] = acc;
+    if (!planar) {
+      Acc[(ec.e * g.lcc + bb) * ldacc + F * g.lcc + bp] = acc;
+    } else if (fdir == 5) {
+      C[(ec.e * g.lcc + bb) * g.lcc + bp] = acc;
+    } else {
+      const int64_t eloc = ec.e - ec.ek * nxy, floc = F - ec.ek * nxy;
+      Acc[ec.ek * P * P + (eloc * g.lcc + bb) * P + floc * g.lcc + bp] = acc;
+    }
   }
 }
 
@@ -630,7 +642,19 @@ void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rc
   // this context's rows of the global n x n matrix
   cudaMemsetAsync(Acc + g.e0 * g.lcc * n, 0, sizeof(double) * (size_t)(g.neo * g.lcc * n), s);
   dim3 grid((unsigned)g.neo, 7);
-  k_acc_assemble<<<grid, g.lcc * g.lcc < 256 ? g.lcc * g.lcc : 256, 0, s>>>(g, Ac, Rcc, Acc, n);
+  k_acc_assemble<<<grid, g.lcc * g.lcc < 256 ? g.lcc * g.lcc : 256, 0, s>>>(g, Ac, Rcc, Acc, n,
+                                                                           nullptr, 0);
+}
+
+// plane blocks + z couplings of A_cc (single slab; acc_planes.cu)
+void launch_acc_assemble_planes(const GridParams& g, const double* Ac, const double* Rcc,
+                                double* Gd, double* C, cudaStream_t s) {
+  const int64_t P = g.ncx * g.ncy * g.lcc;
+  cudaMemsetAsync(Gd, 0, sizeof(double) * (size_t)(g.ncz * P * P), s);
+  cudaMemsetAsync(C, 0, sizeof(double) * (size_t)(g.ncc * g.lcc * g.lcc), s);
+  dim3 grid((unsigned)g.neo, 7);
+  k_acc_assemble<<<grid, g.lcc * g.lcc < 256 ? g.lcc * g.lcc : 256, 0, s>>>(g, Ac, Rcc, Gd, P, C,
+                                                                           1);
 }
 
 // Coarse part of one V-cycle (solver.cpp:292-319): rc -> ec.
@@ -640,7 +664,7 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          const double* Winv, const double* Rcc, const double* Acc_tiles,
                          double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
-                         cudaStream_t s) {
+                         const AccPlanesRef* planes, cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
   const int nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   const int nc = (int)(g.nbo * LC);
@@ -649,7 +673,11 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
   launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Winv, rc, nul, rc0);
   launch_pdl(k_coarse_restrict, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Ac, Rcc, rc, rc0,
              rcc);
-  launch_symv(done, Acc_tiles, n_cc, rcc, symv_partials, ecc, s);
+  if (planes)
+    launch_acc_planes_solve(g, done, planes->T, planes->C, rcc, ecc, planes->wv, symv_partials,
+                            s);
+  else
+    launch_symv(done, Acc_tiles, n_cc, rcc, symv_partials, ecc, s);
   launch_pdl(k_coarse_prolong, dim3((unsigned)g.neo), dim3(nt), 0, s, g, done, Rcc, rc0, ecc, rc1);
   launch_pdl(k_coarse_resid, dim3((unsigned)((nc + 255) / 256)), dim3(256), 0, s, g, done, Ac, rc,
              rc1, tc, nc);

@@ -100,6 +100,21 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
                             cudaStream_t s);
 void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cudaStream_t s);
+// A_cc as a block Thomas over the cc-element z-planes (acc_planes.cu)
+struct AccPlanesRef {
+  const double* T;  // ncz packed symmetric plane inverses
+  const double* C;  // z-lo coupling blocks [element][L_cc][L_cc]
+  double* wv;       // 2 P work doubles
+};
+int64_t acc_planes_doubles(const GridParams& g);
+void launch_acc_assemble_planes(const GridParams& g, const double* Ac, const double* Rcc,
+                                double* Gd, double* C, cudaStream_t s);
+void acc_planes_factor(const GridParams& g, double* Gd, const double* C, double* T, double* work,
+                       int* status, cudaStream_t s);
+void launch_acc_planes_solve(const GridParams& g, const int* done, const double* T,
+                             const double* C, const double* rcc, double* ecc, double* wv,
+                             double* partials, cudaStream_t s);
+int acc_planes_solve_kernels(const GridParams& g);
 // large cc elements (q = sd^3 L_c > 64, coarse_large.cu)
 bool coarse_large_supported(int q, int lcc);
 int64_t coarse_large_work_doubles(int q, int64_t neo, int lcc);
@@ -115,7 +130,7 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          const double* Winv, const double* Rcc, const double* Acc_tiles,
                          double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
-                         cudaStream_t s);
+                         const AccPlanesRef* planes, cudaStream_t s);
 
 // the same cycle as one cooperative kernel (single slab; q = 32, L_cc = 8)
 bool coarse_fused_supported(const GridParams& g, int64_t n_cc);

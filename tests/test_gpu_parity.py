@@ -661,3 +661,25 @@ def test_warm_started_setup_matches_cold():
     rw, rc = warm.pcg(b, rtol=1e-8), cold.pcg(b, rtol=1e-8)
     assert abs(rw.report.iterations - rc.report.iterations) <= 1
     assert np.linalg.norm(rw.x - rc.x) <= 1e-6 * np.linalg.norm(rc.x)
+
+
+@pytest.mark.parametrize("n,ncc,sd,lcc,kmin", [(32, 4, 2, 8, 1e-3), (64, 4, 2, 8, 1e-6),
+                                                (64, 2, 4, 12, 1e-6), (64, 8, 1, 4, 1e-3)])
+def test_acc_planes_matches_dense(monkeypatch, n, ncc, sd, lcc, kmin):
+    """A_cc solved by the block Thomas over cc-element z-planes
+    (acc_planes.cu) against the dense inverse: same preconditioner up to the
+    explicit inverses' rounding, same PCG."""
+    _, kappa = problem(n, kmin)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TMG_ACC_PLANES", mode)
+        c = ctx_for(n, ncc, sd, kappa)
+        c.setup("mmg", MmgOptions(num_cc_basis=lcc))
+        r = np.random.default_rng(9).standard_normal(n ** 3)
+        rhs = c.assemble_rhs(np.ones(n ** 3))
+        out[mode] = (c.apply_preconditioner(r), c.pcg(rhs, rtol=1e-8))
+    (za, ra), (zb, rb) = out["0"], out["1"]
+    assert np.linalg.norm(za - zb) <= 1e-8 * np.linalg.norm(za)
+    assert rb.report.converged
+    assert abs(ra.report.iterations - rb.report.iterations) <= 1
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
