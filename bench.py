@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-side-by-side", action="store_true",
+                    help="skip the LS2 row and the config-1 side-by-side preconditioners")
     ap.add_argument("--ref-iters", type=int, default=8,
                     help="PCG iterations per reference step (bounded sample)")
     return ap.parse_args()
@@ -69,13 +71,14 @@ def config_json(cfg, cfg_id, extra=None, world=1):
                          f"MMG-PCG rtol={RTOL:g}",
              "cells": n ** 3,
              "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} "
-                          f"L_c=4 L_cc=8 nu=1"}
+                          f"L_c=4 L_cc={cfg.get('lcc', 8)} nu=1"}
     else:
         d = {"workload": f"{world} x BASELINE configs[{cfg_id}] slabs: {n}x{n}x{n * world} cells, "
                          f"kmin={cfg['kmin']:g}, MMG-PCG rtol={RTOL:g}",
              "cells": n ** 3 * world,
              "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} "
-                          f"ncc={cfg['ncc']}x{cfg['ncc']}x{cfg['ncc'] * world} L_c=4 L_cc=8 nu=1"}
+                          f"ncc={cfg['ncc']}x{cfg['ncc']}x{cfg['ncc'] * world} L_c=4 "
+                          f"L_cc={cfg.get('lcc', 8)} nu=1"}
     d.update({"kmin": cfg["kmin"], "rtol": RTOL,
               "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
               "l2": "no flush: one solve streams ~1.7 GB/iteration per GPU through the 126 MB L2"})
@@ -239,6 +242,37 @@ def ncu_traffic(kernel):
         return None
 
 
+def side_by_side(ctx, b, M):
+    """SURVEY.md §8(d) second rows, one device-timed solve each on the bench
+    design: LS2 (adjoint rhs 1/M, optim.cpp:16-19) on the resident MMG
+    hierarchy, then config 1's side-by-side preconditioners (M6: the
+    reference kinds jacobi / block_jacobi / two_grid, and mmg with the
+    reference's own fine blocks, one per cc element)."""
+    def row(rep, setup_s=None):
+        return {"iterations": rep.iterations, "converged": rep.converged,
+                "solve_ms": 1e3 * rep.solve_seconds,
+                "setup_ms": 1e3 * (rep.setup_seconds if setup_s is None else setup_s),
+                "mdof_iter_per_s": M * rep.iterations / rep.solve_seconds / 1e6
+                if rep.solve_seconds > 0 else None}
+    out = {}
+    ctx.upload_rhs(np.full(M, 1.0 / M))
+    out["ls2"] = row(ctx.solve_resident(RTOL, 20000))
+    from paper_2410_06850_b200 import MmgOptions
+    rows = {}
+    for name, kind, opts in [("jacobi", "jacobi", MmgOptions()),
+                             ("block_jacobi", "block_jacobi", MmgOptions()),
+                             ("two_grid", "two_grid", MmgOptions()),
+                             ("mmg_reference_fine_blocks", "mmg", MmgOptions(fine_blocks="cc"))]:
+        try:
+            ctx.setup(kind, opts)
+            ctx.upload_rhs(b)
+            rows[name] = row(ctx.solve_resident(RTOL, 20000))
+        except Exception as e:  # reported, not fatal
+            rows[name] = {"unavailable": str(e)[:160]}
+    out["side_by_side"] = rows
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -291,11 +325,13 @@ def run_ours(args):
     b = ctx.assemble_rhs(np.ones(M_local))
     barrier()
     t0 = time.perf_counter()
-    ctx.setup("mmg")  # first set-up: includes module loading and allocations
+    from paper_2410_06850_b200 import MmgOptions
+    mopts = MmgOptions(num_cc_basis=cfg.get("lcc", 8))
+    ctx.setup("mmg", mopts)  # first set-up: includes module loading and allocations
     setup_cold_wall = max_over_ranks(time.perf_counter() - t0)
     barrier()
     t0 = time.perf_counter()
-    ctx.setup("mmg")  # re-set-up (a design iteration's cost; buffers pooled)
+    ctx.setup("mmg", mopts)  # re-set-up (a design iteration's cost; buffers pooled)
     setup_wall = max_over_ranks(time.perf_counter() - t0)
     ctx.upload_rhs(b)
     for _ in range(max(3, args.warmup)):
@@ -389,6 +425,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if world == 1 and not args.no_side_by_side and args.config == 1:  # M6: config 1's rows
+        line.update(side_by_side(ctx, b, M))
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(cfg, kappa, args.ref_iters)
