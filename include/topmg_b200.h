@@ -34,7 +34,7 @@ extern "C" {
 #define TMG_PRECOND_NONE 0
 #define TMG_PRECOND_JACOBI 1
 #define TMG_PRECOND_BLOCK_JACOBI 2 /* cc-element blocks of 8^3 / 16^3 cells */
-#define TMG_PRECOND_TWO_GRID 3     /* R_cc = I; sd^3 L_c <= 32              */
+#define TMG_PRECOND_TWO_GRID 3     /* R_cc = I; sd^3 L_c <= 256             */
 #define TMG_PRECOND_MMG 4
 
 /* Faces, topmg::Face (grid.hpp:57). */

@@ -1629,8 +1629,8 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       return set_err(c, TMG_ENOTSUP, "GPU path is compiled for L_c = %d (got %lld)", compiled_lc(),
                      (long long)o->num_local_basis);
     const int64_t q = (int64_t)c->g.sd * c->g.sd * c->g.sd * o->num_local_basis;
-    if (kind == TMG_PRECOND_TWO_GRID && q > 32)
-      return set_err(c, TMG_ENOTSUP, "GPU two_grid handles sd^3*L_c <= 32 (got %lld)",
+    if (kind == TMG_PRECOND_TWO_GRID && q > 256)
+      return set_err(c, TMG_ENOTSUP, "GPU two_grid handles sd^3*L_c <= 256 (got %lld)",
                      (long long)q);
     if (kind == TMG_PRECOND_MMG && o->num_cc_basis > q)
       return set_err(c, TMG_EARG,

@@ -134,10 +134,26 @@ def test_hierarchy_variants_vs_oracle(kind, fine, n, ncc, sd, kmin):
                                rtol=1e-3)
 
 
+@pytest.mark.parametrize("n,ncc,sd,kmin", [(32, 1, 4, 1e-3), (64, 2, 4, 1e-6)])
+def test_two_grid_large_q_vs_oracle(n, ncc, sd, kmin):
+    """two_grid (R_cc = I) with sd = 4: A_cc = A_c over whole elements of q = 256."""
+    _, kappa = problem(n, kmin)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond("two_grid", s, O.hierarchy(O.grid(n), ncc, sd), fine_blocks="cell",
+                  coarse_blocks="cc")
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("two_grid")
+    r = c.pcg(s.rhs, rtol=1e-8)
+    assert r.report.converged
+    assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
 def test_hierarchy_variant_limits():
-    n = 16
+    n = 32
     _, kappa = problem(n, 1e-3)
-    c = ctx_for(n, 1, 4, kappa)  # q = 256
+    c = ctx_for(n, 1, 8, kappa)  # q = 2048
     with pytest.raises(NotSupportedError, match="two_grid"):
         c.setup("two_grid")
     c = ctx_for(64, 2, 4, problem(64, 1e-3)[1])  # 32^3-cell cc elements
