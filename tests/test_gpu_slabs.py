@@ -103,7 +103,9 @@ def test_slab_count_must_divide_cc_layers():
         Context(GridSpec(32, 32, 32), 4, 2, slabs=3)
 
 
-def test_nccl_transport_single_rank():
+@pytest.mark.parametrize("kind,fine", [("mmg", "coarse_cell"), ("mmg", "cc"),
+                                       ("block_jacobi", "coarse_cell"), ("two_grid", "coarse_cell")])
+def test_nccl_transport_single_rank(kind, fine):
     """The NCCL transport on a one-rank communicator (TMG_FORCE_DIST=1): the
     partitioned path with all-reduce / all-gather and NCCL calls captured in
     the iteration graph must reproduce the single-GPU solve."""
@@ -113,14 +115,14 @@ def test_nccl_transport_single_rank():
     import sys
     code = (
         "import json, numpy as np\n"
-        "from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs\n"
+        "from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, inputs\n"
         "n = 64\n"
         "k = inputs.conductivity(inputs.box_filter_design(n, 0.3), 1e-3)\n"
         "c = Context(GridSpec(n, n, n), 4, 2)\n"
         "c.set_conductivity(k, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))\n"
-        "c.setup('mmg')\n"
+        f"c.setup('{kind}', MmgOptions(fine_blocks='{fine}'))\n"
         "b = c.assemble_rhs(np.ones(n ** 3))\n"
-        "r = c.pcg(b, rtol=1e-8)\n"
+        "r = c.pcg(b, rtol=1e-8, max_iterations=5000)\n"
         "z = c.apply_preconditioner(b)\n"
         "print(json.dumps([r.report.iterations, r.x[::997].tolist(), z[::991].tolist()]))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
