@@ -173,7 +173,7 @@ struct UpdateSmem {
 // CTA size Thomas<CB>::NT (288 at CB = 8: one thread per mat-vec block row);
 // brick cells are strided over the threads.
 template <int CB>
-__global__ void __launch_bounds__(Thomas<CB>::NT, 3) k_update(GridParams g, const double* __restrict__ coef,
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, const double* __restrict__ coef,
                                                              int64_t M, const double* __restrict__ Gf,
                                                              double* x, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* r,

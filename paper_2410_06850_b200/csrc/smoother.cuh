@@ -89,7 +89,6 @@ struct ThomasSmem {
   // part[s][row]: contribution of block column s to a row (8-double pad keeps
   // the stores of a warp's 4 blocks in distinct bank halves by I+J parity)
   double part[Thomas<CB>::NBK][CB * CB + 8];
-  double u[CB * CB * CB];
   uint64_t bars[kSlots];
   double (*slots)[Thomas<CB>::PLANE];
 };
@@ -205,7 +204,8 @@ __device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm) {
 }
 
 // Exact block solve x = A_II^{-1} t for one brick (after thomas_prefetch).
-//  t  : smem, C values (plane k = t[k*P .. k*P+P)); x may alias t
+//  t  : smem, C values (plane k = t[k*P .. k*P+P)); x must alias t (the
+//       forward sweep keeps u_k in x, over the consumed t_k)
 //  tz : smem, C values; tz[l] = T_z between cell l and the cell one plane below
 // Starts and ends with a __syncthreads.
 template <int CB>
@@ -249,17 +249,16 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
       const int row = tid;
       if (n < CB) {  // forward: u_k = G_k w_k ; w_{k+1} = t_{k+1} + Tz_{k+1} u_k
         const int l = n * P + row;
-        sm.u[l] = acc;
+        x[l] = acc;  // u_k overwrites t_k, dead since step k-1 formed w_k
         if (n + 1 < CB) {
           wn[row] = fma(tz[l + P], acc, t[l + P]);
         } else {  // x_{K-1} = u_{K-1};  first backward w = -Tz_{K-1} x_{K-1}
-          x[l] = acc;
           wn[row] = -tz[l] * acc;
         }
       } else {  // backward plane k: x_k = u_k - G_k (B_{k+1} x_{k+1})
         const int k = Thomas<CB>::plane_of(n);
         const int l = k * P + row;
-        const double xv = sm.u[l] - acc;
+        const double xv = x[l] - acc;  // u_k - G_k B_{k+1} x_{k+1}
         x[l] = xv;
         if (k > 0) wn[row] = -tz[l] * xv;
       }

@@ -83,7 +83,7 @@ __device__ __forceinline__ void thomas_solve_rd(ThomasSmem<CB>& sm, const double
       const int row = tid;
       if (n < CB) {
         const int l = n * P + row;
-        sm.u[l] = acc;
+        x[l] = acc;
         if (n + 1 < CB) {
           wn[row] = fma(tz[l + P], acc, t[l + P]);
         } else {
@@ -93,7 +93,7 @@ __device__ __forceinline__ void thomas_solve_rd(ThomasSmem<CB>& sm, const double
       } else {
         const int k = TH::plane_of(n);
         const int l = k * P + row;
-        const double xv = sm.u[l] - acc;
+        const double xv = x[l] - acc;
         x[l] = xv;
         if (k > 0) wn[row] = -tz[l] * xv;
       }
