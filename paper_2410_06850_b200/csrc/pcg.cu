@@ -115,7 +115,7 @@ constexpr int kStencilThreads = 256;  // CTA size of the stencil kernels (2 cell
 
 template <int CB>
 #ifndef TMG_SEARCH_MINB
-#define TMG_SEARCH_MINB 8
+#define TMG_SEARCH_MINB 6
 #endif
 __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(GridParams g, const double* __restrict__ coef,
                                                               int64_t M, const double* __restrict__ z,
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
       const int li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
       r2own[k] = sm.u.st.r2[Tile<CB>::idx(li, lj, lk)];
       sm.tv[c] = r[bofs(bc.b, C) + c] - apply_coef<CB>(sm.u.st.cs, sm.u.st.r2, li, lj, lk);  // solver.cpp:327-330
-      sm.tz[c] = lk > 0 ? sm.u.st.cs.fz[Tile<CB>::fzi(li, lj, lk - 1)] : 0.0;
+      sm.tz[c] = lk > 0 ? coef_tz_below<CB>(sm.u.st.cs, c) : 0.0;
     }
   }
   __syncthreads();  // stencil tiles dead: the slots may now be filled

@@ -223,34 +223,42 @@ struct StencilSmem {
 //   coef[0] = T to the +x neighbour (0 if none), coef[1] = +y, coef[2] = +z,
 //   coef[3] = diagonal (faces summed in reference order, Dirichlet included).
 // A tile needs each axis' coefficients for its cells plus the low halo layer.
+// Natural cell order (conflict-free stores and neighbour reads): cx/cy/cz[c]
+// = T from cell c to its +axis neighbour, dg[c] = diagonal; hx/hy/hz = the
+// low halo layer (the -axis neighbour brick's +axis T), indexed by the two
+// in-face coordinates (x face: lj + CB*lk, y face: li + CB*lk, z face: li + CB*lj).
 template <int CB>
 struct CoefSmem {
-  double fx[Tile<CB>::NF], fy[Tile<CB>::NF], fz[Tile<CB>::NF];
+  double cx[CB * CB * CB], cy[CB * CB * CB], cz[CB * CB * CB];
   double dg[CB * CB * CB];
+  double hx[CB * CB], hy[CB * CB], hz[CB * CB];
 };
+
+// T to the cell one plane below (lk > 0)
+template <int CB>
+__device__ __forceinline__ double coef_tz_below(const CoefSmem<CB>& cs, int c) {
+  return cs.cz[c - CB * CB];
+}
 
 template <int CB>
 __device__ __forceinline__ void load_coefs(const double* __restrict__ coef, int64_t M, CoefSmem<CB>& cs,
                                            const GridParams& g, const BrickCoord& bc) {
   constexpr int C = CB * CB * CB;
   for (int t = threadIdx.x; t < C; t += blockDim.x) {
-    const int li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
     const size_t s = bofs(bc.b, C) + t;
-    cs.fx[Tile<CB>::fxi(li, lj, lk)] = __ldg(coef + s);
-    cs.fy[Tile<CB>::fyi(li, lj, lk)] = __ldg(coef + M + s);
-    cs.fz[Tile<CB>::fzi(li, lj, lk)] = __ldg(coef + 2 * M + s);
+    cs.cx[t] = __ldg(coef + s);
+    cs.cy[t] = __ldg(coef + M + s);
+    cs.cz[t] = __ldg(coef + 2 * M + s);
     cs.dg[t] = __ldg(coef + 3 * M + s);
   }
   // low halo layers: the +axis coefficient of the neighbouring brick's top layer
   for (int h = threadIdx.x; h < 3 * CB * CB; h += blockDim.x) {
     const int ax = h / (CB * CB), q = h % (CB * CB), u = q % CB, w = q / CB;
     const int nb = nbr_brick(g, bc, 2 * ax);
-    int nl, fi;
-    if (ax == 0) { nl = (CB - 1) + CB * (u + CB * w); fi = Tile<CB>::fxi(-1, u, w); }
-    else if (ax == 1) { nl = u + CB * ((CB - 1) + CB * w); fi = Tile<CB>::fyi(u, -1, w); }
-    else { nl = u + CB * (w + CB * (CB - 1)); fi = Tile<CB>::fzi(u, w, -1); }
+    const int nl = ax == 0 ? (CB - 1) + CB * (u + CB * w)
+                           : ax == 1 ? u + CB * ((CB - 1) + CB * w) : u + CB * (w + CB * (CB - 1));
     const double v = nb >= 0 ? __ldg(coef + (size_t)ax * M + bofs(nb, C) + nl) : 0.0;
-    (ax == 0 ? cs.fx : ax == 1 ? cs.fy : cs.fz)[fi] = v;
+    (ax == 0 ? cs.hx : ax == 1 ? cs.hy : cs.hz)[q] = v;
   }
 }
 
@@ -314,9 +322,9 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
     const int c = t + k * NT;
     if (c < C) {
       const int li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
-      cs.fx[Tile<CB>::fxi(li, lj, lk)] = cf[k][0];
-      cs.fy[Tile<CB>::fyi(li, lj, lk)] = cf[k][1];
-      cs.fz[Tile<CB>::fzi(li, lj, lk)] = cf[k][2];
+      cs.cx[c] = cf[k][0];
+      cs.cy[c] = cf[k][1];
+      cs.cz[c] = cf[k][2];
       cs.dg[c] = cf[k][3];
       tile[Tile<CB>::idx(li, lj, lk)] = first ? zo[k] : zo[k] + beta * po[k];
     }
@@ -334,10 +342,8 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
   for (int k = 0; k < KC; ++k) {
     const int h = t + k * NT;
     if (h < 3 * F) {
-      const int ax = h / F, q = h % F, u = q % CB, w = q / CB;
-      const int fi = ax == 0 ? Tile<CB>::fxi(-1, u, w)
-                             : ax == 1 ? Tile<CB>::fyi(u, -1, w) : Tile<CB>::fzi(u, w, -1);
-      (ax == 0 ? cs.fx : ax == 1 ? cs.fy : cs.fz)[fi] = ch[k];
+      const int ax = h / F, q = h % F;
+      (ax == 0 ? cs.hx : ax == 1 ? cs.hy : cs.hz)[q] = ch[k];
     }
   }
 }
@@ -350,13 +356,17 @@ __device__ __forceinline__ double apply_coef(const CoefSmem<CB>& cs, const doubl
                                              int lk) {
   constexpr int E = Tile<CB>::E;
   const int ti = Tile<CB>::idx(li, lj, lk);
-  double s = __dadd_rn(0.0, __dmul_rn(-cs.fz[Tile<CB>::fzi(li, lj, lk - 1)], xt[ti - E * E]));
-  s = __dadd_rn(s, __dmul_rn(-cs.fy[Tile<CB>::fyi(li, lj - 1, lk)], xt[ti - E]));
-  s = __dadd_rn(s, __dmul_rn(-cs.fx[Tile<CB>::fxi(li - 1, lj, lk)], xt[ti - 1]));
-  s = __dadd_rn(s, __dmul_rn(cs.dg[li + CB * (lj + CB * lk)], xt[ti]));
-  s = __dadd_rn(s, __dmul_rn(-cs.fx[Tile<CB>::fxi(li, lj, lk)], xt[ti + 1]));
-  s = __dadd_rn(s, __dmul_rn(-cs.fy[Tile<CB>::fyi(li, lj, lk)], xt[ti + E]));
-  s = __dadd_rn(s, __dmul_rn(-cs.fz[Tile<CB>::fzi(li, lj, lk)], xt[ti + E * E]));
+  const int c = li + CB * (lj + CB * lk);
+  const double* pz = lk > 0 ? cs.cz + (c - CB * CB) : cs.hz + (li + CB * lj);
+  const double* py = lj > 0 ? cs.cy + (c - CB) : cs.hy + (li + CB * lk);
+  const double* px = li > 0 ? cs.cx + (c - 1) : cs.hx + (lj + CB * lk);
+  double s = __dadd_rn(0.0, __dmul_rn(-*pz, xt[ti - E * E]));
+  s = __dadd_rn(s, __dmul_rn(-*py, xt[ti - E]));
+  s = __dadd_rn(s, __dmul_rn(-*px, xt[ti - 1]));
+  s = __dadd_rn(s, __dmul_rn(cs.dg[c], xt[ti]));
+  s = __dadd_rn(s, __dmul_rn(-cs.cx[c], xt[ti + 1]));
+  s = __dadd_rn(s, __dmul_rn(-cs.cy[c], xt[ti + E]));
+  s = __dadd_rn(s, __dmul_rn(-cs.cz[c], xt[ti + E * E]));
   return s;
 }
 
