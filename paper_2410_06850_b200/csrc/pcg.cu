@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
   // p_old and p are distinct buffers: neighbouring CTAs read p_old's halo while
   // this CTA writes the new search direction.
   pdl_trigger();
-  constexpr int C = CB * CB * CB, NT = kStencilThreads < C ? kStencilThreads : C;
-  constexpr int KPT = C / NT;
+  constexpr int C = CB * CB * CB, NT = kStencilThreads < C / 2 ? kStencilThreads : C / 2;
+  constexpr int KPT = C / (2 * NT);  // x-adjacent cell pairs per thread
   __shared__ CoefSmem<CB> cs;
   __shared__ double pt[Tile<CB>::N];
   __shared__ double red[80];
@@ -142,13 +142,16 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
   double pq = 0.0;
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
-    const int c = t + k * NT, li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+    const int c = 2 * (t + k * NT), li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
     const size_t s = bofs(bc.b, C) + c;
-    const double pv = pt[Tile<CB>::idx(li, lj, lk)];
-    const double qv = apply_coef<CB>(cs, pt, li, lj, lk);  // solver.cpp:540
-    p[s] = pv;
-    q[s] = qv;
-    pq += pv * qv;
+    const int ti = Tile<CB>::idx(li, lj, lk);
+    const double2 pv = make_double2(pt[ti], pt[ti + 1]);
+    const double2 qv = make_double2(apply_coef<CB>(cs, pt, li, lj, lk),
+                                    apply_coef<CB>(cs, pt, li + 1, lj, lk));  // solver.cpp:540
+    *reinterpret_cast<double2*>(p + s) = pv;
+    *reinterpret_cast<double2*>(q + s) = qv;
+    pq += pv.x * qv.x;
+    pq += pv.y * qv.y;
   }
   double v[1] = {pq};
   block_sum_k<NT, 1>(v, red);
@@ -452,7 +455,7 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    cudaStream_t s) {
   const int64_t M = g.mst;
   if (cb == 8) launch_pdl(k_search<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, z, p_old, p, q, st, partials);
-  else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, z, p_old, p, q, st, partials);
+  else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, PcgState* st,

@@ -229,8 +229,10 @@ struct StencilSmem {
 // in-face coordinates (x face: lj + CB*lk, y face: li + CB*lk, z face: li + CB*lj).
 template <int CB>
 struct CoefSmem {
-  double cx[CB * CB * CB], cy[CB * CB * CB], cz[CB * CB * CB];
-  double dg[CB * CB * CB];
+  alignas(16) double cx[CB * CB * CB];
+  alignas(16) double cy[CB * CB * CB];
+  alignas(16) double cz[CB * CB * CB];
+  alignas(16) double dg[CB * CB * CB];
   double hx[CB * CB], hy[CB * CB], hz[CB * CB];
 };
 
@@ -262,30 +264,32 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ coef, int6
   }
 }
 
-// load_coefs + load_tile_axpy for a CTA of exactly NT threads: every global
-// load of a thread is issued before the first shared-memory store, so ~16
-// loads per thread are in flight instead of the few of a load/store loop.
+// load_coefs + load_tile_axpy for a CTA of exactly NT threads, each owning
+// pairs of x-adjacent cells (c = 2 pr, 2 pr + 1): the brick's own data moves
+// as coalesced 128-bit loads, and every global load of a thread is issued
+// before the first shared-memory store (~12 loads in flight per thread).
 template <int CB, int NT>
 __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ coef, int64_t M,
                                                      CoefSmem<CB>& cs, const double* __restrict__ z,
                                                      const double* __restrict__ p_old, double beta,
                                                      bool first, double* tile,
                                                      const GridParams& g, const BrickCoord& bc) {
-  constexpr int C = CB * CB * CB, F = CB * CB;
-  constexpr int KO = (C + NT - 1) / NT;          // own cells per thread
+  constexpr int C = CB * CB * CB, F = CB * CB, NPAIR = C / 2;
+  constexpr int KO = (NPAIR + NT - 1) / NT;      // own cell pairs per thread
   constexpr int KH = (6 * F + NT - 1) / NT;      // halo cells per thread
   constexpr int KC = (3 * F + NT - 1) / NT;      // coefficient halo entries per thread
   const int t = threadIdx.x;
-  double cf[KO][4], zo[KO], po[KO], zh[KH], ph[KH], ch[KC];
+  double2 cf[KO][4], zo[KO], po[KO];
+  double zh[KH], ph[KH], ch[KC];
 #pragma unroll
   for (int k = 0; k < KO; ++k) {
-    const int c = t + k * NT;
-    if (c < C) {
-      const size_t s = bofs(bc.b, C) + c;
+    const int pr = t + k * NT;
+    if (pr < NPAIR) {
+      const size_t s = bofs(bc.b, C) + 2 * pr;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) cf[k][a] = __ldg(coef + (size_t)a * M + s);
-      zo[k] = __ldg(z + s);
-      po[k] = first ? 0.0 : __ldg(p_old + s);
+      for (int a = 0; a < 4; ++a) cf[k][a] = __ldg(reinterpret_cast<const double2*>(coef + (size_t)a * M + s));
+      zo[k] = __ldg(reinterpret_cast<const double2*>(z + s));
+      po[k] = first ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2*>(p_old + s));
     }
   }
 #pragma unroll
@@ -319,14 +323,16 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
   // stores
 #pragma unroll
   for (int k = 0; k < KO; ++k) {
-    const int c = t + k * NT;
-    if (c < C) {
-      const int li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
-      cs.cx[c] = cf[k][0];
-      cs.cy[c] = cf[k][1];
-      cs.cz[c] = cf[k][2];
-      cs.dg[c] = cf[k][3];
-      tile[Tile<CB>::idx(li, lj, lk)] = first ? zo[k] : zo[k] + beta * po[k];
+    const int pr = t + k * NT;
+    if (pr < NPAIR) {
+      const int c = 2 * pr, li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+      *reinterpret_cast<double2*>(cs.cx + c) = cf[k][0];
+      *reinterpret_cast<double2*>(cs.cy + c) = cf[k][1];
+      *reinterpret_cast<double2*>(cs.cz + c) = cf[k][2];
+      *reinterpret_cast<double2*>(cs.dg + c) = cf[k][3];
+      const int ti = Tile<CB>::idx(li, lj, lk);
+      tile[ti] = first ? zo[k].x : zo[k].x + beta * po[k].x;
+      tile[ti + 1] = first ? zo[k].y : zo[k].y + beta * po[k].y;
     }
   }
 #pragma unroll
