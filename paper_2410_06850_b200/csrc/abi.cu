@@ -499,6 +499,19 @@ void enqueue_coarse_single(tmg_ctx* c) {
                               s.rc, s.rc0, c->rcc, s.rc1, s.ec, c->gbar, c->stream));
 }
 
+// rc = R_c (r - A r1) after the per-brick fine block solve: the boundary form
+// (k_restrict_bnd) unless TMG_RESTRICT_BND=0 at build time
+#ifndef TMG_RESTRICT_BND
+#define TMG_RESTRICT_BND 1
+#endif
+static void restrict_fine(tmg_ctx* c, Slab& s, cudaStream_t st) {
+#if TMG_RESTRICT_BND
+  launch_restrict_bnd(s.g, c->cb, s.coef, s.phi, s.r1, s.rc, s.st, st);
+#else
+  launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st);
+#endif
+}
+
 // single slab: the fused path (device-side scalars, symmetric tiled A_cc GEMV)
 void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
@@ -506,7 +519,7 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   cudaStream_t st = c->stream;
   KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.st, s.partials,
                       s.history, init, st));
-  KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
   KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
                     st));
@@ -549,8 +562,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
                         s.partials, s.history, init, st));
   if (!init) reduce_finalize(c, kRedUpdate, 0);
   XCH(r1, sizeof(double) * C, false);
-  for (Slab& s : c->slabs)
-    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
     KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
@@ -741,7 +753,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     Slab& s = s0;
     const GridParams& g = s.g;
     timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
-    timed(2, [&] { KL(1, launch_restrict(g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
+    timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
     timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
@@ -792,7 +804,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
       if (hierarchical(c) && !c->fine_bj) {
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
-        timed(2, [&] { KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, c->stream)); });
+        timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
         timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {

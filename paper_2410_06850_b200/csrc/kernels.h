@@ -191,6 +191,9 @@ void launch_update(const GridParams& g, int cb, const double* coef, const double
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s);
+// boundary form of launch_restrict, valid when the fine blocks are the bricks
+void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phi,
+                         const double* r1, double* rc, const PcgState* st, cudaStream_t s);
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s);

@@ -265,6 +265,51 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
   if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
 }
 
+// Boundary form of K3 for the default fine blocks (one exact block per brick).
+// With r1_I = A_II^{-1} r_I, (r - A r1)_I = r_I - A_II r1_I - A_{I,nb} r1_nb
+// = -A_{I,nb} r1_nb up to the rounding of the block solve: only the brick's
+// surface cells carry a residual, T_f r1 across each face f (A's off-diagonal
+// entries are -T). So rc_I = sum over the 6*CB^2 face slots of
+// Phi_I(c_f) T_f r1_nb(f) — the same algebra as solver.cpp:285-289 without
+// the brick's own r, r1 and the interior stencil (43% fewer bytes). Not valid
+// for cc-element fine blocks, which keep k_restrict.
+template <int CB>
+__global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
+    GridParams g, const double* __restrict__ coef, int64_t M, const double* __restrict__ phi,
+    const double* __restrict__ r1, double* rc, const PcgState* st) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  constexpr int C = CB * CB * CB, F = CB * CB, NS = 6 * F;
+  constexpr int NT = kStencilThreads < NS ? kStencilThreads : NS;
+  constexpr int KS = (NS + NT - 1) / NT;
+  __shared__ double red[LCP * (NT / 32) + LCP + 8];
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  const int t = threadIdx.x;
+  const size_t ob = bofs(bc.b, C);
+  double v[LCP] = {};
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int h = t + k * NT;
+    if (h >= NS) break;
+    int f, ti, nl;
+    halo_slot<CB>(h, f, ti, nl);
+    const int nb = nbr_brick(g, bc, f);
+    if (nb < 0) continue;  // domain boundary: Dirichlet terms live in the diagonal
+    const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
+    const bool hi = f & 1;
+    const int e = hi ? CB - 1 : 0;
+    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+    // T of the face: the +axis coefficient of the lower cell of the pair
+    const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
+    const double val = tf * __ldg(r1 + bofs(nb, C) + nl);
+#pragma unroll
+    for (int a = 0; a < LCP; ++a) v[a] = fma(__ldg(phi + ((size_t)bc.b * LCP + a) * C + c), val, v[a]);
+  }
+  block_sum_k<NT, LCP>(v, red);
+  if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
+}
+
 // ---------------------------------------------------------------- K4 post
 template <int CB>
 struct PostSmem {
@@ -470,6 +515,12 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
   const int64_t M = g.mst;
   if (cb == 8) launch_pdl(k_restrict<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
   else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
+}
+void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phi,
+                         const double* r1, double* rc, const PcgState* st, cudaStream_t s) {
+  const int64_t M = g.mst;
+  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r1, rc, st);
+  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phi, r1, rc, st);
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
