@@ -227,12 +227,18 @@ def run_reference(args):
 
 # -------------------------------------------------------------------- ours
 
-# Algorithmic bytes per fine cell of the two block-solve kernels (DESIGN.md
-# §Roofline): streams that must move between HBM and the SMs once per launch.
-#  k_post  : r1 8 + Phi 32 + r 8 + coef 32 + G 288 + z 8          = 376
-#  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8    = 352
-KERNEL_BYTES_PER_CELL = {"post": 376, "update": 352, "search": 64, "restrict": 88}
-ITER_BYTES_PER_CELL = 64 + 352 + 88 + 376  # + coarse levels (~0.1%)
+# Algorithmic bytes per fine cell of the iteration kernels:
+# unique data that must move between HBM and the SMs once per launch. The
+# boundary-form kernels also read the 296 of 512 cells of each brick that lie
+# on its surface (SURF) from the Phi and r1 layers, and the face T's (3 B).
+#  k_post  : r1 8 + r 8 + coef_z 8 + G 288 + z 8 + Phi 32*SURF + T 3  = 341.5
+#  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8         = 352
+#  k_restrict: (Phi 32 + r1 8)*SURF + T 3                             = 26.1
+#  k_search: coef 32 + z 8 + p 16 + q 8                                = 64
+SURF = 296 / 512
+KERNEL_BYTES_PER_CELL = {"post": 320 + 32 * SURF + 3, "update": 352, "search": 64,
+                         "restrict": 40 * SURF + 3}
+ITER_BYTES_PER_CELL = sum(KERNEL_BYTES_PER_CELL.values())  # + coarse levels (~0.1%)
 
 
 def ncu_traffic(kernel):

@@ -409,6 +409,91 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   }
 }
 
+// Boundary form of K4 for the default fine blocks (one exact block per brick).
+// z = r2 + S(r - A r2) with r2 = r1 + R_c^T ec and r1_I = A_II^{-1} r_I gives
+//   z_I = A_II^{-1} r_I - r2_I + r2_I + A_II^{-1} (-A_{I,nb} r2_nb)
+//       = r1_I + A_II^{-1} t_I,   t_c = sum_{surface faces f of c} T_f r2_nb(f),
+// the same algebra as solver.cpp:322-333 without the brick's own Phi, its
+// coefficients and the interior stencil. r2 is needed on the face halo only
+// (r1 + Phi ec of the neighbouring bricks). The shared memory no longer holds
+// stencil tiles, so the first G planes stream from kernel entry.
+template <int CB>
+struct PostBSmem {
+  double slots[kSlots][Thomas<CB>::PLANE];
+  ThomasSmem<CB> th;
+  double tv[CB * CB * CB];
+  double tz[CB * CB * CB];
+  double red[80];
+  int flag;
+};
+
+template <int CB>
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, const double* __restrict__ coef,
+                                                               int64_t M, const double* __restrict__ phi,
+                                                               const double* __restrict__ Gf,
+                                                               const double* __restrict__ r,
+                                                               const double* __restrict__ r1,
+                                                               const double* __restrict__ ec, double* z,
+                                                               PcgState* st, double* partials, int init) {
+  pdl_trigger();
+  constexpr int C = CB * CB * CB, F = CB * CB, NT = Thomas<CB>::NT;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  PostBSmem<CB>& sm = *reinterpret_cast<PostBSmem<CB>*>(smraw);
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  const double* G = Gf + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  sm.th.slots = sm.slots;
+  thomas_init<CB>(sm.th);
+  __syncthreads();
+  thomas_prefetch<CB>(sm.th, G);  // G is constant: stream it before the wait
+  pdl_wait();
+  if (st->done) {
+    thomas_drain<CB>(sm.th);
+    return;
+  }
+  const int t = threadIdx.x;
+  const size_t ob = bofs(bc.b, C);
+  for (int c = t; c < C; c += NT) {
+    sm.tv[c] = 0.0;
+    sm.tz[c] = c >= F ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
+  }
+  // t_c over the surface, one axis per pass (the two faces of a pass touch
+  // disjoint cells; edge and corner cells sum x, then y, then z)
+  for (int ax = 0; ax < 3; ++ax) {
+    __syncthreads();
+    for (int h = t; h < 2 * F; h += NT) {
+      const int f = 2 * ax + h / F, q = h % F, u = q % CB, w = q / CB;
+      int ff, ti, nl;
+      halo_slot<CB>(f * F + q, ff, ti, nl);
+      const int nb = nbr_brick(g, bc, f);
+      if (nb < 0) continue;
+      const bool hi = f & 1;
+      const int e = hi ? CB - 1 : 0;
+      const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+      const size_t onb = bofs(nb, C);
+      double r2 = __ldg(r1 + onb + nl);  // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324)
+#pragma unroll
+      for (int a = 0; a < LCP; ++a)
+        r2 += __ldg(phi + ((size_t)nb * LCP + a) * C + nl) * __ldg(ec + (size_t)nb * LCP + a);
+      const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : onb + nl));
+      sm.tv[c] += tf * r2;
+    }
+  }
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // A_II^{-1} t
+  double rz = 0.0;
+  for (int c = t; c < C; c += NT) {
+    const double zv = __ldg(r1 + ob + c) + sm.tv[c];  // :331-333
+    z[ob + c] = zv;
+    rz += __ldg(r + ob + c) * zv;
+  }
+  double v[1] = {rz};
+  block_sum_k<NT, 1>(v, sm.red);
+  double tot[1];
+  if (grid_reduce_last_k<1>(v, partials, &st->ticket[3], tot, &sm.flag, sm.red) && t == 0) {
+    if (g.dist) st->loc[kRedPost] = tot[0];
+    else fin_post(st, tot[0], init);
+  }
+}
+
 // ---------------------------------------- Jacobi / identity preconditioner
 template <int CB>
 __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, const double* __restrict__ dinv,
@@ -469,12 +554,21 @@ static unsigned persist_grid(K kernel, int threads, size_t smem, int64_t nb) {
 }
 
 size_t update_smem(int cb) { return cb == 8 ? sizeof(UpdateSmem<8>) : sizeof(UpdateSmem<4>); }
+#ifndef TMG_POST_BND
+#define TMG_POST_BND 1
+#endif
+#if TMG_POST_BND
+#define K_POST k_post_bnd
+size_t post_smem(int cb) { return cb == 8 ? sizeof(PostBSmem<8>) : sizeof(PostBSmem<4>); }
+#else
+#define K_POST k_post
 size_t post_smem(int cb) { return cb == 8 ? sizeof(PostSmem<8>) : sizeof(PostSmem<4>); }
+#endif
 
 template <int CB>
 static void set_attrs() {
   cudaFuncSetAttribute(k_update<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem(CB));
-  cudaFuncSetAttribute(k_post<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)post_smem(CB));
+  cudaFuncSetAttribute(K_POST<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)post_smem(CB));
 }
 
 // Called once per context creation (outside any stream capture).
@@ -526,8 +620,8 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_post<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
-  else launch_pdl(k_post<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
