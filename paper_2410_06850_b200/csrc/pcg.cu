@@ -452,32 +452,49 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
   }
   const int t = threadIdx.x;
   const size_t ob = bofs(bc.b, C);
+  // surface terms T_f r2_nb(f): every load of the thread's face slots first
+  constexpr int NS = 6 * F, KS = (NS + NT - 1) / NT;
+  double val[KS];
+  int cell[KS], axis[KS];
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int h = t + k * NT;
+    val[k] = 0.0;
+    axis[k] = -1;
+    cell[k] = 0;
+    if (h < NS) {
+      int f, ti, nl;
+      halo_slot<CB>(h, f, ti, nl);
+      const int nb = nbr_brick(g, bc, f);
+      if (nb >= 0) {
+        const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
+        const bool hi = f & 1;
+        const int e = hi ? CB - 1 : 0;
+        const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+        const size_t onb = bofs(nb, C);
+        double r2 = __ldg(r1 + onb + nl);  // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324)
+#pragma unroll
+        for (int a = 0; a < LCP; ++a)
+          r2 += __ldg(phi + ((size_t)nb * LCP + a) * C + nl) * __ldg(ec + (size_t)nb * LCP + a);
+        val[k] = __ldg(coef + (size_t)ax * M + (hi ? ob + c : onb + nl)) * r2;
+        axis[k] = ax;
+        cell[k] = c;
+      }
+    }
+  }
   for (int c = t; c < C; c += NT) {
     sm.tv[c] = 0.0;
     sm.tz[c] = c >= F ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
   }
-  // t_c over the surface, one axis per pass (the two faces of a pass touch
-  // disjoint cells; edge and corner cells sum x, then y, then z)
+  // t_c, one axis per pass (the two faces of a pass touch disjoint cells;
+  // edge and corner cells sum x, then y, then z)
   for (int ax = 0; ax < 3; ++ax) {
     __syncthreads();
-    for (int h = t; h < 2 * F; h += NT) {
-      const int f = 2 * ax + h / F, q = h % F, u = q % CB, w = q / CB;
-      int ff, ti, nl;
-      halo_slot<CB>(f * F + q, ff, ti, nl);
-      const int nb = nbr_brick(g, bc, f);
-      if (nb < 0) continue;
-      const bool hi = f & 1;
-      const int e = hi ? CB - 1 : 0;
-      const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
-      const size_t onb = bofs(nb, C);
-      double r2 = __ldg(r1 + onb + nl);  // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324)
 #pragma unroll
-      for (int a = 0; a < LCP; ++a)
-        r2 += __ldg(phi + ((size_t)nb * LCP + a) * C + nl) * __ldg(ec + (size_t)nb * LCP + a);
-      const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : onb + nl));
-      sm.tv[c] += tf * r2;
-    }
+    for (int k = 0; k < KS; ++k)
+      if (axis[k] == ax) sm.tv[cell[k]] += val[k];
   }
+  __syncthreads();  // the solve's first step reads plane 0 of t from other threads
   thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // A_II^{-1} t
   double rz = 0.0;
   for (int c = t; c < C; c += NT) {

@@ -207,7 +207,9 @@ __device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm) {
 //  t  : smem, C values (plane k = t[k*P .. k*P+P)); x must alias t (the
 //       forward sweep keeps u_k in x, over the consumed t_k)
 //  tz : smem, C values; tz[l] = T_z between cell l and the cell one plane below
-// Starts and ends with a __syncthreads.
+// Thread i < P reads t[i] before the first __syncthreads: plane 0 of t must
+// be complete (written by thread i itself, or published by a caller barrier).
+// Ends with a __syncthreads.
 template <int CB>
 __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* __restrict__ G,
                                              const double* t, const double* tz, double* x) {
