@@ -77,6 +77,21 @@ __host__ __device__ constexpr int swz(int r, int c) {
 #define TMG_SLOTS 2
 #endif
 constexpr int kSlots = TMG_SLOTS;  // TMA ring depth (planes in flight per CTA)
+#ifndef TMG_G_HINTS
+#define TMG_G_HINTS 1
+#endif
+
+// Plane load n of a solve: forward loads of planes the backward sweep re-reads
+// ask L2 to keep them (evict_last); the last forward plane and the backward
+// re-reads are last uses (evict_first).
+__device__ __forceinline__ void plane_load(void* dst, const double* src, uint32_t bytes, uint64_t* bar,
+                                           int n, int cb) {
+#if TMG_G_HINTS
+  bulk_g2s_hint(dst, src, bytes, bar, l2_policy(n < cb - 1));
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
+}
 
 template <int CB>
 using PlaneSlots = double[kSlots][Thomas<CB>::PLANE];
@@ -188,8 +203,8 @@ __device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double
 #pragma unroll
     for (int n = 0; n < NPRE && n < Thomas<CB>::NL; ++n) {
       mbar_arrive_expect_tx(&sm.bars[n], Thomas<CB>::PLANE * sizeof(double));
-      bulk_g2s(sm.slots[n], G + (size_t)Thomas<CB>::plane_of(n) * Thomas<CB>::PLANE,
-               Thomas<CB>::PLANE * sizeof(double), &sm.bars[n]);
+      plane_load(sm.slots[n], G + (size_t)Thomas<CB>::plane_of(n) * Thomas<CB>::PLANE,
+                 Thomas<CB>::PLANE * sizeof(double), &sm.bars[n], n, CB);
     }
   }
 }
@@ -235,8 +250,8 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
     if (!resident && issuer && n + kSlots < NL) {
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&sm.bars[slot], Thomas<CB>::PLANE * sizeof(double));
-      bulk_g2s(sm.slots[slot], G + (size_t)Thomas<CB>::plane_of(n + kSlots) * Thomas<CB>::PLANE,
-               Thomas<CB>::PLANE * sizeof(double), &sm.bars[slot]);
+      plane_load(sm.slots[slot], G + (size_t)Thomas<CB>::plane_of(n + kSlots) * Thomas<CB>::PLANE,
+                 Thomas<CB>::PLANE * sizeof(double), &sm.bars[slot], n + kSlots, CB);
     }
     if (tid < P) {
       double pr[NBK];
