@@ -539,9 +539,14 @@ void enqueue_coarse_dist(tmg_ctx* c) {
     const int64_t own = s.g.neo * c->lcc;
     NK(ncclAllGather(c->rcc + s.g.e0 * c->lcc, c->rcc, (size_t)own, ncclDouble, c->comm, st));
   }
-  for (Slab& s : c->slabs)
-    KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
-                           c->rcc, c->ecc, st));
+  if (c->acc_planes)  // the whole plane solve, replicated (once for in-process slabs)
+    KL(acc_planes_solve_kernels(c->g),
+       launch_acc_planes_solve(c->g, &c->slabs[0].st->done, c->planes.T, c->planes.C, c->rcc, c->ecc,
+                               c->planes.wv, c->symvP, st));
+  else
+    for (Slab& s : c->slabs)
+      KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
+                             c->rcc, c->ecc, st));
   for (Slab& s : c->slabs)
     KL(1, launch_coarse_prolong(s.g, &s.st->done, s.Rcc, s.rc0, c->ecc, s.rc1, st));
   XCH(rc1, cvec, false);
@@ -1797,15 +1802,29 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       }
       CK(cudaGetLastError());
       mark("thomas_factor");
-      // A_cc. Single slab with several cc-element z-planes and a large n_cc
-      // (or TMG_ACC_PLANES=1): block Thomas over the planes (acc_planes.cu);
+      // A_cc. Several cc-element z-planes and a large n_cc (or
+      // TMG_ACC_PLANES=1): block Thomas over the planes (acc_planes.cu);
       // otherwise the dense inverse (replicated row blocks when partitioned).
+      // Partitioned contexts assemble their own planes, all-gather the plane
+      // blocks and couplings, and every rank factors and applies the whole
+      // (replicated) plane solve after the r_cc all-gather.
+      // Default by a per-V-cycle cost model (5 TB/s streaming, 6 us per
+      // dependent plane step): the plane solve streams 2 ncz symmetric P x P
+      // tiles in sequence; the dense inverse streams its symmetric tiles
+      // (single slab) or each rank's n_cc / N full rows. A dense inverse
+      // above 40 GB is not built. TMG_ACC_PLANES=0/1 overrides.
       const char* ap = getenv("TMG_ACC_PLANES");
-      const bool planes = !c->dist() && c->g.ncz >= 2 &&
-                          (ap ? ap[0] == '1' : c->n_cc > 16384);
+      const double bw = 5e12, step = 6e-6, ncd = (double)c->n_cc;
+      const double Pd = (double)(c->g.ncx * c->g.ncy * lcc);
+      const double t_planes = 2.0 * (double)c->g.ncz * (Pd * Pd * 4.0 / bw + step);
+      const double t_dense = (c->dist() ? ncd * ncd * 8.0 / (double)c->total : ncd * ncd * 4.0) / bw;
+      const bool planes = c->g.ncz >= 2 && (ap ? ap[0] == '1'
+                                                   : (t_planes < t_dense || ncd * ncd * 8.0 > 40e9));
       double* work = nullptr;
       if (planes) {
-        const GridParams& g0 = c->slabs[0].g;
+        GridParams g0 = c->slabs[0].g;  // global dims; the planes factor covers all elements
+        g0.ncz = c->g.ncz;
+        g0.ncc = c->g.ncc;
         const int64_t P = g0.ncx * g0.ncy * lcc;
         double* Gd = dalloc<double>(c, g0.ncz * P * P);
         c->accP = dalloc<double>(c, acc_planes_doubles(g0));
@@ -1813,8 +1832,17 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         double* T = c->accP;
         double* C = T + g0.ncz * ts;
         double* wv = C + g0.ncc * lcc * lcc;
-        launch_acc_assemble_planes(g0, c->slabs[0].Ac, c->slabs[0].Rcc, Gd, C, c->stream);
+        for (size_t k = 0; k < c->slabs.size(); ++k)
+          launch_acc_assemble_planes(c->slabs[k].g, c->slabs[k].Ac, c->slabs[k].Rcc, Gd, C, c->stream,
+                                     k == 0);
         CK(cudaGetLastError());
+        if (c->nccl()) {
+          const Slab& s = c->slabs[0];
+          const int64_t nxy = g0.ncx * g0.ncy, k0 = s.g.e0 / nxy, nk = s.g.neo / nxy;
+          NK(ncclAllGather(Gd + k0 * P * P, Gd, (size_t)(nk * P * P), ncclDouble, c->comm, c->stream));
+          NK(ncclAllGather(C + s.g.e0 * lcc * lcc, C, (size_t)(s.g.neo * lcc * lcc), ncclDouble, c->comm,
+                           c->stream));
+        }
         mark("acc_assemble");
         work = dalloc<double>(c, dense_inverse_work_doubles(P));
         acc_planes_factor(g0, Gd, C, T, work, c->slabs[0].d_status + 2, c->stream);

@@ -647,11 +647,15 @@ void launch_acc_assemble(const GridParams& g, const double* Ac, const double* Rc
 }
 
 // plane blocks + z couplings of A_cc (single slab; acc_planes.cu)
+// The blocks of the caller's elements (g.e0 .. g.e0 + g.neo: whole planes);
+// zero = clear all planes first (single slab, or the first of several slabs).
 void launch_acc_assemble_planes(const GridParams& g, const double* Ac, const double* Rcc,
-                                double* Gd, double* C, cudaStream_t s) {
+                                double* Gd, double* C, cudaStream_t s, bool zero) {
   const int64_t P = g.ncx * g.ncy * g.lcc;
-  cudaMemsetAsync(Gd, 0, sizeof(double) * (size_t)(g.ncz * P * P), s);
-  cudaMemsetAsync(C, 0, sizeof(double) * (size_t)(g.ncc * g.lcc * g.lcc), s);
+  if (zero) {
+    cudaMemsetAsync(Gd, 0, sizeof(double) * (size_t)(g.ncz * P * P), s);
+    cudaMemsetAsync(C, 0, sizeof(double) * (size_t)(g.ncc * g.lcc * g.lcc), s);
+  }
   dim3 grid((unsigned)g.neo, 7);
   k_acc_assemble<<<grid, g.lcc * g.lcc < 256 ? g.lcc * g.lcc : 256, 0, s>>>(g, Ac, Rcc, Gd, P, C,
                                                                            1);

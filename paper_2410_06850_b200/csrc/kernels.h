@@ -108,7 +108,7 @@ struct AccPlanesRef {
 };
 int64_t acc_planes_doubles(const GridParams& g);
 void launch_acc_assemble_planes(const GridParams& g, const double* Ac, const double* Rcc,
-                                double* Gd, double* C, cudaStream_t s);
+                                double* Gd, double* C, cudaStream_t s, bool zero = true);
 void acc_planes_factor(const GridParams& g, double* Gd, const double* C, double* T, double* work,
                        int* status, cudaStream_t s);
 void launch_acc_planes_solve(const GridParams& g, const int* done, const double* T,

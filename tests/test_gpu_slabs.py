@@ -103,12 +103,16 @@ def test_slab_count_must_divide_cc_layers():
         Context(GridSpec(32, 32, 32), 4, 2, slabs=3)
 
 
-@pytest.mark.parametrize("kind,fine", [("mmg", "coarse_cell"), ("mmg", "cc"),
-                                       ("block_jacobi", "coarse_cell"), ("two_grid", "coarse_cell")])
-def test_nccl_transport_single_rank(kind, fine):
+@pytest.mark.parametrize("kind,fine,planes", [("mmg", "coarse_cell", "0"), ("mmg", "cc", "0"),
+                                              ("block_jacobi", "coarse_cell", "0"),
+                                              ("two_grid", "coarse_cell", "0"),
+                                              ("mmg", "coarse_cell", "1")])
+def test_nccl_transport_single_rank(kind, fine, planes):
     """The NCCL transport on a one-rank communicator (TMG_FORCE_DIST=1): the
     partitioned path with all-reduce / all-gather and NCCL calls captured in
-    the iteration graph must reproduce the single-GPU solve."""
+    the iteration graph must reproduce the single-GPU solve. planes = 1: A_cc
+    as the block Thomas over cc-element z-planes (all-gathered plane blocks,
+    replicated plane solve)."""
     import json
     import os
     import subprocess
@@ -128,7 +132,7 @@ def test_nccl_transport_single_rank(kind, fine):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
     for force in ("0", "1"):
-        env = dict(os.environ, TMG_FORCE_DIST=force, PYTHONPATH=root)
+        env = dict(os.environ, TMG_FORCE_DIST=force, TMG_ACC_PLANES=planes, PYTHONPATH=root)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                            timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
@@ -162,3 +166,26 @@ def test_slab_variants_match_single(kind, fine, n, ncc, sd, slabs):
     assert ra.report.converged and rb.report.converged
     assert abs(ra.report.iterations - rb.report.iterations) <= max(1, ra.report.iterations // 50)
     assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
+
+
+@pytest.mark.parametrize("n,ncc,sd,slabs,kmin", [(32, 4, 2, 2, 1e-3), (64, 4, 2, 4, 1e-6),
+                                                 (64, 4, 2, 2, 1e-3)])
+def test_slab_acc_planes_match_single(n, ncc, sd, slabs, kmin, monkeypatch):
+    """A_cc as the block Thomas over cc-element z-planes on partitioned
+    contexts (each slab assembles its planes, the factors cover every plane,
+    the plane solve runs once on the gathered r_cc) against the single-slab
+    plane solve (same factors: summation order only) and the dense A_cc^-1
+    (another direct solver: PCG parity)."""
+    kappa = _problem(n, kmin)
+    dense = _ctx(n, ncc, sd, kappa, 1)
+    monkeypatch.setenv("TMG_ACC_PLANES", "1")
+    single = _ctx(n, ncc, sd, kappa, 1)
+    part = _ctx(n, ncc, sd, kappa, slabs)
+    r = np.random.default_rng(9).standard_normal(n ** 3)
+    zs, zp = single.apply_preconditioner(r), part.apply_preconditioner(r)
+    assert np.linalg.norm(zs - zp) <= 1e-9 * np.linalg.norm(zs)
+    rhs = dense.assemble_rhs(np.ones(n ** 3))
+    rd, rp = dense.pcg(rhs, rtol=1e-8), part.pcg(rhs, rtol=1e-8)
+    assert rd.report.converged and rp.report.converged
+    assert abs(rd.report.iterations - rp.report.iterations) <= 1
+    assert np.linalg.norm(rd.x - rp.x) <= 1e-7 * np.linalg.norm(rd.x)
