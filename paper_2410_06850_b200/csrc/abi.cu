@@ -79,6 +79,7 @@ struct Slab {
   // preconditioner
   double* dinv = nullptr;
   double* phi = nullptr;
+  double* phif = nullptr;  // Phi on each brick's 6 face layers, face-major (k_phi_faces)
   double* phi_keep = nullptr;  // last set-up's bases (warm start of the next one)
   double* evals = nullptr;
   int* eig_iters = nullptr;
@@ -276,6 +277,7 @@ void free_setup(tmg_ctx* c) {
       s.phi = nullptr;
       c->lc_keep = c->lc;
     }
+    dfree_null(c, s.phif);
     dfree_null(c, s.evals);
     dfree_null(c, s.eig_iters);
     dfree_null(c, s.Gf);
@@ -506,7 +508,7 @@ void enqueue_coarse_single(tmg_ctx* c) {
 #endif
 static void restrict_fine(tmg_ctx* c, Slab& s, cudaStream_t st) {
 #if TMG_RESTRICT_BND
-  launch_restrict_bnd(s.g, c->cb, s.coef, s.phi, s.r1, s.rc, s.st, st);
+  launch_restrict_bnd(s.g, c->cb, s.coef, s.phif, s.r1, s.rc, s.st, st);
 #else
   launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st);
 #endif
@@ -521,7 +523,7 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
                       s.history, init, st));
   KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
-  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
+  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
 
@@ -570,7 +572,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
+    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
                       init, st));
   reduce_finalize(c, kRedPost, init);
   XCH(z, sizeof(double) * C, false);
@@ -760,7 +762,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
     timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
     timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
-    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
+    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
@@ -811,7 +813,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
-        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
+        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_precond(c, 0, par); });
       }
@@ -1751,6 +1753,11 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       CK(cudaGetLastError());
       for (double*& pp : phi_prev) dfree_null(c, pp);  // stream-ordered reuse only
       XCH(phi, sizeof(double) * lc * C, false);
+      for (Slab& s : c->slabs) {  // after the exchange: ghost bricks' faces too
+        s.phif = ghosted<double>(c, s, 6 * lc * c->cb * c->cb);
+        launch_phi_faces(s.g, c->cb, s.phi, s.phif, s.bs0, s.nbs, c->stream);
+      }
+      CK(cudaGetLastError());
       mark("local_basis");
       for (Slab& s : c->slabs)
         launch_coarse_blocks(s.g, c->cb, s.kappa, s.dmask, s.phi, s.Ac, s.Bc, c->stream);

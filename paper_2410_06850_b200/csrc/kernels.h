@@ -192,11 +192,15 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s);
 // boundary form of launch_restrict, valid when the fine blocks are the bricks
-void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phi,
+void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
                          const double* r1, double* rc, const PcgState* st, cudaStream_t s);
-void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
+void launch_post(const GridParams& g, int cb, const double* coef, const double* phi, const double* phif,
                  const double* Gf, const double* r, const double* r1, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s);
+// face-major copy of Phi on each stored brick's 6 face layers:
+// phif[((b * 6 + f) * L_c + a) * CB^2 + q], q the in-face index of halo_slot
+void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* phif, int64_t b0,
+                      int64_t nb, cudaStream_t s);
 // sum PcgState::loc[which..] over the slabs in a fixed order and finish the
 // reduction on every slab (partitioned solves)
 void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s);

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
 // for cc-element fine blocks, which keep k_restrict.
 template <int CB>
 __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
-    GridParams g, const double* __restrict__ coef, int64_t M, const double* __restrict__ phi,
+    GridParams g, const double* __restrict__ coef, int64_t M, const double* __restrict__ phif,
     const double* __restrict__ r1, double* rc, const PcgState* st) {
   pdl_trigger();
   pdl_wait();
@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_
     const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
     const double val = tf * __ldg(r1 + bofs(nb, C) + nl);
 #pragma unroll
-    for (int a = 0; a < LCP; ++a) v[a] = fma(__ldg(phi + ((size_t)bc.b * LCP + a) * C + c), val, v[a]);
+    for (int a = 0; a < LCP; ++a)  // own face f (face-major phif)
+      v[a] = fma(__ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q), val, v[a]);
   }
   block_sum_k<NT, LCP>(v, red);
   if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
@@ -429,7 +430,7 @@ struct PostBSmem {
 
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, const double* __restrict__ coef,
-                                                               int64_t M, const double* __restrict__ phi,
+                                                               int64_t M, const double* __restrict__ phif,
                                                                const double* __restrict__ Gf,
                                                                const double* __restrict__ r,
                                                                const double* __restrict__ r1,
@@ -474,8 +475,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
         const size_t onb = bofs(nb, C);
         double r2 = __ldg(r1 + onb + nl);  // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324)
 #pragma unroll
-        for (int a = 0; a < LCP; ++a)
-          r2 += __ldg(phi + ((size_t)nb * LCP + a) * C + nl) * __ldg(ec + (size_t)nb * LCP + a);
+        for (int a = 0; a < LCP; ++a)  // the neighbour's face f^1 (face-major phif)
+          r2 += __ldg(phif + (((size_t)nb * 6 + (f ^ 1)) * LCP + a) * F + q) * __ldg(ec + (size_t)nb * LCP + a);
         val[k] = __ldg(coef + (size_t)ax * M + (hi ? ob + c : onb + nl)) * r2;
         axis[k] = ax;
         cell[k] = c;
@@ -627,16 +628,38 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
   if (cb == 8) launch_pdl(k_restrict<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
   else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
 }
-void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phi,
+void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
                          const double* r1, double* rc, const PcgState* st, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r1, rc, st);
-  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phi, r1, rc, st);
+  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phif, r1, rc, st);
+  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phif, r1, rc, st);
 }
-void launch_post(const GridParams& g, int cb, const double* coef, const double* phi,
-                 const double* Gf, const double* r, const double* r1, const double* ec, double* z,
-                 PcgState* st, double* partials, int init, cudaStream_t s) {
+
+// Face-major copy of Phi for the boundary-form kernels: their Phi reads are
+// whole 16-byte-coalesced face rows instead of stride-CB columns (x faces).
+template <int CB>
+__global__ void __launch_bounds__(256) k_phi_faces(const double* __restrict__ phi, double* phif, int64_t b0) {
+  constexpr int C = CB * CB * CB, F = CB * CB;
+  const int64_t b = b0 + blockIdx.x;
+  for (int i = threadIdx.x; i < 6 * LCP * F; i += blockDim.x) {
+    const int f = i / (LCP * F), a = (i / F) % LCP, q = i % F, u = q % CB, w = q / CB, ax = f >> 1;
+    const int e = (f & 1) ? CB - 1 : 0;
+    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+    phif[(b * 6 + f) * LCP * F + a * F + q] = phi[(b * LCP + a) * C + c];
+  }
+}
+void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* phif, int64_t b0,
+                      int64_t nb, cudaStream_t s) {
+  (void)g;
+  if (cb == 8) k_phi_faces<8><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
+  else k_phi_faces<4><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
+}
+void launch_post(const GridParams& g, int cb, const double* coef, const double* phi_full,
+                 const double* phif, const double* Gf, const double* r, const double* r1,
+                 const double* ec, double* z, PcgState* st, double* partials, int init,
+                 cudaStream_t s) {
   const int64_t M = g.mst;
+  const double* phi = TMG_POST_BND ? phif : phi_full;
   if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
   else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
