@@ -229,14 +229,14 @@ def run_reference(args):
 
 # Algorithmic bytes per fine cell of the iteration kernels:
 # unique data that must move between HBM and the SMs once per launch. The
-# boundary-form kernels also read the 296 of 512 cells of each brick that lie
-# on its surface (SURF) from the Phi and r1 layers, and the face T's (3 B).
-#  k_post  : r1 8 + r 8 + coef_z 8 + G 288 + z 8 + Phi 32*SURF + T 3  = 341.5
-#  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8         = 352
-#  k_restrict: (Phi 32 + r1 8)*SURF + T 3                             = 26.1
-#  k_search: coef 32 + z 8 + p 16 + q 8                                = 64
+# boundary-form kernels touch Phi and r1 only on the 296 of 512 cells of each
+# brick that lie on its surface (SURF), plus the face T's (3 B).
+#  k_post  : r 8 + coef_z 8 + G 288 + z 8 + (Phi 32 + r1 8)*SURF + T 3 = 338.1
+#  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8*SURF     = 348.6
+#  k_restrict: (Phi 32 + r1 8)*SURF + T 3                              = 26.1
+#  k_search: coef 32 + z 8 + p 16 + q 8                                 = 64
 SURF = 296 / 512
-KERNEL_BYTES_PER_CELL = {"post": 320 + 32 * SURF + 3, "update": 352, "search": 64,
+KERNEL_BYTES_PER_CELL = {"post": 312 + 40 * SURF + 3, "update": 344 + 8 * SURF, "search": 64,
                          "restrict": 40 * SURF + 3}
 ITER_BYTES_PER_CELL = sum(KERNEL_BYTES_PER_CELL.values())  # + coarse levels (~0.1%)
 

@@ -94,6 +94,7 @@ struct Slab {
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
          *r1 = nullptr, *stage = nullptr;
+  double* r1f = nullptr;  // r1 on each brick's 6 face layers, face-major (k_update)
   double* pbuf[2] = {nullptr, nullptr};  // ping-pong search directions
   double *rc = nullptr, *rc0 = nullptr, *ec = nullptr, *rc1 = nullptr, *tc = nullptr;
   PcgState* st = nullptr;
@@ -503,12 +504,9 @@ void enqueue_coarse_single(tmg_ctx* c) {
 
 // rc = R_c (r - A r1) after the per-brick fine block solve: the boundary form
 // (k_restrict_bnd) unless TMG_RESTRICT_BND=0 at build time
-#ifndef TMG_RESTRICT_BND
-#define TMG_RESTRICT_BND 1
-#endif
 static void restrict_fine(tmg_ctx* c, Slab& s, cudaStream_t st) {
 #if TMG_RESTRICT_BND
-  launch_restrict_bnd(s.g, c->cb, s.coef, s.phif, s.r1, s.rc, s.st, st);
+  launch_restrict_bnd(s.g, c->cb, s.coef, s.phif, s.r1f, s.rc, s.st, st);
 #else
   launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st);
 #endif
@@ -519,11 +517,11 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
   const GridParams& g = s.g;
   cudaStream_t st = c->stream;
-  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.st, s.partials,
+  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
                       s.history, init, st));
   KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
-  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, init,
+  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
 
@@ -565,14 +563,15 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   cudaStream_t st = c->stream;
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.st,
+    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.r1f, s.st,
                         s.partials, s.history, init, st));
   if (!init) reduce_finalize(c, kRedUpdate, 0);
-  XCH(r1, sizeof(double) * C, false);
+  XCH(r1f, sizeof(double) * 6 * c->cb * c->cb, false);  // the boundary kernels read r1's face layers
+  if (TMG_R1_FULL) XCH(r1, sizeof(double) * C, false);
   for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials,
+    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
                       init, st));
   reduce_finalize(c, kRedPost, init);
   XCH(z, sizeof(double) * C, false);
@@ -759,10 +758,10 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   } else if (hierarchical(c) && !c->fine_bj) {
     Slab& s = s0;
     const GridParams& g = s.g;
-    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.st, s.partials, s.history, 1, c->stream)); });
+    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
     timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
-    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
+    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
@@ -810,10 +809,10 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
       if (hierarchical(c) && !c->fine_bj) {
-        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.st, s.partials, s.history, 0, c->stream)); });
+        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
-        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
+        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_precond(c, 0, par); });
       }
@@ -984,6 +983,8 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
       for (double** v : {&s.b, &s.x, &s.r, &s.q, &s.z, &s.r1}) *v = ghosted<double>(c, s, C);
       s.pbuf[0] = ghosted<double>(c, s, C);
       s.pbuf[1] = ghosted<double>(c, s, C);
+      s.r1f = ghosted<double>(c, s, 6 * c->cb * c->cb);
+      CK(cudaMemset(s.r1f + s.bs0 * 6 * c->cb * c->cb, 0, sizeof(double) * (size_t)(s.nbs * 6 * c->cb * c->cb)));
       s.p = s.pbuf[0];
       s.stage = dalloc<double>(c, s.xcells);
       s.st = dalloc<PcgState>(c, 1);

@@ -10,6 +10,18 @@
 
 namespace tmg {
 
+// Boundary forms of the fine restriction / post-smoothing;
+// build with -DTMG_RESTRICT_BND=0 / -DTMG_POST_BND=0 for the literal kernels.
+// The boundary kernels read r1 only on the brick face layers (r1f); the full
+// r1 is written and exchanged only when a literal kernel needs it.
+#ifndef TMG_RESTRICT_BND
+#define TMG_RESTRICT_BND 1
+#endif
+#ifndef TMG_POST_BND
+#define TMG_POST_BND 1
+#endif
+#define TMG_R1_FULL (!(TMG_RESTRICT_BND && TMG_POST_BND))
+
 // PDL on unless TMG_NO_PDL is set (A/B diagnostics)
 inline bool pdl_enabled() {
   static const bool on = getenv("TMG_NO_PDL") == nullptr;
@@ -186,16 +198,16 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s);
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
-                   const double* p, const double* q, double* r, double* r1, PcgState* st,
+                   const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s);
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s);
 // boundary form of launch_restrict, valid when the fine blocks are the bricks
 void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
-                         const double* r1, double* rc, const PcgState* st, cudaStream_t s);
+                         const double* r1f, double* rc, const PcgState* st, cudaStream_t s);
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi, const double* phif,
-                 const double* Gf, const double* r, const double* r1, const double* ec, double* z,
+                 const double* Gf, const double* r, const double* r1, const double* r1f, const double* ec, double* z,
                  PcgState* st, double* partials, int init, cudaStream_t s);
 // face-major copy of Phi on each stored brick's 6 face layers:
 // phif[((b * 6 + f) * L_c + a) * CB^2 + q], q the in-face index of halo_slot

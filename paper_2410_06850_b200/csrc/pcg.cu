@@ -180,8 +180,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
                                                              int64_t M, const double* __restrict__ Gf,
                                                              double* x, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* r,
-                                                             double* r1, PcgState* st, double* partials,
-                                                             double* history, int init) {
+                                                             double* r1, double* r1f, PcgState* st,
+                                                             double* partials, double* history, int init) {
   pdl_trigger();
   constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -213,7 +213,14 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
     sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
   }
   thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // r1 = S(r), solver.cpp:280-281
-  for (int c = t; c < C; c += NT) r1[bofs(b, C) + c] = sm.tv[c];
+  if (TMG_R1_FULL)
+    for (int c = t; c < C; c += NT) r1[bofs(b, C) + c] = sm.tv[c];
+  // the face layers of r1, face-major: all the boundary-form kernels read
+  for (int h = t; h < 6 * P; h += NT) {
+    const int f = h / P, q = h % P, u = q % CB, w = q / CB, ax = f >> 1, e = (f & 1) ? CB - 1 : 0;
+    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+    r1f[(size_t)b * 6 * P + h] = sm.tv[c];
+  }
   if (!init) {
     double v[1] = {rr};
     block_sum_k<NT, 1>(v, sm.red);
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
 template <int CB>
 __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
     GridParams g, const double* __restrict__ coef, int64_t M, const double* __restrict__ phif,
-    const double* __restrict__ r1, double* rc, const PcgState* st) {
+    const double* __restrict__ r1f, double* rc, const PcgState* st) {
   pdl_trigger();
   pdl_wait();
   if (st->done) return;
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_
     const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
     // T of the face: the +axis coefficient of the lower cell of the pair
     const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
-    const double val = tf * __ldg(r1 + bofs(nb, C) + nl);
+    const double val = tf * __ldg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);  // r1 on the neighbour's face
 #pragma unroll
     for (int a = 0; a < LCP; ++a)  // own face f (face-major phif)
       v[a] = fma(__ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q), val, v[a]);
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
 // Boundary form of K4 for the default fine blocks (one exact block per brick).
 // z = r2 + S(r - A r2) with r2 = r1 + R_c^T ec and r1_I = A_II^{-1} r_I gives
 //   z_I = A_II^{-1} r_I - r2_I + r2_I + A_II^{-1} (-A_{I,nb} r2_nb)
-//       = r1_I + A_II^{-1} t_I,   t_c = sum_{surface faces f of c} T_f r2_nb(f),
+//       = A_II^{-1} (r_I + t_I),   t_c = sum_{surface faces f of c} T_f r2_nb(f),
 // the same algebra as solver.cpp:322-333 without the brick's own Phi, its
 // coefficients and the interior stencil. r2 is needed on the face halo only
 // (r1 + Phi ec of the neighbouring bricks). The shared memory no longer holds
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
                                                                int64_t M, const double* __restrict__ phif,
                                                                const double* __restrict__ Gf,
                                                                const double* __restrict__ r,
-                                                               const double* __restrict__ r1,
+                                                               const double* __restrict__ r1f,
                                                                const double* __restrict__ ec, double* z,
                                                                PcgState* st, double* partials, int init) {
   pdl_trigger();
@@ -473,7 +480,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
         const int e = hi ? CB - 1 : 0;
         const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
         const size_t onb = bofs(nb, C);
-        double r2 = __ldg(r1 + onb + nl);  // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324)
+        // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324), r1 from the neighbour's face
+        double r2 = __ldg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);
 #pragma unroll
         for (int a = 0; a < LCP; ++a)  // the neighbour's face f^1 (face-major phif)
           r2 += __ldg(phif + (((size_t)nb * 6 + (f ^ 1)) * LCP + a) * F + q) * __ldg(ec + (size_t)nb * LCP + a);
@@ -483,9 +491,17 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
       }
     }
   }
-  for (int c = t; c < C; c += NT) {
-    sm.tv[c] = 0.0;
-    sm.tz[c] = c >= F ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
+  // z_I = A_II^{-1} (r_I + t_I) = r1_I + A_II^{-1} t_I: the solve takes r + t
+  constexpr int KC = (C + NT - 1) / NT;
+  double rown[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int c = t + k * NT;
+    rown[k] = c < C ? __ldg(r + ob + c) : 0.0;
+    if (c < C) {
+      sm.tv[c] = rown[k];
+      sm.tz[c] = c >= F ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
+    }
   }
   // t_c, one axis per pass (the two faces of a pass touch disjoint cells;
   // edge and corner cells sum x, then y, then z)
@@ -496,12 +512,16 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
       if (axis[k] == ax) sm.tv[cell[k]] += val[k];
   }
   __syncthreads();  // the solve's first step reads plane 0 of t from other threads
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // A_II^{-1} t
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // z = A_II^{-1} (r + t), solver.cpp:331-333
   double rz = 0.0;
-  for (int c = t; c < C; c += NT) {
-    const double zv = __ldg(r1 + ob + c) + sm.tv[c];  // :331-333
-    z[ob + c] = zv;
-    rz += __ldg(r + ob + c) * zv;
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int c = t + k * NT;
+    if (c < C) {
+      const double zv = sm.tv[c];
+      z[ob + c] = zv;
+      rz += rown[k] * zv;
+    }
   }
   double v[1] = {rz};
   block_sum_k<NT, 1>(v, sm.red);
@@ -615,11 +635,11 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
   else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, coef, M, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
-                   const double* p, const double* q, double* r, double* r1, PcgState* st,
+                   const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
-  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, st, partials, history, init);
+  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
+  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
 }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
@@ -629,10 +649,10 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
   else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
 }
 void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
-                         const double* r1, double* rc, const PcgState* st, cudaStream_t s) {
+                         const double* r1f, double* rc, const PcgState* st, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phif, r1, rc, st);
-  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phif, r1, rc, st);
+  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phif, r1f, rc, st);
+  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phif, r1f, rc, st);
 }
 
 // Face-major copy of Phi for the boundary-form kernels: their Phi reads are
@@ -655,11 +675,12 @@ void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* ph
   else k_phi_faces<4><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* phi_full,
-                 const double* phif, const double* Gf, const double* r, const double* r1,
-                 const double* ec, double* z, PcgState* st, double* partials, int init,
-                 cudaStream_t s) {
+                 const double* phif, const double* Gf, const double* r, const double* r1_full,
+                 const double* r1f, const double* ec, double* z, PcgState* st, double* partials,
+                 int init, cudaStream_t s) {
   const int64_t M = g.mst;
   const double* phi = TMG_POST_BND ? phif : phi_full;
+  const double* r1 = TMG_POST_BND ? r1f : r1_full;
   if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
   else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
