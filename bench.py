@@ -246,7 +246,11 @@ def ncu_traffic(kernel):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["kernels"]["k_" + kernel]["dram_bytes_per_launch"]
+        ks = d["kernels"]
+        for name in ("k_" + kernel + "_bnd", "k_" + kernel):  # boundary-form kernels first
+            if name in ks:
+                return ks[name]["dram_bytes_per_launch"]
+        return None
     except Exception:
         return None
 
