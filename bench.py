@@ -1,27 +1,34 @@
 """Benchmark: FP64 PCG + multiscale-MG solve throughput on B200.
 
-Workload (BASELINE.json configs[1], the single-GPU configuration the metric is
-quoted on): 128^3 cells, seeded box-filter design (vf 0.3, 3 passes, radius 2),
+Headline workload: BASELINE.json configs[3], the configuration the metric
+("... at 1/2/4/8 B200") is quoted on, and it fits one GPU (70 GB): 512^3
+cells (1.34e8 DoF), seeded box-filter design (vf 0.2, 3 passes, radius 4),
 SIMP p = 3, kmin = 1e-6, unit source, T = 0 on the centred 0.2 x 0.2 patch of
-z = 0, PCG to ||r||/||b|| <= 1e-8 with the multiscale V-cycle (L_c = 4,
-L_cc = 8, c = 8, sd = 2, ncc = 8). One step = one full PCG solve from x0 = 0
-on the resident system. value = DoF * iterations / solve time (MDoF*iter/s).
-With N > 1 ranks (torchrun) the solve is partitioned: one configs[1] slab of
-128^3 cells per GPU stacked along z (weak scaling), ghost exchanges and CG
-reductions over NCCL, time = max over ranks, value = all DoF of the job.
+z = 0, PCG to ||r||/||b|| <= 1e-8 (the reference's recurrence rule,
+solver.cpp:549-560) with the multiscale V-cycle (c = 8, sd = 4, ncc = 16,
+L_c = 4, L_cc = 12). The design is generated on the device
+(gen.cu, bit-identical to inputs.box_filter_design). One step = one full PCG
+solve from x0 = 0 on the resident system; value = DoF * iterations / solve
+time (MDoF*iter/s). With N > 1 GPUs the same 512^3 problem is split into N
+z-slabs (strong scaling): ghost exchanges and CG reductions over NCCL, time =
+max over ranks, value = all DoF of the job.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 3]
 
---impl reference times the reference's own CPU implementation of the path
-(oracle/_ref: proj/core compiled unmodified) on the same
-config with all host threads; rank 0 only.
+--gpus N without torchrun re-launches itself under torch.distributed.run
+with N ranks (one per GPU). --impl reference times the reference's own CPU
+implementation of the path (oracle/_ref: proj/core compiled unmodified,
+-O3 -march=native when the host supports it) on a bounded
+sample of the workload with all host threads, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -35,56 +42,69 @@ METRIC = "PCG solve MDoF*iter/s (FP64, rtol 1e-8, multiscale-MG V-cycle)"
 UNIT = "MDoF*iter/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 RTOL = 1e-8
+# the CPU sample of configs[3]: the reference cannot set up 512^3 (its dense
+# per-coarse-cell LDL^T factors alone take ~550 GB of host memory)
+SAMPLE_N = 128
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)  # ~0.55 s timed: enough clock samples
+    ap.add_argument("--steps", type=int, default=10)  # 10 x 1.4 s timed at configs[3]
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=3, choices=[0, 1, 3])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-side-by-side", action="store_true",
-                    help="skip the LS2 row and the config-1 side-by-side preconditioners")
+    ap.add_argument("--no-extra", "--no-side-by-side", dest="no_extra", action="store_true",
+                    help="skip the configs[1] rows (side-by-side kinds, time to solution)")
     ap.add_argument("--ref-iters", type=int, default=8,
                     help="PCG iterations per reference step (bounded sample)")
-    return ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: print the rank/partition plan of the run (CPU test)")
+    return ap.parse_args(argv)
 
 
-def workload(cfg_id, world=1):
-    """configs[cfg_id] design; with world > 1 the weak-scaling grid of the
-    partitioned runs: world slabs of n^3 cells stacked along z."""
+def cfg_of(cfg_id):
     from paper_2410_06850_b200 import inputs
-    cfg = dict(inputs.CONFIGS[cfg_id])
-    n = cfg["n"]
-    shape = n if world == 1 else (n, n, n * world)
-    rho = inputs.box_filter_design(shape, cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
-    kappa = inputs.conductivity(rho, cfg["kmin"])
-    return cfg, kappa
+    return dict(inputs.CONFIGS[cfg_id])
 
 
-def config_json(cfg, cfg_id, extra=None, world=1):
+def hierarchy_str(cfg, n):
+    return (f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} L_c=4 "
+            f"L_cc={cfg.get('lcc', 8)} nu=1")
+
+
+def config_json(cfg, cfg_id, world, extra=None):
     n = cfg["n"]
-    if world == 1:
-        d = {"workload": f"BASELINE configs[{cfg_id}]: {n}^3 cells, kmin={cfg['kmin']:g}, "
-                         f"MMG-PCG rtol={RTOL:g}",
-             "cells": n ** 3,
-             "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} "
-                          f"L_c=4 L_cc={cfg.get('lcc', 8)} nu=1"}
-    else:
-        d = {"workload": f"{world} x BASELINE configs[{cfg_id}] slabs: {n}x{n}x{n * world} cells, "
-                         f"kmin={cfg['kmin']:g}, MMG-PCG rtol={RTOL:g}",
-             "cells": n ** 3 * world,
-             "hierarchy": f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} "
-                          f"ncc={cfg['ncc']}x{cfg['ncc']}x{cfg['ncc'] * world} L_c=4 "
-                          f"L_cc={cfg.get('lcc', 8)} nu=1"}
-    d.update({"kmin": cfg["kmin"], "rtol": RTOL,
-              "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
-              "l2": "no flush: one solve streams ~1.7 GB/iteration per GPU through the 126 MB L2"})
+    d = {"workload": f"BASELINE configs[{cfg_id}]: {n}^3 cells, vf={cfg['vf']}, "
+                     f"radius={cfg['radius']}, kmin={cfg['kmin']:g}, MMG-PCG rtol={RTOL:g}"
+                     + (f", strong scaling over {world} z-slabs" if world > 1 else ""),
+         "cells": n ** 3, "hierarchy": hierarchy_str(cfg, n), "kmin": cfg["kmin"], "rtol": RTOL,
+         "smoother": "exact block-Jacobi per coarse cell (fine) / per cc element (coarse)",
+         "parallelism": f"z-slabs x{world} over NCCL" if world > 1 else "single-gpu",
+         "l2": ("no flush: inputs larger than L2 (one solve streams "
+                f"~{ITER_BYTES_PER_CELL * n ** 3 / 1e9:.0f} GB per iteration through the 126 MB L2)")}
     if extra:
         d.update(extra)
     return d
+
+
+def data_label(cfg_id):
+    return (f"synthetic (seeded box-filter design with BASELINE configs[{cfg_id}]'s generator "
+            "parameters; no dataset involved)")
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cpus": os.cpu_count()}
 
 
 # ------------------------------------------------------------------- clocks
@@ -142,84 +162,108 @@ class ClockSampler:
 
 # --------------------------------------------------------------- reference
 
-def reference_context(cfg, kappa, world=1):
-    """The reference (proj/core, oracle/_ref) on the bench workload: configs[1]
-    for N = 1, the N-slab elongated grid of the partitioned runs for N > 1."""
-    import ctypes as C
+_REF_LIB = None
+
+
+def reference_lib():
+    """oracle/_ref: the -O3 -march=native timing build when
+    it loads and runs on this host, else the portable parity build."""
+    global _REF_LIB
+    if _REF_LIB is not None:
+        return _REF_LIB
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O  # bench's reference / cpu-baseline leg only
-    R = O.ref()
-    R.ref_set_num_threads(0)
-    pa = O._patch_array(O.bottom_center_patch())
-    ts = C.c_double()
-    n = cfg["n"]
-    ctx = R.ref_ctx_create_grid(n, n, n * world, 1.0, 1.0, float(world), cfg["ncc"], cfg["ncc"],
-                                cfg["ncc"] * world, cfg["sd"], O._d(kappa), 1, O._d(pa), 4,
-                                O.BLOCKS["cell"], O.BLOCKS["cc"], 4, 8, 1, C.byref(ts))
-    if not ctx:
-        raise RuntimeError(R.ref_last_error().decode())
-    return O, R, ctx, ts.value, R.ref_num_threads()
+    fast = os.path.join(ROOT, "oracle", "_ref", "libtopmg_ref_native.so")
+    kind = "portable -O2 -march=x86-64-v2 build"
+    if os.path.exists(fast) and O._REF is None:
+        # probe in a child: an ISA the host lacks would kill this process
+        probe = ("import sys; sys.path.insert(0, %r); import oracle as O; O.REF_PATH = %r; "
+                 "import numpy as np; n = 16; k = np.ones(n ** 3); "
+                 "c = O.RefContext(n, 1, 2, k); r = c.solve(); assert r.converged"
+                 % (os.path.join(ROOT, "oracle"), fast))
+        ok = subprocess.run([sys.executable, "-c", probe], capture_output=True,
+                            timeout=120).returncode == 0
+        if ok:
+            O.REF_PATH = fast
+            kind = "-O3 -march=native build (" + open(fast + ".march").read().strip() + ")" \
+                if os.path.exists(fast + ".march") else "-O3 -march=native build"
+    _REF_LIB = (O, kind)
+    return _REF_LIB
 
 
-def reference_steps(O, R, ctx, n, steps, iters):
-    import ctypes as C
-    it, cv, sv = C.c_int(), C.c_int(), C.c_double()
-    tot_it, tot_s = 0, 0.0
-    for _ in range(steps):
-        rc = R.ref_ctx_pcg(ctx, C.c_double(RTOL), C.c_int(iters), None, C.byref(it), C.byref(cv),
-                           C.byref(sv))
-        if rc:
-            raise RuntimeError(R.ref_last_error().decode())
-        tot_it += it.value
-        tot_s += sv.value
-    return tot_it, tot_s
+def reference_sample(O, cfg, n, lcc, iters=None):
+    """The reference on the configs[cfg] generator and hierarchy parameters at
+    n^3 cells; returns (context, setup seconds)."""
+    from paper_2410_06850_b200 import inputs
+    rho = inputs.box_filter_design(n, cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
+    kappa = inputs.conductivity(rho, cfg["kmin"])
+    ncc = n // (8 * cfg["sd"])
+    t0 = time.perf_counter()
+    ctx = O.RefContext(n, ncc, cfg["sd"], kappa, fine_blocks="cell", coarse_blocks="cc", lcc=lcc)
+    return ctx, time.perf_counter() - t0, kappa
 
 
-def cpu_baseline(cfg, kappa, iters):
-    O, R, ctx, setup_s, threads = reference_context(cfg, kappa)
+def cpu_baseline(cfg, cfg_id, iters):
+    """Reference on the bounded sample: set-up (recorded, untimed for the
+    metric) + one PCG solve to rtol (time to solution)."""
+    O, build = reference_lib()
+    n = min(cfg["n"], SAMPLE_N)
+    ctx, setup_s, kappa = reference_sample(O, cfg, n, cfg.get("lcc", 8))
     try:
-        its, secs = reference_steps(O, R, ctx, cfg["n"], 1, iters)
+        r = ctx.solve(rtol=RTOL, maxit=10000)
     finally:
-        R.ref_ctx_destroy(ctx)
-    return {"value": cfg["n"] ** 3 * its / secs / 1e6, "unit": UNIT, "cores": threads,
-            "kind": "reference",
-            "sample": f"reference proj/core (oracle/_ref) on {cfg['n']}^3 configs[1]: "
-                      f"set-up ({setup_s:.1f} s, untimed) + one PCG of {its} iterations",
-            "setup_seconds": setup_s}
+        threads = ctx.threads
+        ctx.close()
+    return {"value": n ** 3 * r.iterations / r.solve_seconds / 1e6, "unit": UNIT,
+            "cores": threads, "kind": "reference",
+            "sample": (f"reference proj/core (oracle/_ref, {build}) on configs[{cfg_id}]'s "
+                       f"generator and hierarchy ({hierarchy_str(cfg, n)}) at {n}^3 cells: set-up "
+                       f"({setup_s:.1f} s, untimed) + one PCG solve to rtol {RTOL:g} "
+                       f"({r.iterations} iterations, {r.solve_seconds:.1f} s)"),
+            "iterations": r.iterations, "setup_seconds": setup_s,
+            "solve_seconds": r.solve_seconds, "time_to_solution_s": setup_s + r.solve_seconds,
+            "sample_cells": n ** 3, **cpu_info()}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    cfg, kappa = workload(args.config, world)
+    cfg = cfg_of(args.config)
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtopmg_ref.so")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtopmg_ref.so not built "
                           "(run bash oracle/build_ref.sh where /root/reference exists)"}))
         return 0
-    O, R, ctx, setup_s, threads = reference_context(cfg, kappa, world)
-    # bounded sample: the N-slab grid is N times larger, so fewer iterations
-    # per step keep the whole run within minutes (the metric is per iteration)
-    ref_iters = max(2, args.ref_iters // world)
+    O, build = reference_lib()
+    n = min(cfg["n"], SAMPLE_N)
+    ctx, setup_s, _ = reference_sample(O, cfg, n, cfg.get("lcc", 8))
     try:
-        reference_steps(O, R, ctx, cfg["n"], args.warmup, ref_iters)
+        for _ in range(args.warmup):
+            ctx.solve(rtol=RTOL, maxit=args.ref_iters)
+        its, secs = 0, 0.0
         t0 = time.perf_counter()
-        its, secs = reference_steps(O, R, ctx, cfg["n"], args.steps, ref_iters)
+        for _ in range(args.steps):
+            r = ctx.solve(rtol=RTOL, maxit=args.ref_iters)
+            its += r.iterations
+            secs += r.solve_seconds
         wall = time.perf_counter() - t0
+        threads = ctx.threads
     finally:
-        R.ref_ctx_destroy(ctx)
-    value = kappa.size * its / secs / 1e6
+        ctx.close()
+    value = n ** 3 * its / secs / 1e6
+    sample = (f"{args.steps} steps x {args.ref_iters} PCG iterations of the reference "
+              f"(oracle/_ref, {build}) on configs[{args.config}]'s generator and hierarchy "
+              f"({hierarchy_str(cfg, n)}) at {n}^3 cells (set-up {setup_s:.1f} s, untimed)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE configs[1])",
-            "config": config_json(cfg, args.config, {"reference_setup_seconds": setup_s,
-                                                     "iterations_per_step": its // args.steps},
-                                  world),
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": data_label(args.config),
+            "config": config_json(cfg, args.config, 1, {
+                "reference_setup_seconds": setup_s, "iterations_per_step": its // args.steps,
+                "sample_cells": n ** 3}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{args.steps} steps x {ref_iters} PCG iterations "
-                                       f"of the reference on {kappa.size} cells (set-up untimed)"},
+                             "sample": sample, **cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -241,49 +285,127 @@ KERNEL_BYTES_PER_CELL = {"post": 312 + 40 * SURF + 3, "update": 344 + 8 * SURF, 
 ITER_BYTES_PER_CELL = sum(KERNEL_BYTES_PER_CELL.values())  # + coarse levels (~0.1%)
 
 
-def ncu_traffic(kernel):
-    path = os.path.join(ROOT, "profiles", "ncu_summary_latest.json")
-    try:
-        with open(path) as f:
-            d = json.load(f)
-        ks = d["kernels"]
+def ncu_traffic(kernel, cfg_id, cells):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of the
+    same configuration (profiles/ncu_summary_*.json with matching config and
+    cells), else None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_*.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        if d.get("config") != cfg_id or d.get("cells") != cells:
+            continue
+        ks = d.get("kernels", {})
         for name in ("k_" + kernel + "_bnd", "k_" + kernel):  # boundary-form kernels first
             if name in ks:
-                return ks[name]["dram_bytes_per_launch"]
-        return None
-    except Exception:
-        return None
+                best = {"bytes": ks[name]["dram_bytes_per_launch"],
+                        "source": os.path.relpath(path, ROOT) + f" ({d.get('tag')})"}
+                break
+    return best
 
 
-def side_by_side(ctx, b, M):
-    """SURVEY.md §8(d) second rows, one device-timed solve each on the bench
-    design: LS2 (adjoint rhs 1/M, optim.cpp:16-19) on the resident MMG
-    hierarchy, then config 1's side-by-side preconditioners (M6: the
-    reference kinds jacobi / block_jacobi / two_grid, and mmg with the
-    reference's own fine blocks, one per cc element)."""
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(args):
+    """--gpus N outside torchrun: one rank per GPU under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """The rank/partition plan of the run, without a GPU (gloo)."""
+    import torch.distributed as dist
+    from paper_2410_06850_b200 import GridSpec
+    from paper_2410_06850_b200 import dist as D
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = cfg_of(args.config)
+    n = cfg["n"]
+    part = D.partition(GridSpec(n, n, n), cfg["ncc"], cfg["sd"], world, rank)
+    parts = [part]
+    if world > 1:
+        dist.init_process_group("gloo")
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "config": args.config,
+                          "impl": args.impl, "cells": n ** 3, "partitions": parts}))
+    return 0
+
+
+def configs1_rows(device):
+    """BASELINE configs[1] (128^3, contrast 1e6) on the GPU: the MMG solve, the
+    adjoint LS2 on the resident hierarchy (optim.cpp:16-19) and config 1's
+    side-by-side preconditioners (the reference kinds
+    jacobi / block_jacobi / two_grid, and mmg with the reference's own fine
+    blocks, one per cc element). One device-timed solve each."""
+    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions
+    cfg = cfg_of(1)
+    n = cfg["n"]
+    M = n ** 3
+    ctx = Context(GridSpec(n, n, n), cfg["ncc"], cfg["sd"], device=device)
+    ctx.set_design_generated(cfg["vf"], cfg["kmin"], 1.0, 3,
+                             BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0),
+                             passes=cfg["passes"], radius=cfg["radius"])
+    b = ctx.assemble_rhs(np.ones(M))
+
     def row(rep, setup_s=None):
+        s = rep.setup_seconds if setup_s is None else setup_s
         return {"iterations": rep.iterations, "converged": rep.converged,
-                "solve_ms": 1e3 * rep.solve_seconds,
-                "setup_ms": 1e3 * (rep.setup_seconds if setup_s is None else setup_s),
+                "solve_ms": 1e3 * rep.solve_seconds, "setup_ms": 1e3 * s,
+                "time_to_solution_ms": 1e3 * (s + rep.solve_seconds),
                 "mdof_iter_per_s": M * rep.iterations / rep.solve_seconds / 1e6
                 if rep.solve_seconds > 0 else None}
     out = {}
+    cell = MmgOptions(fine_blocks="coarse_cell")
+    ctx.setup("mmg", cell)
+    ctx.setup("mmg", cell)  # warm (module loading, pools)
+    ctx.upload_rhs(b)
+    ctx.solve_resident(RTOL, 20000)
+    out["mmg"] = row(ctx.solve_resident(RTOL, 20000))
     ctx.upload_rhs(np.full(M, 1.0 / M))
-    out["ls2"] = row(ctx.solve_resident(RTOL, 20000))
-    from paper_2410_06850_b200 import MmgOptions
-    rows = {}
+    out["mmg_ls2"] = row(ctx.solve_resident(RTOL, 20000))
     for name, kind, opts in [("jacobi", "jacobi", MmgOptions()),
                              ("block_jacobi", "block_jacobi", MmgOptions()),
-                             ("two_grid", "two_grid", MmgOptions()),
+                             ("two_grid", "two_grid", cell),
                              ("mmg_reference_fine_blocks", "mmg", MmgOptions(fine_blocks="cc"))]:
         try:
             ctx.setup(kind, opts)
             ctx.upload_rhs(b)
-            rows[name] = row(ctx.solve_resident(RTOL, 20000))
+            out[name] = row(ctx.solve_resident(RTOL, 20000))
         except Exception as e:  # reported, not fatal
-            rows[name] = {"unavailable": str(e)[:160]}
-    out["side_by_side"] = rows
+            out[name] = {"unavailable": str(e)[:160]}
+    ctx.close()
     return out
+
+
+def reference_tts_config1():
+    """The reference's time to solution at configs[1] (set-up + LS1 solve,
+    bench.cpp:54-66 / solver.cpp:494,570-573) on the host cores."""
+    O, build = reference_lib()
+    cfg = cfg_of(1)
+    ctx, setup_s, _ = reference_sample(O, cfg, cfg["n"], 8)
+    try:
+        r = ctx.solve(rtol=RTOL, maxit=10000)
+        threads = ctx.threads
+    finally:
+        ctx.close()
+    return {"iterations": r.iterations, "setup_s": setup_s, "solve_s": r.solve_seconds,
+            "time_to_solution_s": setup_s + r.solve_seconds, "cores": threads, "build": build,
+            "mdof_iter_per_s": cfg["n"] ** 3 * r.iterations / r.solve_seconds / 1e6}
 
 
 def run_ours(args):
@@ -301,45 +423,40 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    def max_over_ranks(v):
+    def reduce(v, op):
         if world == 1:
             return v
         t = torch.tensor([v], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max_over_ranks(v):
+        return reduce(v, dist.ReduceOp.MAX if world > 1 else None)
 
     def sum_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce(v, dist.ReduceOp.SUM if world > 1 else None)
 
-    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, inputs
+    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions
     from paper_2410_06850_b200 import dist as D
-    n = inputs.CONFIGS[args.config]["n"]
+    cfg = cfg_of(args.config)
+    n = cfg["n"]
+    grid = GridSpec(n, n, n)
     patch = BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0)
-    cfg, kappa = workload(args.config, world)
     if world == 1:
-        grid = GridSpec(n, n, n)
         ctx = Context(grid, cfg["ncc"], cfg["sd"], device=local)
-        kappa_local = kappa
     else:
-        # weak scaling: one configs[1] slab (n^3 cells) per GPU, stacked along z
-        # into an n x n x (n * world) grid with cubic cells (lz = world); the
-        # design is the same generator on the whole grid.
-        grid = GridSpec(n, n, n * world, 1.0, 1.0, float(world))
-        ncc = (cfg["ncc"], cfg["ncc"], cfg["ncc"] * world)
-        ctx = D.dist_context(grid, ncc, cfg["sd"], dist, local)
-        kappa_local = D.slab(kappa, D.partition(grid, ncc, cfg["sd"], world, rank))
+        # strong scaling: the same grid in `world` z-slabs of whole cc layers
+        ctx = D.dist_context(grid, cfg["ncc"], cfg["sd"], dist, local)
     M_local = ctx.cells
     M = grid.num_cells()
-    ctx.set_conductivity(kappa_local, patch)
+    t0 = time.perf_counter()
+    ctx.set_design_generated(cfg["vf"], cfg["kmin"], 1.0, 3, patch, passes=cfg["passes"],
+                             radius=cfg["radius"])
+    gen_s = time.perf_counter() - t0
     b = ctx.assemble_rhs(np.ones(M_local))
+    mopts = MmgOptions(num_cc_basis=cfg.get("lcc", 8), fine_blocks="coarse_cell")
     barrier()
     t0 = time.perf_counter()
-    from paper_2410_06850_b200 import MmgOptions
-    mopts = MmgOptions(num_cc_basis=cfg.get("lcc", 8))
     ctx.setup("mmg", mopts)  # first set-up: includes module loading and allocations
     setup_cold_wall = max_over_ranks(time.perf_counter() - t0)
     barrier()
@@ -367,6 +484,12 @@ def run_ours(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     iters = int(np.mean(its))
     value = M * iters / (ms * 1e-3) / 1e6
+    setup_s = max_over_ranks(rep.setup_seconds)
+
+    # time to rtol on the TRUE residual (residual replacement, not in the
+    # reference: DESIGN.md §5 "true residual")
+    ver = ctx.solve_resident(RTOL, 10000, true_residual=True)
+    ver_s = max_over_ranks(ver.solve_seconds)
 
     # e2e through the C ABI with pinned host buffers (H2D b, solve, D2H x)
     b_pin = torch.from_numpy(b).pin_memory().numpy()
@@ -384,25 +507,32 @@ def run_ours(args):
     b2 = sum_over_ranks(float(np.sum(b ** 2)))
     true_rel = float(np.sqrt(res2 / b2))
 
-    peak = None
-    peak_src = "fallback 6650 GB/s (B200_PROFILING.md)"
+    peak_src = "measured MEASURED_PEAKS.json hbm_gbs"
     try:
         with open(PEAKS) as f:
             peak = float(json.load(f)["hbm_gbs"])
-            peak_src = "measured MEASURED_PEAKS.json hbm_gbs"
     except Exception:
-        peak = 6650.0
+        peak, peak_src = 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
     iter_achieved = ITER_BYTES_PER_CELL * M_local * iters / (ms * 1e-3) / 1e9  # per GPU
     if world == 1:
-        # per-kernel CUDA-event times during one live solve (roofline)
+        # per-kernel CUDA-event times during one live solve, on the context's
+        # stream (roofline)
         prof = ctx.profile_solve(RTOL, 10000)
         per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
         dominant = max(("post", "update", "search", "restrict"), key=lambda k: prof[k][0])
         bytes_launch = KERNEL_BYTES_PER_CELL[dominant] * M
         achieved = bytes_launch / (per[dominant] * 1e-3) / 1e9
+        tr = ncu_traffic(dominant, args.config, M)
         roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(dominant),
-                "algorithmic_bytes_per_launch": bytes_launch, "peak_source": peak_src}
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": tr["bytes"] if tr else None,
+                "traffic_source": tr["source"] if tr else "no ncu capture of this config",
+                "algorithmic_bytes_per_launch": bytes_launch,
+                "algorithmic_bytes_per_cell": KERNEL_BYTES_PER_CELL[dominant],
+                "peak_source": peak_src,
+                "kernel_share_of_iteration": prof[dominant][0] / sum(
+                    v[0] for k, v in prof.items() if k in ("post", "update", "search",
+                                                           "restrict", "coarse"))}
     else:
         per = {}
         roof = {"bound": "hbm", "kernel": "whole iteration, per GPU (incl. exchanges)",
@@ -411,48 +541,93 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": ITER_BYTES_PER_CELL * M_local,
                 "peak_source": peak_src}
 
+    extra = None
+    if world == 1 and not args.no_extra:
+        try:
+            extra = {"configs1": configs1_rows(local)}
+        except Exception as e:
+            extra = {"configs1": {"unavailable": str(e)[:200]}}
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, args.config, args.ref_iters)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unavailable": str(e)[:200]}
+        if extra is not None:
+            try:
+                extra["configs1"]["reference"] = reference_tts_config1()
+            except Exception as e:
+                extra["configs1"]["reference"] = {"unavailable": str(e)[:200]}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
-    extra = {
-        "iterations": iters, "setup_ms": 1e3 * rep.setup_seconds,
+    cj = config_json(cfg, args.config, world, {
+        "iterations": iters, "setup_ms": 1e3 * setup_s,
         "setup_wall_ms": 1e3 * setup_wall, "setup_cold_wall_ms": 1e3 * setup_cold_wall,
-        "time_to_solution_ms": 1e3 * rep.setup_seconds + ms,
+        "design_generation_s": gen_s,
+        "time_to_solution_ms": 1e3 * setup_s + ms,
         "true_relative_residual": true_rel,
-        "parallelism": f"z-slabs x{world} over NCCL (one {n}^3 slab per GPU)" if world > 1
-                       else "single-gpu",
+        "true_residual_solve": {"iterations": ver.iterations, "restarts": ver.restarts,
+                                "solve_ms": 1e3 * ver_s,
+                                "true_relative_residual": ver.final_relative_residual,
+                                "time_to_true_rtol_ms": 1e3 * (setup_s + ver_s)},
         "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items() if v},
         "iteration_hbm_gbs_algorithmic_per_gpu": iter_achieved,
-        "device_bytes": ctx.device_bytes()}
-    cj = config_json(cfg, args.config, extra, world)
+        "iteration_bytes_per_cell": ITER_BYTES_PER_CELL,
+        "device_bytes_per_gpu": ctx.device_bytes()})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded box-filter design, BASELINE configs[1])",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": data_label(args.config),
         "config": cj,
         "roofline": roof,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * M_local,
-                "d2h_bytes_per_step": 8 * M_local},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * M,
+                "d2h_bytes_per_step": 8 * M},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
-    if world == 1 and not args.no_side_by_side and args.config == 1:  # M6: config 1's rows
-        line.update(side_by_side(ctx, b, M))
-    if world == 1 and not args.no_cpu_baseline:
-        try:
-            line["cpu_baseline"] = cpu_baseline(cfg, kappa, args.ref_iters)
-        except Exception as e:  # reported, not fatal
-            line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+        if cpu.get("time_to_solution_s") and cpu.get("sample_cells"):
+            cpu["gpu_same_sample"] = gpu_sample_tts(cfg, local)
+    if extra:
+        line.update(extra)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
+def gpu_sample_tts(cfg, device):
+    """The GPU on the CPU baseline's exact sample (same n, generator and
+    hierarchy): warm set-up + solve, for a like-for-like time to solution."""
+    from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions
+    n = min(cfg["n"], SAMPLE_N)
+    ctx = Context(GridSpec(n, n, n), n // (8 * cfg["sd"]), cfg["sd"], device=device)
+    ctx.set_design_generated(cfg["vf"], cfg["kmin"], 1.0, 3,
+                             BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0),
+                             passes=cfg["passes"], radius=cfg["radius"])
+    b = ctx.assemble_rhs(np.ones(n ** 3))
+    opts = MmgOptions(num_cc_basis=cfg.get("lcc", 8), fine_blocks="coarse_cell")
+    ctx.setup("mmg", opts)
+    ctx.setup("mmg", opts)
+    ctx.upload_rhs(b)
+    rep = ctx.solve_resident(RTOL, 10000)
+    ctx.close()
+    return {"iterations": rep.iterations, "setup_ms": 1e3 * rep.setup_seconds,
+            "solve_ms": 1e3 * rep.solve_seconds,
+            "time_to_solution_ms": 1e3 * (rep.setup_seconds + rep.solve_seconds)}
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -74,22 +74,29 @@ typedef struct {
   int warm_start;      /* 1: start the local eigensolver from the previous set-up's
                           bases (same context; a design iteration's re-set-up) */
   int fine_blocks;     /* fine smoother partition (mmg, two_grid):
-                          TMG_FINE_BLOCKS_COARSE_CELL (GPU default) or
-                          TMG_FINE_BLOCKS_CC (build_mmg's fine_blocks_by_cc,
-                          solver.cpp:353-361; cc elements of 8^3 / 16^3 cells) */
+                          TMG_FINE_BLOCKS_CC (0, the default: build_mmg's
+                          fine_blocks_by_cc, solver.cpp:353-361, one exact block per
+                          cc element of 8^3, 16^3 or 32^3 cells; TMG_ENOTSUP for
+                          other sizes or when the block factors exceed device
+                          memory) or TMG_FINE_BLOCKS_COARSE_CELL (1, opt-in: one
+                          block per coarse cell, the fast GPU partition of
+                          DESIGN.md §2; the reference builds it through
+                          build_hierarchy_operators, solver.hpp:132-135) */
 } tmg_mmg_options;
 
-#define TMG_FINE_BLOCKS_COARSE_CELL 0
-#define TMG_FINE_BLOCKS_CC 1
+#define TMG_FINE_BLOCKS_CC 0
+#define TMG_FINE_BLOCKS_COARSE_CELL 1
 
 /* SolveReport (solver.hpp:15-22). */
 typedef struct {
   int iterations;
   int converged;
-  int status; /* 0 running,1 converged,2 max iterations,3 zero rhs,4 indefinite,5 non-finite */
+  int status; /* 0 running,1 converged,2 max iterations,3 zero rhs,4 indefinite,5 non-finite,
+                 6 true residual at the FP64 floor (TMG_SOLVE_TRUE_RESIDUAL) */
   double setup_seconds;
   double solve_seconds;
   double final_relative_residual; /* ||r||/||b|| of the recurrence residual */
+  int restarts;                   /* residual replacements (TMG_SOLVE_TRUE_RESIDUAL) */
 } tmg_report;
 
 /* Context ------------------------------------------------------------------ */
@@ -273,6 +280,10 @@ int tmg_pcg(tmg_ctx* ctx, const double* b, const double* x0, double rtol, int ma
 
 /* y = A x, SparseOperator::apply on the assembled TPFA matrix (sparse.cpp:71-84). */
 int tmg_apply_operator(tmg_ctx* ctx, const double* x, double* y);
+/* y = |A| |x| (every stencil term made nonnegative; no reference
+ * counterpart): eps ||(|A||x|)|| / ||b|| is the rounding floor of any FP64
+ * residual b - A x of x. */
+int tmg_apply_operator_abs(tmg_ctx* ctx, const double* x, double* y);
 /* z = M r, Preconditioner::apply (solver.hpp:28). */
 int tmg_apply_preconditioner(tmg_ctx* ctx, const double* r, double* z);
 
@@ -282,6 +293,19 @@ int tmg_upload_rhs(tmg_ctx* ctx, const double* b);
 int tmg_upload_x0(tmg_ctx* ctx, const double* x0);
 int tmg_solve_resident(tmg_ctx* ctx, double rtol, int max_iterations, int use_x0,
                        tmg_report* report);
+/* tmg_solve_resident with flags. TMG_SOLVE_TRUE_RESIDUAL (no reference
+ * counterpart; the reference stops on the recurrence residual,
+ * solver.cpp:549-560): after the recurrence meets rtol, the true residual
+ * b - A x is formed on the device and, while it exceeds rtol, the solve
+ * restarts from it (residual replacement): at most 4 restarts, and none once
+ * a restart no longer halves it (the FP64 floor eps |A||x| / |b| of the
+ * problem is above rtol: status 6). report->converged then
+ * means TRUE residual <= rtol; final_relative_residual is the true relative
+ * residual of the returned x; iterations and solve_seconds cover every
+ * restart; restarts counts them. The history buffer holds the last restart. */
+#define TMG_SOLVE_TRUE_RESIDUAL 1
+int tmg_solve_resident_ex(tmg_ctx* ctx, double rtol, int max_iterations, int use_x0, int flags,
+                          tmg_report* report);
 int tmg_download_solution(tmg_ctx* ctx, double* x);
 
 /* Introspection / measurement ------------------------------------------- */

@@ -40,12 +40,16 @@ class GpuMmgPreconditioner final : public topmg::Preconditioner {
   // make_preconditioner (solver.cpp:462-481) for all five kinds. The operator
   // is rebuilt matrix-free from system.kappa and system.boundary
   // (fvm.hpp:20-26); system.matrix is not copied to the device. fine_blocks
-  // selects the Mmg / TwoGrid fine smoother partition: TMG_FINE_BLOCKS_CC is
-  // the reference's own (fine_blocks_by_cc, cc elements of 8^3 / 16^3 cells),
-  // TMG_FINE_BLOCKS_COARSE_CELL the GPU default.
+  // selects the Mmg / TwoGrid fine smoother partition: the default
+  // TMG_FINE_BLOCKS_CC is the reference's own (build_mmg's fine_blocks_by_cc,
+  // solver.cpp:353-361; cc elements of 8^3, 16^3 or 32^3 cells), so this
+  // factory is a faithful drop-in for topmg::make_preconditioner;
+  // TMG_FINE_BLOCKS_COARSE_CELL opts into the fast GPU partition (one block
+  // per coarse cell; fewer bytes per V-cycle, a few more
+  // iterations: INTEGRATION.md).
   GpuMmgPreconditioner(topmg::PrecondKind kind, const topmg::AssembledSystem& system,
                        const topmg::HierarchicalGrid& hgrid, const topmg::MmgOptions& opts = {},
-                       int device = 0, int fine_blocks = TMG_FINE_BLOCKS_COARSE_CELL)
+                       int device = 0, int fine_blocks = TMG_FINE_BLOCKS_CC)
       : kind_(kind), n_(system.grid.num_cells()) {
     tmg_grid g{};
     g.nx = system.grid.nx;
@@ -99,7 +103,7 @@ class GpuMmgPreconditioner final : public topmg::Preconditioner {
 inline std::unique_ptr<topmg::Preconditioner> make_preconditioner(
     topmg::PrecondKind kind, const topmg::AssembledSystem& system,
     const topmg::HierarchicalGrid& hgrid, const topmg::MmgOptions& opts = {}, int device = 0,
-    int fine_blocks = TMG_FINE_BLOCKS_COARSE_CELL) {
+    int fine_blocks = TMG_FINE_BLOCKS_CC) {
   return std::make_unique<GpuMmgPreconditioner>(kind, system, hgrid, opts, device, fine_blocks);
 }
 

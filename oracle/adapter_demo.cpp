@@ -27,11 +27,40 @@ int main() {
                                               BoundarySpec::bottom_center_patch(1, 1, 0.2, 0.0));
   const PcgOptions opts{1e-8, 1000};
 
-  auto gpu = topmg_b200::make_preconditioner(PrecondKind::Mmg, sys, h);
-  const PcgResult via_ref_pcg = topmg::pcg(sys.matrix, sys.rhs, *gpu, opts);  // reference loop
-  const PcgResult device = topmg_b200::pcg(sys.matrix, sys.rhs, *gpu, opts);  // device loop
+  bool ok = true;
+  auto rel = [](const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+      num += (a[i] - b[i]) * (a[i] - b[i]);
+      den += b[i] * b[i];
+    }
+    return std::sqrt(num / den);
+  };
+  auto check = [&](const char* what, const PcgResult& ref, const Preconditioner& gpu) {
+    const PcgResult via_ref_pcg = topmg::pcg(sys.matrix, sys.rhs, gpu, opts);  // reference loop
+    const PcgResult device = topmg_b200::pcg(sys.matrix, sys.rhs, gpu, opts);  // device loop
+    std::printf("%s: reference %d it; topmg::pcg + GPU V-cycle %d it, rel %.3e; "
+                "topmg_b200::pcg %d it, rel %.3e (%s)\n",
+                what, ref.report.iterations, via_ref_pcg.report.iterations,
+                rel(via_ref_pcg.x, ref.x), device.report.iterations, rel(device.x, ref.x),
+                device.report.preconditioner.c_str());
+    ok = ok && via_ref_pcg.report.converged && device.report.converged && ref.report.converged;
+    ok = ok && std::abs(via_ref_pcg.report.iterations - ref.report.iterations) <= 1;
+    ok = ok && std::abs(device.report.iterations - ref.report.iterations) <= 1;
+    ok = ok && rel(via_ref_pcg.x, ref.x) < 1e-6 && rel(device.x, ref.x) < 1e-6;
+  };
 
-  // reference MMG with the GPU's partition (per coarse cell / per cc element)
+  // (1) the drop-in's defaults against the reference's own factory defaults
+  // (make_preconditioner -> build_mmg / build_two_grid, fine_blocks_by_cc)
+  for (const PrecondKind kind : {PrecondKind::Mmg, PrecondKind::TwoGrid}) {
+    const auto ref_m = topmg::make_preconditioner(kind, sys, h);
+    const PcgResult ref = topmg::pcg(sys.matrix, sys.rhs, *ref_m, opts);
+    const auto gpu = topmg_b200::make_preconditioner(kind, sys, h);
+    check(kind == PrecondKind::Mmg ? "mmg (defaults)" : "two_grid (defaults)", ref, *gpu);
+  }
+
+  // (2) the opt-in coarse-cell fine blocks against the reference built with
+  // the same partition through its public build_hierarchy_operators
   CoarseSpaces cs = build_coarse_spaces(h, kappa, 4, 8);
   std::vector<std::vector<index_t>> fine, coarse;
   for (index_t e = 0; e < h.num_coarse(); ++e) fine.push_back(h.cells_of_coarse(e));
@@ -44,24 +73,10 @@ int main() {
   MultiscaleHierarchy ref_m = build_hierarchy_operators(
       sys.matrix, std::move(cs.restriction_c), std::move(cs.restriction_cc), fine, coarse, 1);
   const PcgResult ref = topmg::pcg(sys.matrix, sys.rhs, ref_m, opts);
+  auto gpu = topmg_b200::make_preconditioner(PrecondKind::Mmg, sys, h, {}, 0,
+                                             TMG_FINE_BLOCKS_COARSE_CELL);
+  check("mmg (coarse-cell fine blocks)", ref, *gpu);
 
-  auto rel = [&](const std::vector<double>& a) {
-    double num = 0, den = 0;
-    for (std::size_t i = 0; i < a.size(); ++i) {
-      num += (a[i] - ref.x[i]) * (a[i] - ref.x[i]);
-      den += ref.x[i] * ref.x[i];
-    }
-    return std::sqrt(num / den);
-  };
-  std::printf("reference mmg(cell,cc): %d it\n", ref.report.iterations);
-  std::printf("topmg::pcg + GPU V-cycle: %d it, rel %.3e\n", via_ref_pcg.report.iterations,
-              rel(via_ref_pcg.x));
-  std::printf("topmg_b200::pcg (device): %d it, rel %.3e, %s\n", device.report.iterations,
-              rel(device.x), device.report.preconditioner.c_str());
-  bool ok = via_ref_pcg.report.converged && device.report.converged && ref.report.converged;
-  ok = ok && std::abs(via_ref_pcg.report.iterations - ref.report.iterations) <= 1;
-  ok = ok && std::abs(device.report.iterations - ref.report.iterations) <= 1;
-  ok = ok && rel(via_ref_pcg.x) < 1e-6 && rel(device.x) < 1e-6;
   // the exceptions of the reference surface through the adapter
   try {
     topmg_b200::pcg(sys.matrix, std::vector<double>(3, 1.0), *gpu, opts);

@@ -35,6 +35,27 @@ pids+=($!)
 for p in "${pids[@]}"; do wait "$p"; done
 $CXX -shared -pthread -o "$OUT/libtopmg_ref.so" "$OUT"/obj/*.o -lm -ldl
 echo "built $OUT/libtopmg_ref.so"
+# Timing variant for bench.py's CPU arm (-O3 -march=native).
+# Built here for this container's CPU; bench.py probes it in a child process
+# on the GPU box and falls back to the portable build if the ISA is missing.
+NFLAGS="-O3 -march=native -fPIC -pthread"
+mkdir -p "$OUT/obj_native"
+pids=()
+for s in $SRCS; do
+  $CXX -std=c++20 $NFLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$REF/src/$s.cpp" -o "$OUT/obj_native/$s.o" &
+  pids+=($!)
+done
+$CXX -std=c++20 $NFLAGS -I"$REF/include" -I"$HERE/eigen_shim" -c "$HERE/ref_harness.cpp" -o "$OUT/obj_native/ref_harness.o" &
+pids+=($!)
+$CC -std=c11 $NFLAGS -c "$HERE/dense_la.c" -o "$OUT/obj_native/dense_la.o" &
+pids+=($!)
+$CC -std=c11 $NFLAGS -c "$HERE/lapack_glue.c" -o "$OUT/obj_native/lapack_glue.o" &
+pids+=($!)
+for p in "${pids[@]}"; do wait "$p"; done
+$CXX -shared -pthread -o "$OUT/libtopmg_ref_native.so" "$OUT"/obj_native/*.o -lm -ldl
+$CXX -march=native -Q --help=target 2>/dev/null | awk '$1 == "-march=" {print "march=" $2}' \
+  > "$OUT/libtopmg_ref_native.so.march"
+echo "built $OUT/libtopmg_ref_native.so ($(cat "$OUT/libtopmg_ref_native.so.march"))"
 # integration demo of include/topmg_b200.hpp inside the reference code base
 if [ -f "$HERE/../paper_2410_06850_b200/libtopmg_b200.so" ]; then
   $CXX -std=c++20 $FLAGS -I"$REF/include" -I"$HERE/../include" "$HERE/adapter_demo.cpp" \

@@ -485,3 +485,60 @@ def interpolate_design(values_lo, n_lo, n_hi):
     out = np.empty(ghi.nx * ghi.ny * ghi.nz)
     _check(lib().orc_interpolate_design(_d(v), C.byref(glo), C.byref(ghi), _d(out)))
     return out
+
+
+class RefContext:
+    """The reference's set-up kept alive (oracle/_ref, ref_ctx_*): one
+    make_preconditioner / build_hierarchy_operators, then any number of
+    pcg() calls with any rhs and x0 (solver.cpp:483-575). fine_blocks None =
+    the reference's make_preconditioner default (fine_blocks_by_cc)."""
+
+    def __init__(self, shape, ncc, sd, kappa, patches=None, kind="mmg", fine_blocks="cell",
+                 coarse_blocks="cc", lc=4, lcc=8, sweeps=1, extent=None, threads=0):
+        nx, ny, nz = (shape,) * 3 if np.isscalar(shape) else tuple(shape)
+        ncx, ncy, ncz = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
+        ext = extent or (1.0, 1.0, 1.0)
+        R = ref()
+        R.ref_set_num_threads(threads)
+        R.ref_ctx_solve.argtypes = [C.c_void_p, DP, DP, C.c_double, C.c_int, DP, DP,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int), DP]
+        R.ref_ctx_apply.argtypes = [C.c_void_p, DP, DP]
+        self.m = nx * ny * nz
+        pa = _patch_array(patches if patches is not None else bottom_center_patch())
+        ts = C.c_double()
+        fb = -1 if fine_blocks is None else BLOCKS[fine_blocks]
+        cb = -1 if coarse_blocks is None else BLOCKS[coarse_blocks]
+        self.ptr = R.ref_ctx_create_grid(nx, ny, nz, ext[0], ext[1], ext[2], ncx, ncy, ncz, sd,
+                                         _d(np.ascontiguousarray(kappa, np.float64)),
+                                         len(pa) // 6, _d(pa), KIND[kind], fb, cb, lc, lcc,
+                                         sweeps, C.byref(ts))
+        if not self.ptr:
+            raise OracleError(4, R.ref_last_error().decode())
+        self.setup_seconds = ts.value
+        self.threads = R.ref_num_threads()
+
+    def solve(self, b=None, rtol=1e-8, maxit=10000, x0=None):
+        x = np.empty(self.m)
+        hist = np.zeros(max(1, maxit))
+        it, cv, sv = C.c_int(), C.c_int(), C.c_double()
+        bp = _d(np.ascontiguousarray(b, np.float64)) if b is not None else None
+        xp = _d(np.ascontiguousarray(x0, np.float64)) if x0 is not None else None
+        _ref_check(ref().ref_ctx_solve(self.ptr, bp, xp, C.c_double(rtol), C.c_int(maxit), _d(x),
+                                       _d(hist), C.byref(it), C.byref(cv), C.byref(sv)))
+        return PcgResult(x, it.value, bool(cv.value), hist[:it.value].copy(), sv.value)
+
+    def apply(self, x):
+        y = np.empty(self.m)
+        _ref_check(ref().ref_ctx_apply(self.ptr, _d(np.ascontiguousarray(x, np.float64)), _d(y)))
+        return y
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            ref().ref_ctx_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -275,6 +275,42 @@ int ref_ctx_pcg(void* ctx, double rtol, int maxit, double* x_out, int* iteration
   });
 }
 
+// pcg() on the context's operator and preconditioner with any rhs (LS2:
+// adjoint_rhs, optim.cpp:16-19) and optional x0; b == nullptr uses the
+// assembled rhs. history (optional) receives residual_history.
+int ref_ctx_solve(void* ctx, const double* b, const double* x0, double rtol, int maxit,
+                  double* x_out, double* history, int* iterations, int* converged,
+                  double* solve_seconds) {
+  RefCtx* c = static_cast<RefCtx*>(ctx);
+  return guarded([&] {
+    const index_t m = c->sys.matrix.rows();
+    PcgOptions po;
+    po.rtol = rtol;
+    po.max_iterations = maxit;
+    const std::vector<double> bb = b ? std::vector<double>(b, b + m) : c->sys.rhs;
+    std::vector<double> xx0;
+    if (x0) xx0.assign(x0, x0 + m);
+    const PcgResult r = pcg(c->sys.matrix, bb, *c->pre, po, xx0);
+    if (x_out) std::memcpy(x_out, r.x.data(), sizeof(double) * r.x.size());
+    if (history)
+      std::memcpy(history, r.report.residual_history.data(),
+                  sizeof(double) * r.report.residual_history.size());
+    *iterations = r.report.iterations;
+    *converged = r.report.converged ? 1 : 0;
+    *solve_seconds = r.report.solve_seconds;
+  });
+}
+
+// y = A x with the reference's assembled operator (SparseOperator::apply).
+int ref_ctx_apply(void* ctx, const double* x, double* y) {
+  RefCtx* c = static_cast<RefCtx*>(ctx);
+  return guarded([&] {
+    const index_t m = c->sys.matrix.rows();
+    c->sys.matrix.apply(std::span<const double>(x, static_cast<std::size_t>(m)),
+                        std::span<double>(y, static_cast<std::size_t>(m)));
+  });
+}
+
 void ref_ctx_destroy(void* ctx) { delete static_cast<RefCtx*>(ctx); }
 
 // topmg::sensitivity (optim.cpp:21-84) on a design rho with MaterialModel

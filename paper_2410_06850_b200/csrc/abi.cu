@@ -90,6 +90,7 @@ struct Slab {
   double* cc_evals = nullptr;
   double* Winv = nullptr;
   double* Gbj = nullptr;  // block-Jacobi plane Schur inverses (virtual-global per element)
+  double* ybj = nullptr;  // E = 32 block-Jacobi apply: per-cell plane-sweep values
   double *r2 = nullptr, *t2 = nullptr;  // cc-block-smoothed V-cycle: r1 + R_c^T e_c, r - A r2
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
@@ -288,6 +289,7 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.cc_evals);
     dfree_null(c, s.Winv);
     dfree_null(c, s.Gbj);
+    dfree_null(c, s.ybj);
     dfree_null(c, s.r2);
     dfree_null(c, s.t2);
     dfree_null(c, s.rc);
@@ -588,9 +590,10 @@ void enqueue_block_jacobi(tmg_ctx* c, int init, int par_new) {
     if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
   }
   const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+  const int nk = bj_apply_kernels(c->cb, c->g.sd);
   for (Slab& s : c->slabs)
-    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r, s.st,
-                          s.partials, init, c->stream));
+    KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r, s.st,
+                           s.partials, init, s.ybj, c->stream));
   if (c->dist()) {
     reduce_finalize(c, kRedPost, init);
     XCH(z, sizeof(double) * C, false);
@@ -624,9 +627,10 @@ void enqueue_vcycle_bj(tmg_ctx* c, int init, int par_new) {
     if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
   }
   const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+  const int nk = bj_apply_kernels(c->cb, c->g.sd);
   for (Slab& s : c->slabs)
-    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.r1, nullptr,
-                          s.st, s.partials, init, st));
+    KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.r1, nullptr,
+                           s.st, s.partials, init, s.ybj, st));
   if (c->dist()) XCH(r1, sizeof(double) * C, false);
   for (Slab& s : c->slabs)
     KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
@@ -637,8 +641,8 @@ void enqueue_vcycle_bj(tmg_ctx* c, int init, int par_new) {
   if (c->dist()) XCH(r2, sizeof(double) * C, false);
   for (Slab& s : c->slabs) KL(1, launch_resid(s.g, c->cb, s.coef, s.r, s.r2, s.t2, s.st, st));
   for (Slab& s : c->slabs)
-    KL(1, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.t2, s.r2, s.z, s.r, s.st,
-                          s.partials, init, st));
+    KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.t2, s.r2, s.z, s.r, s.st,
+                           s.partials, init, s.ybj, st));
   if (c->dist()) {
     reduce_finalize(c, kRedPost, init);
     XCH(z, sizeof(double) * C, false);
@@ -1638,8 +1642,23 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     return set_err(c, TMG_EARG, "fine_blocks must be TMG_FINE_BLOCKS_COARSE_CELL or _CC");
   if ((kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj) && !bj_supported((int)c->cb, c->g.sd))
     return set_err(c, TMG_ENOTSUP,
-                   "GPU block_jacobi handles cc elements of 8^3 or 16^3 cells (got %lld^3)",
+                   "GPU block_jacobi / cc-element fine blocks handle cc elements of 8^3, 16^3 or "
+                   "32^3 cells (got %lld^3); use fine_blocks = coarse_cell",
                    (long long)(c->cb * c->g.sd));
+  if (kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj) {
+    // the exact per-element factors (E^5 doubles per element) must fit
+    size_t fr = 0, tot = 0;
+    if (cudaSetDevice(c->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+      double need = 0.0;
+      for (const Slab& s : c->slabs)
+        need += 8.0 * (double)s.g.neo * (double)bj_doubles_per_element((int)c->cb, c->g.sd);
+      if (need > 0.9 * (double)(fr + c->bytes))
+        return set_err(c, TMG_ENOTSUP,
+                       "cc-element block factors need %.1f GB (device has %.1f GB); use "
+                       "fine_blocks = coarse_cell",
+                       need / 1e9, (double)tot / 1e9);
+    }
+  }
   if (kind < 0 || kind > 4) return set_err(c, TMG_ECONFIG, "make_preconditioner: unknown kind");
   if (hier) {
     const int64_t cells = (int64_t)c->cb * c->cb * c->cb;
@@ -1692,8 +1711,12 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
       for (Slab& s : c->slabs) {
         s.Gbj = owned_e<double>(c, s, per);
-        launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, c->stream);
+        if (bj_apply_kernels((int)c->cb, c->g.sd) > 1) s.ybj = owned<double>(c, s, C);
+        const int64_t wd = bj_factor_work_doubles((int)c->cb, c->g.sd, s.g.neo);
+        double* w = wd ? dalloc<double>(c, wd) : nullptr;
+        launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, w, c->stream);
         CK(cudaGetLastError());
+        if (w) dfree(c, w);
       }
     } else if (hier) {
       c->lc = (int)o->num_local_basis;
@@ -1713,6 +1736,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         s.eig_iters = owned<int>(c, s, 1);
         if (fine_bj) {
           s.Gbj = owned_e<double>(c, s, bj_doubles_per_element(c->cb, c->g.sd));
+          if (bj_apply_kernels((int)c->cb, c->g.sd) > 1) s.ybj = owned<double>(c, s, C);
           s.r2 = ghosted<double>(c, s, C);
           s.t2 = ghosted<double>(c, s, C);
         } else {
@@ -1803,7 +1827,10 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       for (Slab& s : c->slabs) {
         if (fine_bj) {
           const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
-          launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, c->stream);
+          const int64_t wd = bj_factor_work_doubles((int)c->cb, c->g.sd, s.g.neo);
+          double* w = wd ? dalloc<double>(c, wd) : nullptr;
+          launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, w, c->stream);
+          if (w) dfree(c, w);
         } else {
           launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.Gf, s.d_status, c->stream);
         }
@@ -1952,6 +1979,74 @@ int tmg_solve_resident(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_repor
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
     solve_device(c, rtol, maxit, use_x0, rep, nullptr, nullptr);
+  });
+}
+
+int tmg_solve_resident_ex(tmg_ctx* c, double rtol, int maxit, int use_x0, int flags,
+                          tmg_report* rep) {
+  if (!c) return set_err(c, TMG_EARG, "null context");
+  if (maxit < 0) return set_err(c, TMG_EARG, "pcg: negative max_iterations");
+  tmg_report local{};
+  const int rc = guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    solve_device(c, rtol, maxit, use_x0, &local, nullptr, nullptr);
+    if (!(flags & TMG_SOLVE_TRUE_RESIDUAL) || !local.converged || local.status == kStatusZeroRhs)
+      return;
+    // Residual replacement. A use_x0 solve with max_iterations = 0 runs only
+    // the init kernel: r = b - A x exactly as pcg() forms it for x0
+    // (solver.cpp:515-521), i.e. the TRUE residual of the resident x.
+    int total = local.iterations;
+    double secs = local.solve_seconds, prev = 0.0;
+    for (int k = 0;; ++k) {
+      tmg_report chk{};
+      solve_device(c, rtol, 0, 1, &chk, nullptr, nullptr);
+      secs += chk.solve_seconds;
+      const double tr = chk.final_relative_residual;
+      local.final_relative_residual = tr;
+      if (tr <= rtol) {
+        local.converged = 1;
+        local.status = kStatusConverged;
+        break;
+      }
+      // no progress: the FP64 floor eps |A||x| / |b| of the problem
+      // is above rtol; further restarts cannot go lower
+      if ((k > 0 && tr > 0.5 * prev) || k == 4 || total >= maxit) {
+        local.converged = 0;
+        local.status = (k > 0 && tr > 0.5 * prev) ? kStatusFloor : kStatusMaxIt;
+        break;
+      }
+      prev = tr;
+      tmg_report r2{};
+      solve_device(c, rtol, maxit - total, 1, &r2, nullptr, nullptr);
+      total += r2.iterations;
+      secs += r2.solve_seconds;
+      local.restarts = k + 1;
+      if (!r2.converged) {  // max iterations inside a restart
+        local.converged = 0;
+        local.status = r2.status;
+        local.final_relative_residual = r2.final_relative_residual;
+        break;
+      }
+    }
+    local.iterations = total;
+    local.solve_seconds = secs;
+  });
+  if (rep) *rep = local;
+  return rc;
+}
+
+int tmg_apply_operator_abs(tmg_ctx* c, const double* x, double* y) {
+  if (!c || !x || !y) return set_err(c, TMG_EARG, "tmg_apply_operator_abs: null argument");
+  if (!c->have_problem) return set_err(c, TMG_EARG, "apply: no problem set");
+  return guard(c, [&] {
+    CK(cudaSetDevice(c->device));
+    UP(x, p);
+    XCH(p, sizeof(double) * cells_per_brick(c), false);
+    for (Slab& s : c->slabs) {
+      launch_apply_abs(s.g, c->cb, s.coef, s.p, s.q, c->stream);
+      CK(cudaGetLastError());
+    }
+    DOWN(q, y);
   });
 }
 

@@ -14,6 +14,15 @@
 //   y_k = G_k (r_k + D_k y_{k-1}),  x_k = y_k + G_k D_{k+1} x_{k+1}.
 // Storage G[e][k][P][P] (symmetric, full): 4.3 GB at 128^3 / c = 8 / sd = 2.
 // Each apply streams it once (two GEMVs per plane): an HBM-bound baseline.
+//
+// E = 32 (32^3-cell elements: c = 8 with sd = 4, the configs[3] hierarchy;
+// c = 4 with sd = 8): P = 1024, 8 MB per plane, 256 MB per element. The
+// planes are stored plane-major G[k][e][P][P] so the E Schur complements of
+// one plane index form one batch for the tensor-core Gauss-Jordan
+// (dense_spd_inverse_batched); the LDL^T pivots of all E planes of an element
+// are folded into one min / max so the reference's rule (pivot <= 1e-14 max
+// over the block) applies per block. The apply runs one launch per plane
+// step, each CTA computing a 128-column slice of one element's GEMV.
 #include "gj_global.cuh"
 #include "kernels.h"
 #include "pcg_fin.cuh"
@@ -195,9 +204,175 @@ __global__ void __launch_bounds__(CB * CB * CB) k_resid(GridParams g, const doub
   t[s] = r[s] - apply_coef<CB>(cs, xt, li, lj, lk);
 }
 
+// ------------------------------------------------------ E = 32 (P = 1024)
+constexpr int kE32 = 32, kP32 = kE32 * kE32, kSlice = 128, kSlices = kP32 / kSlice;
+
+// Plane k's matrix for every owned element: A_kk - D_k G_{k-1} D_k
+// (G_{k-1} already inverted in place). grid (P / 4, neo), 256 threads.
+__global__ void __launch_bounds__(256) k_bj32_assemble(GridParams g, int cb,
+                                                       const double* __restrict__ coef,
+                                                       const double* __restrict__ Gp, double* Gk,
+                                                       int k) {
+  constexpr int E = kE32, P = kP32;
+  const int64_t el = blockIdx.y, e = el + g.e0, M = g.mst;
+  const int row0 = blockIdx.x * 4;  // 4 rows per CTA
+  for (int idx = row0 * P + threadIdx.x; idx < (row0 + 4) * P; idx += 256) {
+    const int a = idx / P, b = idx % P;
+    const int ia = a % E, ja = a / E, ib = b % E, jb = b / E;
+    double v = 0.0;
+    if (a == b) {
+      v = coef[3 * M + elem_cell(g, cb, e, ia, ja, k)];
+    } else if (ja == jb && (ib == ia + 1 || ia == ib + 1)) {
+      v = -coef[elem_cell(g, cb, e, min(ia, ib), ja, k)];
+    } else if (ia == ib && (jb == ja + 1 || ja == jb + 1)) {
+      v = -coef[M + elem_cell(g, cb, e, ia, min(ja, jb), k)];
+    }
+    if (k > 0) {
+      const double da = coef[2 * M + elem_cell(g, cb, e, ia, ja, k - 1)];
+      const double db = coef[2 * M + elem_cell(g, cb, e, ib, jb, k - 1)];
+      v -= da * Gp[(size_t)el * P * P + idx] * db;
+    }
+    Gk[(size_t)el * P * P + idx] = v;
+  }
+}
+
+// fold plane k's pivots into the element's extrema (ext[2 e] = min, +1 = max)
+__global__ void k_bj32_fold(const double* __restrict__ work, int64_t stride, int64_t off,
+                            double* ext, int k) {
+  const int64_t el = blockIdx.x;
+  const double* piv = work + el * stride + off;
+  __shared__ double rmn[32], rmx[32];
+  double mn = 1e300, mx = 0.0;
+  for (int i = threadIdx.x; i < kP32; i += blockDim.x) {
+    mn = fmin(mn, piv[i]);
+    mx = fmax(mx, fabs(piv[i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    rmn[threadIdx.x >> 5] = mn;
+    rmx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mn = fmin(mn, rmn[w]);
+      mx = fmax(mx, rmx[w]);
+    }
+    mn = fmin(mn, rmn[0]);
+    mx = fmax(mx, rmx[0]);
+    if (k == 0) {
+      ext[2 * el] = mn;
+      ext[2 * el + 1] = mx;
+    } else {
+      ext[2 * el] = fmin(ext[2 * el], mn);
+      ext[2 * el + 1] = fmax(ext[2 * el + 1], mx);
+    }
+  }
+}
+
+// the reference's singular-pivot rule over the whole block (solver.cpp:86-92)
+__global__ void k_bj32_check(const double* __restrict__ ext, int64_t neo, int* status) {
+  for (int64_t el = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; el < neo;
+       el += (int64_t)gridDim.x * blockDim.x)
+    if (!(ext[2 * el] > 1e-14 * ext[2 * el + 1])) atomicExch(status, 1);
+}
+
+// One plane step of the block Thomas apply, grid (kSlices, neo), 1024
+// threads: thread (qg, col) sums G_k[q][col] v[q] over 128 q of group qg.
+//   fwd (bwd = 0): y_k = G_k (in_k + D_k y_{k-1})      -> ybuf plane k
+//   bwd (bwd = 1): x_k = y_k + G_k (D_{k+1} x_{k+1})   -> ybuf plane k
+__global__ void __launch_bounds__(1024) k_bj32_step(GridParams g, int cb,
+                                                    const double* __restrict__ coef,
+                                                    const double* __restrict__ G,
+                                                    const double* __restrict__ in, double* ybuf,
+                                                    const PcgState* st, int k, int bwd) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  constexpr int E = kE32, P = kP32;
+  __shared__ double v[P];
+  __shared__ double part[kSlices][kSlice];
+  const int t = threadIdx.x;
+  const int64_t el = blockIdx.y, e = el + g.e0, M = g.mst;
+  for (int q = t; q < P; q += 1024) {
+    const int i = q % E, j = q / E;
+    double val;
+    if (!bwd) {
+      val = in[elem_cell(g, cb, e, i, j, k)];
+      if (k > 0) {
+        const size_t sp = elem_cell(g, cb, e, i, j, k - 1);
+        val += coef[2 * M + sp] * ybuf[sp];
+      }
+    } else {
+      val = coef[2 * M + elem_cell(g, cb, e, i, j, k)] * ybuf[elem_cell(g, cb, e, i, j, k + 1)];
+    }
+    v[q] = val;
+  }
+  __syncthreads();
+  const int col = blockIdx.x * kSlice + (t % kSlice), qg = t / kSlice;
+  const double* Gk = G + ((size_t)k * g.neo + el) * P * P + col;
+  const int q0 = qg * (P / kSlices);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 2
+  for (int q = q0; q < q0 + P / kSlices; q += 4) {
+    s0 = fma(Gk[(size_t)q * P], v[q], s0);
+    s1 = fma(Gk[(size_t)(q + 1) * P], v[q + 1], s1);
+    s2 = fma(Gk[(size_t)(q + 2) * P], v[q + 2], s2);
+    s3 = fma(Gk[(size_t)(q + 3) * P], v[q + 3], s3);
+  }
+  part[qg][t % kSlice] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (t < kSlice) {
+    double tot = 0.0;
+#pragma unroll
+    for (int w = 0; w < kSlices; ++w) tot += part[w][t];
+    const size_t so = elem_cell(g, cb, e, col % E, col / E, k);
+    ybuf[so] = bwd ? ybuf[so] + tot : tot;
+  }
+}
+
+// out = add + x (x in ybuf) over the owned bricks; with rdot, rdot . out
+// finishes the iteration (fin_post) like k_bj_apply
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_bj32_finish(GridParams g,
+                                                             const double* __restrict__ ybuf,
+                                                             const double* __restrict__ add,
+                                                             double* out,
+                                                             const double* __restrict__ rdot,
+                                                             PcgState* st, double* partials,
+                                                             int init) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->done) return;
+  constexpr int C = CB * CB * CB;
+  __shared__ double red[80];
+  __shared__ int flag;
+  const size_t s = (size_t)(blockIdx.x + g.b0) * C + threadIdx.x;
+  const double o = add ? add[s] + ybuf[s] : ybuf[s];
+  out[s] = o;
+  if (!rdot) return;
+  double vv[1] = {rdot[s] * o};
+  block_sum_k<C, 1>(vv, red);
+  double tot[1];
+  if (grid_reduce_last_k<1>(vv, partials, &st->ticket[5], tot, &flag, red) && threadIdx.x == 0) {
+    if (g.dist) st->loc[kRedPost] = tot[0];
+    else fin_post(st, tot[0], init);
+  }
+}
+
 bool bj_supported(int cb, int sd) {
   const int E = cb * sd;
-  return E == 8 || E == 16;
+  return E == 8 || E == 16 || E == kE32;
+}
+
+int bj_apply_kernels(int cb, int sd) { return cb * sd == kE32 ? 2 * kE32 : 1; }
+
+int64_t bj_factor_work_doubles(int cb, int sd, int64_t neo) {
+  if (cb * sd != kE32) return 0;
+  return neo * (dense_inverse_work_doubles(kP32) + 2);
 }
 
 int64_t bj_doubles_per_element(int cb, int sd) {
@@ -206,8 +381,22 @@ int64_t bj_doubles_per_element(int cb, int sd) {
 }
 
 void launch_bj_factor(const GridParams& g, int cb, const double* coef, double* G, int* status,
-                      cudaStream_t s) {
+                      double* work, cudaStream_t s) {
   const int E = cb * g.sd, P = E * E;
+  if (E == kE32) {
+    const int64_t plane = g.neo * (int64_t)P * P;
+    double* ext = work + g.neo * dense_inverse_work_doubles(P);
+    for (int k = 0; k < E; ++k) {
+      double* Gk = G + k * plane;
+      k_bj32_assemble<<<dim3(P / 4, (unsigned)g.neo), 256, 0, s>>>(g, cb, coef,
+                                                                  k ? Gk - plane : nullptr, Gk, k);
+      dense_spd_inverse_batched(Gk, P, g.neo, work, status, s);
+      k_bj32_fold<<<(unsigned)g.neo, 256, 0, s>>>(work, dense_inverse_work_doubles(P),
+                                                  dense_inverse_pivots(work, P, 0) - work, ext, k);
+    }
+    k_bj32_check<<<(unsigned)((g.neo + 255) / 256), 256, 0, s>>>(ext, g.neo, status);
+    return;
+  }
   const size_t smem = gj_global_smem_bytes(P);
   cudaFuncSetAttribute(k_bj_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_bj_factor<<<(unsigned)g.neo, kGjThreads, smem, s>>>(g, cb, E, coef, G, status);
@@ -215,8 +404,24 @@ void launch_bj_factor(const GridParams& g, int cb, const double* coef, double* G
 
 void launch_bj_apply(const GridParams& g, int cb, const double* coef, const double* G,
                      const double* in, const double* add, double* out, const double* rdot,
-                     PcgState* st, double* partials, int init, cudaStream_t s) {
+                     PcgState* st, double* partials, int init, double* ybuf, cudaStream_t s) {
   const int E = cb * g.sd;
+  if (E == kE32) {
+    const dim3 grid(kSlices, (unsigned)g.neo);
+    for (int k = 0; k < E; ++k)
+      launch_pdl(k_bj32_step, grid, dim3(1024), 0, s, g, cb, coef, G, in, ybuf,
+                 (const PcgState*)st, k, 0);
+    for (int k = E - 2; k >= 0; --k)
+      launch_pdl(k_bj32_step, grid, dim3(1024), 0, s, g, cb, coef, G, in, ybuf,
+                 (const PcgState*)st, k, 1);
+    if (cb == 8)
+      launch_pdl(k_bj32_finish<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, (const double*)ybuf,
+                 add, out, rdot, st, partials, init);
+    else
+      launch_pdl(k_bj32_finish<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, (const double*)ybuf,
+                 add, out, rdot, st, partials, init);
+    return;
+  }
   if (E == 16)
     launch_pdl(k_bj_apply<16>, dim3((unsigned)g.neo), dim3(256), 0, s, g, cb, coef, G, in, add,
                out, rdot, st, partials, init);

@@ -417,6 +417,11 @@ void dense_spd_inverse_batched(double* A, int64_t n, int64_t batch, double* work
 // (+ NB: the identity-padded last pivot block writes NB pivots)
 int64_t dense_inverse_work_doubles(int64_t n) { return NB * NB + 2 * (int64_t)NB * n + n + NB; }
 
+// the n LDL^T pivots of batch matrix z after dense_spd_inverse_batched
+const double* dense_inverse_pivots(const double* work, int64_t n, int64_t z) {
+  return work + z * dense_inverse_work_doubles(n) + NB * NB + 2 * (int64_t)NB * n;
+}
+
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
                  cudaStream_t s) {
   k_gemv<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(done, A, n, n, x, y);

@@ -51,6 +51,7 @@ enum : int {
   kStatusZeroRhs = 3,
   kStatusIndefinite = 4,
   kStatusNonFinite = 5,
+  kStatusFloor = 6,  // TMG_SOLVE_TRUE_RESIDUAL: true residual stuck above rtol
 };
 
 // Device-resident CG scalars (one per solve context).
@@ -89,6 +90,9 @@ void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int n
                         double ly, double lz, const double* rho, const double* kappa,
                         const double* t, const double* u, double kappa_lo, double kappa_hi,
                         double f0, int p, double* grad, cudaStream_t s);
+// y = |A| |x| (entrywise absolute values; the FP64 residual floor)
+void launch_apply_abs(const GridParams& g, int cb, const double* coef, const double* x, double* y,
+                      cudaStream_t s);
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s);
 
@@ -164,6 +168,7 @@ void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac,
 // dense.cu
 void dense_spd_inverse(double* A, int64_t n, double* work, int* status, cudaStream_t s);
 int64_t dense_inverse_work_doubles(int64_t n);
+const double* dense_inverse_pivots(const double* work, int64_t n, int64_t z);
 void dense_spd_inverse_batched(double* A, int64_t n, int64_t batch, double* work, int* status,
                                cudaStream_t s);
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,
@@ -244,11 +249,18 @@ void launch_mma_primal(const double* x, const double* grad, const double* low, c
 // block-Jacobi with one block per cc element (block_jacobi.cu)
 bool bj_supported(int cb, int sd);
 int64_t bj_doubles_per_element(int cb, int sd);
+// kernels one launch_bj_apply enqueues (1, or 2E for the per-plane E = 32 path)
+int bj_apply_kernels(int cb, int sd);
+// doubles of scratch the E = 32 factor (inverse work + pivot extrema) and apply
+// (one value per owned cell) need; 0 for E <= 16
+int64_t bj_factor_work_doubles(int cb, int sd, int64_t neo);
+// work: bj_factor_work_doubles (E = 32 only, else unused)
 void launch_bj_factor(const GridParams& g, int cb, const double* coef, double* G, int* status,
-                      cudaStream_t s);
+                      double* work, cudaStream_t s);
+// ybuf: one value per owned cell, brick layout (virtual global; E = 32 only)
 void launch_bj_apply(const GridParams& g, int cb, const double* coef, const double* G,
                      const double* in, const double* add, double* out, const double* rdot,
-                     PcgState* st, double* partials, int init, cudaStream_t s);
+                     PcgState* st, double* partials, int init, double* ybuf, cudaStream_t s);
 void launch_prolong_add(const GridParams& g, int cb, const double* phi, const double* r1,
                         const double* ec, double* r2, const PcgState* st, cudaStream_t s);
 void launch_resid(const GridParams& g, int cb, const double* coef, const double* r,

@@ -206,6 +206,32 @@ __global__ void __launch_bounds__(CB * CB * CB) k_apply(GridParams g, const doub
   if (dinv) dinv[s] = 1.0 / cs.dg[t];  // solver.cpp:27
 }
 
+// y = |A| |x|: every term of the row sum made nonnegative (the scale of the
+// rounding error of b - A x, eps |A||x|).
+template <int CB>
+__global__ void __launch_bounds__(CB * CB * CB) k_apply_abs(GridParams g,
+                                                           const double* __restrict__ coef,
+                                                           int64_t M, const double* __restrict__ x,
+                                                           double* y) {
+  __shared__ CoefSmem<CB> cs;
+  __shared__ double xt[Tile<CB>::N];
+  constexpr int C = CB * CB * CB;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  load_coefs<CB>(coef, M, cs, g, bc);
+  load_tile<CB, true>(x, xt, g, bc);
+  __syncthreads();
+  const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
+  constexpr int E = Tile<CB>::E;
+  const int ti = Tile<CB>::idx(li, lj, lk);
+  const double* pz = lk > 0 ? cs.cz + (t - CB * CB) : cs.hz + (li + CB * lj);
+  const double* py = lj > 0 ? cs.cy + (t - CB) : cs.hy + (li + CB * lk);
+  const double* px = li > 0 ? cs.cx + (t - 1) : cs.hx + (lj + CB * lk);
+  double v = fabs(*pz * xt[ti - E * E]) + fabs(*py * xt[ti - E]) + fabs(*px * xt[ti - 1]) +
+             fabs(cs.dg[t] * xt[ti]) + fabs(cs.cx[t] * xt[ti + 1]) + fabs(cs.cy[t] * xt[ti + E]) +
+             fabs(cs.cz[t] * xt[ti + E * E]);
+  y[bofs(bc.b, C) + t] = v;
+}
+
 static int grid1d(int64_t m) {
   int64_t b = (m + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -259,6 +285,14 @@ void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int n
   const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
   k_sensitivity<<<grid1d(m), 256, 0, s>>>(g, cb, ps, rho, kappa, t, u, kappa_lo, kappa_hi, f0, p,
                                           grad, g.b0 * C, m);
+}
+void launch_apply_abs(const GridParams& g, int cb, const double* coef, const double* x, double* y,
+                      cudaStream_t s) {
+  const int64_t M = g.mst;
+  if (cb == 8)
+    k_apply_abs<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, x, y);
+  else
+    k_apply_abs<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, x, y);
 }
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s) {

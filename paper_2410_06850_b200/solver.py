@@ -60,7 +60,7 @@ class _Opts(C.Structure):
 class _Report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("status", C.c_int),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
-                ("final_relative_residual", C.c_double)]
+                ("final_relative_residual", C.c_double), ("restarts", C.c_int)]
 
 
 class _SimpOpts(C.Structure):
@@ -128,7 +128,7 @@ EXPORTED_SYMBOLS = (
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
     "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
-    "tmg_set_design_generated",
+    "tmg_set_design_generated", "tmg_solve_resident_ex", "tmg_apply_operator_abs",
 )
 
 
@@ -215,12 +215,14 @@ class MmgOptions:
     eig_degree: int = 0
     eig_max_outer: int = 0
     warm_start: bool = False  # start the local eigensolver from the previous set-up's bases
-    # fine smoother partition: "coarse_cell" (GPU default) or "cc" (the reference
-    # build_mmg's fine_blocks_by_cc, solver.cpp:353-361)
-    fine_blocks: str = "coarse_cell"
+    # fine smoother partition (mmg, two_grid): "cc", the default, is the
+    # reference build_mmg's fine_blocks_by_cc (solver.cpp:353-361; cc elements
+    # of 8^3, 16^3 or 32^3 cells on the GPU); "coarse_cell" opts into one
+    # exact block per coarse cell, the fast GPU partition
+    fine_blocks: str = "cc"
 
     def _c(self, kind):
-        fb = {"coarse_cell": 0, "cc": 1}
+        fb = {"cc": 0, "coarse_cell": 1}
         if self.fine_blocks not in fb:
             raise ValueError(f"fine_blocks must be one of {list(fb)}")
         return _Opts(kind, self.num_local_basis, self.num_cc_basis, self.smoother_sweeps,
@@ -239,6 +241,7 @@ class SolveReport:
     solve_seconds: float = 0.0
     status: int = 0
     final_relative_residual: float = 0.0
+    restarts: int = 0  # residual replacements (solve_resident(true_residual=True))
 
 
 @dataclass
@@ -375,7 +378,8 @@ class Context:
 
     # SIMP design loop (BASELINE configs[2]; include/topmg_b200.h tmg_simp_*)
     def simp_init(self, volfrac=0.3, rmin=1.5, move=0.2, kappa_lo=1e-6, kappa_hi=1.0, p=3,
-                  source=1.0, rtol=1e-8, maxit=10000, rho0=None, mmg: MmgOptions = MmgOptions()):
+                  source=1.0, rtol=1e-8, maxit=10000, rho0=None,
+                  mmg: MmgOptions = MmgOptions(fine_blocks="coarse_cell")):
         o = _SimpOpts(volfrac, rmin, move, kappa_lo, kappa_hi, p, source, rtol, maxit)
         m = mmg._c(PrecondKind.parse("mmg"))
         r0 = _ptr(_f64(rho0)) if rho0 is not None else None
@@ -441,6 +445,19 @@ class Context:
         self._check(native().tmg_apply_operator(self._p, _ptr(xx), _ptr(y)))
         return y
 
+    def apply_operator_abs(self, x):
+        """|A| |x| (tmg_apply_operator_abs)."""
+        xx = _f64(x)
+        y = np.empty_like(xx)
+        self._check(native().tmg_apply_operator_abs(self._p, _ptr(xx), _ptr(y)))
+        return y
+
+    def residual_floor(self, x, b):
+        """eps ||(|A||x|)|| / ||b||: the rounding floor of any FP64 residual
+        b - A x of x ("true residual")."""
+        return float(np.finfo(np.float64).eps / 2 * np.linalg.norm(self.apply_operator_abs(x))
+                     / np.linalg.norm(b))
+
     def apply_preconditioner(self, r):
         rr = _f64(r)
         z = np.empty_like(rr)
@@ -466,17 +483,24 @@ class Context:
         return SolveReport(self.kind_name or "", rep.iterations, bool(rep.converged),
                            hist[:rep.iterations].copy() if hist is not None else np.zeros(0),
                            rep.setup_seconds, rep.solve_seconds, rep.status,
-                           rep.final_relative_residual)
+                           rep.final_relative_residual, rep.restarts)
 
     # resident (bench)
     def upload_rhs(self, b):
         self._check(native().tmg_upload_rhs(self._p, _ptr(_f64(b))))
 
-    def solve_resident(self, rtol, max_iterations, use_x0=False) -> SolveReport:
+    def solve_resident(self, rtol, max_iterations, use_x0=False,
+                       true_residual=False) -> SolveReport:
+        """PCG on the resident rhs. The default is the reference's recurrence
+        stopping rule. true_residual=True: residual replacement until
+        ||b - A x|| / ||b|| <= rtol (tmg_solve_resident_ex,
+        TMG_SOLVE_TRUE_RESIDUAL): converged and final_relative_residual then
+        refer to the TRUE residual; status 6 = stuck at the FP64 floor."""
         rep = _Report()
-        self._check(native().tmg_solve_resident(self._p, C.c_double(rtol),
-                                                C.c_int(max_iterations), C.c_int(int(use_x0)),
-                                                C.byref(rep)))
+        self._check(native().tmg_solve_resident_ex(self._p, C.c_double(rtol),
+                                                   C.c_int(max_iterations), C.c_int(int(use_x0)),
+                                                   C.c_int(1 if true_residual else 0),
+                                                   C.byref(rep)))
         return self._report(rep)
 
     def download_solution(self):

@@ -42,8 +42,9 @@ def test_optimize_matches_reference(levels, iters, vstar, kmin):
 
 
 def test_optimize_gpu_default_blocks_and_warm_start():
-    """The GPU's default fine blocks (one per coarse cell) and the warm-started
-    variant follow the same design trajectory (the solves agree to rtol)."""
+    """The default (reference) fine blocks, one per cc element, and the
+    warm-started variant follow the same design trajectory (the solves agree
+    to rtol)."""
     cfg = OptimConfig(vstar=0.3, schedule=[GridSpec(32, 32, 32)], iters_per_level=[5],
                       ncc=(2, 2, 2), sd=2, rtol=1e-8)
     a = optimize(cfg, MaterialModel(1e-3), BC)

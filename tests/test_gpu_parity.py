@@ -34,6 +34,10 @@ def ctx_for(n, ncc, sd, kappa, bc=BC, grid=None):
     return c
 
 
+# the GPU's coarse-cell fine blocks, compared with the oracle's "cell" partition
+CELL = MmgOptions(fine_blocks="coarse_cell")
+
+
 def iters_close(a, b):
     return abs(a - b) <= max(1, int(0.1 * b))
 
@@ -143,7 +147,7 @@ def test_two_grid_large_q_vs_oracle(n, ncc, sd, kmin):
                   coarse_blocks="cc")
     ref = O.pcg(s, s.rhs, m, rtol=1e-8)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("two_grid")
+    c.setup("two_grid", CELL)
     r = c.pcg(s.rhs, rtol=1e-8)
     assert r.report.converged
     assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
@@ -155,18 +159,38 @@ def test_hierarchy_variant_limits():
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 1, 8, kappa)  # q = 2048
     with pytest.raises(NotSupportedError, match="two_grid"):
-        c.setup("two_grid")
-    c = ctx_for(64, 2, 4, problem(64, 1e-3)[1])  # 32^3-cell cc elements
-    with pytest.raises(NotSupportedError, match="block_jacobi"):
-        c.setup("mmg", MmgOptions(fine_blocks="cc"))
+        c.setup("two_grid", CELL)
+    c = ctx_for(64, 1, 8, problem(64, 1e-3)[1])  # 64^3-cell cc elements
+    with pytest.raises(NotSupportedError, match="coarse_cell"):
+        c.setup("mmg")  # the reference default partition: factors of 8.6 GB per element
 
 
 def test_block_jacobi_limits():
     n = 64
     _, kappa = problem(n, 1e-3)
-    c = ctx_for(n, 2, 4, kappa)  # 32^3-cell blocks
+    c = ctx_for(n, 1, 8, kappa)  # 64^3-cell blocks
     with pytest.raises(NotSupportedError, match="block_jacobi"):
         c.setup("block_jacobi")
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("kind", ["mmg", "two_grid", "block_jacobi"])
+def test_cc_blocks_32_vs_reference_defaults(kind):
+    """32^3-cell cc elements (sd = 4 at c = 8: the configs[3] hierarchy): the
+    GPU's default fine partition against the compiled reference's own
+    make_preconditioner (fine_blocks_by_cc, SimplicialLDLT per element)."""
+    n, ncc, sd = 64, 2, 4
+    _, kappa = problem(n, 1e-3)
+    ref = O.RefContext(n, ncc, sd, kappa, kind=kind, fine_blocks=None, coarse_blocks=None)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup(kind)  # defaults: the reference's partition
+    b = c.assemble_rhs(np.ones(n ** 3))
+    rr = ref.solve(b, rtol=1e-8, maxit=5000)
+    r = c.pcg(b, rtol=1e-8, max_iterations=5000)
+    assert r.report.converged and rr.converged
+    assert iters_close(r.report.iterations, rr.iterations), (r.report.iterations, rr.iterations)
+    assert np.linalg.norm(r.x - rr.x) <= 1e-6 * np.linalg.norm(rr.x)
 
 
 @pytest.mark.parametrize("n,ncc,sd,kmin", [(16, 2, 2, 1e-3), (16, 2, 2, 1e-6), (32, 2, 2, 1e-3),
@@ -180,7 +204,7 @@ def test_mmg_pcg_vs_oracle(n, ncc, sd, kmin):
                   coarse_blocks="cc")
     ref = O.pcg(s, s.rhs, m, rtol=1e-8)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     r = c.pcg(s.rhs, rtol=1e-8)
     assert r.report.converged
     assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
@@ -249,7 +273,7 @@ def _rc_from_gpu(c, n, ncc, sd):
 def test_local_bases_vs_oracle(n, ncc, sd, kmin):
     _, kappa = problem(n, kmin)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     phi, ev, it = c.local_bases()
     assert (it >= 0).all(), "local eigensolver did not converge"
     h = O.hierarchy(O.grid(n), ncc, sd)
@@ -276,7 +300,7 @@ def test_coarse_operator_is_galerkin_product():
     n, ncc, sd = 32, 2, 2
     _, kappa = problem(n, 1e-6)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     A = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH).matrix
     Rc, _, _ = _rc_from_gpu(c, n, ncc, sd)
     Ac_ref = (Rc @ A @ Rc.T).toarray()
@@ -312,7 +336,7 @@ def _numpy_vcycle(A, Rc, Rcc, fine_blocks, coarse_blocks, r):
 def test_vcycle_matches_numpy_reference(n, ncc, sd, kmin):
     _, kappa = problem(n, kmin)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     A = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH).matrix
     Rc, _, _ = _rc_from_gpu(c, n, ncc, sd)
     Rcc = c.cc_restriction()
@@ -364,7 +388,7 @@ def test_cc_basis_large_q_matches_oracle(n, ncc, sd, kmin):
                   coarse_blocks="cc")
     P_ref = (m.op(2) @ m.op(1)).toarray()
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     Rc, _, _ = _rc_from_gpu(c, n, ncc, sd)
     Rcc = c.cc_restriction()
     P = (Rc.T @ Rcc.T).T
@@ -394,7 +418,7 @@ def test_large_q_wide_subspace_vs_oracle(n, ncc, sd, lcc, kmin):
                   coarse_blocks="cc")
     ref = O.pcg(s, s.rhs, m, rtol=1e-8)
     c = ctx_for(n, ncc, sd, kappa)
-    c.setup("mmg", MmgOptions(num_cc_basis=lcc))
+    c.setup("mmg", MmgOptions(num_cc_basis=lcc, fine_blocks="coarse_cell"))
     r = c.pcg(s.rhs, rtol=1e-8)
     assert r.report.converged
     assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
@@ -411,8 +435,8 @@ def test_large_q_limits():
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 1, 4, kappa)
     with pytest.raises(NotSupportedError, match="num_cc_basis"):
-        c.setup("mmg", MmgOptions(num_cc_basis=21))
-    c.setup("mmg", MmgOptions(num_cc_basis=12))
+        c.setup("mmg", MmgOptions(num_cc_basis=21, fine_blocks="coarse_cell"))
+    c.setup("mmg", MmgOptions(num_cc_basis=12, fine_blocks="coarse_cell"))
     r = c.pcg(np.ones(n ** 3), rtol=1e-8)
     assert r.report.converged
 
@@ -421,7 +445,7 @@ def test_preconditioner_symmetric_positive_definite():
     n = 32
     _, kappa = problem(n, 1e-6)
     c = ctx_for(n, 2, 2, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     rng = np.random.default_rng(4)
     r1, r2 = rng.standard_normal((2, n ** 3))
     z1, z2 = c.apply_preconditioner(r1), c.apply_preconditioner(r2)
@@ -443,7 +467,7 @@ def test_zero_rhs_returns_zero():
     n = 16
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 2, 2, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     r = c.pcg(np.zeros(n ** 3), x0=np.ones(n ** 3))  # solver.cpp:506-513
     assert r.report.converged and r.report.iterations == 0
     assert not r.x.any()
@@ -453,7 +477,7 @@ def test_exact_initial_guess_zero_iterations():
     n = 16
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 2, 2, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(n ** 3))
     x = c.pcg(b, rtol=1e-12).x
     r = c.pcg(b, rtol=1e-6, x0=x)  # solver.cpp:523-531
@@ -466,7 +490,7 @@ def test_max_iterations_not_converged(maxit):
     n = 16
     _, kappa = problem(n, 1e-3)
     c = ctx_for(n, 2, 2, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(n ** 3))
     r = c.pcg(b, rtol=1e-14, max_iterations=maxit)  # solver.hpp:179-182
     assert not r.report.converged and r.report.iterations == maxit
@@ -486,11 +510,11 @@ def test_warm_start_interpolated_coarse_solution():
     rho_hi = O.interpolate_design(inputs.box_filter_design(lo, 0.3), lo, hi)
     k_hi = inputs.conductivity(rho_hi, 1e-3)
     c_lo = ctx_for(lo, 2, 2, k_lo)
-    c_lo.setup("mmg")
+    c_lo.setup("mmg", CELL)
     x_lo = c_lo.pcg(c_lo.assemble_rhs(np.ones(lo ** 3)), rtol=1e-10).x
     x0 = O.interpolate_design(x_lo, lo, hi)
     c = ctx_for(hi, 2, 2, k_hi)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(hi ** 3))
     cold = c.pcg(b, rtol=1e-8)
     warm = c.pcg(b, rtol=1e-8, x0=x0)
@@ -520,10 +544,10 @@ def test_configuration_errors():
     with pytest.raises(ConfigError, match="MaterialModel"):
         c.set_design(np.zeros(n ** 3), 0.0, 1.0, 3, BC)
     with pytest.raises(ValueError, match="no problem"):
-        c.setup("mmg")
+        c.setup("mmg", CELL)
     c.set_conductivity(kappa, BC)
     with pytest.raises(ValueError, match="more eigenvectors"):
-        c.setup("mmg", MmgOptions(num_cc_basis=33))
+        c.setup("mmg", MmgOptions(num_cc_basis=33, fine_blocks="coarse_cell"))
     with pytest.raises(ValueError, match="fine_blocks"):
         c.setup("mmg", MmgOptions(fine_blocks="bogus"))
     with pytest.raises(ValueError, match="no preconditioner"):
@@ -537,7 +561,7 @@ def test_solves_are_deterministic():
     n = 32
     _, kappa = problem(n, 1e-6)
     c = ctx_for(n, 2, 2, kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(n ** 3))
     a1, a2 = c.pcg(b, rtol=1e-8), c.pcg(b, rtol=1e-8)
     np.testing.assert_array_equal(a1.x, a2.x)
@@ -564,7 +588,7 @@ def test_config1_full_size_properties():
     n = cfg["n"]
     _, kappa = problem(n, cfg["kmin"])
     c = ctx_for(n, cfg["ncc"], cfg["sd"], kappa)
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(n ** 3))
     r = c.pcg(b, rtol=1e-8)
     assert r.report.converged and 15 <= r.report.iterations <= 80
@@ -608,7 +632,7 @@ def test_device_interpolation_bitwise_and_warm_start():
     x = rng.standard_normal(hi ** 3)
     np.testing.assert_array_equal(c.apply_operator(x), ref.apply_operator(x))
     # interpolated x0 on the device == host interpolation passed as x0
-    c.setup("mmg")
+    c.setup("mmg", CELL)
     b = c.assemble_rhs(np.ones(hi ** 3))
     x_lo = rng.standard_normal(lo[0] * lo[1] * lo[2])
     c.set_x0_interpolated(x_lo, lo)
@@ -664,12 +688,12 @@ def test_warm_started_setup_matches_cold():
     rho2 = np.clip(rho + 0.05 * rng.standard_normal(n ** 3), 0.0, 1.0)
     k2 = inputs.conductivity(rho2, 1e-6)
     warm = ctx_for(n, 2, 2, inputs.conductivity(rho, 1e-6))
-    warm.setup("mmg")
+    warm.setup("mmg", CELL)
     warm.set_conductivity(k2, BC)
-    warm.setup("mmg", MmgOptions(warm_start=True))
+    warm.setup("mmg", MmgOptions(warm_start=True, fine_blocks="coarse_cell"))
     _, _, it_w = warm.local_bases()
     cold = ctx_for(n, 2, 2, k2)
-    cold.setup("mmg")
+    cold.setup("mmg", CELL)
     _, _, it_c = cold.local_bases()
     # every brick converges (a stagnating seed restarts cold) to the same spans
     assert (it_w >= 0).all() and (it_c >= 0).all()
@@ -690,7 +714,7 @@ def test_acc_planes_matches_dense(monkeypatch, n, ncc, sd, lcc, kmin):
     for mode in ("0", "1"):
         monkeypatch.setenv("TMG_ACC_PLANES", mode)
         c = ctx_for(n, ncc, sd, kappa)
-        c.setup("mmg", MmgOptions(num_cc_basis=lcc))
+        c.setup("mmg", MmgOptions(num_cc_basis=lcc, fine_blocks="coarse_cell"))
         r = np.random.default_rng(9).standard_normal(n ** 3)
         rhs = c.assemble_rhs(np.ones(n ** 3))
         out[mode] = (c.apply_preconditioner(r), c.pcg(rhs, rtol=1e-8))

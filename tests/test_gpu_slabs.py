@@ -18,9 +18,10 @@ PATCH = BoundarySpec.bottom_center_patch(1, 1, 0.2, 0)
 
 
 def _ctx(n, ncc, sd, kappa, slabs, kind="mmg"):
+    from paper_2410_06850_b200 import MmgOptions
     c = Context(GridSpec(n, n, n), ncc, sd, slabs=slabs)
     c.set_conductivity(kappa, PATCH)
-    c.setup(kind)
+    c.setup(kind, MmgOptions(fine_blocks="coarse_cell"))
     return c
 
 

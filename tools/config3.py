@@ -46,7 +46,7 @@ else:  # on the device (gen.cu), bit-identical
 t_gen = time.perf_counter() - t0
 b = c.assemble_rhs(np.ones(n ** 3))
 t0 = time.perf_counter()
-c.setup("mmg", MmgOptions(num_cc_basis=a.lcc))
+c.setup("mmg", MmgOptions(num_cc_basis=a.lcc, fine_blocks="coarse_cell"))
 t_setup = time.perf_counter() - t0
 c.upload_rhs(b)
 reps = [c.solve_resident(1e-8, 20000) for _ in range(a.solves)]

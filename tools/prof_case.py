@@ -25,7 +25,7 @@ b = ctx.assemble_rhs(np.ones(n ** 3))
 import time
 for _ in range(a.setups):
     t0 = time.perf_counter()
-    ctx.setup(a.kind, MmgOptions(num_cc_basis=a.lcc))
+    ctx.setup(a.kind, MmgOptions(num_cc_basis=a.lcc, fine_blocks="coarse_cell"))
     print("setup wall ms %.2f" % ((time.perf_counter() - t0) * 1e3))
 ctx.upload_rhs(b)
 for _ in range(a.solves):
