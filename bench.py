@@ -70,8 +70,9 @@ def cfg_of(cfg_id):
 
 
 def hierarchy_str(cfg, n):
-    return (f"c={n // (cfg['ncc'] * cfg['sd'])} sd={cfg['sd']} ncc={cfg['ncc']} L_c=4 "
-            f"L_cc={cfg.get('lcc', 8)} nu=1")
+    """c = 8 throughout; ncc follows n (the CPU sample is smaller)."""
+    ncc = n // (8 * cfg["sd"])
+    return f"c=8 sd={cfg['sd']} ncc={ncc} L_c=4 L_cc={cfg.get('lcc', 8)} nu=1"
 
 
 def config_json(cfg, cfg_id, world, extra=None):

@@ -161,6 +161,35 @@ int tmg_set_design_generated(tmg_ctx* ctx, const tmg_design_gen* gen, double kap
                              double kappa_hi, int p, const tmg_patch* patches, int npatch,
                              double* rho_out);
 
+/* BASELINE configs[4]'s "seeded tree-like binary field" (no reference
+ * generator exists, inputs.tree_design restates it): a binary
+ * tree of `depth` levels of capsule segments rooted at the centre of the z = 0
+ * face, built from Lcg64(seed ^ 0x9E3779B97F4A7C15) in breadth-first order in
+ * the frame of the domain [0, dom]^3 (dom = 0: the context's own extents);
+ * field = max over segments of (1 - distance / width)_+ + amp * u (u the
+ * design generator's LCG noise), then `passes` box means of `radius` and the
+ * ceil(vf M) largest -> 1 (ties by lower index, rng.cpp:39-51). The cell
+ * centres are the context's own, so a slab context whose domain is the bottom
+ * of dom (e.g. 1024 x 1024 x 128 cells of extent 1 x 1 x 0.125 in the unit
+ * cube) gets the bottom slab of the tree. */
+typedef struct {
+  double vf;
+  uint64_t seed;
+  int passes;
+  int radius;
+  int depth;       /* tree levels: 2^depth - 1 segments (<= 12) */
+  double length0;  /* root segment length (domain units); level k: length0 * lshrink^k */
+  double lshrink;
+  double width0;   /* root capsule radius; level k: width0 * wshrink^k */
+  double wshrink;
+  double spread;   /* child direction = normalize(parent + spread * (u - 1/2)^3) */
+  double amp;      /* noise amplitude */
+  double dom[3];   /* extents of the whole domain the tree lives in (0: own) */
+} tmg_tree_gen;
+
+int tmg_set_design_tree(tmg_ctx* ctx, const tmg_tree_gen* gen, double kappa_lo, double kappa_hi,
+                        int p, const tmg_patch* patches, int npatch, double* rho_out);
+
 int tmg_set_design(tmg_ctx* ctx, const double* rho, double kappa_lo, double kappa_hi, int p,
                    const tmg_patch* patches, int npatches);
 /* interpolate_design (grid.cpp:220-241) on the device: piecewise-constant

@@ -1109,13 +1109,49 @@ int tmg_set_conductivity(tmg_ctx* c, const double* kappa, const tmg_patch* patch
   return finish_problem(c);
 }
 
-int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, double hi, int p,
-                             const tmg_patch* patches, int np, double* rho_out) {
-  if (!c || !gen) return set_err(c, TMG_EARG, "tmg_set_design_generated: null argument");
+namespace {
+// tmg_tree_gen's segments (7 doubles each: a, b, width), breadth-first.
+// Plain IEEE double arithmetic in a fixed order; inputs.tree_segments
+// restates it bit for bit.
+std::vector<double> tree_segments(const tmg_tree_gen& t, double lx, double ly, double lz) {
+  uint64_t st = t.seed ^ 0x9E3779B97F4A7C15ULL;
+  auto uni = [&st]() {  // Lcg64::next_uniform (rng.hpp:17-25)
+    st = 6364136223846793005ULL * st + 1442695040888963407ULL;
+    return (double)(st >> 11) * 0x1.0p-53;
+  };
+  struct Node {
+    double a[3], d[3];
+    int level;
+  };
+  std::vector<Node> q;
+  q.push_back(Node{{0.5 * lx, 0.5 * ly, 0.0}, {0.0, 0.0, 1.0}, 0});
+  std::vector<double> seg;
+  for (size_t n = 0; n < q.size(); ++n) {
+    const Node nd = q[n];
+    double len = t.length0, w = t.width0;
+    for (int k = 0; k < nd.level; ++k) {
+      len = len * t.lshrink;
+      w = w * t.wshrink;
+    }
+    const double b[3] = {nd.a[0] + len * nd.d[0], nd.a[1] + len * nd.d[1], nd.a[2] + len * nd.d[2]};
+    seg.insert(seg.end(), {nd.a[0], nd.a[1], nd.a[2], b[0], b[1], b[2], w});
+    if (nd.level + 1 >= t.depth) continue;
+    for (int c = 0; c < 2; ++c) {
+      double v[3];
+      for (int i = 0; i < 3; ++i) v[i] = nd.d[i] + t.spread * (uni() - 0.5);
+      const double nrm = std::sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+      q.push_back(Node{{b[0], b[1], b[2]}, {v[0] / nrm, v[1] / nrm, v[2] / nrm}, nd.level + 1});
+    }
+  }
+  return seg;
+}
+
+int set_design_common(tmg_ctx* c, double lo, double hi, int p, const tmg_patch* patches, int np,
+                      double vf, int passes, int radius) {
   if (!(lo > 0.0) || !(hi > lo))  // material.cpp:11-12
     return set_err(c, TMG_ECONFIG, "MaterialModel: requires 0 < kappa_lo < kappa_hi");
   if (p < 1) return set_err(c, TMG_ECONFIG, "MaterialModel: penalization p must be >= 1");
-  if (!(gen->vf >= 0.0 && gen->vf <= 1.0) || gen->passes < 0 || gen->radius < 0)
+  if (!(vf >= 0.0 && vf <= 1.0) || passes < 0 || radius < 0)
     return set_err(c, TMG_ECONFIG, "design generator: need 0 <= vf <= 1, passes, radius >= 0");
   int rc = validate_patches(c, patches, np);
   if (rc) return rc;
@@ -1123,15 +1159,20 @@ int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, d
   for (int i = 0; i < np; ++i)
     c->patches.push_back(Patch{patches[i].face, patches[i].u0, patches[i].v0, patches[i].u1,
                                patches[i].v1, patches[i].value});
-  rc = guard(c, [&] {
+  return TMG_OK;
+}
+
+// generate (x-fastest, whole grid) with `gen`, distribute to the slabs, kappa
+int generate_design(tmg_ctx* c, double lo, double hi, int p, double* rho_out,
+                    const std::function<void(double* rho, double* f, void* scratch)>& gen) {
+  const int rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
     const tmg_grid& G = c->grid;
     const int64_t m = G.nx * G.ny * G.nz;  // the whole design (every rank generates it)
     double* rho = dalloc<double>(c, m);
     double* f = dalloc<double>(c, m);
     double* scratch = dalloc<double>(c, (int64_t)(gen_scratch_bytes(m) / sizeof(double)) + 1);
-    launch_box_filter_design(G.nx, G.ny, G.nz, gen->vf, gen->seed, gen->passes, gen->radius, rho,
-                             f, scratch, c->stream);
+    gen(rho, f, scratch);
     CK(cudaGetLastError());
     for (Slab& s : c->slabs) {
       launch_to_brick(s.g, c->cb, rho + s.xoff, s.r, c->stream);
@@ -1148,6 +1189,44 @@ int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, d
   });
   if (rc) return rc;
   return finish_problem(c);
+}
+}  // namespace
+
+int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, double hi, int p,
+                             const tmg_patch* patches, int np, double* rho_out) {
+  if (!c || !gen) return set_err(c, TMG_EARG, "tmg_set_design_generated: null argument");
+  const int rc = set_design_common(c, lo, hi, p, patches, np, gen->vf, gen->passes, gen->radius);
+  if (rc) return rc;
+  const tmg_grid& G = c->grid;
+  return generate_design(c, lo, hi, p, rho_out, [&](double* rho, double* f, void* scratch) {
+    launch_box_filter_design(G.nx, G.ny, G.nz, gen->vf, gen->seed, gen->passes, gen->radius, rho,
+                             f, scratch, c->stream);
+  });
+}
+
+int tmg_set_design_tree(tmg_ctx* c, const tmg_tree_gen* t, double lo, double hi, int p,
+                        const tmg_patch* patches, int np, double* rho_out) {
+  if (!c || !t) return set_err(c, TMG_EARG, "tmg_set_design_tree: null argument");
+  if (t->depth < 1 || t->depth > 12 || !(t->length0 > 0.0) || !(t->width0 > 0.0) ||
+      !(t->lshrink > 0.0) || !(t->wshrink > 0.0))
+    return set_err(c, TMG_ECONFIG,
+                   "tree generator: need 1 <= depth <= 12 and positive lengths, widths, shrinks");
+  const int rc = set_design_common(c, lo, hi, p, patches, np, t->vf, t->passes, t->radius);
+  if (rc) return rc;
+  const tmg_grid& G = c->grid;
+  const double dx = t->dom[0] > 0 ? t->dom[0] : G.lx, dy = t->dom[1] > 0 ? t->dom[1] : G.ly,
+               dz = t->dom[2] > 0 ? t->dom[2] : G.lz;
+  const std::vector<double> seg = tree_segments(*t, dx, dy, dz);
+  const int nseg = (int)(seg.size() / 7);
+  return generate_design(c, lo, hi, p, rho_out, [&](double* rho, double* f, void* scratch) {
+    double* dseg = dalloc<double>(c, (int64_t)seg.size());
+    CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(double) * seg.size(), cudaMemcpyHostToDevice,
+                       c->stream));
+    launch_tree_design(G.nx, G.ny, G.nz, G.lx, G.ly, G.lz, t->vf, t->seed, t->passes, t->radius,
+                       dseg, nseg, t->amp, rho, f, scratch, c->stream);
+    CK(cudaStreamSynchronize(c->stream));  // seg host vector outlives the copy
+    dfree(c, dseg);
+  });
 }
 
 int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,

@@ -572,18 +572,9 @@ void launch_coarse_fused(const GridParams& g, const int* done, const double* Ac,
                          double* rcc, double* rc1, double* ec, unsigned int* bar,
                          cudaStream_t s) {
   const size_t smem = symv_dyn_smem(n_cc);
-  static int grid = 0;
-  static size_t grid_smem = 0;
-  if (!grid || grid_smem != smem) {
-    cudaFuncSetAttribute(k_coarse_fused<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_fused<32, 8>, 256, smem);
-    grid = (per < 1 ? 1 : per) * sms;
-    grid_smem = smem;
-  }
+  // co-residency of the grid barriers: every CTA of the grid resident at
+  // once, per device (device_occupancy also raises the smem limit there)
+  const int grid = device_occupancy(k_coarse_fused<32, 8>, 256, smem) * device_sm_count();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(256);
@@ -594,8 +585,9 @@ void launch_coarse_fused(const GridParams& g, const int* done, const double* Ac,
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_coarse_fused<32, 8>, g, done, Ac, Winv, Rcc, Acc_tiles, n_cc, symv_partials,
-                     rc, rc0, rcc, rc1, ec, bar);
+  launch_check(cudaLaunchKernelEx(&cfg, k_coarse_fused<32, 8>, g, done, Ac, Winv, Rcc, Acc_tiles,
+                                  n_cc, symv_partials, rc, rc0, rcc, rc1, ec, bar),
+               "k_coarse_fused (cooperative) launch");
 }
 
 void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,

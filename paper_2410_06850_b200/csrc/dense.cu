@@ -359,21 +359,9 @@ void pack_sym_tiles(const double* A, int64_t n, double* T, cudaStream_t s) {
 void launch_symv(const int* done, const double* T, int64_t n, const double* x, double* P, double* y,
                  cudaStream_t s) {
   const int64_t nt = (n + TS - 1) / TS;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const size_t smem = symv_dyn_smem(n);
-  cudaFuncSetAttribute(k_symv_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_symv_tiles, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
   const int64_t ntiles = nt * (nt + 1) / 2;
-  const int64_t slots = (int64_t)per_sm * sms;
+  const int64_t slots = (int64_t)device_occupancy(k_symv_tiles, 256, smem) * device_sm_count();
   const unsigned grid = (unsigned)(ntiles < slots ? ntiles : slots);
   launch_pdl(k_symv_tiles, dim3(grid), dim3(256), smem, s, done, T, n, x, P);
   launch_pdl(k_symv_reduce, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, s, done, P, n, y);

@@ -177,21 +177,85 @@ size_t gen_scratch_bytes(int64_t m) {
          sizeof(uint64_t) * 4;
 }
 
+// Tree-like field (BASELINE configs[4], no reference generator; DESIGN.md
+// §6 and inputs.tree_design): f = max over the seeded branch segments of the
+// capsule profile (1 - d / w)_+ plus amp * u, u the LCG noise already in f.
+// d is the distance from the cell centre to the segment, evaluated with
+// explicitly rounded FP64 operations (no contraction) so the host restatement
+// is bit-identical.
+__global__ void k_tree_field(double* f, int64_t nx, int64_t ny, int64_t nz, double hx, double hy,
+                             double hz, const double* __restrict__ seg, int nseg, double amp) {
+  extern __shared__ double sseg[];  // 7 doubles per segment: a, b, w
+  for (int i = threadIdx.x; i < 7 * nseg; i += blockDim.x) sseg[i] = seg[i];
+  __syncthreads();
+  const int64_t m = nx * ny * nz;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = s % nx, j = (s / nx) % ny, k = s / (nx * ny);
+    const double px = __dmul_rn((double)i + 0.5, hx), py = __dmul_rn((double)j + 0.5, hy),
+                 pz = __dmul_rn((double)k + 0.5, hz);
+    double best = 0.0;
+    for (int q = 0; q < nseg; ++q) {
+      const double* g = sseg + 7 * q;
+      const double ex = __dsub_rn(g[3], g[0]), ey = __dsub_rn(g[4], g[1]), ez = __dsub_rn(g[5], g[2]);
+      const double wx = __dsub_rn(px, g[0]), wy = __dsub_rn(py, g[1]), wz = __dsub_rn(pz, g[2]);
+      const double ee = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey)), __dmul_rn(ez, ez));
+      const double we = __dadd_rn(__dadd_rn(__dmul_rn(wx, ex), __dmul_rn(wy, ey)), __dmul_rn(wz, ez));
+      double t = __ddiv_rn(we, ee);
+      t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+      const double dx = __dsub_rn(wx, __dmul_rn(t, ex)), dy = __dsub_rn(wy, __dmul_rn(t, ey)),
+                   dz = __dsub_rn(wz, __dmul_rn(t, ez));
+      const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                            __dmul_rn(dz, dz)));
+      const double v = __dsub_rn(1.0, __ddiv_rn(d, g[6]));
+      best = v > best ? v : best;
+    }
+    f[s] = __dadd_rn(best, __dmul_rn(amp, f[s]));
+  }
+}
+
+static void filter_select(int64_t nx, int64_t ny, int64_t nz, double vf, int passes, int radius,
+                          double* rho, double* f, void* scratch, cudaStream_t s);
+
+static void lcg_fill(double* f, int64_t m, uint64_t seed, cudaStream_t s) {
+  const int G = 16;
+  const int64_t nthreads = (m + G - 1) / G;
+  k_lcg_uniforms<<<(unsigned)((nthreads + kGenThreads - 1) / kGenThreads), kGenThreads, 0, s>>>(
+      f, m, seed, G);
+}
+
 // rho (x-fastest, M = nx ny nz doubles) from the seeded generator; scratch of
 // gen_scratch_bytes(M); f is a second M-double work array.
 void launch_box_filter_design(int64_t nx, int64_t ny, int64_t nz, double vf, uint64_t seed,
                               int passes, int radius, double* rho, double* f, void* scratch,
                               cudaStream_t s) {
+  lcg_fill(f, nx * ny * nz, seed, s);
+  filter_select(nx, ny, nz, vf, passes, radius, rho, f, scratch, s);
+}
+
+// The tree-like design: noise (as above), k_tree_field over the segments
+// (device array, 7 doubles each), then the same box means and top-k select.
+void launch_tree_design(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                        double vf, uint64_t seed, int passes, int radius, const double* seg,
+                        int nseg, double amp, double* rho, double* f, void* scratch,
+                        cudaStream_t s) {
+  const int64_t m = nx * ny * nz;
+  lcg_fill(f, m, seed, s);
+  int64_t gb = (m + kGenThreads - 1) / kGenThreads;
+  if (gb > 148 * 64) gb = 148 * 64;
+  k_tree_field<<<(unsigned)gb, kGenThreads, sizeof(double) * 7 * nseg, s>>>(
+      f, nx, ny, nz, lx / (double)nx, ly / (double)ny, lz / (double)nz, seg, nseg, amp);
+  filter_select(nx, ny, nz, vf, passes, radius, rho, f, scratch, s);
+}
+
+static void filter_select(int64_t nx, int64_t ny, int64_t nz, double vf, int passes, int radius,
+                          double* rho, double* f, void* scratch, cudaStream_t s) {
   const int64_t m = nx * ny * nz;
   double* t = (double*)scratch;
   unsigned long long* hist = (unsigned long long*)(t + m);
   const int64_t chunk = 65536, chunks = (m + chunk - 1) / chunk;
   unsigned long long* eq = hist + 256;
   uint64_t* sel = (uint64_t*)(eq + chunks);
-  const int G = 16;
-  const int64_t nthreads = (m + G - 1) / G;
-  k_lcg_uniforms<<<(unsigned)((nthreads + kGenThreads - 1) / kGenThreads), kGenThreads, 0, s>>>(
-      f, m, seed, G);
   int64_t gb = (m + kGenThreads - 1) / kGenThreads;
   if (gb > 148 * 64) gb = 148 * 64;
   for (int p = 0; p < passes; ++p) {

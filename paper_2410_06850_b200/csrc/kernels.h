@@ -3,6 +3,10 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
 #include <utility>
 #include <cuda_runtime.h>
 
@@ -28,6 +32,54 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// A failed launch throws; the C ABI's guard() turns it into TMG_ECUDA with
+// the message (the launchers run inside every tmg_* entry point's guard).
+inline void launch_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                             cudaGetErrorString(e) + ")");
+}
+
+// SM count of the current device (cached per device ordinal).
+inline int device_sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  launch_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  launch_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev),
+               "cudaDeviceGetAttribute");
+  cache[dev] = sms;
+  return sms;
+}
+
+// Resident CTAs per SM of `kernel` with `smem` dynamic bytes on the current
+// device, after raising its dynamic shared-memory limit there (the attribute
+// is per device). Cached per (device, kernel, threads, smem).
+template <typename K>
+inline int device_occupancy(K kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<std::pair<int, const void*>, std::pair<int, size_t>>, int> cache;
+  int dev = 0;
+  launch_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const auto key = std::make_pair(std::make_pair(dev, (const void*)kernel),
+                                  std::make_pair(threads, smem));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (smem > 48 * 1024)
+    launch_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                 "cudaFuncSetAttribute");
+  int per = 0;
+  launch_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem),
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  cache[key] = per < 1 ? 1 : per;
+  return cache[key];
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args&&... args) {
@@ -41,7 +93,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  launch_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
 }
 
 enum : int {
@@ -229,6 +281,10 @@ size_t gen_scratch_bytes(int64_t m);
 void launch_box_filter_design(int64_t nx, int64_t ny, int64_t nz, double vf, uint64_t seed,
                               int passes, int radius, double* rho, double* f, void* scratch,
                               cudaStream_t s);
+void launch_tree_design(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
+                        double vf, uint64_t seed, int passes, int radius, const double* seg,
+                        int nseg, double amp, double* rho, double* f, void* scratch,
+                        cudaStream_t s);
 // design loop with MMA (optim.cu; MmaOptions, optim.hpp:27-32)
 struct MmaParams {
   double move, asy_init, asy_incr, asy_decr, xmin, xmax;

@@ -234,16 +234,9 @@ __global__ void k_max_partials(const double* partials, int n, double* out) {
 
 // ------------------------------------------------------------ launchers
 
-static int mma_grid() {
-  static int g = 0;
-  if (!g) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mma_dual, kMmaThreads, 0);
-    g = sms * (per < 2 ? (per < 1 ? 1 : per) : 2);
-  }
-  return g;
+static int mma_grid() {  // per device: co-resident CTAs of the cooperative dual
+  const int per = device_occupancy(k_mma_dual, kMmaThreads, 0);
+  return device_sm_count() * (per < 2 ? per : 2);
 }
 
 int mma_partials_doubles() { return 2 * mma_grid() + 8; }
@@ -267,8 +260,9 @@ void launch_mma_dual(const double* x, const double* grad, const double* low, con
                      unsigned int* bar, double* out, cudaStream_t s) {
   void* args[] = {(void*)&x, (void*)&grad, (void*)&low, (void*)&upp, (void*)&n,
                   (void*)&constraint, (void*)&o, (void*)&partials, (void*)&bar, (void*)&out};
-  cudaLaunchCooperativeKernel((const void*)k_mma_dual, dim3(mma_grid()), dim3(kMmaThreads), args,
-                              0, s);
+  launch_check(cudaLaunchCooperativeKernel((const void*)k_mma_dual, dim3(mma_grid()),
+                                           dim3(kMmaThreads), args, 0, s),
+               "k_mma_dual (cooperative) launch");
 }
 
 void launch_mma_primal(const double* x, const double* grad, const double* low, const double* upp,

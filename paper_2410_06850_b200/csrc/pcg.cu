@@ -579,15 +579,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, cons
 // at the number of bricks.
 template <typename K>
 static unsigned persist_grid(K kernel, int threads, size_t smem, int64_t nb) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
-  const int64_t n = (int64_t)sms * (per > 0 ? per : 1);
+  const int64_t n = (int64_t)device_sm_count() * device_occupancy(kernel, threads, smem);
   return (unsigned)(n < nb ? n : nb);
 }
 

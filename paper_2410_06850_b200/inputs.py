@@ -90,6 +90,88 @@ def box_filter_design(n, vf: float, seed: int = 20240501, passes: int = 3,
     return binarize_top(f.ravel(), vf)
 
 
+# BASELINE configs[4]: "seeded tree-like binary field (filter radius 6, volume
+# fraction 0.15)". The reference has no such generator; this
+# one is documented in DESIGN.md §6 and run on the device by
+# tmg_set_design_tree (csrc/gen.cu), bit-identical to tree_design below.
+TREE_DEFAULTS = dict(depth=8, length0=0.28, lshrink=0.78, width0=0.10, wshrink=0.80, spread=1.8,
+                     amp=0.05)
+_MASK64 = (1 << 64) - 1
+
+
+def tree_segments(seed: int = 20240501, depth=8, length0=0.28, lshrink=0.78, width0=0.10,
+                  wshrink=0.80, spread=1.8, dom=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """Breadth-first binary tree of capsule segments rooted at the centre of
+    the z = 0 face (the Dirichlet patch), heading +z; each child direction
+    is normalize(parent + spread * (u - 1/2, u - 1/2, u - 1/2)) with u from
+    Lcg64(seed ^ 0x9E3779B97F4A7C15) (rng.hpp:17-25). Rows: a(3), b(3),
+    width. Plain IEEE double arithmetic in the order of tree_segments() in
+    csrc/abi.cu."""
+    st = (seed ^ 0x9E3779B97F4A7C15) & _MASK64
+
+    def uni():
+        nonlocal st
+        st = (6364136223846793005 * st + 1442695040888963407) & _MASK64
+        return float(st >> 11) * 2.0 ** -53
+
+    q = [((0.5 * dom[0], 0.5 * dom[1], 0.0), (0.0, 0.0, 1.0), 0)]
+    seg = []
+    n = 0
+    while n < len(q):
+        a, d, level = q[n]
+        n += 1
+        ln, w = length0, width0
+        for _ in range(level):
+            ln = ln * lshrink
+            w = w * wshrink
+        b = (a[0] + ln * d[0], a[1] + ln * d[1], a[2] + ln * d[2])
+        seg.append((*a, *b, w))
+        if level + 1 >= depth:
+            continue
+        for _ in range(2):
+            v = [d[i] + spread * (uni() - 0.5) for i in range(3)]
+            nrm = float(np.sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]))
+            q.append((b, (v[0] / nrm, v[1] / nrm, v[2] / nrm), level + 1))
+    return np.array(seg, dtype=np.float64)
+
+
+def tree_design(n, vf: float = 0.15, seed: int = 20240501, passes: int = 1, radius: int = 6,
+                extent=(1.0, 1.0, 1.0), dom=None, **tree) -> np.ndarray:
+    """BASELINE configs[4] density (tmg_set_design_tree): tree capsule
+    profile (1 - d / w)_+ maxed over the segments, plus amp * LCG noise, then
+    `passes` box means of `radius` and the top ceil(vf M) -> 1. Returns rho
+    in {0, 1}, x-fastest; cell centres ((i + 1/2) lx / nx, ...)."""
+    p = dict(TREE_DEFAULTS)
+    p.update(tree)
+    amp = p.pop("amp")
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    seg = tree_segments(seed, dom=dom or extent, **p)
+    u = lcg_uniforms(nx * ny * nz, seed).reshape(nz, ny, nx)
+    hx, hy, hz = extent[0] / nx, extent[1] / ny, extent[2] / nz
+    px = ((np.arange(nx) + 0.5) * hx)[None, None, :]
+    py = ((np.arange(ny) + 0.5) * hy)[None, :, None]
+    pz = ((np.arange(nz) + 0.5) * hz)[:, None, None]
+    best = np.zeros((nz, ny, nx))
+    for ax, ay, az, bx, by, bz, w in seg:
+        ex, ey, ez = bx - ax, by - ay, bz - az
+        wx, wy, wz = px - ax, py - ay, pz - az
+        ee = (ex * ex + ey * ey) + ez * ez
+        we = (wx * ex + wy * ey) + wz * ez
+        t = np.clip(we / ee, 0.0, 1.0)
+        dx, dy, dz = wx - t * ex, wy - t * ey, wz - t * ez
+        d = np.sqrt((dx * dx + dy * dy) + dz * dz)
+        best = np.maximum(best, 1.0 - d / w)
+    f = best + amp * u
+    cx, cy, cz = _counts(nx, radius), _counts(ny, radius), _counts(nz, radius)
+    denom = (cx[None, None, :] * cy[None, :, None]) * cz[:, None, None]
+    for _ in range(passes):
+        t = _window_sum(f, 2, radius)
+        t = _window_sum(t, 1, radius)
+        t = _window_sum(t, 0, radius)
+        f = t / denom
+    return binarize_top(f.ravel(), vf)
+
+
 def conductivity(rho: np.ndarray, kappa_lo: float, kappa_hi: float = 1.0, p: int = 3):
     """SIMP kappa = lo + rho^p (hi - lo) by repeated multiplication
     (material.cpp:45-59)."""
@@ -107,4 +189,8 @@ CONFIGS = {
     # sd = 4 / ncc = 16 / L_cc = 12 needs 50 iterations, sd = 8 / L_cc = 20 400
     #
     3: dict(n=512, vf=0.2, passes=3, radius=4, kmin=1e-6, ncc=16, sd=4, lcc=12),
+    # 1024^3 on 8 B200 (z-slabs of 1024 x 1024 x 128); tree-like design
+    # (tree_design / tmg_set_design_tree), c = 8 with L_c = 4 as BASELINE
+    # states; sd = 4 / L_cc = 12 as configs[3]
+    4: dict(n=1024, vf=0.15, passes=1, radius=6, kmin=1e-6, ncc=32, sd=4, lcc=12, design="tree"),
 }

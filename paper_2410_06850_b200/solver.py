@@ -81,6 +81,13 @@ class _DesignGen(C.Structure):
                 ("radius", C.c_int)]
 
 
+class _TreeGen(C.Structure):
+    _fields_ = [("vf", C.c_double), ("seed", C.c_uint64), ("passes", C.c_int),
+                ("radius", C.c_int), ("depth", C.c_int), ("length0", C.c_double),
+                ("lshrink", C.c_double), ("width0", C.c_double), ("wshrink", C.c_double),
+                ("spread", C.c_double), ("amp", C.c_double), ("dom", C.c_double * 3)]
+
+
 class _OptimOpts(C.Structure):
     _fields_ = [("vstar", C.c_double), ("move_limit", C.c_double), ("asy_init", C.c_double),
                 ("asy_incr", C.c_double), ("asy_decr", C.c_double), ("kappa_lo", C.c_double),
@@ -129,6 +136,7 @@ EXPORTED_SYMBOLS = (
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
     "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
     "tmg_set_design_generated", "tmg_solve_resident_ex", "tmg_apply_operator_abs",
+    "tmg_set_design_tree",
 )
 
 
@@ -345,6 +353,25 @@ class Context:
         parr, n = boundary._c()
         rho = np.empty(self.grid.num_cells()) if return_rho else None
         self._check(native().tmg_set_design_generated(
+            self._p, C.byref(g), C.c_double(kappa_lo), C.c_double(kappa_hi), C.c_int(p), parr,
+            C.c_int(n), _ptr(rho) if rho is not None else None))
+        return rho
+
+    def set_design_tree(self, vf, kappa_lo, kappa_hi=1.0, p=3, boundary: BoundarySpec = None,
+                        seed=20240501, passes=1, radius=6, dom=None, return_rho=False, **tree):
+        """BASELINE configs[4]'s tree-like design generated on the device
+        (tmg_set_design_tree; bit-identical to inputs.tree_design), then as
+        set_design. dom: extents of the whole domain the tree lives in
+        (default: the context's own)."""
+        from .inputs import TREE_DEFAULTS
+        t = dict(TREE_DEFAULTS)
+        t.update(tree)
+        g = _TreeGen(vf, seed, passes, radius, t["depth"], t["length0"], t["lshrink"],
+                     t["width0"], t["wshrink"], t["spread"], t["amp"],
+                     (C.c_double * 3)(*(dom or (0.0, 0.0, 0.0))))
+        parr, n = boundary._c()
+        rho = np.empty(self.grid.num_cells()) if return_rho else None
+        self._check(native().tmg_set_design_tree(
             self._p, C.byref(g), C.c_double(kappa_lo), C.c_double(kappa_hi), C.c_int(p), parr,
             C.c_int(n), _ptr(rho) if rho is not None else None))
         return rho

@@ -40,3 +40,39 @@ def test_generated_config0_solid_count():
     rho = c.set_design_generated(0.3, 1e-3, boundary=BC, return_rho=True)
     assert int(rho.sum()) == 78644
     np.testing.assert_array_equal(rho, O.box_filter_design(O.grid(64), 0.3))
+
+
+# --------------------------------------------- configs[4]: tree-like design
+
+@pytest.mark.parametrize("dims,ext,dom,ncc,sd,vf,radius,depth", [
+    ((32, 32, 32), (1.0, 1.0, 1.0), None, 2, 2, 0.15, 2, 6),
+    ((64, 64, 64), (1.0, 1.0, 1.0), None, 4, 2, 0.15, 6, 8),  # configs[4]'s parameters at 64^3
+    ((64, 64, 16), (1.0, 1.0, 0.25), (1.0, 1.0, 1.0), (4, 4, 1), 2, 0.15, 3, 8),  # bottom slab
+    ((16, 24, 32), (1.0, 1.5, 2.0), None, (2, 3, 4), 1, 0.3, 1, 5),
+])
+def test_tree_design_bitwise(dims, ext, dom, ncc, sd, vf, radius, depth):
+    nx, ny, nz = dims
+    ref = inputs.tree_design(dims, vf, radius=radius, extent=ext, dom=dom, depth=depth)
+    c = Context(GridSpec(nx, ny, nz, *ext), ncc, sd)
+    rho = c.set_design_tree(vf, 1e-6, boundary=BC, radius=radius, dom=dom, depth=depth,
+                            return_rho=True)
+    np.testing.assert_array_equal(rho, ref)
+    assert rho.sum() == int(np.ceil(vf * nx * ny * nz))
+
+
+def test_tree_design_is_a_tree_touching_the_sink():
+    from scipy import ndimage
+    n = 64
+    c = Context(GridSpec(n, n, n), 4, 2)
+    rho = c.set_design_tree(0.15, 1e-6, boundary=BC, return_rho=True).reshape(n, n, n)
+    lab, _ = ndimage.label(rho)
+    sizes = np.bincount(lab.ravel())[1:]
+    main = np.argmax(sizes) + 1
+    assert sizes.max() >= 0.9 * sizes.sum()  # one connected tree carries the solid
+    assert (lab[0, 28:36, 28:36] == main).any()  # rooted in the Dirichlet patch
+    # and it solves: MMG-PCG at contrast 1e6
+    from paper_2410_06850_b200 import MmgOptions
+    c.setup("mmg", MmgOptions(fine_blocks="coarse_cell"))
+    b = c.assemble_rhs(np.ones(n ** 3))
+    r = c.pcg(b, rtol=1e-8)
+    assert r.report.converged and r.report.iterations < 100

@@ -305,3 +305,18 @@ def test_interpolate_design_matches_oracle():
     lo = rng.random(4 * 6 * 8)
     hi = interpolate_design(lo, GridSpec(4, 6, 8), GridSpec(8, 12, 24))
     np.testing.assert_array_equal(hi, O.interpolate_design(lo, (4, 6, 8), (8, 12, 24)))
+
+
+def test_tree_segments_deterministic_and_rooted():
+    """configs[4]'s tree generator (inputs.tree_segments; the device builds
+    the same list in csrc/abi.cu): root at the z = 0 face centre heading +z,
+    2^depth - 1 segments, children start where their parent ends."""
+    from paper_2410_06850_b200 import inputs
+    s = inputs.tree_segments(20240501, depth=6)
+    assert s.shape == (63, 7)
+    np.testing.assert_array_equal(s, inputs.tree_segments(20240501, depth=6))
+    assert tuple(s[0, :3]) == (0.5, 0.5, 0.0) and s[0, 3:5].tolist() == [0.5, 0.5]
+    for k in range(1, 63):
+        parent = (k - 1) // 2
+        np.testing.assert_array_equal(s[k, :3], s[parent, 3:6])
+    assert not np.array_equal(s, inputs.tree_segments(7, depth=6))

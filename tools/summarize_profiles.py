@@ -1,11 +1,12 @@
 """Summarise ncu output into profiles/ (committed evidence).
 
     python tools/summarize_profiles.py <round-tag> <launches.csv> <full.ncu-rep> [more.ncu-rep ...]
+        [--config K --cells M --cmd "..."]
 
 Writes profiles/<tag>_launches.md (per-kernel launch count, time share from the
 cold-cache serialised launch list), profiles/<tag>_ncu_full.md (DRAM bytes,
 throughput, occupancy and stall reasons per kernel from one --set full
-capture) and profiles/ncu_summary_latest.json (read by bench.py for the
+capture) and profiles/ncu_summary_<tag>.json (read by bench.py for the
 roofline `traffic` field).
 """
 import csv
@@ -75,16 +76,26 @@ def full(path):
 
 
 def main():
-    tag, lpath, fpaths = sys.argv[1], sys.argv[2], sys.argv[3:]
+    argv = list(sys.argv[1:])
+    opt = {}
+    for key in ("--config", "--cells", "--cmd"):
+        if key in argv:
+            i = argv.index(key)
+            opt[key] = argv[i + 1]
+            del argv[i:i + 2]
+    tag, lpath, fpaths = argv[0], argv[1], argv[2:]
+    cfg = int(opt.get("--config", 1))
+    cells = int(opt.get("--cells", 128 ** 3))
+    cmd = opt.get("--cmd", "python bench.py --config 1 --steps 1 --warmup 3 --no-cpu-baseline --no-extra")
+    size = f"{round(cells ** (1 / 3))}^3"
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     agg = launches(lpath)
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(prof, f"{tag}_launches.md"), "w") as f:
         f.write(f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)\n\n")
-        f.write("Command: `python bench.py --steps 1 --warmup 3 --no-cpu-baseline` (BASELINE configs[1], "
-                "128^3: set-up + 5 solves). Cold-cache, serialised per-launch times: compare shares, "
-                "not absolutes.\n\n")
+        f.write(f"Command: `{cmd}` (BASELINE configs[{cfg}], {size}: set-up + solves). "
+                "Cold-cache, serialised per-launch times: compare shares, not absolutes.\n\n")
         f.write("| kernel | launches | total us | share |\n|---|---:|---:|---:|\n")
         for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"| {k} | {n} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |\n")
@@ -93,15 +104,15 @@ def main():
         for k, v in full(fp).items():
             fr.setdefault(k, v)
     with open(os.path.join(prof, f"{tag}_ncu_full.md"), "w") as f:
-        f.write(f"# {tag}: ncu --set full (one launch per kernel, 128^3: solve and set-up kernels)\n\n")
+        f.write(f"# {tag}: ncu --set full (one launch per kernel, configs[{cfg}] {size})\n\n")
         f.write("| kernel | us | DRAM MB/launch | achieved GB/s | DRAM % peak | warps active % | regs | top stalls |\n")
         f.write("|---|---:|---:|---:|---:|---:|---:|---|\n")
         for k, v in fr.items():
             f.write(f"| {k} | {v['duration_us']:.1f} | {v['dram_bytes_per_launch'] / 1e6:.1f} | "
                     f"{(v['achieved_gbs'] or 0):.0f} | {v['dram_pct_peak'] or 0:.1f} | "
                     f"{v['warps_active_pct'] or 0:.1f} | {v['registers'] or 0:.0f} | {v['top_stalls']} |\n")
-    with open(os.path.join(prof, "ncu_summary_latest.json"), "w") as f:
-        json.dump({"tag": tag, "kernels": fr,
+    with open(os.path.join(prof, f"ncu_summary_{tag}.json"), "w") as f:
+        json.dump({"tag": tag, "config": cfg, "cells": cells, "command": cmd, "kernels": fr,
                    "launch_share": {k: {"launches": n, "total_us": t / 1e3, "share": t / tot}
                                     for k, (n, t) in agg.items()}}, f, indent=1)
     print(open(os.path.join(prof, f"{tag}_launches.md")).read())
