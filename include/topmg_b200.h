@@ -130,6 +130,13 @@ int tmg_create_dist(const tmg_grid* grid, int device, int rank, int nranks, cons
  * first brick, bricks, first cc element, cc elements, first x-fastest cell,
  * cells, has neighbour below, has neighbour above}. */
 int tmg_partition(const tmg_grid* grid, int nranks, int rank, int64_t* out);
+/* The halo exchange of slab `rank` as exchange() issues it over NCCL:
+ * returns the number of operations (<= 4, or -error), each 4 int64 in ops:
+ * {1 = send / 0 = receive, peer rank, first global unit, units}, units =
+ * bricks (elem = 0) or cc elements (elem = 1), one z-layer per neighbour.
+ * Host-only (no GPU). */
+int tmg_halo_plan(const tmg_grid* grid, int nranks, int rank, int elem, int64_t* ops,
+                  int max_ops);
 /* Message of the last failed call on this context (or of tmg_create when ctx
  * is NULL). */
 const char* tmg_last_error(const tmg_ctx* ctx);

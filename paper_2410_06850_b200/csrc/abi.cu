@@ -64,6 +64,31 @@ Part partition(const GridParams& g, int slab, int total) {
 }
 }  // namespace
 
+// One rank's halo exchange as a list of point-to-point operations, in
+// global units (bricks, or cc elements with elem): the own bottom layer goes
+// to rank - 1 and its top layer comes back as the lower ghost, symmetrically
+// above. exchange() issues exactly these as grouped ncclSend / ncclRecv;
+// tmg_halo_plan exports them so the multi-process host logic is tested with
+// gloo on CPU (tests/test_dist_cpu.py).
+struct HaloOp {
+  int send;  // 1 send, 0 receive
+  int peer;
+  int64_t unit0, units;
+};
+std::vector<HaloOp> halo_ops(const Part& p, int rank, int64_t Lu, bool elem) {
+  const int64_t u0 = elem ? p.e0 : p.b0, nu = elem ? p.neo : p.nbo;
+  std::vector<HaloOp> ops;
+  if (p.lo) {
+    ops.push_back({1, rank - 1, u0, Lu});
+    ops.push_back({0, rank - 1, u0 - Lu, Lu});
+  }
+  if (p.hi) {
+    ops.push_back({1, rank + 1, u0 + nu - Lu, Lu});
+    ops.push_back({0, rank + 1, u0 + nu, Lu});
+  }
+  return ops;
+}
+
 struct Slab {
   int id = 0;  // global slab index (= rank for NCCL contexts)
   GridParams g{};
@@ -377,17 +402,13 @@ void exchange(tmg_ctx* c, const std::function<void*(Slab&)>& get, size_t bytes, 
     return;
   }
   Slab& s = c->slabs[0];
-  const int64_t u0 = elem ? s.g.e0 : s.g.b0, nu = elem ? s.g.neo : s.g.nbo;
-  const int64_t Lu = elem ? s.Le : s.L;
-  const size_t lb = (size_t)Lu * bytes;
+  const std::vector<HaloOp> ops =
+      halo_ops(partition(c->g, s.id, c->total), s.id, elem ? s.Le : s.L, elem);
   NK(ncclGroupStart());
-  if (s.lo) {
-    NK(ncclSend(unit(s, u0), lb, ncclChar, s.id - 1, c->comm, st));
-    NK(ncclRecv(unit(s, u0 - Lu), lb, ncclChar, s.id - 1, c->comm, st));
-  }
-  if (s.hi) {
-    NK(ncclSend(unit(s, u0 + nu - Lu), lb, ncclChar, s.id + 1, c->comm, st));
-    NK(ncclRecv(unit(s, u0 + nu), lb, ncclChar, s.id + 1, c->comm, st));
+  for (const HaloOp& o : ops) {
+    const size_t nb = (size_t)o.units * bytes;
+    if (o.send) NK(ncclSend(unit(s, o.unit0), nb, ncclChar, o.peer, c->comm, st));
+    else NK(ncclRecv(unit(s, o.unit0), nb, ncclChar, o.peer, c->comm, st));
   }
   NK(ncclGroupEnd());
 }
@@ -1075,6 +1096,30 @@ int tmg_partition(const tmg_grid* grid, int nranks, int rank, int64_t* out) {
   out[8] = p.lo;                                // neighbour below
   out[9] = p.hi;                                // neighbour above
   return TMG_OK;
+}
+
+int tmg_halo_plan(const tmg_grid* grid, int nranks, int rank, int elem, int64_t* ops,
+                  int max_ops) {
+  if (!grid || !ops) return -set_err(nullptr, TMG_EARG, "tmg_halo_plan: null argument");
+  int64_t cb = 0;
+  int rc = check_grid(grid, &cb);
+  if (!rc) rc = check_partition(grid, nranks);
+  if (rc) return -rc;
+  if (rank < 0 || rank >= nranks)
+    return -set_err(nullptr, TMG_EARG, "tmg_halo_plan: bad rank %d of %d", rank, nranks);
+  const GridParams g = global_params(*grid, (int)cb);
+  const std::vector<HaloOp> v =
+      halo_ops(partition(g, rank, nranks), rank, elem ? g.ncx * g.ncy : g.nbx * g.nby, elem != 0);
+  if ((int)v.size() > max_ops)
+    return -set_err(nullptr, TMG_EARG, "tmg_halo_plan: %d operations, buffer holds %d",
+                    (int)v.size(), max_ops);
+  for (size_t i = 0; i < v.size(); ++i) {
+    ops[4 * i + 0] = v[i].send;
+    ops[4 * i + 1] = v[i].peer;
+    ops[4 * i + 2] = v[i].unit0;
+    ops[4 * i + 3] = v[i].units;
+  }
+  return (int)v.size();
 }
 
 void tmg_destroy(tmg_ctx* c) {

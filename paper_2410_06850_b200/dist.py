@@ -6,9 +6,9 @@ bricks) and keeps one ghost brick layer per neighbouring rank. The CUDA
 library moves the data (NCCL send/recv of whole brick layers, all-reduce of
 the CG dot products, all-gather of the coarse-coarse right-hand side); this
 module holds what the host needs around it: the slab of a global array, the
-NCCL id hand-off over torch.distributed, and the halo plan the library
-follows, written out as data so it can be checked on CPU with gloo
-(tests/test_dist_cpu.py).
+NCCL id hand-off over torch.distributed, and the library's own halo plan
+(tmg_halo_plan, the operations exchange() issues) so the multi-process logic
+can be checked on CPU with gloo (tests/test_dist_cpu.py).
 """
 from __future__ import annotations
 
@@ -22,18 +22,24 @@ def slab(values: np.ndarray, part: dict) -> np.ndarray:
     return np.ascontiguousarray(values[part["cell0"]:part["cell0"] + part["cells"]])
 
 
-def halo_plan(part: dict, rank: int, layer: int) -> list[tuple[int, tuple, tuple]]:
-    """(peer, (send start, stop), (recv start, stop)) in global brick (or cc
-    element) units for one ghost exchange; `layer` units per z-layer. Mirrors
-    exchange() in csrc/abi.cu: the own bottom layer goes to rank - 1 and its
-    top layer comes back as the lower ghost; symmetrically above."""
-    u0, nu = part["brick0"], part["bricks"]
-    plan = []
-    if part["lo"]:
-        plan.append((rank - 1, (u0, u0 + layer), (u0 - layer, u0)))
-    if part["hi"]:
-        plan.append((rank + 1, (u0 + nu - layer, u0 + nu), (u0 + nu, u0 + nu + layer)))
-    return plan
+def halo_plan(grid: GridSpec, ncc, sd: int, nranks: int, rank: int,
+              elem: bool = False) -> list[tuple[str, int, int, int]]:
+    """The library's own halo exchange of slab `rank` (tmg_halo_plan: the
+    operations exchange() in csrc/abi.cu issues as ncclSend / ncclRecv):
+    [("send" | "recv", peer, first global unit, units)], units = bricks or
+    cc elements (elem)."""
+    import ctypes as C
+    from .solver import _Grid, _raise, native
+    L = native()
+    ncc3 = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
+    g = _Grid(grid.nx, grid.ny, grid.nz, grid.lx, grid.ly, grid.lz, (C.c_int64 * 3)(*ncc3), sd)
+    ops = (C.c_int64 * 16)()
+    n = L.tmg_halo_plan(C.byref(g), C.c_int(nranks), C.c_int(rank), C.c_int(int(elem)), ops,
+                        C.c_int(4))
+    if n < 0:
+        _raise(-n, L.tmg_last_error(None).decode())
+    return [("send" if ops[4 * i] else "recv", int(ops[4 * i + 1]), int(ops[4 * i + 2]),
+             int(ops[4 * i + 3])) for i in range(n)]
 
 
 def broadcast_nccl_id(torch_dist) -> bytes:

@@ -136,7 +136,7 @@ EXPORTED_SYMBOLS = (
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
     "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
     "tmg_set_design_generated", "tmg_solve_resident_ex", "tmg_apply_operator_abs",
-    "tmg_set_design_tree",
+    "tmg_set_design_tree", "tmg_halo_plan",
 )
 
 

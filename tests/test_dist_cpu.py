@@ -4,7 +4,8 @@ The GPU data path of a partitioned solve is covered on one device by
 tests/test_gpu_slabs.py (same kernels, ghost layers and reductions; device
 copies instead of NCCL). Here real processes check what the NCCL transport
 relies on: the partition every rank computes independently is one consistent
-cover of the grid, the halo plan pairs every send with the matching receive
+cover of the grid, the library's own halo plan (tmg_halo_plan: the operations
+exchange() issues as ncclSend / ncclRecv) pairs every send with the matching receive
 and delivers exactly the neighbour's boundary layer, the NCCL id reaches all
 ranks, and the slabs of a global array reassemble it.
 """
@@ -52,23 +53,35 @@ def _worker(rank, world, port, out):
         assert [p["hi"] for p in parts] == [1] * (world - 1) + [0]
         # halo exchange following the library's plan: bricks hold their
         # global index; ghosts start at -1 and must end as the neighbour's ids
-        L = (GRID.nx // 8) * (GRID.ny // 8)
-        lo_b = part["brick0"] - part["lo"] * L
-        n_st = part["bricks"] + (part["lo"] + part["hi"]) * L
-        win = -np.ones(n_st, dtype=np.int64)
-        win[part["brick0"] - lo_b:part["brick0"] - lo_b + part["bricks"]] = np.arange(
-            part["brick0"], part["brick0"] + part["bricks"])
-        reqs, recv = [], []
-        for peer, (s0, s1), (r0, r1) in D.halo_plan(part, rank, L):
-            send = torch.from_numpy(win[s0 - lo_b:s1 - lo_b].copy())
-            buf = torch.empty(r1 - r0, dtype=torch.int64)
-            reqs += [dist.isend(send, peer), dist.irecv(buf, peer)]
-            recv.append((r0, buf))
-        for q in reqs:
-            q.wait()
-        for r0, buf in recv:
-            win[r0 - lo_b:r0 - lo_b + len(buf)] = buf.numpy()
-        np.testing.assert_array_equal(win, np.arange(lo_b, lo_b + n_st))
+        L = (GRID.nx // 8) * (GRID.ny // 8)  # bricks per z-layer
+        Le = NCC * NCC  # cc elements per z-layer
+        # the library's own plan (tmg_halo_plan = the ops exchange() issues
+        # over NCCL), carried out with gloo point-to-point
+        for elem, base, count, layer in ((False, part["brick0"], part["bricks"], L),
+                                         (True, part["elem0"], part["elems"], Le)):
+            lo_u = base - part["lo"] * layer
+            n_u = count + (part["lo"] + part["hi"]) * layer
+            win = -np.ones(n_u, dtype=np.int64)
+            win[base - lo_u:base - lo_u + count] = np.arange(base, base + count)
+            plan = D.halo_plan(GRID, NCC, SD, world, rank, elem=elem)
+            assert len(plan) == 2 * (part["lo"] + part["hi"])
+            reqs, recv = [], []
+            for op, peer, u0, nu in plan:
+                assert nu == layer and abs(peer - rank) == 1
+                if op == "send":  # own layers only
+                    assert base <= u0 and u0 + nu <= base + count
+                    reqs.append(dist.isend(torch.from_numpy(win[u0 - lo_u:u0 - lo_u + nu].copy()),
+                                           peer))
+                else:  # ghost layers only
+                    assert u0 + nu <= base or u0 >= base + count
+                    buf = torch.empty(nu, dtype=torch.int64)
+                    reqs.append(dist.irecv(buf, peer))
+                    recv.append((u0, buf))
+            for q in reqs:
+                q.wait()
+            for u0, buf in recv:
+                win[u0 - lo_u:u0 - lo_u + len(buf)] = buf.numpy()
+            np.testing.assert_array_equal(win, np.arange(lo_u, lo_u + n_u))
         # NCCL unique id hand-off (host-only call)
         nid = D.broadcast_nccl_id(dist)
         ids = [None] * world
