@@ -137,6 +137,7 @@ struct tmg_ctx {
   GridParams g{};  // global grid (b0 = 0, nbo = nb, ...)
   int cb = 0;
   int fine_bj = 0;  // fine smoother blocks = cc elements (tmg_mmg_options.fine_blocks)
+  int nu = 1;       // smoother sweeps (MmgOptions::smoother_sweeps); != 1: enqueue_vcycle_nu
   int64_t M = 0;   // global cells
   std::string err;
   // partition
@@ -670,6 +671,133 @@ void enqueue_vcycle_bj(tmg_ctx* c, int init, int par_new) {
   }
 }
 
+// The V-cycle of solver.cpp:272-334 with any number nu of smoother sweeps
+// (MmgOptions::smoother_sweeps; BlockJacobiSmoother::apply, :221-243) on
+// both levels, from unfused phase kernels. Every smoothing stage iterates on
+// its output: y = a + S(b - A a) first, then y += S(b - A y) for each further
+// sweep (from a = 0 for the pre-smoothers), which is the reference's sweep
+// loop written on y; nu = 0 leaves the coarse corrections only.
+void enqueue_vcycle_nu(tmg_ctx* c, int init, int par_new) {
+  const int64_t C = cells_per_brick(c);
+  cudaStream_t st = c->stream;
+  const int nu = c->nu;
+  const size_t cvec = sizeof(double) * (size_t)c->lc;
+  const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+  const int nk = c->fine_bj ? bj_apply_kernels(c->cb, c->g.sd) : 1;
+  if (!init) {  // x, r update + stopping test (the z write is deferred)
+    for (Slab& s : c->slabs)
+      KL(1, launch_jacobi_step(s.g, c->cb, nullptr, s.x, s.pbuf[par_new], s.q, s.r, s.z, s.st,
+                               s.partials, s.history, 0, 1, st));
+    if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
+  }
+  // out = add + B^-1 in (per coarse cell or per cc element), optional r.out
+  auto fine_solve = [&](Slab& s, const double* in, const double* add, double* out,
+                        const double* rdot) {
+    if (c->fine_bj)
+      KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, in, add, out, rdot, s.st,
+                             s.partials, init, s.ybj, st));
+    else
+      KL(1, launch_brick_solve(s.g, c->cb, s.coef, s.Gf, in, add, out, rdot, s.st, s.partials,
+                               init, st));
+  };
+  // ---- fine pre-smoothing r1 = S_nu(r) ----
+  for (int sw = 0; sw < nu; ++sw) {
+    if (sw == 0) {
+      for (Slab& s : c->slabs) fine_solve(s, s.r, nullptr, s.r1, nullptr);
+    } else {
+      XCH(r1, sizeof(double) * C, false);
+      for (Slab& s : c->slabs) KL(1, launch_resid(s.g, c->cb, s.coef, s.r, s.r1, s.t2, s.st, st));
+      for (Slab& s : c->slabs) fine_solve(s, s.t2, s.r1, s.r1, nullptr);
+    }
+  }
+  if (nu == 0)
+    for (Slab& s : c->slabs)
+      CK(cudaMemsetAsync(s.r1 + s.g.b0 * C, 0, sizeof(double) * (size_t)(s.g.nbo * C), st));
+  XCH(r1, sizeof(double) * C, false);
+  for (Slab& s : c->slabs)  // rc = R_c (r - A r1)
+    KL(1, launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st));
+  // ---- coarse pre-smoothing rc0 = S_nu(rc) ----
+  for (int sw = 0; sw < nu; ++sw) {
+    if (sw == 0) {
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.rc, nullptr, s.rc0, st));
+    } else {
+      XCH(rc0, cvec, false);
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_resid(s.g, &s.st->done, s.Ac, s.rc, s.rc0, s.tc, st));
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.tc, s.rc0, s.rc0, st));
+    }
+  }
+  if (nu == 0)
+    for (Slab& s : c->slabs)
+      CK(cudaMemsetAsync(s.rc0 + s.bs0 * c->lc, 0, sizeof(double) * (size_t)(s.nbs * c->lc), st));
+  XCH(rc0, cvec, false);
+  // ---- coarse-coarse: rcc = R_cc (rc - A_c rc0); ecc = A_cc^-1 rcc ----
+  for (Slab& s : c->slabs)
+    KL(1, launch_coarse_restrict(s.g, &s.st->done, s.Ac, s.Rcc, s.rc, s.rc0, c->rcc, st));
+  if (c->nccl()) {
+    const Slab& s = c->slabs[0];
+    NK(ncclAllGather(c->rcc + s.g.e0 * c->lcc, c->rcc, (size_t)(s.g.neo * c->lcc), ncclDouble,
+                     c->comm, st));
+  }
+  if (c->acc_planes)
+    KL(acc_planes_solve_kernels(c->g),
+       launch_acc_planes_solve(c->g, &c->slabs[0].st->done, c->planes.T, c->planes.C, c->rcc,
+                               c->ecc, c->planes.wv, c->symvP, st));
+  else if (c->AccT)
+    KL(2, launch_symv(&c->slabs[0].st->done, c->AccT, c->n_cc, c->rcc, c->symvP, c->ecc, st));
+  else
+    for (Slab& s : c->slabs)
+      KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
+                             c->rcc, c->ecc, st));
+  for (Slab& s : c->slabs)  // rc1 = rc0 + R_cc^T ecc
+    KL(1, launch_coarse_prolong(s.g, &s.st->done, s.Rcc, s.rc0, c->ecc, s.rc1, st));
+  // ---- coarse post-smoothing ec = rc1 + S_nu(rc - A_c rc1) ----
+  if (nu == 0)
+    for (Slab& s : c->slabs)
+      CK(cudaMemcpyAsync(s.ec + s.bs0 * c->lc, s.rc1 + s.bs0 * c->lc,
+                         sizeof(double) * (size_t)(s.nbs * c->lc), cudaMemcpyDeviceToDevice, st));
+  for (int sw = 0; sw < nu; ++sw) {
+    if (sw == 0) {
+      XCH(rc1, cvec, false);
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_resid(s.g, &s.st->done, s.Ac, s.rc, s.rc1, s.tc, st));
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.tc, s.rc1, s.ec, st));
+    } else {
+      XCH(ec, cvec, false);
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_resid(s.g, &s.st->done, s.Ac, s.rc, s.ec, s.tc, st));
+      for (Slab& s : c->slabs)
+        KL(1, launch_coarse_smooth(s.g, &s.st->done, s.Winv, s.tc, s.ec, s.ec, st));
+    }
+  }
+  // ---- fine: r2 = r1 + R_c^T ec; z = r2 + S_nu(r - A r2); r.z ----
+  for (Slab& s : c->slabs)
+    KL(1, launch_prolong_add(s.g, c->cb, s.phi, s.r1, s.ec, s.r2, s.st, st));
+  if (nu == 0) {
+    for (Slab& s : c->slabs)
+      KL(1, launch_add_finish(s.g, c->cb, s.r2, nullptr, s.z, s.r, s.st, s.partials, init, st));
+  }
+  for (int sw = 0; sw < nu; ++sw) {
+    const bool last = sw + 1 == nu;
+    if (sw == 0) {
+      XCH(r2, sizeof(double) * C, false);
+      for (Slab& s : c->slabs) KL(1, launch_resid(s.g, c->cb, s.coef, s.r, s.r2, s.t2, s.st, st));
+      for (Slab& s : c->slabs) fine_solve(s, s.t2, s.r2, s.z, last ? s.r : nullptr);
+    } else {
+      XCH(z, sizeof(double) * C, false);
+      for (Slab& s : c->slabs) KL(1, launch_resid(s.g, c->cb, s.coef, s.r, s.z, s.t2, s.st, st));
+      for (Slab& s : c->slabs) fine_solve(s, s.t2, s.z, s.z, last ? s.r : nullptr);
+    }
+  }
+  if (c->dist()) {
+    reduce_finalize(c, kRedPost, init);
+    XCH(z, sizeof(double) * C, false);
+  }
+}
+
 bool hierarchical(const tmg_ctx* c) {
   return c->kind == TMG_PRECOND_MMG || c->kind == TMG_PRECOND_TWO_GRID;
 }
@@ -678,7 +806,8 @@ bool hierarchical(const tmg_ctx* c) {
 // x0 residual already in r); otherwise after the search step of an iteration.
 void enqueue_precond(tmg_ctx* c, int init, int par_new) {
   if (!hierarchical(c)) return enqueue_jacobi(c, init, par_new);
-  if (c->fine_bj) enqueue_vcycle_bj(c, init, par_new);
+  if (c->nu != 1) enqueue_vcycle_nu(c, init, par_new);
+  else if (c->fine_bj) enqueue_vcycle_bj(c, init, par_new);
   else if (c->dist()) enqueue_vcycle_dist(c, init, par_new);
   else enqueue_vcycle_single(c, init, c->slabs[0].pbuf[par_new]);
 }
@@ -780,7 +909,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   });
   if (!prof) {
     enqueue_precond_init(c);
-  } else if (hierarchical(c) && !c->fine_bj) {
+  } else if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
     Slab& s = s0;
     const GridParams& g = s.g;
     timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
@@ -833,7 +962,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       par ^= 1;
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
-      if (hierarchical(c) && !c->fine_bj) {
+      if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
@@ -1805,8 +1934,9 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
                      "GPU coarse level handles sd^3*L_c <= 64, or a multiple of 64 up to 4096 with "
                      "num_cc_basis <= 20 (got %lld, %lld)",
                      (long long)q, (long long)o->num_cc_basis);
-    if (o->smoother_sweeps != 1)
-      return set_err(c, TMG_ENOTSUP, "GPU smoother is built for smoother_sweeps = 1");
+    if (o->smoother_sweeps < 0 || o->smoother_sweeps > 64)
+      return set_err(c, TMG_ECONFIG, "MmgOptions: smoother_sweeps must lie in [0, 64] (got %d)",
+                     o->smoother_sweeps);
   }
   return guard(c, [&] {
     CK(cudaSetDevice(c->device));
@@ -1861,10 +1991,12 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         if (fine_bj) {
           s.Gbj = owned_e<double>(c, s, bj_doubles_per_element(c->cb, c->g.sd));
           if (bj_apply_kernels((int)c->cb, c->g.sd) > 1) s.ybj = owned<double>(c, s, C);
-          s.r2 = ghosted<double>(c, s, C);
-          s.t2 = ghosted<double>(c, s, C);
         } else {
           s.Gf = owned<double>(c, s, thomas_doubles_per_brick(c->cb));
+        }
+        if (fine_bj || o->smoother_sweeps != 1) {  // unfused V-cycles
+          s.r2 = ghosted<double>(c, s, C);
+          s.t2 = ghosted<double>(c, s, C);
         }
         s.Ac = owned<double>(c, s, 7 * lc * lc);
         s.Bc = owned<double>(c, s, lc * lc);
@@ -2076,6 +2208,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     }
     c->kind = kind;
     c->fine_bj = fine_bj ? 1 : 0;
+    c->nu = hier ? o->smoother_sweeps : 1;
     c->have_setup = true;
     build_graph(c, 4);
   });

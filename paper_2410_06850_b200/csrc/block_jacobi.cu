@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(1024) k_bj32_step(GridParams g, int cb,
 // out = add + x (x in ybuf) over the owned bricks; with rdot, rdot . out
 // finishes the iteration (fin_post) like k_bj_apply
 template <int CB>
-__global__ void __launch_bounds__(CB * CB * CB) k_bj32_finish(GridParams g,
+__global__ void __launch_bounds__(CB * CB * CB) k_add_finish(GridParams g,
                                                              const double* __restrict__ ybuf,
                                                              const double* __restrict__ add,
                                                              double* out,
@@ -415,10 +415,10 @@ void launch_bj_apply(const GridParams& g, int cb, const double* coef, const doub
       launch_pdl(k_bj32_step, grid, dim3(1024), 0, s, g, cb, coef, G, in, ybuf,
                  (const PcgState*)st, k, 1);
     if (cb == 8)
-      launch_pdl(k_bj32_finish<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, (const double*)ybuf,
+      launch_pdl(k_add_finish<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, (const double*)ybuf,
                  add, out, rdot, st, partials, init);
     else
-      launch_pdl(k_bj32_finish<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, (const double*)ybuf,
+      launch_pdl(k_add_finish<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, (const double*)ybuf,
                  add, out, rdot, st, partials, init);
     return;
   }
@@ -428,6 +428,17 @@ void launch_bj_apply(const GridParams& g, int cb, const double* coef, const doub
   else
     launch_pdl(k_bj_apply<8>, dim3((unsigned)g.neo), dim3(64), 0, s, g, cb, coef, G, in, add, out,
                rdot, st, partials, init);
+}
+
+void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
+                       double* out, const double* rdot, PcgState* st, double* partials, int init,
+                       cudaStream_t s) {
+  if (cb == 8)
+    launch_pdl(k_add_finish<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, y, add, out, rdot, st,
+               partials, init);
+  else
+    launch_pdl(k_add_finish<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, y, add, out, rdot, st,
+               partials, init);
 }
 
 void launch_prolong_add(const GridParams& g, int cb, const double* phi, const double* r1,

@@ -254,6 +254,15 @@ void launch_init(const GridParams& g, int cb, const double* coef, const double* 
 void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s);
+// out = add + A_II^{-1} in per brick (per-coarse-cell fine blocks); rdot: also
+// rdot . out -> fin_post (the generic nu-sweep V-cycle)
+void launch_brick_solve(const GridParams& g, int cb, const double* coef, const double* Gf,
+                        const double* in, const double* add, double* out, const double* rdot,
+                        PcgState* st, double* partials, int init, cudaStream_t s);
+// out = add + y over the owned bricks (add nullable); rdot: rdot . out -> fin_post
+void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
+                       double* out, const double* rdot, PcgState* st, double* partials, int init,
+                       cudaStream_t s);
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s);

@@ -532,6 +532,62 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
   }
 }
 
+// --------------------------------- generic block solve (nu != 1 V-cycles)
+// out = add + A_II^{-1} in on every owned brick (add nullable, may alias
+// out); with rdot, rdot . out is reduced and finishes the iteration like K4
+// (fin_post). One smoother sweep z += S (r - A z) of BlockJacobiSmoother
+// (solver.cpp:221-243) for the per-coarse-cell blocks, composed with k_resid
+// by the generic V-cycle (abi.cu enqueue_vcycle_nu).
+template <int CB>
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
+                                                                  const double* __restrict__ coef,
+                                                                  int64_t M,
+                                                                  const double* __restrict__ Gf,
+                                                                  const double* __restrict__ in,
+                                                                  const double* add, double* out,
+                                                                  const double* __restrict__ rdot,
+                                                                  PcgState* st, double* partials,
+                                                                  int init) {
+  pdl_trigger();
+  constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
+  const int b = (int)(blockIdx.x + g.b0);
+  const double* G = Gf + (size_t)b * Thomas<CB>::PER_BRICK;
+  sm.th.slots = sm.slots;
+  thomas_init<CB>(sm.th);
+  __syncthreads();
+  thomas_prefetch<CB>(sm.th, G);
+  pdl_wait();
+  if (st->done) {
+    thomas_drain<CB>(sm.th);
+    return;
+  }
+  const int t = threadIdx.x;
+  for (int c = t; c < C; c += NT) {
+    const size_t s = bofs(b, C) + c;
+    sm.tv[c] = in[s];
+    sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
+  }
+  __syncthreads();
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);
+  double rz = 0.0;
+  for (int c = t; c < C; c += NT) {
+    const size_t s = bofs(b, C) + c;
+    const double o = add ? add[s] + sm.tv[c] : sm.tv[c];
+    out[s] = o;
+    if (rdot) rz += rdot[s] * o;
+  }
+  if (!rdot) return;
+  double v[1] = {rz};
+  block_sum_k<NT, 1>(v, sm.red);
+  double tot[1];
+  if (grid_reduce_last_k<1>(v, partials, &st->ticket[3], tot, &sm.flag, sm.red) && t == 0) {
+    if (g.dist) st->loc[kRedPost] = tot[0];
+    else fin_post(st, tot[0], init);
+  }
+}
+
 // ---------------------------------------- Jacobi / identity preconditioner
 template <int CB>
 __global__ void __launch_bounds__(CB * CB * CB) k_jacobi_step(GridParams g, const double* __restrict__ dinv,
@@ -598,6 +654,8 @@ size_t post_smem(int cb) { return cb == 8 ? sizeof(PostSmem<8>) : sizeof(PostSme
 template <int CB>
 static void set_attrs() {
   cudaFuncSetAttribute(k_update<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem(CB));
+  cudaFuncSetAttribute(k_brick_solve<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)update_smem(CB));
   cudaFuncSetAttribute(K_POST<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)post_smem(CB));
 }
 
@@ -612,6 +670,17 @@ void launch_coefficients(const GridParams& g, int cb, const double* kappa, const
   const int64_t M = g.mst;
   if (cb == 8) k_coefficients<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, coef, M);
   else k_coefficients<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, coef, M);
+}
+void launch_brick_solve(const GridParams& g, int cb, const double* coef, const double* Gf,
+                        const double* in, const double* add, double* out, const double* rdot,
+                        PcgState* st, double* partials, int init, cudaStream_t s) {
+  const int64_t M = g.mst;
+  if (cb == 8)
+    launch_pdl(k_brick_solve<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g,
+               coef, M, Gf, in, add, out, rdot, st, partials, init);
+  else
+    launch_pdl(k_brick_solve<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g,
+               coef, M, Gf, in, add, out, rdot, st, partials, init);
 }
 void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
                  int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s) {

@@ -721,3 +721,55 @@ def test_acc_planes_matches_dense(monkeypatch, n, ncc, sd, lcc, kmin):
     assert rb.report.converged
     assert abs(ra.report.iterations - rb.report.iterations) <= 1
     assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
+
+
+# ---------------------------------------------- smoother sweeps nu != 1
+
+@pytest.mark.parametrize("nu", [0, 2, 3])
+@pytest.mark.parametrize("fine", ["cell", "cc"])
+def test_smoother_sweeps_vs_oracle(nu, fine):
+    """MmgOptions::smoother_sweeps (solver.hpp:141-146; BlockJacobiSmoother
+    sweeps, solver.cpp:221-243) on both levels: the generic V-cycle
+    (enqueue_vcycle_nu) against the oracle with the same partition."""
+    n, ncc, sd = 32, 2, 2
+    _, kappa = problem(n, 1e-3)
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    m = O.Precond("mmg", s, O.hierarchy(O.grid(n), ncc, sd), fine_blocks=fine,
+                  coarse_blocks="cc", sweeps=nu)
+    r = np.random.default_rng(3).standard_normal(n ** 3)
+    c = ctx_for(n, ncc, sd, kappa)
+    c.setup("mmg", MmgOptions(smoother_sweeps=nu, fine_blocks="cc" if fine == "cc" else "coarse_cell"))
+    z_ref = m.apply(r)
+    z = c.apply_preconditioner(r)
+    assert np.linalg.norm(z - z_ref) <= 1e-9 * np.linalg.norm(z_ref)
+    if nu == 0:  # coarse corrections only: singular M, PCG stalls (the reference's too)
+        ref = O.pcg(s, s.rhs, m, rtol=1e-8, max_iterations=8)
+        res = c.pcg(s.rhs, rtol=1e-8, max_iterations=8)
+        np.testing.assert_allclose(res.report.residual_history, ref.residual_history, rtol=1e-6)
+        return
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8, max_iterations=3000)
+    res = c.pcg(s.rhs, rtol=1e-8, max_iterations=3000)
+    assert res.report.converged == ref.converged
+    assert iters_close(res.report.iterations, ref.iterations), (res.report.iterations,
+                                                                ref.iterations)
+    assert np.linalg.norm(res.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("nu", [2, 3])
+def test_smoother_sweeps_on_slabs(nu):
+    """nu != 1 on the partitioned path (in-process slabs): same
+    preconditioner and PCG as one slab."""
+    n, ncc, sd = 32, 2, 2
+    _, kappa = problem(n, 1e-6)
+    out = []
+    for slabs in (1, 2):
+        c = Context(GridSpec(n, n, n), ncc, sd, slabs=slabs)
+        c.set_conductivity(kappa, BC)
+        c.setup("mmg", MmgOptions(smoother_sweeps=nu, fine_blocks="coarse_cell"))
+        r = np.random.default_rng(4).standard_normal(n ** 3)
+        b = c.assemble_rhs(np.ones(n ** 3))
+        out.append((c.apply_preconditioner(r), c.pcg(b, rtol=1e-8, max_iterations=3000)))
+    (za, ra), (zb, rb) = out
+    assert np.linalg.norm(za - zb) <= 1e-9 * np.linalg.norm(za)
+    assert abs(ra.report.iterations - rb.report.iterations) <= 1
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
