@@ -168,6 +168,14 @@ int tmg_set_design_generated(tmg_ctx* ctx, const tmg_design_gen* gen, double kap
                              double kappa_hi, int p, const tmg_patch* patches, int npatch,
                              double* rho_out);
 
+/* frozen_bench_design (rng.cpp:16-53, the reference's bench design) on the
+ * device: Lcg64(seed) uniforms, `passes` 7-point averaging sweeps, the
+ * ceil(vstar M) largest -> 1 (ties by lower index); bit-identical to the
+ * reference's. Then as tmg_set_design; rho_out (nullable) gets the design. */
+int tmg_set_design_frozen(tmg_ctx* ctx, double vstar, uint64_t seed, int passes, double kappa_lo,
+                          double kappa_hi, int p, const tmg_patch* patches, int npatch,
+                          double* rho_out);
+
 /* BASELINE configs[4]'s "seeded tree-like binary field" (no reference
  * generator exists, inputs.tree_design restates it): a binary
  * tree of `depth` levels of capsule segments rooted at the centre of the z = 0

@@ -1378,6 +1378,17 @@ int tmg_set_design_generated(tmg_ctx* c, const tmg_design_gen* gen, double lo, d
   });
 }
 
+int tmg_set_design_frozen(tmg_ctx* c, double vstar, uint64_t seed, int passes, double lo,
+                          double hi, int p, const tmg_patch* patches, int np, double* rho_out) {
+  if (!c) return set_err(c, TMG_EARG, "tmg_set_design_frozen: null argument");
+  const int rc = set_design_common(c, lo, hi, p, patches, np, vstar, passes, 0);
+  if (rc) return rc;
+  const tmg_grid& G = c->grid;
+  return generate_design(c, lo, hi, p, rho_out, [&](double* rho, double* f, void* scratch) {
+    launch_frozen_design(G.nx, G.ny, G.nz, vstar, seed, passes, rho, f, scratch, c->stream);
+  });
+}
+
 int tmg_set_design_tree(tmg_ctx* c, const tmg_tree_gen* t, double lo, double hi, int p,
                         const tmg_patch* patches, int np, double* rho_out) {
   if (!c || !t) return set_err(c, TMG_EARG, "tmg_set_design_tree: null argument");

@@ -216,6 +216,46 @@ __global__ void k_tree_field(double* f, int64_t nx, int64_t ny, int64_t nz, doub
 
 static void filter_select(int64_t nx, int64_t ny, int64_t nz, double vf, int passes, int radius,
                           double* rho, double* f, void* scratch, cudaStream_t s);
+static void select_top(int64_t m, double vf, double* rho, const double* f, void* scratch,
+                       cudaStream_t s);
+static void lcg_fill(double* f, int64_t m, uint64_t seed, cudaStream_t s);
+
+// One 7-point averaging sweep of frozen_bench_design (rng.cpp:21-37): the
+// cell and its in-domain face neighbours summed in the reference's order
+// (self, x-, x+, y-, y+, z-, z+), divided by their count.
+__global__ void k_star_average(const double* __restrict__ in, double* out, int64_t nx, int64_t ny,
+                               int64_t nz) {
+  const int64_t m = nx * ny * nz, sy = nx, sz = nx * ny;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < m;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = s % nx, j = (s / nx) % ny, k = s / sz;
+    double sum = in[s];
+    int n = 1;
+    if (i > 0) { sum += in[s - 1]; ++n; }
+    if (i < nx - 1) { sum += in[s + 1]; ++n; }
+    if (j > 0) { sum += in[s - sy]; ++n; }
+    if (j < ny - 1) { sum += in[s + sy]; ++n; }
+    if (k > 0) { sum += in[s - sz]; ++n; }
+    if (k < nz - 1) { sum += in[s + sz]; ++n; }
+    out[s] = sum / n;
+  }
+}
+
+// frozen_bench_design (rng.cpp:16-53): LCG uniforms, `passes` 7-point
+// averaging sweeps, the ceil(vstar M) largest -> 1 (ties by lower index).
+void launch_frozen_design(int64_t nx, int64_t ny, int64_t nz, double vstar, uint64_t seed,
+                          int passes, double* rho, double* f, void* scratch, cudaStream_t s) {
+  const int64_t m = nx * ny * nz;
+  lcg_fill(f, m, seed, s);
+  double* t = (double*)scratch;  // the first m doubles of the scratch
+  int64_t gb = (m + kGenThreads - 1) / kGenThreads;
+  if (gb > 148 * 64) gb = 148 * 64;
+  for (int p = 0; p < passes; ++p) {
+    k_star_average<<<(unsigned)gb, kGenThreads, 0, s>>>(f, t, nx, ny, nz);
+    cudaMemcpyAsync(f, t, sizeof(double) * (size_t)m, cudaMemcpyDeviceToDevice, s);
+  }
+  select_top(m, vstar, rho, f, scratch, s);
+}
 
 static void lcg_fill(double* f, int64_t m, uint64_t seed, cudaStream_t s) {
   const int G = 16;
@@ -252,10 +292,6 @@ static void filter_select(int64_t nx, int64_t ny, int64_t nz, double vf, int pas
                           double* rho, double* f, void* scratch, cudaStream_t s) {
   const int64_t m = nx * ny * nz;
   double* t = (double*)scratch;
-  unsigned long long* hist = (unsigned long long*)(t + m);
-  const int64_t chunk = 65536, chunks = (m + chunk - 1) / chunk;
-  unsigned long long* eq = hist + 256;
-  uint64_t* sel = (uint64_t*)(eq + chunks);
   int64_t gb = (m + kGenThreads - 1) / kGenThreads;
   if (gb > 148 * 64) gb = 148 * 64;
   for (int p = 0; p < passes; ++p) {
@@ -263,6 +299,20 @@ static void filter_select(int64_t nx, int64_t ny, int64_t nz, double vf, int pas
     k_window_sum<<<(unsigned)gb, kGenThreads, 0, s>>>(t, rho, nx, ny, nz, 1, radius, 0);
     k_window_sum<<<(unsigned)gb, kGenThreads, 0, s>>>(rho, f, nx, ny, nz, 2, radius, 1);
   }
+  select_top(m, vf, rho, f, scratch, s);
+}
+
+// rho = the ceil(vf M) largest values of f -> 1, ties by lower index
+// (rng.cpp:39-51); f is not modified.
+static void select_top(int64_t m, double vf, double* rho, const double* f, void* scratch,
+                       cudaStream_t s) {
+  double* t = (double*)scratch;
+  unsigned long long* hist = (unsigned long long*)(t + m);
+  const int64_t chunk = 65536, chunks = (m + chunk - 1) / chunk;
+  unsigned long long* eq = hist + 256;
+  uint64_t* sel = (uint64_t*)(eq + chunks);
+  int64_t gb = (m + kGenThreads - 1) / kGenThreads;
+  if (gb > 148 * 64) gb = 148 * 64;
   // solid = min(M, ceil(vf M)) largest (rng.cpp:39-51)
   int64_t solid = (int64_t)ceil(vf * (double)m);
   if (solid > m) solid = m;

@@ -290,6 +290,8 @@ size_t gen_scratch_bytes(int64_t m);
 void launch_box_filter_design(int64_t nx, int64_t ny, int64_t nz, double vf, uint64_t seed,
                               int passes, int radius, double* rho, double* f, void* scratch,
                               cudaStream_t s);
+void launch_frozen_design(int64_t nx, int64_t ny, int64_t nz, double vstar, uint64_t seed,
+                          int passes, double* rho, double* f, void* scratch, cudaStream_t s);
 void launch_tree_design(int64_t nx, int64_t ny, int64_t nz, double lx, double ly, double lz,
                         double vf, uint64_t seed, int passes, int radius, const double* seg,
                         int nseg, double amp, double* rho, double* f, void* scratch,

@@ -136,7 +136,7 @@ EXPORTED_SYMBOLS = (
     "tmg_sensitivity", "tmg_simp_init", "tmg_simp_step", "tmg_simp_download",
     "tmg_optim_init", "tmg_optim_step", "tmg_optim_evaluate", "tmg_optim_download",
     "tmg_set_design_generated", "tmg_solve_resident_ex", "tmg_apply_operator_abs",
-    "tmg_set_design_tree", "tmg_halo_plan",
+    "tmg_set_design_tree", "tmg_halo_plan", "tmg_set_design_frozen",
 )
 
 
@@ -355,6 +355,19 @@ class Context:
         self._check(native().tmg_set_design_generated(
             self._p, C.byref(g), C.c_double(kappa_lo), C.c_double(kappa_hi), C.c_int(p), parr,
             C.c_int(n), _ptr(rho) if rho is not None else None))
+        return rho
+
+    def set_design_frozen(self, vstar, kappa_lo, kappa_hi=1.0, p=3,
+                          boundary: BoundarySpec = None, seed=20240501, passes=2,
+                          return_rho=False):
+        """frozen_bench_design (rng.cpp:16-53) on the device, bit-identical
+        to the reference's (tmg_set_design_frozen), then as set_design."""
+        parr, n = boundary._c()
+        rho = np.empty(self.grid.num_cells()) if return_rho else None
+        self._check(native().tmg_set_design_frozen(
+            self._p, C.c_double(vstar), C.c_uint64(seed), C.c_int(passes), C.c_double(kappa_lo),
+            C.c_double(kappa_hi), C.c_int(p), parr, C.c_int(n),
+            _ptr(rho) if rho is not None else None))
         return rho
 
     def set_design_tree(self, vf, kappa_lo, kappa_hi=1.0, p=3, boundary: BoundarySpec = None,

@@ -76,3 +76,18 @@ def test_tree_design_is_a_tree_touching_the_sink():
     b = c.assemble_rhs(np.ones(n ** 3))
     r = c.pcg(b, rtol=1e-8)
     assert r.report.converged and r.report.iterations < 100
+
+
+# ------------------------------ the reference's own bench design generator
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("n,vstar,passes,seed", [(16, 0.3, 2, 20240501), (32, 0.3, 2, 20240501),
+                                                 (32, 0.15, 0, 7), (64, 0.4, 3, 11)])
+def test_frozen_bench_design_bitwise_vs_reference(n, vstar, passes, seed):
+    """tmg_set_design_frozen against the compiled reference's
+    frozen_bench_design (rng.cpp:16-53) itself."""
+    ref = O.ref_frozen_bench_design(n, vstar, seed=seed, passes=passes)
+    c = Context(GridSpec(n, n, n), n // 8 // 2 or 1, 2)
+    rho = c.set_design_frozen(vstar, 1e-3, boundary=BC, seed=seed, passes=passes,
+                              return_rho=True)
+    np.testing.assert_array_equal(rho, ref)

@@ -1,9 +1,11 @@
-"""Set-up cost vs local-eigensolver settings at BASELINE configs[1] (diagnostics):
-for each (eig_tol, eig_degree) the set-up time (second set-up, buffers pooled),
-PCG iterations and solve time. Prints one JSON line per setting.
+"""Set-up cost vs local-eigensolver settings (diagnostics): for each
+(eig_tol, eig_degree) the warm set-up time (second set-up, buffers pooled),
+PCG iterations and solve time at BASELINE configs[K]. Run with
+TMG_SETUP_PROFILE=1 for the per-phase device times on stderr.
 
-    python tools/setup_sweep.py
+    python tools/setup_sweep.py [--config 3] [--settings "1e-11:32,1e-9:32,1e-9:24"]
 """
+import argparse
 import json
 import os
 import sys
@@ -14,20 +16,27 @@ R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, R)
 from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, inputs  # noqa: E402
 
-cfg = dict(inputs.CONFIGS[1])
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=1)
+ap.add_argument("--settings", default="1e-11:32,1e-10:32,1e-9:32,1e-8:32,1e-11:24,1e-9:24,1e-9:16")
+a = ap.parse_args()
+cfg = dict(inputs.CONFIGS[a.config])
 n = cfg["n"]
-rho = inputs.box_filter_design(n, cfg["vf"], passes=cfg["passes"], radius=cfg["radius"])
-kappa = inputs.conductivity(rho, cfg["kmin"])
 ctx = Context(GridSpec(n, n, n), cfg["ncc"], cfg["sd"], device=0)
-ctx.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0))
+ctx.set_design_generated(cfg["vf"], cfg["kmin"], 1.0, 3,
+                         BoundarySpec.bottom_center_patch(1.0, 1.0, 0.2, 0.0),
+                         passes=cfg["passes"], radius=cfg["radius"])
 b = ctx.assemble_rhs(np.ones(n ** 3))
-settings = [(0.0, 0), (1e-10, 0), (1e-9, 0), (1e-8, 0), (1e-7, 0), (0.0, 24), (0.0, 16), (1e-9, 24), (1e-8, 16)]
-for tol, deg in settings:
-    o = MmgOptions(eig_tol=tol, eig_degree=deg)
+ctx.upload_rhs(b)
+for item in a.settings.split(","):
+    tol, deg = item.split(":")
+    o = MmgOptions(eig_tol=float(tol), eig_degree=int(deg), num_cc_basis=cfg.get("lcc", 8),
+                   fine_blocks="coarse_cell")
     ctx.setup("mmg", o)
+    print(f"--- eig_tol {tol} degree {deg} (warm set-up below)", file=sys.stderr, flush=True)
     ctx.setup("mmg", o)
-    res = ctx.pcg(b, rtol=1e-8, max_iterations=1000)
-    rep = res.report
-    print(json.dumps({"eig_tol": tol or 1e-11, "eig_degree": deg or 32, "setup_ms": rep.setup_seconds * 1e3,
-                      "iterations": rep.iterations, "solve_ms": rep.solve_seconds * 1e3,
-                      "converged": rep.converged}), flush=True)
+    ctx.upload_rhs(b)
+    rep = ctx.solve_resident(1e-8, 5000)
+    print(json.dumps({"config": a.config, "eig_tol": float(tol), "eig_degree": int(deg),
+                      "setup_ms": rep.setup_seconds * 1e3, "iterations": rep.iterations,
+                      "solve_ms": rep.solve_seconds * 1e3, "converged": rep.converged}), flush=True)
