@@ -116,6 +116,7 @@ struct Slab {
   double* Winv = nullptr;
   double* Gbj = nullptr;  // block-Jacobi plane Schur inverses (virtual-global per element)
   double* ybj = nullptr;  // E = 32 block-Jacobi apply: per-cell plane-sweep values
+  double* accRows = nullptr;  // row-distributed A_cc planes: this slab's rows [ncz][P/total][P]
   double *r2 = nullptr, *t2 = nullptr;  // cc-block-smoothed V-cycle: r1 + R_c^T e_c, r - A r2
   // vectors
   double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr,
@@ -162,6 +163,7 @@ struct tmg_ctx {
   double* AccT = nullptr;   // single slab: lower 64x64 tiles of A_cc^-1
   double* accP = nullptr;   // single slab, plane-Thomas A_cc solve: tiles + couplings + work
   bool acc_planes = false;
+  bool acc_rows = false;  // partitioned: row blocks of the plane inverses per slab
   AccPlanesRef planes{};
   double* symvP = nullptr;  // single slab: GEMV partials
   double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
@@ -327,6 +329,8 @@ void free_setup(tmg_ctx* c) {
   dfree_null(c, c->AccT);
   dfree_null(c, c->accP);
   c->acc_planes = false;
+  c->acc_rows = false;
+  for (Slab& s : c->slabs) dfree_null(c, s.accRows);
   dfree_null(c, c->symvP);
   dfree_null(c, c->Ainv);
   dfree_null(c, c->rcc);
@@ -549,6 +553,39 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
                     st));
 }
 
+// ecc = A_cc^-1 rcc on the full-length process vectors (rcc complete on
+// every process): the plane block Thomas (replicated, or row-distributed with
+// an in-place all-gather per plane step), the symmetric-tiles GEMV (single
+// slab), or the row blocks of the dense inverse (partitioned).
+void enqueue_acc_solve(tmg_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int* done = &c->slabs[0].st->done;
+  if (c->acc_rows) {
+    const int64_t P = c->g.ncx * c->g.ncy * c->lcc, nr = P / c->total;
+    std::vector<AccRowBlock> blocks;
+    for (Slab& s : c->slabs) blocks.push_back(AccRowBlock{s.accRows, (int64_t)s.id * nr, nr});
+    const int rank = c->slabs[0].id;
+    KL(acc_rows_solve_kernels(c->g, (int)blocks.size()),
+       launch_acc_rows_solve(c->g, done, c->planes.C, c->rcc, c->ecc, c->planes.wv, blocks,
+                             [&](double* plane) {
+                               if (c->nccl())
+                                 NK(ncclAllGather(plane + (int64_t)rank * nr, plane, (size_t)nr,
+                                                  ncclDouble, c->comm, st));
+                             },
+                             st));
+  } else if (c->acc_planes) {
+    KL(acc_planes_solve_kernels(c->g),
+       launch_acc_planes_solve(c->g, done, c->planes.T, c->planes.C, c->rcc, c->ecc,
+                               c->planes.wv, c->symvP, st));
+  } else if (c->AccT) {
+    KL(2, launch_symv(done, c->AccT, c->n_cc, c->rcc, c->symvP, c->ecc, st));
+  } else {
+    for (Slab& s : c->slabs)
+      KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
+                             c->rcc, c->ecc, st));
+  }
+}
+
 // partitioned coarse + coarse-coarse levels (solver.cpp:292-319): rc -> ec
 void enqueue_coarse_dist(tmg_ctx* c) {
   cudaStream_t st = c->stream;
@@ -563,14 +600,7 @@ void enqueue_coarse_dist(tmg_ctx* c) {
     const int64_t own = s.g.neo * c->lcc;
     NK(ncclAllGather(c->rcc + s.g.e0 * c->lcc, c->rcc, (size_t)own, ncclDouble, c->comm, st));
   }
-  if (c->acc_planes)  // the whole plane solve, replicated (once for in-process slabs)
-    KL(acc_planes_solve_kernels(c->g),
-       launch_acc_planes_solve(c->g, &c->slabs[0].st->done, c->planes.T, c->planes.C, c->rcc, c->ecc,
-                               c->planes.wv, c->symvP, st));
-  else
-    for (Slab& s : c->slabs)
-      KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
-                             c->rcc, c->ecc, st));
+  enqueue_acc_solve(c);  // replicated or row-distributed (once for in-process slabs)
   for (Slab& s : c->slabs)
     KL(1, launch_coarse_prolong(s.g, &s.st->done, s.Rcc, s.rc0, c->ecc, s.rc1, st));
   XCH(rc1, cvec, false);
@@ -741,16 +771,7 @@ void enqueue_vcycle_nu(tmg_ctx* c, int init, int par_new) {
     NK(ncclAllGather(c->rcc + s.g.e0 * c->lcc, c->rcc, (size_t)(s.g.neo * c->lcc), ncclDouble,
                      c->comm, st));
   }
-  if (c->acc_planes)
-    KL(acc_planes_solve_kernels(c->g),
-       launch_acc_planes_solve(c->g, &c->slabs[0].st->done, c->planes.T, c->planes.C, c->rcc,
-                               c->ecc, c->planes.wv, c->symvP, st));
-  else if (c->AccT)
-    KL(2, launch_symv(&c->slabs[0].st->done, c->AccT, c->n_cc, c->rcc, c->symvP, c->ecc, st));
-  else
-    for (Slab& s : c->slabs)
-      KL(1, launch_gemv_rows(&s.st->done, c->Ainv, c->n_cc, s.g.e0 * c->lcc, s.g.neo * c->lcc,
-                             c->rcc, c->ecc, st));
+  enqueue_acc_solve(c);
   for (Slab& s : c->slabs)  // rc1 = rc0 + R_cc^T ecc
     KL(1, launch_coarse_prolong(s.g, &s.st->done, s.Rcc, s.rc0, c->ecc, s.rc1, st));
   // ---- coarse post-smoothing ec = rc1 + S_nu(rc - A_c rc1) ----
@@ -2128,11 +2149,17 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         g0.ncz = c->g.ncz;
         g0.ncc = c->g.ncc;
         const int64_t P = g0.ncx * g0.ncy * lcc;
+        // partitioned contexts: every slab keeps only its row block of the
+        // plane inverses (launch_acc_rows_solve; TMG_ACC_ROWS=0/1 overrides
+        // the default of >= 4 slabs)
+        const char* arow = getenv("TMG_ACC_ROWS");
+        const bool rows = c->dist() && c->total > 1 && P % c->total == 0 &&
+                          (arow ? arow[0] == '1' : c->total >= 4);
         double* Gd = dalloc<double>(c, g0.ncz * P * P);
-        c->accP = dalloc<double>(c, acc_planes_doubles(g0));
         const int64_t ts = sym_tiles_doubles(P);
-        double* T = c->accP;
-        double* C = T + g0.ncz * ts;
+        c->accP = dalloc<double>(c, acc_planes_doubles(g0) - (rows ? g0.ncz * ts : 0));
+        double* T = rows ? nullptr : c->accP;
+        double* C = c->accP + (rows ? 0 : g0.ncz * ts);
         double* wv = C + g0.ncc * lcc * lcc;
         for (size_t k = 0; k < c->slabs.size(); ++k)
           launch_acc_assemble_planes(c->slabs[k].g, c->slabs[k].Ac, c->slabs[k].Rcc, Gd, C, c->stream,
@@ -2149,10 +2176,21 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         work = dalloc<double>(c, dense_inverse_work_doubles(P));
         acc_planes_factor(g0, Gd, C, T, work, c->slabs[0].d_status + 2, c->stream);
         CK(cudaGetLastError());
+        if (rows) {  // each slab's rows of every dense plane inverse
+          const int64_t nr = P / c->total;
+          for (Slab& s : c->slabs) {
+            s.accRows = dalloc<double>(c, g0.ncz * nr * P);
+            for (int64_t k = 0; k < g0.ncz; ++k)
+              CK(cudaMemcpyAsync(s.accRows + k * nr * P, Gd + k * P * P + (int64_t)s.id * nr * P,
+                                 sizeof(double) * (size_t)(nr * P), cudaMemcpyDeviceToDevice,
+                                 c->stream));
+          }
+        }
         mark("acc_planes");
         c->symvP = dalloc<double>(c, sym_partials_doubles(P));
         c->planes = AccPlanesRef{T, C, wv};
         c->acc_planes = true;
+        c->acc_rows = rows;
         CK(cudaStreamSynchronize(c->stream));
         dfree(c, Gd);
       } else {

@@ -96,7 +96,7 @@ void acc_planes_factor(const GridParams& g, double* Gd, const double* C, double*
       k_acc_schur<<<dim3((unsigned)nxy, (unsigned)nxy), 128, sm, s>>>(
           Sk, Sk - P * P, C + k * nxy * L * L, P, L);
     dense_spd_inverse(Sk, P, work, status, s);
-    pack_sym_tiles(Sk, P, T + k * sym_tiles_doubles(P), s);
+    if (T) pack_sym_tiles(Sk, P, T + k * sym_tiles_doubles(P), s);  // T null: keep Gd only
   }
 }
 
@@ -127,6 +127,49 @@ void launch_acc_planes_solve(const GridParams& g, const int* done, const double*
     launch_symv(done, T + k * ts, P, w, partials, t, s);
     launch_pdl(k_acc_sub, dim3(nb), dim3(256), 0, s, done, ecc + k * P, (const double*)t, P);
   }
+}
+
+// Row-distributed plane solve (partitioned contexts): slab j
+// keeps rows [r0, r0 + nr) of every dense plane inverse, R[k][nr][P]; every
+// plane step forms the coupled right-hand side (replicated, P values), each
+// slab multiplies its row block, and the caller all-gathers the plane's
+// rows between steps (`gather`, an in-place NCCL all-gather; nothing for the
+// slabs of one process, which share x).
+void launch_acc_rows_solve(const GridParams& g, const int* done, const double* C,
+                           const double* rcc, double* ecc, double* wv,
+                           const std::vector<AccRowBlock>& blocks,
+                           const std::function<void(double* plane)>& gather, cudaStream_t s) {
+  const int64_t P = g.ncx * g.ncy * g.lcc, nxy = g.ncx * g.ncy, K = g.ncz;
+  const int L = g.lcc;
+  double* w = wv;
+  double* t = wv + P;
+  const unsigned nb = (unsigned)((P + 255) / 256);
+  for (int64_t k = 0; k < K; ++k) {
+    const double* rk = rcc + k * P;
+    const double* in = rk;
+    if (k > 0) {
+      launch_pdl(k_acc_couple, dim3(nb), dim3(256), 0, s, done, C + k * nxy * L * L,
+                 (const double*)(ecc + (k - 1) * P), rk, w, P, L, 0);
+      in = w;
+    }
+    for (const AccRowBlock& b : blocks)
+      launch_gemv_block(done, b.R + k * b.nr * P, b.nr, P, in, ecc + k * P + b.r0, s);
+    gather(ecc + k * P);
+  }
+  for (int64_t k = K - 2; k >= 0; --k) {
+    launch_pdl(k_acc_couple, dim3(nb), dim3(256), 0, s, done, C + (k + 1) * nxy * L * L,
+               (const double*)(ecc + (k + 1) * P), (const double*)nullptr, w, P, L, 1);
+    for (const AccRowBlock& b : blocks) {
+      launch_gemv_block(done, b.R + k * b.nr * P, b.nr, P, w, t + b.r0, s);
+      launch_pdl(k_acc_sub, dim3((unsigned)((b.nr + 255) / 256)), dim3(256), 0, s, done,
+                 ecc + k * P + b.r0, (const double*)(t + b.r0), b.nr);
+    }
+    gather(ecc + k * P);
+  }
+}
+
+int acc_rows_solve_kernels(const GridParams& g, int nblocks) {
+  return (int)((g.ncz - 1) + g.ncz * nblocks + (g.ncz - 1) * (1 + 2 * nblocks));
 }
 
 // kernels launched per solve (for the launch count)

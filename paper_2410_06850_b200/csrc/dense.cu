@@ -415,6 +415,12 @@ void launch_gemv(const int* done, const double* A, int64_t n, const double* x, d
   k_gemv<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(done, A, n, n, x, y);
 }
 
+void launch_gemv_block(const int* done, const double* A, int64_t nrows, int64_t ncols,
+                       const double* x, double* y, cudaStream_t s) {
+  launch_pdl(k_gemv, dim3((unsigned)((nrows + 7) / 8)), dim3(256), 0, s, done, A, nrows, ncols, x,
+             y);
+}
+
 void launch_gemv_rows(const int* done, const double* A, int64_t n, int64_t row0, int64_t nrows,
                       const double* x, double* y, cudaStream_t s) {
   // rows of A and y shifted so the kernel's row r is global row row0 + r

@@ -3,7 +3,9 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <functional>
 #include <map>
+#include <vector>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -169,6 +171,18 @@ void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv,
                             cudaStream_t s);
 void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cudaStream_t s);
 // A_cc as a block Thomas over the cc-element z-planes (acc_planes.cu)
+struct AccRowBlock {  // rows [r0, r0 + nr) of every plane inverse: R[k][nr][P]
+  const double* R;
+  int64_t r0, nr;
+};
+void launch_acc_rows_solve(const GridParams& g, const int* done, const double* C,
+                           const double* rcc, double* ecc, double* wv,
+                           const std::vector<AccRowBlock>& blocks,
+                           const std::function<void(double* plane)>& gather, cudaStream_t s);
+int acc_rows_solve_kernels(const GridParams& g, int nblocks);
+// y[0..nrows) = A x for a dense nrows x ncols block (one warp per row)
+void launch_gemv_block(const int* done, const double* A, int64_t nrows, int64_t ncols,
+                       const double* x, double* y, cudaStream_t s);
 struct AccPlanesRef {
   const double* T;  // ncz packed symmetric plane inverses
   const double* C;  // z-lo coupling blocks [element][L_cc][L_cc]

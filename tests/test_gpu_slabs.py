@@ -190,3 +190,28 @@ def test_slab_acc_planes_match_single(n, ncc, sd, slabs, kmin, monkeypatch):
     assert rd.report.converged and rp.report.converged
     assert abs(rd.report.iterations - rp.report.iterations) <= 1
     assert np.linalg.norm(rd.x - rp.x) <= 1e-7 * np.linalg.norm(rd.x)
+
+
+@pytest.mark.parametrize("slabs", [2, 4])
+def test_row_distributed_acc_planes(monkeypatch, slabs):
+    """A_cc's plane block Thomas with each slab keeping only its row block of
+    every plane inverse (TMG_ACC_ROWS=1, the default from 4 ranks; an
+    all-gather of each plane's rows per step under NCCL): the same
+    preconditioner and PCG as the replicated plane solve on one slab."""
+    from paper_2410_06850_b200 import MmgOptions
+    n, ncc, sd = 64, 4, 2
+    kappa = _problem(n, 1e-6)
+    monkeypatch.setenv("TMG_ACC_PLANES", "1")
+    out = []
+    for s, rows in ((1, "0"), (slabs, "1")):
+        monkeypatch.setenv("TMG_ACC_ROWS", rows)
+        c = Context(GridSpec(n, n, n), ncc, sd, slabs=s)
+        c.set_conductivity(kappa, PATCH)
+        c.setup("mmg", MmgOptions(fine_blocks="coarse_cell"))
+        r = np.random.default_rng(8).standard_normal(n ** 3)
+        b = c.assemble_rhs(np.ones(n ** 3))
+        out.append((c.apply_preconditioner(r), c.pcg(b, rtol=1e-8, max_iterations=3000)))
+    (za, ra), (zb, rb) = out
+    assert np.linalg.norm(za - zb) <= 1e-9 * np.linalg.norm(za)
+    assert abs(ra.report.iterations - rb.report.iterations) <= 1
+    assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
