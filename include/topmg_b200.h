@@ -186,7 +186,8 @@ int tmg_set_design_frozen(tmg_ctx* ctx, double vstar, uint64_t seed, int passes,
  * ceil(vf M) largest -> 1 (ties by lower index, rng.cpp:39-51). The cell
  * centres are the context's own, so a slab context whose domain is the bottom
  * of dom (e.g. 1024 x 1024 x 128 cells of extent 1 x 1 x 0.125 in the unit
- * cube) gets the bottom slab of the tree. */
+ * cube) gets the bottom slab of the tree; with global_n the design is the
+ * global one's slab exactly (its threshold is the whole domain's). */
 typedef struct {
   double vf;
   uint64_t seed;
@@ -200,6 +201,10 @@ typedef struct {
   double spread;   /* child direction = normalize(parent + spread * (u - 1/2)^3) */
   double amp;      /* noise amplitude */
   double dom[3];   /* extents of the whole domain the tree lives in (0: own) */
+  int64_t global_n[3]; /* nonzero: generate the whole design on global_n cells over
+                          dom (field, filter and top-k threshold of the global
+                          problem) and keep z-layers [z0, z0 + nz) */
+  int64_t z0;
 } tmg_tree_gen;
 
 int tmg_set_design_tree(tmg_ctx* ctx, const tmg_tree_gen* gen, double kappa_lo, double kappa_hi,

@@ -1357,28 +1357,33 @@ int set_design_common(tmg_ctx* c, double lo, double hi, int p, const tmg_patch* 
   return TMG_OK;
 }
 
-// generate (x-fastest, whole grid) with `gen`, distribute to the slabs, kappa
+// generate (x-fastest, whole grid) with `gen`, distribute to the slabs, kappa.
+// m_gen > 0: `gen` fills a larger field of m_gen cells of which the context's
+// grid is the part from cell `offset` (a bottom slab of a bigger domain).
 int generate_design(tmg_ctx* c, double lo, double hi, int p, double* rho_out,
-                    const std::function<void(double* rho, double* f, void* scratch)>& gen) {
+                    const std::function<void(double* rho, double* f, void* scratch)>& gen,
+                    int64_t m_gen = 0, int64_t offset = 0) {
   const int rc = guard(c, [&] {
     CK(cudaSetDevice(c->device));
     const tmg_grid& G = c->grid;
-    const int64_t m = G.nx * G.ny * G.nz;  // the whole design (every rank generates it)
+    const int64_t m_own = G.nx * G.ny * G.nz;  // the whole design (every rank generates it)
+    const int64_t m = m_gen > 0 ? m_gen : m_own;
     double* rho = dalloc<double>(c, m);
     double* f = dalloc<double>(c, m);
     double* scratch = dalloc<double>(c, (int64_t)(gen_scratch_bytes(m) / sizeof(double)) + 1);
     gen(rho, f, scratch);
     CK(cudaGetLastError());
+    rho += offset;
     for (Slab& s : c->slabs) {
       launch_to_brick(s.g, c->cb, rho + s.xoff, s.r, c->stream);
       launch_conductivity(s.g, c->cb, s.r, s.kappa, lo, hi, p, c->stream);
       CK(cudaGetLastError());
     }
     if (rho_out)
-      CK(cudaMemcpyAsync(rho_out, rho, sizeof(double) * (size_t)m, cudaMemcpyDeviceToHost,
+      CK(cudaMemcpyAsync(rho_out, rho, sizeof(double) * (size_t)m_own, cudaMemcpyDeviceToHost,
                          c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    dfree(c, rho);
+    dfree(c, rho - offset);
     dfree(c, f);
     dfree(c, scratch);
   });
@@ -1422,17 +1427,36 @@ int tmg_set_design_tree(tmg_ctx* c, const tmg_tree_gen* t, double lo, double hi,
   const tmg_grid& G = c->grid;
   const double dx = t->dom[0] > 0 ? t->dom[0] : G.lx, dy = t->dom[1] > 0 ? t->dom[1] : G.ly,
                dz = t->dom[2] > 0 ? t->dom[2] : G.lz;
+  // whole-domain generation (global_n): the field, its filter and its top-k
+  // threshold are those of the global design; the context keeps its slab
+  int64_t gn[3] = {G.nx, G.ny, G.nz}, offset = 0;
+  double ex[3] = {G.lx, G.ly, G.lz};
+  if (t->global_n[0] > 0) {
+    if (t->global_n[0] != G.nx || t->global_n[1] != G.ny || t->z0 < 0 ||
+        t->z0 + G.nz > t->global_n[2] || !(t->dom[0] > 0 && t->dom[1] > 0 && t->dom[2] > 0))
+      return set_err(c, TMG_ECONFIG,
+                     "tree generator: the context must be the z-slab [z0, z0 + nz) of the "
+                     "global_n grid over dom");
+    for (int a = 0; a < 3; ++a) {
+      gn[a] = t->global_n[a];
+      ex[a] = t->dom[a];
+    }
+    offset = t->z0 * G.nx * G.ny;
+  }
   const std::vector<double> seg = tree_segments(*t, dx, dy, dz);
   const int nseg = (int)(seg.size() / 7);
-  return generate_design(c, lo, hi, p, rho_out, [&](double* rho, double* f, void* scratch) {
-    double* dseg = dalloc<double>(c, (int64_t)seg.size());
-    CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(double) * seg.size(), cudaMemcpyHostToDevice,
-                       c->stream));
-    launch_tree_design(G.nx, G.ny, G.nz, G.lx, G.ly, G.lz, t->vf, t->seed, t->passes, t->radius,
-                       dseg, nseg, t->amp, rho, f, scratch, c->stream);
-    CK(cudaStreamSynchronize(c->stream));  // seg host vector outlives the copy
-    dfree(c, dseg);
-  });
+  return generate_design(
+      c, lo, hi, p, rho_out,
+      [&](double* rho, double* f, void* scratch) {
+        double* dseg = dalloc<double>(c, (int64_t)seg.size());
+        CK(cudaMemcpyAsync(dseg, seg.data(), sizeof(double) * seg.size(), cudaMemcpyHostToDevice,
+                           c->stream));
+        launch_tree_design(gn[0], gn[1], gn[2], ex[0], ex[1], ex[2], t->vf, t->seed, t->passes,
+                           t->radius, dseg, nseg, t->amp, rho, f, scratch, c->stream);
+        CK(cudaStreamSynchronize(c->stream));  // seg host vector outlives the copy
+        dfree(c, dseg);
+      },
+      t->global_n[0] > 0 ? gn[0] * gn[1] * gn[2] : 0, offset);
 }
 
 int tmg_set_design(tmg_ctx* c, const double* rho, double lo, double hi, int p,

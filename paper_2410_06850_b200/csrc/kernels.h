@@ -58,11 +58,30 @@ inline int device_sm_count() {
   return sms;
 }
 
+// Raise `kernel`'s dynamic shared-memory limit on the current device to at
+// least `smem` (the attribute is per device and per function; it is never
+// lowered, so launches of the same kernel with different sizes all stay
+// valid).
+template <typename K>
+inline void ensure_dyn_smem(K kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limit;
+  if (smem <= 48 * 1024) return;
+  int dev = 0;
+  launch_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = limit[std::make_pair(dev, (const void*)kernel)];
+  if (smem <= cur) return;
+  launch_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "cudaFuncSetAttribute");
+  cur = smem;
+}
+
 // Resident CTAs per SM of `kernel` with `smem` dynamic bytes on the current
-// device, after raising its dynamic shared-memory limit there (the attribute
-// is per device). Cached per (device, kernel, threads, smem).
+// device (after ensure_dyn_smem). Cached per (device, kernel, threads, smem).
 template <typename K>
 inline int device_occupancy(K kernel, int threads, size_t smem) {
+  ensure_dyn_smem(kernel, smem);
   static std::mutex mu;
   static std::map<std::pair<std::pair<int, const void*>, std::pair<int, size_t>>, int> cache;
   int dev = 0;
@@ -72,9 +91,6 @@ inline int device_occupancy(K kernel, int threads, size_t smem) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (smem > 48 * 1024)
-    launch_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                 "cudaFuncSetAttribute");
   int per = 0;
   launch_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem),
                "cudaOccupancyMaxActiveBlocksPerMultiprocessor");

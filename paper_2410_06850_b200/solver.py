@@ -85,7 +85,8 @@ class _TreeGen(C.Structure):
     _fields_ = [("vf", C.c_double), ("seed", C.c_uint64), ("passes", C.c_int),
                 ("radius", C.c_int), ("depth", C.c_int), ("length0", C.c_double),
                 ("lshrink", C.c_double), ("width0", C.c_double), ("wshrink", C.c_double),
-                ("spread", C.c_double), ("amp", C.c_double), ("dom", C.c_double * 3)]
+                ("spread", C.c_double), ("amp", C.c_double), ("dom", C.c_double * 3),
+                ("global_n", C.c_int64 * 3), ("z0", C.c_int64)]
 
 
 class _OptimOpts(C.Structure):
@@ -371,17 +372,20 @@ class Context:
         return rho
 
     def set_design_tree(self, vf, kappa_lo, kappa_hi=1.0, p=3, boundary: BoundarySpec = None,
-                        seed=20240501, passes=1, radius=6, dom=None, return_rho=False, **tree):
+                        seed=20240501, passes=1, radius=6, dom=None, return_rho=False,
+                        global_n=None, z0=0, **tree):
         """BASELINE configs[4]'s tree-like design generated on the device
         (tmg_set_design_tree; bit-identical to inputs.tree_design), then as
         set_design. dom: extents of the whole domain the tree lives in
-        (default: the context's own)."""
+        (default: the context's own); global_n: generate the whole design on
+        that grid over dom and keep this context's z-slab from layer z0."""
         from .inputs import TREE_DEFAULTS
         t = dict(TREE_DEFAULTS)
         t.update(tree)
         g = _TreeGen(vf, seed, passes, radius, t["depth"], t["length0"], t["lshrink"],
                      t["width0"], t["wshrink"], t["spread"], t["amp"],
-                     (C.c_double * 3)(*(dom or (0.0, 0.0, 0.0))))
+                     (C.c_double * 3)(*(dom or (0.0, 0.0, 0.0))),
+                     (C.c_int64 * 3)(*(global_n or (0, 0, 0))), z0)
         parr, n = boundary._c()
         rho = np.empty(self.grid.num_cells()) if return_rho else None
         self._check(native().tmg_set_design_tree(

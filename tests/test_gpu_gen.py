@@ -91,3 +91,14 @@ def test_frozen_bench_design_bitwise_vs_reference(n, vstar, passes, seed):
     rho = c.set_design_frozen(vstar, 1e-3, boundary=BC, seed=seed, passes=passes,
                               return_rho=True)
     np.testing.assert_array_equal(rho, ref)
+
+
+def test_tree_design_global_slab():
+    """global_n: a slab context gets exactly its layers of the global design
+    (the configs[4] proxy's design: the whole-domain threshold)."""
+    n, nz, z0 = 64, 16, 16
+    glob = inputs.tree_design(n, 0.15, radius=3).reshape(n, n, n)
+    c = Context(GridSpec(n, n, nz, 1.0, 1.0, nz / n), (4, 4, 1), 2)
+    rho = c.set_design_tree(0.15, 1e-6, boundary=BC, radius=3, dom=(1.0, 1.0, 1.0),
+                            global_n=(n, n, n), z0=z0, return_rho=True)
+    np.testing.assert_array_equal(rho.reshape(nz, n, n), glob[z0:z0 + nz])

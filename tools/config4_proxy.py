@@ -2,8 +2,9 @@
 
 BASELINE configs[4] is 1024^3 cells on 8 B200 in z-slabs of 1024 x 1024 x 128.
 This runs one such slab on one GPU as a standalone problem: the bottom slab
-of the tree design (tmg_set_design_tree with the tree in the unit cube,
-dom = (1, 1, 1)), cells of the global size (extent 1 x 1 x 0.125), the
+of the global 1024^3 tree design (tmg_set_design_tree generates the whole
+design on the device, global_n = 1024^3, and keeps the slab), cells of the
+global size (extent 1 x 1 x 0.125), the
 Dirichlet patch of the global problem on its z = 0 face, Neumann on top
 (where the distributed run has the next slab's ghost layer). It measures
 what one GPU of the 8-GPU run holds and moves: device memory, set-up time,
@@ -36,8 +37,10 @@ lz = nz / n
 c = Context(GridSpec(n, n, nz, 1.0, 1.0, lz), ncc, sd)
 bc = BoundarySpec.bottom_center_patch(1, 1, 0.2, 0)
 t0 = time.perf_counter()
+# the global 1024^3 design (its filter and volume-fraction threshold), of
+# which this context keeps the bottom slab
 c.set_design_tree(cfg["vf"], cfg["kmin"], 1.0, 3, bc, passes=cfg["passes"], radius=cfg["radius"],
-                  dom=(1.0, 1.0, 1.0))
+                  dom=(1.0, 1.0, 1.0), global_n=(n, n, n), z0=0)
 t_gen = time.perf_counter() - t0
 b = c.assemble_rhs(np.ones(n * n * nz))
 opts = MmgOptions(num_cc_basis=cfg["lcc"], fine_blocks="coarse_cell")
