@@ -164,6 +164,7 @@ struct tmg_ctx {
   double* accP = nullptr;   // single slab, plane-Thomas A_cc solve: tiles + couplings + work
   bool acc_planes = false;
   bool acc_rows = false;  // partitioned: row blocks of the plane inverses per slab
+  unsigned int* ready = nullptr;  // single slab, fused restriction: per-brick counters
   AccPlanesRef planes{};
   double* symvP = nullptr;  // single slab: GEMV partials
   double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
@@ -327,6 +328,7 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.tc);
   }
   dfree_null(c, c->AccT);
+  dfree_null(c, c->ready);
   dfree_null(c, c->accP);
   c->acc_planes = false;
   c->acc_rows = false;
@@ -545,9 +547,14 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
   const GridParams& g = s.g;
   cudaStream_t st = c->stream;
-  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
-                      s.history, init, st));
-  KL(1, restrict_fine(c, s, st));
+  if (c->ready) {  // restriction fused into the update (TMG_FUSE_RESTRICT)
+    KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
+                        s.history, init, st, c->ready, s.phif, s.rc));
+  } else {
+    KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
+                        s.history, init, st));
+    KL(1, restrict_fine(c, s, st));
+  }
   enqueue_coarse_single(c);
   KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
                     st));
@@ -933,8 +940,8 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   } else if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
     Slab& s = s0;
     const GridParams& g = s.g;
-    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
-    timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
+    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream, c->ready, s.phif, s.rc)); });
+    if (!c->ready) timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
     timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
@@ -984,8 +991,8 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
       if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
-        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
-        timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
+        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream, c->ready, s.phif, s.rc)); });
+        if (!c->ready) timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
         timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
@@ -2282,6 +2289,11 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     c->kind = kind;
     c->fine_bj = fine_bj ? 1 : 0;
     c->nu = hier ? o->smoother_sweeps : 1;
+    if (hier && !fine_bj && c->nu == 1 && !c->dist() && fused_restrict_enabled()) {
+      c->ready = dalloc<unsigned int>(c, c->g.nb);
+      CK(cudaMemsetAsync(c->ready, 0, sizeof(unsigned int) * (size_t)c->g.nb, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
     c->have_setup = true;
     build_graph(c, 4);
   });

@@ -293,9 +293,13 @@ void launch_brick_solve(const GridParams& g, int cb, const double* coef, const d
 void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
                        double* out, const double* rdot, PcgState* st, double* partials, int init,
                        cudaStream_t s);
+// ready / phif / rc (single slab, TMG_FUSE_RESTRICT): K3 fused into the update
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
-                   double* partials, double* history, int init, cudaStream_t s);
+                   double* partials, double* history, int init, cudaStream_t s,
+                   unsigned int* ready = nullptr, const double* phif = nullptr,
+                   double* rc = nullptr);
+bool fused_restrict_enabled();
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s);

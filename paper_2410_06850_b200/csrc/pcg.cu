@@ -163,6 +163,45 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
 }
 
 // ------------------------------------------------- K2 update + pre-smooth
+#ifndef TMG_FUSE_RESTRICT
+#define TMG_FUSE_RESTRICT 0
+#endif
+
+// rc_I of brick bc in the boundary form of K3 (see k_restrict_bnd) by the
+// NT threads of the calling CTA; r1f is read through L2 (written by other
+// CTAs of the same kernel when called from k_update).
+template <int CB, int NT>
+__device__ __forceinline__ void restrict_bnd_brick(const GridParams& g, const BrickCoord& bc,
+                                                   const double* __restrict__ coef, int64_t M,
+                                                   const double* __restrict__ phif,
+                                                   const double* r1f, double* rc, double* red) {
+  constexpr int C = CB * CB * CB, F = CB * CB, NS = 6 * F;
+  constexpr int KS = (NS + NT - 1) / NT;
+  const int t = threadIdx.x;
+  const size_t ob = bofs(bc.b, C);
+  double v[LCP] = {};
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int h = t + k * NT;
+    if (h >= NS) break;
+    int f, ti, nl;
+    halo_slot<CB>(h, f, ti, nl);
+    const int nb = nbr_brick(g, bc, f);
+    if (nb < 0) continue;
+    const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
+    const bool hi = f & 1;
+    const int e = hi ? CB - 1 : 0;
+    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+    const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
+    const double val = tf * __ldcg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);
+#pragma unroll
+    for (int a = 0; a < LCP; ++a)
+      v[a] = fma(__ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q), val, v[a]);
+  }
+  block_sum_k<NT, LCP>(v, red);
+  if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
+}
+
 template <int CB>
 struct UpdateSmem {
   double slots[kSlots][Thomas<CB>::PLANE];
@@ -171,17 +210,25 @@ struct UpdateSmem {
   double tz[CB * CB * CB];
   double red[80];
   int flag;
+  int todo[8], ntodo;
 };
 
 // CTA size Thomas<CB>::NT (288 at CB = 8: one thread per mat-vec block row);
 // brick cells are strided over the threads.
+// With `ready` (single-slab solves, TMG_FUSE_RESTRICT) the restriction K3 is
+// done here too: each CTA, once its r1 face layers are stored, counts itself
+// in at its own brick and its 6 neighbours; the CTA that completes a brick's
+// count (itself + all its neighbours done) computes that brick's rc and
+// re-arms the counter. No CTA waits on another.
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, const double* __restrict__ coef,
                                                              int64_t M, const double* __restrict__ Gf,
                                                              double* x, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* r,
                                                              double* r1, double* r1f, PcgState* st,
-                                                             double* partials, double* history, int init) {
+                                                             double* partials, double* history, int init,
+                                                             unsigned int* ready, const double* phif,
+                                                             double* rc) {
   pdl_trigger();
   constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -228,6 +275,31 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
     if (grid_reduce_last_k<1>(v, partials, &st->ticket[2], tot, &sm.flag, sm.red) && t == 0) {
       if (g.dist) st->loc[kRedUpdate] = tot[0];
       else finish_rr(st, tot[0], history);  // :554-560
+    }
+  }
+  if (ready) {  // fused K3 (see above)
+    __syncthreads();  // every thread's r1f stores are issued
+    if (t == 0) {
+      __threadfence();  // ... and visible device-wide before the counts
+      const BrickCoord bc = brick_coord(g, b);
+      int n = 0;
+      for (int f = -1; f < 6; ++f) {
+        const int nb = f < 0 ? b : nbr_brick(g, bc, f);
+        if (nb < 0) continue;
+        const BrickCoord nc = brick_coord(g, nb);
+        unsigned need = 1;
+        for (int h = 0; h < 6; ++h) need += nbr_brick(g, nc, h) >= 0;
+        if (atomicAdd(&ready[nb], 1u) + 1u == need) sm.todo[n++] = nb;
+      }
+      __threadfence();
+      sm.ntodo = n;
+    }
+    __syncthreads();
+    for (int i = 0; i < sm.ntodo; ++i) {
+      const int nb = sm.todo[i];
+      restrict_bnd_brick<CB, NT>(g, brick_coord(g, nb), coef, M, phif, r1f, rc, sm.red);
+      if (t == 0) ready[nb] = 0u;  // re-armed for the next V-cycle
+      __syncthreads();
     }
   }
 }
@@ -697,11 +769,13 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
-                   double* partials, double* history, int init, cudaStream_t s) {
+                   double* partials, double* history, int init, cudaStream_t s,
+                   unsigned int* ready, const double* phif, double* rc) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
-  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
+  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init, ready, phif, rc);
+  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init, ready, phif, rc);
 }
+bool fused_restrict_enabled() { return TMG_FUSE_RESTRICT && TMG_RESTRICT_BND; }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {

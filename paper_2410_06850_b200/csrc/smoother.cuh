@@ -80,6 +80,11 @@ constexpr int kSlots = TMG_SLOTS;  // TMA ring depth (planes in flight per CTA)
 #ifndef TMG_G_HINTS
 #define TMG_G_HINTS 1
 #endif
+// Forward-sweep planes requested into L2 ahead of the TMA ring (bulk L2
+// prefetch: bytes in flight that hold no shared memory). 0 = off.
+#ifndef TMG_L2_AHEAD
+#define TMG_L2_AHEAD 0
+#endif
 
 // Plane load n of a solve: forward loads of planes the backward sweep re-reads
 // ask L2 to keep them (evict_last); the last forward plane and the backward
@@ -206,6 +211,11 @@ __device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double
       plane_load(sm.slots[n], G + (size_t)Thomas<CB>::plane_of(n) * Thomas<CB>::PLANE,
                  Thomas<CB>::PLANE * sizeof(double), &sm.bars[n], n, CB);
     }
+#if TMG_L2_AHEAD > 0
+#pragma unroll
+    for (int n = NPRE; n < NPRE + TMG_L2_AHEAD && n < CB; ++n)
+      prefetch_l2(G + (size_t)n * Thomas<CB>::PLANE, Thomas<CB>::PLANE * sizeof(double));
+#endif
   }
 }
 
@@ -252,6 +262,11 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
       mbar_arrive_expect_tx(&sm.bars[slot], Thomas<CB>::PLANE * sizeof(double));
       plane_load(sm.slots[slot], G + (size_t)Thomas<CB>::plane_of(n + kSlots) * Thomas<CB>::PLANE,
                  Thomas<CB>::PLANE * sizeof(double), &sm.bars[slot], n + kSlots, CB);
+#if TMG_L2_AHEAD > 0
+      if (n + kSlots + TMG_L2_AHEAD < CB)
+        prefetch_l2(G + (size_t)(n + kSlots + TMG_L2_AHEAD) * Thomas<CB>::PLANE,
+                    Thomas<CB>::PLANE * sizeof(double));
+#endif
     }
     if (tid < P) {
       double pr[NBK];
