@@ -94,13 +94,18 @@ def box_filter_design(n, vf: float, seed: int = 20240501, passes: int = 3,
 # fraction 0.15)". The reference has no such generator; this
 # one is documented in DESIGN.md §6 and run on the device by
 # tmg_set_design_tree (csrc/gen.cu), bit-identical to tree_design below.
-TREE_DEFAULTS = dict(depth=8, length0=0.28, lshrink=0.78, width0=0.10, wshrink=0.80, spread=1.8,
+# The capsules' support (profile > 0) covers ~24% of the domain, above the
+# 15% volume fraction, so the threshold keeps one connected tree: with a
+# thinner tree (5% support) the remaining solid came from filtered noise,
+# thousands of floating islands at 1024^3 / radius 6, and the reference's own
+# MMG needed > 2000 iterations.
+TREE_DEFAULTS = dict(depth=9, length0=0.28, lshrink=0.78, width0=0.22, wshrink=0.85, spread=1.8,
                      amp=0.05)
 _MASK64 = (1 << 64) - 1
 
 
-def tree_segments(seed: int = 20240501, depth=8, length0=0.28, lshrink=0.78, width0=0.10,
-                  wshrink=0.80, spread=1.8, dom=(1.0, 1.0, 1.0)) -> np.ndarray:
+def tree_segments(seed: int = 20240501, depth=9, length0=0.28, lshrink=0.78, width0=0.22,
+                  wshrink=0.85, spread=1.8, dom=(1.0, 1.0, 1.0)) -> np.ndarray:
     """Breadth-first binary tree of capsule segments rooted at the centre of
     the z = 0 face (the Dirichlet patch), heading +z; each child direction
     is normalize(parent + spread * (u - 1/2, u - 1/2, u - 1/2)) with u from
