@@ -30,8 +30,19 @@
 
 #include "../../include/topmg_b200.h"
 #include "kernels.h"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace tmg;
+
+// NVTX ranges (SURVEY.md §5 tracing): every ABI entry point that launches
+// work and every set-up phase shows up as a named range in Nsight Systems /
+// Compute timelines. Header-only NVTX v3; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 thread_local std::string g_create_error;
@@ -1949,6 +1960,7 @@ int tmg_assemble_rhs(tmg_ctx* c, const double* source, double* rhs_out) {
 }
 
 int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
+  NvtxRange nvtx("tmg_setup");
   if (!c || !o) return set_err(c, TMG_EARG, "tmg_setup: null argument");
   if (!c->have_problem) return set_err(c, TMG_EARG, "tmg_setup: no problem set");
   const int kind = o->kind;
@@ -2080,6 +2092,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       int nph = 0;
       const char* phname[12];
       auto mark = [&](const char* name) {
+        nvtxMarkA(name);  // NVTX: set-up phase `name` enqueued
         if (!sprof) return;
         CK(cudaEventCreate(&ph[nph]));
         CK(cudaEventRecord(ph[nph], c->stream));
@@ -2316,6 +2329,7 @@ int tmg_upload_x0(tmg_ctx* c, const double* x0) {
 }
 
 int tmg_solve_resident(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* rep) {
+  NvtxRange nvtx("tmg_solve_resident");
   if (!c) return set_err(c, TMG_EARG, "null context");
   if (maxit < 0) return set_err(c, TMG_EARG, "pcg: negative max_iterations");
   return guard(c, [&] {
@@ -2326,6 +2340,7 @@ int tmg_solve_resident(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_repor
 
 int tmg_solve_resident_ex(tmg_ctx* c, double rtol, int maxit, int use_x0, int flags,
                           tmg_report* rep) {
+  NvtxRange nvtx("tmg_solve_resident");
   if (!c) return set_err(c, TMG_EARG, "null context");
   if (maxit < 0) return set_err(c, TMG_EARG, "pcg: negative max_iterations");
   tmg_report local{};
@@ -2402,6 +2417,7 @@ int tmg_download_solution(tmg_ctx* c, double* x) {
 
 int tmg_pcg(tmg_ctx* c, const double* b, const double* x0, double rtol, int maxit, double* x_out,
             double* history, tmg_report* rep) {
+  NvtxRange nvtx("tmg_pcg");
   if (!c || !b || !x_out) return set_err(c, TMG_EARG, "pcg: null argument");
   if (maxit < 0) return set_err(c, TMG_EARG, "pcg: negative max_iterations");
   tmg_report local{};

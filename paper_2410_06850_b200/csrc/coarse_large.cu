@@ -422,7 +422,13 @@ bool coarse_large_supported(int q, int lcc) {
   return q > 64 && q % GB == 0 && q <= 4096 && lcc <= 20;
 }
 
-static int subspace_width(int lcc) { return lcc <= 12 ? 16 : 24; }
+// TMG_CC_KS=16/24 overrides (diagnostics)
+static int subspace_width(int lcc) {
+  const char* e = getenv("TMG_CC_KS");
+  if (e && atoi(e) == 24) return 24;
+  if (e && atoi(e) == 16 && lcc <= 12) return 16;
+  return lcc <= 12 ? 16 : 24;
+}
 
 static bool subspace_in_smem(int q, int ks) { return q <= 256 && 3 * q * ks * 8 <= 160 * 1024; }
 
@@ -475,6 +481,8 @@ void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* 
                            int* scratch_status, int* iters, double tol, int maxit,
                            cudaStream_t s) {
   const int q = g.sd * g.sd * g.sd * LC;
+  if (const char* e = getenv("TMG_CC_TOL")) tol = atof(e);  // diagnostics
+  if (const char* e = getenv("TMG_CC_MAXIT")) maxit = atoi(e);
   double* Hs = scratch + g.e0 * q * q;
   k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, Bc, 1e-5, Hs);
   invert_elements(Hs, q, g.neo, work, scratch_status, s);
