@@ -68,7 +68,7 @@ typedef struct {
   int64_t num_local_basis; /* L_c  (reference default 4) */
   int64_t num_cc_basis;    /* L_cc (reference default 8) */
   int smoother_sweeps;     /* nu   (reference default 1) */
-  double eig_tol;      /* residual tolerance relative to ||B||, 0 -> 1e-11 */
+  double eig_tol;      /* residual tolerance relative to ||B||, 0 -> 1e-9 */
   int eig_degree;      /* Chebyshev filter degree, 0 -> 32 */
   int eig_max_outer;   /* filter/Rayleigh-Ritz rounds, 0 -> 60 */
   int warm_start;      /* 1: start the local eigensolver from the previous set-up's

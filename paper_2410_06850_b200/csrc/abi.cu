@@ -111,6 +111,7 @@ struct Slab {
   // problem (virtual global pointers)
   double* kappa = nullptr;
   double* coef = nullptr;  // 4 x mst operator coefficients (Tx+, Ty+, Tz+, diag)
+  double* tf = nullptr;    // face-major T of the owned bricks' 6 faces (k_face_t)
   uint8_t* dmask = nullptr;
   // preconditioner
   double* dinv = nullptr;
@@ -175,7 +176,6 @@ struct tmg_ctx {
   double* accP = nullptr;   // single slab, plane-Thomas A_cc solve: tiles + couplings + work
   bool acc_planes = false;
   bool acc_rows = false;  // partitioned: row blocks of the plane inverses per slab
-  unsigned int* ready = nullptr;  // single slab, fused restriction: per-brick counters
   AccPlanesRef planes{};
   double* symvP = nullptr;  // single slab: GEMV partials
   double* Ainv = nullptr;   // partitioned: dense A_cc^-1 (row blocks per slab)
@@ -339,7 +339,6 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.tc);
   }
   dfree_null(c, c->AccT);
-  dfree_null(c, c->ready);
   dfree_null(c, c->accP);
   c->acc_planes = false;
   c->acc_rows = false;
@@ -516,6 +515,11 @@ int finish_problem(tmg_ctx* c) {
       CK(cudaGetLastError());
     }
     exchange_coef(c);
+    for (Slab& s : c->slabs) {  // face-major T (after the ghost coefficients)
+      if (!s.tf) s.tf = owned<double>(c, s, 6 * c->cb * c->cb);
+      launch_face_t(s.g, c->cb, s.coef, s.tf, c->stream);
+      CK(cudaGetLastError());
+    }
     c->have_problem = true;
     free_setup(c);
   });
@@ -547,7 +551,7 @@ void enqueue_coarse_single(tmg_ctx* c) {
 // (k_restrict_bnd) unless TMG_RESTRICT_BND=0 at build time
 static void restrict_fine(tmg_ctx* c, Slab& s, cudaStream_t st) {
 #if TMG_RESTRICT_BND
-  launch_restrict_bnd(s.g, c->cb, s.coef, s.phif, s.r1f, s.rc, s.st, st);
+  launch_restrict_bnd(s.g, c->cb, s.tf, s.phif, s.r1f, s.rc, s.st, st);
 #else
   launch_restrict(s.g, c->cb, s.coef, s.phi, s.r, s.r1, s.rc, s.st, st);
 #endif
@@ -558,16 +562,11 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
   const GridParams& g = s.g;
   cudaStream_t st = c->stream;
-  if (c->ready) {  // restriction fused into the update (TMG_FUSE_RESTRICT)
-    KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
-                        s.history, init, st, c->ready, s.phif, s.rc));
-  } else {
-    KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
-                        s.history, init, st));
-    KL(1, restrict_fine(c, s, st));
-  }
+  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
+                      s.history, init, st));
+  KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
-  KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
+  KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
 
@@ -643,7 +642,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
+    KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
                       init, st));
   reduce_finalize(c, kRedPost, init);
   XCH(z, sizeof(double) * C, false);
@@ -951,10 +950,10 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   } else if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
     Slab& s = s0;
     const GridParams& g = s.g;
-    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream, c->ready, s.phif, s.rc)); });
-    if (!c->ready) timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
+    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
+    timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
-    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
+    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
@@ -1002,10 +1001,10 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
       if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
-        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream, c->ready, s.phif, s.rc)); });
-        if (!c->ready) timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
+        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
+        timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
-        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
+        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_precond(c, 0, par); });
       }
@@ -2099,7 +2098,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         phname[nph++] = name;
       };
       mark("alloc");
-      const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-11;
+      const double tol = o->eig_tol > 0 ? o->eig_tol : 1e-9;  // residual / ||B|| (DESIGN.md §4 set-up)
       const int degree = o->eig_degree > 0 ? o->eig_degree : 32;
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
       for (size_t k = 0; k < c->slabs.size(); ++k) {
@@ -2137,7 +2136,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         else if (q <= 64) launch_cc_basis(s.g, s.Ac, s.Bc, s.Rcc, s.cc_evals, c->stream);
         else  // Winv's storage holds the shifted inverses until the smoother overwrites it
           launch_cc_basis_large(s.g, s.Ac, s.Bc, s.Winv, large_work, s.Rcc, s.cc_evals,
-                                s.d_status + 3, cc_iters, 1e-12, 100, c->stream);
+                                s.d_status + 3, cc_iters, 1e-10, 100, c->stream);
       }
       if (cc_iters) {
         int it = 0;
@@ -2302,11 +2301,6 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     c->kind = kind;
     c->fine_bj = fine_bj ? 1 : 0;
     c->nu = hier ? o->smoother_sweeps : 1;
-    if (hier && !fine_bj && c->nu == 1 && !c->dist() && fused_restrict_enabled()) {
-      c->ready = dalloc<unsigned int>(c, c->g.nb);
-      CK(cudaMemsetAsync(c->ready, 0, sizeof(unsigned int) * (size_t)c->g.nb, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-    }
     c->have_setup = true;
     build_graph(c, 4);
   });

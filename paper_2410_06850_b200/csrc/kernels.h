@@ -279,6 +279,8 @@ void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 void init_kernel_attributes();
 void launch_coefficients(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                          double* coef, cudaStream_t s);
+// face-major T of every owned brick's 6 CB^2 face slots (k_face_t)
+void launch_face_t(const GridParams& g, int cb, const double* coef, double* tf, cudaStream_t s);
 void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
                  int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s);
 void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
@@ -293,22 +295,20 @@ void launch_brick_solve(const GridParams& g, int cb, const double* coef, const d
 void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
                        double* out, const double* rdot, PcgState* st, double* partials, int init,
                        cudaStream_t s);
-// ready / phif / rc (single slab, TMG_FUSE_RESTRICT): K3 fused into the update
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
-                   double* partials, double* history, int init, cudaStream_t s,
-                   unsigned int* ready = nullptr, const double* phif = nullptr,
-                   double* rc = nullptr);
-bool fused_restrict_enabled();
+                   double* partials, double* history, int init, cudaStream_t s);
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s);
 // boundary form of launch_restrict, valid when the fine blocks are the bricks
-void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
+// tf: the face-major T of launch_face_t
+void launch_restrict_bnd(const GridParams& g, int cb, const double* tf, const double* phif,
                          const double* r1f, double* rc, const PcgState* st, cudaStream_t s);
-void launch_post(const GridParams& g, int cb, const double* coef, const double* phi, const double* phif,
-                 const double* Gf, const double* r, const double* r1, const double* r1f, const double* ec, double* z,
-                 PcgState* st, double* partials, int init, cudaStream_t s);
+void launch_post(const GridParams& g, int cb, const double* coef, const double* tf, const double* phi,
+                 const double* phif, const double* Gf, const double* r, const double* r1,
+                 const double* r1f, const double* ec, double* z, PcgState* st, double* partials,
+                 int init, cudaStream_t s);
 // face-major copy of Phi on each stored brick's 6 face layers:
 // phif[((b * 6 + f) * L_c + a) * CB^2 + q], q the in-face index of halo_slot
 void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* phif, int64_t b0,

@@ -71,6 +71,32 @@ void launch_finalize(const FinArgs& a, int which, int init, cudaStream_t s) {
   launch_pdl(k_finalize, dim3(1), dim3(32), 0, s, a, which, init);
 }
 
+// Face-major T of every brick face slot (set-up): tf[b][f][q] = T of the face
+// between face cell q of face f and the neighbour brick's cell, 0 on the
+// domain boundary. The boundary-form kernels read these 6 CB^2 values
+// coalesced instead of gathering one coefficient per 32-byte sector from the
+// x faces (stride CB) and from the neighbours' coefficient arrays.
+template <int CB>
+__global__ void k_face_t(GridParams g, const double* __restrict__ coef, int64_t M, double* tf) {
+  constexpr int C = CB * CB * CB, F = CB * CB;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  const size_t ob = bofs(bc.b, C);
+  for (int h = threadIdx.x; h < 6 * F; h += blockDim.x) {
+    int f, ti, nl;
+    halo_slot<CB>(h, f, ti, nl);
+    const int nb = nbr_brick(g, bc, f);
+    double v = 0.0;
+    if (nb >= 0) {
+      const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
+      const bool hi = f & 1;
+      const int e = hi ? CB - 1 : 0;
+      const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
+      v = coef[(size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl)];
+    }
+    tf[(size_t)bc.b * 6 * F + h] = v;
+  }
+}
+
 // ------------------------------------------------------------------ K0 init
 template <int CB>
 __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const double* __restrict__ coef,
@@ -163,45 +189,6 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
 }
 
 // ------------------------------------------------- K2 update + pre-smooth
-#ifndef TMG_FUSE_RESTRICT
-#define TMG_FUSE_RESTRICT 0
-#endif
-
-// rc_I of brick bc in the boundary form of K3 (see k_restrict_bnd) by the
-// NT threads of the calling CTA; r1f is read through L2 (written by other
-// CTAs of the same kernel when called from k_update).
-template <int CB, int NT>
-__device__ __forceinline__ void restrict_bnd_brick(const GridParams& g, const BrickCoord& bc,
-                                                   const double* __restrict__ coef, int64_t M,
-                                                   const double* __restrict__ phif,
-                                                   const double* r1f, double* rc, double* red) {
-  constexpr int C = CB * CB * CB, F = CB * CB, NS = 6 * F;
-  constexpr int KS = (NS + NT - 1) / NT;
-  const int t = threadIdx.x;
-  const size_t ob = bofs(bc.b, C);
-  double v[LCP] = {};
-#pragma unroll
-  for (int k = 0; k < KS; ++k) {
-    const int h = t + k * NT;
-    if (h >= NS) break;
-    int f, ti, nl;
-    halo_slot<CB>(h, f, ti, nl);
-    const int nb = nbr_brick(g, bc, f);
-    if (nb < 0) continue;
-    const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
-    const bool hi = f & 1;
-    const int e = hi ? CB - 1 : 0;
-    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
-    const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
-    const double val = tf * __ldcg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);
-#pragma unroll
-    for (int a = 0; a < LCP; ++a)
-      v[a] = fma(__ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q), val, v[a]);
-  }
-  block_sum_k<NT, LCP>(v, red);
-  if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
-}
-
 template <int CB>
 struct UpdateSmem {
   double slots[kSlots][Thomas<CB>::PLANE];
@@ -210,25 +197,17 @@ struct UpdateSmem {
   double tz[CB * CB * CB];
   double red[80];
   int flag;
-  int todo[8], ntodo;
 };
 
 // CTA size Thomas<CB>::NT (288 at CB = 8: one thread per mat-vec block row);
 // brick cells are strided over the threads.
-// With `ready` (single-slab solves, TMG_FUSE_RESTRICT) the restriction K3 is
-// done here too: each CTA, once its r1 face layers are stored, counts itself
-// in at its own brick and its 6 neighbours; the CTA that completes a brick's
-// count (itself + all its neighbours done) computes that brick's rc and
-// re-arms the counter. No CTA waits on another.
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, const double* __restrict__ coef,
                                                              int64_t M, const double* __restrict__ Gf,
                                                              double* x, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* r,
                                                              double* r1, double* r1f, PcgState* st,
-                                                             double* partials, double* history, int init,
-                                                             unsigned int* ready, const double* phif,
-                                                             double* rc) {
+                                                             double* partials, double* history, int init) {
   pdl_trigger();
   constexpr int C = CB * CB * CB, P = CB * CB, NT = Thomas<CB>::NT;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -275,31 +254,6 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
     if (grid_reduce_last_k<1>(v, partials, &st->ticket[2], tot, &sm.flag, sm.red) && t == 0) {
       if (g.dist) st->loc[kRedUpdate] = tot[0];
       else finish_rr(st, tot[0], history);  // :554-560
-    }
-  }
-  if (ready) {  // fused K3 (see above)
-    __syncthreads();  // every thread's r1f stores are issued
-    if (t == 0) {
-      __threadfence();  // ... and visible device-wide before the counts
-      const BrickCoord bc = brick_coord(g, b);
-      int n = 0;
-      for (int f = -1; f < 6; ++f) {
-        const int nb = f < 0 ? b : nbr_brick(g, bc, f);
-        if (nb < 0) continue;
-        const BrickCoord nc = brick_coord(g, nb);
-        unsigned need = 1;
-        for (int h = 0; h < 6; ++h) need += nbr_brick(g, nc, h) >= 0;
-        if (atomicAdd(&ready[nb], 1u) + 1u == need) sm.todo[n++] = nb;
-      }
-      __threadfence();
-      sm.ntodo = n;
-    }
-    __syncthreads();
-    for (int i = 0; i < sm.ntodo; ++i) {
-      const int nb = sm.todo[i];
-      restrict_bnd_brick<CB, NT>(g, brick_coord(g, nb), coef, M, phif, r1f, rc, sm.red);
-      if (t == 0) ready[nb] = 0u;  // re-armed for the next V-cycle
-      __syncthreads();
     }
   }
 }
@@ -354,7 +308,7 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
 // for cc-element fine blocks, which keep k_restrict.
 template <int CB>
 __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
-    GridParams g, const double* __restrict__ coef, int64_t M, const double* __restrict__ phif,
+    GridParams g, const double* __restrict__ tfa, int64_t M, const double* __restrict__ phif,
     const double* __restrict__ r1f, double* rc, const PcgState* st) {
   pdl_trigger();
   pdl_wait();
@@ -379,8 +333,8 @@ __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_
     const bool hi = f & 1;
     const int e = hi ? CB - 1 : 0;
     const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
-    // T of the face: the +axis coefficient of the lower cell of the pair
-    const double tf = __ldg(coef + (size_t)ax * M + (hi ? ob + c : bofs(nb, C) + nl));
+    // T of the face (face-major copy, k_face_t)
+    const double tf = __ldg(tfa + (size_t)bc.b * 6 * F + h);
     const double val = tf * __ldg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);  // r1 on the neighbour's face
 #pragma unroll
     for (int a = 0; a < LCP; ++a)  // own face f (face-major phif)
@@ -409,6 +363,7 @@ struct PostSmem {
 
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const double* __restrict__ coef,
+                                                           const double* __restrict__ /*tfa*/,
                                                            int64_t M, const double* __restrict__ phi,
                                                            const double* __restrict__ Gf,
                                                            const double* __restrict__ r,
@@ -509,6 +464,7 @@ struct PostBSmem {
 
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, const double* __restrict__ coef,
+                                                               const double* __restrict__ tfa,
                                                                int64_t M, const double* __restrict__ phif,
                                                                const double* __restrict__ Gf,
                                                                const double* __restrict__ r,
@@ -557,7 +513,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
 #pragma unroll
         for (int a = 0; a < LCP; ++a)  // the neighbour's face f^1 (face-major phif)
           r2 += __ldg(phif + (((size_t)nb * 6 + (f ^ 1)) * LCP + a) * F + q) * __ldg(ec + (size_t)nb * LCP + a);
-        val[k] = __ldg(coef + (size_t)ax * M + (hi ? ob + c : onb + nl)) * r2;
+        val[k] = __ldg(tfa + (size_t)bc.b * 6 * F + h) * r2;  // face-major T (k_face_t)
         axis[k] = ax;
         cell[k] = c;
       }
@@ -754,6 +710,11 @@ void launch_brick_solve(const GridParams& g, int cb, const double* coef, const d
     launch_pdl(k_brick_solve<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g,
                coef, M, Gf, in, add, out, rdot, st, partials, init);
 }
+void launch_face_t(const GridParams& g, int cb, const double* coef, double* tf, cudaStream_t s) {
+  const int64_t M = g.mst;
+  if (cb == 8) k_face_t<8><<<(unsigned)g.nbo, 384, 0, s>>>(g, coef, M, tf);
+  else k_face_t<4><<<(unsigned)g.nbo, 96, 0, s>>>(g, coef, M, tf);
+}
 void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
                  int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s) {
   const int64_t M = g.mst;
@@ -769,13 +730,11 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
-                   double* partials, double* history, int init, cudaStream_t s,
-                   unsigned int* ready, const double* phif, double* rc) {
+                   double* partials, double* history, int init, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init, ready, phif, rc);
-  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init, ready, phif, rc);
+  if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
+  else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
 }
-bool fused_restrict_enabled() { return TMG_FUSE_RESTRICT && TMG_RESTRICT_BND; }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
@@ -783,11 +742,11 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
   if (cb == 8) launch_pdl(k_restrict<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
   else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
 }
-void launch_restrict_bnd(const GridParams& g, int cb, const double* coef, const double* phif,
+void launch_restrict_bnd(const GridParams& g, int cb, const double* tf, const double* phif,
                          const double* r1f, double* rc, const PcgState* st, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phif, r1f, rc, st);
-  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, coef, M, phif, r1f, rc, st);
+  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, tf, M, phif, r1f, rc, st);
+  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, tf, M, phif, r1f, rc, st);
 }
 
 // Face-major copy of Phi for the boundary-form kernels: their Phi reads are
@@ -809,15 +768,15 @@ void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* ph
   if (cb == 8) k_phi_faces<8><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
   else k_phi_faces<4><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
 }
-void launch_post(const GridParams& g, int cb, const double* coef, const double* phi_full,
-                 const double* phif, const double* Gf, const double* r, const double* r1_full,
-                 const double* r1f, const double* ec, double* z, PcgState* st, double* partials,
-                 int init, cudaStream_t s) {
+void launch_post(const GridParams& g, int cb, const double* coef, const double* tf,
+                 const double* phi_full, const double* phif, const double* Gf, const double* r,
+                 const double* r1_full, const double* r1f, const double* ec, double* z, PcgState* st,
+                 double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
   const double* phi = TMG_POST_BND ? phif : phi_full;
   const double* r1 = TMG_POST_BND ? r1f : r1_full;
-  if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
-  else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
