@@ -1991,8 +1991,8 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     const int64_t cells = (int64_t)c->cb * c->cb * c->cb;
     if (o->num_local_basis > cells)
       return set_err(c, TMG_EARG, "local_spectral_basis: more eigenvectors than cells requested");
-    if (o->num_local_basis != compiled_lc())
-      return set_err(c, TMG_ENOTSUP, "GPU path is compiled for L_c = %d (got %lld)", compiled_lc(),
+    if (o->num_local_basis < 1 || o->num_local_basis > max_lc())
+      return set_err(c, TMG_ENOTSUP, "GPU path handles L_c = 1..%d (got %lld)", max_lc(),
                      (long long)o->num_local_basis);
     const int64_t q = (int64_t)c->g.sd * c->g.sd * c->g.sd * o->num_local_basis;
     if (kind == TMG_PRECOND_TWO_GRID && q > 256)

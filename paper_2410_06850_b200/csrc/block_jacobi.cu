@@ -174,12 +174,12 @@ __global__ void __launch_bounds__(CB * CB * CB) k_prolong_add(GridParams g,
   pdl_trigger();
   pdl_wait();
   if (st->done) return;
-  constexpr int C = CB * CB * CB, LCB = 4;
+  constexpr int C = CB * CB * CB;
+  const int lc = g.lc;
   const int64_t b = blockIdx.x + g.b0;
   const size_t s = (size_t)b * C + threadIdx.x;
   double v = r1[s];
-#pragma unroll
-  for (int a = 0; a < LCB; ++a) v = fma(phi[((size_t)b * LCB + a) * C + threadIdx.x], ec[b * LCB + a], v);
+  for (int a = 0; a < lc; ++a) v = fma(phi[((size_t)b * lc + a) * C + threadIdx.x], ec[b * lc + a], v);
   r2[s] = v;
 }
 

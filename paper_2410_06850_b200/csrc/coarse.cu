@@ -11,6 +11,8 @@
 // per element (cyclic Jacobi, one warp) and its L_cc lowest eigenvectors are
 // the rows of R_cc. A_cc = R_cc A_c R_cc^T is again block 7-point at the cc
 // level and is assembled densely for the direct solve.
+#include <type_traits>
+
 #include "kernels.h"
 #include "stencil.cuh"
 #include "symv.cuh"
@@ -20,7 +22,7 @@ namespace tmg {
 
 // ------------------------------------------------------------ A_c blocks
 
-template <int CB>
+template <int CB, int LM>
 __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
                                                                const double* __restrict__ kappa,
                                                                const uint8_t* __restrict__ dmask,
@@ -28,17 +30,17 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
                                                                double* Ac, double* Bc) {
   constexpr int C = CB * CB * CB, NW = C / 32;
   __shared__ StencilSmem<CB> ss;
-  __shared__ double ph[LC][C];
-  __shared__ double red[LC * LC * NW + LC * LC + 8];
+  constexpr int K2 = LM * LM;  // LM = L_c (template: exact register arrays)
+  __shared__ double red[K2 * NW + K2 + 8];
+  constexpr int lc = LM;
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   load_tile<CB, true>(kappa, ss.kt, g, bc);
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
-  double f[LC];
+  double f[LM];
 #pragma unroll
-  for (int a = 0; a < LC; ++a) {
-    f[a] = phi[((size_t)bc.b * LC + a) * C + t];
-    ph[a][t] = f[a];
-  }
+  for (int a = 0; a < LM; ++a) f[a] = a < lc ? phi[((size_t)bc.b * lc + a) * C + t] : 0.0;
+  // Phi at an in-brick neighbour j (read through L1; set-up only)
+  auto ph = [&](int a, int j) { return a < lc ? __ldg(phi + ((size_t)bc.b * lc + a) * C + j) : 0.0; };
   __syncthreads();
   tile_faces<CB>(ss.kt, ss.fx, ss.fy, ss.fz, g, bc);
   __syncthreads();
@@ -46,25 +48,25 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
   const FaceSet fs = cell_faces<CB>(ss.fx, ss.fy, ss.fz, ss.kt[Tile<CB>::idx(li, lj, lk)], li, lj, lk, g, bc, dm);
   // --- self block: sum_l d_l f_a f_b - sum_{+x,+y,+z in brick} T (f_a(l) f_b(j) + f_a(j) f_b(l))
   {
-    double v[LC * LC];
+    double v[K2];  // v[a * LM + b]; entries a, b >= lc stay 0
     const int st[3] = {1, CB, CB * CB};
     const int co[3] = {li, lj, lk};
 #pragma unroll
-    for (int a = 0; a < LC; ++a)
+    for (int a = 0; a < LM; ++a)
 #pragma unroll
-      for (int b = 0; b < LC; ++b) v[a * LC + b] = fs.diag * f[a] * f[b];
+      for (int b = 0; b < LM; ++b) v[a * LM + b] = fs.diag * f[a] * f[b];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
       if (co[ax] + 1 >= CB) continue;
       const int j = t + st[ax];
       const double T = fs.t[2 * ax + 1];
 #pragma unroll
-      for (int a = 0; a < LC; ++a)
+      for (int a = 0; a < LM; ++a)
 #pragma unroll
-        for (int b = 0; b < LC; ++b) v[a * LC + b] -= T * (f[a] * ph[b][j] + ph[a][j] * f[b]);
+        for (int b = 0; b < LM; ++b) v[a * LM + b] -= T * (f[a] * ph(b, j) + ph(a, j) * f[b]);
     }
-    block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Ac[((size_t)bc.b * 7 + 0) * LC * LC + t] = v[t];
+    block_sum_k<C, K2>(v, red);
+    if (t < lc * lc) Ac[((size_t)bc.b * 7 + 0) * lc * lc + t] = v[(t / lc) * LM + t % lc];
   }
   // --- face blocks: -T_lj f_a(l) phi_J,b(j) over the CB^2 face pairs
   int nbr[6];
@@ -72,9 +74,9 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
   for (int f6 = 0; f6 < 6; ++f6) nbr[f6] = nbr_brick(g, bc, f6);
   const int co[3] = {li, lj, lk};
   for (int fc = 0; fc < 6; ++fc) {
-    double v[LC * LC];
+    double v[K2];
 #pragma unroll
-    for (int e = 0; e < LC * LC; ++e) v[e] = 0.0;
+    for (int e = 0; e < K2; ++e) v[e] = 0.0;
     const int ax = fc >> 1;
     const bool on_face = (fc & 1) ? co[ax] == CB - 1 : co[ax] == 0;
     if (nbr[fc] >= 0 && on_face) {
@@ -84,14 +86,14 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
       const int lj2 = nc3[0] + CB * (nc3[1] + CB * nc3[2]);
       const double T = fs.t[fc];
 #pragma unroll
-      for (int b = 0; b < LC; ++b) {
-        const double pj = phi[((size_t)nbr[fc] * LC + b) * C + lj2];
+      for (int b = 0; b < LM; ++b) {
+        const double pj = b < lc ? phi[((size_t)nbr[fc] * lc + b) * C + lj2] : 0.0;
 #pragma unroll
-        for (int a = 0; a < LC; ++a) v[a * LC + b] = -T * f[a] * pj;
+        for (int a = 0; a < LM; ++a) v[a * LM + b] = -T * f[a] * pj;
       }
     }
-    block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Ac[((size_t)bc.b * 7 + 1 + fc) * LC * LC + t] = v[t];
+    block_sum_k<C, K2>(v, red);
+    if (t < lc * lc) Ac[((size_t)bc.b * 7 + 1 + fc) * lc * lc + t] = v[(t / lc) * LM + t % lc];
   }
   // --- cc-boundary correction: faces leaving the cc element + Dirichlet terms
   {
@@ -110,13 +112,13 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
         e += fs.t[fc];
       }
     }
-    double v[LC * LC];
+    double v[K2];
 #pragma unroll
-    for (int a = 0; a < LC; ++a)
+    for (int a = 0; a < LM; ++a)
 #pragma unroll
-      for (int b = 0; b < LC; ++b) v[a * LC + b] = e * f[a] * f[b];
-    block_sum_k<C, LC * LC>(v, red);
-    if (t < LC * LC) Bc[(size_t)bc.b * LC * LC + t] = v[t];
+      for (int b = 0; b < LM; ++b) v[a * LM + b] = e * f[a] * f[b];
+    block_sum_k<C, K2>(v, red);
+    if (t < lc * lc) Bc[(size_t)bc.b * lc * lc + t] = v[(t / lc) * LM + t % lc];
   }
 }
 
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_coarse_blocks(GridParams g,
 __global__ void k_cc_basis(GridParams g, const double* __restrict__ Ac,
                            const double* __restrict__ Bc, double* Rcc, double* cc_evals) {
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   double* M = sm;
   double* V = M + q * q;
   const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
@@ -200,7 +202,7 @@ __device__ bool smem_gj_inverse(double* M, int n, double* col, double* rowp, dou
 __global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, double* Winv,
                                   int* status) {
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   double* M = sm;
   double* col = M + q * q;
   double* rowp = col + q;
@@ -220,7 +222,7 @@ __global__ void k_coarse_smoother(GridParams g, const double* __restrict__ Ac, d
 __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
                                const double* __restrict__ Rcc, double* Acc, int64_t ldacc,
                                double* C, int planar) {
-  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
+  const int q = g.sd * g.sd * g.sd * g.lc, nch = g.sd * g.sd * g.sd;
   const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   const int fdir = blockIdx.y;  // 0 self, 1..6 faces
   int64_t F = ec.e;
@@ -248,11 +250,11 @@ __global__ void k_acc_assemble(GridParams g, const double* __restrict__ Ac,
         if (J < 0) continue;
         const int cj = child_index(g, fc, J);
         if (cj < 0) continue;
-        const double* blk = Ac + (I * 7 + dir) * LC * LC;
-        for (int a = 0; a < LC; ++a) {
+        const double* blk = Ac + (I * 7 + dir) * g.lc * g.lc;
+        for (int a = 0; a < g.lc; ++a) {
           double s = 0.0;
-          for (int b = 0; b < LC; ++b) s += blk[a * LC + b] * RF[cj * LC + b];
-          acc += RE[ci * LC + a] * s;
+          for (int b = 0; b < g.lc; ++b) s += blk[a * g.lc + b] * RF[cj * g.lc + b];
+          acc += RE[ci * g.lc + a] * s;
         }
       }
     }
@@ -278,11 +280,11 @@ struct ElemDofs {
 __device__ __forceinline__ ElemDofs elem_dof(const GridParams& g, int e, int i) {
   const int ncx = (int)g.ncx, ncy = (int)g.ncy, sd = g.sd;
   const int ei = e % ncx, ej = (e / ncx) % ncy, ek = e / (ncx * ncy);
-  const int ci = i / LC;
+  const int ci = i / g.lc;
   const int di = ci % sd, dj = (ci / sd) % sd, dk = ci / (sd * sd);
   ElemDofs d;
   d.brick = (ei * sd + di) + (int)g.nbx * ((ej * sd + dj) + (int)g.nby * (ek * sd + dk));
-  d.a = i % LC;
+  d.a = i % g.lc;
   return d;
 }
 
@@ -298,10 +300,15 @@ __device__ __forceinline__ double coarse_apply_row(const GridParams& g, const do
 #pragma unroll
   for (int dir = 0; dir < 7; ++dir) {
     if (nb[dir] < 0) continue;
-    const double* blk = Ac + ((size_t)I * 7 + dir) * LC * LC + a * LC;
-    const double* xv = x + (size_t)nb[dir] * LC;
+    const int lc = g.lc;
+    const double* blk = Ac + ((size_t)I * 7 + dir) * lc * lc + a * lc;
+    const double* xv = x + (size_t)nb[dir] * lc;
+    if (lc == 4) {  // the default L_c, unrolled
 #pragma unroll
-    for (int b = 0; b < LC; ++b) s = fma(blk[b], xv[b], s);
+      for (int b = 0; b < 4; ++b) s = fma(blk[b], xv[b], s);
+    } else {
+      for (int b = 0; b < lc; ++b) s = fma(blk[b], xv[b], s);
+    }
   }
   return s;
 }
@@ -320,10 +327,15 @@ __device__ __forceinline__ double coarse_apply_row_cg(const GridParams& g,
 #pragma unroll
   for (int dir = 0; dir < 7; ++dir) {
     if (nb[dir] < 0) continue;
-    const double* blk = Ac + ((size_t)I * 7 + dir) * LC * LC + a * LC;
-    const double* xv = x + (size_t)nb[dir] * LC;
+    const int lc = g.lc;
+    const double* blk = Ac + ((size_t)I * 7 + dir) * lc * lc + a * lc;
+    const double* xv = x + (size_t)nb[dir] * lc;
+    if (lc == 4) {  // the default L_c, unrolled
 #pragma unroll
-    for (int b = 0; b < LC; ++b) s = fma(blk[b], __ldcg(xv + b), s);
+      for (int b = 0; b < 4; ++b) s = fma(blk[b], __ldcg(xv + b), s);
+    } else {
+      for (int b = 0; b < lc; ++b) s = fma(blk[b], __ldcg(xv + b), s);
+    }
   }
   return s;
 }
@@ -337,11 +349,11 @@ __global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
   pdl_wait();
   if (*done) return;
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
+  const int q = g.sd * g.sd * g.sd * g.lc, e = (int)(blockIdx.x + g.e0);
   double* xin = sm;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
-    xin[i] = in[(size_t)d.brick * LC + d.a];
+    xin[i] = in[(size_t)d.brick * g.lc + d.a];
   }
   __syncthreads();
   const double* W = Winv + (size_t)e * q * q;
@@ -354,7 +366,7 @@ __global__ void k_coarse_smooth(GridParams g, const int* __restrict__ done,
     }
     if (j < q) s0 = fma(W[(size_t)j * q + i], xin[j], s0);
     const ElemDofs d = elem_dof(g, e, i);
-    const size_t gi = (size_t)d.brick * LC + d.a;
+    const size_t gi = (size_t)d.brick * g.lc + d.a;
     out[gi] = (add ? add[gi] : 0.0) + (s0 + s1);
   }
 }
@@ -369,11 +381,11 @@ __global__ void k_coarse_restrict(GridParams g, const int* __restrict__ done,
   pdl_wait();
   if (*done) return;
   extern __shared__ double sm[];
-  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
+  const int q = g.sd * g.sd * g.sd * g.lc, e = (int)(blockIdx.x + g.e0);
   double* wc = sm;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
-    wc[i] = rc[(size_t)d.brick * LC + d.a] - coarse_apply_row(g, Ac, rc0, d.brick, d.a);
+    wc[i] = rc[(size_t)d.brick * g.lc + d.a] - coarse_apply_row(g, Ac, rc0, d.brick, d.a);
   }
   __syncthreads();
   for (int b = threadIdx.x; b < g.lcc; b += blockDim.x) {
@@ -391,13 +403,13 @@ __global__ void k_coarse_prolong(GridParams g, const int* __restrict__ done,
   pdl_trigger();
   pdl_wait();
   if (*done) return;
-  const int q = g.sd * g.sd * g.sd * LC, e = (int)(blockIdx.x + g.e0);
+  const int q = g.sd * g.sd * g.sd * g.lc, e = (int)(blockIdx.x + g.e0);
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     const ElemDofs d = elem_dof(g, e, i);
     double s = 0.0;
     for (int b = 0; b < g.lcc; ++b)
       s = fma(Rcc[((size_t)e * g.lcc + b) * q + i], ecc[(size_t)e * g.lcc + b], s);
-    const size_t gi = (size_t)d.brick * LC + d.a;
+    const size_t gi = (size_t)d.brick * g.lc + d.a;
     rc1[gi] = rc0[gi] + s;
   }
 }
@@ -409,9 +421,9 @@ __global__ void k_coarse_resid(GridParams g, const int* __restrict__ done,
   pdl_trigger();
   pdl_wait();
   if (*done) return;
-  const int64_t k = g.b0 * LC + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= g.b0 * LC + n) return;
-  out[k] = rc[k] - coarse_apply_row(g, Ac, x, k / LC, k % LC);
+  const int64_t k = g.b0 * g.lc + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= g.b0 * g.lc + n) return;
+  out[k] = rc[k] - coarse_apply_row(g, Ac, x, k / g.lc, k % g.lc);
 }
 
 // ---------------------------------------- fused coarse level (one kernel)
@@ -455,6 +467,8 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+constexpr int kFusedLc = 4;  // the fused coarse kernel is built for L_c = 4 (q = 32)
+
 template <int Q, int LCC>
 __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int* __restrict__ done,
                                                         const double* __restrict__ Ac,
@@ -484,7 +498,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int
   // 1: rc0 = W rc
   for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
     const ElemDofs d = elem_dof(g, (int)e, lane);
-    const size_t gi = (size_t)d.brick * LC + d.a;
+    const size_t gi = (size_t)d.brick * kFusedLc + d.a;
     const double* W = Winv + (size_t)e * Q * Q;
     double wcol[Q];
 #pragma unroll
@@ -505,7 +519,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int
     double rr[LCC];
 #pragma unroll
     for (int b = 0; b < LCC; ++b) rr[b] = Rcc[((size_t)e * LCC + b) * Q + lane];
-    const double wc = rc[(size_t)d.brick * LC + d.a] - coarse_apply_row_cg(g, Ac, rc0, d.brick, d.a);
+    const double wc = rc[(size_t)d.brick * kFusedLc + d.a] - coarse_apply_row_cg(g, Ac, rc0, d.brick, d.a);
 #pragma unroll
     for (int b = 0; b < LCC; ++b) {
       const double v = warp_sum(rr[b] * wc);
@@ -520,7 +534,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int
   const int64_t nt = (n + TS - 1) / TS;
   for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
     const ElemDofs d = elem_dof(g, (int)e, lane);
-    const size_t gi = (size_t)d.brick * LC + d.a;
+    const size_t gi = (size_t)d.brick * kFusedLc + d.a;
     double rr[LCC], pv[LCC][2];
 #pragma unroll
     for (int b = 0; b < LCC; ++b) {
@@ -543,7 +557,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int
   // 5: ec = rc1 + W (rc - A_c rc1)
   for (int64_t e = g.e0 + w0; e < e_end; e += nw) {
     const ElemDofs d = elem_dof(g, (int)e, lane);
-    const size_t gi = (size_t)d.brick * LC + d.a;
+    const size_t gi = (size_t)d.brick * kFusedLc + d.a;
     const double* W = Winv + (size_t)e * Q * Q;
     double wcol[Q];
 #pragma unroll
@@ -561,7 +575,7 @@ __global__ void __launch_bounds__(256, 2) k_coarse_fused(GridParams g, const int
 
 // true when launch_coarse_fused handles the hierarchy (q = 32, L_cc = 8, n_cc <= 4096)
 bool coarse_fused_supported(const GridParams& g, int64_t n_cc) {
-  return g.sd * g.sd * g.sd * LC == 32 && g.lcc == 8 && n_cc <= 64 * TS;
+  return g.lc == kFusedLc && g.sd * g.sd * g.sd * g.lc == 32 && g.lcc == 8 && n_cc <= 64 * TS;
 }
 
 // ------------------------------------------------------------- launchers
@@ -592,15 +606,26 @@ void launch_coarse_fused(const GridParams& g, const int* done, const double* Ac,
 
 void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                           const double* phi, double* Ac, double* Bc, cudaStream_t s) {
-  if (cb == 8)
-    k_coarse_blocks<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
-  else
-    k_coarse_blocks<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+  auto go = [&](auto L) {
+    constexpr int LM = decltype(L)::value;
+    if (cb == 8)
+      k_coarse_blocks<8, LM><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+    else
+      k_coarse_blocks<4, LM><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, phi, Ac, Bc);
+  };
+  switch (g.lc) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    case 5: go(std::integral_constant<int, 5>{}); break;
+    default: go(std::integral_constant<int, 6>{}); break;
+  }
 }
 
 void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, double* Rcc,
                      double* cc_evals, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   const size_t smem = sizeof(double) * (size_t)(2 * q * q + q + 8);
   cudaFuncSetAttribute(k_cc_basis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cc_basis<<<(unsigned)g.neo, 64, smem, s>>>(g, Ac, Bc, Rcc, cc_evals);
@@ -609,7 +634,7 @@ void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, do
 // two_grid: R_cc = I (build_two_grid, solver.cpp:401-420), lcc = q: row
 // (E, k) of R_cc is the unit vector of the element's k-th coarse dof.
 __global__ void k_cc_identity(GridParams g, double* Rcc, double* cc_evals) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   const int64_t e = blockIdx.x + g.e0;
   for (int i = threadIdx.x; i < q * q; i += blockDim.x)
     Rcc[e * q * q + i] = (i / q == i % q) ? 1.0 : 0.0;
@@ -622,7 +647,7 @@ void launch_cc_identity(const GridParams& g, double* Rcc, double* cc_evals, cuda
 
 void launch_coarse_smoother(const GridParams& g, const double* Ac, double* Winv, int* status,
                             cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   const size_t smem = sizeof(double) * (size_t)(q * q + 3 * q + 8);
   cudaFuncSetAttribute(k_coarse_smoother, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_coarse_smoother<<<(unsigned)g.neo, 256, smem, s>>>(g, Ac, Winv, status);
@@ -661,9 +686,9 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
                          double* symv_partials, int64_t n_cc, const double* rc, double* rc0,
                          double* rcc, double* ecc, double* rc1, double* tc, double* ec,
                          const AccPlanesRef* planes, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   const int nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
-  const int nc = (int)(g.nbo * LC);
+  const int nc = (int)(g.nbo * g.lc);
   const size_t sm = sizeof(double) * (size_t)q;
   const double* nul = nullptr;
   launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sm, s, g, done, Winv, rc, nul, rc0);
@@ -684,29 +709,29 @@ void launch_coarse_cycle(const GridParams& g, const int* done, const double* Ac,
 // and the A_cc row-block GEMV go between them).
 void launch_coarse_smooth(const GridParams& g, const int* done, const double* Winv,
                           const double* in, const double* add, double* out, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
+  const int q = g.sd * g.sd * g.sd * g.lc, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_smooth, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
              done, Winv, in, add, out);
 }
 void launch_coarse_restrict(const GridParams& g, const int* done, const double* Ac,
                             const double* Rcc, const double* rc, const double* rc0, double* rcc,
                             cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
+  const int q = g.sd * g.sd * g.sd * g.lc, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_restrict, dim3((unsigned)g.neo), dim3(nt), sizeof(double) * (size_t)q, s, g,
              done, Ac, Rcc, rc, rc0, rcc);
 }
 void launch_coarse_prolong(const GridParams& g, const int* done, const double* Rcc,
                            const double* rc0, const double* ecc, double* rc1, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
+  const int q = g.sd * g.sd * g.sd * g.lc, nt = (q < 256 ? (q + 31) / 32 * 32 : 256);
   launch_pdl(k_coarse_prolong, dim3((unsigned)g.neo), dim3(nt), 0, s, g, done, Rcc, rc0, ecc, rc1);
 }
 void launch_coarse_resid(const GridParams& g, const int* done, const double* Ac, const double* rc,
                          const double* x, double* out, cudaStream_t s) {
-  const int nc = (int)(g.nbo * LC);
+  const int nc = (int)(g.nbo * g.lc);
   launch_pdl(k_coarse_resid, dim3((unsigned)((nc + 255) / 256)), dim3(256), 0, s, g, done, Ac, rc,
              x, out, nc);
 }
 
-int compiled_lc() { return LC; }
+int max_lc() { return kMaxLcCoarse; }
 
 }  // namespace tmg

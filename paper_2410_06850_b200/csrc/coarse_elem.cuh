@@ -6,7 +6,10 @@
 
 namespace tmg {
 
-constexpr int LC = 4;  // compiled L_c (BASELINE "4 local eigenvectors per coarse cell")
+// L_c (basis vectors per coarse cell) is the runtime g.lc throughout the
+// coarse level; kMaxLcCoarse bounds the register / shared arrays of
+// k_coarse_blocks.
+constexpr int kMaxLcCoarse = 6;
 
 // ----------------------------------------------------- per-element helpers
 
@@ -41,16 +44,16 @@ __device__ __forceinline__ int child_index(const GridParams& g, const ElemCoord&
   return (int)(di + g.sd * (dj + g.sd * dk));
 }
 
-// Element matrix (q x q, q = sd^3 * LC) into smem: A_c restricted to E's
+// Element matrix (q x q, q = sd^3 * g.lc) into smem: A_c restricted to E's
 // children, optionally minus Bc on diagonal blocks. Symmetrised.
 __device__ inline void build_elem_matrix(const GridParams& g, const ElemCoord& ec, const double* Ac,
                                   const double* Bc, bool subtract_bc, double* M, int q) {
   const int nch = g.sd * g.sd * g.sd;
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) M[e] = 0.0;
   __syncthreads();
-  for (int e = threadIdx.x; e < nch * 7 * LC * LC; e += blockDim.x) {
-    const int ci = e / (7 * LC * LC), rem = e % (7 * LC * LC);
-    const int dir = rem / (LC * LC), ab = rem % (LC * LC), a = ab / LC, b = ab % LC;
+  for (int e = threadIdx.x; e < nch * 7 * g.lc * g.lc; e += blockDim.x) {
+    const int ci = e / (7 * g.lc * g.lc), rem = e % (7 * g.lc * g.lc);
+    const int dir = rem / (g.lc * g.lc), ab = rem % (g.lc * g.lc), a = ab / g.lc, b = ab % g.lc;
     const int64_t I = child_brick(g, ec, ci);
     int cj;
     if (dir == 0) cj = ci;
@@ -59,9 +62,9 @@ __device__ inline void build_elem_matrix(const GridParams& g, const ElemCoord& e
       cj = J >= 0 ? child_index(g, ec, J) : -1;
     }
     if (cj < 0) continue;
-    double v = Ac[(I * 7 + dir) * LC * LC + ab];
-    if (dir == 0 && subtract_bc) v -= Bc[I * LC * LC + ab];
-    M[(ci * LC + a) * q + cj * LC + b] = v;
+    double v = Ac[(I * 7 + dir) * g.lc * g.lc + ab];
+    if (dir == 0 && subtract_bc) v -= Bc[I * g.lc * g.lc + ab];
+    M[(ci * g.lc + a) * q + cj * g.lc + b] = v;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {

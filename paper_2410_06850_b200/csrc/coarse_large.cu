@@ -32,14 +32,14 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 __global__ void k_elem_matrix(GridParams g, const double* __restrict__ Ac,
                               const double* __restrict__ Bc, double shift_rel, double* out) {
   __shared__ double red[32];
-  const int q = g.sd * g.sd * g.sd * LC, nch = g.sd * g.sd * g.sd;
+  const int q = g.sd * g.sd * g.sd * g.lc, nch = g.sd * g.sd * g.sd;
   const ElemCoord ec = elem_coord(g, blockIdx.x + g.e0);
   double* M = out + (int64_t)blockIdx.x * q * q;
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) M[e] = 0.0;
   __syncthreads();
-  for (int e = threadIdx.x; e < nch * 7 * LC * LC; e += blockDim.x) {
-    const int ci = e / (7 * LC * LC), rem = e % (7 * LC * LC);
-    const int dir = rem / (LC * LC), ab = rem % (LC * LC), a = ab / LC, b = ab % LC;
+  for (int e = threadIdx.x; e < nch * 7 * g.lc * g.lc; e += blockDim.x) {
+    const int ci = e / (7 * g.lc * g.lc), rem = e % (7 * g.lc * g.lc);
+    const int dir = rem / (g.lc * g.lc), ab = rem % (g.lc * g.lc), a = ab / g.lc, b = ab % g.lc;
     const int64_t I = child_brick(g, ec, ci);
     int cj;
     if (dir == 0) cj = ci;
@@ -48,9 +48,9 @@ __global__ void k_elem_matrix(GridParams g, const double* __restrict__ Ac,
       cj = J >= 0 ? child_index(g, ec, J) : -1;
     }
     if (cj < 0) continue;
-    double v = Ac[(I * 7 + dir) * LC * LC + ab];
-    if (dir == 0 && Bc) v -= Bc[I * LC * LC + ab];
-    M[(ci * LC + a) * q + cj * LC + b] += v;
+    double v = Ac[(I * 7 + dir) * g.lc * g.lc + ab];
+    if (dir == 0 && Bc) v -= Bc[I * g.lc * g.lc + ab];
+    M[(ci * g.lc + a) * q + cj * g.lc + b] += v;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
@@ -253,7 +253,7 @@ template <int KS>
 __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const double* Ac,
                                 const double* Bc, const double* X, double* Z, int q) {
   for (int r = threadIdx.x; r < q; r += blockDim.x) {
-    const int ci = r / LC, a = r % LC;
+    const int ci = r / g.lc, a = r % g.lc;
     const int64_t I = child_brick(g, ec, ci);
     double z[KS];
 #pragma unroll
@@ -266,10 +266,10 @@ __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const 
       }
       if (cj < 0) continue;
 #pragma unroll
-      for (int b = 0; b < LC; ++b) {
-        double h = Ac[(I * 7 + dir) * LC * LC + a * LC + b];
-        if (dir == 0) h -= Bc[I * LC * LC + a * LC + b];
-        const double* xr = X + (cj * LC + b) * KS;
+      for (int b = 0; b < g.lc; ++b) {
+        double h = Ac[(I * 7 + dir) * g.lc * g.lc + a * g.lc + b];
+        if (dir == 0) h -= Bc[I * g.lc * g.lc + a * g.lc + b];
+        const double* xr = X + (cj * g.lc + b) * KS;
 #pragma unroll
         for (int k = 0; k < KS; ++k) z[k] = fma(h, xr[k], z[k]);
       }
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
                                                      int maxit, double* Rcc, double* cc_evals,
                                                      int* iters, double* gscr) {
   extern __shared__ __align__(16) double sms[];
-  const int q = g.sd * g.sd * g.sd * LC, t = threadIdx.x, nt = blockDim.x;
+  const int q = g.sd * g.sd * g.sd * g.lc, t = threadIdx.x, nt = blockDim.x;
   double* T = sms;
   double* V = T + KS * KS;
   double* F = V + KS * KS;
@@ -307,9 +307,9 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
   const double* H = Hs + (int64_t)blockIdx.x * q * q;
   double hd = 0.0;
   for (int r = t; r < q; r += nt) {
-    const int64_t I = child_brick(g, ec, r / LC);
-    const int a = r % LC;
-    hd = fmax(hd, Ac[I * 7 * LC * LC + a * (LC + 1)] - Bc[I * LC * LC + a * (LC + 1)]);
+    const int64_t I = child_brick(g, ec, r / g.lc);
+    const int a = r % g.lc;
+    hd = fmax(hd, Ac[I * 7 * g.lc * g.lc + a * (g.lc + 1)] - Bc[I * g.lc * g.lc + a * (g.lc + 1)]);
   }
   const double thr = tol * block_max(hd, red);
   // start: the constant vector and hashed columns
@@ -456,7 +456,7 @@ static void invert_elements(double* A, int q, int64_t neo, double* work, int* st
 // Winv of every owned cc element (coarse_blocks_by_cc smoother) for large q.
 void launch_coarse_smoother_large(const GridParams& g, const double* Ac, double* Winv,
                                   double* work, int* status, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   k_elem_matrix<<<(unsigned)g.neo, 256, 0, s>>>(g, Ac, nullptr, 0.0, Winv + g.e0 * q * q);
   invert_elements(Winv + g.e0 * q * q, q, g.neo, work, status, s);
 }
@@ -465,7 +465,7 @@ template <int KS>
 static void launch_subspace(const GridParams& g, const double* Ac, const double* Bc,
                             const double* Hs, double tol, int maxit, double* Rcc, double* cc_evals,
                             int* iters, double* work, cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   const bool in_smem = subspace_in_smem(q, KS);
   const size_t sm2 = sizeof(double) * (size_t)((in_smem ? 3 * q * KS : 0) + 3 * KS * KS + 3 * KS);
   cudaFuncSetAttribute(k_cc_subspace<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -480,7 +480,7 @@ void launch_cc_basis_large(const GridParams& g, const double* Ac, const double* 
                            double* scratch, double* work, double* Rcc, double* cc_evals,
                            int* scratch_status, int* iters, double tol, int maxit,
                            cudaStream_t s) {
-  const int q = g.sd * g.sd * g.sd * LC;
+  const int q = g.sd * g.sd * g.sd * g.lc;
   if (const char* e = getenv("TMG_CC_TOL")) tol = atof(e);  // diagnostics
   if (const char* e = getenv("TMG_CC_MAXIT")) maxit = atoi(e);
   double* Hs = scratch + g.e0 * q * q;

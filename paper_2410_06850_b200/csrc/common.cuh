@@ -13,7 +13,6 @@
 
 namespace tmg {
 
-constexpr int kMaxLc = 8;     // max local basis functions per coarse cell
 constexpr int kMaxPatches = 16;
 
 struct Patch {

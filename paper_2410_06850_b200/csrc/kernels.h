@@ -178,7 +178,7 @@ void launch_local_basis(const GridParams& g, int cb, const double* kappa, const 
                         int max_outer, cudaStream_t s);
 
 // coarse.cu
-int compiled_lc();
+int max_lc();  // largest supported L_c (num_local_basis)
 void launch_coarse_blocks(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                           const double* phi, double* Ac, double* Bc, cudaStream_t s);
 void launch_cc_basis(const GridParams& g, const double* Ac, const double* Bc, double* Rcc,

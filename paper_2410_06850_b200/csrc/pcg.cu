@@ -14,13 +14,29 @@
 // `done`, after which every later kernel returns immediately. No host round
 // trip is needed inside an iteration; the host only polls `done` between
 // chunks of captured iterations.
+#include <type_traits>
+
 #include "kernels.h"
 #include "pcg_fin.cuh"
 #include "smoother.cuh"
 
 namespace tmg {
 
-constexpr int LCP = 4;  // compiled L_c (see coarse.cu)
+// L_c (basis vectors per coarse cell) is a template parameter of the fine
+// kernels that touch Phi: 1..kMaxLcFine, dispatched at launch (lc_dispatch).
+constexpr int kMaxLcFine = 6;
+template <typename F>
+static void lc_dispatch(int lc, F&& f) {
+  switch (lc) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    default: throw std::runtime_error("L_c outside 1..6");
+  }
+}
 
 // ------------------------------------------------------------ coefficients
 template <int CB>
@@ -259,7 +275,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
 }
 
 // ------------------------------------------------------------ K3 restrict
-template <int CB>
+template <int CB, int LCP>
 __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, const double* __restrict__ coef,
                                                                 int64_t M, const double* __restrict__ phi,
                                                                 const double* __restrict__ r,
@@ -306,7 +322,7 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
 // Phi_I(c_f) T_f r1_nb(f) — the same algebra as solver.cpp:285-289 without
 // the brick's own r, r1 and the interior stencil (43% fewer bytes). Not valid
 // for cc-element fine blocks, which keep k_restrict.
-template <int CB>
+template <int CB, int LCP>
 __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
     GridParams g, const double* __restrict__ tfa, int64_t M, const double* __restrict__ phif,
     const double* __restrict__ r1f, double* rc, const PcgState* st) {
@@ -361,7 +377,7 @@ struct PostSmem {
   int flag;
 };
 
-template <int CB>
+template <int CB, int LCP>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const double* __restrict__ coef,
                                                            const double* __restrict__ /*tfa*/,
                                                            int64_t M, const double* __restrict__ phi,
@@ -462,7 +478,7 @@ struct PostBSmem {
   int flag;
 };
 
-template <int CB>
+template <int CB, int LCP>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, const double* __restrict__ coef,
                                                                const double* __restrict__ tfa,
                                                                int64_t M, const double* __restrict__ phif,
@@ -684,7 +700,11 @@ static void set_attrs() {
   cudaFuncSetAttribute(k_update<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem(CB));
   cudaFuncSetAttribute(k_brick_solve<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)update_smem(CB));
-  cudaFuncSetAttribute(K_POST<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)post_smem(CB));
+  for (int lc = 1; lc <= kMaxLcFine; ++lc)
+    lc_dispatch(lc, [](auto L) {
+      cudaFuncSetAttribute(K_POST<CB, decltype(L)::value>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)post_smem(CB));
+    });
 }
 
 // Called once per context creation (outside any stream capture).
@@ -739,19 +759,25 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_restrict<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
-  else launch_pdl(k_restrict<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
+  lc_dispatch(g.lc, [&](auto L) {
+    constexpr int LCP = decltype(L)::value;
+    if (cb == 8) launch_pdl(k_restrict<8, LCP>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
+    else launch_pdl(k_restrict<4, LCP>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, coef, M, phi, r, r1, rc, st);
+  });
 }
 void launch_restrict_bnd(const GridParams& g, int cb, const double* tf, const double* phif,
                          const double* r1f, double* rc, const PcgState* st, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8) launch_pdl(k_restrict_bnd<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, tf, M, phif, r1f, rc, st);
-  else launch_pdl(k_restrict_bnd<4>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, tf, M, phif, r1f, rc, st);
+  lc_dispatch(g.lc, [&](auto L) {
+    constexpr int LCP = decltype(L)::value;
+    if (cb == 8) launch_pdl(k_restrict_bnd<8, LCP>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, tf, M, phif, r1f, rc, st);
+    else launch_pdl(k_restrict_bnd<4, LCP>, dim3((unsigned)g.nbo), dim3(96), 0, s, g, tf, M, phif, r1f, rc, st);
+  });
 }
 
 // Face-major copy of Phi for the boundary-form kernels: their Phi reads are
 // whole 16-byte-coalesced face rows instead of stride-CB columns (x faces).
-template <int CB>
+template <int CB, int LCP>
 __global__ void __launch_bounds__(256) k_phi_faces(const double* __restrict__ phi, double* phif, int64_t b0) {
   constexpr int C = CB * CB * CB, F = CB * CB;
   const int64_t b = b0 + blockIdx.x;
@@ -764,9 +790,11 @@ __global__ void __launch_bounds__(256) k_phi_faces(const double* __restrict__ ph
 }
 void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* phif, int64_t b0,
                       int64_t nb, cudaStream_t s) {
-  (void)g;
-  if (cb == 8) k_phi_faces<8><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
-  else k_phi_faces<4><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
+  lc_dispatch(g.lc, [&](auto L) {
+    constexpr int LCP = decltype(L)::value;
+    if (cb == 8) k_phi_faces<8, LCP><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
+    else k_phi_faces<4, LCP><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
+  });
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* tf,
                  const double* phi_full, const double* phif, const double* Gf, const double* r,
@@ -775,8 +803,11 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
   const int64_t M = g.mst;
   const double* phi = TMG_POST_BND ? phif : phi_full;
   const double* r1 = TMG_POST_BND ? r1f : r1_full;
-  if (cb == 8) launch_pdl(K_POST<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
-  else launch_pdl(K_POST<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  lc_dispatch(g.lc, [&](auto L) {
+    constexpr int LCP = decltype(L)::value;
+    if (cb == 8) launch_pdl(K_POST<8, LCP>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
+    else launch_pdl(K_POST<4, LCP>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
+  });
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,

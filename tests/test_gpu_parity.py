@@ -773,3 +773,39 @@ def test_smoother_sweeps_on_slabs(nu):
     assert np.linalg.norm(za - zb) <= 1e-9 * np.linalg.norm(za)
     assert abs(ra.report.iterations - rb.report.iterations) <= 1
     assert np.linalg.norm(ra.x - rb.x) <= 1e-7 * np.linalg.norm(ra.x)
+
+
+# ------------------------------------------------ L_c != 4 (num_local_basis)
+
+@pytest.mark.parametrize("lc", [1, 2, 3, 5, 6])
+@pytest.mark.parametrize("n,ncc,sd,fine", [(32, 2, 2, "cell"), (32, 1, 4, "cell"), (32, 2, 2, "cc")])
+def test_num_local_basis_vs_oracle(lc, n, ncc, sd, fine):
+    """MmgOptions::num_local_basis (solver.hpp:142) other than the default 4:
+    the fine kernels are instantiated for L_c = 1..6 and the coarse level runs
+    with the runtime L_c; PCG against the oracle with the same partition."""
+    _, kappa = problem(n, 1e-3)
+    q = sd ** 3 * lc
+    s = O.System(O.grid(n), kappa, np.ones(n ** 3), PATCH)
+    lcc = min(8, q)
+    m = O.Precond("mmg", s, O.hierarchy(O.grid(n), ncc, sd), lc=lc, lcc=lcc, fine_blocks=fine,
+                  coarse_blocks="cc")
+    ref = O.pcg(s, s.rhs, m, rtol=1e-8, max_iterations=3000)
+    c = ctx_for(n, ncc, sd, kappa)
+    opts = MmgOptions(num_local_basis=lc, num_cc_basis=lcc,
+                      fine_blocks="cc" if fine == "cc" else "coarse_cell")
+    if q > 64 and q % 64 != 0:
+        with pytest.raises(NotSupportedError):
+            c.setup("mmg", opts)
+        return
+    c.setup("mmg", opts)
+    r = c.pcg(s.rhs, rtol=1e-8, max_iterations=3000)
+    assert r.report.converged == ref.converged
+    assert iters_close(r.report.iterations, ref.iterations), (r.report.iterations, ref.iterations)
+    assert np.linalg.norm(r.x - ref.x) <= 1e-6 * np.linalg.norm(ref.x)
+
+
+def test_num_local_basis_limits():
+    _, kappa = problem(16, 1e-3)
+    c = ctx_for(16, 1, 2, kappa)
+    with pytest.raises(NotSupportedError, match="L_c"):
+        c.setup("mmg", MmgOptions(num_local_basis=7, fine_blocks="coarse_cell"))
