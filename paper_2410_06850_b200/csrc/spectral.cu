@@ -274,8 +274,18 @@ __device__ __forceinline__ bool cholqr_apply(double (&x)[K], const double* g, do
   return ok;
 }
 
+// TMG_EIG_MINB CTAs per SM (register cap) and TMG_EIG_GROUP vectors per
+// Chebyshev pass (the filter is independent per vector, so smaller groups
+// keep fewer vectors live); the Gram staging buffer aliases the mat-vec
+// buffer so two CTAs fit one SM's shared memory.
+#ifndef TMG_EIG_MINB
+#define TMG_EIG_MINB 1
+#endif
+#ifndef TMG_EIG_GROUP
+#define TMG_EIG_GROUP 8
+#endif
 template <int CB, int K>
-__global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
+__global__ void __launch_bounds__(CB * CB * CB, (CB == 8 ? TMG_EIG_MINB : 1)) k_local_basis(GridParams g,
                                                              const double* __restrict__ kappa,
                                                              const double* __restrict__ phi0,
                                                              double* phi, double* evals,
@@ -285,15 +295,15 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
   constexpr int NW = C / 32;
   constexpr int NP = K * (K + 1) / 2;
   extern __shared__ double sm[];
-  double* u = sm;                     // K*C exchange buffer
-  double* kt = u + K * C;             // C
+  double* u = sm;                     // K*(C+4): mat-vec exchange, aliased by the Gram staging xs
+  double* kt = u + K * (C + 4);       // C
   double* red = kt + C;               // max(NP*NW + NP + 8, 64*NW)
   double* gs = red + (NP * NW + NP + 8 > 64 * NW ? NP * NW + NP + 8 : 64 * NW);  // K*K
   double* qv = gs + K * K;            // K*K
   double* rsm = qv + K * K;           // K*K
   double* scal = rsm + K * K;         // K + 8 scalars
-  double* xs = scal + K + 8;          // K*(C+4) Gram staging
-  double* ys = xs + K * (C + 4);      // K*(C+4)
+  double* xs = u;                     // K*(C+4) Gram staging (u is idle during Gram)
+  double* ys = scal + K + 8;          // K*(C+4)
   __shared__ int okflag;
   const int t = threadIdx.x, li = t % CB, lj = (t / CB) % CB, lk = t / (CB * CB);
   const int64_t b = blockIdx.x + g.b0;
@@ -417,29 +427,35 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
     a_cut = fmin(fmax(theta[K - 1], 1e-6 * bmax), 0.95 * bmax);
     const double e = 0.5 * (bmax - a_cut), c0 = 0.5 * (bmax + a_cut);
     const double sigma1 = e / (0.0 - c0);
-    double sigma = sigma1;
     const double gam = 2.0 / sigma1;
-    double x0[K];
-    bmatvec<CB, K>(x, y, u, tf, sl, sll, nb);
+    constexpr int KG = TMG_EIG_GROUP < K ? TMG_EIG_GROUP : K;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      x0[k] = x[k];
-      y[k] = (y[k] - c0 * x[k]) * (sigma1 / e);
-    }
-    for (int d = 2; d <= degree; ++d) {
-      const double sig2 = 1.0 / (gam - sigma);
-      double by[K];
-      bmatvec<CB, K>(y, by, u, tf, sl, sll, nb);
+    for (int g0 = 0; g0 < K; g0 += KG) {  // vector groups, each filtered on its own
+      double xg[KG], yg[KG], x0[KG];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const double ynew = (by[k] - c0 * y[k]) * (2.0 * sig2 / e) - (sigma * sig2) * x0[k];
-        x0[k] = y[k];
-        y[k] = ynew;
+      for (int k = 0; k < KG; ++k) xg[k] = x[g0 + k];
+      double sigma = sigma1;
+      bmatvec<CB, KG>(xg, yg, u, tf, sl, sll, nb);
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        x0[k] = xg[k];
+        yg[k] = (yg[k] - c0 * xg[k]) * (sigma1 / e);
       }
-      sigma = sig2;
-    }
+      for (int d = 2; d <= degree; ++d) {
+        const double sig2 = 1.0 / (gam - sigma);
+        double by[KG];
+        bmatvec<CB, KG>(yg, by, u, tf, sl, sll, nb);
 #pragma unroll
-    for (int k = 0; k < K; ++k) x[k] = y[k];
+        for (int k = 0; k < KG; ++k) {
+          const double ynew = (by[k] - c0 * yg[k]) * (2.0 * sig2 / e) - (sigma * sig2) * x0[k];
+          x0[k] = yg[k];
+          yg[k] = ynew;
+        }
+        sigma = sig2;
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) x[g0 + k] = yg[k];
+    }
   }
   outer_total += outer;
   }  // attempt
@@ -461,7 +477,7 @@ __global__ void __launch_bounds__(CB * CB * CB) k_local_basis(GridParams g,
 size_t local_basis_smem(int cb, int K) {
   const int C = cb * cb * cb, NW = C / 32, NP = K * (K + 1) / 2;
   const int red = NP * NW + NP + 8 > 64 * NW ? NP * NW + NP + 8 : 64 * NW;
-  return sizeof(double) * (size_t)(K * C + C + red + 3 * K * K + K + 8 + 2 * K * (C + 4));
+  return sizeof(double) * (size_t)(K * (C + 4) + C + red + 3 * K * K + K + 8 + K * (C + 4));
 }
 
 void launch_local_basis(const GridParams& g, int cb, const double* kappa, const double* phi0,
