@@ -76,9 +76,10 @@ typedef struct {
   int fine_blocks;     /* fine smoother partition (mmg, two_grid):
                           TMG_FINE_BLOCKS_CC (0, the default: build_mmg's
                           fine_blocks_by_cc, solver.cpp:353-361, one exact block per
-                          cc element of 8^3, 16^3 or 32^3 cells; TMG_ENOTSUP for
-                          other sizes or when the block factors exceed device
-                          memory) or TMG_FINE_BLOCKS_COARSE_CELL (1, opt-in: one
+                          cc element: 8^3, 16^3 or 32^3 cells with cubic 4^3 / 8^3
+                          coarse cells, any element whose z planes hold <= 4096
+                          cells otherwise; TMG_ENOTSUP beyond, or when the block
+                          factors exceed device memory) or TMG_FINE_BLOCKS_COARSE_CELL (1, opt-in: one
                           block per coarse cell, the fast GPU partition of
                           DESIGN.md §2; the reference builds it through
                           build_hierarchy_operators, solver.hpp:132-135) */
@@ -102,7 +103,13 @@ typedef struct {
 /* Context ------------------------------------------------------------------ */
 
 /* Validates the hierarchy like build_hierarchy (grid.cpp:196-218; ConfigError
- * on non-divisible axes) and allocates the context on CUDA device `device`. */
+ * on non-divisible axes) and allocates the context on CUDA device `device`.
+ * Any coarse-cell shape cells_per_c = n / (ncc sd) per axis is accepted up to
+ * 2^20 fine cells per coarse cell (TMG_ENOTSUP above): cubic 4^3 / 8^3 run
+ * the tuned kernels, every other shape (non-cubic, 2^3, 12^3, 17^3 with the
+ * reference's Lanczos-path ordering above 4096 cells, ...) the generic ones
+ * (csrc/generic.cu); TMG_FORCE_GENERIC=1 in the environment forces the
+ * generic kernels for 4^3 / 8^3 too (A/B tests). */
 int tmg_create(const tmg_grid* grid, int device, tmg_ctx** out);
 void tmg_destroy(tmg_ctx* ctx);
 
@@ -359,6 +366,10 @@ int tmg_download_solution(tmg_ctx* ctx, double* x);
 
 /* Introspection / measurement ------------------------------------------- */
 
+/* Fine smoother factor slots after tmg_setup (per-coarse-cell fine blocks):
+ * interior bricks whose cells and face halo carry one conductivity share one
+ * scaled factor, so slots <= bricks ("shared factors"). */
+int tmg_get_fine_factor_slots(tmg_ctx* ctx, int64_t* slots, int64_t* bricks);
 /* Local bases in the reference's R_c row order: phi[(I*Lc + a)*cells + i] is
  * entry i (cells_of_coarse order) of basis a of coarse cell I; evals[I*Lc+a]. */
 int tmg_get_local_bases(tmg_ctx* ctx, double* phi, double* evals, int* eig_iterations);

@@ -453,6 +453,20 @@ def ref_local_basis(n, ncc, sd, kappa, cid, count):
     return vals, vecs.reshape(count, cpc ** 3)
 
 
+def ref_local_basis_grid(shape, ncc, sd, kappa, cid, count):
+    """local_spectral_basis on an (nx, ny, nz) grid with per-axis ncc; boxes
+    above 4096 cells run the reference's Lanczos path."""
+    nx, ny, nz = shape
+    ncx, ncy, ncz = (ncc,) * 3 if np.isscalar(ncc) else tuple(ncc)
+    cpc = (nx // (ncx * sd)) * (ny // (ncy * sd)) * (nz // (ncz * sd))
+    vals = np.empty(count)
+    vecs = np.empty(count * cpc)
+    _ref_check(ref().ref_local_basis_grid(I64(nx), I64(ny), I64(nz), I64(ncx), I64(ncy), I64(ncz),
+                                          I64(sd), _d(np.ascontiguousarray(kappa, np.float64)),
+                                          I64(cid), I64(count), _d(vals), _d(vecs)))
+    return vals, vecs.reshape(count, cpc)
+
+
 def ref_solve(n, ncc, sd, kappa, rhs, patches, kind="mmg", fine_blocks=None,
               coarse_blocks=None, lc=4, lcc=8, sweeps=1, rtol=1e-8, maxit=10000, x0=None):
     """Reference make_preconditioner/build_hierarchy_operators + pcg. Blocks:

@@ -153,6 +153,22 @@ int ref_local_basis(int64_t nx, int64_t ny, int64_t nz, int64_t ncc, int64_t sd,
   });
 }
 
+// local_spectral_basis on any grid / hierarchy (per-axis ncc): boxes above
+// SpectralOptions::dense_threshold = 4096 cells take the reference's Lanczos
+// path (coarse_space.cpp:61-198, 229-230).
+int ref_local_basis_grid(int64_t nx, int64_t ny, int64_t nz, int64_t ncx, int64_t ncy, int64_t ncz,
+                         int64_t sd, const double* kappa, int64_t coarse_id, int64_t count,
+                         double* values, double* vectors) {
+  return guarded([&] {
+    const GridSpec g(nx, ny, nz);
+    const HierarchicalGrid h = build_hierarchy(g, {ncx, ncy, ncz}, sd);
+    const LocalSpectralBasis b = local_spectral_basis(
+        h, std::vector<double>(kappa, kappa + g.num_cells()), coarse_id, count);
+    std::memcpy(values, b.eigenvalues.data(), sizeof(double) * b.eigenvalues.size());
+    std::memcpy(vectors, b.vectors.data(), sizeof(double) * b.vectors.size());
+  });
+}
+
 // Full reference solve: assemble, make_preconditioner (kind 0 none, 1 jacobi,
 // 2 block_jacobi, 3 two_grid, 4 mmg) or — when fine_blocks/coarse_blocks >= 0
 // with kind 4 — build_coarse_spaces + build_hierarchy_operators with the given

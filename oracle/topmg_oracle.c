@@ -690,16 +690,134 @@ static void box_stiffness(const orc_grid* g, const double* kappa,
   free(t);
 }
 
-/* coarse_space.cpp:279-304 with generalized_smallest :203-234 and the dense
- * path dense_smallest :38-56 (Lanczos :61-198 is used by the reference only
- * for c^3 > 4096 and is not restated: such boxes return ORC_EARG). */
+/* lanczos_smallest (coarse_space.cpp:61-198): Lanczos with full (two-pass)
+ * reorthogonalisation on sigma I - B (sigma = max(Gershgorin row bound, 1)),
+ * random unit starts from Lcg64(0x5eedbeef) drawn as next_uniform() - 0.5 and
+ * Gram-Schmidt'ed against the basis, Ritz pairs of the tridiagonal T checked
+ * every step once m >= count (residual nb |last component| <= 1e-10 sigma),
+ * deflated restart on an invariant subspace (nb < 1e-14 sigma). The j-th
+ * largest Ritz value goes to slot count - 1 - j (descending in lambda); the
+ * returned block is re-orthonormalised in order. b: dense n x n (row-major). */
+static int lanczos_smallest(orc_index n, const double* b, orc_index count, double* values,
+                            double* vecs /* count x n */) {
+  double sigma = 0.0;
+  for (orc_index r = 0; r < n; ++r) {
+    double row = 0.0;
+    for (orc_index c = 0; c < n; ++c) {
+      const double v = b[r * n + c];
+      if (v != 0.0 || c == r) row += (c == r) ? v : fabs(v);
+    }
+    if (row > sigma) sigma = row;
+  }
+  if (sigma < 1.0) sigma = 1.0;
+  lcg64 rng = {0x5eedbeefULL};
+  double* basis = XMALLOC(double, (n + 1) * n);
+  double* alpha = XMALLOC(double, n + 1);
+  double* beta = XMALLOC(double, n + 1);
+  double* w = XMALLOC(double, n);
+  orc_index m = 0;
+  const double conv_tol = 1e-10 * sigma;
+#define FRESH(dst)                                                                   \
+  do {                                                                               \
+    for (orc_index i_ = 0; i_ < n; ++i_) (dst)[i_] = lcg_uniform(&rng) - 0.5;         \
+    for (orc_index q_ = 0; q_ < m; ++q_) {                                           \
+      double d_ = 0.0;                                                               \
+      for (orc_index i_ = 0; i_ < n; ++i_) d_ += basis[q_ * n + i_] * (dst)[i_];      \
+      for (orc_index i_ = 0; i_ < n; ++i_) (dst)[i_] -= d_ * basis[q_ * n + i_];      \
+    }                                                                                \
+    double nn_ = 0.0;                                                                \
+    for (orc_index i_ = 0; i_ < n; ++i_) nn_ += (dst)[i_] * (dst)[i_];               \
+    nn_ = sqrt(nn_);                                                                 \
+    for (orc_index i_ = 0; i_ < n; ++i_) (dst)[i_] /= nn_;                           \
+  } while (0)
+  FRESH(basis);
+  orc_index nbasis = 1;
+  int rc = ORC_ESOLVER;
+  for (orc_index step = 0; step < n; ++step) {
+    const double* q = basis + (nbasis - 1) * n;
+    for (orc_index r = 0; r < n; ++r) {  /* w = sigma q - B q */
+      double y = 0.0;
+      for (orc_index c = 0; c < n; ++c) y += b[r * n + c] * q[c];
+      w[r] = sigma * q[r] - y;
+    }
+    double a = 0.0;
+    for (orc_index i = 0; i < n; ++i) a += q[i] * w[i];
+    alpha[m++] = a;
+    for (int pass = 0; pass < 2; ++pass)
+      for (orc_index k = 0; k < nbasis; ++k) {
+        double d = 0.0;
+        for (orc_index i = 0; i < n; ++i) d += basis[k * n + i] * w[i];
+        for (orc_index i = 0; i < n; ++i) w[i] -= d * basis[k * n + i];
+      }
+    double nb = 0.0;
+    for (orc_index i = 0; i < n; ++i) nb += w[i] * w[i];
+    nb = sqrt(nb);
+    if (m >= count) {
+      double* t = XCALLOC(double, m * m);
+      double* tw = XMALLOC(double, m);
+      double* tv = XMALLOC(double, m * m);
+      for (orc_index i = 0; i < m; ++i) {
+        t[i * m + i] = alpha[i];
+        if (i + 1 < m) t[i * m + i + 1] = t[(i + 1) * m + i] = beta[i];
+      }
+      if (dla_syev_all((int)m, t, tw, tv)) {
+        free(t), free(tw), free(tv);
+        break;
+      }
+      int converged = 1;
+      for (orc_index j = 0; j < count; ++j)
+        if (nb * fabs(tv[(m - 1) * m + (m - 1 - j)]) > conv_tol) converged = 0;
+      if (converged || m == n || nb < 1e-14 * sigma) {
+        for (orc_index j = 0; j < count; ++j) {
+          const orc_index col = m - 1 - j, dst = count - 1 - j;
+          values[dst] = sigma - tw[col];
+          double* v = vecs + dst * n;
+          for (orc_index i = 0; i < n; ++i) v[i] = 0.0;
+          for (orc_index s2 = 0; s2 < m; ++s2)
+            for (orc_index i = 0; i < n; ++i) v[i] += tv[s2 * m + col] * basis[s2 * n + i];
+        }
+        rc = ORC_OK;
+        for (orc_index j = 0; j < count && rc == ORC_OK; ++j) {
+          double* vj = vecs + j * n;
+          for (orc_index k2 = 0; k2 < j; ++k2) {
+            double d = 0.0;
+            for (orc_index i = 0; i < n; ++i) d += vecs[k2 * n + i] * vj[i];
+            for (orc_index i = 0; i < n; ++i) vj[i] -= d * vecs[k2 * n + i];
+          }
+          double nn = 0.0;
+          for (orc_index i = 0; i < n; ++i) nn += vj[i] * vj[i];
+          nn = sqrt(nn);
+          if (nn < 1e-14) rc = ORC_ESOLVER;
+          for (orc_index i = 0; i < n; ++i) vj[i] /= nn;
+        }
+        free(t), free(tw), free(tv);
+        break;
+      }
+      free(t), free(tw), free(tv);
+    }
+    if (m == n) break;
+    if (nb < 1e-14 * sigma) {
+      beta[m - 1] = 0.0;
+      FRESH(basis + nbasis * n);
+    } else {
+      beta[m - 1] = nb;
+      for (orc_index i = 0; i < n; ++i) basis[nbasis * n + i] = w[i] / nb;
+    }
+    ++nbasis;
+  }
+#undef FRESH
+  free(basis), free(alpha), free(beta), free(w);
+  return rc;
+}
+
+/* coarse_space.cpp:279-304 with generalized_smallest :203-234: the dense path
+ * dense_smallest :38-56 up to SpectralOptions::dense_threshold = 4096 cells
+ * (coarse_space.hpp:37-42), lanczos_smallest :61-198 above. */
 int orc_local_basis(const orc_hgrid* h, const double* kappa, orc_index cid,
                     orc_index count, double* values, double* vectors) {
   const orc_index n = h_cells_in_coarse(h);
   if (count > n)
     return fail(ORC_EARG, "local_spectral_basis: more eigenvectors than cells requested");
-  if (n > 4096)
-    return fail(ORC_EARG, "oracle: Lanczos path (n > 4096) not restated");
   orc_index o[3];
   h_coarse_origin(h, cid, o);
   orc_csr s;
@@ -723,11 +841,19 @@ int orc_local_basis(const orc_hgrid* h, const double* kappa, orc_index cid,
     for (orc_index p = s.off[r]; p < s.off[r + 1]; ++p)
       dense[r * n + s.col[p]] = s.val[p] * (inv_sqrt[r] * inv_sqrt[s.col[p]]);
   double* v = XMALLOC(double, n * count);
-  const int rc = dla_syev_smallest((int)n, (int)count, dense, values, v);
-  if (rc == 0)
-    for (orc_index c = 0; c < count; ++c)
-      for (orc_index i = 0; i < n; ++i)
-        vectors[c * n + i] = v[i * count + c] * inv_sqrt[i];
+  int rc;
+  if (n <= 4096) {
+    rc = dla_syev_smallest((int)n, (int)count, dense, values, v);
+    if (rc == 0)
+      for (orc_index c = 0; c < count; ++c)
+        for (orc_index i = 0; i < n; ++i)
+          vectors[c * n + i] = v[i * count + c] * inv_sqrt[i];
+  } else {  /* v: count x n */
+    rc = lanczos_smallest(n, dense, count, values, v);
+    if (rc == 0)
+      for (orc_index c = 0; c < count; ++c)
+        for (orc_index i = 0; i < n; ++i) vectors[c * n + i] = v[c * n + i] * inv_sqrt[i];
+  }
   free(v);
   free(dense);
   free(inv_sqrt);

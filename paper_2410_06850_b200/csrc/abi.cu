@@ -120,7 +120,11 @@ struct Slab {
   double* phi_keep = nullptr;  // last set-up's bases (warm start of the next one)
   double* evals = nullptr;
   int* eig_iters = nullptr;
-  double* Gf = nullptr;
+  double* Gf = nullptr;        // fine block factors: compact slots (tuned bricks) or boxes
+  GSlot* gmap = nullptr;       // brick -> factor slot + scale (owned, virtual global)
+  int64_t* flist = nullptr;    // factor slot -> brick
+  int64_t nslots = 0;
+  FineFactors ff() const { return FineFactors{Gf, gmap}; }
   double* Ac = nullptr;
   double* Bc = nullptr;
   double* Rcc = nullptr;
@@ -148,8 +152,11 @@ struct tmg_ctx {
   cudaStream_t stream = nullptr;
   tmg_grid grid{};
   GridParams g{};  // global grid (b0 = 0, nbo = nb, ...)
-  int cb = 0;
+  int cb = 0;       // cubic brick edge of the templated kernels; 0 = generic shape (generic.cu)
   int fine_bj = 0;  // fine smoother blocks = cc elements (tmg_mmg_options.fine_blocks)
+  // exact fine blocks by the generic box block Thomas (generic.cu): -1 none,
+  // 0 = one box per brick, 1 = one box per cc element
+  int box_kind = -1;
   int nu = 1;       // smoother sweeps (MmgOptions::smoother_sweeps); != 1: enqueue_vcycle_nu
   int64_t M = 0;   // global cells
   std::string err;
@@ -323,6 +330,9 @@ void free_setup(tmg_ctx* c) {
     dfree_null(c, s.evals);
     dfree_null(c, s.eig_iters);
     dfree_null(c, s.Gf);
+    dfree_null(c, s.gmap);
+    dfree_null(c, s.flist);
+    s.nslots = 0;
     dfree_null(c, s.Ac);
     dfree_null(c, s.Bc);
     dfree_null(c, s.Rcc);
@@ -353,6 +363,7 @@ void free_setup(tmg_ctx* c) {
   }
   c->have_setup = false;
   c->kind = -1;
+  c->box_kind = -1;
 }
 
 int guard(tmg_ctx* c, const std::function<void()>& fn) {
@@ -392,7 +403,7 @@ int validate_patches(tmg_ctx* c, const tmg_patch* p, int np) {
 // cells of the host arrays this context reads/writes (NCCL: the own slab)
 int64_t host_cells(const tmg_ctx* c) { return c->nccl() ? c->slabs[0].xcells : c->M; }
 
-int64_t cells_per_brick(const tmg_ctx* c) { return (int64_t)c->cb * c->cb * c->cb; }
+int64_t cells_per_brick(const tmg_ctx* c) { return brick_cells(c->g); }
 
 // ------------------------------------------------------- ghost exchanges
 //
@@ -516,6 +527,7 @@ int finish_problem(tmg_ctx* c) {
     }
     exchange_coef(c);
     for (Slab& s : c->slabs) {  // face-major T (after the ghost coefficients)
+      if (c->cb == 0) break;    // read only by the templated boundary-form kernels
       if (!s.tf) s.tf = owned<double>(c, s, 6 * c->cb * c->cb);
       launch_face_t(s.g, c->cb, s.coef, s.tf, c->stream);
       CK(cudaGetLastError());
@@ -523,6 +535,51 @@ int finish_problem(tmg_ctx* c) {
     c->have_problem = true;
     free_setup(c);
   });
+}
+
+// Factor slots of the per-brick exact fine blocks (FineFactors): interior
+// bricks of one uniform conductivity (cells and face halo) share the factor
+// of the first such brick, scaled; every other brick gets its own slot.
+// TMG_G_SHARE=0 gives every brick its own slot (A/B diagnostics).
+void plan_fine_factors(tmg_ctx* c, Slab& s) {
+  const char* e = getenv("TMG_G_SHARE");
+  const bool share = !(e && e[0] == '0');
+  const int64_t nbo = s.g.nbo;
+  std::vector<int> flag((size_t)nbo, 0);
+  int* dflag = dalloc<int>(c, nbo);
+  if (share) {
+    launch_uniform_bricks(s.g, c->cb, s.kappa, dflag, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(flag.data(), dflag, sizeof(int) * (size_t)nbo, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  int64_t repb = -1;
+  for (int64_t i = 0; i < nbo && repb < 0; ++i)
+    if (flag[(size_t)i]) repb = s.g.b0 + i;
+  std::vector<GSlot> map((size_t)nbo);
+  std::vector<int64_t> list;
+  list.reserve((size_t)nbo);
+  if (repb >= 0) list.push_back(repb);  // slot 0: the shared factor
+  for (int64_t i = 0; i < nbo; ++i) {
+    if (flag[(size_t)i]) {
+      map[(size_t)i] = GSlot{0, 1.0};
+    } else {
+      map[(size_t)i] = GSlot{(int64_t)list.size(), 1.0};
+      list.push_back(s.g.b0 + i);
+    }
+  }
+  s.nslots = (int64_t)list.size();
+  s.gmap = owned<GSlot>(c, s, 1);
+  s.flist = dalloc<int64_t>(c, s.nslots);
+  CK(cudaMemcpyAsync(s.gmap + s.g.b0, map.data(), sizeof(GSlot) * (size_t)nbo,
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(s.flist, list.data(), sizeof(int64_t) * (size_t)s.nslots,
+                     cudaMemcpyHostToDevice, c->stream));
+  if (repb >= 0 && share) launch_factor_scales(s.g, c->cb, s.kappa, dflag, repb, s.gmap, c->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c->stream));  // the host vectors die here
+  dfree(c, dflag);
 }
 
 // ---------------------------------------------------------------- V-cycle
@@ -562,11 +619,11 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
   const GridParams& g = s.g;
   cudaStream_t st = c->stream;
-  KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
+  KL(1, launch_update(g, c->cb, s.coef, s.ff(), s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
                       s.history, init, st));
   KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
-  KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
+  KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
 
@@ -634,7 +691,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   cudaStream_t st = c->stream;
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.r1f, s.st,
+    KL(1, launch_update(s.g, c->cb, s.coef, s.ff(), s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.r1f, s.st,
                         s.partials, s.history, init, st));
   if (!init) reduce_finalize(c, kRedUpdate, 0);
   XCH(r1f, sizeof(double) * 6 * c->cb * c->cb, false);  // the boundary kernels read r1's face layers
@@ -642,7 +699,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
+    KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
                       init, st));
   reduce_finalize(c, kRedPost, init);
   XCH(z, sizeof(double) * C, false);
@@ -658,11 +715,19 @@ void enqueue_block_jacobi(tmg_ctx* c, int init, int par_new) {
                                s.partials, s.history, 0, 1, c->stream));
     if (c->dist()) reduce_finalize(c, kRedUpdate, 0);
   }
-  const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
-  const int nk = bj_apply_kernels(c->cb, c->g.sd);
-  for (Slab& s : c->slabs)
-    KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r, s.st,
-                           s.partials, init, s.ybj, c->stream));
+  if (c->box_kind == 1) {  // box block Thomas over the cc elements (generic.cu)
+    const int64_t per = box_doubles(c->g, 1);
+    for (Slab& s : c->slabs)
+      KL(box_apply_kernels(s.g, 1),
+         launch_box_apply(s.g, 1, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r, s.st,
+                          s.partials, init, s.ybj, c->stream));
+  } else {
+    const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
+    const int nk = bj_apply_kernels(c->cb, c->g.sd);
+    for (Slab& s : c->slabs)
+      KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, s.r, nullptr, s.z, s.r,
+                             s.st, s.partials, init, s.ybj, c->stream));
+  }
   if (c->dist()) {
     reduce_finalize(c, kRedPost, init);
     XCH(z, sizeof(double) * C, false);
@@ -729,8 +794,11 @@ void enqueue_vcycle_nu(tmg_ctx* c, int init, int par_new) {
   cudaStream_t st = c->stream;
   const int nu = c->nu;
   const size_t cvec = sizeof(double) * (size_t)c->lc;
-  const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
-  const int nk = c->fine_bj ? bj_apply_kernels(c->cb, c->g.sd) : 1;
+  const bool gen = c->box_kind >= 0;
+  const int64_t per = gen ? box_doubles(c->g, c->box_kind)
+                          : bj_doubles_per_element(c->cb, c->g.sd);
+  const int nk = gen ? box_apply_kernels(c->g, c->box_kind)
+                     : c->fine_bj ? bj_apply_kernels(c->cb, c->g.sd) : 1;
   if (!init) {  // x, r update + stopping test (the z write is deferred)
     for (Slab& s : c->slabs)
       KL(1, launch_jacobi_step(s.g, c->cb, nullptr, s.x, s.pbuf[par_new], s.q, s.r, s.z, s.st,
@@ -740,11 +808,17 @@ void enqueue_vcycle_nu(tmg_ctx* c, int init, int par_new) {
   // out = add + B^-1 in (per coarse cell or per cc element), optional r.out
   auto fine_solve = [&](Slab& s, const double* in, const double* add, double* out,
                         const double* rdot) {
-    if (c->fine_bj)
+    if (c->box_kind == 1)  // box block Thomas (generic.cu)
+      KL(nk, launch_box_apply(s.g, 1, s.coef, s.Gbj + s.g.e0 * per, in, add, out, rdot, s.st,
+                              s.partials, init, s.ybj, st));
+    else if (c->box_kind == 0)
+      KL(nk, launch_box_apply(s.g, 0, s.coef, s.Gf + s.g.b0 * per, in, add, out, rdot, s.st,
+                              s.partials, init, s.ybj, st));
+    else if (c->fine_bj)
       KL(nk, launch_bj_apply(s.g, c->cb, s.coef, s.Gbj + s.g.e0 * per, in, add, out, rdot, s.st,
                              s.partials, init, s.ybj, st));
     else
-      KL(1, launch_brick_solve(s.g, c->cb, s.coef, s.Gf, in, add, out, rdot, s.st, s.partials,
+      KL(1, launch_brick_solve(s.g, c->cb, s.coef, s.ff(), in, add, out, rdot, s.st, s.partials,
                                init, st));
   };
   // ---- fine pre-smoothing r1 = S_nu(r) ----
@@ -844,7 +918,7 @@ bool hierarchical(const tmg_ctx* c) {
 // x0 residual already in r); otherwise after the search step of an iteration.
 void enqueue_precond(tmg_ctx* c, int init, int par_new) {
   if (!hierarchical(c)) return enqueue_jacobi(c, init, par_new);
-  if (c->nu != 1) enqueue_vcycle_nu(c, init, par_new);
+  if (c->nu != 1 || c->cb == 0 || c->box_kind >= 0) enqueue_vcycle_nu(c, init, par_new);
   else if (c->fine_bj) enqueue_vcycle_bj(c, init, par_new);
   else if (c->dist()) enqueue_vcycle_dist(c, init, par_new);
   else enqueue_vcycle_single(c, init, c->slabs[0].pbuf[par_new]);
@@ -947,13 +1021,13 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   });
   if (!prof) {
     enqueue_precond_init(c);
-  } else if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
+  } else if (hierarchical(c) && !c->fine_bj && c->nu == 1 && c->cb != 0) {
     Slab& s = s0;
     const GridParams& g = s.g;
-    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.Gf, s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
+    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.ff(), s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
     timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
-    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
+    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
@@ -1000,11 +1074,11 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       par ^= 1;
       const int64_t kb = c->kcount;
       timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
-      if (hierarchical(c) && !c->fine_bj && c->nu == 1) {
-        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.Gf, s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
+      if (hierarchical(c) && !c->fine_bj && c->nu == 1 && c->cb != 0) {
+        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.ff(), s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
-        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.Gf, s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
+        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_precond(c, 0, par); });
       }
@@ -1046,7 +1120,11 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   }
 }
 
-int check_grid(const tmg_grid* grid, int64_t* cpc_out) {
+// Validates the hierarchy like build_hierarchy (grid.cpp:191-218) and picks
+// the kernels: cubic 4^3 / 8^3 coarse cells run the templated ones (*cb_out =
+// edge), every other shape the generic ones (*cb_out = 0; TMG_FORCE_GENERIC=1
+// forces them for 4^3 / 8^3 too, for A/B tests).
+int check_grid(const tmg_grid* grid, int64_t* cb_out) {
   const tmg_grid& G = *grid;
   if (G.nx <= 0 || G.ny <= 0 || G.nz <= 0)
     return set_err(nullptr, TMG_ECONFIG, "GridSpec: cell counts must be positive");
@@ -1065,18 +1143,22 @@ int check_grid(const tmg_grid* grid, int64_t* cpc_out) {
                      a, (long long)n[a], (long long)G.ncc[a], (long long)G.sd, (long long)div);
     cpc[a] = n[a] / div;
   }
-  if (cpc[0] != cpc[1] || cpc[1] != cpc[2] || !(cpc[0] == 4 || cpc[0] == 8))
+  if (cpc[0] * cpc[1] * cpc[2] > (int64_t)1 << 20)
     return set_err(nullptr, TMG_ENOTSUP,
-                   "GPU path builds cubic coarse cells of 4^3 or 8^3 fine cells (got %lldx%lldx%lld)",
+                   "GPU path handles coarse cells of up to 2^20 fine cells (got %lldx%lldx%lld)",
                    (long long)cpc[0], (long long)cpc[1], (long long)cpc[2]);
-  *cpc_out = cpc[0];
+  const char* fg = getenv("TMG_FORCE_GENERIC");
+  const bool force = fg && atoi(fg) > 0;
+  const bool tuned = cpc[0] == cpc[1] && cpc[1] == cpc[2] && (cpc[0] == 4 || cpc[0] == 8);
+  *cb_out = tuned && !force ? cpc[0] : 0;
   return TMG_OK;
 }
 
-GridParams global_params(const tmg_grid& G, int cb) {
+GridParams global_params(const tmg_grid& G) {
   GridParams g{};
   g.nx = G.nx; g.ny = G.ny; g.nz = G.nz;
-  g.nbx = G.nx / cb; g.nby = G.ny / cb; g.nbz = G.nz / cb;
+  g.nbx = G.ncc[0] * G.sd; g.nby = G.ncc[1] * G.sd; g.nbz = G.ncc[2] * G.sd;
+  g.bx = (int)(G.nx / g.nbx); g.by = (int)(G.ny / g.nby); g.bz = (int)(G.nz / g.nbz);
   g.nb = g.nbx * g.nby * g.nbz;
   g.ncx = G.ncc[0]; g.ncy = G.ncc[1]; g.ncz = G.ncc[2];
   g.ncc = g.ncx * g.ncy * g.ncz;
@@ -1126,7 +1208,7 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
   c->device = device;
   c->cb = (int)cb;
   c->M = grid->nx * grid->ny * grid->nz;
-  c->g = global_params(*grid, c->cb);
+  c->g = global_params(*grid);
   c->total = total;
   const int64_t C = cells_per_brick(c);
   rc = guard(c, [&] {
@@ -1162,8 +1244,8 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
       s.nbs = p.nbo + (p.lo + p.hi) * s.L;
       s.es0 = p.e0 - p.lo * s.Le;
       s.nes = p.neo + (p.lo + p.hi) * s.Le;
-      s.xoff = p.cz0 * c->cb * c->g.nx * c->g.ny;
-      s.xcells = (p.cz1 - p.cz0) * c->cb * c->g.nx * c->g.ny;
+      s.xoff = p.cz0 * c->g.bz * c->g.nx * c->g.ny;
+      s.xcells = (p.cz1 - p.cz0) * c->g.bz * c->g.nx * c->g.ny;
       s.g.mst = s.nbs * C;
       s.kappa = ghosted<double>(c, s, C);
       s.dmask = ghosted<uint8_t>(c, s, C);
@@ -1250,16 +1332,16 @@ int tmg_partition(const tmg_grid* grid, int nranks, int rank, int64_t* out) {
   if (rc) return rc;
   if (rank < 0 || rank >= nranks)
     return set_err(nullptr, TMG_EARG, "tmg_partition: bad rank %d of %d", rank, nranks);
-  const GridParams g = global_params(*grid, (int)cb);
+  const GridParams g = global_params(*grid);
   const Part p = partition(g, rank, nranks);
-  out[0] = p.cz0 * cb;                          // first fine z layer
-  out[1] = p.cz1 * cb;                          // end fine z layer
+  out[0] = p.cz0 * g.bz;                        // first fine z layer
+  out[1] = p.cz1 * g.bz;                        // end fine z layer
   out[2] = p.b0;                                // first owned brick
   out[3] = p.nbo;                               // owned bricks
   out[4] = p.e0;                                // first owned cc element
   out[5] = p.neo;                               // owned cc elements
-  out[6] = p.cz0 * cb * g.nx * g.ny;            // first x-fastest cell
-  out[7] = (p.cz1 - p.cz0) * cb * g.nx * g.ny;  // cells
+  out[6] = p.cz0 * g.bz * g.nx * g.ny;            // first x-fastest cell
+  out[7] = (p.cz1 - p.cz0) * g.bz * g.nx * g.ny;  // cells
   out[8] = p.lo;                                // neighbour below
   out[9] = p.hi;                                // neighbour above
   return TMG_OK;
@@ -1274,7 +1356,7 @@ int tmg_halo_plan(const tmg_grid* grid, int nranks, int rank, int elem, int64_t*
   if (rc) return -rc;
   if (rank < 0 || rank >= nranks)
     return -set_err(nullptr, TMG_EARG, "tmg_halo_plan: bad rank %d of %d", rank, nranks);
-  const GridParams g = global_params(*grid, (int)cb);
+  const GridParams g = global_params(*grid);
   const std::vector<HaloOp> v =
       halo_ops(partition(g, rank, nranks), rank, elem ? g.ncx * g.ncy : g.nbx * g.nby, elem != 0);
   if ((int)v.size() > max_ops)
@@ -1967,18 +2049,28 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
   const bool fine_bj = hier && o->fine_blocks == TMG_FINE_BLOCKS_CC;
   if (hier && o->fine_blocks != TMG_FINE_BLOCKS_COARSE_CELL && !fine_bj)
     return set_err(c, TMG_EARG, "fine_blocks must be TMG_FINE_BLOCKS_COARSE_CELL or _CC");
-  if ((kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj) && !bj_supported((int)c->cb, c->g.sd))
+  const bool gen = c->cb == 0;  // generic brick shape (generic.cu)
+  const bool want_cc = kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj;
+  // exact fine blocks by the generic box block Thomas (generic.cu): every
+  // block of a generic shape, and the cc elements the tuned kernels of
+  // block_jacobi.cu (8^3, 16^3, 32^3 cells) do not cover
+  const int box_kind = (want_cc && (gen || !bj_supported((int)c->cb, c->g.sd))) ? 1
+                       : (gen && hier) ? 0 : -1;
+  const bool gen_boxes = box_kind >= 0;
+  const int gen_kind = box_kind;
+  if (gen_boxes && box_plane_cells(c->g, gen_kind) > 4096)
     return set_err(c, TMG_ENOTSUP,
-                   "GPU block_jacobi / cc-element fine blocks handle cc elements of 8^3, 16^3 or "
-                   "32^3 cells (got %lld^3); use fine_blocks = coarse_cell",
-                   (long long)(c->cb * c->g.sd));
-  if (kind == TMG_PRECOND_BLOCK_JACOBI || fine_bj) {
-    // the exact per-element factors (E^5 doubles per element) must fit
+                   "GPU fine blocks of this shape have z planes of %d cells (limit 4096); use "
+                   "fine_blocks = coarse_cell or a finer hierarchy",
+                   box_plane_cells(c->g, gen_kind));
+  if (want_cc || gen_boxes) {
+    // the exact per-block factors (E^5 doubles per element) must fit
     size_t fr = 0, tot = 0;
     if (cudaSetDevice(c->device) == cudaSuccess && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
       double need = 0.0;
       for (const Slab& s : c->slabs)
-        need += 8.0 * (double)s.g.neo * (double)bj_doubles_per_element((int)c->cb, c->g.sd);
+        need += gen_boxes ? 8.0 * (double)(gen_kind ? s.g.neo : s.g.nbo) * (double)box_doubles(s.g, gen_kind)
+                    : 8.0 * (double)s.g.neo * (double)bj_doubles_per_element((int)c->cb, c->g.sd);
       if (need > 0.9 * (double)(fr + c->bytes))
         return set_err(c, TMG_ENOTSUP,
                        "cc-element block factors need %.1f GB (device has %.1f GB); use "
@@ -1988,7 +2080,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
   }
   if (kind < 0 || kind > 4) return set_err(c, TMG_ECONFIG, "make_preconditioner: unknown kind");
   if (hier) {
-    const int64_t cells = (int64_t)c->cb * c->cb * c->cb;
+    const int64_t cells = cells_per_brick(c);
     if (o->num_local_basis > cells)
       return set_err(c, TMG_EARG, "local_spectral_basis: more eigenvectors than cells requested");
     if (o->num_local_basis < 1 || o->num_local_basis > max_lc())
@@ -2035,6 +2127,16 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         launch_apply(s.g, c->cb, s.coef, nullptr, nullptr, s.dinv, c->stream);
         CK(cudaGetLastError());
       }
+    } else if (kind == TMG_PRECOND_BLOCK_JACOBI && box_kind == 1) {
+      const int64_t per = box_doubles(c->g, 1);
+      for (Slab& s : c->slabs) {
+        s.Gbj = owned_e<double>(c, s, per);
+        s.ybj = owned<double>(c, s, C);
+        double* w = dalloc<double>(c, box_factor_work_doubles(s.g, 1));
+        launch_box_factor(s.g, 1, s.coef, s.Gbj + s.g.e0 * per, s.d_status, w, c->stream);
+        CK(cudaGetLastError());
+        dfree(c, w);
+      }
     } else if (kind == TMG_PRECOND_BLOCK_JACOBI) {
       const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
       for (Slab& s : c->slabs) {
@@ -2062,13 +2164,18 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
         s.phi = ghosted<double>(c, s, lc * C);
         s.evals = owned<double>(c, s, lc);
         s.eig_iters = owned<int>(c, s, 1);
-        if (fine_bj) {
+        if (box_kind >= 0) {  // box factors of the cc elements or of the bricks
+          if (box_kind == 1) s.Gbj = owned_e<double>(c, s, box_doubles(c->g, 1));
+          else s.Gf = owned<double>(c, s, box_doubles(c->g, 0));
+          s.ybj = owned<double>(c, s, C);
+        } else if (fine_bj) {
           s.Gbj = owned_e<double>(c, s, bj_doubles_per_element(c->cb, c->g.sd));
           if (bj_apply_kernels((int)c->cb, c->g.sd) > 1) s.ybj = owned<double>(c, s, C);
         } else {
-          s.Gf = owned<double>(c, s, thomas_doubles_per_brick(c->cb));
+          plan_fine_factors(c, s);
+          s.Gf = dalloc<double>(c, s.nslots * thomas_doubles_per_brick(c->cb));
         }
-        if (fine_bj || o->smoother_sweeps != 1) {  // unfused V-cycles
+        if (fine_bj || o->smoother_sweeps != 1 || gen) {  // unfused V-cycles
           s.r2 = ghosted<double>(c, s, C);
           s.t2 = ghosted<double>(c, s, C);
         }
@@ -2103,20 +2210,61 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       const int max_outer = o->eig_max_outer > 0 ? o->eig_max_outer : 60;
       for (size_t k = 0; k < c->slabs.size(); ++k) {
         Slab& s = c->slabs[k];
-        launch_local_basis(s.g, c->cb, s.kappa, phi_prev[k], s.phi, s.evals, s.eig_iters, tol,
-                           degree, max_outer, c->stream);
+        if (gen) {
+          const int64_t wd = g_local_basis_scratch_doubles(s.g);
+          double* w = wd ? dalloc<double>(c, wd) : nullptr;
+          launch_g_local_basis(s.g, s.kappa, phi_prev[k], s.phi, s.evals, s.eig_iters, tol,
+                               degree, max_outer, w, c->stream);
+          if (w) dfree(c, w);  // stream-ordered reuse only
+        } else {
+          // bricks of one uniform conductivity share one eigensolve (their
+          // local problems are scalar multiples, spectral.cu); TMG_EIG_SHARE=0: off
+          const char* es = getenv("TMG_EIG_SHARE");
+          const bool share = !(es && es[0] == '0');
+          std::vector<int> flag((size_t)s.g.nbo, 0);
+          int* dflag = dalloc<int>(c, s.g.nbo);
+          if (share) {
+            launch_uniform_inside(s.g, c->cb, s.kappa, dflag, c->stream);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(flag.data(), dflag, sizeof(int) * flag.size(),
+                               cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+          }
+          int64_t repb = -1;
+          std::vector<int64_t> list;
+          for (int64_t i = 0; i < s.g.nbo; ++i) {
+            if (flag[(size_t)i] && repb >= 0) continue;
+            if (flag[(size_t)i]) repb = s.g.b0 + i;
+            list.push_back(s.g.b0 + i);
+          }
+          int64_t* dlist = dalloc<int64_t>(c, (int64_t)list.size());
+          CK(cudaMemcpyAsync(dlist, list.data(), sizeof(int64_t) * list.size(),
+                             cudaMemcpyHostToDevice, c->stream));
+          launch_local_basis(s.g, c->cb, s.kappa, phi_prev[k], s.phi, s.evals, s.eig_iters, tol,
+                             degree, max_outer, dlist, (int64_t)list.size(), c->stream);
+          if (repb >= 0)
+            launch_local_basis_share(s.g, c->cb, s.kappa, dflag, repb, s.phi, s.evals,
+                                     s.eig_iters, c->stream);
+          CK(cudaGetLastError());
+          CK(cudaStreamSynchronize(c->stream));  // list lives on the host stack
+          dfree(c, dlist);
+          dfree(c, dflag);
+        }
       }
       CK(cudaGetLastError());
       for (double*& pp : phi_prev) dfree_null(c, pp);  // stream-ordered reuse only
       XCH(phi, sizeof(double) * lc * C, false);
       for (Slab& s : c->slabs) {  // after the exchange: ghost bricks' faces too
+        if (gen) break;           // read only by the templated boundary-form kernels
         s.phif = ghosted<double>(c, s, 6 * lc * c->cb * c->cb);
         launch_phi_faces(s.g, c->cb, s.phi, s.phif, s.bs0, s.nbs, c->stream);
       }
       CK(cudaGetLastError());
       mark("local_basis");
-      for (Slab& s : c->slabs)
-        launch_coarse_blocks(s.g, c->cb, s.kappa, s.dmask, s.phi, s.Ac, s.Bc, c->stream);
+      for (Slab& s : c->slabs) {
+        if (gen) launch_g_coarse_blocks(s.g, s.kappa, s.dmask, s.coef, s.phi, s.Ac, s.Bc, c->stream);
+        else launch_coarse_blocks(s.g, c->cb, s.kappa, s.dmask, s.phi, s.Ac, s.Bc, c->stream);
+      }
       CK(cudaGetLastError());
       mark("coarse_blocks");
       int* cc_iters = nullptr;
@@ -2156,14 +2304,22 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
       CK(cudaGetLastError());
       mark("coarse_smoother");
       for (Slab& s : c->slabs) {
-        if (fine_bj) {
+        if (box_kind >= 0) {
+          const int bk = box_kind;
+          const int64_t per = box_doubles(s.g, bk);
+          double* G = bk ? s.Gbj + s.g.e0 * per : s.Gf + s.g.b0 * per;
+          double* w = dalloc<double>(c, box_factor_work_doubles(s.g, bk));
+          launch_box_factor(s.g, bk, s.coef, G, s.d_status, w, c->stream);
+          dfree(c, w);
+        } else if (fine_bj) {
           const int64_t per = bj_doubles_per_element(c->cb, c->g.sd);
           const int64_t wd = bj_factor_work_doubles((int)c->cb, c->g.sd, s.g.neo);
           double* w = wd ? dalloc<double>(c, wd) : nullptr;
           launch_bj_factor(s.g, (int)c->cb, s.coef, s.Gbj + s.g.e0 * per, s.d_status, w, c->stream);
           if (w) dfree(c, w);
         } else {
-          launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.Gf, s.d_status, c->stream);
+          launch_thomas_factor(s.g, c->cb, s.kappa, s.dmask, s.flist, s.nslots, s.Gf, s.d_status,
+                               c->stream);
         }
       }
       CK(cudaGetLastError());
@@ -2300,6 +2456,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
     }
     c->kind = kind;
     c->fine_bj = fine_bj ? 1 : 0;
+    c->box_kind = box_kind;
     c->nu = hier ? o->smoother_sweeps : 1;
     c->have_setup = true;
     build_graph(c, 4);
@@ -2466,6 +2623,17 @@ int tmg_get_sizes(tmg_ctx* c, int64_t* s) {
   s[3] = c->g.ncc;
   s[4] = c->g.ncc * c->lcc;
   s[5] = cells_per_brick(c);
+  return TMG_OK;
+}
+
+int tmg_get_fine_factor_slots(tmg_ctx* c, int64_t* slots, int64_t* bricks) {
+  if (!c || !slots || !bricks) return set_err(c, TMG_EARG, "null argument");
+  *slots = 0;
+  *bricks = 0;
+  for (const Slab& s : c->slabs) {
+    *slots += s.nslots;
+    *bricks += s.g.nbo;
+  }
   return TMG_OK;
 }
 

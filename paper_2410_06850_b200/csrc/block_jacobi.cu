@@ -433,6 +433,7 @@ void launch_bj_apply(const GridParams& g, int cb, const double* coef, const doub
 void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
                        double* out, const double* rdot, PcgState* st, double* partials, int init,
                        cudaStream_t s) {
+  if (cb == 0) return launch_g_add_finish(g, y, add, out, rdot, st, partials, init, s);
   if (cb == 8)
     launch_pdl(k_add_finish<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, y, add, out, rdot, st,
                partials, init);
@@ -443,6 +444,7 @@ void launch_add_finish(const GridParams& g, int cb, const double* y, const doubl
 
 void launch_prolong_add(const GridParams& g, int cb, const double* phi, const double* r1,
                         const double* ec, double* r2, const PcgState* st, cudaStream_t s) {
+  if (cb == 0) return launch_g_prolong_add(g, phi, r1, ec, r2, st, s);
   if (cb == 8)
     launch_pdl(k_prolong_add<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, phi, r1, ec, r2, st);
   else
@@ -451,6 +453,7 @@ void launch_prolong_add(const GridParams& g, int cb, const double* phi, const do
 
 void launch_resid(const GridParams& g, int cb, const double* coef, const double* r,
                   const double* x, double* t, const PcgState* st, cudaStream_t s) {
+  if (cb == 0) return launch_g_resid(g, coef, r, x, t, st, s);
   if (cb == 8)
     launch_pdl(k_resid<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, coef, r, x, t, st);
   else

@@ -78,15 +78,16 @@ __device__ inline void build_elem_matrix(const GridParams& g, const ElemCoord& e
   __syncthreads();
 }
 
-// Warp-parallel Jacobi on q x q (q even, q <= 64) symmetric M in smem;
-// V (q x q) eigenvectors in columns. Lanes own rows r = lane, lane+32.
+// Warp-parallel Jacobi on q x q (q <= 64) symmetric M in smem; V (q x q)
+// eigenvectors in columns. Lanes own rows r = lane, lane+32.
 __device__ inline void warp_jacobi(double* M, double* V, int q) {
-  // round-robin ("tournament") ordering: a sweep is q-1 rounds of q/2
-  // disjoint rotations (q even, q <= 64); lane g computes rotation g of the
-  // round, then every lane applies all of them to its rows / columns.
+  // round-robin ("tournament") ordering: a sweep is Q-1 rounds of Q/2
+  // disjoint rotations (Q = q rounded up to even: for odd q one player is a
+  // bye, its pair is skipped); lane g computes rotation g of the round, then
+  // every lane applies all of them to its rows / columns.
   __shared__ double rc[32], rs[32];
   __shared__ int rp[32], rq[32];
-  const int lane = threadIdx.x & 31, np = q / 2;
+  const int lane = threadIdx.x & 31, Q = q + (q & 1), np = Q / 2;
   for (int r = lane; r < q; r += 32)
     for (int c = 0; c < q; ++c) V[r * q + c] = r == c ? 1.0 : 0.0;
   __syncwarp();
@@ -103,25 +104,26 @@ __device__ inline void warp_jacobi(double* M, double* V, int q) {
       tot += __shfl_xor_sync(0xffffffffu, tot, o);
     }
     if (off <= 1e-26 * tot || off == 0.0) break;
-    for (int round = 0; round < q - 1; ++round) {
-      if (lane < np) {  // circle method: player q-1 fixed
+    for (int round = 0; round < Q - 1; ++round) {
+      if (lane < np) {  // circle method: player Q-1 fixed
         int p, qq;
         if (lane == 0) {
           p = round;
-          qq = q - 1;
+          qq = Q - 1;
         } else {
-          p = (round + lane) % (q - 1);
-          qq = (round - lane + (q - 1)) % (q - 1);
+          p = (round + lane) % (Q - 1);
+          qq = (round - lane + (Q - 1)) % (Q - 1);
         }
         if (p > qq) {
           const int tmp = p;
           p = qq;
           qq = tmp;
         }
-        const double apq = M[p * q + qq];
-        const double app = M[p * q + p], aqq = M[qq * q + qq];
+        const bool bye = qq >= q;  // odd q: the pair with the bye player
+        const double apq = bye ? 0.0 : M[p * q + qq];
+        const double app = M[p * q + p], aqq = bye ? 0.0 : M[qq * q + qq];
         double c = 1.0, sn = 0.0;
-        if (!(fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq)))) {
+        if (!bye && !(fabs(apq) <= 1e-300 || fabs(apq) <= 1e-18 * sqrt(fabs(app * aqq)))) {
           const double theta = (aqq - app) / (2.0 * apq);
           const double tt = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
           c = 1.0 / sqrt(tt * tt + 1.0);
@@ -130,12 +132,13 @@ __device__ inline void warp_jacobi(double* M, double* V, int q) {
         rc[lane] = c;
         rs[lane] = sn;
         rp[lane] = p;
-        rq[lane] = qq;
+        rq[lane] = bye ? p : qq;  // a bye pair rotates p with itself by c = 1, s = 0
       }
       __syncwarp();
       for (int r = lane; r < q; r += 32)  // columns p, qq of row r (pairs disjoint)
         for (int g = 0; g < np; ++g) {
           const int p = rp[g], qq = rq[g];
+          if (p == qq) continue;
           const double c = rc[g], sn = rs[g];
           const double akp = M[r * q + p], akq = M[r * q + qq];
           M[r * q + p] = c * akp - sn * akq;
@@ -148,6 +151,7 @@ __device__ inline void warp_jacobi(double* M, double* V, int q) {
       for (int r = lane; r < q; r += 32)  // rows p, qq at column r
         for (int g = 0; g < np; ++g) {
           const int p = rp[g], qq = rq[g];
+          if (p == qq) continue;
           const double c = rc[g], sn = rs[g];
           const double apk = M[p * q + r], aqk = M[qq * q + r];
           M[p * q + r] = c * apk - sn * aqk;

@@ -248,6 +248,58 @@ __device__ void svqb_pass(const double* Y, double* X, int q, double* T, double* 
   __syncthreads();
 }
 
+// X = Y R^-1 with Y^T Y = R^T R (CholQR; Y == X allowed): one warp factors
+// the KS x KS Gram matrix with shuffles, every thread back-substitutes its
+// rows. Returns false (X untouched) when the Gram matrix is not numerically
+// positive definite, for the caller's SVQB fallback.
+template <int KS>
+__device__ bool cholqr_pass(const double* Y, double* X, int q, double* T, double* R,
+                            int* okflag) {
+  const int t = threadIdx.x;
+  gram<KS>(Y, Y, q, T, false);
+  if (t < 32) {
+    const int lane = t;
+    double a[KS];
+#pragma unroll
+    for (int i = 0; i < KS; ++i) a[i] = lane < KS ? T[i * KS + lane] : 0.0;
+    double gmax = lane < KS ? T[lane * KS + lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      const double d = __shfl_sync(0xffffffffu, a[k], k);
+      ok = ok && (d > 1e-24 * gmax);
+      const double rkk = ok ? sqrt(d) : 1.0;
+      const double rkj = lane >= k && lane < KS ? a[k] / rkk : 0.0;
+      if (lane < KS) R[k * KS + lane] = lane >= k ? rkj : 0.0;
+#pragma unroll
+      for (int i = k + 1; i < KS; ++i) {
+        const double rki = __shfl_sync(0xffffffffu, rkj, i);
+        if (lane > k) a[i] -= rki * rkj;
+      }
+    }
+    if (lane == 0) *okflag = ok;
+  }
+  __syncthreads();
+  if (!*okflag) return false;
+  for (int r = t; r < q; r += blockDim.x) {
+    double x[KS];
+#pragma unroll
+    for (int i = 0; i < KS; ++i) x[i] = Y[r * KS + i];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      double v = x[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) v = fma(-x[k], R[k * KS + j], v);
+      x[j] = v / R[j * KS + j];
+    }
+#pragma unroll
+    for (int i = 0; i < KS; ++i) X[r * KS + i] = x[i];
+  }
+  __syncthreads();
+  return true;
+}
+
 // Z = H X with H = (A_c - Bc on the diagonal blocks) restricted to E's children.
 template <int KS>
 __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const double* Ac,
@@ -320,9 +372,10 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
   __syncthreads();
   int it = 0;
   for (;; ++it) {
-    svqb_pass<KS>(Y, X, q, T, V, F, dsc, red);
-    svqb_pass<KS>(X, Y, q, T, V, F, dsc, red);
-    { double* tmp = X; X = Y; Y = tmp; }
+    // orthonormalise Y -> X: CholQR twice (one warp, no block-wide Jacobi
+    // sweeps); SVQB for a pass whose Gram matrix is not numerically PD
+    if (!cholqr_pass<KS>(Y, X, q, T, F, &flag)) svqb_pass<KS>(Y, X, q, T, V, F, dsc, red);
+    if (!cholqr_pass<KS>(X, X, q, T, F, &flag)) svqb_pass<KS>(X, X, q, T, V, F, dsc, red);
     // Rayleigh-Ritz on H
     apply_projected<KS>(g, ec, Ac, Bc, X, Z, q);
     __syncthreads();
@@ -418,9 +471,12 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
 // q <= 256: one CTA per element (k_batched_gj); larger q (sd = 8: 2048) with
 // the tensor-core blocked Gauss-Jordan batched over the elements (dense.cu).
 // L_cc <= 12: 16 subspace columns, <= 20: 24.
-bool coarse_large_supported(int q, int lcc) {
-  return q > 64 && q % GB == 0 && q <= 4096 && lcc <= 20;
-}
+bool coarse_large_supported(int q, int lcc) { return q > 64 && q <= 4096 && lcc <= 20; }
+
+// element inverses: one CTA per element (register/shared Gauss-Jordan,
+// gj_global.cuh) for q = 128, 192, 256; the tensor-core blocked Gauss-Jordan
+// batched over the elements (dense.cu) for every other q
+static bool gj_per_cta(int q) { return q % GB == 0 && q <= GJT; }
 
 // TMG_CC_KS=16/24 overrides (diagnostics)
 static int subspace_width(int lcc) {
@@ -434,8 +490,8 @@ static bool subspace_in_smem(int q, int ks) { return q <= 256 && 3 * q * ks * 8 
 
 // scratch doubles the large-q set-up needs besides Winv's storage
 int64_t coarse_large_work_doubles(int q, int64_t neo, int lcc) {
-  if (q <= 256 && subspace_in_smem(q, subspace_width(lcc))) return 0;
-  const int64_t inv = q > 256 ? neo * dense_inverse_work_doubles(q) : 0;
+  if (gj_per_cta(q) && subspace_in_smem(q, subspace_width(lcc))) return 0;
+  const int64_t inv = gj_per_cta(q) ? 0 : neo * dense_inverse_work_doubles(q);
   const int64_t sub = neo * 3 * (int64_t)q * subspace_width(lcc);
   return inv > sub ? inv : sub;
 }
@@ -444,7 +500,7 @@ size_t batched_gj_smem(int q) { return gj_global_smem_bytes(q); }
 
 static void invert_elements(double* A, int q, int64_t neo, double* work, int* status,
                             cudaStream_t s) {
-  if (q <= GJT) {
+  if (gj_per_cta(q)) {
     const size_t smem = batched_gj_smem(q);
     cudaFuncSetAttribute(k_batched_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_batched_gj<<<(unsigned)neo, GJT, smem, s>>>(A, q, status);

@@ -40,7 +40,17 @@ struct GridParams {
   // stored cells per fine vector (component stride of coef).
   int64_t b0, nbo, e0, neo, mst;
   int dist;  // 1: reductions finish in k_finalize after the cross-slab sum
+  // Brick (= coarse cell) extent in fine cells per axis: the reference's
+  // HierarchicalGrid::cells_per_c (grid.hpp:100). The templated kernels are
+  // built for cubic 4^3 / 8^3 bricks; any other shape runs the generic
+  // kernels of generic.cu (cb = 0 at the launchers).
+  int bx, by, bz;
 };
+
+// cells per brick
+__host__ __device__ __forceinline__ int64_t brick_cells(const GridParams& g) {
+  return (int64_t)g.bx * g.by * g.bz;
+}
 
 // ------------------------------------------ programmatic dependent launch
 // Iteration kernels are launched with PDL (launch_pdl): each CTA lets the next

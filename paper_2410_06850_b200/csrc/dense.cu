@@ -20,6 +20,9 @@
 namespace tmg {
 
 constexpr int NB = 64;  // Gauss-Jordan pivot block
+// leading dimension of the Pn panel: rows start 16-byte aligned for the TMA
+// bulk copies whatever the parity of n
+__host__ __device__ __forceinline__ int64_t pn_ld(int64_t n) { return (n + 1) & ~(int64_t)1; }
 
 // Invert the pivot block A[K,K] (nbk x nbk, nbk <= NB, identity-padded to NB)
 // into Dinv and record the pivots: one CTA, register-resident Gauss-Jordan
@@ -88,6 +91,9 @@ __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A,
     As[c][jx] = (c < nbk && j < n) ? (j <= r ? A[r * n + j] : A[j * n + r]) : 0.0;
   }
   __syncthreads();
+  const int64_t ldp = pn_ld(n);
+  if (j == n && j < ldp)  // odd n: the padding column (read by the even-width TMA rows)
+    for (int q = 0; q < NB / 8; ++q) Pn[(ry * (NB / 8) + q) * ldp + j] = 0.0;
   if (j < n) {
     constexpr int RG = NB / 8;
     double acc[RG];
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(256) k_gj_panels(const double* __restrict__ A,
       for (int q = 0; q < RG; ++q) acc[q] = fma(Ds[ry * RG + q][c], a, acc[q]);
     }
 #pragma unroll
-    for (int q = 0; q < RG; ++q) Pn[(ry * RG + q) * n + j] = acc[q];
+    for (int q = 0; q < RG; ++q) Pn[(ry * RG + q) * ldp + j] = acc[q];
   }
   // Cold: this CTA's 32 rows i = j-range, NB columns each; A_{i,K} from the
   // lower triangle (processed rows i < k0 carry the sign of the sweep:
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
   const int64_t i0 = (int64_t)blockIdx.y * GT, j0 = (int64_t)blockIdx.x * GN;
   if (i0 + GT - 1 < j0) return;  // strictly above the diagonal: not maintained
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t < GT && i0 + t < n) {
+  if (t < GT && i0 + t < n && !(n & 1)) {  // (16-byte aligned rows only)
     const int64_t cols = (n - j0) < GN ? (n - j0) : GN;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A + (i0 + t) * n + j0),
                  "r"((unsigned)(cols * sizeof(double)))
@@ -155,7 +161,10 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
   // mbarrier; rows past n are zero-filled by the threads instead
   __shared__ uint64_t bar;
   const int rows_a = (int)((n - i0) < GT ? (n - i0) : GT);
-  const int cols_b = (int)((n - j0) < GN ? (n - j0) : GN);
+  const int64_t ldp = pn_ld(n);
+  // even width: the copy size stays a multiple of 16 bytes (odd n: one
+  // padding column of Pn, zero, rides along)
+  const int cols_b = (int)((ldp - j0) < GN ? (ldp - j0) : GN);
   if (t == 0) {
     mbar_init(&bar, 1);
     fence_barrier_init();
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
     for (int r = lane; r < rows_a; r += 32)
       bulk_g2s(As + r * AS_LD, Cold + (i0 + r) * NB, NB * sizeof(double), &bar);
     for (int r = lane; r < NB; r += 32)
-      bulk_g2s(Bs + r * BS_LD, Pn + r * n + j0, (uint32_t)(cols_b * sizeof(double)), &bar);
+      bulk_g2s(Bs + r * BS_LD, Pn + r * ldp + j0, (uint32_t)(cols_b * sizeof(double)), &bar);
   }
   for (int e = rows_a * AS_LD + t; e < GT * AS_LD; e += 256) As[e] = 0.0;
   if (cols_b < GN)
@@ -204,11 +213,16 @@ __global__ void __launch_bounds__(256, 2) k_gj_gemm(double* A, int64_t n,
     for (int ni = 0; ni < 4; ++ni) {
       const int64_t j = j0 + 32 * wn + 8 * ni + 2 * (lane & 3);
       if (j >= n) continue;
-      double2* cp = reinterpret_cast<double2*>(A + i * n + j);
-      double2 c = *cp;
-      c.x -= acc[mi][ni][0];
-      c.y -= acc[mi][ni][1];
-      *cp = c;
+      if (!(n & 1)) {
+        double2* cp = reinterpret_cast<double2*>(A + i * n + j);
+        double2 c = *cp;
+        c.x -= acc[mi][ni][0];
+        c.y -= acc[mi][ni][1];
+        *cp = c;
+      } else {  // odd n: rows are not 16-byte aligned; column n is padding
+        A[i * n + j] -= acc[mi][ni][0];
+        if (j + 1 < n) A[i * n + j + 1] -= acc[mi][ni][1];
+      }
     }
   }
 }
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(256) k_gj_fix(double* A, int64_t n, int64_t k0
     const int r = (int)(e / n);
     const int64_t j = e % n;
     const bool jK = j >= k0 && j < k0 + nbk;
-    if (j < k0 + nbk) A[(k0 + r) * n + j] = jK ? Dinv[r * nbk + (j - k0)] : Pn[r * n + j];
+    if (j < k0 + nbk) A[(k0 + r) * n + j] = jK ? Dinv[r * nbk + (j - k0)] : Pn[r * pn_ld(n) + j];
   }
   // columns: e -> (i, c); below the pivot block only
   {
@@ -367,13 +381,15 @@ void launch_symv(const int* done, const double* T, int64_t n, const double* x, d
   launch_pdl(k_symv_reduce, dim3((unsigned)((n + 127) / 128)), dim3(128), 0, s, done, P, n, y);
 }
 
-// work per matrix: NB*NB (Dinv) + NB*n (Pn) + n*NB (Cold) + n + NB (pivots)
+// work per matrix: NB*NB (Dinv) + NB*ldp (Pn) + ldp*NB (Cold) + ldp + NB
+// (pivots), ldp = n rounded up to even: every panel starts 16-byte aligned
 static void gj_inverse_impl(double* A, int64_t n, int64_t batch, int64_t sA, double* work,
                             int64_t sW, int* status, cudaStream_t s) {
+  const int64_t ldp = pn_ld(n);
   double* Dinv = work;
   double* Pn = Dinv + NB * NB;
-  double* Cold = Pn + (int64_t)NB * n;
-  double* piv = Cold + n * NB;
+  double* Cold = Pn + (int64_t)NB * ldp;
+  double* piv = Cold + ldp * NB;
   const unsigned B = (unsigned)batch;
   cudaFuncSetAttribute(k_gj_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   const dim3 grid((unsigned)((n + GN - 1) / GN), (unsigned)((n + GT - 1) / GT), B);
@@ -403,11 +419,13 @@ void dense_spd_inverse_batched(double* A, int64_t n, int64_t batch, double* work
 }
 
 // (+ NB: the identity-padded last pivot block writes NB pivots)
-int64_t dense_inverse_work_doubles(int64_t n) { return NB * NB + 2 * (int64_t)NB * n + n + NB; }
+int64_t dense_inverse_work_doubles(int64_t n) {
+  return NB * NB + 2 * (int64_t)NB * pn_ld(n) + pn_ld(n) + NB;
+}
 
 // the n LDL^T pivots of batch matrix z after dense_spd_inverse_batched
 const double* dense_inverse_pivots(const double* work, int64_t n, int64_t z) {
-  return work + z * dense_inverse_work_doubles(n) + NB * NB + 2 * (int64_t)NB * n;
+  return work + z * dense_inverse_work_doubles(n) + NB * NB + 2 * (int64_t)NB * pn_ld(n);
 }
 
 void launch_gemv(const int* done, const double* A, int64_t n, const double* x, double* y,

@@ -124,6 +124,21 @@ enum : int {
   kStatusFloor = 6,  // TMG_SOLVE_TRUE_RESIDUAL: true residual stuck above rtol
 };
 
+// Per-brick exact fine blocks (smoother.cuh): brick b's plane inverses are
+// at G + map[b].slot * PER_BRICK and scale by map[b].scale. Interior bricks
+// whose cells and face halo carry one conductivity k have
+// A_II = face_t(k, k) A_hat, so they share one factor (of a representative
+// uniform brick) scaled by face_t(k_rep, k_rep) / face_t(k, k); every other
+// brick has its own slot and scale 1 ("shared factors").
+struct GSlot {
+  int64_t slot;
+  double scale;
+};
+struct FineFactors {
+  const double* G;
+  const GSlot* map;  // virtual global (indexed by brick)
+};
+
 // Device-resident CG scalars (one per solve context).
 struct PcgState {
   double bnorm, rnorm, rho, alpha, beta, pq, rtol;
@@ -167,15 +182,33 @@ void launch_apply(const GridParams& g, int cb, const double* coef, const double*
                   double* dinv, cudaStream_t s);
 
 // setup_fine.cu
+// factor slot i of G <- brick list[i] (list: nslots bricks)
 void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                          double* G, int* status, cudaStream_t s);
+                          const int64_t* list, int64_t nslots, double* G, int* status,
+                          cudaStream_t s);
 int64_t thomas_doubles_per_brick(int cb);
+// shared factors of uniform bricks: flag[b - b0] = 1 for an interior brick
+// whose cells and face halo have bitwise one conductivity
+void launch_uniform_bricks(const GridParams& g, int cb, const double* kappa, int* flag,
+                           cudaStream_t s);
+// map[b].scale = face_t(k_rep, k_rep) / face_t(k_b, k_b) for the bricks with
+// map[b].slot == 0 && shared, 1 otherwise (slots already set)
+void launch_factor_scales(const GridParams& g, int cb, const double* kappa, const int* flag,
+                          int64_t rep, GSlot* map, cudaStream_t s);
 
 // spectral.cu
 // phi0: previous bases as the initial block (warm start) or nullptr
+// list: the bricks to solve (nlist of them), nullptr = every owned brick
 void launch_local_basis(const GridParams& g, int cb, const double* kappa, const double* phi0,
                         double* phi, double* evals, int* iters, double tol, int degree,
-                        int max_outer, cudaStream_t s);
+                        int max_outer, const int64_t* list, int64_t nlist, cudaStream_t s);
+// bricks of one uniform conductivity inside: flag[b - b0] = 1
+void launch_uniform_inside(const GridParams& g, int cb, const double* kappa, int* flag,
+                           cudaStream_t s);
+// bases of the flagged bricks from the representative's (after its solve)
+void launch_local_basis_share(const GridParams& g, int cb, const double* kappa, const int* flag,
+                              int64_t rep, double* phi, double* evals, int* iters,
+                              cudaStream_t s);
 
 // coarse.cu
 int max_lc();  // largest supported L_c (num_local_basis)
@@ -288,14 +321,14 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    cudaStream_t s);
 // out = add + A_II^{-1} in per brick (per-coarse-cell fine blocks); rdot: also
 // rdot . out -> fin_post (the generic nu-sweep V-cycle)
-void launch_brick_solve(const GridParams& g, int cb, const double* coef, const double* Gf,
+void launch_brick_solve(const GridParams& g, int cb, const double* coef, const FineFactors& Gf,
                         const double* in, const double* add, double* out, const double* rdot,
                         PcgState* st, double* partials, int init, cudaStream_t s);
 // out = add + y over the owned bricks (add nullable); rdot: rdot . out -> fin_post
 void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
                        double* out, const double* rdot, PcgState* st, double* partials, int init,
                        cudaStream_t s);
-void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
+void launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s);
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
@@ -306,7 +339,7 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
 void launch_restrict_bnd(const GridParams& g, int cb, const double* tf, const double* phif,
                          const double* r1f, double* rc, const PcgState* st, cudaStream_t s);
 void launch_post(const GridParams& g, int cb, const double* coef, const double* tf, const double* phi,
-                 const double* phif, const double* Gf, const double* r, const double* r1,
+                 const double* phif, const FineFactors& Gf, const double* r, const double* r1,
                  const double* r1f, const double* ec, double* z, PcgState* st, double* partials,
                  int init, cudaStream_t s);
 // face-major copy of Phi on each stored brick's 6 face layers:
@@ -366,5 +399,49 @@ void launch_prolong_add(const GridParams& g, int cb, const double* phi, const do
                         const double* ec, double* r2, const PcgState* st, cudaStream_t s);
 void launch_resid(const GridParams& g, int cb, const double* coef, const double* r,
                   const double* x, double* t, const PcgState* st, cudaStream_t s);
+
+// generic.cu: any brick shape (cb = 0 at the launchers above; GridParams
+// bx, by, bz give the shape). Fine-block boxes: kind 0 = bricks (one exact
+// block per coarse cell), kind 1 = cc elements (fine_blocks_by_cc).
+void launch_g_coefficients(const GridParams& g, const double* kappa, const uint8_t* dmask,
+                           double* coef, cudaStream_t s);
+// y = A x (absval: |A||x|; x, y nullable), dinv = 1/diag (nullable)
+void launch_g_apply(const GridParams& g, const double* coef, const double* x, double* y,
+                    double* dinv, int absval, cudaStream_t s);
+void launch_g_init(const GridParams& g, const double* coef, const double* b, double* x,
+                   int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s);
+void launch_g_search(const GridParams& g, const double* coef, const double* z, const double* p_old,
+                     double* p, double* q, PcgState* st, double* partials, cudaStream_t s);
+void launch_g_jacobi_step(const GridParams& g, const double* dinv, double* x, const double* p,
+                          const double* q, double* r, double* z, PcgState* st, double* partials,
+                          double* history, int init, int defer, cudaStream_t s);
+void launch_g_resid(const GridParams& g, const double* coef, const double* r, const double* x,
+                    double* t, const PcgState* st, cudaStream_t s);
+void launch_g_prolong_add(const GridParams& g, const double* phi, const double* r1,
+                          const double* ec, double* r2, const PcgState* st, cudaStream_t s);
+void launch_g_add_finish(const GridParams& g, const double* y, const double* add, double* out,
+                         const double* rdot, PcgState* st, double* partials, int init,
+                         cudaStream_t s);
+void launch_g_restrict(const GridParams& g, const double* coef, const double* phi, const double* r,
+                       const double* r1, double* rc, const PcgState* st, cudaStream_t s);
+void launch_g_coarse_blocks(const GridParams& g, const double* kappa, const uint8_t* dmask,
+                            const double* coef, const double* phi, double* Ac, double* Bc,
+                            cudaStream_t s);
+int64_t g_local_basis_scratch_doubles(const GridParams& g);
+void launch_g_local_basis(const GridParams& g, const double* kappa, const double* phi0,
+                          double* phi, double* evals, int* iters, double tol, int degree,
+                          int max_outer, double* scratch, cudaStream_t s);
+// exact block solves on boxes: G plane-major [z][box][P][P] over the owned boxes
+int64_t box_doubles(const GridParams& g, int kind);
+int box_plane_cells(const GridParams& g, int kind);
+int box_apply_kernels(const GridParams& g, int kind);  // plane-step launches (+1 finish)
+int64_t box_factor_work_doubles(const GridParams& g, int kind);
+void launch_box_factor(const GridParams& g, int kind, const double* coef, double* G, int* status,
+                       double* work, cudaStream_t s);
+// out = add + A_box^-1 in (add nullable); rdot: rdot . out -> fin_post;
+// ybuf: one value per owned cell (brick layout, virtual global)
+void launch_box_apply(const GridParams& g, int kind, const double* coef, const double* G,
+                      const double* in, const double* add, double* out, const double* rdot,
+                      PcgState* st, double* partials, int init, double* ybuf, cudaStream_t s);
 
 }  // namespace tmg

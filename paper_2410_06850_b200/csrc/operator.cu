@@ -6,41 +6,42 @@
 
 namespace tmg {
 
-// global x-fastest index of brick-layout slot s
-__device__ __forceinline__ int64_t brick_to_global(const GridParams& g, int cb, int64_t s) {
-  const int c = cb * cb * cb;
+// global x-fastest index of brick-layout slot s (bricks of g.bx x g.by x g.bz
+// cells, x-fastest inside)
+__device__ __forceinline__ int64_t brick_to_global(const GridParams& g, int64_t s) {
+  const int64_t c = brick_cells(g);
   const int64_t b = s / c;
   const int l = (int)(s % c);
   const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
-  const int li = l % cb, lj = (l / cb) % cb, lk = l / (cb * cb);
-  const int64_t i = bi * cb + li, j = bj * cb + lj, k = bk * cb + lk;
+  const int li = l % g.bx, lj = (l / g.bx) % g.by, lk = l / (g.bx * g.by);
+  const int64_t i = bi * g.bx + li, j = bj * g.by + lj, k = bk * g.bz + lk;
   return i + g.nx * (j + g.ny * k);
 }
 
 // src/dst: x-fastest cells of this context's z-slab (global index - xoff).
-__global__ void k_to_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
+__global__ void k_to_brick(GridParams g, const double* __restrict__ src, double* dst,
                            int64_t s0, int64_t m, int64_t xoff) {
   for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x)
-    dst[s] = src[brick_to_global(g, cb, s) - xoff];
+    dst[s] = src[brick_to_global(g, s) - xoff];
 }
 
-__global__ void k_from_brick(GridParams g, int cb, const double* __restrict__ src, double* dst,
+__global__ void k_from_brick(GridParams g, const double* __restrict__ src, double* dst,
                              int64_t s0, int64_t m, int64_t xoff) {
   for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x)
-    dst[brick_to_global(g, cb, s) - xoff] = src[s];
+    dst[brick_to_global(g, s) - xoff] = src[s];
 }
 
 // interpolate_design (grid.cpp:220-241): piecewise-constant prolongation of a
 // field on an (nxl, nyl, nzl) grid by integer factors, into this context's
 // own cells (brick layout).
-__global__ void k_interpolate(GridParams g, int cb, const double* __restrict__ lo, int64_t nxl,
+__global__ void k_interpolate(GridParams g, const double* __restrict__ lo, int64_t nxl,
                               int64_t nyl, int64_t fx, int64_t fy, int64_t fz, double* dst,
                               int64_t s0, int64_t m) {
   for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t gx = brick_to_global(g, cb, s);
+    const int64_t gx = brick_to_global(g, s);
     const int64_t i = gx % g.nx, j = (gx / g.nx) % g.ny, k = gx / (g.nx * g.ny);
     dst[s] = lo[(i / fx) + nxl * ((j / fy) + nyl * (k / fz))];
   }
@@ -97,16 +98,17 @@ __device__ bool dirichlet_value(const GridParams& g, const PatchSet& ps, int64_t
 
 // Per-cell Dirichlet face bits (brick layout) and the rhs
 // b = f*vol + sum_D t_D * T_D in the reference face order (fvm.cpp:63-112).
-__global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __restrict__ kappa,
+__global__ void k_boundary(GridParams g, PatchSet ps, const double* __restrict__ kappa,
                            const double* __restrict__ source, uint8_t* dmask, double* rhs,
                            int64_t s0, int64_t m, unsigned long long* count) {
   for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const int c = cb * cb * cb;
+    const int64_t c = brick_cells(g);
     const int64_t b = s / c;
     const int l = (int)(s % c);
     const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
-    const int64_t i = bi * cb + l % cb, j = bj * cb + (l / cb) % cb, k = bk * cb + l / (cb * cb);
+    const int64_t i = bi * g.bx + l % g.bx, j = bj * g.by + (l / g.bx) % g.by,
+                  k = bk * g.bz + l / (g.bx * g.by);
     unsigned mask = 0;
     double bval = source ? __dmul_rn(source[s], g.vol) : 0.0;
     const bool bnd = i == 0 || j == 0 || k == 0 || i == g.nx - 1 || j == g.ny - 1 || k == g.nz - 1;
@@ -130,19 +132,20 @@ __global__ void k_boundary(GridParams g, int cb, PatchSet ps, const double* __re
 // cell, face by face, in the reference's operation order (no contraction:
 // bitwise). rho = design x, t = state, u = adjoint (brick layout, ghosts of
 // t and u filled), kappa = the system's conductivity.
-__global__ void k_sensitivity(GridParams g, int cb, PatchSet ps, const double* __restrict__ rho,
+__global__ void k_sensitivity(GridParams g, PatchSet ps, const double* __restrict__ rho,
                               const double* __restrict__ kappa, const double* __restrict__ t,
                               const double* __restrict__ u, double kappa_lo, double kappa_hi,
                               double f0, int p, double* grad, int64_t s0, int64_t m) {
-  const int64_t C = (int64_t)cb * cb * cb;
+  const int64_t C = brick_cells(g);
+  const int bd[3] = {g.bx, g.by, g.bz};
   const double dkm = __dsub_rn(kappa_hi, kappa_lo), pd = (double)p;
   for (int64_t s = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < s0 + m;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = s / C;
     const int l = (int)(s % C);
     const int64_t bi = b % g.nbx, bj = (b / g.nbx) % g.nby, bk = b / (g.nbx * g.nby);
-    const int li = l % cb, lj = (l / cb) % cb, lk = l / (cb * cb);
-    const int64_t ijk[3] = {bi * cb + li, bj * cb + lj, bk * cb + lk};
+    const int li = l % g.bx, lj = (l / g.bx) % g.by, lk = l / (g.bx * g.by);
+    const int64_t ijk[3] = {bi * g.bx + li, bj * g.by + lj, bk * g.bz + lk};
     const int64_t n_axis[3] = {g.nx, g.ny, g.nz};
     // material_derivatives (material.cpp:61-74)
     double xp1 = 1.0;
@@ -154,7 +157,7 @@ __global__ void k_sensitivity(GridParams g, int cb, PatchSet ps, const double* _
     double value = __dmul_rn(__dmul_rn(uc, dsrc), g.vol);
     if (dk != 0.0) {
       const double kc = kappa[s];
-      const int st_in[3] = {1, cb, cb * cb};
+      const int st_in[3] = {1, g.bx, g.bx * g.by};
       const int64_t st_b[3] = {1, g.nbx, g.nbx * g.nby};
       const int lc3[3] = {li, lj, lk};
       for (int a = 0; a < 3; ++a) {
@@ -164,9 +167,9 @@ __global__ void k_sensitivity(GridParams g, int cb, PatchSet ps, const double* _
           // neighbour's storage index: inside the brick or across its face
           int64_t ns;
           if (side == 0)
-            ns = lc3[a] > 0 ? s - st_in[a] : (b - st_b[a]) * C + (l + (cb - 1) * st_in[a]);
+            ns = lc3[a] > 0 ? s - st_in[a] : (b - st_b[a]) * C + (l + (bd[a] - 1) * st_in[a]);
           else
-            ns = lc3[a] < cb - 1 ? s + st_in[a] : (b + st_b[a]) * C + (l - (cb - 1) * st_in[a]);
+            ns = lc3[a] < bd[a] - 1 ? s + st_in[a] : (b + st_b[a]) * C + (l - (bd[a] - 1) * st_in[a]);
           const double kf = face_t(kc, kappa[ns]);
           const double ratio = __ddiv_rn(kf, kc);
           const double dt =
@@ -240,28 +243,28 @@ static int grid1d(int64_t m) {
 }
 
 // own cells of the context: brick-layout [b0*C, (b0+nbo)*C); x-fastest slab
-// arrays start at global cell (b0 / (nbx*nby)) * cb * nx * ny
-static int64_t slab_xoff(const GridParams& g, int cb) {
-  return (g.b0 / (g.nbx * g.nby)) * cb * g.nx * g.ny;
+// arrays start at global cell (b0 / (nbx*nby)) * bz * nx * ny
+static int64_t slab_xoff(const GridParams& g) {
+  return (g.b0 / (g.nbx * g.nby)) * g.bz * g.nx * g.ny;
 }
 void launch_to_brick(const GridParams& g, int cb, const double* src, double* dst, cudaStream_t s) {
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
-  k_to_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, g.b0 * C, m, slab_xoff(g, cb));
+  const int64_t C = brick_cells(g), m = g.nbo * C;
+  k_to_brick<<<grid1d(m), 256, 0, s>>>(g, src, dst, g.b0 * C, m, slab_xoff(g));
 }
 void launch_from_brick(const GridParams& g, int cb, const double* src, double* dst,
                        cudaStream_t s) {
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
-  k_from_brick<<<grid1d(m), 256, 0, s>>>(g, cb, src, dst, g.b0 * C, m, slab_xoff(g, cb));
+  const int64_t C = brick_cells(g), m = g.nbo * C;
+  k_from_brick<<<grid1d(m), 256, 0, s>>>(g, src, dst, g.b0 * C, m, slab_xoff(g));
 }
 void launch_interpolate(const GridParams& g, int cb, const double* lo, const int64_t* nlo,
                         double* dst, cudaStream_t s) {
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
-  k_interpolate<<<grid1d(m), 256, 0, s>>>(g, cb, lo, nlo[0], nlo[1], g.nx / nlo[0], g.ny / nlo[1],
+  const int64_t C = brick_cells(g), m = g.nbo * C;
+  k_interpolate<<<grid1d(m), 256, 0, s>>>(g, lo, nlo[0], nlo[1], g.nx / nlo[0], g.ny / nlo[1],
                                           g.nz / nlo[2], dst, g.b0 * C, m);
 }
 void launch_conductivity(const GridParams& g, int cb, const double* x, double* kappa, double lo,
                          double hi, int p, cudaStream_t s) {
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  const int64_t C = brick_cells(g), m = g.nbo * C;
   k_conductivity<<<grid1d(m), 256, 0, s>>>(x, kappa, g.b0 * C, m, lo, hi, p);
 }
 void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
@@ -271,8 +274,8 @@ void launch_boundary(const GridParams& g, int cb, const Patch* patches, int npat
   ps.n = npatch;
   for (int i = 0; i < npatch && i < kMaxPatches; ++i) ps.p[i] = patches[i];
   ps.lx = lx; ps.ly = ly; ps.lz = lz;
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
-  k_boundary<<<grid1d(m), 256, 0, s>>>(g, cb, ps, kappa, source, dmask, rhs, g.b0 * C, m, count);
+  const int64_t C = brick_cells(g), m = g.nbo * C;
+  k_boundary<<<grid1d(m), 256, 0, s>>>(g, ps, kappa, source, dmask, rhs, g.b0 * C, m, count);
 }
 void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int npatch, double lx,
                         double ly, double lz, const double* rho, const double* kappa,
@@ -282,14 +285,16 @@ void launch_sensitivity(const GridParams& g, int cb, const Patch* patches, int n
   ps.n = npatch;
   for (int i = 0; i < npatch && i < kMaxPatches; ++i) ps.p[i] = patches[i];
   ps.lx = lx; ps.ly = ly; ps.lz = lz;
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
-  k_sensitivity<<<grid1d(m), 256, 0, s>>>(g, cb, ps, rho, kappa, t, u, kappa_lo, kappa_hi, f0, p,
+  const int64_t C = brick_cells(g), m = g.nbo * C;
+  k_sensitivity<<<grid1d(m), 256, 0, s>>>(g, ps, rho, kappa, t, u, kappa_lo, kappa_hi, f0, p,
                                           grad, g.b0 * C, m);
 }
 void launch_apply_abs(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                       cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8)
+  if (cb == 0)
+    launch_g_apply(g, coef, x, y, nullptr, 1, s);
+  else if (cb == 8)
     k_apply_abs<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, x, y);
   else
     k_apply_abs<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, x, y);
@@ -297,7 +302,9 @@ void launch_apply_abs(const GridParams& g, int cb, const double* coef, const dou
 void launch_apply(const GridParams& g, int cb, const double* coef, const double* x, double* y,
                   double* dinv, cudaStream_t s) {
   const int64_t M = g.mst;
-  if (cb == 8)
+  if (cb == 0)
+    launch_g_apply(g, coef, x, y, dinv, 0, s);
+  else if (cb == 8)
     k_apply<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, x, y, dinv);
   else
     k_apply<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, x, y, dinv);

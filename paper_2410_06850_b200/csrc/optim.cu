@@ -243,7 +243,8 @@ int mma_partials_doubles() { return 2 * mma_grid() + 8; }
 
 void launch_heat_source(const GridParams& g, int cb, const double* x, double* f, double f0, int p,
                         cudaStream_t s) {
-  const int64_t C = (int64_t)cb * cb * cb, m = g.nbo * C;
+  (void)cb;
+  const int64_t C = brick_cells(g), m = g.nbo * C;
   int64_t b = (m + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
   k_heat_source<<<(unsigned)(b < 1 ? 1 : b), 256, 0, s>>>(x, f, g.b0 * C, m, f0, p);

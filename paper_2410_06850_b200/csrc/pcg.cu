@@ -219,7 +219,7 @@ struct UpdateSmem {
 // brick cells are strided over the threads.
 template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, const double* __restrict__ coef,
-                                                             int64_t M, const double* __restrict__ Gf,
+                                                             int64_t M, const FineFactors Gf,
                                                              double* x, const double* __restrict__ p,
                                                              const double* __restrict__ q, double* r,
                                                              double* r1, double* r1f, PcgState* st,
@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
   extern __shared__ __align__(128) unsigned char smraw[];
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
   const int b = (int)(blockIdx.x + g.b0);
-  const double* G = Gf + (size_t)b * Thomas<CB>::PER_BRICK;
+  const GSlot gsl = Gf.map[b];
+  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
     sm.tv[c] = rv;
     sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
   }
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // r1 = S(r), solver.cpp:280-281
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);  // r1 = S(r), solver.cpp:280-281
   if (TMG_R1_FULL)
     for (int c = t; c < C; c += NT) r1[bofs(b, C) + c] = sm.tv[c];
   // the face layers of r1, face-major: all the boundary-form kernels read
@@ -381,7 +382,7 @@ template <int CB, int LCP>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const double* __restrict__ coef,
                                                            const double* __restrict__ /*tfa*/,
                                                            int64_t M, const double* __restrict__ phi,
-                                                           const double* __restrict__ Gf,
+                                                           const FineFactors Gf,
                                                            const double* __restrict__ r,
                                                            const double* __restrict__ r1,
                                                            const double* __restrict__ ec, double* z,
@@ -391,7 +392,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   extern __shared__ __align__(128) unsigned char smraw[];
   PostSmem<CB>& sm = *reinterpret_cast<PostSmem<CB>*>(smraw);
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
-  const double* G = Gf + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  const GSlot gsl = Gf.map[bc.b];
+  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   if (threadIdx.x == 0)  // warm L2 with the first G planes (constant) before the wait
     prefetch_l2(G, (uint32_t)(2 * Thomas<CB>::PLANE * sizeof(double)));
   pdl_wait();
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   }
   __syncthreads();  // stencil tiles dead: the slots may now be filled
   thomas_prefetch<CB>(sm.th, G);
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);
   double rz = 0.0;
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
@@ -482,7 +484,7 @@ template <int CB, int LCP>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, const double* __restrict__ coef,
                                                                const double* __restrict__ tfa,
                                                                int64_t M, const double* __restrict__ phif,
-                                                               const double* __restrict__ Gf,
+                                                               const FineFactors Gf,
                                                                const double* __restrict__ r,
                                                                const double* __restrict__ r1f,
                                                                const double* __restrict__ ec, double* z,
@@ -492,7 +494,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
   extern __shared__ __align__(128) unsigned char smraw[];
   PostBSmem<CB>& sm = *reinterpret_cast<PostBSmem<CB>*>(smraw);
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
-  const double* G = Gf + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  const GSlot gsl = Gf.map[bc.b];
+  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
       if (axis[k] == ax) sm.tv[cell[k]] += val[k];
   }
   __syncthreads();  // the solve's first step reads plane 0 of t from other threads
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);  // z = A_II^{-1} (r + t), solver.cpp:331-333
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);  // z = A_II^{-1} (r + t), solver.cpp:331-333
   double rz = 0.0;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
@@ -586,7 +589,7 @@ template <int CB>
 __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
                                                                   const double* __restrict__ coef,
                                                                   int64_t M,
-                                                                  const double* __restrict__ Gf,
+                                                                  const FineFactors Gf,
                                                                   const double* __restrict__ in,
                                                                   const double* add, double* out,
                                                                   const double* __restrict__ rdot,
@@ -597,7 +600,8 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
   extern __shared__ __align__(128) unsigned char smraw[];
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
   const int b = (int)(blockIdx.x + g.b0);
-  const double* G = Gf + (size_t)b * Thomas<CB>::PER_BRICK;
+  const GSlot gsl = Gf.map[b];
+  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
     sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
   }
   __syncthreads();
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);
+  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);
   double rz = 0.0;
   for (int c = t; c < C; c += NT) {
     const size_t s = bofs(b, C) + c;
@@ -716,10 +720,11 @@ void init_kernel_attributes() {
 void launch_coefficients(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                          double* coef, cudaStream_t s) {
   const int64_t M = g.mst;
+  if (cb == 0) return launch_g_coefficients(g, kappa, dmask, coef, s);
   if (cb == 8) k_coefficients<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, kappa, dmask, coef, M);
   else k_coefficients<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, dmask, coef, M);
 }
-void launch_brick_solve(const GridParams& g, int cb, const double* coef, const double* Gf,
+void launch_brick_solve(const GridParams& g, int cb, const double* coef, const FineFactors& Gf,
                         const double* in, const double* add, double* out, const double* rdot,
                         PcgState* st, double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
@@ -738,6 +743,7 @@ void launch_face_t(const GridParams& g, int cb, const double* coef, double* tf, 
 void launch_init(const GridParams& g, int cb, const double* coef, const double* b, double* x,
                  int has_x0, double* r, PcgState* st, double* partials, cudaStream_t s) {
   const int64_t M = g.mst;
+  if (cb == 0) return launch_g_init(g, coef, b, x, has_x0, r, st, partials, s);
   if (cb == 8) k_init<8><<<(unsigned)g.nbo, 512, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
   else k_init<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, coef, M, b, x, has_x0, r, st, partials);
 }
@@ -745,10 +751,11 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s) {
   const int64_t M = g.mst;
+  if (cb == 0) return launch_g_search(g, coef, z, p_old, p, q, st, partials, s);
   if (cb == 8) launch_pdl(k_search<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, z, p_old, p, q, st, partials);
   else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, coef, M, z, p_old, p, q, st, partials);
 }
-void launch_update(const GridParams& g, int cb, const double* coef, const double* Gf, double* x,
+void launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s) {
   const int64_t M = g.mst;
@@ -759,6 +766,7 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
                      const double* r, const double* r1, double* rc, const PcgState* st,
                      cudaStream_t s) {
   const int64_t M = g.mst;
+  if (cb == 0) return launch_g_restrict(g, coef, phi, r, r1, rc, st, s);
   lc_dispatch(g.lc, [&](auto L) {
     constexpr int LCP = decltype(L)::value;
     if (cb == 8) launch_pdl(k_restrict<8, LCP>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, phi, r, r1, rc, st);
@@ -797,7 +805,7 @@ void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* ph
   });
 }
 void launch_post(const GridParams& g, int cb, const double* coef, const double* tf,
-                 const double* phi_full, const double* phif, const double* Gf, const double* r,
+                 const double* phi_full, const double* phif, const FineFactors& Gf, const double* r,
                  const double* r1_full, const double* r1f, const double* ec, double* z, PcgState* st,
                  double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
@@ -812,6 +820,8 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,
                         double* history, int init, int defer, cudaStream_t s) {
+  if (cb == 0)
+    return launch_g_jacobi_step(g, dinv, x, p, q, r, z, st, partials, history, init, defer, s);
   if (cb == 8) launch_pdl(k_jacobi_step<8>, dim3((unsigned)g.nbo), dim3(512), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init, defer);
   else launch_pdl(k_jacobi_step<4>, dim3((unsigned)g.nbo), dim3(64), 0, s, g, dinv, x, p, q, r, z, st, partials, history, init, defer);
 }

@@ -15,6 +15,7 @@ template <int CB>
 __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridParams g,
                                                                const double* __restrict__ kappa,
                                                                const uint8_t* __restrict__ dmask,
+                                                               const int64_t* __restrict__ list,
                                                                double* G, int* status) {
   constexpr int P = Thomas<CB>::P, C = CB * CB * CB, NTF = factor_threads<CB>();
   constexpr int GP = P + 1;        // padded row stride of Gprev (conflict-free transpose)
@@ -29,7 +30,7 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
   double* ty = tx + C;             // C
   double* tzb = ty + C;            // C  T to the cell one plane below (0 for lk=0)
   __shared__ double red[64];
-  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  const BrickCoord bc = brick_coord(g, (int)list[blockIdx.x]);  // factor slot blockIdx.x
   load_tile<CB, true>(kappa, kt, g, bc);
   __syncthreads();
   tile_faces<CB>(kt, fx, fy, fz, g, bc);
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
     tzb[c] = lk > 0 ? fs.t[4] : 0.0;
   }
   __syncthreads();
-  double* Gout = G + (size_t)bc.b * Thomas<CB>::PER_BRICK;
+  double* Gout = G + (size_t)blockIdx.x * Thomas<CB>::PER_BRICK;
   // Register-resident Gauss-Jordan per plane (gj.cuh)
   using L = GjLayout<P, NTF>;
   constexpr int CW = L::CW, RH = L::RH;
@@ -133,17 +134,78 @@ size_t thomas_smem_bytes(int cb) {
 }
 
 void launch_thomas_factor(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
-                          double* G, int* status, cudaStream_t s) {
+                          const int64_t* list, int64_t nslots, double* G, int* status,
+                          cudaStream_t s) {
   const size_t smem = thomas_smem_bytes(cb);
+  if (nslots < 1) return;
   if (cb == 8) {
-    cudaFuncSetAttribute(k_thomas_factor<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<8><<<(unsigned)g.nbo, factor_threads<8>(), smem, s>>>(g, kappa, dmask, G,
-                                                                          status);
+    ensure_dyn_smem(k_thomas_factor<8>, smem);
+    k_thomas_factor<8><<<(unsigned)nslots, factor_threads<8>(), smem, s>>>(g, kappa, dmask, list,
+                                                                           G, status);
   } else {
-    cudaFuncSetAttribute(k_thomas_factor<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_thomas_factor<4><<<(unsigned)g.nbo, factor_threads<4>(), smem, s>>>(g, kappa, dmask, G,
-                                                                          status);
+    ensure_dyn_smem(k_thomas_factor<4>, smem);
+    k_thomas_factor<4><<<(unsigned)nslots, factor_threads<4>(), smem, s>>>(g, kappa, dmask, list,
+                                                                           G, status);
   }
+}
+
+// An interior brick (all six neighbours exist) whose cells and six face halo
+// layers carry bitwise the same conductivity k: every face T is
+// face_t(k, k) * area/h and A_II = face_t(k, k) A_hat with A_hat fixed.
+template <int CB>
+__global__ void __launch_bounds__(256) k_uniform_bricks(GridParams g,
+                                                       const double* __restrict__ kappa,
+                                                       int* flag) {
+  constexpr int C = CB * CB * CB;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  __shared__ int same;
+  const bool interior = bc.bi > 0 && bc.bj > 0 && bc.bk > 0 && bc.bi + 1 < g.nbx &&
+                        bc.bj + 1 < g.nby && bc.bk + 1 < g.nbz;
+  if (threadIdx.x == 0) same = interior ? 1 : 0;
+  __syncthreads();
+  if (!interior) {
+    if (threadIdx.x == 0) flag[blockIdx.x] = 0;
+    return;
+  }
+  const double k0 = kappa[bofs(bc.b, C)];
+  bool ok = true;
+  for (int t = threadIdx.x; t < C; t += blockDim.x) ok = ok && kappa[bofs(bc.b, C) + t] == k0;
+  for (int h = threadIdx.x; h < 6 * CB * CB; h += blockDim.x) {
+    int f, ti, nl;
+    halo_slot<CB>(h, f, ti, nl);
+    ok = ok && kappa[bofs(nbr_brick(g, bc, f), C) + nl] == k0;
+  }
+  if (!ok) same = 0;  // benign race: every writer stores 0
+  __syncthreads();
+  if (threadIdx.x == 0) flag[blockIdx.x] = same;
+}
+
+void launch_uniform_bricks(const GridParams& g, int cb, const double* kappa, int* flag,
+                           cudaStream_t s) {
+  if (cb == 8) k_uniform_bricks<8><<<(unsigned)g.nbo, 256, 0, s>>>(g, kappa, flag);
+  else k_uniform_bricks<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, flag);
+}
+
+template <int CB>
+__global__ void k_factor_scales(GridParams g, const double* __restrict__ kappa,
+                                const int* __restrict__ flag, int64_t rep, GSlot* map) {
+  constexpr int C = CB * CB * CB;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= g.nbo) return;
+  const int64_t b = g.b0 + i;
+  double sc = 1.0;
+  if (flag[i] && b != rep) {
+    const double kr = kappa[rep * C], kb = kappa[b * C];
+    sc = face_t(kr, kr) / face_t(kb, kb);
+  }
+  map[b].scale = sc;
+}
+
+void launch_factor_scales(const GridParams& g, int cb, const double* kappa, const int* flag,
+                          int64_t rep, GSlot* map, cudaStream_t s) {
+  const unsigned grid = (unsigned)((g.nbo + 255) / 256);
+  if (cb == 8) k_factor_scales<8><<<grid, 256, 0, s>>>(g, kappa, flag, rep, map);
+  else k_factor_scales<4><<<grid, 256, 0, s>>>(g, kappa, flag, rep, map);
 }
 
 int64_t thomas_doubles_per_brick(int cb) {

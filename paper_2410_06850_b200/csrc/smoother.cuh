@@ -235,9 +235,12 @@ __device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm) {
 // Thread i < P reads t[i] before the first __syncthreads: plane 0 of t must
 // be complete (written by thread i itself, or published by a caller barrier).
 // Ends with a __syncthreads.
+// scale: every plane mat-vec result is multiplied by it (the shared factor
+// of a uniform brick, FineFactors; 1.0 leaves the solve bitwise unchanged).
 template <int CB>
 __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* __restrict__ G,
-                                             const double* t, const double* tz, double* x) {
+                                             const double* t, const double* tz, double* x,
+                                             double scale = 1.0) {
   constexpr int P = Thomas<CB>::P, NL = Thomas<CB>::NL, NBK = Thomas<CB>::NBK;
   const int tid = threadIdx.x;
   const MvRole<CB> m = mv_role<CB>();
@@ -276,7 +279,7 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
       for (int w = 1; w < NBK; w *= 2)  // fixed pairwise tree
 #pragma unroll
         for (int s = 0; s + w < NBK; s += 2 * w) pr[s] += pr[s + w];
-      const double acc = pr[0];
+      const double acc = pr[0] * scale;
       double* wn = sm.w2[(n + 1) & 1];
       const int row = tid;
       if (n < CB) {  // forward: u_k = G_k w_k ; w_{k+1} = t_{k+1} + Tz_{k+1} u_k

@@ -131,6 +131,7 @@ EXPORTED_SYMBOLS = (
     "tmg_assemble_rhs", "tmg_setup", "tmg_pcg", "tmg_apply_operator",
     "tmg_apply_preconditioner", "tmg_upload_rhs", "tmg_upload_x0", "tmg_solve_resident",
     "tmg_download_solution", "tmg_get_local_bases", "tmg_get_coarse_operator",
+    "tmg_get_fine_factor_slots",
     "tmg_get_cc_restriction", "tmg_get_sizes", "tmg_profile_solve", "tmg_device_bytes",
     "tmg_stream", "tmg_kernel_launches", "tmg_create_slabs", "tmg_nccl_unique_id",
     "tmg_create_dist", "tmg_partition", "tmg_set_x0_interpolated", "tmg_set_design_interpolated",
@@ -594,6 +595,13 @@ class Context:
 
     def device_bytes(self):
         return native().tmg_device_bytes(self._p)
+
+    def fine_factor_slots(self):
+        """(factor slots, bricks) of the per-coarse-cell fine blocks: uniform
+        interior bricks share one scaled factor."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(native().tmg_get_fine_factor_slots(self._p, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def stream(self):
         return native().tmg_stream(self._p)

@@ -160,16 +160,16 @@ def test_hierarchy_variant_limits():
     c = ctx_for(n, 1, 8, kappa)  # q = 2048
     with pytest.raises(NotSupportedError, match="two_grid"):
         c.setup("two_grid", CELL)
-    c = ctx_for(64, 1, 8, problem(64, 1e-3)[1])  # 64^3-cell cc elements
+    c = ctx_for(128, 1, 16, problem(128, 1e-3)[1])  # 128^3-cell cc elements
     with pytest.raises(NotSupportedError, match="coarse_cell"):
-        c.setup("mmg")  # the reference default partition: factors of 8.6 GB per element
+        c.setup("mmg")  # the reference default partition: z planes of 16384 cells
 
 
 def test_block_jacobi_limits():
-    n = 64
+    n = 128
     _, kappa = problem(n, 1e-3)
-    c = ctx_for(n, 1, 8, kappa)  # 64^3-cell blocks
-    with pytest.raises(NotSupportedError, match="block_jacobi"):
+    c = ctx_for(n, 1, 16, kappa)  # 128^3-cell blocks
+    with pytest.raises(NotSupportedError, match="z planes"):
         c.setup("block_jacobi")
 
 

@@ -233,6 +233,22 @@ def test_live_reference_solve(kind, fb, cb):
 
 
 @needs_ref
+def test_lanczos_restatement_vs_reference():
+    """Boxes above dense_threshold = 4096 cells (17^3 = 4913): the restated
+    lanczos_smallest (coarse_space.cpp:61-198) against the reference's own,
+    same Lcg64 start, same descending slot order"""
+    n = 34
+    kappa = inputs.conductivity(inputs.box_filter_design(n, 0.3), 1e-3)
+    v_ref, V_ref = O.ref_local_basis_grid((n, n, n), 1, 2, kappa, 3, 4)
+    v, V = O.local_basis(O.hierarchy(O.grid(n), 1, 2), kappa, 3, 4)
+    assert np.all(np.diff(v_ref) <= 0) and np.all(np.diff(v) <= 0)
+    np.testing.assert_allclose(v, v_ref, rtol=0, atol=1e-9 * v_ref.max())
+    for a in range(4):
+        cosang = abs(V[a] @ V_ref[a]) / (np.linalg.norm(V[a]) * np.linalg.norm(V_ref[a]))
+        assert cosang >= 1 - 1e-9, (a, cosang)
+
+
+@needs_ref
 def test_live_reference_warm_start_x0():
     # pcg(..., x0) (solver.cpp:485,515-516): same x0 -> same iterations
     n = 16
