@@ -1374,6 +1374,7 @@ int tmg_halo_plan(const tmg_grid* grid, int nranks, int rank, int elem, int64_t*
 void tmg_destroy(tmg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);  // no kernel may outlive its buffers
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->comm) ncclCommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);

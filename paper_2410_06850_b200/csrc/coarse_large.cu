@@ -332,6 +332,8 @@ __device__ void apply_projected(const GridParams& g, const ElemCoord& ec, const 
 }
 }  // namespace
 
+constexpr int kRREvery = 4;
+
 // One CTA (256 threads) per element. X, Y, Z (q x KS each) in shared memory,
 // or in gscr (3 q KS doubles per element) when they do not fit (q > 256).
 template <int KS>
@@ -376,64 +378,68 @@ __global__ void __launch_bounds__(256) k_cc_subspace(GridParams g, const double*
     // sweeps); SVQB for a pass whose Gram matrix is not numerically PD
     if (!cholqr_pass<KS>(Y, X, q, T, F, &flag)) svqb_pass<KS>(Y, X, q, T, V, F, dsc, red);
     if (!cholqr_pass<KS>(X, X, q, T, F, &flag)) svqb_pass<KS>(X, X, q, T, V, F, dsc, red);
-    // Rayleigh-Ritz on H
-    apply_projected<KS>(g, ec, Ac, Bc, X, Z, q);
-    __syncthreads();
-    gram<KS>(X, Z, q, T, true);
-    block_jacobi<KS>(T, V, red);
-    if (t == 0) {  // ascending, ties by index
-      unsigned used = 0;
-      for (int k = 0; k < KS; ++k) {
-        int best = -1;
-        for (int i = 0; i < KS; ++i)
-          if (!(used >> i & 1u) && (best < 0 || T[i * (KS + 1)] < T[best * (KS + 1)])) best = i;
-        used |= 1u << best;
-        perm[k] = best;
-        th[k] = T[best * (KS + 1)];
+    // Rayleigh-Ritz on H and the convergence test every kRREvery steps (the
+    // iteration itself only needs the orthonormalised block; the Ritz pairs
+    // are read out at the end)
+    if ((it % kRREvery == kRREvery - 1) || it + 1 >= maxit) {
+      apply_projected<KS>(g, ec, Ac, Bc, X, Z, q);
+      __syncthreads();
+      gram<KS>(X, Z, q, T, true);
+      block_jacobi<KS>(T, V, red);
+      if (t == 0) {  // ascending, ties by index
+        unsigned used = 0;
+        for (int k = 0; k < KS; ++k) {
+          int best = -1;
+          for (int i = 0; i < KS; ++i)
+            if (!(used >> i & 1u) && (best < 0 || T[i * (KS + 1)] < T[best * (KS + 1)])) best = i;
+          used |= 1u << best;
+          perm[k] = best;
+          th[k] = T[best * (KS + 1)];
+        }
       }
-    }
-    __syncthreads();
-    for (int r = t; r < q; r += nt) {
-      double xr[KS], zr[KS];
-#pragma unroll
-      for (int i = 0; i < KS; ++i) {
-        xr[i] = X[r * KS + i];
-        zr[i] = Z[r * KS + i];
-      }
-#pragma unroll
-      for (int k = 0; k < KS; ++k) {
-        const int pk = perm[k];
-        double xs = 0.0, zs = 0.0;
-#pragma unroll
+      __syncthreads();
+      for (int r = t; r < q; r += nt) {
+        double xr[KS], zr[KS];
+  #pragma unroll
         for (int i = 0; i < KS; ++i) {
-          xs = fma(xr[i], V[i * KS + pk], xs);
-          zs = fma(zr[i], V[i * KS + pk], zs);
+          xr[i] = X[r * KS + i];
+          zr[i] = Z[r * KS + i];
         }
-        X[r * KS + k] = xs;
-        Z[r * KS + k] = zs;
+  #pragma unroll
+        for (int k = 0; k < KS; ++k) {
+          const int pk = perm[k];
+          double xs = 0.0, zs = 0.0;
+  #pragma unroll
+          for (int i = 0; i < KS; ++i) {
+            xs = fma(xr[i], V[i * KS + pk], xs);
+            zs = fma(zr[i], V[i * KS + pk], zs);
+          }
+          X[r * KS + k] = xs;
+          Z[r * KS + k] = zs;
+        }
       }
+      __syncthreads();
+      // residual norms of the wanted pairs: 16 lanes per column
+      for (int k0 = 0; k0 < KS; k0 += nt >> 4) {
+        const int k = k0 + (t >> 4), part = t & 15;
+        double s = 0.0;
+        if (k < KS)
+          for (int r = part; r < q; r += 16) {
+            const double d = Z[r * KS + k] - th[k] * X[r * KS + k];
+            s = fma(d, d, s);
+          }
+        for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (k < KS && part == 0) res[k] = sqrt(s);
+      }
+      __syncthreads();
+      if (t == 0) {
+        int ok = 1;
+        for (int k = 0; k < g.lcc; ++k) ok &= res[k] <= thr;
+        flag = ok;
+      }
+      __syncthreads();
+      if (flag || it + 1 >= maxit) break;
     }
-    __syncthreads();
-    // residual norms of the wanted pairs: 16 lanes per column
-    for (int k0 = 0; k0 < KS; k0 += nt >> 4) {
-      const int k = k0 + (t >> 4), part = t & 15;
-      double s = 0.0;
-      if (k < KS)
-        for (int r = part; r < q; r += 16) {
-          const double d = Z[r * KS + k] - th[k] * X[r * KS + k];
-          s = fma(d, d, s);
-        }
-      for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (k < KS && part == 0) res[k] = sqrt(s);
-    }
-    __syncthreads();
-    if (t == 0) {
-      int ok = 1;
-      for (int k = 0; k < g.lcc; ++k) ok &= res[k] <= thr;
-      flag = ok;
-    }
-    __syncthreads();
-    if (flag || it + 1 >= maxit) break;
     // Y = Hs X (Hs symmetric: column r read coalesced)
     for (int r = t; r < q; r += nt) {
       double acc[KS];
