@@ -280,9 +280,18 @@ def run_reference(args):
 #  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8*SURF     = 348.6
 #  k_restrict: (Phi 32 + r1 8)*SURF + T 3                              = 26.1
 #  k_search: coef 32 + z 8 + p 16 + q 8                                 = 64
+# G counts only the distinct factors (x slots / bricks): uniform interior
+# bricks share one factor, whose planes stay in L2.
 SURF = 296 / 512
-KERNEL_BYTES_PER_CELL = {"post": 312 + 40 * SURF + 3, "update": 344 + 8 * SURF, "search": 64,
-                         "restrict": 40 * SURF + 3}
+
+
+def kernel_bytes_per_cell(g_fraction=1.0):
+    g = 288 * g_fraction
+    return {"post": 24 + g + 40 * SURF + 3, "update": 56 + g + 8 * SURF, "search": 64,
+            "restrict": 40 * SURF + 3}
+
+
+KERNEL_BYTES_PER_CELL = kernel_bytes_per_cell()
 ITER_BYTES_PER_CELL = sum(KERNEL_BYTES_PER_CELL.values())  # + coarse levels (~0.1%)
 
 
@@ -514,14 +523,18 @@ def run_ours(args):
             peak = float(json.load(f)["hbm_gbs"])
     except Exception:
         peak, peak_src = 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
-    iter_achieved = ITER_BYTES_PER_CELL * M_local * iters / (ms * 1e-3) / 1e9  # per GPU
+    slots, bricks = ctx.fine_factor_slots()
+    gfrac = slots / bricks if bricks else 1.0
+    kbytes = kernel_bytes_per_cell(gfrac)
+    iter_bytes = sum(kbytes.values())
+    iter_achieved = iter_bytes * M_local * iters / (ms * 1e-3) / 1e9  # per GPU
     if world == 1:
         # per-kernel CUDA-event times during one live solve, on the context's
         # stream (roofline)
         prof = ctx.profile_solve(RTOL, 10000)
         per = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
         dominant = max(("post", "update", "search", "restrict"), key=lambda k: prof[k][0])
-        bytes_launch = KERNEL_BYTES_PER_CELL[dominant] * M
+        bytes_launch = kbytes[dominant] * M
         achieved = bytes_launch / (per[dominant] * 1e-3) / 1e9
         tr = ncu_traffic(dominant, args.config, M)
         roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
@@ -529,7 +542,8 @@ def run_ours(args):
                 "traffic": tr["bytes"] if tr else None,
                 "traffic_source": tr["source"] if tr else "no ncu capture of this config",
                 "algorithmic_bytes_per_launch": bytes_launch,
-                "algorithmic_bytes_per_cell": KERNEL_BYTES_PER_CELL[dominant],
+                "algorithmic_bytes_per_cell": kbytes[dominant],
+                "fine_factor_slots_per_brick": gfrac,
                 "peak_source": peak_src,
                 "kernel_share_of_iteration": prof[dominant][0] / sum(
                     v[0] for k, v in prof.items() if k in ("post", "update", "search",
@@ -539,7 +553,7 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": "whole iteration, per GPU (incl. exchanges)",
                 "achieved": iter_achieved, "peak": peak, "unit": "GB/s",
                 "frac": iter_achieved / peak, "traffic": None,
-                "algorithmic_bytes_per_launch": ITER_BYTES_PER_CELL * M_local,
+                "algorithmic_bytes_per_launch": iter_bytes * M_local,
                 "peak_source": peak_src}
 
     extra = None
@@ -576,7 +590,7 @@ def run_ours(args):
                                 "time_to_true_rtol_ms": 1e3 * (setup_s + ver_s)},
         "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items() if v},
         "iteration_hbm_gbs_algorithmic_per_gpu": iter_achieved,
-        "iteration_bytes_per_cell": ITER_BYTES_PER_CELL,
+        "iteration_bytes_per_cell": iter_bytes,
         "device_bytes_per_gpu": ctx.device_bytes()})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

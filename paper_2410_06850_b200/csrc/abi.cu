@@ -262,31 +262,62 @@ int set_err(tmg_ctx* c, int code, const char* fmt, ...) {
     }                                                                                   \
   } while (0)
 
+// Every pointer the context hands out is a handle dfree() must map back to
+// one allocation: a plain allocation's address, or a windowed array's
+// virtual base (allocation - offset, `virt`). The two sets never overlap: an
+// address that equals a live virtual base is not handed out as a plain
+// allocation, and a window whose virtual base equals another allocation's
+// address is moved (otherwise freeing one array would release the other's
+// storage to the pool while it is still in use).
+void dfree(tmg_ctx* c, void* p);
+
 template <typename T>
 T* dalloc(tmg_ctx* c, int64_t n) {
-  void* p = nullptr;
   const size_t bytes = sizeof(T) * (size_t)std::max<int64_t>(n, 1);
-  for (size_t i = 0; i < c->pool.size(); ++i)
-    if (c->pool[i].second == bytes) {
-      p = c->pool[i].first;
-      c->pool.erase(c->pool.begin() + (std::ptrdiff_t)i);
-      c->allocs.push_back(p);
-      return (T*)p;
+  std::vector<void*> aside;
+  void* p = nullptr;
+  for (;;) {
+    p = nullptr;
+    for (size_t i = 0; i < c->pool.size(); ++i)
+      if (c->pool[i].second == bytes && !c->virt.count(c->pool[i].first)) {
+        p = c->pool[i].first;
+        c->pool.erase(c->pool.begin() + (std::ptrdiff_t)i);
+        break;
+      }
+    if (!p) {
+      CK(cudaMalloc(&p, bytes));
+      c->sizes[p] = bytes;
+      c->bytes += (int64_t)bytes;
     }
-  CK(cudaMalloc(&p, bytes));
+    if (!c->virt.count(p)) break;
+    aside.push_back(p);  // a windowed array's handle: not usable as a plain one
+  }
+  for (void* q : aside) c->pool.emplace_back(q, c->sizes[q]);
   c->allocs.push_back(p);
-  c->sizes[p] = bytes;
-  c->bytes += (int64_t)bytes;
   return (T*)p;
+}
+
+// windowed allocation of n elements addressed as (virtual base + i), i in
+// [off, off + n)
+template <typename T>
+T* wwindow(tmg_ctx* c, int64_t n, int64_t off) {
+  std::vector<T*> aside;
+  for (;;) {
+    T* a = dalloc<T>(c, n + (int64_t)aside.size());  // a new size: not a pooled twin
+    T* v = a - off;
+    if (!c->virt.count((void*)v) && (v == a || !c->sizes.count((void*)v))) {
+      for (T* q : aside) dfree(c, (void*)q);
+      c->virt[(void*)v] = (void*)a;
+      return v;
+    }
+    aside.push_back(a);
+  }
 }
 
 // windowed allocation: `units` stored, first stored global unit `first`
 template <typename T>
 T* walloc(tmg_ctx* c, int64_t units, int64_t per, int64_t first) {
-  T* a = dalloc<T>(c, units * per);
-  T* v = a - first * per;
-  c->virt[(void*)v] = (void*)a;
-  return v;
+  return wwindow<T>(c, units * per, first * per);
 }
 template <typename T>
 T* ghosted(tmg_ctx* c, const Slab& s, int64_t per) { return walloc<T>(c, s.nbs, per, s.bs0); }
@@ -538,9 +569,9 @@ int finish_problem(tmg_ctx* c) {
 }
 
 // Factor slots of the per-brick exact fine blocks (FineFactors): interior
-// bricks of one uniform conductivity (cells and face halo) share the factor
-// of the first such brick, scaled; every other brick gets its own slot.
-// TMG_G_SHARE=0 gives every brick its own slot (A/B diagnostics).
+// bricks of one uniform conductivity (cells and face halo) need no factor
+// (slot -1, fast diagonalisation with scale 1 / face_t(k, k)); every other
+// brick gets its own slot. TMG_G_SHARE=0 gives every brick a slot (A/B).
 void plan_fine_factors(tmg_ctx* c, Slab& s) {
   const char* e = getenv("TMG_G_SHARE");
   const bool share = !(e && e[0] == '0');
@@ -554,16 +585,12 @@ void plan_fine_factors(tmg_ctx* c, Slab& s) {
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
   }
-  int64_t repb = -1;
-  for (int64_t i = 0; i < nbo && repb < 0; ++i)
-    if (flag[(size_t)i]) repb = s.g.b0 + i;
   std::vector<GSlot> map((size_t)nbo);
   std::vector<int64_t> list;
   list.reserve((size_t)nbo);
-  if (repb >= 0) list.push_back(repb);  // slot 0: the shared factor
   for (int64_t i = 0; i < nbo; ++i) {
     if (flag[(size_t)i]) {
-      map[(size_t)i] = GSlot{0, 1.0};
+      map[(size_t)i] = GSlot{-1, 1.0};
     } else {
       map[(size_t)i] = GSlot{(int64_t)list.size(), 1.0};
       list.push_back(s.g.b0 + i);
@@ -571,12 +598,13 @@ void plan_fine_factors(tmg_ctx* c, Slab& s) {
   }
   s.nslots = (int64_t)list.size();
   s.gmap = owned<GSlot>(c, s, 1);
-  s.flist = dalloc<int64_t>(c, s.nslots);
+  s.flist = dalloc<int64_t>(c, std::max<int64_t>(s.nslots, 1));
   CK(cudaMemcpyAsync(s.gmap + s.g.b0, map.data(), sizeof(GSlot) * (size_t)nbo,
                      cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(s.flist, list.data(), sizeof(int64_t) * (size_t)s.nslots,
-                     cudaMemcpyHostToDevice, c->stream));
-  if (repb >= 0 && share) launch_factor_scales(s.g, c->cb, s.kappa, dflag, repb, s.gmap, c->stream);
+  if (s.nslots)
+    CK(cudaMemcpyAsync(s.flist, list.data(), sizeof(int64_t) * (size_t)s.nslots,
+                       cudaMemcpyHostToDevice, c->stream));
+  if (share) launch_factor_scales(s.g, c->cb, s.kappa, dflag, s.gmap, c->stream);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(c->stream));  // the host vectors die here
   dfree(c, dflag);
@@ -1249,11 +1277,7 @@ int create_impl(const tmg_grid* grid, int device, int first, int count, int tota
       s.g.mst = s.nbs * C;
       s.kappa = ghosted<double>(c, s, C);
       s.dmask = ghosted<uint8_t>(c, s, C);
-      {
-        double* a = dalloc<double>(c, 4 * s.g.mst);
-        s.coef = a - s.bs0 * C;
-        c->virt[(void*)s.coef] = (void*)a;
-      }
+      s.coef = wwindow<double>(c, 4 * s.g.mst, s.bs0 * C);
       for (double** v : {&s.b, &s.x, &s.r, &s.q, &s.z, &s.r1}) *v = ghosted<double>(c, s, C);
       s.pbuf[0] = ghosted<double>(c, s, C);
       s.pbuf[1] = ghosted<double>(c, s, C);
@@ -2174,7 +2198,7 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
           if (bj_apply_kernels((int)c->cb, c->g.sd) > 1) s.ybj = owned<double>(c, s, C);
         } else {
           plan_fine_factors(c, s);
-          s.Gf = dalloc<double>(c, s.nslots * thomas_doubles_per_brick(c->cb));
+          s.Gf = dalloc<double>(c, std::max<int64_t>(s.nslots, 1) * thomas_doubles_per_brick(c->cb));
         }
         if (fine_bj || o->smoother_sweeps != 1 || gen) {  // unfused V-cycles
           s.r2 = ghosted<double>(c, s, C);
@@ -2218,8 +2242,9 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
                                degree, max_outer, w, c->stream);
           if (w) dfree(c, w);  // stream-ordered reuse only
         } else {
-          // bricks of one uniform conductivity share one eigensolve (their
-          // local problems are scalar multiples, spectral.cu); TMG_EIG_SHARE=0: off
+          // bricks of one conductivity inside get their bases in closed form
+          // (separable modes, k_local_basis_uniform); the eigensolver runs on
+          // the others. TMG_EIG_SHARE=0: every brick through the eigensolver
           const char* es = getenv("TMG_EIG_SHARE");
           const bool share = !(es && es[0] == '0');
           std::vector<int> flag((size_t)s.g.nbo, 0);
@@ -2231,21 +2256,17 @@ int tmg_setup(tmg_ctx* c, const tmg_mmg_options* o) {
                                cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
           }
-          int64_t repb = -1;
           std::vector<int64_t> list;
-          for (int64_t i = 0; i < s.g.nbo; ++i) {
-            if (flag[(size_t)i] && repb >= 0) continue;
-            if (flag[(size_t)i]) repb = s.g.b0 + i;
-            list.push_back(s.g.b0 + i);
-          }
+          for (int64_t i = 0; i < s.g.nbo; ++i)
+            if (!flag[(size_t)i]) list.push_back(s.g.b0 + i);
           int64_t* dlist = dalloc<int64_t>(c, (int64_t)list.size());
           CK(cudaMemcpyAsync(dlist, list.data(), sizeof(int64_t) * list.size(),
                              cudaMemcpyHostToDevice, c->stream));
           launch_local_basis(s.g, c->cb, s.kappa, phi_prev[k], s.phi, s.evals, s.eig_iters, tol,
                              degree, max_outer, dlist, (int64_t)list.size(), c->stream);
-          if (repb >= 0)
-            launch_local_basis_share(s.g, c->cb, s.kappa, dflag, repb, s.phi, s.evals,
-                                     s.eig_iters, c->stream);
+          if (share)
+            launch_local_basis_uniform(s.g, c->cb, s.kappa, dflag, s.phi, s.evals, s.eig_iters,
+                                       c->stream);
           CK(cudaGetLastError());
           CK(cudaStreamSynchronize(c->stream));  // list lives on the host stack
           dfree(c, dlist);

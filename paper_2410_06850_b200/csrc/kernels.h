@@ -111,7 +111,12 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  launch_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) {  // name the kernel (with CUDA_LAUNCH_BLOCKING=1: the faulting one)
+    const char* name = nullptr;
+    if (cudaFuncGetName(&name, (const void*)kernel) != cudaSuccess || !name) name = "?";
+    launch_check(e, (std::string("kernel launch ") + name).c_str());
+  }
 }
 
 enum : int {
@@ -125,11 +130,11 @@ enum : int {
 };
 
 // Per-brick exact fine blocks (smoother.cuh): brick b's plane inverses are
-// at G + map[b].slot * PER_BRICK and scale by map[b].scale. Interior bricks
-// whose cells and face halo carry one conductivity k have
-// A_II = face_t(k, k) A_hat, so they share one factor (of a representative
-// uniform brick) scaled by face_t(k_rep, k_rep) / face_t(k, k); every other
-// brick has its own slot and scale 1 ("shared factors").
+// at G + map[b].slot * PER_BRICK (scale 1). Interior bricks whose cells and
+// face halo carry one conductivity k have A_II = face_t(k, k) A_hat with
+// A_hat = sum over axes of (area/h) times the 1-D Dirichlet Laplacian: they
+// store no factor (slot -1) and are solved by fast diagonalisation with
+// scale 1 / face_t(k, k) (smoother.cuh, brick_inverse).
 struct GSlot {
   int64_t slot;
   double scale;
@@ -191,10 +196,10 @@ int64_t thomas_doubles_per_brick(int cb);
 // whose cells and face halo have bitwise one conductivity
 void launch_uniform_bricks(const GridParams& g, int cb, const double* kappa, int* flag,
                            cudaStream_t s);
-// map[b].scale = face_t(k_rep, k_rep) / face_t(k_b, k_b) for the bricks with
-// map[b].slot == 0 && shared, 1 otherwise (slots already set)
+// map[b].scale = 1 / face_t(k_b, k_b) for the flagged (shared) bricks, 1
+// otherwise (slots already set)
 void launch_factor_scales(const GridParams& g, int cb, const double* kappa, const int* flag,
-                          int64_t rep, GSlot* map, cudaStream_t s);
+                          GSlot* map, cudaStream_t s);
 
 // spectral.cu
 // phi0: previous bases as the initial block (warm start) or nullptr
@@ -205,10 +210,9 @@ void launch_local_basis(const GridParams& g, int cb, const double* kappa, const 
 // bricks of one uniform conductivity inside: flag[b - b0] = 1
 void launch_uniform_inside(const GridParams& g, int cb, const double* kappa, int* flag,
                            cudaStream_t s);
-// bases of the flagged bricks from the representative's (after its solve)
-void launch_local_basis_share(const GridParams& g, int cb, const double* kappa, const int* flag,
-                              int64_t rep, double* phi, double* evals, int* iters,
-                              cudaStream_t s);
+// bases of the flagged bricks in closed form (separable DCT-II modes)
+void launch_local_basis_uniform(const GridParams& g, int cb, const double* kappa, const int* flag,
+                                double* phi, double* evals, int* iters, cudaStream_t s);
 
 // coarse.cu
 int max_lc();  // largest supported L_c (num_local_basis)

@@ -230,14 +230,15 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
   const int b = (int)(blockIdx.x + g.b0);
   const GSlot gsl = Gf.map[b];
-  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
+  // uniform bricks (slot < 0): no factor, fast diagonalisation (brick_inverse)
+  const double* G = gsl.slot < 0 ? nullptr : Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
   thomas_prefetch<CB>(sm.th, G);  // G is constant: stream it before the wait
   pdl_wait();
   if (st->done) {
-    thomas_drain<CB>(sm.th);  // no bulk copy may land after the CTA exits
+    thomas_drain<CB>(sm.th, G);  // no bulk copy may land after the CTA exits
     return;
   }
   const int t = threadIdx.x;
@@ -253,9 +254,9 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
       rr += rv * rv;
     }
     sm.tv[c] = rv;
-    sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
+    sm.tz[c] = (G && c >= P) ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
   }
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);  // r1 = S(r), solver.cpp:280-281
+  brick_inverse<CB>(sm.th, G, sm.tv, sm.tz, gsl.scale, g);  // r1 = S(r), solver.cpp:280-281
   if (TMG_R1_FULL)
     for (int c = t; c < C; c += NT) r1[bofs(b, C) + c] = sm.tv[c];
   // the face layers of r1, face-major: all the boundary-form kernels read
@@ -393,8 +394,9 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   PostSmem<CB>& sm = *reinterpret_cast<PostSmem<CB>*>(smraw);
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const GSlot gsl = Gf.map[bc.b];
-  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
-  if (threadIdx.x == 0)  // warm L2 with the first G planes (constant) before the wait
+  // uniform bricks (slot < 0): no factor, fast diagonalisation (brick_inverse)
+  const double* G = gsl.slot < 0 ? nullptr : Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
+  if (threadIdx.x == 0 && G)  // warm L2 with the first G planes (constant) before the wait
     prefetch_l2(G, (uint32_t)(2 * Thomas<CB>::PLANE * sizeof(double)));
   pdl_wait();
   if (st->done) return;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post(GridParams g, const 
   }
   __syncthreads();  // stencil tiles dead: the slots may now be filled
   thomas_prefetch<CB>(sm.th, G);
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);
+  brick_inverse<CB>(sm.th, G, sm.tv, sm.tz, gsl.scale, g);
   double rz = 0.0;
 #pragma unroll
   for (int k = 0; k < KPT; ++k) {
@@ -495,14 +497,15 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
   PostBSmem<CB>& sm = *reinterpret_cast<PostBSmem<CB>*>(smraw);
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const GSlot gsl = Gf.map[bc.b];
-  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
+  // uniform bricks (slot < 0): no factor, fast diagonalisation (brick_inverse)
+  const double* G = gsl.slot < 0 ? nullptr : Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
   thomas_prefetch<CB>(sm.th, G);  // G is constant: stream it before the wait
   pdl_wait();
   if (st->done) {
-    thomas_drain<CB>(sm.th);
+    thomas_drain<CB>(sm.th, G);
     return;
   }
   const int t = threadIdx.x;
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
     rown[k] = c < C ? __ldg(r + ob + c) : 0.0;
     if (c < C) {
       sm.tv[c] = rown[k];
-      sm.tz[c] = c >= F ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
+      sm.tz[c] = (G && c >= F) ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
     }
   }
   // t_c, one axis per pass (the two faces of a pass touch disjoint cells;
@@ -559,7 +562,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
       if (axis[k] == ax) sm.tv[cell[k]] += val[k];
   }
   __syncthreads();  // the solve's first step reads plane 0 of t from other threads
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);  // z = A_II^{-1} (r + t), solver.cpp:331-333
+  brick_inverse<CB>(sm.th, G, sm.tv, sm.tz, gsl.scale, g);  // z = A_II^{-1} (r + t), solver.cpp:331-333
   double rz = 0.0;
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
@@ -601,14 +604,15 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
   UpdateSmem<CB>& sm = *reinterpret_cast<UpdateSmem<CB>*>(smraw);
   const int b = (int)(blockIdx.x + g.b0);
   const GSlot gsl = Gf.map[b];
-  const double* G = Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
+  // uniform bricks (slot < 0): no factor, fast diagonalisation (brick_inverse)
+  const double* G = gsl.slot < 0 ? nullptr : Gf.G + (size_t)gsl.slot * Thomas<CB>::PER_BRICK;
   sm.th.slots = sm.slots;
   thomas_init<CB>(sm.th);
   __syncthreads();
   thomas_prefetch<CB>(sm.th, G);
   pdl_wait();
   if (st->done) {
-    thomas_drain<CB>(sm.th);
+    thomas_drain<CB>(sm.th, G);
     return;
   }
   const int t = threadIdx.x;
@@ -618,7 +622,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_brick_solve(GridParams g,
     sm.tz[c] = c >= P ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
   }
   __syncthreads();
-  thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, gsl.scale);
+  brick_inverse<CB>(sm.th, G, sm.tv, sm.tz, gsl.scale, g);
   double rz = 0.0;
   for (int c = t; c < C; c += NT) {
     const size_t s = bofs(b, C) + c;

@@ -186,26 +186,24 @@ void launch_uniform_bricks(const GridParams& g, int cb, const double* kappa, int
   else k_uniform_bricks<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, flag);
 }
 
+// uniform bricks: A_II = face_t(k, k) A_hat, solved by fast diagonalisation
+// of A_hat with scale 1 / face_t(k, k) (smoother.cuh, brick_inverse)
 template <int CB>
 __global__ void k_factor_scales(GridParams g, const double* __restrict__ kappa,
-                                const int* __restrict__ flag, int64_t rep, GSlot* map) {
+                                const int* __restrict__ flag, GSlot* map) {
   constexpr int C = CB * CB * CB;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= g.nbo) return;
   const int64_t b = g.b0 + i;
-  double sc = 1.0;
-  if (flag[i] && b != rep) {
-    const double kr = kappa[rep * C], kb = kappa[b * C];
-    sc = face_t(kr, kr) / face_t(kb, kb);
-  }
-  map[b].scale = sc;
+  const double kb = kappa[b * C];
+  map[b].scale = flag[i] ? 1.0 / face_t(kb, kb) : 1.0;
 }
 
 void launch_factor_scales(const GridParams& g, int cb, const double* kappa, const int* flag,
-                          int64_t rep, GSlot* map, cudaStream_t s) {
+                          GSlot* map, cudaStream_t s) {
   const unsigned grid = (unsigned)((g.nbo + 255) / 256);
-  if (cb == 8) k_factor_scales<8><<<grid, 256, 0, s>>>(g, kappa, flag, rep, map);
-  else k_factor_scales<4><<<grid, 256, 0, s>>>(g, kappa, flag, rep, map);
+  if (cb == 8) k_factor_scales<8><<<grid, 256, 0, s>>>(g, kappa, flag, map);
+  else k_factor_scales<4><<<grid, 256, 0, s>>>(g, kappa, flag, map);
 }
 
 int64_t thomas_doubles_per_brick(int cb) {

@@ -111,6 +111,11 @@ struct ThomasSmem {
   double part[Thomas<CB>::NBK][CB * CB + 8];
   uint64_t bars[kSlots];
   double (*slots)[Thomas<CB>::PLANE];
+  // fast diagonalisation of uniform bricks (brick_inverse): the orthonormal
+  // DST-I matrix Q[i][j] = sqrt(2/(CB+1)) sin(pi (i+1)(j+1)/(CB+1)) and the
+  // eigenvalues 2 - 2 cos(pi (j+1)/(CB+1)) of the 1-D Dirichlet Laplacian
+  double fdq[CB * CB];
+  double fdl[CB];
 };
 
 template <int CB>
@@ -195,12 +200,18 @@ __device__ __forceinline__ void thomas_init(ThomasSmem<CB>& sm) {
     for (int s = 0; s < kSlots; ++s) mbar_init(&sm.bars[s], 1);
     fence_barrier_init();
   }
+  for (int e = threadIdx.x; e < CB * CB; e += blockDim.x) {
+    const int i = e / CB, j = e % CB;
+    sm.fdq[e] = sqrt(2.0 / (CB + 1)) * sinpi((double)((i + 1) * (j + 1)) / (CB + 1));
+    if (i == 0) sm.fdl[j] = 2.0 - 2.0 * cospi((double)(j + 1) / (CB + 1));
+  }
 }
 
 // Issue the first kSlots plane loads of a solve (thread 0). Call after
 // thomas_init + __syncthreads, as early as possible in the kernel.
 template <int CB>
 __device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double* __restrict__ G) {
+  if (!G) return;  // uniform brick: no factor planes (brick_inverse)
   // resident mode (kSlots >= CB): all CB planes stay in shared memory and the
   // backward sweep reuses them; otherwise a ring refilled kSlots steps ahead.
   constexpr int NPRE = kSlots >= CB ? CB : kSlots;
@@ -222,9 +233,9 @@ __device__ __forceinline__ void thomas_prefetch(ThomasSmem<CB>& sm, const double
 // Wait for the loads thomas_prefetch issued (a CTA that exits early must not
 // leave bulk copies in flight into its shared memory).
 template <int CB>
-__device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm) {
+__device__ __forceinline__ void thomas_drain(ThomasSmem<CB>& sm, const double* G) {
   constexpr int NPRE = kSlots >= CB ? CB : kSlots;
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0 && G)
     for (int n = 0; n < NPRE && n < Thomas<CB>::NL; ++n) mbar_wait(&sm.bars[n], 0);
 }
 
@@ -302,6 +313,54 @@ __device__ __forceinline__ void thomas_solve(ThomasSmem<CB>& sm, const double* _
       mbar_wait(&sm.bars[slot_of(n + 1)], parity_of(n + 1));
     __syncthreads();
   }
+}
+
+// x = A_II^-1 t of an interior brick of one conductivity k (cells and face
+// halo): A_II = face_t(k, k) sum_ax (area/h)_ax K_ax with K the 1-D Dirichlet
+// Laplacian tridiag(-1, 2, -1) along each axis (every face of every cell,
+// inside and to the neighbours, carries face_t(k, k) area/h), so
+//   A_II^-1 = scale (Q x Q x Q) diag(1 / sum_ax (area/h)_ax lambda_ax) (Q x Q x Q),
+// scale = 1 / face_t(k, k), Q the symmetric orthonormal DST-I: six 8-point
+// transforms and a division instead of the 15 dependent plane mat-vecs. w:
+// C doubles of scratch. Starts and ends with a __syncthreads; x aliases t.
+template <int CB>
+__device__ __forceinline__ void fastdiag_solve(const ThomasSmem<CB>& sm, double* t, double* w,
+                                               double scale, const double* cpl) {
+  constexpr int C = CB * CB * CB;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // one transform along axis ax (stride st) from src to dst
+  auto transform = [&](const double* src, double* dst, int st) {
+    __syncthreads();
+    for (int o = tid; o < C; o += nt) {
+      const int io = (o / st) % CB, base = o - io * st;
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < CB; ++i) v = fma(sm.fdq[i * CB + io], src[base + i * st], v);
+      dst[o] = v;
+    }
+  };
+  transform(t, w, 1);
+  transform(w, t, CB);
+  transform(t, w, CB * CB);
+  __syncthreads();
+  for (int o = tid; o < C; o += nt) {
+    const int i = o % CB, j = (o / CB) % CB, k = o / (CB * CB);
+    w[o] *= scale / (cpl[0] * sm.fdl[i] + cpl[1] * sm.fdl[j] + cpl[2] * sm.fdl[k]);
+  }
+  transform(w, t, CB * CB);
+  transform(t, w, CB);
+  transform(w, t, 1);
+  __syncthreads();
+}
+
+// The exact block solve of one brick: the plane-factor block Thomas (G), or
+// the fast diagonalisation of a uniform interior brick (G == nullptr, tz
+// used as scratch).
+template <int CB>
+__device__ __forceinline__ void brick_inverse(ThomasSmem<CB>& sm, const double* G, double* t,
+                                              double* tz, double scale, const GridParams& g) {
+  if (G) thomas_solve<CB>(sm, G, t, tz, t, scale);
+  else fastdiag_solve<CB>(sm, t, tz, scale, g.cpl);
 }
 
 }  // namespace tmg

@@ -361,10 +361,6 @@ void launch_local_basis(const GridParams& g, int cb, const double* kappa, const 
 }
 
 // flag[i] = 1: every cell of brick b0 + i has bitwise the same conductivity.
-// Its local problem (box_interior_stiffness + mass, coarse_space.cpp:238-304)
-// is then t(k) S_hat and k vol I with t(k) = face_t(k, k): the eigenvectors
-// of any such brick are those of one representative, the M-orthonormal bases
-// scale by sqrt(k_rep / k) and the eigenvalues by t(k) k_rep / (t(k_rep) k).
 template <int CB>
 __global__ void __launch_bounds__(256) k_uniform_inside(GridParams g, const double* __restrict__ kappa,
                                                        int* flag) {
@@ -381,21 +377,66 @@ __global__ void __launch_bounds__(256) k_uniform_inside(GridParams g, const doub
   if (threadIdx.x == 0) flag[blockIdx.x] = same;
 }
 
+// Local bases of the flagged bricks in closed form. With one conductivity k
+// inside, the local problem (box_interior_stiffness + mass,
+// coarse_space.cpp:238-304) is t S_hat, t = face_t(k, k), and k vol I, where
+// S_hat = sum over axes of area/h times the 1-D Neumann Laplacian (unit
+// coupling). Its eigenvectors are the separable DCT-II products
+//   v_pqr(i, j, l) = cos(pi p (i + 1/2) / CB) cos(pi q (j + 1/2) / CB) cos(pi r (l + 1/2) / CB)
+// with B-eigenvalues t / (k vol) sum_ax (area/h)_ax (2 - 2 cos(pi p_ax / CB)).
+// The L_c smallest (ties by mode index p + CB (q + CB r): a fixed choice
+// inside a degenerate cluster cut by L_c, as any eigensolver makes one) are
+// written M-orthonormal, phi = v / ||v|| / sqrt(k vol). Exact, and the same
+// bits in every partition of the grid.
 template <int CB>
-__global__ void __launch_bounds__(256) k_local_basis_share(GridParams g, const double* __restrict__ kappa,
-                                                          const int* __restrict__ flag, int64_t rep,
-                                                          double* phi, double* evals, int* iters) {
+__global__ void __launch_bounds__(256) k_local_basis_uniform(GridParams g,
+                                                            const double* __restrict__ kappa,
+                                                            const int* __restrict__ flag,
+                                                            double* phi, double* evals, int* iters) {
   constexpr int C = CB * CB * CB;
+  constexpr int LMAX = 8;
   const int64_t b = g.b0 + blockIdx.x;
-  if (!flag[blockIdx.x] || b == rep) return;
-  const double kr = kappa[rep * C], kb = kappa[b * C];
-  const double sphi = sqrt(kr / kb);
-  const double sev = (face_t(kb, kb) * kr) / (face_t(kr, kr) * kb);
+  if (!flag[blockIdx.x]) return;
   const int lc = g.lc;
-  for (int e = threadIdx.x; e < lc * C; e += blockDim.x)
-    phi[b * lc * C + e] = sphi * phi[rep * lc * C + e];
-  if (threadIdx.x < lc) evals[b * lc + threadIdx.x] = sev * evals[rep * lc + threadIdx.x];
-  if (threadIdx.x == 0) iters[b] = iters[rep];
+  __shared__ int mode[LMAX];
+  __shared__ double mu[LMAX];
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int m = 0; m < C; ++m) {
+      const int pm[3] = {m % CB, (m / CB) % CB, m / (CB * CB)};
+      double v = 0.0;
+      for (int ax = 0; ax < 3; ++ax) v += g.cpl[ax] * (2.0 - 2.0 * cospi((double)pm[ax] / CB));
+      // insertion into the sorted (mu, mode) list of the lc smallest
+      int pos = n < lc ? n : lc;
+      while (pos > 0 && v < mu[pos - 1]) --pos;
+      if (pos >= lc) continue;
+      for (int k = (n < lc ? n : lc - 1); k > pos; --k) {
+        mu[k] = mu[k - 1];
+        mode[k] = mode[k - 1];
+      }
+      mu[pos] = v;
+      mode[pos] = m;
+      if (n < lc) ++n;
+    }
+  }
+  __syncthreads();
+  const double kb = kappa[b * C];
+  const double sc = 1.0 / sqrt(kb * g.vol);
+  for (int e = threadIdx.x; e < lc * C; e += blockDim.x) {
+    const int a = e / C, l = e % C;
+    const int m = mode[a];
+    const int pm[3] = {m % CB, (m / CB) % CB, m / (CB * CB)};
+    const int co[3] = {l % CB, (l / CB) % CB, l / (CB * CB)};
+    double v = 1.0, nrm2 = 1.0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      v *= cospi((double)pm[ax] * (co[ax] + 0.5) / CB);
+      nrm2 *= pm[ax] == 0 ? (double)CB : 0.5 * CB;
+    }
+    phi[(b * lc + a) * C + l] = sc * v / sqrt(nrm2);
+  }
+  if ((int)threadIdx.x < lc) evals[b * lc + threadIdx.x] = face_t(kb, kb) / (kb * g.vol) * mu[threadIdx.x];
+  if (threadIdx.x == 0) iters[b] = 0;
 }
 
 void launch_uniform_inside(const GridParams& g, int cb, const double* kappa, int* flag,
@@ -404,13 +445,12 @@ void launch_uniform_inside(const GridParams& g, int cb, const double* kappa, int
   else k_uniform_inside<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, flag);
 }
 
-void launch_local_basis_share(const GridParams& g, int cb, const double* kappa, const int* flag,
-                              int64_t rep, double* phi, double* evals, int* iters,
-                              cudaStream_t s) {
+void launch_local_basis_uniform(const GridParams& g, int cb, const double* kappa, const int* flag,
+                                double* phi, double* evals, int* iters, cudaStream_t s) {
   if (cb == 8)
-    k_local_basis_share<8><<<(unsigned)g.nbo, 256, 0, s>>>(g, kappa, flag, rep, phi, evals, iters);
+    k_local_basis_uniform<8><<<(unsigned)g.nbo, 256, 0, s>>>(g, kappa, flag, phi, evals, iters);
   else
-    k_local_basis_share<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, flag, rep, phi, evals, iters);
+    k_local_basis_uniform<4><<<(unsigned)g.nbo, 64, 0, s>>>(g, kappa, flag, phi, evals, iters);
 }
 
 }  // namespace tmg

@@ -21,7 +21,10 @@ def close_iters(a, b):
 
 @needs_ref
 @pytest.mark.parametrize("levels,iters,vstar,kmin", [([16], [6], 0.3, 1e-3),
-                                                     ([16, 32], [4, 3], 0.2, 1e-3)])
+                                                     ([16, 32], [4, 3], 0.2, 1e-3),
+                                                     # three levels: 2^3 coarse cells at 8^3
+                                                     # (generic kernels)
+                                                     ([8, 16, 32], [3, 2, 2], 0.3, 1e-3)])
 def test_optimize_matches_reference(levels, iters, vstar, kmin):
     ref, x_ref, fc_ref, failed = O.ref_optimize(levels, iters, 2, 2, vstar=vstar, kappa_lo=kmin)
     assert not failed

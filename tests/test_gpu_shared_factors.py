@@ -1,8 +1,10 @@
 """Shared fine-smoother factors: interior bricks whose cells
-and face halo carry one conductivity share one factor, scaled by
-face_t(k_rep, k_rep) / face_t(k, k) (A_II = face_t(k, k) A_hat). Checked
-against the oracle's exact per-coarse-cell blocks and against the unshared
-factors (TMG_G_SHARE=0)."""
+and face halo carry one conductivity k share the canonical factor A_hat^-1
+of a unit-conductivity brick, scaled by 1 / face_t(k, k) (A_II = face_t(k, k)
+A_hat); bricks of one conductivity inside get their local bases in closed
+form. Checked against the oracle's exact per-coarse-cell blocks and
+eigensolver, and against the unshared paths (TMG_G_SHARE=0,
+TMG_EIG_SHARE=0)."""
 import os
 
 import numpy as np
@@ -75,9 +77,9 @@ def test_shared_factor_preconditioner_is_the_exact_block_solve():
 
 
 def test_shared_local_eigensolves_match_individual():
-    """Bricks of one uniform conductivity take the representative's local
-    bases scaled by sqrt(k_rep / k) (and eigenvalues by t(k) k_rep / (t(k_rep)
-    k)); they match solving every brick (TMG_EIG_SHARE=0) and the oracle."""
+    """Bricks of one conductivity inside take closed-form bases (separable
+    DCT-II modes, M-orthonormal); they match solving every brick
+    (TMG_EIG_SHARE=0) and the oracle's dense eigensolver."""
     n = 32
     rho = inputs.box_filter_design(n, 0.2, radius=4)
     kappa = inputs.conductivity(rho, 1e-3)
