@@ -279,7 +279,8 @@ def run_reference(args):
 #  k_post  : r 8 + coef_z 8 + G 288 + z 8 + (Phi 32 + r1 8)*SURF + T 3 = 338.1
 #  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8*SURF     = 348.6
 #  k_restrict: (Phi 32 + r1 8)*SURF + T 3                              = 26.1
-#  k_search: coef 32 + z 8 + p 16 + q 8                                 = 64
+#  k_search: coef 32 + z 8 + p 16 + q 8 (TMG_SEARCH_KAPPA=1: the
+#            coefficients recomputed from kappa, 8 instead of 32)      = 64
 # G counts only the distinct factors (x slots / bricks): uniform interior
 # bricks share one factor, whose planes stay in L2.
 SURF = 296 / 512
@@ -287,7 +288,8 @@ SURF = 296 / 512
 
 def kernel_bytes_per_cell(g_fraction=1.0):
     g = 288 * g_fraction
-    return {"post": 24 + g + 40 * SURF + 3, "update": 56 + g + 8 * SURF, "search": 64,
+    search = 40 if os.environ.get("TMG_SEARCH_KAPPA", "0")[:1] == "1" else 64
+    return {"post": 24 + g + 40 * SURF + 3, "update": 56 + g + 8 * SURF, "search": search,
             "restrict": 40 * SURF + 3}
 
 

@@ -938,6 +938,19 @@ void enqueue_vcycle_nu(tmg_ctx* c, int init, int par_new) {
   }
 }
 
+// p = z + beta p_old, q = A p, p.q from the stored coefficients (64 B/cell).
+// TMG_SEARCH_KAPPA=1 recomputes them from kappa instead (40 B/cell, bitwise
+// the same q): measured slower at configs[3], 3.94 against 2.35 ms per launch
+// -- the 3.4 face divisions per cell and the face/diagonal assembly make the
+// kernel issue-bound.
+void search(tmg_ctx* c, Slab& s, const double* pold, double* pnew, cudaStream_t st) {
+  static const bool from_kappa = getenv("TMG_SEARCH_KAPPA") && getenv("TMG_SEARCH_KAPPA")[0] == '1';
+  if (c->cb != 0 && from_kappa)
+    launch_search_kappa(s.g, c->cb, s.kappa, s.dmask, s.z, pold, pnew, s.q, s.st, s.partials, st);
+  else
+    launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, st);
+}
+
 bool hierarchical(const tmg_ctx* c) {
   return c->kind == TMG_PRECOND_MMG || c->kind == TMG_PRECOND_TWO_GRID;
 }
@@ -958,8 +971,7 @@ void enqueue_precond_init(tmg_ctx* c) { enqueue_precond(c, 1, 0); }
 void enqueue_iteration(tmg_ctx* c, int par) {
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_search(s.g, c->cb, s.coef, s.z, s.pbuf[par], s.pbuf[par ^ 1], s.q, s.st,
-                        s.partials, c->stream));
+    KL(1, search(c, s, s.pbuf[par], s.pbuf[par ^ 1], c->stream));
   if (c->dist()) {
     reduce_finalize(c, kRedSearch, 0);
     exchange(c, [&](Slab& s) { return (void*)s.pbuf[par ^ 1]; }, sizeof(double) * C, false);
@@ -1101,7 +1113,7 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       double* pnew = s.pbuf[par ^ 1];
       par ^= 1;
       const int64_t kb = c->kcount;
-      timed(0, [&] { KL(1, launch_search(s.g, c->cb, s.coef, s.z, pold, pnew, s.q, s.st, s.partials, c->stream)); });
+      timed(0, [&] { KL(1, search(c, s, pold, pnew, c->stream)); });
       if (hierarchical(c) && !c->fine_bj && c->nu == 1 && c->cb != 0) {
         timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.ff(), s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });

@@ -323,6 +323,10 @@ void launch_init(const GridParams& g, int cb, const double* coef, const double* 
 void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s);
+// launch_search with the coefficients recomputed from kappa (tuned bricks)
+void launch_search_kappa(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                         const double* z, const double* p_old, double* p, double* q, PcgState* st,
+                         double* partials, cudaStream_t s);
 // out = add + A_II^{-1} in per brick (per-coarse-cell fine blocks); rdot: also
 // rdot . out -> fin_post (the generic nu-sweep V-cycle)
 void launch_brick_solve(const GridParams& g, int cb, const double* coef, const FineFactors& Gf,

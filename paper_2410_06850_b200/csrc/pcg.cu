@@ -204,6 +204,64 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
   }
 }
 
+// K1 from the conductivity (opt-in, TMG_SEARCH_KAPPA=1; slower, abi.cu
+// search()): the tile's face transmissibilities
+// and diagonals are recomputed from kappa (8 B/cell, plus the Dirichlet bits
+// on boundary bricks) with the expressions of k_coefficients instead of
+// streaming the four coefficient arrays (32 B/cell), 40 instead of 64 B/cell;
+// the faces (constant) are formed before the grid dependency wait. q is
+// bitwise the q of k_search: the same coefficients, the row summed in the
+// same order (apply_row / apply_coef differ only in the sign of a zero).
+template <int CB>
+__global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search_kappa(
+    GridParams g, const double* __restrict__ kappa, const uint8_t* __restrict__ dmask,
+    const double* __restrict__ z, const double* __restrict__ p_old, double* p, double* q,
+    PcgState* st, double* partials) {
+  pdl_trigger();
+  constexpr int C = CB * CB * CB, NT = kStencilThreads < C / 2 ? kStencilThreads : C / 2;
+  constexpr int KPT = C / (2 * NT);  // x-adjacent cell pairs per thread
+  __shared__ StencilSmem<CB> ss;
+  __shared__ double pt[Tile<CB>::N];
+  __shared__ double red[80];
+  __shared__ int flag;
+  const int t = threadIdx.x;
+  const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
+  load_tile<CB, true>(kappa, ss.kt, g, bc);
+  __syncthreads();
+  tile_faces<CB>(ss.kt, ss.fx, ss.fy, ss.fz, g, bc);  // fvm.cpp:73-76, 91-94
+  pdl_wait();
+  if (st->done) return;
+  const bool first = st->first;
+  const double beta = st->beta;
+  load_tile_axpy<CB>(z, p_old, beta, first, pt, g, bc);  // solver.cpp:565-567
+  __syncthreads();
+  const bool bnd = brick_on_boundary(g, bc);
+  double pq = 0.0;
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int c = 2 * (t + k * NT), li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+    const size_t s = bofs(bc.b, C) + c;
+    const int ti = Tile<CB>::idx(li, lj, lk);
+    const unsigned dm0 = bnd ? dmask[s] : 0u, dm1 = bnd ? dmask[s + 1] : 0u;
+    const FaceSet f0 = cell_faces<CB>(ss.fx, ss.fy, ss.fz, ss.kt[ti], li, lj, lk, g, bc, dm0);
+    const FaceSet f1 = cell_faces<CB>(ss.fx, ss.fy, ss.fz, ss.kt[ti + 1], li + 1, lj, lk, g, bc, dm1);
+    const double2 pv = make_double2(pt[ti], pt[ti + 1]);
+    const double2 qv = make_double2(apply_row<CB>(f0, pt, li, lj, lk),
+                                    apply_row<CB>(f1, pt, li + 1, lj, lk));  // solver.cpp:540
+    *reinterpret_cast<double2*>(p + s) = pv;
+    *reinterpret_cast<double2*>(q + s) = qv;
+    pq += pv.x * qv.x;
+    pq += pv.y * qv.y;
+  }
+  double v[1] = {pq};
+  block_sum_k<NT, 1>(v, red);
+  double tot[1];
+  if (grid_reduce_last_k<1>(v, partials, &st->ticket[1], tot, &flag, red) && t == 0) {
+    if (g.dist) st->loc[kRedSearch] = tot[0];
+    else fin_search(st, tot[0]);
+  }
+}
+
 // ------------------------------------------------- K2 update + pre-smooth
 template <int CB>
 struct UpdateSmem {
@@ -758,6 +816,12 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
   if (cb == 0) return launch_g_search(g, coef, z, p_old, p, q, st, partials, s);
   if (cb == 8) launch_pdl(k_search<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, z, p_old, p, q, st, partials);
   else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, coef, M, z, p_old, p, q, st, partials);
+}
+void launch_search_kappa(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
+                         const double* z, const double* p_old, double* p, double* q, PcgState* st,
+                         double* partials, cudaStream_t s) {
+  if (cb == 8) launch_pdl(k_search_kappa<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, kappa, dmask, z, p_old, p, q, st, partials);
+  else launch_pdl(k_search_kappa<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, kappa, dmask, z, p_old, p, q, st, partials);
 }
 void launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,

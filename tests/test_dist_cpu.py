@@ -33,12 +33,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, shape=(64, 64, 64), ncc=(NCC,) * 3, sd=SD):
+    GRID = GridSpec(*shape)
+    NCC3 = tuple(ncc)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        part = D.partition(GRID, NCC, SD, world, rank)
+        part = D.partition(GRID, NCC3, sd, world, rank)
         parts = [None] * world
         dist.all_gather_object(parts, part)
         # one consistent cover of z, bricks, cc elements and cells
@@ -53,8 +55,8 @@ def _worker(rank, world, port, out):
         assert [p["hi"] for p in parts] == [1] * (world - 1) + [0]
         # halo exchange following the library's plan: bricks hold their
         # global index; ghosts start at -1 and must end as the neighbour's ids
-        L = (GRID.nx // 8) * (GRID.ny // 8)  # bricks per z-layer
-        Le = NCC * NCC  # cc elements per z-layer
+        L = (NCC3[0] * sd) * (NCC3[1] * sd)  # bricks per z-layer
+        Le = NCC3[0] * NCC3[1]  # cc elements per z-layer
         # the library's own plan (tmg_halo_plan = the ops exchange() issues
         # over NCCL), carried out with gloo point-to-point
         for elem, base, count, layer in ((False, part["brick0"], part["bricks"], L),
@@ -63,7 +65,7 @@ def _worker(rank, world, port, out):
             n_u = count + (part["lo"] + part["hi"]) * layer
             win = -np.ones(n_u, dtype=np.int64)
             win[base - lo_u:base - lo_u + count] = np.arange(base, base + count)
-            plan = D.halo_plan(GRID, NCC, SD, world, rank, elem=elem)
+            plan = D.halo_plan(GRID, NCC3, sd, world, rank, elem=elem)
             assert len(plan) == 2 * (part["lo"] + part["hi"])
             reqs, recv = [], []
             for op, peer, u0, nu in plan:
@@ -104,6 +106,17 @@ def test_partition_and_halo_plan_gloo(world):
     mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True,
                        start_method="spawn")
     assert sorted(out.keys()) == list(range(world))
+
+
+def test_partition_and_halo_plan_gloo_generic_shape():
+    """a non-cubic hierarchy (coarse cells of 12 x 8 x 8, generic kernels):
+    the slab partition and the halo plan are per brick / cc-element layer,
+    whatever the brick shape"""
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_worker, args=(2, _free_port(), out, (48, 32, 64), (2, 2, 4), 2),
+                       nprocs=2, join=True, start_method="spawn")
+    assert sorted(out.keys()) == [0, 1]
 
 
 def test_partition_errors():

@@ -122,3 +122,27 @@ def O_cells(n, b):
     bi, bj, bk = b % nb, (b // nb) % nb, b // (nb * nb)
     return [(8 * bi + i) + n * ((8 * bj + j) + n * (8 * bk + k))
             for k in range(8) for j in range(8) for i in range(8)]
+
+
+def test_search_from_kappa_is_bitwise_the_coefficient_search():
+    """k_search_kappa (coefficients recomputed from kappa, 40 B/cell) and
+    k_search (stored coefficients, 64 B/cell) give bitwise the same PCG
+    (TMG_SEARCH_KAPPA is read once per process: two processes)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2410_06850_b200 import BoundarySpec, Context, GridSpec, MmgOptions, inputs\n"
+        "n = 32; kappa = inputs.conductivity(inputs.box_filter_design(n, 0.3), 1e-6)\n"
+        "c = Context(GridSpec(n, n, n), 2, 2)\n"
+        "c.set_conductivity(kappa, BoundarySpec.bottom_center_patch(1, 1, 0.2, 0))\n"
+        "c.setup('mmg', MmgOptions(fine_blocks='coarse_cell'))\n"
+        "r = c.pcg(c.assemble_rhs(np.ones(n ** 3)), rtol=1e-10)\n"
+        "sys.stdout.write(r.x.tobytes().hex()[:4000] + ' ' + r.report.residual_history.tobytes().hex())\n"
+    ) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for v in ("1", "0"):  # kappa-based (opt-in) and the default
+        env = dict(os.environ, TMG_SEARCH_KAPPA=v)
+        out.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                                  text=True, check=True).stdout)
+    assert out[0] == out[1]
