@@ -37,6 +37,12 @@ for item in a.settings.split(","):
     ctx.setup("mmg", o)
     ctx.upload_rhs(b)
     rep = ctx.solve_resident(1e-8, 5000)
+    extra = {}
+    if n <= 256:  # local-eigensolver rounds (downloads the bases)
+        _, _, its = ctx.local_bases()
+        extra = {"eig_rounds_mean": float(np.mean(np.abs(its))), "eig_rounds_max": int(np.max(its)),
+                 "eig_unconverged": int(np.sum(its < 0))}
     print(json.dumps({"config": a.config, "eig_tol": float(tol), "eig_degree": int(deg),
                       "setup_ms": rep.setup_seconds * 1e3, "iterations": rep.iterations,
-                      "solve_ms": rep.solve_seconds * 1e3, "converged": rep.converged}), flush=True)
+                      "solve_ms": rep.solve_seconds * 1e3, "converged": rep.converged, **extra}),
+          flush=True)
