@@ -280,15 +280,17 @@ def run_reference(args):
 #  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8*SURF     = 348.6
 #  k_restrict: (Phi 32 + r1 8)*SURF + T 3                              = 26.1
 #  k_search: coef 32 + z 8 + p 16 + q 8 (TMG_SEARCH_KAPPA=1: the
-#            coefficients recomputed from kappa, 8 instead of 32)      = 64
+#            coefficients recomputed from kappa, 8 instead of 32)      = 64;
+#            bricks off the domain boundary of a single-slab context sum
+#            the diagonal from the face coefficients (coef 24): 56
 # G counts only the distinct factors (x slots / bricks): uniform interior
 # bricks share one factor, whose planes stay in L2.
 SURF = 296 / 512
 
 
-def kernel_bytes_per_cell(g_fraction=1.0):
+def kernel_bytes_per_cell(g_fraction=1.0, interior_fraction=0.0):
     g = 288 * g_fraction
-    search = 40 if os.environ.get("TMG_SEARCH_KAPPA", "0")[:1] == "1" else 64
+    search = 40 if os.environ.get("TMG_SEARCH_KAPPA", "0")[:1] == "1" else 64 - 8 * interior_fraction
     return {"post": 24 + g + 40 * SURF + 3, "update": 56 + g + 8 * SURF, "search": search,
             "restrict": 40 * SURF + 3}
 
@@ -527,7 +529,9 @@ def run_ours(args):
         peak, peak_src = 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
     slots, bricks = ctx.fine_factor_slots()
     gfrac = slots / bricks if bricks else 1.0
-    kbytes = kernel_bytes_per_cell(gfrac)
+    nbr = [max(d // 8, 1) for d in (n, n, n)] if world == 1 else None  # bricks per axis (c = 8)
+    interior = float(np.prod([max(k - 2, 0) / k for k in nbr])) if nbr else 0.0
+    kbytes = kernel_bytes_per_cell(gfrac, interior)
     iter_bytes = sum(kbytes.values())
     iter_achieved = iter_bytes * M_local * iters / (ms * 1e-3) / 1e9  # per GPU
     if world == 1:

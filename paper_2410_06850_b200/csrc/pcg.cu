@@ -159,6 +159,9 @@ template <int CB>
 #ifndef TMG_SEARCH_MINB
 #define TMG_SEARCH_MINB 6
 #endif
+#ifndef TMG_SEARCH_DIAG  // 1: every brick reads the stored diagonal (A/B)
+#define TMG_SEARCH_DIAG 0
+#endif
 __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(GridParams g, const double* __restrict__ coef,
                                                               int64_t M, const double* __restrict__ z,
                                                               const double* __restrict__ p_old, double* p,
@@ -178,23 +181,31 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
   if (st->done) return;
   const bool first = st->first;
   const double beta = st->beta;
-  // coefficients + p = z + beta p over the tile (solver.cpp:565-567)
-  load_coefs_tile_axpy<CB, NT>(coef, M, cs, z, p_old, beta, first, pt, g, bc);
+  // coefficients + p = z + beta p over the tile (solver.cpp:565-567). Bricks
+  // off the domain boundary (no Dirichlet faces; single-slab contexts) do not
+  // read the diagonal: it is the sum of the six face coefficients (56 instead
+  // of 64 B/cell).
+  const bool with_dg = TMG_SEARCH_DIAG || g.dist || brick_on_boundary(g, bc);
+  load_coefs_tile_axpy<CB, NT>(coef, M, cs, z, p_old, beta, first, pt, g, bc, with_dg);
   __syncthreads();
   double pq = 0.0;
+  auto rows = [&](auto dgc) {
 #pragma unroll
-  for (int k = 0; k < KPT; ++k) {
-    const int c = 2 * (t + k * NT), li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
-    const size_t s = bofs(bc.b, C) + c;
-    const int ti = Tile<CB>::idx(li, lj, lk);
-    const double2 pv = make_double2(pt[ti], pt[ti + 1]);
-    const double2 qv = make_double2(apply_coef<CB>(cs, pt, li, lj, lk),
-                                    apply_coef<CB>(cs, pt, li + 1, lj, lk));  // solver.cpp:540
-    *reinterpret_cast<double2*>(p + s) = pv;
-    *reinterpret_cast<double2*>(q + s) = qv;
-    pq += pv.x * qv.x;
-    pq += pv.y * qv.y;
-  }
+    for (int k = 0; k < KPT; ++k) {
+      const int c = 2 * (t + k * NT), li = c % CB, lj = (c / CB) % CB, lk = c / (CB * CB);
+      const size_t s = bofs(bc.b, C) + c;
+      const int ti = Tile<CB>::idx(li, lj, lk);
+      const double2 pv = make_double2(pt[ti], pt[ti + 1]);
+      const double2 qv = make_double2(apply_coef<CB, decltype(dgc)::value>(cs, pt, li, lj, lk),
+                                      apply_coef<CB, decltype(dgc)::value>(cs, pt, li + 1, lj, lk));  // solver.cpp:540
+      *reinterpret_cast<double2*>(p + s) = pv;
+      *reinterpret_cast<double2*>(q + s) = qv;
+      pq += pv.x * qv.x;
+      pq += pv.y * qv.y;
+    }
+  };
+  if (with_dg) rows(std::true_type{});
+  else rows(std::false_type{});
   double v[1] = {pq};
   block_sum_k<NT, 1>(v, red);
   double tot[1];

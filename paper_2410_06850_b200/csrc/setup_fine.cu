@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
       const int blk = e / 64, rr = (e % 64) / 8, cc = e % 8;
       int I, J;
       block_of<CB>(blk, I, J);
-      Gout[(size_t)k * Thomas<CB>::PLANE + blk * 64 + swz(rr, cc)] = Gprev[(8 * I + rr) * GP + 8 * J + cc];
+      Gout[(size_t)k * Thomas<CB>::PLANE + plane_off(blk, rr, cc)] = Gprev[(8 * I + rr) * GP + 8 * J + cc];
     }
     __syncthreads();
   }

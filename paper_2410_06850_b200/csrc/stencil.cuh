@@ -273,7 +273,10 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
                                                      CoefSmem<CB>& cs, const double* __restrict__ z,
                                                      const double* __restrict__ p_old, double beta,
                                                      bool first, double* tile,
-                                                     const GridParams& g, const BrickCoord& bc) {
+                                                     const GridParams& g, const BrickCoord& bc,
+                                                     bool with_dg = true) {
+  // with_dg = false (CTA-uniform): the diagonal array is neither read nor
+  // staged; apply_coef<CB, false> sums it from the six face coefficients
   constexpr int C = CB * CB * CB, F = CB * CB, NPAIR = C / 2;
   constexpr int KO = (NPAIR + NT - 1) / NT;      // own cell pairs per thread
   constexpr int KH = (6 * F + NT - 1) / NT;      // halo cells per thread
@@ -287,7 +290,8 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
     if (pr < NPAIR) {
       const size_t s = bofs(bc.b, C) + 2 * pr;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) cf[k][a] = __ldg(reinterpret_cast<const double2*>(coef + (size_t)a * M + s));
+      for (int a = 0; a < 4; ++a)
+        if (a < 3 || with_dg) cf[k][a] = __ldg(reinterpret_cast<const double2*>(coef + (size_t)a * M + s));
       zo[k] = __ldg(reinterpret_cast<const double2*>(z + s));
       po[k] = first ? make_double2(0.0, 0.0) : __ldg(reinterpret_cast<const double2*>(p_old + s));
     }
@@ -329,7 +333,7 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
       *reinterpret_cast<double2*>(cs.cx + c) = cf[k][0];
       *reinterpret_cast<double2*>(cs.cy + c) = cf[k][1];
       *reinterpret_cast<double2*>(cs.cz + c) = cf[k][2];
-      *reinterpret_cast<double2*>(cs.dg + c) = cf[k][3];
+      if (with_dg) *reinterpret_cast<double2*>(cs.dg + c) = cf[k][3];
       const int ti = Tile<CB>::idx(li, lj, lk);
       tile[ti] = first ? zo[k].x : zo[k].x + beta * po[k].x;
       tile[ti + 1] = first ? zo[k].y : zo[k].y + beta * po[k].y;
@@ -357,7 +361,11 @@ __device__ __forceinline__ void load_coefs_tile_axpy(const double* __restrict__ 
 // (A x)_c, branch-free: missing neighbours have T = 0 and a 0 halo value, so
 // their -0 terms leave the sum bitwise unchanged; order and rounding are those
 // of SparseOperator::apply on the assembled row (sparse.cpp:76-83).
-template <int CB>
+// DG = false: the diagonal is summed from the six face coefficients in the
+// assembly's face order (x-lo, x-hi, y-lo, y-hi, z-lo, z-hi; fvm.cpp:71-112,
+// cell_faces) instead of read from cs.dg -- bitwise the stored diagonal of a
+// cell without Dirichlet faces (a missing neighbour's T = 0 adds +0).
+template <int CB, bool DG = true>
 __device__ __forceinline__ double apply_coef(const CoefSmem<CB>& cs, const double* xt, int li, int lj,
                                              int lk) {
   constexpr int E = Tile<CB>::E;
@@ -369,7 +377,11 @@ __device__ __forceinline__ double apply_coef(const CoefSmem<CB>& cs, const doubl
   double s = __dadd_rn(0.0, __dmul_rn(-*pz, xt[ti - E * E]));
   s = __dadd_rn(s, __dmul_rn(-*py, xt[ti - E]));
   s = __dadd_rn(s, __dmul_rn(-*px, xt[ti - 1]));
-  s = __dadd_rn(s, __dmul_rn(cs.dg[c], xt[ti]));
+  double dg;
+  if constexpr (DG) dg = cs.dg[c];
+  else
+    dg = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(*px, cs.cx[c]), *py), cs.cy[c]), *pz), cs.cz[c]);
+  s = __dadd_rn(s, __dmul_rn(dg, xt[ti]));
   s = __dadd_rn(s, __dmul_rn(-cs.cx[c], xt[ti + 1]));
   s = __dadd_rn(s, __dmul_rn(-cs.cy[c], xt[ti + E]));
   s = __dadd_rn(s, __dmul_rn(-cs.cz[c], xt[ti + E * E]));

@@ -8,6 +8,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
 //        --expt-relaxed-constexpr -I paper_2410_06850_b200/csrc tools/thomas_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "smoother.cuh"
@@ -62,6 +63,59 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __res
   for (int c = threadIdx.x; c < C; c += NT) xout[(size_t)b * C + c] = sm.tv[c];
 }
 
+// Persistent variant of mode 0: one CTA per resident slot, bricks strided over
+// the grid, the TMA ring carried across bricks (the next brick's first planes
+// are requested while this brick's last planes are consumed).
+__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench_persist(const double* __restrict__ Gf,
+                                                                    const double* __restrict__ tin,
+                                                                    double* xout, int nb, int chain) {
+  constexpr int C = CB * CB * CB, NT = Thomas<CB>::NT;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  struct Sm {
+    double slots[kSlots][Thomas<CB>::PLANE];
+    ThomasSmem<CB> th;
+    double tv[C];
+    double tz[C];
+  };
+  Sm& sm = *reinterpret_cast<Sm*>(smraw);
+  sm.th.slots = sm.slots;
+  thomas_init<CB>(sm.th);
+  __syncthreads();
+  uint32_t m = 0;
+  int b = blockIdx.x;
+  if (b < nb) thomas_prefetch<CB>(sm.th, Gf + (size_t)b * Thomas<CB>::PER_BRICK, 0);
+  for (; b < nb; b += gridDim.x) {
+    const double* G = Gf + (size_t)b * Thomas<CB>::PER_BRICK;
+    const int bn = b + (int)gridDim.x;
+    const double* Gn = bn < nb ? Gf + (size_t)bn * Thomas<CB>::PER_BRICK : nullptr;
+    if (!chain && b != (int)blockIdx.x) thomas_prefetch<CB>(sm.th, G, m);
+    for (int c = threadIdx.x; c < C; c += NT) {
+      sm.tv[c] = tin[(size_t)b * C + c];
+      sm.tz[c] = c >= CB * CB ? -0.1 : 0.0;
+    }
+    thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv, 1.0, m, chain ? Gn : nullptr);
+    m += Thomas<CB>::NL;
+    for (int c = threadIdx.x; c < C; c += NT) xout[(size_t)b * C + c] = sm.tv[c];
+    __syncthreads();
+  }
+}
+
+float run_persist(const double* G, const double* t, double* x, int nb, size_t smem, int grid, int chain) {
+  cudaFuncSetAttribute(k_bench_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t a, e;
+  cudaEventCreate(&a);
+  cudaEventCreate(&e);
+  for (int w = 0; w < 3; ++w) k_bench_persist<<<grid, Thomas<CB>::NT, smem>>>(G, t, x, nb, chain);
+  cudaEventRecord(a);
+  const int reps = 20;
+  for (int i = 0; i < reps; ++i) k_bench_persist<<<grid, Thomas<CB>::NT, smem>>>(G, t, x, nb, chain);
+  cudaEventRecord(e);
+  cudaEventSynchronize(e);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, e);
+  return 1e3f * ms / reps;
+}
+
 template <int MODE>
 float run(const double* G, const double* t, double* x, int nb, size_t smem) {
   cudaFuncSetAttribute(k_bench<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -105,8 +159,8 @@ float run_after_dirty(const double* G, const double* t, double* x, int nb, size_
   return 1e3f * tot / reps;
 }
 
-int main() {
-  const int nb = 4096;
+int main(int argc, char** argv) {
+  const int nb = argc > 1 ? atoi(argv[1]) : 4096;  // bricks (4096 = 128^3 cells)
   const size_t per = Thomas<CB>::PER_BRICK, C = CB * CB * CB;
   std::vector<double> hg(per * nb), ht(C * nb);
   for (size_t i = 0; i < hg.size(); ++i) hg[i] = 1e-3 * (double)((i * 2654435761u) % 1000) / 1000.0;
@@ -124,6 +178,21 @@ int main() {
   printf("real   %7.1f us  (%.0f GB/s of G)\n", t0, gb / (t0 * 1e-6));
   printf("L2     %7.1f us\n", t1);
   printf("copy   %7.1f us  (%.0f GB/s of G)\n", t2, gb / (t2 * 1e-6));
+  {
+    // reference result of the one-CTA-per-brick kernel, then the persistent ones
+    std::vector<double> x0(C * nb), x1(C * nb);
+    k_bench<0><<<nb, Thomas<CB>::NT, smem>>>(G, t, x);
+    cudaMemcpy(x0.data(), x, sizeof(double) * x0.size(), cudaMemcpyDeviceToHost);
+    for (int chain = 0; chain < 2; ++chain)
+      for (int per_sm : {3, 4}) {
+        const float tp = run_persist(G, t, x, nb, smem, 148 * per_sm, chain);
+        cudaMemcpy(x1.data(), x, sizeof(double) * x1.size(), cudaMemcpyDeviceToHost);
+        size_t bad = 0;
+        for (size_t i = 0; i < x0.size(); ++i) bad += x0[i] != x1[i];
+        printf("persist chain=%d grid=148x%d  %7.1f us  (%.0f GB/s of G)  mismatches %zu\n", chain, per_sm, tp,
+               gb / (tp * 1e-6), bad);
+      }
+  }
   double* buf;
   cudaMalloc(&buf, (size_t)512 << 20);
   for (size_t mb : {0, 32, 64, 128, 256})
