@@ -278,6 +278,8 @@ def run_reference(args):
 # brick that lie on its surface (SURF), plus the face T's (3 B).
 #  k_post  : r 8 + coef_z 8 + G 288 + z 8 + (Phi 32 + r1 8)*SURF + T 3 = 338.1
 #  k_update: x 16 + p 8 + q 8 + r 16 + coef_z 8 + G 288 + r1 8*SURF     = 348.6
+#  (G: 8 planes of 36 stored 8x8 blocks = 2304 doubles per 64 cells,
+#   smoother.cuh; 264 with the opt-in packed diagonal blocks, TMG_DIAG_PACK=1)
 #  k_restrict: (Phi 32 + r1 8)*SURF + T 3                              = 26.1
 #  k_search: coef 32 + z 8 + p 16 + q 8 (TMG_SEARCH_KAPPA=1: the
 #            coefficients recomputed from kappa, 8 instead of 32)      = 64;
@@ -286,10 +288,11 @@ def run_reference(args):
 # G counts only the distinct factors (x slots / bricks): uniform interior
 # bricks share one factor, whose planes stay in L2.
 SURF = 296 / 512
+G_BYTES_PER_CELL = 2304 * 8 / 64  # Thomas<8>::PLANE doubles per plane of 64 cells
 
 
 def kernel_bytes_per_cell(g_fraction=1.0, interior_fraction=0.0):
-    g = 288 * g_fraction
+    g = G_BYTES_PER_CELL * g_fraction
     search = 40 if os.environ.get("TMG_SEARCH_KAPPA", "0")[:1] == "1" else 64 - 8 * interior_fraction
     return {"post": 24 + g + 40 * SURF + 3, "update": 56 + g + 8 * SURF, "search": search,
             "restrict": 40 * SURF + 3}

@@ -616,6 +616,10 @@ void plan_fine_factors(tmg_ctx* c, Slab& s) {
     call;                       \
     c->kcount += (n_kernels);   \
   } while (0)
+#define KLR(call) /* launcher returns its kernel count */ \
+  do {                                                    \
+    c->kcount += (call);                                  \
+  } while (0)
 
 // single slab: coarse + coarse-coarse levels as one cooperative kernel
 void enqueue_coarse_single(tmg_ctx* c) {
@@ -647,11 +651,11 @@ void enqueue_vcycle_single(tmg_ctx* c, int init, const double* p) {
   Slab& s = c->slabs[0];
   const GridParams& g = s.g;
   cudaStream_t st = c->stream;
-  KL(1, launch_update(g, c->cb, s.coef, s.ff(), s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
+  KLR(launch_update(g, c->cb, s.coef, s.ff(), s.x, p, s.q, s.r, s.r1, s.r1f, s.st, s.partials,
                       s.history, init, st));
   KL(1, restrict_fine(c, s, st));
   enqueue_coarse_single(c);
-  KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
+  KLR(launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, init,
                     st));
 }
 
@@ -719,7 +723,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   cudaStream_t st = c->stream;
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_update(s.g, c->cb, s.coef, s.ff(), s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.r1f, s.st,
+    KLR(launch_update(s.g, c->cb, s.coef, s.ff(), s.x, s.pbuf[par_new], s.q, s.r, s.r1, s.r1f, s.st,
                         s.partials, s.history, init, st));
   if (!init) reduce_finalize(c, kRedUpdate, 0);
   XCH(r1f, sizeof(double) * 6 * c->cb * c->cb, false);  // the boundary kernels read r1's face layers
@@ -727,7 +731,7 @@ void enqueue_vcycle_dist(tmg_ctx* c, int init, int par_new) {
   for (Slab& s : c->slabs) KL(1, restrict_fine(c, s, st));
   enqueue_coarse_dist(c);
   for (Slab& s : c->slabs)
-    KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
+    KLR(launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials,
                       init, st));
   reduce_finalize(c, kRedPost, init);
   XCH(z, sizeof(double) * C, false);
@@ -971,7 +975,7 @@ void enqueue_precond_init(tmg_ctx* c) { enqueue_precond(c, 1, 0); }
 void enqueue_iteration(tmg_ctx* c, int par) {
   const int64_t C = cells_per_brick(c);
   for (Slab& s : c->slabs)
-    KL(1, search(c, s, s.pbuf[par], s.pbuf[par ^ 1], c->stream));
+    KL(search_kernels(c->cb), search(c, s, s.pbuf[par], s.pbuf[par ^ 1], c->stream));
   if (c->dist()) {
     reduce_finalize(c, kRedSearch, 0);
     exchange(c, [&](Slab& s) { return (void*)s.pbuf[par ^ 1]; }, sizeof(double) * C, false);
@@ -1064,10 +1068,10 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
   } else if (hierarchical(c) && !c->fine_bj && c->nu == 1 && c->cb != 0) {
     Slab& s = s0;
     const GridParams& g = s.g;
-    timed(1, [&] { KL(1, launch_update(g, c->cb, s.coef, s.ff(), s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
+    timed(1, [&] { KLR(launch_update(g, c->cb, s.coef, s.ff(), s.x, s.p, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 1, c->stream)); });
     timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
     timed(3, [&] { enqueue_coarse_single(c); });
-    timed(6, [&] { KL(1, launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
+    timed(6, [&] { KLR(launch_post(g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 1, c->stream)); });
   } else {
     timed(7, [&] { enqueue_precond(c, 1, 0); });
   }
@@ -1113,12 +1117,12 @@ void solve_device(tmg_ctx* c, double rtol, int maxit, int use_x0, tmg_report* re
       double* pnew = s.pbuf[par ^ 1];
       par ^= 1;
       const int64_t kb = c->kcount;
-      timed(0, [&] { KL(1, search(c, s, pold, pnew, c->stream)); });
+      timed(0, [&] { KL(search_kernels(c->cb), search(c, s, pold, pnew, c->stream)); });
       if (hierarchical(c) && !c->fine_bj && c->nu == 1 && c->cb != 0) {
-        timed(1, [&] { KL(1, launch_update(s.g, c->cb, s.coef, s.ff(), s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
+        timed(1, [&] { KLR(launch_update(s.g, c->cb, s.coef, s.ff(), s.x, pnew, s.q, s.r, s.r1, s.r1f, s.st, s.partials, s.history, 0, c->stream)); });
         timed(2, [&] { KL(1, restrict_fine(c, s, c->stream)); });
         timed(3, [&] { enqueue_coarse_single(c); });
-        timed(6, [&] { KL(1, launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
+        timed(6, [&] { KLR(launch_post(s.g, c->cb, s.coef, s.tf, s.phi, s.phif, s.ff(), s.r, s.r1, s.r1f, s.ec, s.z, s.st, s.partials, 0, c->stream)); });
       } else {
         timed(7, [&] { enqueue_precond(c, 0, par); });
       }

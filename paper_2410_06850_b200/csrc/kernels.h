@@ -323,6 +323,8 @@ void launch_init(const GridParams& g, int cb, const double* coef, const double* 
 void launch_search(const GridParams& g, int cb, const double* coef, const double* z,
                    const double* p_old, double* p, double* q, PcgState* st, double* partials,
                    cudaStream_t s);
+// kernels launch_search enqueues (k_search + k_search_reduce on the brick kernels)
+int search_kernels(int cb);
 // launch_search with the coefficients recomputed from kappa (tuned bricks)
 void launch_search_kappa(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                          const double* z, const double* p_old, double* p, double* q, PcgState* st,
@@ -336,7 +338,8 @@ void launch_brick_solve(const GridParams& g, int cb, const double* coef, const F
 void launch_add_finish(const GridParams& g, int cb, const double* y, const double* add,
                        double* out, const double* rdot, PcgState* st, double* partials, int init,
                        cudaStream_t s);
-void launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
+// returns the kernels enqueued (the solve kernel, plus k_reduce_fin when its grid sum is deferred)
+int launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
                    const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
                    double* partials, double* history, int init, cudaStream_t s);
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
@@ -346,7 +349,7 @@ void launch_restrict(const GridParams& g, int cb, const double* coef, const doub
 // tf: the face-major T of launch_face_t
 void launch_restrict_bnd(const GridParams& g, int cb, const double* tf, const double* phif,
                          const double* r1f, double* rc, const PcgState* st, cudaStream_t s);
-void launch_post(const GridParams& g, int cb, const double* coef, const double* tf, const double* phi,
+int launch_post(const GridParams& g, int cb, const double* coef, const double* tf, const double* phi,
                  const double* phif, const FineFactors& Gf, const double* r, const double* r1,
                  const double* r1f, const double* ec, double* z, PcgState* st, double* partials,
                  int init, cudaStream_t s);

@@ -152,6 +152,58 @@ __global__ void __launch_bounds__(CB * CB * CB) k_init(GridParams g, const doubl
   }
 }
 
+// Grid sum of an iteration kernel's per-CTA partials (fixed order:
+// thread-strided, warp tree, warps in sequence), then the scalar step of
+// pcg() that follows it: `which` = kRedSearch (p.q -> alpha, solver.cpp:541-549),
+// kRedUpdate (r.r -> stopping rule, :554-560) or kRedPost (r.z -> beta,
+// :562-564). The producers end with their last store: no device-scope fence,
+// no ticket, no CTA waiting to learn whether it was the last one. One CTA;
+// with PDL it is resident while the producer drains.
+__global__ void __launch_bounds__(1024) k_reduce_fin(const double* __restrict__ partials,
+                                                     unsigned int n, PcgState* st, int dist,
+                                                     int which, int init, double* history) {
+  pdl_trigger();
+  __shared__ double red[32];
+  pdl_wait();
+  if (st->done) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four loads in flight per thread
+  unsigned int i = threadIdx.x;
+  for (; i + 3 * 1024 < n; i += 4 * 1024) {
+    s0 += partials[i];
+    s1 += partials[i + 1024];
+    s2 += partials[i + 2 * 1024];
+    s3 += partials[i + 3 * 1024];
+  }
+  for (; i < n; i += 1024) s0 += partials[i];
+  double sum = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < 32; ++w) tot += red[w];
+    if (dist) st->loc[which] = tot;
+    else if (which == kRedSearch) fin_search(st, tot);
+    else if (which == kRedUpdate) finish_rr(st, tot, history);
+    else fin_post(st, tot, init);
+  }
+}
+
+// CTA sum of v in a fixed order into partials[blockIdx.x] (for k_reduce_fin).
+template <int NT>
+__device__ __forceinline__ void cta_partial(double v, double* red, double* partials) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < NT / 32; ++w) sum += red[w];
+    partials[blockIdx.x] = sum;
+  }
+}
+
 // --------------------------------------------------------------- K1 search
 constexpr int kStencilThreads = 256;  // CTA size of the stencil kernels (2 cells/thread at CB = 8)
 
@@ -159,8 +211,14 @@ template <int CB>
 #ifndef TMG_SEARCH_MINB
 #define TMG_SEARCH_MINB 6
 #endif
+#ifndef TMG_FINE_DEFER  // 1: r.r / r.z of k_update / k_post_bnd summed by k_reduce_fin (no tickets)
+#define TMG_FINE_DEFER 1
+#endif
 #ifndef TMG_SEARCH_DIAG  // 1: every brick reads the stored diagonal (A/B)
 #define TMG_SEARCH_DIAG 0
+#endif
+#ifndef TMG_SEARCH_DEFER  // 1: p.q summed by k_reduce_fin instead of the last CTA (ticket)
+#define TMG_SEARCH_DEFER 1
 #endif
 __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(GridParams g, const double* __restrict__ coef,
                                                               int64_t M, const double* __restrict__ z,
@@ -206,6 +264,9 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
   };
   if (with_dg) rows(std::true_type{});
   else rows(std::false_type{});
+#if TMG_SEARCH_DEFER
+  cta_partial<NT>(pq, red, partials);  // the grid sum is k_reduce_fin's
+#else
   double v[1] = {pq};
   block_sum_k<NT, 1>(v, red);
   double tot[1];
@@ -213,6 +274,7 @@ __global__ void __launch_bounds__(kStencilThreads, TMG_SEARCH_MINB) k_search(Gri
     if (g.dist) st->loc[kRedSearch] = tot[0];
     else fin_search(st, tot[0]);
   }
+#endif
 }
 
 // K1 from the conductivity (opt-in, TMG_SEARCH_KAPPA=1; slower, abi.cu
@@ -335,6 +397,9 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
     r1f[(size_t)b * 6 * P + h] = sm.tv[c];
   }
   if (!init) {
+#if TMG_FINE_DEFER
+    cta_partial<NT>(rr, sm.red, partials);  // r.r and the stopping rule: k_reduce_fin
+#else
     double v[1] = {rr};
     block_sum_k<NT, 1>(v, sm.red);
     double tot[1];
@@ -342,6 +407,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
       if (g.dist) st->loc[kRedUpdate] = tot[0];
       else finish_rr(st, tot[0], history);  // :554-560
     }
+#endif
   }
 }
 
@@ -642,6 +708,9 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
       rz += rown[k] * zv;
     }
   }
+#if TMG_FINE_DEFER
+  cta_partial<NT>(rz, sm.red, partials);  // r.z and beta: k_reduce_fin
+#else
   double v[1] = {rz};
   block_sum_k<NT, 1>(v, sm.red);
   double tot[1];
@@ -649,6 +718,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
     if (g.dist) st->loc[kRedPost] = tot[0];
     else fin_post(st, tot[0], init);
   }
+#endif
 }
 
 // --------------------------------- generic block solve (nu != 1 V-cycles)
@@ -827,19 +897,28 @@ void launch_search(const GridParams& g, int cb, const double* coef, const double
   if (cb == 0) return launch_g_search(g, coef, z, p_old, p, q, st, partials, s);
   if (cb == 8) launch_pdl(k_search<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, coef, M, z, p_old, p, q, st, partials);
   else launch_pdl(k_search<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, coef, M, z, p_old, p, q, st, partials);
+#if TMG_SEARCH_DEFER
+  launch_pdl(k_reduce_fin, dim3(1), dim3(1024), 0, s, (const double*)partials, (unsigned int)g.nbo, st,
+             (int)g.dist, (int)kRedSearch, 0, (double*)nullptr);
+#endif
 }
+int search_kernels(int cb) { return cb != 0 && TMG_SEARCH_DEFER ? 2 : 1; }
 void launch_search_kappa(const GridParams& g, int cb, const double* kappa, const uint8_t* dmask,
                          const double* z, const double* p_old, double* p, double* q, PcgState* st,
                          double* partials, cudaStream_t s) {
   if (cb == 8) launch_pdl(k_search_kappa<8>, dim3((unsigned)g.nbo), dim3(kStencilThreads), 0, s, g, kappa, dmask, z, p_old, p, q, st, partials);
   else launch_pdl(k_search_kappa<4>, dim3((unsigned)g.nbo), dim3(32), 0, s, g, kappa, dmask, z, p_old, p, q, st, partials);
 }
-void launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
-                   const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
-                   double* partials, double* history, int init, cudaStream_t s) {
+int launch_update(const GridParams& g, int cb, const double* coef, const FineFactors& Gf, double* x,
+                  const double* p, const double* q, double* r, double* r1, double* r1f, PcgState* st,
+                  double* partials, double* history, int init, cudaStream_t s) {
   const int64_t M = g.mst;
   if (cb == 8) launch_pdl(k_update<8>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
   else launch_pdl(k_update<4>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), update_smem(cb), s, g, coef, M, Gf, x, p, q, r, r1, r1f, st, partials, history, init);
+  if (!TMG_FINE_DEFER || init) return 1;
+  launch_pdl(k_reduce_fin, dim3(1), dim3(1024), 0, s, (const double*)partials, (unsigned int)g.nbo, st,
+             (int)g.dist, (int)kRedUpdate, 0, history);
+  return 2;
 }
 void launch_restrict(const GridParams& g, int cb, const double* coef, const double* phi,
                      const double* r, const double* r1, double* rc, const PcgState* st,
@@ -883,10 +962,10 @@ void launch_phi_faces(const GridParams& g, int cb, const double* phi, double* ph
     else k_phi_faces<4, LCP><<<(unsigned)nb, 256, 0, s>>>(phi, phif, b0);
   });
 }
-void launch_post(const GridParams& g, int cb, const double* coef, const double* tf,
-                 const double* phi_full, const double* phif, const FineFactors& Gf, const double* r,
-                 const double* r1_full, const double* r1f, const double* ec, double* z, PcgState* st,
-                 double* partials, int init, cudaStream_t s) {
+int launch_post(const GridParams& g, int cb, const double* coef, const double* tf,
+                const double* phi_full, const double* phif, const FineFactors& Gf, const double* r,
+                const double* r1_full, const double* r1f, const double* ec, double* z, PcgState* st,
+                double* partials, int init, cudaStream_t s) {
   const int64_t M = g.mst;
   const double* phi = TMG_POST_BND ? phif : phi_full;
   const double* r1 = TMG_POST_BND ? r1f : r1_full;
@@ -895,6 +974,10 @@ void launch_post(const GridParams& g, int cb, const double* coef, const double* 
     if (cb == 8) launch_pdl(K_POST<8, LCP>, dim3((unsigned)g.nbo), dim3(Thomas<8>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
     else launch_pdl(K_POST<4, LCP>, dim3((unsigned)g.nbo), dim3(Thomas<4>::NT), post_smem(cb), s, g, coef, tf, M, phi, Gf, r, r1, ec, z, st, partials, init);
   });
+  if (!(TMG_FINE_DEFER && TMG_POST_BND)) return 1;  // the literal k_post keeps its ticket
+  launch_pdl(k_reduce_fin, dim3(1), dim3(1024), 0, s, (const double*)partials, (unsigned int)g.nbo, st,
+             (int)g.dist, (int)kRedPost, init, (double*)nullptr);
+  return 2;
 }
 void launch_jacobi_step(const GridParams& g, int cb, const double* dinv, double* x, const double* p,
                         const double* q, double* r, double* z, PcgState* st, double* partials,

@@ -96,12 +96,23 @@ __global__ void __launch_bounds__(factor_threads<CB>()) k_thomas_factor(GridPara
       }
     }
     __syncthreads();
-    // lower block-triangle of 8 x 8 blocks, block (I, J <= I) at I(I+1)/2 + J
-    for (int e = t; e < Thomas<CB>::PLANE; e += NTF) {
+    // stored blocks in smoother.cuh's order and swizzle (block_of / plane_off);
+    // packed diagonals: the off-diagonal blocks, then 40 doubles per diagonal block
+    constexpr int NWHOLE = kDiagPacked ? Thomas<CB>::NOFF : Thomas<CB>::NBLK;
+    for (int e = t; e < NWHOLE * 64; e += NTF) {
       const int blk = e / 64, rr = (e % 64) / 8, cc = e % 8;
       int I, J;
       block_of<CB>(blk, I, J);
       Gout[(size_t)k * Thomas<CB>::PLANE + plane_off(blk, rr, cc)] = Gprev[(8 * I + rr) * GP + 8 * J + cc];
+    }
+    if constexpr (kDiagPacked) {
+      for (int e = t; e < Thomas<CB>::NBK * kDiagBlock; e += NTF) {
+        const int d = e / kDiagBlock;
+        int row, col;
+        const bool stored = diag_slot(e % kDiagBlock, row, col);
+        Gout[(size_t)k * Thomas<CB>::PLANE + NWHOLE * 64 + e] =
+            stored ? Gprev[(8 * d + row) * GP + 8 * d + col] : 0.0;
+      }
     }
     __syncthreads();
   }

@@ -41,23 +41,36 @@ namespace tmg {
 constexpr int kMvRows = TMG_MV_ROWS;
 constexpr int kMvTpb = 8 / kMvRows;  // threads per 8 x 8 block
 static_assert(kMvRows == 1 || kMvRows == 2 || kMvRows == 4, "TMG_MV_ROWS");
+// Opt-in (TMG_DIAG_PACK=1): diagonal 8 x 8 blocks stored as their lower
+// triangle (two rows per thread only): 40 instead of 64 doubles per block,
+// 2112 instead of 2304 per CB = 8 plane (264 instead of 288 B/cell of factor
+// traffic, 2.4 GB less at 512^3). The diagonal blocks get a warp of their own
+// (mv_partials_diag). Measured at configs[3]: the same time per iteration
+// (21.82 against 21.77 ms) -- a plane step is bound by its per-warp chain and
+// shared-memory wavefronts (quarter-warp granular, so the predicated loads
+// save none), not by the plane's bytes -- so the whole-block layout stays the
+// default.
+#ifndef TMG_DIAG_PACK
+#define TMG_DIAG_PACK 0
+#endif
+constexpr bool kDiagPacked = TMG_DIAG_PACK && kMvRows == 2;
+constexpr int kDiagBlock = kDiagPacked ? 40 : 64;  // stored doubles per diagonal block
 
 template <int CB>
 struct Thomas {
   static constexpr int P = CB * CB;                 // cells per plane
   static constexpr int NBK = P / 8;                 // 8-row block rows per plane
   static constexpr int NBLK = NBK * (NBK + 1) / 2;  // stored blocks per plane
-  static constexpr int PLANE = NBLK * 64;           // doubles per plane
+  static constexpr int NOFF = NBK * (NBK - 1) / 2;  // of which off-diagonal
+  // doubles per plane: the off-diagonal blocks first, then the diagonal ones
+  static constexpr int PLANE = kDiagPacked ? NOFF * 64 + NBK * kDiagBlock : NBLK * 64;
   static constexpr int PER_BRICK = CB * PLANE;      // doubles per brick
   static constexpr int NL = 2 * CB - 1;             // plane mat-vecs per solve
-  static constexpr int MV = NBLK * kMvTpb;          // mat-vec threads
+  // mat-vec threads: packed diagonals start at a warp boundary (DW)
+  static constexpr int DW = kDiagPacked ? (NOFF * kMvTpb + 31) / 32 * 32 : 0;
+  static constexpr int MV = kDiagPacked ? DW + NBK * kMvTpb : NBLK * kMvTpb;
   static constexpr int NT = (MV + 31) / 32 * 32;    // CTA size of the solve kernels
   __host__ __device__ static constexpr int plane_of(int n) { return n < CB ? n : 2 * CB - 2 - n; }
-  // storage offset of element (i, j), i, j < P (any order: symmetric)
-  __host__ __device__ static constexpr int off(int i, int j) {
-    return (i / 8 >= j / 8) ? (((i / 8) * (i / 8 + 1) / 2 + j / 8) * 64 + (i % 8) * 8 + j % 8)
-                            : (((j / 8) * (j / 8 + 1) / 2 + i / 8) * 64 + (j % 8) * 8 + i % 8);
-  }
 };
 
 // Storage / thread order of the 36 stored 8x8 blocks (I, J <= I) of a CB = 8
@@ -70,9 +83,15 @@ struct Thomas {
 // warp's blocks share w_J (broadcast loads) and their row products land in
 // one contiguous run of part[J][]: warp 0 = column 0, warp 1 = column 1 +
 // (7,7), warp 2 = columns 2 + 6, warp 3 = columns 3 + 5, warp 4 = column 4.
+// Packed diagonals: the 28 off-diagonal blocks only, block columns again:
+// warp 0 = column 0 + (7,6), warp 1 = columns 1 + 5, warp 2 = columns 2 + 4,
+// warp 3 = column 3; the diagonal blocks (I, I) follow in order of I.
 static __constant__ unsigned char kBlockOrder8[36] =
 #if TMG_MV_ROWS == 1
     {44, 33, 41, 36, 60, 51, 59, 52, 17, 18, 25, 9, 26, 50, 63, 58, 24, 27, 16, 0, 57, 62, 54, 49, 45, 8, 32, 40, 61, 56, 53, 48, 34, 43, 42, 35};
+#elif TMG_DIAG_PACK && TMG_MV_ROWS == 2
+    {8, 16, 24, 32, 40, 48, 56, 62, 17, 25, 33, 41, 49, 57, 53, 61, 26, 34, 42, 50, 58, 44, 52, 60,
+     35, 43, 51, 59, 0, 9, 18, 27, 36, 45, 54, 63};
 #else
     {0, 8, 16, 24, 32, 40, 48, 56, 9, 17, 25, 33, 41, 49, 57, 63, 18, 26, 34, 42, 50, 58, 54, 62,
      27, 35, 43, 51, 59, 45, 53, 61, 36, 44, 52, 60};
@@ -84,6 +103,15 @@ __device__ __forceinline__ void block_of(int blk, int& I, int& J) {
     const int v = kBlockOrder8[blk];
     I = v >> 3;
     J = v & 7;
+  } else if constexpr (kDiagPacked) {  // strictly lower blocks row-major, then the diagonal
+    constexpr int NOFF = Thomas<CB>::NOFF;
+    if (blk >= NOFF) {
+      I = J = blk - NOFF;
+    } else {
+      I = 1;
+      while (I * (I + 1) / 2 <= blk) ++I;
+      J = blk - I * (I - 1) / 2;
+    }
   } else {  // row-major lower block triangle
     I = 0;
     while ((I + 1) * (I + 2) / 2 <= blk) ++I;
@@ -103,10 +131,27 @@ __host__ __device__ constexpr int mv_chunk_pos(int k, int sub, int tid) {
   return kMvRows == 1 ? ((k + (sub >> 1)) & 3) : ((k & ~7) | ((k + (tid & 7)) & 7));
 }
 
-// Storage offset (doubles) of element (r, c) of stored block `blk` in a plane.
+// Storage offset (doubles) of element (r, c) of stored block `blk` in a plane
+// (whole blocks: every block, or the off-diagonal ones with packed diagonals).
 __host__ __device__ constexpr int plane_off(int blk, int r, int c) {
   const int sub = r / kMvRows, k = (r % kMvRows) * 4 + (c >> 1);
   return blk * 64 + sub * 8 * kMvRows + 2 * mv_chunk_pos(k, sub, blk * kMvTpb + sub) + (c & 1);
+}
+
+// Packed diagonal block (40 doubles): thread `sub` of the block owns rows
+// 2 sub and 2 sub + 1; its region starts at 2 sub (sub + 1) doubles and holds
+// row 2 sub, columns 0 .. 2 sub + 1 (the last one, above the diagonal, stored
+// as 0), then row 2 sub + 1, columns 0 .. 2 sub + 1.
+// diag_slot: the element (row, col) stored at slot s of a packed block;
+// returns false for the zero pads.
+__host__ __device__ constexpr int diag_region(int sub) { return 2 * sub * (sub + 1); }
+__host__ __device__ constexpr bool diag_slot(int s, int& row, int& col) {
+  int sub = 0;
+  while (sub < 3 && s >= diag_region(sub + 1)) ++sub;
+  const int o = s - diag_region(sub), len = 2 * sub + 2;
+  row = o < len ? 2 * sub : 2 * sub + 1;
+  col = o < len ? o : o - len;
+  return col <= row;
 }
 
 #ifndef TMG_SLOTS
@@ -159,8 +204,17 @@ template <int CB>
 __device__ __forceinline__ MvRole<CB> mv_role() {
   MvRole<CB> m;
   const int tid = threadIdx.x;
-  m.active = tid < Thomas<CB>::MV;
-  m.blk = m.active ? tid / kMvTpb : 0;
+  if constexpr (kDiagPacked) {
+    // off-diagonal blocks on threads [0, NOFF * TPB), the diagonal warp(s)
+    // from DW: block NOFF + d on threads DW + d * TPB ...
+    constexpr int NOFF = Thomas<CB>::NOFF, DW = Thomas<CB>::DW;
+    const bool diag = tid >= DW;
+    m.active = diag ? tid < Thomas<CB>::MV : tid < NOFF * kMvTpb;
+    m.blk = !m.active ? (diag ? NOFF : 0) : diag ? NOFF + (tid - DW) / kMvTpb : tid / kMvTpb;
+  } else {
+    m.active = tid < Thomas<CB>::MV;
+    m.blk = m.active ? tid / kMvTpb : 0;
+  }
   m.r = tid % kMvTpb;  // index inside the block: rows R m.r .. R m.r + R - 1
   block_of<CB>(m.blk, m.I, m.J);
   return m;
@@ -237,6 +291,59 @@ __device__ __forceinline__ void ld_run(const double* p, double (&v)[R]) {
     }
 }
 
+// Packed diagonal block (I, I) of a plane mat-vec step (two rows per thread,
+// the diagonal warp): the stored lower triangle gives the row products over
+// columns <= row and, transposed, the column products of the strictly lower
+// part; both land on the thread's own rows 8 I + 2 sub, + 1 after the
+// reduce-scatter, so the block contributes one partial per row (part[I][]).
+template <int CB>
+__device__ __forceinline__ void mv_partials_diag(ThomasSmem<CB>& sm, const double* Gp, const double* w,
+                                                 const MvRole<CB>& m) {
+  const int sub = m.r, d = m.blk - Thomas<CB>::NOFF;
+  const uint32_t reg = smem_u32(Gp + Thomas<CB>::NOFF * 64 + d * kDiagBlock + diag_region(sub));
+  double gv[2][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // chunk q (columns 2q, 2q + 1) of both rows, stored for q <= sub
+    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+    if (q <= sub) {
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0.x), "=d"(v0.y) : "r"(reg + 16u * q));
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                   : "=d"(v1.x), "=d"(v1.y)
+                   : "r"(reg + 16u * (sub + 1 + q)));
+    }
+    gv[0][2 * q] = v0.x;
+    gv[0][2 * q + 1] = v0.y;
+    gv[1][2 * q] = v1.x;
+    gv[1][2 * q + 1] = v1.y;
+  }
+  double ro[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) {
+      const double2 wv = *reinterpret_cast<const double2*>(w + 8 * m.I + c);  // broadcast
+      a0 = fma(gv[i][c], wv.x, a0);
+      a1 = fma(gv[i][c + 1], wv.y, a1);
+    }
+    ro[i] = a0 + a1;
+  }
+  double wr[2];
+  ld_run<2>(w + 8 * m.I + 2 * sub, wr);
+  if (!m.active) wr[0] = wr[1] = 0.0;
+  double b[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {  // strictly lower entries only: the diagonal belongs to the row products
+    b[c] = (c == 2 * sub ? 0.0 : gv[0][c]) * wr[0];
+    b[c] = fma(c == 2 * sub + 1 ? 0.0 : gv[1][c], wr[1], b[c]);
+  }
+  double cs[2];
+  reduce_scatter<4>(b, sub, cs);
+  ro[0] += cs[0];
+  ro[1] += cs[1];
+  if (m.active) st_run<2>(&sm.part[m.I][8 * m.I + 2 * sub], ro);
+}
+
 // One plane mat-vec step: partial products into part[][].
 template <int CB>
 __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp, const double* w,
@@ -244,6 +351,9 @@ __device__ __forceinline__ void mv_partials(ThomasSmem<CB>& sm, const double* Gp
   constexpr int R = kMvRows, TPB = kMvTpb;
   // whole warps take part (the shuffles below need every lane)
   if ((int)(threadIdx.x >> 5) >= (Thomas<CB>::MV + 31) / 32) return;
+  if constexpr (kDiagPacked) {
+    if ((int)threadIdx.x >= Thomas<CB>::DW) return mv_partials_diag<CB>(sm, Gp, w, m);
+  }
   const bool off_diag = m.active && m.J < m.I;
   double gv[R][8];
   const uint32_t reg = smem_u32(Gp + m.blk * 64 + m.r * 8 * R);  // the thread's R rows
