@@ -375,17 +375,39 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_update(GridParams g, cons
   const int t = threadIdx.x;
   const double alpha = init ? 0.0 : st->alpha;
   double rr = 0.0;
-  for (int c = t; c < C; c += NT) {
-    const size_t s = bofs(b, C) + c;
-    double rv = r[s];
-    if (!init) {
-      x[s] = x[s] + alpha * p[s];  // solver.cpp:550-553
-      rv = rv - alpha * q[s];
-      r[s] = rv;
-      rr += rv * rv;
+  {
+    // every global load of the thread's cells first, then the updates and
+    // stores (x and r are read and written: in one rolled loop the stores
+    // fence the next cell's loads and the brick pays one DRAM round trip per
+    // NT cells)
+    constexpr int KC = (C + NT - 1) / NT;
+    double rv[KC], xv[KC], pv[KC], qv[KC], tzv[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const int c = t + k * NT, cc = c < C ? c : t;
+      const size_t s = bofs(b, C) + cc;
+      rv[k] = r[s];
+      xv[k] = init ? 0.0 : x[s];
+      pv[k] = init ? 0.0 : p[s];
+      qv[k] = init ? 0.0 : q[s];
+      tzv[k] = (G && cc >= P) ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
     }
-    sm.tv[c] = rv;
-    sm.tz[c] = (G && c >= P) ? __ldg(coef + 2 * M + s - P) : 0.0;  // T_z to the cell below
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      const int c = t + k * NT;
+      if (c < C) {
+        const size_t s = bofs(b, C) + c;
+        double v = rv[k];
+        if (!init) {
+          x[s] = xv[k] + alpha * pv[k];  // solver.cpp:550-553
+          v = v - alpha * qv[k];
+          r[s] = v;
+          rr += v * v;
+        }
+        sm.tv[c] = v;
+        sm.tz[c] = tzv[k];
+      }
+    }
   }
   brick_inverse<CB>(sm.th, G, sm.tv, sm.tz, gsl.scale, g);  // r1 = S(r), solver.cpp:280-281
   if (TMG_R1_FULL)
@@ -459,8 +481,11 @@ __global__ void __launch_bounds__(kStencilThreads, 6) k_restrict(GridParams g, c
 // Phi_I(c_f) T_f r1_nb(f) — the same algebra as solver.cpp:285-289 without
 // the brick's own r, r1 and the interior stencil (43% fewer bytes). Not valid
 // for cc-element fine blocks, which keep k_restrict.
+#ifndef TMG_RESTRICT_MINB
+#define TMG_RESTRICT_MINB 8
+#endif
 template <int CB, int LCP>
-__global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, 8) k_restrict_bnd(
+__global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, TMG_RESTRICT_MINB) k_restrict_bnd(
     GridParams g, const double* __restrict__ tfa, int64_t M, const double* __restrict__ phif,
     const double* __restrict__ r1f, double* rc, const PcgState* st) {
   pdl_trigger();
@@ -645,47 +670,59 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_post_bnd(GridParams g, co
   }
   const int t = threadIdx.x;
   const size_t ob = bofs(bc.b, C);
-  // surface terms T_f r2_nb(f): every load of the thread's face slots first
-  constexpr int NS = 6 * F, KS = (NS + NT - 1) / NT;
+  // surface terms T_f r2_nb(f), r2 = r1 + R_c^T ec on the halo (solver.cpp:
+  // 322-324): every global load of the thread first -- unconditional, on
+  // clamped indices, so none of them waits behind a branch or a dependent
+  // FMA chain (one DRAM round trip per brick instead of one per face slot
+  // and cell) -- then the arithmetic. The neighbours' ec go through shared
+  // memory (24 values, sm.red is free until the final sum).
+  constexpr int NS = 6 * F, KS = (NS + NT - 1) / NT, KC = (C + NT - 1) / NT;
+  if (t < 6 * LCP) {
+    const int nb = nbr_brick(g, bc, t / LCP);
+    sm.red[t] = nb >= 0 ? __ldg(ec + (size_t)nb * LCP + t % LCP) : 0.0;
+  }
+  double r1v[KS], tfv[KS], phv[KS][LCP], rown[KC], tzv[KC];
+  int face[KS];  // face of slot k, or -1: no neighbour / no slot
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int h = t + k * NT, hc = h < NS ? h : 0, f = hc / F, q = hc % F;
+    const int nb = nbr_brick(g, bc, f);
+    face[k] = (h < NS && nb >= 0) ? f : -1;
+    const size_t fb = ((size_t)(nb >= 0 ? nb : bc.b) * 6 + (f ^ 1));  // the neighbour's face f^1 (face-major)
+    r1v[k] = __ldg(r1f + fb * F + q);
+#pragma unroll
+    for (int a = 0; a < LCP; ++a) phv[k][a] = __ldg(phif + (fb * LCP + a) * F + q);
+    tfv[k] = __ldg(tfa + (size_t)bc.b * 6 * F + hc);  // face-major T (k_face_t)
+  }
+  // z_I = A_II^{-1} (r_I + t_I) = r1_I + A_II^{-1} t_I: the solve takes r + t
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int c = t + k * NT, cc = c < C ? c : t;
+    rown[k] = __ldg(r + ob + cc);
+    tzv[k] = (G && cc >= F) ? __ldg(coef + 2 * M + ob + cc - F) : 0.0;  // T_z to the cell below
+  }
+  __syncthreads();  // ec of the six neighbours
   double val[KS];
   int cell[KS], axis[KS];
 #pragma unroll
   for (int k = 0; k < KS; ++k) {
-    const int h = t + k * NT;
-    val[k] = 0.0;
-    axis[k] = -1;
-    cell[k] = 0;
-    if (h < NS) {
-      int f, ti, nl;
-      halo_slot<CB>(h, f, ti, nl);
-      const int nb = nbr_brick(g, bc, f);
-      if (nb >= 0) {
-        const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
-        const bool hi = f & 1;
-        const int e = hi ? CB - 1 : 0;
-        const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
-        const size_t onb = bofs(nb, C);
-        // r2 = r1 + R_c^T ec on the halo (solver.cpp:322-324), r1 from the neighbour's face
-        double r2 = __ldg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);
+    const int f = face[k] < 0 ? 0 : face[k], q = (t + k * NT) % F, u = q % CB, w = q / CB, ax = f >> 1;
+    const int e = (f & 1) ? CB - 1 : 0;
+    double r2 = r1v[k];
 #pragma unroll
-        for (int a = 0; a < LCP; ++a)  // the neighbour's face f^1 (face-major phif)
-          r2 += __ldg(phif + (((size_t)nb * 6 + (f ^ 1)) * LCP + a) * F + q) * __ldg(ec + (size_t)nb * LCP + a);
-        val[k] = __ldg(tfa + (size_t)bc.b * 6 * F + h) * r2;  // face-major T (k_face_t)
-        axis[k] = ax;
-        cell[k] = c;
-      }
-    }
+    for (int a = 0; a < LCP; ++a) r2 += phv[k][a] * sm.red[f * LCP + a];
+    val[k] = face[k] < 0 ? 0.0 : tfv[k] * r2;
+    axis[k] = face[k] < 0 ? -1 : ax;
+    cell[k] = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
   }
-  // z_I = A_II^{-1} (r_I + t_I) = r1_I + A_II^{-1} t_I: the solve takes r + t
-  constexpr int KC = (C + NT - 1) / NT;
-  double rown[KC];
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
     const int c = t + k * NT;
-    rown[k] = c < C ? __ldg(r + ob + c) : 0.0;
     if (c < C) {
       sm.tv[c] = rown[k];
-      sm.tz[c] = (G && c >= F) ? __ldg(coef + 2 * M + ob + c - F) : 0.0;  // T_z to the cell below
+      sm.tz[c] = tzv[k];
+    } else {
+      rown[k] = 0.0;
     }
   }
   // t_c, one axis per pass (the two faces of a pass touch disjoint cells;

@@ -49,15 +49,14 @@ __device__ __forceinline__ size_t bofs(int b, int C) { return (size_t)b * (size_
 
 // Neighbour brick across face f (0 x-lo .. 5 z-hi) or -1.
 __device__ __forceinline__ int nbr_brick(const GridParams& g, const BrickCoord& bc, int f) {
+  // selects, no branches: f differs between the lanes of a warp
   const int nbx = (int)g.nbx, nby = (int)g.nby, nbz = (int)g.nbz;
-  switch (f) {
-    case 0: return bc.bi > 0 ? bc.b - 1 : -1;
-    case 1: return bc.bi + 1 < nbx ? bc.b + 1 : -1;
-    case 2: return bc.bj > 0 ? bc.b - nbx : -1;
-    case 3: return bc.bj + 1 < nby ? bc.b + nbx : -1;
-    case 4: return bc.bk > 0 ? bc.b - nbx * nby : -1;
-    default: return bc.bk + 1 < nbz ? bc.b + nbx * nby : -1;
-  }
+  const int ax = f >> 1;
+  const int coord = ax == 0 ? bc.bi : ax == 1 ? bc.bj : bc.bk;
+  const int n = ax == 0 ? nbx : ax == 1 ? nby : nbz;
+  const int stride = ax == 0 ? 1 : ax == 1 ? nbx : nbx * nby;
+  const bool inside = (f & 1) ? coord + 1 < n : coord > 0;
+  return inside ? bc.b + ((f & 1) ? stride : -stride) : -1;
 }
 
 // Halo slot s in [0, 6*CB^2): face f = s / CB^2; returns the tile index and the
