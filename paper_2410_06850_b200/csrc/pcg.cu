@@ -498,28 +498,32 @@ __global__ void __launch_bounds__(CB == 8 ? kStencilThreads : 96, TMG_RESTRICT_M
   const BrickCoord bc = brick_coord(g, (int)(blockIdx.x + g.b0));
   const int t = threadIdx.x;
   const size_t ob = bofs(bc.b, C);
+  // every load of the thread's face slots first (unconditional, clamped
+  // indices), then the products: one DRAM round trip per brick
+  double tfv[KS], r1v[KS], phv[KS][LCP];
+  bool ok[KS];
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    const int h = t + k * NT, hc = h < NS ? h : 0, f = hc / F, q = hc % F;
+    const int nb = nbr_brick(g, bc, f);
+    ok[k] = h < NS && nb >= 0;  // domain boundary: Dirichlet terms live in the diagonal
+    tfv[k] = __ldg(tfa + (size_t)bc.b * 6 * F + hc);  // T of the face (face-major copy, k_face_t)
+    r1v[k] = __ldg(r1f + ((size_t)(nb >= 0 ? nb : bc.b) * 6 + (f ^ 1)) * F + q);  // r1 on the neighbour's face
+#pragma unroll
+    for (int a = 0; a < LCP; ++a)  // own face f (face-major phif)
+      phv[k][a] = __ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q);
+  }
   double v[LCP] = {};
 #pragma unroll
   for (int k = 0; k < KS; ++k) {
-    const int h = t + k * NT;
-    if (h >= NS) break;
-    int f, ti, nl;
-    halo_slot<CB>(h, f, ti, nl);
-    const int nb = nbr_brick(g, bc, f);
-    if (nb < 0) continue;  // domain boundary: Dirichlet terms live in the diagonal
-    const int q = h % F, u = q % CB, w = q / CB, ax = f >> 1;
-    const bool hi = f & 1;
-    const int e = hi ? CB - 1 : 0;
-    const int c = ax == 0 ? e + CB * (u + CB * w) : ax == 1 ? u + CB * (e + CB * w) : u + CB * (w + CB * e);
-    // T of the face (face-major copy, k_face_t)
-    const double tf = __ldg(tfa + (size_t)bc.b * 6 * F + h);
-    const double val = tf * __ldg(r1f + ((size_t)nb * 6 + (f ^ 1)) * F + q);  // r1 on the neighbour's face
+    const double val = ok[k] ? tfv[k] * r1v[k] : 0.0;
 #pragma unroll
-    for (int a = 0; a < LCP; ++a)  // own face f (face-major phif)
-      v[a] = fma(__ldg(phif + (((size_t)bc.b * 6 + f) * LCP + a) * F + q), val, v[a]);
+    for (int a = 0; a < LCP; ++a) v[a] = fma(phv[k][a], val, v[a]);
   }
   block_sum_k<NT, LCP>(v, red);
-  if (t < LCP) rc[(size_t)bc.b * LCP + t] = v[t];
+#pragma unroll
+  for (int a = 0; a < LCP; ++a)
+    if (t == a) rc[(size_t)bc.b * LCP + a] = v[a];
 }
 
 // ---------------------------------------------------------------- K4 post
