@@ -19,10 +19,11 @@
 // blocks are kept whole. 36 blocks = 2304 doubles (18 KiB) per plane at
 // CB = 8. Planes stream global -> shared through a ring of kSlots TMA bulk
 // copies (cp.async.bulk + mbarrier complete_tx) issued kSlots plane-steps
-// ahead. Each mat-vec thread owns one row of one block: it applies the row to
-// w (row product, y_I) and — for off-diagonal blocks — its transpose (column
-// products, y_J, reduce-scattered across the block's 8 lanes with shuffles).
-// Every output row then has exactly NBK partial sums, added in a fixed order.
+// ahead. Each mat-vec thread owns R rows of one block (TMG_MV_ROWS, default
+// 2): it applies them to w (row products, y_I) and — for off-diagonal blocks
+// — their transposes (column products, y_J, reduce-scattered across the
+// block's 8/R lanes with shuffles). Every output row then has exactly NBK
+// partial sums, added in a fixed order.
 #pragma once
 #include "stencil.cuh"
 #include "tma.cuh"

@@ -5,6 +5,11 @@
 //   0  real: each brick's 8 G planes (forward + backward sweep)
 //   1  L2:   every plane load reads brick 0 / plane 0 (L2-resident)
 //   2  copy: ring only (loads issued and awaited, no mat-vec work)
+// plus a persistent variant of mode 0 (k_bench_persist: 148 x 3 / 4 CTAs,
+// bricks strided, with and without the TMA ring carried across bricks).
+// argv[1] = number of bricks (default 4096 = 128^3 cells; 32768 for a
+// steady-state figure). -DTMG_MV_ROWS / -DTMG_DIAG_PACK / -DTMG_L2_AHEAD /
+// -DTMG_G_HINTS select the variants measured in DESIGN.md §4.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
 //        --expt-relaxed-constexpr -I paper_2410_06850_b200/csrc tools/thomas_bench.cu
 #include <cstdio>
