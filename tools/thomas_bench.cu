@@ -21,9 +21,19 @@
 using namespace tmg;
 
 constexpr int CB = 8;
+// -DBENCH_CTAS=5 -DBENCH_TZ_GLOBAL=1 (with -DTMG_DIAG_PACK=1): the shared-memory
+// budget of five CTAs per SM -- T_z read through a global pointer instead of
+// the 4 KB shared array
+#ifndef BENCH_CTAS
+#define BENCH_CTAS 4
+#endif
+#ifndef BENCH_TZ_GLOBAL
+#define BENCH_TZ_GLOBAL 0
+#endif
+__device__ double g_tz[CB * CB * CB];
 
 template <int MODE>
-__global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __restrict__ Gf,
+__global__ void __launch_bounds__(Thomas<CB>::NT, BENCH_CTAS) k_bench(const double* __restrict__ Gf,
                                                             const double* __restrict__ tin,
                                                             double* xout) {
   constexpr int C = CB * CB * CB, NT = Thomas<CB>::NT;
@@ -32,9 +42,16 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __res
     double slots[kSlots][Thomas<CB>::PLANE];
     ThomasSmem<CB> th;
     double tv[C];
+#if !BENCH_TZ_GLOBAL
     double tz[C];
+#endif
   };
   Sm& sm = *reinterpret_cast<Sm*>(smraw);
+#if BENCH_TZ_GLOBAL
+  const double* tzp = g_tz;
+#else
+  double* tzp = sm.tz;
+#endif
   const int b = blockIdx.x;
   const double* G = Gf + (MODE == 1 ? 0 : (size_t)b * Thomas<CB>::PER_BRICK);
   sm.th.slots = sm.slots;
@@ -43,7 +60,9 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __res
   thomas_prefetch<CB>(sm.th, G);
   for (int c = threadIdx.x; c < C; c += NT) {
     sm.tv[c] = tin[(size_t)b * C + c];
+#if !BENCH_TZ_GLOBAL
     sm.tz[c] = c >= CB * CB ? -0.1 : 0.0;
+#endif
   }
   if (MODE == 2) {
     // stream the same 15 plane loads through the ring, no compute
@@ -62,7 +81,7 @@ __global__ void __launch_bounds__(Thomas<CB>::NT, 4) k_bench(const double* __res
       __syncthreads();
     }
   } else {
-    thomas_solve<CB>(sm.th, G, sm.tv, sm.tz, sm.tv);
+    thomas_solve<CB>(sm.th, G, sm.tv, tzp, sm.tv);
   }
   __syncthreads();
   for (int c = threadIdx.x; c < C; c += NT) xout[(size_t)b * C + c] = sm.tv[c];
@@ -176,13 +195,19 @@ int main(int argc, char** argv) {
   cudaMalloc(&x, sizeof(double) * ht.size());
   cudaMemcpy(G, hg.data(), sizeof(double) * hg.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(t, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice);
-  const size_t smem = sizeof(double) * (kSlots * Thomas<CB>::PLANE + 2 * C) + sizeof(ThomasSmem<CB>) + 256;
+  const size_t smem = sizeof(double) * (kSlots * Thomas<CB>::PLANE + (BENCH_TZ_GLOBAL ? 1 : 2) * C) + sizeof(ThomasSmem<CB>) + 256;
+  {
+    std::vector<double> htz(C);
+    for (size_t c = 0; c < C; ++c) htz[c] = c >= CB * CB ? -0.1 : 0.0;
+    cudaMemcpyToSymbol(g_tz, htz.data(), sizeof(double) * C);
+  }
   const double gb = (double)sizeof(double) * per * nb / 1e9;
   const float t0 = run<0>(G, t, x, nb, smem), t1 = run<1>(G, t, x, nb, smem), t2 = run<2>(G, t, x, nb, smem);
   printf("threads %d smem %zu KB  G %.0f MB\n", Thomas<CB>::NT, smem >> 10, gb * 1e3);
   printf("real   %7.1f us  (%.0f GB/s of G)\n", t0, gb / (t0 * 1e-6));
   printf("L2     %7.1f us\n", t1);
   printf("copy   %7.1f us  (%.0f GB/s of G)\n", t2, gb / (t2 * 1e-6));
+#if !BENCH_TZ_GLOBAL
   {
     // reference result of the one-CTA-per-brick kernel, then the persistent ones
     std::vector<double> x0(C * nb), x1(C * nb);
@@ -198,6 +223,7 @@ int main(int argc, char** argv) {
                gb / (tp * 1e-6), bad);
       }
   }
+#endif
   double* buf;
   cudaMalloc(&buf, (size_t)512 << 20);
   for (size_t mb : {0, 32, 64, 128, 256})
